@@ -1,0 +1,232 @@
+/*
+ * h2b.h — C ABI of the B200-native H^2-matvec + Galerkin nearfield quadrature
+ * library (libh2b.so), the drop-in boundary for the hot path of the reference
+ * package `h2bem` (arXiv 2001.05523).
+ *
+ * Every entry point is `extern "C"`, takes plain pointers and sizes, returns an
+ * int status (H2B_OK == 0) and never throws.  The message of the last failure
+ * on the calling thread is available through h2b_last_error().  Pointers named
+ * d_* are DEVICE pointers (owned by the caller, e.g. torch tensors); h_* are
+ * host pointers.  `stream` is a cudaStream_t passed as void* (NULL = legacy
+ * default stream).  All device work is stream-ordered; functions that must
+ * return host-visible sizes synchronise the stream and say so.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/pkg/src/h2bem):
+ *   h2b_cluster_tree     <- clustering.build_cluster_tree          clustering.py:78-121
+ *   h2b_block_tree       <- clustering.BlockTree._descend          clustering.py:137-160
+ *   h2b_panel_points     <- quadrature.triangle_points             quadrature.py:71-87
+ *   h2b_touch_count/fill <- kernels.touching_pairs/_classify_pairs  kernels.py:246-254,333-343
+ *                           + quadrature.classify_panel_pair        quadrature.py:90-118
+ *   h2b_singular         <- kernels.pair_integrals / SingularTable kernels.py:260-362
+ *   h2b_pair_blocks_slp  <- kernels.panel_pair_matrix(SLP)+slp_block kernels.py:365-445
+ *   h2b_pair_blocks_dlp  <- kernels.panel_pair_matrix(DLP)+dlp_block kernels.py:365-434,448-468
+ *   h2b_plan_create /
+ *   h2b_matvec           <- containers.H2Matrix.matvec             containers.py:254-270
+ *                           (ClusterBasis.forward/backward          containers.py:201-228)
+ *   h2b_diagonal         <- containers.H2Matrix.diagonal           containers.py:290-301
+ */
+#ifndef H2B_H
+#define H2B_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (mapped to the reference's Python exceptions) ---------- */
+#define H2B_OK 0
+#define H2B_ERR_INVALID 1   /* ValueError: bad argument                         */
+#define H2B_ERR_CUDA 2      /* RuntimeError: CUDA failure                       */
+#define H2B_ERR_NONFINITE 3 /* FloatingPointError: non-finite nearfield entry   */
+#define H2B_ERR_TOUCHING 4  /* ValueError: touching pair with require_disjoint  */
+#define H2B_ERR_MISSING 5   /* KeyError: pair missing from the singular table   */
+#define H2B_ERR_CAPACITY 6  /* output capacity too small; sizes were returned   */
+
+/* operator kinds (kernels.SLP / kernels.DLP) */
+#define H2B_SLP 0
+#define H2B_DLP 1
+
+/* touching-pair case codes = number of shared vertices (kernels.py:246-254) */
+#define H2B_DISJOINT 0
+#define H2B_VERTEX 1
+#define H2B_EDGE 2
+#define H2B_IDENTICAL 3
+
+int h2b_last_error(char* buf, size_t n);
+int h2b_abi_version(void);
+
+/* ======================= structure (host, bit-exact) ======================= */
+
+/* Geometric bisection tree over support boxes (n x 2 x 3, [min; max]).
+ * Node arrays have capacity 2n-1 and are filled in preorder (uid order);
+ * left/right = -1 for leaves, node_boxes is (2n-1) x 2 x 3. */
+int h2b_cluster_tree(const double* h_boxes, int64_t n, int64_t r_leaf, int64_t* h_perm,
+                     int64_t* h_n_nodes, int64_t* h_start, int64_t* h_end, int64_t* h_depth,
+                     int64_t* h_left, int64_t* h_right, double* h_node_boxes);
+
+typedef struct {
+    int64_t n_nodes;
+    const int64_t* left;  /* child uids, -1 for leaves (root = uid 0) */
+    const int64_t* right;
+    const double* boxes;  /* n_nodes x 2 x 3 */
+} h2b_tree;
+
+/* Admissibility-driven leaf partition in the reference's depth-first order.
+ * far/near are (cap x 2) [row uid, col uid].  On H2B_ERR_CAPACITY the counts
+ * are still written and the call may be repeated with larger buffers. */
+int h2b_block_tree(const h2b_tree* row, const h2b_tree* col, double eta, int64_t* h_far,
+                   int64_t far_cap, int64_t* h_near, int64_t near_cap, int64_t* h_n_far,
+                   int64_t* h_n_near);
+
+/* ======================= Galerkin quadrature (device) ====================== */
+
+typedef struct {
+    int64_t n_vertices, n_triangles;
+    const double* d_vertices;   /* V x 3 */
+    const int32_t* d_triangles; /* F x 3 */
+    const double* d_normals;    /* F x 3 */
+    const double* d_areas;      /* F     */
+    const int64_t* d_vt_ptr;    /* V+1: vertex -> incident triangles (CSR) */
+    const int32_t* d_vt_idx;    /* 3F  */
+} h2b_mesh;
+
+/* Regular (Duffy tensor) rule points on every panel: out = SoA [4][F][Q]
+ * (x, y, z, weight incl. 2*area).  rule_xy: Q x 2 reference points, rule_w: Q. */
+int h2b_panel_points(const h2b_mesh* m, const double* d_rule_xy, const double* d_rule_w,
+                     int32_t Q, double* d_out, void* stream);
+
+typedef struct {
+    int64_t n_panels, n_pairs;
+    const int64_t* d_row_ptr; /* F+1, CSR over row panel                      */
+    const int32_t* d_col;     /* n_pairs, ascending within a row              */
+    const int32_t* d_info;    /* code | perm_a << 2 | perm_b << 8 (2 bits/idx) */
+    const int32_t* d_case_list; /* n_pairs pair ids grouped by case          */
+    const int64_t* h_case_off;  /* 4: start of identical/edge/vertex/end in case_list */
+} h2b_touch;
+
+/* Pass 1: per row panel touching count -> exclusive scan in d_row_ptr (F+1),
+ * per-case counts in h_case_count[4] (identical, edge, vertex, total).
+ * Synchronises the stream. */
+int h2b_touch_count(const h2b_mesh* m, int64_t* d_row_ptr, int64_t* h_case_count, void* stream);
+/* Pass 2: sorted columns, case/permutation info and the case-grouped pair list. */
+int h2b_touch_fill(const h2b_mesh* m, const int64_t* d_row_ptr, const int64_t* h_case_count,
+                   int32_t* d_col, int32_t* d_info, int32_t* d_case_list, void* stream);
+
+typedef struct {
+    int64_t n;         /* number of rule points */
+    const double* d_p; /* n x 4: (u1, v1, u2, v2) */
+    const double* d_w; /* n */
+} h2b_rule;
+
+/* Sauter-Schwab integrals of every touching pair.  rules[0..2] = identical,
+ * edge, vertex rules (quadrature.sauter_schwab_rule).  values: n_pairs (SLP)
+ * or n_pairs x 3 (DLP, original local vertex order of the column panel). */
+int h2b_singular(const h2b_mesh* m, const h2b_touch* t, int kind, const h2b_rule* rules,
+                 double* d_values, void* stream);
+
+typedef struct {
+    int64_t n_jobs;
+    const int64_t* d_jobs;    /* n_jobs x 6: row_off, n_rows, col_off, n_cols, out_off, out_ld */
+    const int32_t* d_row_idx; /* row panels */
+    const int32_t* d_col_idx; /* column panels (SLP) */
+} h2b_jobs;
+
+/* Dense SLP blocks out[out_off + r*ld + c] = G(row_idx[row_off+r], col_idx[col_off+c]).
+ * Regular pairs: tensor rule with Q points per panel (panel_points).  Touching
+ * pairs: value from the singular table (t != NULL) or, when t == NULL
+ * (require_disjoint), the call fails with H2B_ERR_TOUCHING.  Synchronises. */
+int h2b_pair_blocks_slp(const h2b_mesh* m, const double* d_panel_points, int32_t Q,
+                        const h2b_jobs* jobs, const h2b_touch* t, const double* d_touch_values,
+                        double* d_out, void* stream);
+
+typedef struct {
+    int64_t n_jobs;
+    const int64_t* d_jobs;     /* n_jobs x 8: row_off, n_rows, pan_off, n_pan, col_off, n_cols, out_off, out_ld */
+    const int32_t* d_row_idx;  /* row panels (P0 dofs)                                  */
+    const int32_t* d_pan_idx;  /* column panels incident to the job's column vertices  */
+    const int32_t* d_inc_ptr;  /* per job column: CSR into inc (size sum n_cols + n_jobs) */
+    const int32_t* d_inc;      /* (local panel << 2 | local vertex) contributions        */
+    const int64_t* d_inc_base; /* n_jobs: offset of the job's CSR row pointers           */
+} h2b_dlp_jobs;
+
+/* Dense DLP blocks (P0 rows x P1 columns) with the vertex scatter of
+ * kernels.dlp_block fused in.  Synchronises. */
+int h2b_pair_blocks_dlp(const h2b_mesh* m, const double* d_panel_points, const double* d_lam,
+                        int32_t Q, const h2b_dlp_jobs* jobs, const h2b_touch* t,
+                        const double* d_touch_values, double* d_out, void* stream);
+
+/* ============================ H^2 matvec (device) ========================== */
+
+/* Packed operator layout (all device pointers; int32 unless noted).
+ * Column tree (forward transform) and row tree (backward) are described by
+ * per-node arrays indexed by uid; couplings S are stored per row cluster as one
+ * row-major k_t x K_t matrix (K_t = sum of k_s over its far blocks, in far-list
+ * order); nearfield D per row leaf as one row-major |t| x C_t matrix (C_t = sum
+ * of |s| over its near blocks). */
+typedef struct {
+    int64_t n_rows, n_cols;
+    /* permutations: x_p[i] = x[col_perm[i]], y[row_perm[i]] = y_p[i] */
+    const int64_t* col_perm;
+    const int64_t* row_perm;
+    /* column tree */
+    int32_t c_nodes, c_leaves;
+    const int32_t* c_parent;  /* -1 root */
+    const int32_t* c_child;   /* 2 per node, -1 */
+    const int32_t* c_start;
+    const int32_t* c_size;
+    const int32_t* c_rank;
+    const int64_t* c_v_off;   /* leaves: offset of V (|t| x k) in c_V */
+    const int64_t* c_e_off;   /* non-root: offset of E (k x k_parent) in c_E */
+    const int64_t* c_xhat_off;
+    const int32_t* c_leaf_list;
+    const double* c_V;
+    const double* c_E;
+    int64_t xhat_len;
+    /* row tree */
+    int32_t r_nodes, r_leaves;
+    const int32_t* r_parent;
+    const int32_t* r_start;
+    const int32_t* r_size;
+    const int32_t* r_rank;
+    const int64_t* r_v_off;
+    const int64_t* r_e_off;
+    const int64_t* r_yhat_off;
+    const int32_t* r_order;   /* top-down processing order (parents first) */
+    const double* r_V;
+    const double* r_E;
+    int64_t yhat_len;
+    /* couplings per row node */
+    const int64_t* s_off;     /* offset of the k_t x K_t matrix */
+    const int32_t* s_cols;    /* K_t */
+    const int32_t* far_ptr;   /* n_rnodes+1 into far_col */
+    const int32_t* far_col;   /* column uid per far block, far-list order within the row */
+    const double* S;
+    /* nearfield per row leaf */
+    const int64_t* d_off;     /* offset of the |t| x C_t matrix (per row node; leaves only) */
+    const int32_t* d_cols;    /* C_t */
+    const int32_t* near_ptr;  /* n_rnodes+1 into near_col */
+    const int32_t* near_col;  /* column uid per near block */
+    const double* D;
+    /* which row nodes this rank processes (multi-GPU row sharding); all if NULL */
+    int32_t n_owned;
+    const int32_t* owned;     /* subset of r_order, still parents first */
+} h2b_layout;
+
+typedef struct h2b_plan h2b_plan;
+
+int h2b_plan_create(const h2b_layout* layout, h2b_plan** out);
+int h2b_plan_destroy(h2b_plan* plan);
+/* y = A x for device vectors in natural dof order (x: n_cols, y: n_rows). */
+int h2b_matvec(h2b_plan* plan, const double* d_x, double* d_y, void* stream);
+/* Same through host buffers: H2D copy of x, matvec, D2H copy of y, synchronised. */
+int h2b_matvec_host(h2b_plan* plan, const double* h_x, double* h_y, void* stream);
+/* Diagonal of the (square) operator from the nearfield, natural order. */
+int h2b_diagonal(h2b_plan* plan, double* d_diag, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* H2B_H */

@@ -1,0 +1,898 @@
+// Galerkin panel-pair quadrature for the Laplace single- and double-layer
+// operators on flat triangles, fp64, sm_100a.
+//
+//   k_panel_points   regular Duffy tensor rule on every panel   (quadrature.py:58-87)
+//   k_touch_*        touching-pair enumeration + Sauter-Schwab case/permutation
+//                    classification                               (kernels.py:246-254,333-343;
+//                                                                  quadrature.py:90-118)
+//   k_singular       Sauter-Schwab integrals of all touching pairs (kernels.py:260-319)
+//   k_blocks_slp     dense SLP blocks: regular tensor rule, touching pairs patched
+//                    from the singular table                      (kernels.py:365-445)
+//   k_blocks_dlp     dense DLP blocks with the P1 vertex scatter  (kernels.py:365-434,448-468)
+//
+// All quadrature loops are FP64-pipe bound.  1/r is a hardware rsqrt seed plus
+// one Newton correction folded into the accumulation; squared distances of
+// regular pairs use the Gram form on block-centred coordinates (the
+// reference's _dist2, kernels.py:75-85, without its cancellation because both
+// point sets are shifted to a block-local origin first).
+
+#include <cub/device/device_scan.cuh>
+
+#include "device_common.cuh"
+
+namespace h2b {
+namespace {
+
+constexpr int kMaxCand = 128;   // touching candidates per panel (3 x vertex valence)
+constexpr int kTile = 64;       // max rows / columns of one pair-block job
+constexpr int kDlpMaxPanels = 128;  // max column panels of one DLP job
+constexpr int kDlpRowChunk = 8;
+
+// flags bits (reduced per launch, mapped to the reference's exceptions)
+constexpr int kFlagNonFinite = 1;
+constexpr int kFlagTouching = 2;
+constexpr int kFlagMissing = 4;
+constexpr int kFlagShape = 8;
+constexpr int kFlagCandidates = 16;
+
+// ----------------------------------------------------------------------------
+// regular panel points
+__global__ void k_panel_points(const double* __restrict__ V, const int32_t* __restrict__ T,
+                               const double* __restrict__ A, int64_t F,
+                               const double* __restrict__ rxy, const double* __restrict__ rw, int Q,
+                               double* __restrict__ out) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= F * Q) return;
+    const int64_t f = e / Q;
+    const int j = (int)(e - f * Q);
+    const int i0 = T[3 * f], i1 = T[3 * f + 1], i2 = T[3 * f + 2];
+    const double x = rxy[2 * j], y = rxy[2 * j + 1];
+    const int64_t FQ = F * Q;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double c0 = V[3 * i0 + k], c1 = V[3 * i1 + k], c2 = V[3 * i2 + k];
+        // c0 + x (c1 - c0) + y (c2 - c0), evaluated as written (no contraction)
+        out[k * FQ + e] = __dadd_rn(__dadd_rn(c0, __dmul_rn(x, c1 - c0)), __dmul_rn(y, c2 - c0));
+    }
+    out[3 * FQ + e] = rw[j] * (2.0 * A[f]);
+}
+
+// ----------------------------------------------------------------------------
+// touching pairs
+__device__ int gather_touching(const int32_t* __restrict__ T, const int64_t* __restrict__ vt_ptr,
+                               const int32_t* __restrict__ vt_idx, int64_t a, int* cand, int* flags) {
+    int n = 0;
+    for (int k = 0; k < 3; ++k) {
+        const int v = T[3 * a + k];
+        for (int64_t p = vt_ptr[v]; p < vt_ptr[v + 1]; ++p) {
+            if (n < kMaxCand) cand[n] = vt_idx[p];
+            ++n;
+        }
+    }
+    if (n > kMaxCand) {
+        atomicOr(flags, kFlagCandidates);
+        n = kMaxCand;
+    }
+    // insertion sort + unique
+    for (int i = 1; i < n; ++i) {
+        const int v = cand[i];
+        int j = i - 1;
+        while (j >= 0 && cand[j] > v) {
+            cand[j + 1] = cand[j];
+            --j;
+        }
+        cand[j + 1] = v;
+    }
+    int m = 0;
+    for (int i = 0; i < n; ++i)
+        if (m == 0 || cand[m - 1] != cand[i]) cand[m++] = cand[i];
+    return m;
+}
+
+// quadrature.py:90-118: case = #shared vertices (3 when identical); shared
+// vertices first in ascending global id, remaining local vertices in order.
+__device__ int classify(const int* ta, const int* tb, bool same) {
+    if (same) return H2B_IDENTICAL | (0 << 2) | (1 << 4) | (2 << 6) | (0 << 8) | (1 << 10) | (2 << 12);
+    int sa[3], sb[3], ns = 0;
+    // shared vertices, ascending global id
+    int sh[3];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            if (ta[i] == tb[j]) sh[ns++] = ta[i];
+    if (ns == 2 && sh[0] > sh[1]) {
+        const int t = sh[0];
+        sh[0] = sh[1];
+        sh[1] = t;
+    }
+    if (ns == 0) return H2B_DISJOINT | (0 << 2) | (1 << 4) | (2 << 6) | (0 << 8) | (1 << 10) | (2 << 12);
+    int pa[3], pb[3];
+    for (int s = 0; s < ns; ++s) {
+        for (int i = 0; i < 3; ++i) {
+            if (ta[i] == sh[s]) sa[s] = i;
+            if (tb[i] == sh[s]) sb[s] = i;
+        }
+        pa[s] = sa[s];
+        pb[s] = sb[s];
+    }
+    int ka = ns, kb = ns;
+    for (int i = 0; i < 3; ++i) {
+        bool ua = false, ub = false;
+        for (int s = 0; s < ns; ++s) {
+            ua |= (sa[s] == i);
+            ub |= (sb[s] == i);
+        }
+        if (!ua) pa[ka++] = i;
+        if (!ub) pb[kb++] = i;
+    }
+    const int code = ns == 2 ? H2B_EDGE : H2B_VERTEX;
+    return code | (pa[0] << 2) | (pa[1] << 4) | (pa[2] << 6) | (pb[0] << 8) | (pb[1] << 10) |
+           (pb[2] << 12);
+}
+
+__global__ void k_touch_count(const int32_t* __restrict__ T, int64_t F,
+                              const int64_t* __restrict__ vt_ptr, const int32_t* __restrict__ vt_idx,
+                              int64_t* __restrict__ counts, unsigned long long* __restrict__ case_count,
+                              int* flags) {
+    const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    __shared__ unsigned long long sc[4];
+    if (threadIdx.x < 4) sc[threadIdx.x] = 0;
+    __syncthreads();
+    if (a < F) {
+        int cand[kMaxCand];
+        const int m = gather_touching(T, vt_ptr, vt_idx, a, cand, flags);
+        counts[a] = m;
+        int ta[3] = {T[3 * a], T[3 * a + 1], T[3 * a + 2]};
+        int c[4] = {0, 0, 0, 0};
+        for (int i = 0; i < m; ++i) {
+            const int b = cand[i];
+            int tb[3] = {T[3 * b], T[3 * b + 1], T[3 * b + 2]};
+            const int code = classify(ta, tb, b == a) & 3;
+            c[code]++;
+        }
+        for (int k = 1; k < 4; ++k)
+            if (c[k]) atomicAdd(&sc[k], (unsigned long long)c[k]);
+        if (c[0]) atomicOr(flags, kFlagCandidates);  // cannot happen on a valid mesh
+    }
+    __syncthreads();
+    if (threadIdx.x > 0 && threadIdx.x < 4 && sc[threadIdx.x]) atomicAdd(&case_count[threadIdx.x], sc[threadIdx.x]);
+}
+
+__global__ void k_touch_fill(const int32_t* __restrict__ T, int64_t F,
+                             const int64_t* __restrict__ vt_ptr, const int32_t* __restrict__ vt_idx,
+                             const int64_t* __restrict__ row_ptr, int32_t* __restrict__ col,
+                             int32_t* __restrict__ info, int32_t* __restrict__ case_list,
+                             unsigned long long* __restrict__ case_cursor, int* flags) {
+    const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= F) return;
+    int cand[kMaxCand];
+    const int m = gather_touching(T, vt_ptr, vt_idx, a, cand, flags);
+    int ta[3] = {T[3 * a], T[3 * a + 1], T[3 * a + 2]};
+    const int64_t base = row_ptr[a];
+    for (int i = 0; i < m; ++i) {
+        const int b = cand[i];
+        int tb[3] = {T[3 * b], T[3 * b + 1], T[3 * b + 2]};
+        const int inf = classify(ta, tb, b == a);
+        col[base + i] = b;
+        info[base + i] = inf;
+        // case-grouped list: identical, edge, vertex segments (order within a
+        // segment is irrelevant: values are written per pair id)
+        const int code = inf & 3;
+        const int seg = code == H2B_IDENTICAL ? 0 : (code == H2B_EDGE ? 1 : 2);
+        const unsigned long long slot = atomicAdd(&case_cursor[seg], 1ull);
+        case_list[slot] = (int32_t)(base + i);
+    }
+}
+
+// ----------------------------------------------------------------------------
+// Sauter-Schwab integrals
+struct SegDesc {
+    int64_t list_off, count;
+    int32_t first_block, n_blocks;
+    const double* p;
+    const double* w;
+    int64_t n;
+    int kase;  // H2B_IDENTICAL / H2B_EDGE / H2B_VERTEX
+};
+
+struct SegSet {
+    SegDesc s[3];
+    int nseg;
+};
+
+constexpr int kRuleChunk = 256;
+constexpr int kRuleStride = 8;
+
+__device__ __forceinline__ int64_t find_row(const int64_t* __restrict__ row_ptr, int64_t F, int64_t pid) {
+    int64_t lo = 0, hi = F;  // row_ptr[lo] <= pid < row_ptr[hi]
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (row_ptr[mid] <= pid) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(128) k_singular(const double* __restrict__ V, const int32_t* __restrict__ T,
+                                                 const double* __restrict__ Nrm, const double* __restrict__ Ar,
+                                                 const int64_t* __restrict__ row_ptr, int64_t F,
+                                                 const int32_t* __restrict__ col, const int32_t* __restrict__ info,
+                                                 const int32_t* __restrict__ case_list, SegSet segs,
+                                                 double* __restrict__ values) {
+    __shared__ double srule[kRuleChunk * kRuleStride];
+    int si = 0;
+    while (si + 1 < segs.nseg && (int)blockIdx.x >= segs.s[si + 1].first_block) ++si;
+    const SegDesc sd = segs.s[si];
+    const int kase = sd.kase;
+    const int64_t local = (int64_t)(blockIdx.x - sd.first_block) * blockDim.x + threadIdx.x;
+    const bool active = local < sd.count;
+
+    double base[3] = {0, 0, 0}, ea1[3] = {0, 0, 0}, ea2[3] = {0, 0, 0}, eb1[3] = {0, 0, 0},
+           eb2[3] = {0, 0, 0}, nb[3] = {0, 0, 0};
+    double scale = 0.0;
+    int64_t pid = 0;
+    int inf = 0;
+    if (active) {
+        pid = case_list[sd.list_off + local];
+        const int64_t a = find_row(row_ptr, F, pid);
+        const int b = col[pid];
+        inf = info[pid];
+        int pa[3] = {(inf >> 2) & 3, (inf >> 4) & 3, (inf >> 6) & 3};
+        int pb[3] = {(inf >> 8) & 3, (inf >> 10) & 3, (inf >> 12) & 3};
+        double ca[3][3], cb[3][3];
+        for (int r = 0; r < 3; ++r) {
+            const int va = T[3 * a + pa[r]], vb = T[3 * b + pb[r]];
+            for (int k = 0; k < 3; ++k) {
+                ca[r][k] = V[3 * va + k];
+                cb[r][k] = V[3 * vb + k];
+            }
+        }
+        for (int k = 0; k < 3; ++k) {
+            base[k] = ca[0][k] - cb[0][k];
+            ea1[k] = ca[1][k] - ca[0][k];
+            ea2[k] = ca[2][k] - ca[1][k];
+            eb1[k] = -(cb[1][k] - cb[0][k]);
+            eb2[k] = -(cb[2][k] - cb[1][k]);
+            nb[k] = Nrm[3 * b + k];
+        }
+        scale = 4.0 * Ar[a] * Ar[b];
+    }
+
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+    const bool sym = (KIND == H2B_SLP) && (kase != H2B_IDENTICAL);
+    for (int64_t c0 = 0; c0 < sd.n; c0 += kRuleChunk) {
+        const int cn = (int)min((int64_t)kRuleChunk, sd.n - c0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < cn; e += blockDim.x) {
+            const double* p = sd.p + 4 * (c0 + e);
+            const double w = sd.w[c0 + e];
+            double* d = srule + e * kRuleStride;
+            d[0] = p[0];
+            d[1] = p[1];
+            d[2] = p[2];
+            d[3] = p[3];
+            d[4] = w;
+            d[5] = w * (1.0 - p[2]);
+            d[6] = w * (p[2] - p[3]);
+            d[7] = w * p[3];
+        }
+        __syncthreads();
+        if (!active) continue;
+        if (KIND == H2B_SLP) {
+            if (kase == H2B_IDENTICAL) {
+                // same panel: d = (u1-u2) E1 + (v1-v2) E2 (base = 0)
+#pragma unroll 4
+                for (int e = 0; e < cn; ++e) {
+                    const double* d = srule + e * kRuleStride;
+                    const double du = d[0] - d[2], dv = d[1] - d[3];
+                    const double dx = fma(dv, ea2[0], du * ea1[0]);
+                    const double dy = fma(dv, ea2[1], du * ea1[1]);
+                    const double dz = fma(dv, ea2[2], du * ea1[2]);
+                    const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+                    const double t = rsqrt_seed(r2);
+                    const double s = t * t;
+                    const double c = fma(-r2, s, 3.0);
+                    acc0 = fma(d[4] * t, c, acc0);
+                }
+            } else {
+#pragma unroll 2
+                for (int e = 0; e < cn; ++e) {
+                    const double* d = srule + e * kRuleStride;
+                    const double u1 = d[0], v1 = d[1], u2 = d[2], v2 = d[3], w = d[4];
+                    double dx = fma(v2, eb2[0], fma(u2, eb1[0], fma(v1, ea2[0], fma(u1, ea1[0], base[0]))));
+                    double dy = fma(v2, eb2[1], fma(u2, eb1[1], fma(v1, ea2[1], fma(u1, ea1[1], base[1]))));
+                    double dz = fma(v2, eb2[2], fma(u2, eb1[2], fma(v1, ea2[2], fma(u1, ea1[2], base[2]))));
+                    double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+                    double t = rsqrt_seed(r2);
+                    double s = t * t;
+                    double c = fma(-r2, s, 3.0);
+                    acc0 = fma(w * t, c, acc0);
+                    // orientation-swapped rule (kernels.py:303-309)
+                    dx = fma(v1, eb2[0], fma(u1, eb1[0], fma(v2, ea2[0], fma(u2, ea1[0], base[0]))));
+                    dy = fma(v1, eb2[1], fma(u1, eb1[1], fma(v2, ea2[1], fma(u2, ea1[1], base[1]))));
+                    dz = fma(v1, eb2[2], fma(u1, eb1[2], fma(v2, ea2[2], fma(u2, ea1[2], base[2]))));
+                    r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+                    t = rsqrt_seed(r2);
+                    s = t * t;
+                    c = fma(-r2, s, 3.0);
+                    acc1 = fma(w * t, c, acc1);
+                }
+            }
+        } else {
+            // DLP: <x - y, n_b> / r^3 weighted by the column chart barycentrics
+#pragma unroll 2
+            for (int e = 0; e < cn; ++e) {
+                const double* d = srule + e * kRuleStride;
+                const double u1 = d[0], v1 = d[1], u2 = d[2], v2 = d[3];
+                const double dx = fma(v2, eb2[0], fma(u2, eb1[0], fma(v1, ea2[0], fma(u1, ea1[0], base[0]))));
+                const double dy = fma(v2, eb2[1], fma(u2, eb1[1], fma(v1, ea2[1], fma(u1, ea1[1], base[1]))));
+                const double dz = fma(v2, eb2[2], fma(u2, eb1[2], fma(v1, ea2[2], fma(u1, ea1[2], base[2]))));
+                const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+                const double t = rsqrt_seed(r2);
+                const double s = t * t;
+                const double c3 = fma(-r2, s, 5.0 / 3.0);
+                const double num = fma(dz, nb[2], fma(dy, nb[1], dx * nb[0]));
+                const double k = (num * c3) * (s * t);
+                acc0 = fma(k, d[5], acc0);
+                acc1 = fma(k, d[6], acc1);
+                acc2 = fma(k, d[7], acc2);
+            }
+        }
+    }
+    if (!active) return;
+    if (KIND == H2B_SLP) {
+        // 1/r = t (3 - r^2 t^2) / 2; symmetrised pairs average both orientations
+        double v = sym ? 0.25 * (acc0 + acc1) : 0.5 * acc0;
+        values[pid] = v * kInv4Pi * scale;
+    } else {
+        // 1/r^3 = 1.5 t^3 (5/3 - r^2 t^2); scatter back to original local vertices
+        const double f = 1.5 * kInv4Pi * scale;
+        double out[3];
+        const int pb0 = (inf >> 8) & 3, pb1 = (inf >> 10) & 3, pb2 = (inf >> 12) & 3;
+        out[pb0] = acc0 * f;
+        out[pb1] = acc1 * f;
+        out[pb2] = acc2 * f;
+        values[3 * pid] = out[0];
+        values[3 * pid + 1] = out[1];
+        values[3 * pid + 2] = out[2];
+    }
+}
+
+// ----------------------------------------------------------------------------
+// regular SLP pair blocks
+__device__ __forceinline__ bool shares_vertex(const int* ra, const int* cb) {
+    bool h = false;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) h |= (ra[i] == cb[j]);
+    return h;
+}
+
+__device__ __forceinline__ int64_t touch_find(const int64_t* __restrict__ row_ptr,
+                                              const int32_t* __restrict__ col, int a, int b) {
+    for (int64_t p = row_ptr[a]; p < row_ptr[a + 1]; ++p)
+        if (col[p] == b) return p;
+    return -1;
+}
+
+// constant factor of the folded Newton step: with g = -r^2/2 and t ~ rsqrt(-g),
+// 1/(4 pi r) = t (3 + g t^2) / (8 sqrt(2) pi)
+constexpr double kSlpFold = 1.0 / (8.0 * 1.4142135623730950488016887 * kPi);
+
+template <int Q, int JC>
+__global__ void __launch_bounds__(256) k_blocks_slp(const double* __restrict__ P, int64_t F,
+                                                   const int32_t* __restrict__ T,
+                                                   const int64_t* __restrict__ jobs,
+                                                   const int32_t* __restrict__ row_idx,
+                                                   const int32_t* __restrict__ col_idx,
+                                                   const int64_t* __restrict__ t_row_ptr,
+                                                   const int32_t* __restrict__ t_col,
+                                                   const double* __restrict__ t_val,
+                                                   double* __restrict__ out, int* __restrict__ flags) {
+    extern __shared__ double smem[];
+    double* rx = smem;                 // [5][Q][kTile]: x', y', z', -|x'|^2/2, W
+    double* cx = smem + 5 * Q * kTile; // [5][Q][kTile]: y', ..., W / (8 sqrt2 pi)
+    int* rv = reinterpret_cast<int*>(cx + 5 * Q * kTile);  // [kTile][3]
+    int* cv = rv + 3 * kTile;
+    int* rp = cv + 3 * kTile;
+    int* cp = rp + kTile;
+
+    const int64_t* jb = jobs + 6 * (int64_t)blockIdx.x;
+    const int64_t row_off = jb[0], col_off = jb[2], out_off = jb[4], ld = jb[5];
+    const int nr = (int)jb[1], nc = (int)jb[3];
+    if (nr > kTile || nc > kTile) {
+        if (threadIdx.x == 0) atomicOr(flags, kFlagShape);
+        return;
+    }
+    if (nr == 0 || nc == 0) return;
+    const int64_t FQ = F * Q;
+    const int64_t o_idx = (int64_t)row_idx[row_off] * Q;
+    const double ox = P[o_idx], oy = P[FQ + o_idx], oz = P[2 * FQ + o_idx];
+
+    for (int e = threadIdx.x; e < nr * Q; e += blockDim.x) {
+        const int r = e / Q, i = e - r * Q;
+        const int pnl = row_idx[row_off + r];
+        const int64_t g = (int64_t)pnl * Q + i;
+        const double x = P[g] - ox, y = P[FQ + g] - oy, z = P[2 * FQ + g] - oz;
+        const int s = i * kTile + r;
+        rx[s] = x;
+        rx[Q * kTile + s] = y;
+        rx[2 * Q * kTile + s] = z;
+        rx[3 * Q * kTile + s] = -0.5 * fma(z, z, fma(y, y, x * x));
+        rx[4 * Q * kTile + s] = P[3 * FQ + g];
+        if (i == 0) {
+            rp[r] = pnl;
+            rv[3 * r] = T[3 * pnl];
+            rv[3 * r + 1] = T[3 * pnl + 1];
+            rv[3 * r + 2] = T[3 * pnl + 2];
+        }
+    }
+    for (int e = threadIdx.x; e < nc * Q; e += blockDim.x) {
+        const int c = e / Q, j = e - c * Q;
+        const int pnl = col_idx[col_off + c];
+        const int64_t g = (int64_t)pnl * Q + j;
+        const double x = P[g] - ox, y = P[FQ + g] - oy, z = P[2 * FQ + g] - oz;
+        const int s = j * kTile + c;
+        cx[s] = x;
+        cx[Q * kTile + s] = y;
+        cx[2 * Q * kTile + s] = z;
+        cx[3 * Q * kTile + s] = -0.5 * fma(z, z, fma(y, y, x * x));
+        cx[4 * Q * kTile + s] = P[3 * FQ + g] * kSlpFold;
+        if (j == 0) {
+            cp[c] = pnl;
+            cv[3 * c] = T[3 * pnl];
+            cv[3 * c + 1] = T[3 * pnl + 1];
+            cv[3 * c + 2] = T[3 * pnl + 2];
+        }
+    }
+    __syncthreads();
+
+    int lflags = 0;
+    const int np = nr * nc;
+    for (int p = threadIdx.x; p < np; p += blockDim.x) {
+        const int a = p / nc, b = p - a * nc;
+        double val;
+        if (shares_vertex(rv + 3 * a, cv + 3 * b)) {
+            if (t_row_ptr == nullptr) {
+                lflags |= kFlagTouching;
+                val = 0.0;
+            } else {
+                const int64_t k = touch_find(t_row_ptr, t_col, rp[a], cp[b]);
+                if (k < 0) {
+                    lflags |= kFlagMissing;
+                    val = 0.0;
+                } else {
+                    val = t_val[k];
+                }
+            }
+        } else {
+            double tot = 0.0;
+#pragma unroll
+            for (int j0 = 0; j0 < Q; j0 += JC) {
+                double y0[JC], y1[JC], y2[JC], yh[JC], yw[JC];
+#pragma unroll
+                for (int j = 0; j < JC; ++j) {
+                    const int s = (j0 + j) * kTile + b;
+                    y0[j] = cx[s];
+                    y1[j] = cx[Q * kTile + s];
+                    y2[j] = cx[2 * Q * kTile + s];
+                    yh[j] = cx[3 * Q * kTile + s];
+                    yw[j] = cx[4 * Q * kTile + s];
+                }
+#pragma unroll
+                for (int i = 0; i < Q; ++i) {
+                    const int s = i * kTile + a;
+                    const double x0 = rx[s], x1 = rx[Q * kTile + s], x2 = rx[2 * Q * kTile + s];
+                    const double xh = rx[3 * Q * kTile + s], xw = rx[4 * Q * kTile + s];
+                    double acc = 0.0;
+#pragma unroll
+                    for (int j = 0; j < JC; ++j) {
+                        // g = x'.y' - |x'|^2/2 - |y'|^2/2 = -r^2/2
+                        const double g = fma(x0, y0[j], fma(x1, y1[j], fma(x2, y2[j], xh + yh[j])));
+                        const double t = rsqrt_seed(-g);
+                        const double c = fma(g, t * t, 3.0);
+                        acc = fma(yw[j] * t, c, acc);
+                    }
+                    tot = fma(xw, acc, tot);
+                }
+            }
+            val = tot;
+        }
+        if (!isfinite(val)) lflags |= kFlagNonFinite;
+        out[out_off + (int64_t)a * ld + b] = val;
+    }
+    if (lflags) atomicOr(flags, lflags);
+}
+
+// ----------------------------------------------------------------------------
+// regular DLP pair blocks (P0 rows x P1 columns) with the vertex scatter
+template <int Q>
+struct DlpLam {
+    double v[Q * 3];
+};
+__constant__ double c_lam[64 * 3];  // barycentrics of the regular rule, Q <= 64
+
+// 1/r^3 = 1.5 (1/2)^(3/2) t^3 (5/3 + g t^2) with g = -r^2/2, t ~ rsqrt(-g)
+constexpr double kDlpFold = 1.5 * 0.35355339059327376220042218 / (4.0 * kPi);
+
+template <int Q>
+__global__ void __launch_bounds__(256) k_blocks_dlp(const double* __restrict__ P, int64_t F,
+                                                   const int32_t* __restrict__ T,
+                                                   const double* __restrict__ Nrm,
+                                                   const int64_t* __restrict__ jobs,
+                                                   const int32_t* __restrict__ row_idx,
+                                                   const int32_t* __restrict__ pan_idx,
+                                                   const int32_t* __restrict__ inc_ptr,
+                                                   const int32_t* __restrict__ inc,
+                                                   const int64_t* __restrict__ inc_base,
+                                                   const int64_t* __restrict__ t_row_ptr,
+                                                   const int32_t* __restrict__ t_col,
+                                                   const double* __restrict__ t_val,
+                                                   double* __restrict__ out, int* __restrict__ flags) {
+    extern __shared__ double smem[];
+    constexpr int RT = kTile, PT = kDlpMaxPanels;
+    double* rx = smem;                  // [5][Q][RT]
+    double* px = rx + 5 * Q * RT;       // [6][Q][PT]: y', -|y'|^2/2, W, y'.n
+    double* pn = px + 6 * Q * PT;       // [3][PT]
+    double* scr = pn + 3 * PT;          // [kDlpRowChunk][PT][3]
+    int* rv = reinterpret_cast<int*>(scr + kDlpRowChunk * PT * 3);
+    int* pv = rv + 3 * RT;
+    int* rp = pv + 3 * PT;
+    int* pp = rp + RT;
+
+    const int64_t* jb = jobs + 8 * (int64_t)blockIdx.x;
+    const int64_t row_off = jb[0], pan_off = jb[2], out_off = jb[6], ld = jb[7];
+    const int nr = (int)jb[1], npn = (int)jb[3], nc = (int)jb[5];
+    const int64_t ibase = inc_base[blockIdx.x];
+    if (nr > RT || npn > PT || nc > kTile) {
+        if (threadIdx.x == 0) atomicOr(flags, kFlagShape);
+        return;
+    }
+    if (nr == 0 || nc == 0) return;
+    const int64_t FQ = F * Q;
+    const int64_t o_idx = (int64_t)row_idx[row_off] * Q;
+    const double ox = P[o_idx], oy = P[FQ + o_idx], oz = P[2 * FQ + o_idx];
+
+    for (int e = threadIdx.x; e < nr * Q; e += blockDim.x) {
+        const int r = e / Q, i = e - r * Q;
+        const int pnl = row_idx[row_off + r];
+        const int64_t g = (int64_t)pnl * Q + i;
+        const double x = P[g] - ox, y = P[FQ + g] - oy, z = P[2 * FQ + g] - oz;
+        const int s = i * RT + r;
+        rx[s] = x;
+        rx[Q * RT + s] = y;
+        rx[2 * Q * RT + s] = z;
+        rx[3 * Q * RT + s] = -0.5 * fma(z, z, fma(y, y, x * x));
+        rx[4 * Q * RT + s] = P[3 * FQ + g];
+        if (i == 0) {
+            rp[r] = pnl;
+            rv[3 * r] = T[3 * pnl];
+            rv[3 * r + 1] = T[3 * pnl + 1];
+            rv[3 * r + 2] = T[3 * pnl + 2];
+        }
+    }
+    for (int e = threadIdx.x; e < npn * Q; e += blockDim.x) {
+        const int c = e / Q, j = e - c * Q;
+        const int pnl = pan_idx[pan_off + c];
+        const int64_t g = (int64_t)pnl * Q + j;
+        const double x = P[g] - ox, y = P[FQ + g] - oy, z = P[2 * FQ + g] - oz;
+        const double n0 = Nrm[3 * pnl], n1 = Nrm[3 * pnl + 1], n2 = Nrm[3 * pnl + 2];
+        const int s = j * PT + c;
+        px[s] = x;
+        px[Q * PT + s] = y;
+        px[2 * Q * PT + s] = z;
+        px[3 * Q * PT + s] = -0.5 * fma(z, z, fma(y, y, x * x));
+        px[4 * Q * PT + s] = P[3 * FQ + g] * kDlpFold;
+        px[5 * Q * PT + s] = fma(z, n2, fma(y, n1, x * n0));
+        if (j == 0) {
+            pp[c] = pnl;
+            pn[c] = n0;
+            pn[PT + c] = n1;
+            pn[2 * PT + c] = n2;
+            pv[3 * c] = T[3 * pnl];
+            pv[3 * c + 1] = T[3 * pnl + 1];
+            pv[3 * c + 2] = T[3 * pnl + 2];
+        }
+    }
+    __syncthreads();
+
+    int lflags = 0;
+    for (int r0 = 0; r0 < nr; r0 += kDlpRowChunk) {
+        const int rc = min(kDlpRowChunk, nr - r0);
+        const int np = rc * npn;
+        for (int p = threadIdx.x; p < np; p += blockDim.x) {
+            const int al = p / npn, b = p - al * npn;
+            const int a = r0 + al;
+            double v0, v1, v2;
+            if (shares_vertex(rv + 3 * a, pv + 3 * b)) {
+                v0 = v1 = v2 = 0.0;
+                if (t_row_ptr == nullptr) {
+                    lflags |= kFlagTouching;
+                } else {
+                    const int64_t k = touch_find(t_row_ptr, t_col, rp[a], pp[b]);
+                    if (k < 0) {
+                        lflags |= kFlagMissing;
+                    } else {
+                        v0 = t_val[3 * k];
+                        v1 = t_val[3 * k + 1];
+                        v2 = t_val[3 * k + 2];
+                    }
+                }
+            } else {
+                const double n0 = pn[b], n1 = pn[PT + b], n2 = pn[2 * PT + b];
+                double y0[Q], y1[Q], y2[Q], yh[Q], yw[Q], yn[Q];
+#pragma unroll
+                for (int j = 0; j < Q; ++j) {
+                    const int s = j * PT + b;
+                    y0[j] = px[s];
+                    y1[j] = px[Q * PT + s];
+                    y2[j] = px[2 * Q * PT + s];
+                    yh[j] = px[3 * Q * PT + s];
+                    yw[j] = px[4 * Q * PT + s];
+                    yn[j] = px[5 * Q * PT + s];
+                }
+                double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+#pragma unroll
+                for (int i = 0; i < Q; ++i) {
+                    const int s = i * RT + a;
+                    const double x0 = rx[s], x1 = rx[Q * RT + s], x2 = rx[2 * Q * RT + s];
+                    const double xh = rx[3 * Q * RT + s], xw = rx[4 * Q * RT + s];
+                    const double xn = fma(x2, n2, fma(x1, n1, x0 * n0));
+                    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll
+                    for (int j = 0; j < Q; ++j) {
+                        const double g = fma(x0, y0[j], fma(x1, y1[j], fma(x2, y2[j], xh + yh[j])));
+                        const double t = rsqrt_seed(-g);
+                        const double s2 = t * t;
+                        const double c3 = fma(g, s2, 5.0 / 3.0);
+                        const double k = ((xn - yn[j]) * c3) * ((s2 * t) * yw[j]);
+                        a0 = fma(k, c_lam[3 * j], a0);
+                        a1 = fma(k, c_lam[3 * j + 1], a1);
+                        a2 = fma(k, c_lam[3 * j + 2], a2);
+                    }
+                    t0 = fma(xw, a0, t0);
+                    t1 = fma(xw, a1, t1);
+                    t2 = fma(xw, a2, t2);
+                }
+                v0 = t0;
+                v1 = t1;
+                v2 = t2;
+            }
+            double* sp = scr + (al * PT + b) * 3;
+            sp[0] = v0;
+            sp[1] = v1;
+            sp[2] = v2;
+        }
+        __syncthreads();
+        // vertex scatter, fixed order per column (l-major, ascending panel:
+        // the order np.add.at applies in kernels.dlp_block)
+        for (int p = threadIdx.x; p < rc * nc; p += blockDim.x) {
+            const int al = p / nc, c = p - al * nc;
+            const int32_t* ip = inc_ptr + ibase + c;
+            double s = 0.0;
+            for (int k = ip[0]; k < ip[1]; ++k) {
+                const int code = inc[k];
+                s += scr[(al * PT + (code >> 2)) * 3 + (code & 3)];
+            }
+            if (!isfinite(s)) lflags |= kFlagNonFinite;
+            out[out_off + (int64_t)(r0 + al) * ld + c] = s;
+        }
+        __syncthreads();
+    }
+    if (lflags) atomicOr(flags, lflags);
+}
+
+int check_flags(int* d_flags, cudaStream_t st) {
+    int h = 0;
+    H2B_CUDA_TRY(cudaMemcpyAsync(&h, d_flags, sizeof(int), cudaMemcpyDeviceToHost, st));
+    H2B_CUDA_TRY(cudaStreamSynchronize(st));
+    H2B_CUDA_TRY(cudaFreeAsync(d_flags, st));
+    if (h & kFlagShape) return fail(H2B_ERR_INVALID, "pair-block job exceeds the tile size");
+    if (h & kFlagCandidates) return fail(H2B_ERR_INVALID, "vertex valence too large or invalid mesh topology");
+    if (h & kFlagTouching) return fail(H2B_ERR_TOUCHING, "expected well-separated panels, found touching pair");
+    if (h & kFlagMissing) return fail(H2B_ERR_MISSING, "panel pair missing from the singular table");
+    if (h & kFlagNonFinite) return fail(H2B_ERR_NONFINITE, "non-finite nearfield entries");
+    return ok();
+}
+
+int alloc_flags(int** d, cudaStream_t st) {
+    H2B_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(d), sizeof(int), st));
+    H2B_CUDA_TRY(cudaMemsetAsync(*d, 0, sizeof(int), st));
+    return ok();
+}
+
+template <int Q, int JC>
+int launch_slp(const h2b_mesh* m, const double* P, const h2b_jobs* jobs, const h2b_touch* t,
+               const double* tv, double* out, int* flags, cudaStream_t st) {
+    const size_t sm = (size_t)10 * Q * kTile * sizeof(double) + (size_t)8 * kTile * sizeof(int);
+    auto kern = k_blocks_slp<Q, JC>;
+    H2B_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    const int64_t nj = jobs->n_jobs;
+    for (int64_t j0 = 0; j0 < nj; j0 += 2147483647LL) {
+        const unsigned g = (unsigned)std::min<int64_t>(nj - j0, 2147483647LL);
+        kern<<<g, 256, sm, st>>>(P, m->n_triangles, m->d_triangles, jobs->d_jobs + 6 * j0, jobs->d_row_idx,
+                                 jobs->d_col_idx, t ? t->d_row_ptr : nullptr, t ? t->d_col : nullptr, tv,
+                                 out, flags);
+    }
+    H2B_CUDA_TRY(cudaGetLastError());
+    return ok();
+}
+
+template <int Q>
+int launch_dlp(const h2b_mesh* m, const double* P, const h2b_dlp_jobs* jobs, const h2b_touch* t,
+               const double* tv, double* out, int* flags, cudaStream_t st) {
+    const size_t sm = (size_t)(5 * Q * kTile + 6 * Q * kDlpMaxPanels + 3 * kDlpMaxPanels +
+                               kDlpRowChunk * kDlpMaxPanels * 3) * sizeof(double) +
+                      (size_t)(4 * kTile + 4 * kDlpMaxPanels) * sizeof(int);
+    auto kern = k_blocks_dlp<Q>;
+    H2B_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    if (jobs->n_jobs > 0)
+        kern<<<(unsigned)jobs->n_jobs, 256, sm, st>>>(P, m->n_triangles, m->d_triangles, m->d_normals,
+                                                      jobs->d_jobs, jobs->d_row_idx, jobs->d_pan_idx,
+                                                      jobs->d_inc_ptr, jobs->d_inc, jobs->d_inc_base,
+                                                      t ? t->d_row_ptr : nullptr, t ? t->d_col : nullptr,
+                                                      tv, out, flags);
+    H2B_CUDA_TRY(cudaGetLastError());
+    return ok();
+}
+
+}  // namespace
+}  // namespace h2b
+
+using namespace h2b;
+
+extern "C" int h2b_panel_points(const h2b_mesh* m, const double* d_rule_xy, const double* d_rule_w,
+                                int32_t Q, double* d_out, void* stream) {
+    if (!m || !d_rule_xy || !d_rule_w || !d_out || Q < 1) return fail(H2B_ERR_INVALID, "h2b_panel_points: bad argument");
+    const int64_t n = m->n_triangles * Q;
+    if (n == 0) return ok();
+    k_panel_points<<<(unsigned)((n + 255) / 256), 256, 0, as_stream(stream)>>>(
+        m->d_vertices, m->d_triangles, m->d_areas, m->n_triangles, d_rule_xy, d_rule_w, Q, d_out);
+    H2B_CUDA_TRY(cudaGetLastError());
+    return ok();
+}
+
+extern "C" int h2b_touch_count(const h2b_mesh* m, int64_t* d_row_ptr, int64_t* h_case_count, void* stream) {
+    if (!m || !d_row_ptr || !h_case_count) return fail(H2B_ERR_INVALID, "h2b_touch_count: bad argument");
+    cudaStream_t st = as_stream(stream);
+    const int64_t F = m->n_triangles;
+    int* flags;
+    if (int rc = alloc_flags(&flags, st)) return rc;
+    unsigned long long* cc;
+    int64_t* counts;
+    H2B_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&cc), 4 * sizeof(unsigned long long), st));
+    H2B_CUDA_TRY(cudaMemsetAsync(cc, 0, 4 * sizeof(unsigned long long), st));
+    H2B_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&counts), (F + 1) * sizeof(int64_t), st));
+    H2B_CUDA_TRY(cudaMemsetAsync(counts, 0, (F + 1) * sizeof(int64_t), st));
+    if (F > 0)
+        k_touch_count<<<(unsigned)((F + 127) / 128), 128, 0, st>>>(m->d_triangles, F, m->d_vt_ptr, m->d_vt_idx,
+                                                                  counts, cc, flags);
+    H2B_CUDA_TRY(cudaGetLastError());
+    size_t tmp_bytes = 0;
+    H2B_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, d_row_ptr, F + 1, st));
+    void* tmp;
+    H2B_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, st));
+    H2B_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, d_row_ptr, F + 1, st));
+    unsigned long long hc[4];
+    H2B_CUDA_TRY(cudaMemcpyAsync(hc, cc, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    H2B_CUDA_TRY(cudaFreeAsync(tmp, st));
+    H2B_CUDA_TRY(cudaFreeAsync(counts, st));
+    H2B_CUDA_TRY(cudaFreeAsync(cc, st));
+    if (int rc = check_flags(flags, st)) return rc;  // synchronises
+    h_case_count[0] = (int64_t)hc[H2B_IDENTICAL];
+    h_case_count[1] = (int64_t)hc[H2B_EDGE];
+    h_case_count[2] = (int64_t)hc[H2B_VERTEX];
+    h_case_count[3] = (int64_t)(hc[1] + hc[2] + hc[3]);
+    return ok();
+}
+
+extern "C" int h2b_touch_fill(const h2b_mesh* m, const int64_t* d_row_ptr, const int64_t* h_case_count,
+                              int32_t* d_col, int32_t* d_info, int32_t* d_case_list, void* stream) {
+    if (!m || !d_row_ptr || !h_case_count || !d_col || !d_info || !d_case_list)
+        return fail(H2B_ERR_INVALID, "h2b_touch_fill: bad argument");
+    cudaStream_t st = as_stream(stream);
+    const int64_t F = m->n_triangles;
+    int* flags;
+    if (int rc = alloc_flags(&flags, st)) return rc;
+    unsigned long long hcur[3] = {0ull, (unsigned long long)h_case_count[0],
+                                  (unsigned long long)(h_case_count[0] + h_case_count[1])};
+    unsigned long long* cur;
+    H2B_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&cur), sizeof(hcur), st));
+    H2B_CUDA_TRY(cudaMemcpyAsync(cur, hcur, sizeof(hcur), cudaMemcpyHostToDevice, st));
+    if (F > 0)
+        k_touch_fill<<<(unsigned)((F + 127) / 128), 128, 0, st>>>(m->d_triangles, F, m->d_vt_ptr, m->d_vt_idx,
+                                                                 d_row_ptr, d_col, d_info, d_case_list, cur, flags);
+    H2B_CUDA_TRY(cudaGetLastError());
+    H2B_CUDA_TRY(cudaFreeAsync(cur, st));
+    return check_flags(flags, st);
+}
+
+extern "C" int h2b_singular(const h2b_mesh* m, const h2b_touch* t, int kind, const h2b_rule* rules,
+                            double* d_values, void* stream) {
+    if (!m || !t || !rules || !d_values || !t->h_case_off) return fail(H2B_ERR_INVALID, "h2b_singular: bad argument");
+    if (kind != H2B_SLP && kind != H2B_DLP) return fail(H2B_ERR_INVALID, "h2b_singular: unknown kind");
+    cudaStream_t st = as_stream(stream);
+    if (kind == H2B_DLP) {
+        // identical flat panels: <x - y, n> = 0 identically (kernels.py:278-279)
+        H2B_CUDA_TRY(cudaMemsetAsync(d_values, 0, 3 * sizeof(double) * t->n_pairs, st));
+    }
+    SegSet ss;
+    ss.nseg = 0;
+    int32_t block = 0;
+    // heaviest case first (edge: 5 q^4 points x 2 orientations)
+    const int order[3] = {1, 0, 2};
+    const int kases[3] = {H2B_IDENTICAL, H2B_EDGE, H2B_VERTEX};
+    for (int oi = 0; oi < 3; ++oi) {
+        const int c = order[oi];
+        if (kind == H2B_DLP && c == 0) continue;
+        const int64_t cnt = t->h_case_off[c + 1] - t->h_case_off[c];
+        if (cnt <= 0) continue;
+        SegDesc& sd = ss.s[ss.nseg++];
+        sd.list_off = t->h_case_off[c];
+        sd.count = cnt;
+        sd.first_block = block;
+        sd.n_blocks = (int32_t)((cnt + 127) / 128);
+        sd.p = rules[c].d_p;
+        sd.w = rules[c].d_w;
+        sd.n = rules[c].n;
+        sd.kase = kases[c];
+        block += sd.n_blocks;
+    }
+    if (block > 0) {
+        if (kind == H2B_SLP)
+            k_singular<H2B_SLP><<<block, 128, 0, st>>>(m->d_vertices, m->d_triangles, m->d_normals, m->d_areas,
+                                                       t->d_row_ptr, t->n_panels, t->d_col, t->d_info,
+                                                       t->d_case_list, ss, d_values);
+        else
+            k_singular<H2B_DLP><<<block, 128, 0, st>>>(m->d_vertices, m->d_triangles, m->d_normals, m->d_areas,
+                                                       t->d_row_ptr, t->n_panels, t->d_col, t->d_info,
+                                                       t->d_case_list, ss, d_values);
+        H2B_CUDA_TRY(cudaGetLastError());
+    }
+    return ok();
+}
+
+extern "C" int h2b_pair_blocks_slp(const h2b_mesh* m, const double* d_panel_points, int32_t Q,
+                                   const h2b_jobs* jobs, const h2b_touch* t, const double* d_touch_values,
+                                   double* d_out, void* stream) {
+    if (!m || !d_panel_points || !jobs || !d_out) return fail(H2B_ERR_INVALID, "h2b_pair_blocks_slp: bad argument");
+    if (t && !d_touch_values) return fail(H2B_ERR_INVALID, "h2b_pair_blocks_slp: table without values");
+    if (jobs->n_jobs == 0) return ok();
+    cudaStream_t st = as_stream(stream);
+    int* flags;
+    if (int rc = alloc_flags(&flags, st)) return rc;
+    int rc;
+    switch (Q) {
+        case 1: rc = launch_slp<1, 1>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
+        case 4: rc = launch_slp<4, 4>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
+        case 9: rc = launch_slp<9, 9>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
+        case 16: rc = launch_slp<16, 8>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
+        case 25: rc = launch_slp<25, 5>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
+        default: rc = fail(H2B_ERR_INVALID, "h2b_pair_blocks_slp: supported regular orders q = 1..5");
+    }
+    if (rc) return rc;
+    return check_flags(flags, st);
+}
+
+extern "C" int h2b_pair_blocks_dlp(const h2b_mesh* m, const double* d_panel_points, const double* d_lam,
+                                   int32_t Q, const h2b_dlp_jobs* jobs, const h2b_touch* t,
+                                   const double* d_touch_values, double* d_out, void* stream) {
+    if (!m || !d_panel_points || !jobs || !d_out || !d_lam) return fail(H2B_ERR_INVALID, "h2b_pair_blocks_dlp: bad argument");
+    if (t && !d_touch_values) return fail(H2B_ERR_INVALID, "h2b_pair_blocks_dlp: table without values");
+    if (Q > 64) return fail(H2B_ERR_INVALID, "h2b_pair_blocks_dlp: Q > 64");
+    if (jobs->n_jobs == 0) return ok();
+    cudaStream_t st = as_stream(stream);
+    H2B_CUDA_TRY(cudaMemcpyToSymbolAsync(c_lam, d_lam, sizeof(double) * 3 * Q, 0, cudaMemcpyDeviceToDevice, st));
+    int* flags;
+    if (int rc = alloc_flags(&flags, st)) return rc;
+    int rc;
+    switch (Q) {
+        case 1: rc = launch_dlp<1>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
+        case 4: rc = launch_dlp<4>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
+        case 9: rc = launch_dlp<9>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
+        case 16: rc = launch_dlp<16>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
+        default: rc = fail(H2B_ERR_INVALID, "h2b_pair_blocks_dlp: supported regular orders q = 1..4");
+    }
+    if (rc) return rc;
+    return check_flags(flags, st);
+}
