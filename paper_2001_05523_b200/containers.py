@@ -1,0 +1,625 @@
+"""Operators and containers.  API of h2bem.containers (containers.py:1-328).
+
+Device layout (HBM) of an H^2 operator, built once from the block tree and
+the bases:
+
+  D  nearfield, one row-major |t| x C_t matrix per row leaf t whose columns are
+     its near blocks side by side (near-list order), C_t padded to even so rows
+     start 16-byte aligned;
+  S  couplings, one row-major k_t x K_t matrix per row cluster t, far blocks
+     side by side (far-list order), K_t padded to even;
+  V  leaf bases |t| x k_t, E transfer matrices k_child x k_parent (row-major).
+
+The matvec streams D and S row by row (libh2b k_backward) and V/E once each
+way; per-block numpy views for the reference API (`.near`, `.far`) are cut
+from host copies on demand.
+"""
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from . import device as D
+from . import kernels
+from . import quadrature as quad
+
+ORACLE_CAP = 4096
+
+
+class AssemblyContext:
+    """Per-mesh caches: device mesh, regular panel points per order, touching
+    table and singular integrals per (kind, order) (containers.py:14-45)."""
+
+    def __init__(self, mesh):
+        self.mesh = mesh
+        self._dmesh = None
+        self._host_pq = {}
+        self._singular = {}
+
+    @property
+    def dmesh(self):
+        if self._dmesh is None:
+            self._dmesh = kernels.DeviceMesh(self.mesh)
+        return self._dmesh
+
+    @property
+    def vertex_tris(self):
+        return self.mesh.vertex_triangles()
+
+    def host_panel_quad(self, q):
+        """Host panel points (GCA Green columns); reference: panel_quad(q)."""
+        if q not in self._host_pq:
+            self._host_pq[q] = quad.triangle_points(self.mesh, np.arange(self.mesh.n_triangles), q)
+        return self._host_pq[q]
+
+    panel_quad = host_panel_quad
+
+    def singular_table(self, kind, q):
+        kind = kernels.SLP if kind == kernels.HYP else kind
+        key = (kind, q)
+        if key not in self._singular:
+            self._singular[key] = kernels.SingularTable(self.dmesh, kind, q)
+        return self._singular[key]
+
+    def incident_panels(self, verts):
+        ptr, idx = self.mesh.vertex_triangle_csr()
+        verts = np.asarray(verts, dtype=np.int64)
+        if len(verts) == 0:
+            return np.empty(0, dtype=np.int64)
+        return np.unique(np.concatenate([idx[ptr[v] : ptr[v + 1]] for v in verts]))
+
+
+def _blocks_to_device(ctx, kind, blocks, q, q_singular, require_disjoint, out):
+    """Run (row dofs, col dofs, out_off, ld) dense blocks through the kernels."""
+    table = None if require_disjoint else ctx.singular_table(kind, q_singular)
+    if kind == kernels.SLP:
+        ri = np.concatenate([np.asarray(b[0], dtype=np.int64) for b in blocks]) if blocks else np.zeros(0)
+        ci = np.concatenate([np.asarray(b[1], dtype=np.int64) for b in blocks]) if blocks else np.zeros(0)
+        jobs = []
+        r0 = c0 = 0
+        for rows, cols, off, ld in blocks:
+            jobs.append((r0, len(rows), c0, len(cols), off, ld))
+            r0 += len(rows)
+            c0 += len(cols)
+        kernels.run_slp_jobs(ctx.dmesh, q, np.array(jobs, dtype=np.int64).reshape(-1, 6), ri.astype(np.int32),
+                             ci.astype(np.int32), table, out)
+    elif kind == kernels.DLP:
+        kernels.run_dlp_jobs(ctx.dmesh, q, kernels.build_dlp_jobs(ctx.mesh, blocks), table, out)
+    else:
+        raise ValueError(f"unknown operator kind {kind!r}")
+
+
+def dense_block(ctx, kind, row_dofs, col_dofs, q, require_disjoint=False, q_singular=None):
+    """Dense Galerkin block over original dof lists (containers.py:48-66)."""
+    if kind not in (kernels.SLP, kernels.DLP):
+        raise ValueError(f"unknown operator kind {kind!r}")
+    rows = np.asarray(row_dofs, dtype=np.int64)
+    cols = np.asarray(col_dofs, dtype=np.int64)
+    out = D.zeros((max(len(rows) * len(cols), 1),))
+    if len(rows) and len(cols):
+        _blocks_to_device(ctx, kind, [(rows, cols, 0, len(cols))], q, q if q_singular is None else q_singular,
+                          require_disjoint, out)
+    return D.host(out)[: len(rows) * len(cols)].reshape(len(rows), len(cols))
+
+
+def assemble_dense(ctx, kind, q, cap=ORACLE_CAP, q_singular=None):
+    mesh = ctx.mesh
+    nr = mesh.n_triangles
+    nc = mesh.n_triangles if kind == kernels.SLP else mesh.n_vertices
+    if max(nr, nc) > cap:
+        raise ValueError(f"dense oracle dimension {max(nr, nc)} exceeds cap {cap}")
+    return dense_block(ctx, kind, np.arange(nr), np.arange(nc), q, q_singular=q_singular)
+
+
+# ---------------------------------------------------------------------------
+# packed layouts
+
+def _pad2(a):
+    return a + (a & 1)
+
+
+class NearLayout:
+    """Per-row-leaf packing of the nearfield blocks."""
+
+    def __init__(self, bt):
+        rt, ct = bt.row_tree, bt.col_tree
+        nu = bt.near_uids
+        self.n_blocks = len(nu)
+        order = np.argsort(nu[:, 0], kind="stable")
+        su = nu[order]
+        rows, cols = su[:, 0], su[:, 1]
+        width = ct.end[cols] - ct.start[cols]
+        nr_nodes = rt.n_nodes
+        cnt = np.bincount(rows, minlength=nr_nodes)
+        ptr = np.zeros(nr_nodes + 1, dtype=np.int64)
+        np.cumsum(cnt, out=ptr[1:])
+        wsum = np.zeros(nr_nodes + 1, dtype=np.int64)
+        np.cumsum(np.bincount(rows, weights=width, minlength=nr_nodes).astype(np.int64), out=wsum[1:])
+        C = _pad2(np.diff(wsum))
+        # column offset of each block inside its row's matrix
+        coloff = np.cumsum(width) - width - wsum[rows]
+        height = rt.end - rt.start
+        size = height * C
+        off = np.zeros(nr_nodes + 1, dtype=np.int64)
+        np.cumsum(size, out=off[1:])
+        self.total = int(off[-1])
+        self.C, self.off, self.ptr, self.col = C, off[:-1], ptr, cols
+        # per block in reference near order
+        inv = np.empty_like(order)
+        inv[order] = np.arange(len(order))
+        self.blk_off = (off[:-1][rows] + coloff)[inv]
+        self.blk_ld = C[rows][inv]
+        self.blk_rows = (rt.end - rt.start)[nu[:, 0]]
+        self.blk_cols = (ct.end - ct.start)[nu[:, 1]]
+        self.entries = int((self.blk_rows * self.blk_cols).sum())
+
+
+class FarLayout:
+    """Per-row-cluster packing of the coupling matrices (needs ranks)."""
+
+    def __init__(self, bt, rank_r, rank_c):
+        fu = bt.far_uids
+        self.n_blocks = len(fu)
+        nr_nodes = bt.row_tree.n_nodes
+        order = np.argsort(fu[:, 0], kind="stable") if len(fu) else np.zeros(0, dtype=np.int64)
+        su = fu[order]
+        rows, cols = su[:, 0], su[:, 1]
+        width = rank_c[cols]
+        cnt = np.bincount(rows, minlength=nr_nodes)
+        ptr = np.zeros(nr_nodes + 1, dtype=np.int64)
+        np.cumsum(cnt, out=ptr[1:])
+        wsum = np.zeros(nr_nodes + 1, dtype=np.int64)
+        np.cumsum(np.bincount(rows, weights=width, minlength=nr_nodes).astype(np.int64), out=wsum[1:])
+        K = _pad2(np.diff(wsum))
+        coloff = np.cumsum(width) - width - wsum[rows]
+        size = rank_r * K
+        off = np.zeros(nr_nodes + 1, dtype=np.int64)
+        np.cumsum(size, out=off[1:])
+        self.total = int(off[-1])
+        self.K, self.off, self.ptr, self.col = K, off[:-1], ptr, cols
+        inv = np.empty_like(order)
+        inv[order] = np.arange(len(order))
+        self.blk_off = (off[:-1][rows] + coloff)[inv] if len(fu) else np.zeros(0, dtype=np.int64)
+        self.blk_ld = K[rows][inv] if len(fu) else np.zeros(0, dtype=np.int64)
+        self.blk_rows = rank_r[fu[:, 0]] if len(fu) else np.zeros(0, dtype=np.int64)
+        self.blk_cols = rank_c[fu[:, 1]] if len(fu) else np.zeros(0, dtype=np.int64)
+        self.entries = int((self.blk_rows * self.blk_cols).sum())
+
+
+def near_layout(bt):
+    if getattr(bt, "_near_layout", None) is None:
+        bt._near_layout = NearLayout(bt)
+    return bt._near_layout
+
+
+def _near_blocks(bt, lay):
+    rt, ct = bt.row_tree, bt.col_tree
+    return [
+        (rt.perm[rt.start[t] : rt.end[t]], ct.perm[ct.start[s] : ct.end[s]], int(lay.blk_off[i]), int(lay.blk_ld[i]))
+        for i, (t, s) in enumerate(bt.near_uids)
+    ]
+
+
+def assemble_nearfield_device(ctx, kind, bt, q, q_singular=None, cache=None):
+    """Packed device nearfield D (see module docstring)."""
+    qs = q if q_singular is None else q_singular
+    key = ("packed", kind, q, qs, id(bt))
+    if cache is not None and key in cache:
+        return cache[key]
+    lay = near_layout(bt)
+    out = D.zeros((max(lay.total, 1),))
+    if kind == kernels.SLP:
+        rt, ct = bt.row_tree, bt.col_tree
+        nu = bt.near_uids
+        jobs = np.stack([rt.start[nu[:, 0]], lay.blk_rows, ct.start[nu[:, 1]], lay.blk_cols, lay.blk_off,
+                         lay.blk_ld], axis=1)
+        kernels.run_slp_jobs(ctx.dmesh, q, jobs, rt.perm.astype(np.int32), ct.perm.astype(np.int32),
+                             ctx.singular_table(kind, qs), out)
+    else:
+        _blocks_to_device(ctx, kind, _near_blocks(bt, lay), q, qs, False, out)
+    if cache is not None:
+        cache[key] = out
+    return out
+
+
+def assemble_nearfield(ctx, kind, block_tree, q, cache=None, threads=1, q_singular=None):
+    """Dense nearfield payloads in block order (containers.py:79-98); computed
+    on the device, returned as host arrays.  Raises FloatingPointError on a
+    non-finite entry."""
+    out = assemble_nearfield_device(ctx, kind, block_tree, q, q_singular, cache)
+    lay = near_layout(block_tree)
+    h = D.host(out)
+    return [_view(h, lay.blk_off[i], lay.blk_rows[i], lay.blk_cols[i], lay.blk_ld[i]) for i in range(lay.n_blocks)]
+
+
+def _view(flat, off, nr, nc, ld):
+    off, nr, nc, ld = int(off), int(nr), int(nc), int(ld)
+    if nr == 0 or nc == 0:
+        return np.zeros((nr, nc))
+    return np.lib.stride_tricks.as_strided(flat[off:], shape=(nr, nc), strides=(8 * ld, 8)).copy()
+
+
+def _pivots_concat(basis, n_nodes):
+    ranks = np.array([basis.rank[u] for u in range(n_nodes)], dtype=np.int64)
+    off = np.zeros(n_nodes + 1, dtype=np.int64)
+    np.cumsum(ranks, out=off[1:])
+    piv = np.concatenate([np.asarray(basis.pivots[u], dtype=np.int64) for u in range(n_nodes)]) if n_nodes else []
+    return ranks, off, np.asarray(piv, dtype=np.int64)
+
+
+def assemble_couplings(ctx, kind, bt, row_basis, col_basis, q):
+    """Packed device couplings S_b = G[pivots_t, pivots_s] (gca.py:198-203)."""
+    rr, roff, rpiv = _pivots_concat(row_basis, bt.row_tree.n_nodes)
+    cr, coff, cpiv = _pivots_concat(col_basis, bt.col_tree.n_nodes)
+    lay = FarLayout(bt, rr, cr)
+    out = D.zeros((max(lay.total, 1),))
+    fu = bt.far_uids
+    if len(fu):
+        if kind == kernels.SLP:
+            jobs = np.stack([roff[fu[:, 0]], lay.blk_rows, coff[fu[:, 1]], lay.blk_cols, lay.blk_off, lay.blk_ld],
+                            axis=1)
+            kernels.run_slp_jobs(ctx.dmesh, q, jobs, rpiv.astype(np.int32), cpiv.astype(np.int32), None, out)
+        else:
+            blocks = [(rpiv[roff[t] : roff[t + 1]], cpiv[coff[s] : coff[s + 1]], int(lay.blk_off[i]),
+                       int(lay.blk_ld[i])) for i, (t, s) in enumerate(fu)]
+            _blocks_to_device(ctx, kind, blocks, q, q, True, out)
+    return out
+
+
+# ---------------------------------------------------------------------------
+
+class DenseOperator:
+    def __init__(self, matrix):
+        self.matrix = matrix
+        self.shape = matrix.shape
+
+    def matvec(self, x):
+        return self.matrix @ x
+
+    def rmatvec(self, x):
+        return self.matrix.T @ x
+
+    def diagonal(self):
+        return np.diag(self.matrix).copy()
+
+    def to_dense(self):
+        return self.matrix
+
+    def storage_report(self):
+        return {"basis": 0, "coupling": 0, "lowrank": 0, "nearfield": 8 * self.matrix.size}
+
+
+class ClusterBasis:
+    """Nested cluster basis: V[leaf uid] (|t| x k_t), E[child uid]
+    (k_child x k_parent), rank and pivots per uid (containers.py:189-238)."""
+
+    def __init__(self, tree):
+        self.tree = tree
+        self.V = {}
+        self.E = {}
+        self.rank = {}
+        self.pivots = {}
+
+    def expand(self, cluster):
+        """Dense V_t through the transfer matrices (testing aid)."""
+        if cluster.is_leaf:
+            return self.V[cluster.uid]
+        return np.vstack([self.expand(ch) @ self.E[ch.uid] for ch in cluster.children])
+
+    def storage_floats(self):
+        return sum(v.size for v in self.V.values()) + sum(e.size for e in self.E.values())
+
+    def forward(self, xp):
+        """x_hat_t = V_t^T x|_t for every cluster, on the device (permuted input)."""
+        return _basis_transform(self, np.asarray(xp, dtype=float))
+
+    def packed(self):
+        """(ranks, V flat, v_off, E flat, e_off, hat_off) in uid order; cached."""
+        if getattr(self, "_packed", None) is None:
+            t = self.tree
+            n = t.n_nodes
+            ranks = np.array([self.rank[u] for u in range(n)], dtype=np.int64)
+            v_off = np.full(n, -1, dtype=np.int64)
+            e_off = np.full(n, -1, dtype=np.int64)
+            vs, es = [], []
+            pos = 0
+            for u in t.leaf_uids():
+                v_off[u] = pos
+                vs.append(np.ascontiguousarray(self.V[u]).ravel())
+                pos += vs[-1].size
+            pos = 0
+            for u in range(n):
+                if t.parent_of[u] >= 0:
+                    e_off[u] = pos
+                    es.append(np.ascontiguousarray(self.E[u]).ravel())
+                    pos += es[-1].size
+            hat = np.zeros(n + 1, dtype=np.int64)
+            np.cumsum(ranks, out=hat[1:])
+            self._packed = (ranks, np.concatenate(vs) if vs else np.zeros(1), v_off,
+                            np.concatenate(es) if es else np.zeros(1), e_off, hat)
+        return self._packed
+
+
+def _basis_transform(basis, xp):
+    """Forward transform via a matvec plan with no far/near blocks reading out
+    x_hat (device path; used by the reference-API ClusterBasis.forward)."""
+    raise NotImplementedError("ClusterBasis.forward: use H2Matrix.forward_coefficients (device)")
+
+
+class _DeviceBasis:
+    def __init__(self, basis):
+        ranks, V, v_off, E, e_off, hat = basis.packed()
+        self.ranks = ranks
+        self.V = D.dev(V)
+        self.E = D.dev(E)
+        self.v_off = v_off
+        self.e_off = e_off
+        self.hat = hat
+
+
+class H2Matrix:
+    """Device-resident H^2 operator (containers.py:241-324).  matvec accepts a
+    numpy array (copied in/out) or a CUDA tensor (zero-copy) in natural dof
+    order and returns the same type."""
+
+    def __init__(self, block_tree, row_basis, col_basis, couplings, near_payloads):
+        """Reference constructor from host payload lists (block-tree order)."""
+        rr = np.array([row_basis.rank[u] for u in range(block_tree.row_tree.n_nodes)], dtype=np.int64)
+        cr = np.array([col_basis.rank[u] for u in range(block_tree.col_tree.n_nodes)], dtype=np.int64)
+        fl = FarLayout(block_tree, rr, cr)
+        nl = near_layout(block_tree)
+        S = np.zeros(max(fl.total, 1))
+        Dn = np.zeros(max(nl.total, 1))
+        for i, s in enumerate(couplings):
+            _scatter(S, fl.blk_off[i], fl.blk_ld[i], np.asarray(s, dtype=float))
+        for i, d in enumerate(near_payloads):
+            _scatter(Dn, nl.blk_off[i], nl.blk_ld[i], np.asarray(d, dtype=float))
+        self._init(block_tree, row_basis, col_basis, D.dev(S), D.dev(Dn), fl)
+
+    @classmethod
+    def from_device(cls, block_tree, row_basis, col_basis, S, Dn):
+        self = cls.__new__(cls)
+        rr = np.array([row_basis.rank[u] for u in range(block_tree.row_tree.n_nodes)], dtype=np.int64)
+        cr = np.array([col_basis.rank[u] for u in range(block_tree.col_tree.n_nodes)], dtype=np.int64)
+        self._init(block_tree, row_basis, col_basis, S, Dn, FarLayout(block_tree, rr, cr))
+        return self
+
+    def _init(self, bt, rb, cb, S, Dn, far_layout):
+        self.block_tree = bt
+        self.row_tree = bt.row_tree
+        self.col_tree = bt.col_tree
+        self.row_basis = rb
+        self.col_basis = cb
+        self.shape = (self.row_tree.n_dofs, self.col_tree.n_dofs)
+        self.S_dev = S
+        self.D_dev = Dn
+        self.far_layout = far_layout
+        self.near_layout = near_layout(bt)
+        self._plan = None
+        self._tplan = None
+        self._far = None
+        self._near = None
+
+    # -- reference attribute views ------------------------------------------------
+    @property
+    def far(self):
+        if self._far is None:
+            h = D.host(self.S_dev)
+            fl = self.far_layout
+            self._far = [(b, _view(h, fl.blk_off[i], fl.blk_rows[i], fl.blk_cols[i], fl.blk_ld[i]))
+                         for i, b in enumerate(self.block_tree.far)]
+        return self._far
+
+    @property
+    def near(self):
+        if self._near is None:
+            h = D.host(self.D_dev)
+            nl = self.near_layout
+            self._near = [(b, _view(h, nl.blk_off[i], nl.blk_rows[i], nl.blk_cols[i], nl.blk_ld[i]))
+                          for i, b in enumerate(self.block_tree.near)]
+        return self._near
+
+    # -- device plan ----------------------------------------------------------------
+    def plan(self):
+        if self._plan is None:
+            self._plan = MatvecPlan(self.block_tree, self.row_basis, self.col_basis, self.S_dev, self.D_dev,
+                                    self.far_layout, self.near_layout)
+        return self._plan
+
+    def matvec(self, x):
+        return self.plan().apply(x)
+
+    def rmatvec(self, x):
+        if self._tplan is None:
+            self._tplan = _transposed_plan(self)
+        return self._tplan.apply(x)
+
+    def diagonal(self):
+        assert self.shape[0] == self.shape[1], "diagonal extraction requires a square operator"
+        return self.plan().diagonal()
+
+    def to_dense(self):
+        n = self.shape[1]
+        out = np.empty((self.shape[0], n))
+        eye = np.zeros(n)
+        for j in range(n):
+            eye[j] = 1.0
+            out[:, j] = self.matvec(eye)
+            eye[j] = 0.0
+        return out
+
+    def rank_stats(self):
+        if self.far_layout.n_blocks == 0:
+            return {"max": 0, "mean": 0.0}
+        flat = np.concatenate([self.far_layout.blk_rows, self.far_layout.blk_cols])
+        return {"max": int(flat.max()), "mean": float(flat.mean())}
+
+    def storage_report(self):
+        basis = self.row_basis.storage_floats()
+        if self.col_basis is not self.row_basis:
+            basis += self.col_basis.storage_floats()
+        return {"basis": 8 * basis, "coupling": 8 * self.far_layout.entries, "lowrank": 0,
+                "nearfield": 8 * self.near_layout.entries}
+
+    def matvec_bytes(self):
+        """Algorithmic HBM bytes of one matvec: every operator
+        entry once, each basis in both roles, plus x and y."""
+        basis_r = self.row_basis.storage_floats()
+        basis_c = self.col_basis.storage_floats()
+        return 8 * (self.near_layout.entries + self.far_layout.entries + basis_r + basis_c + self.shape[0]
+                    + self.shape[1])
+
+
+def _scatter(flat, off, ld, block):
+    nr, nc = block.shape
+    if nr == 0 or nc == 0:
+        return
+    view = np.lib.stride_tricks.as_strided(flat[int(off):], shape=(nr, nc), strides=(8 * int(ld), 8))
+    view[...] = block
+
+
+class MatvecPlan:
+    """Device layout + libh2b plan for y = A x."""
+
+    def __init__(self, bt, rb, cb, S, Dn, fl, nl, owned=None):
+        t = D.require_cuda()
+        rt, ct = bt.row_tree, bt.col_tree
+        self.n_rows, self.n_cols = rt.n_dofs, ct.n_dofs
+        self._rb = _DeviceBasis(rb)
+        self._cb = self._rb if cb is rb else _DeviceBasis(cb)
+        i32 = np.int32
+        keep = {}
+
+        def put(name, arr, dtype):
+            keep[name] = D.dev(arr, dtype)
+            return keep[name].data_ptr()
+
+        cbd, rbd = self._cb, self._rb
+        c_child = np.stack([ct.left, ct.right], axis=1)
+        c_leaves = ct.leaf_uids()
+        r_order = np.argsort(rt.depth_of, kind="stable")
+        r_vo = rbd.v_off.copy()
+        lay = _lib.Layout()
+        lay.n_rows, lay.n_cols = self.n_rows, self.n_cols
+        lay.col_perm = put("col_perm", ct.perm, np.int64)
+        lay.row_perm = put("row_perm", rt.perm, np.int64)
+        lay.c_nodes, lay.c_leaves = ct.n_nodes, len(c_leaves)
+        lay.c_parent = put("c_parent", ct.parent_of, i32)
+        lay.c_child = put("c_child", c_child, i32)
+        lay.c_start = put("c_start", ct.start, i32)
+        lay.c_size = put("c_size", ct.end - ct.start, i32)
+        lay.c_rank = put("c_rank", cbd.ranks, i32)
+        lay.c_v_off = put("c_v_off", cbd.v_off, np.int64)
+        lay.c_e_off = put("c_e_off", cbd.e_off, np.int64)
+        lay.c_xhat_off = put("c_xhat_off", cbd.hat[:-1], np.int64)
+        lay.c_leaf_list = put("c_leaf_list", c_leaves, i32)
+        lay.c_V, lay.c_E = cbd.V.data_ptr(), cbd.E.data_ptr()
+        lay.xhat_len = int(cbd.hat[-1])
+        lay.r_nodes, lay.r_leaves = rt.n_nodes, len(rt.leaf_uids())
+        lay.r_parent = put("r_parent", rt.parent_of, i32)
+        lay.r_start = put("r_start", rt.start, i32)
+        lay.r_size = put("r_size", rt.end - rt.start, i32)
+        lay.r_rank = put("r_rank", rbd.ranks, i32)
+        lay.r_v_off = put("r_v_off", r_vo, np.int64)
+        lay.r_e_off = put("r_e_off", rbd.e_off, np.int64)
+        lay.r_yhat_off = put("r_yhat_off", rbd.hat[:-1], np.int64)
+        lay.r_order = put("r_order", r_order, i32)
+        lay.r_V, lay.r_E = rbd.V.data_ptr(), rbd.E.data_ptr()
+        lay.yhat_len = int(rbd.hat[-1])
+        lay.s_off = put("s_off", fl.off, np.int64)
+        lay.s_cols = put("s_cols", fl.K, i32)
+        lay.far_ptr = put("far_ptr", fl.ptr, i32)
+        lay.far_col = put("far_col", fl.col if len(fl.col) else np.zeros(1), i32)
+        lay.S = S.data_ptr()
+        lay.d_off = put("d_off", nl.off, np.int64)
+        lay.d_cols = put("d_cols", nl.C, i32)
+        lay.near_ptr = put("near_ptr", nl.ptr, i32)
+        lay.near_col = put("near_col", nl.col if len(nl.col) else np.zeros(1), i32)
+        lay.D = Dn.data_ptr()
+        if owned is not None:
+            lay.n_owned = len(owned)
+            lay.owned = put("owned", owned, i32)
+        else:
+            lay.n_owned = 0
+            lay.owned = None
+        self._keep = keep
+        self._S, self._D = S, Dn
+        self.layout = lay
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().h2b_plan_create(ctypes.byref(lay), ctypes.byref(h)))
+        self.handle = h
+        self._torch = t
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                _lib.lib().h2b_plan_destroy(h)
+            except Exception:
+                pass
+
+    def apply_device(self, x, y=None, stream=None):
+        """y = A x for CUDA float64 tensors (natural order), stream-ordered."""
+        t = self._torch
+        if y is None:
+            y = t.empty(self.n_rows, dtype=t.float64, device=x.device)
+        _lib.check(_lib.lib().h2b_matvec(self.handle, x.data_ptr(), y.data_ptr(), _lib.stream_ptr(stream)))
+        return y
+
+    def apply(self, x):
+        t = self._torch
+        if isinstance(x, t.Tensor):
+            if x.dtype != t.float64 or not x.is_cuda:
+                raise ValueError("expected a CUDA float64 tensor")
+            return self.apply_device(x.contiguous())
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        if x.ndim != 1 or len(x) != self.n_cols:
+            raise ValueError(f"expected a vector of length {self.n_cols}")
+        y = np.empty(self.n_rows)
+        _lib.check(_lib.lib().h2b_matvec_host(self.handle, _lib.ptr(x), _lib.ptr(y), _lib.stream_ptr()))
+        return y
+
+    def diagonal(self):
+        d = D.zeros((self.n_rows,))
+        _lib.check(_lib.lib().h2b_diagonal(self.handle, d.data_ptr(), _lib.stream_ptr()))
+        return D.host(d)
+
+
+def _transposed_plan(H):
+    """Plan for A^T: swapped trees/bases, S_b^T and D_b^T repacked on the device."""
+    from .clustering import BlockTree
+
+    bt = H.block_tree
+    tb = BlockTree.__new__(BlockTree)
+    tb.row_tree, tb.col_tree, tb.eta = bt.col_tree, bt.row_tree, bt.eta
+    tb.far_uids = bt.far_uids[:, ::-1].copy()
+    tb.near_uids = bt.near_uids[:, ::-1].copy()
+    tb._far = tb._near = None
+    rr = np.array([H.col_basis.rank[u] for u in range(tb.row_tree.n_nodes)], dtype=np.int64)
+    cr = np.array([H.row_basis.rank[u] for u in range(tb.col_tree.n_nodes)], dtype=np.int64)
+    fl = FarLayout(tb, rr, cr)
+    nl = NearLayout(tb)
+    St = _transpose_packed(H.S_dev, H.far_layout, fl, max(fl.total, 1))
+    Dt = _transpose_packed(H.D_dev, H.near_layout, nl, max(nl.total, 1))
+    return MatvecPlan(tb, H.col_basis, H.row_basis, St, Dt, fl, nl)
+
+
+def _transpose_packed(src, la, lb, total):
+    """Gather map: entry (i, j) of block b in layout `la` -> (j, i) in `lb`."""
+    t = D.torch()
+    idx = np.zeros(total, dtype=np.int64)
+    mask = np.zeros(total, dtype=bool)
+    for b in range(len(la.blk_off)):
+        nr, nc = int(la.blk_rows[b]), int(la.blk_cols[b])
+        if nr == 0 or nc == 0:
+            continue
+        i = np.arange(nr)[:, None]
+        j = np.arange(nc)[None, :]
+        s = la.blk_off[b] + i * la.blk_ld[b] + j
+        d = lb.blk_off[b] + j * lb.blk_ld[b] + i
+        idx[d.ravel()] = s.ravel()
+        mask[d.ravel()] = True
+    out = src[D.dev(idx)]
+    out[D.dev(~mask)] = 0.0
+    return out.contiguous()

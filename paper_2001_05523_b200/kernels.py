@@ -1,0 +1,278 @@
+"""Galerkin quadrature on the GPU.  API of h2bem.kernels (kernels.py:1-527)
+for the operator kinds on the hot path (SLP, DLP).
+
+Host side of the boundary: uploads the mesh once, builds the touching-pair
+table (h2b_touch_count/fill: every ordered panel pair sharing a vertex with
+its Sauter-Schwab case and vertex permutations), evaluates the singular
+integrals of all touching pairs (h2b_singular) and packs dense-block jobs for
+the pair-block kernels (h2b_pair_blocks_slp / _dlp).  Regular pairs use the
+q_reg^2-point Duffy tensor rule per panel; touching pairs take the singular
+table value (kernels.py:429-433), or make the call fail when the caller
+requires disjoint panels (coupling matrices, kernels.py:441-444, 455-458).
+"""
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from . import device as D
+from . import quadrature as quad
+
+FOUR_PI = 4.0 * np.pi
+
+SLP = "slp"
+DLP = "dlp"
+HYP = "hyp"
+
+K_VALUE = "value"
+K_DN_Z = "dn_z"
+K_DN_X = "dn_x"
+K_DN_X_DN_Z = "dn_x_dn_z"
+
+TILE = 64           # max rows/cols of one device job (kernel tile)
+DLP_MAX_PANELS = 128
+
+_KIND_CODE = {SLP: _lib.H2B_SLP, DLP: _lib.H2B_DLP}
+
+
+def kind_code(kind):
+    if kind not in _KIND_CODE:
+        raise ValueError(f"unknown operator kind {kind!r}")
+    return _KIND_CODE[kind]
+
+
+class DeviceMesh:
+    """Mesh arrays resident in HBM + the ctypes descriptor."""
+
+    def __init__(self, mesh):
+        self.mesh = mesh
+        ptr, idx = mesh.vertex_triangle_csr()
+        self.vertices = D.dev(mesh.vertices, np.float64)
+        self.triangles = D.dev(mesh.triangles, np.int32)
+        self.normals = D.dev(mesh.normals, np.float64)
+        self.areas = D.dev(mesh.areas, np.float64)
+        self.vt_ptr = D.dev(ptr, np.int64)
+        self.vt_idx = D.dev(idx, np.int32)
+        self.c = _lib.Mesh(mesh.n_vertices, mesh.n_triangles, self.vertices.data_ptr(), self.triangles.data_ptr(),
+                           self.normals.data_ptr(), self.areas.data_ptr(), self.vt_ptr.data_ptr(),
+                           self.vt_idx.data_ptr())
+        self._pp = {}
+        self._touch = None
+
+    def panel_points(self, q):
+        """(4, F, q^2) device tensor: x, y, z, weight*2A per rule point."""
+        if q not in self._pp:
+            pts, w = quad.triangle_rule(q)
+            Q = len(w)
+            out = D.empty((4, self.mesh.n_triangles, Q))
+            rxy, rw = D.dev(pts), D.dev(w)
+            _lib.check(_lib.lib().h2b_panel_points(ctypes.byref(self.c), rxy.data_ptr(), rw.data_ptr(), Q,
+                                                   out.data_ptr(), D.stream()))
+            lam = np.column_stack([1.0 - pts[:, 0] - pts[:, 1], pts[:, 0], pts[:, 1]])
+            self._pp[q] = (out, Q, D.dev(lam))
+        return self._pp[q]
+
+    def touch(self):
+        if self._touch is None:
+            self._touch = TouchTable(self)
+        return self._touch
+
+
+class TouchTable:
+    """All ordered touching panel pairs (sharing >= 1 vertex, incl. identical),
+    CSR by row panel with ascending columns -- the reference's sorted keys
+    pa * F + pb (kernels.py:333-343) -- plus case codes and permutations."""
+
+    def __init__(self, dmesh):
+        L = _lib.lib()
+        F = dmesh.mesh.n_triangles
+        self.dmesh = dmesh
+        self.row_ptr = D.empty((F + 1,), "int64")
+        counts = np.zeros(4, dtype=np.int64)
+        _lib.check(L.h2b_touch_count(ctypes.byref(dmesh.c), self.row_ptr.data_ptr(), _lib.ptr(counts), D.stream()))
+        n = int(counts[3])
+        self.n_pairs = n
+        self.case_counts = counts[:3].copy()  # identical, edge, vertex
+        self.col = D.empty((max(n, 1),), "int32")
+        self.info = D.empty((max(n, 1),), "int32")
+        self.case_list = D.empty((max(n, 1),), "int32")
+        _lib.check(L.h2b_touch_fill(ctypes.byref(dmesh.c), self.row_ptr.data_ptr(), _lib.ptr(counts),
+                                    self.col.data_ptr(), self.info.data_ptr(), self.case_list.data_ptr(),
+                                    D.stream()))
+        self.case_off = np.array([0, counts[0], counts[0] + counts[1], n], dtype=np.int64)
+        self.c = _lib.Touch(F, n, self.row_ptr.data_ptr(), self.col.data_ptr(), self.info.data_ptr(),
+                            self.case_list.data_ptr(), _lib.ptr(self.case_off))
+
+    def keys(self):
+        """Sorted int64 keys pa * F + pb (reference SingularTable.keys)."""
+        F = self.dmesh.mesh.n_triangles
+        rp = D.host(self.row_ptr)
+        rows = np.repeat(np.arange(F, dtype=np.int64), np.diff(rp))
+        return rows * F + D.host(self.col[: self.n_pairs]).astype(np.int64)
+
+    def codes_perms(self):
+        """(codes, perms (n, 6)) decoded from the device info words."""
+        info = D.host(self.info[: self.n_pairs]).astype(np.int64)
+        perms = np.stack([(info >> s) & 3 for s in (2, 4, 6, 8, 10, 12)], axis=1)
+        return info & 3, perms
+
+
+class SingularTable:
+    """Sauter-Schwab integrals of every touching pair at order q, on the device
+    (reference: kernels.SingularTable, kernels.py:346-362)."""
+
+    def __init__(self, dmesh, kind, q):
+        L = _lib.lib()
+        self.kind = kind
+        self.q = q
+        self.touch = dmesh.touch()
+        n = self.touch.n_pairs
+        width = 3 if kind == DLP else 1
+        self.values_dev = D.zeros((max(n, 1) * width,))
+        rules = (_lib.Rule * 3)()
+        self._keep = []
+        for i, case in enumerate((quad.IDENTICAL, quad.SHARED_EDGE, quad.SHARED_VERTEX)):
+            r = quad.sauter_schwab_rule(case, q)
+            p, w = D.dev(r.points), D.dev(r.weights)
+            self._keep += [p, w]
+            rules[i] = _lib.Rule(len(r.weights), p.data_ptr(), w.data_ptr())
+        _lib.check(L.h2b_singular(ctypes.byref(dmesh.c), ctypes.byref(self.touch.c), kind_code(kind), rules,
+                                  self.values_dev.data_ptr(), D.stream()))
+        self.n = dmesh.mesh.n_triangles
+        self._keys = None
+
+    @property
+    def keys(self):
+        if self._keys is None:
+            self._keys = self.touch.keys()
+        return self._keys
+
+    @property
+    def values(self):
+        v = D.host(self.values_dev)[: self.touch.n_pairs * (3 if self.kind == DLP else 1)]
+        return v.reshape(-1, 3) if self.kind == DLP else v
+
+    def lookup(self, pa, pb):
+        key = np.asarray(pa, dtype=np.int64) * self.n + np.asarray(pb, dtype=np.int64)
+        pos = np.searchsorted(self.keys, key)
+        safe = np.minimum(pos, len(self.keys) - 1)
+        if not np.array_equal(self.keys[safe], key):
+            raise KeyError("panel pair missing from the singular table")
+        return self.values[safe]
+
+
+# ---------------------------------------------------------------------------
+# job packing
+
+def tile_jobs(jobs):
+    """Split (row_off, nr, col_off, nc, out_off, ld) jobs into <= TILE x TILE tiles."""
+    jobs = np.asarray(jobs, dtype=np.int64).reshape(-1, 6)
+    if len(jobs) == 0 or (jobs[:, 1].max() <= TILE and jobs[:, 3].max() <= TILE):
+        return jobs
+    out = []
+    for r0, nr, c0, nc, o, ld in jobs:
+        for i in range(0, max(nr, 1), TILE):
+            for j in range(0, max(nc, 1), TILE):
+                out.append((r0 + i, min(TILE, nr - i), c0 + j, min(TILE, nc - j), o + i * ld + j, ld))
+    return np.array(out, dtype=np.int64).reshape(-1, 6)
+
+
+def run_slp_jobs(dmesh, q, jobs, row_idx, col_idx, table, out):
+    """Device SLP pair blocks into `out` (device float64)."""
+    jobs = tile_jobs(jobs)
+    if len(jobs) == 0:
+        return
+    pp, Q, _ = dmesh.panel_points(q)
+    dj = D.dev(jobs, np.int64)
+    ri = row_idx if not isinstance(row_idx, np.ndarray) else D.dev(row_idx, np.int32)
+    ci = col_idx if not isinstance(col_idx, np.ndarray) else D.dev(col_idx, np.int32)
+    cj = _lib.Jobs(len(jobs), dj.data_ptr(), ri.data_ptr(), ci.data_ptr())
+    tptr = ctypes.byref(table.touch.c) if table is not None else None
+    tv = table.values_dev.data_ptr() if table is not None else None
+    _lib.check(_lib.lib().h2b_pair_blocks_slp(ctypes.byref(dmesh.c), pp.data_ptr(), Q, ctypes.byref(cj), tptr, tv,
+                                              out.data_ptr(), D.stream()))
+
+
+def build_dlp_jobs(mesh, blocks):
+    """DLP jobs for dense blocks (row panels, column vertices, out_off, ld):
+    the column-panel set of each job is the sorted union of the panels incident
+    to its column vertices (kernels.py:454), tiled so that a job holds at most
+    TILE rows, TILE columns and DLP_MAX_PANELS panels; the incidence CSR lists,
+    per column, (local panel, local vertex) contributions l-major then by
+    panel -- the accumulation order of np.add.at in kernels.dlp_block."""
+    vptr, vidx = mesh.vertex_triangle_csr()
+    tris = mesh.triangles
+    jobs, row_idx, pan_idx, inc_ptr, inc, inc_base = [], [], [], [], [], []
+    nrow = npan = ninc = nptr = 0
+    for rows, cols, out_off, ld in blocks:
+        rows = np.asarray(rows, dtype=np.int64)
+        cols = np.asarray(cols, dtype=np.int64)
+        # column tiles bounded by the panel budget
+        c0 = 0
+        while c0 < len(cols):
+            c1 = min(len(cols), c0 + TILE)
+            while True:
+                sel = cols[c0:c1]
+                pans = np.unique(np.concatenate([vidx[vptr[v] : vptr[v + 1]] for v in sel]))
+                if len(pans) <= DLP_MAX_PANELS or c1 - c0 == 1:
+                    break
+                c1 = c0 + max(1, (c1 - c0) // 2)
+            if len(pans) > DLP_MAX_PANELS:
+                raise ValueError("vertex valence too large for the DLP panel tile")
+            pos = {int(v): i for i, v in enumerate(sel)}
+            trip = []
+            t3 = tris[pans]
+            for l in range(3):
+                for p in range(len(pans)):
+                    c = pos.get(int(t3[p, l]))
+                    if c is not None:
+                        trip.append((c, l, p))
+            trip.sort()
+            counts = np.zeros(len(sel) + 1, dtype=np.int64)
+            for c, _, _ in trip:
+                counts[c + 1] += 1
+            cptr = np.cumsum(counts) + ninc
+            codes = [(p << 2) | l for _, l, p in trip]
+            for r0 in range(0, len(rows), TILE):
+                r1 = min(len(rows), r0 + TILE)
+                jobs.append((nrow, r1 - r0, npan, len(pans), c0, len(sel), out_off + r0 * ld + c0, ld))
+                row_idx.append(rows[r0:r1])
+                nrow += r1 - r0
+                inc_base.append(nptr)
+            pan_idx.append(pans)
+            npan += len(pans)
+            inc_ptr.append(cptr)
+            nptr += len(cptr)
+            inc.extend(codes)
+            ninc += len(codes)
+            c0 = c1
+    if not jobs:
+        return None
+    # jobs of one column tile share pan/inc data; all row tiles point at it
+    return dict(
+        jobs=np.array(jobs, dtype=np.int64),
+        row_idx=np.concatenate(row_idx).astype(np.int32),
+        pan_idx=np.concatenate(pan_idx).astype(np.int32),
+        inc_ptr=np.concatenate(inc_ptr).astype(np.int32),
+        inc=np.array(inc, dtype=np.int32) if inc else np.zeros(1, dtype=np.int32),
+        inc_base=np.array(inc_base, dtype=np.int64),
+    )
+
+
+def run_dlp_jobs(dmesh, q, packed, table, out):
+    if packed is None:
+        return
+    pp, Q, lam = dmesh.panel_points(q)
+    t = {k: D.dev(v) for k, v in packed.items()}
+    cj = _lib.DlpJobs(len(packed["jobs"]), t["jobs"].data_ptr(), t["row_idx"].data_ptr(), t["pan_idx"].data_ptr(),
+                      t["inc_ptr"].data_ptr(), t["inc"].data_ptr(), t["inc_base"].data_ptr())
+    tptr = ctypes.byref(table.touch.c) if table is not None else None
+    tv = table.values_dev.data_ptr() if table is not None else None
+    _lib.check(_lib.lib().h2b_pair_blocks_dlp(ctypes.byref(dmesh.c), pp.data_ptr(), lam.data_ptr(), Q,
+                                              ctypes.byref(cj), tptr, tv, out.data_ptr(), D.stream()))
+
+
+def touching_pairs(mesh):
+    """Sorted keys pa * F + pb of all touching ordered pairs (device classifier)."""
+    return DeviceMesh(mesh).touch().keys()

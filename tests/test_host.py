@@ -1,0 +1,126 @@
+"""Host-side product logic: rules, GCA basis construction, ABI surface."""
+
+import ctypes
+import re
+
+import numpy as np
+import pytest
+
+from paper_2001_05523_b200 import _lib, gca
+from paper_2001_05523_b200 import quadrature as quad
+from paper_2001_05523_b200 import spaces as S
+from paper_2001_05523_b200.containers import AssemblyContext
+from paper_2001_05523_b200.lowrank import aca_inverse_core
+
+from .conftest import ROOT, golden
+from .helpers import sphere, trees
+
+
+def test_product_rules_match_reference_bits():
+    g = golden("rules.npz")
+    for q in range(1, 9):
+        r = quad.gauss_legendre(q)
+        assert np.array_equal(r.points, g[f"gl{q}_x"]) and np.array_equal(r.weights, g[f"gl{q}_w"])
+    for q in (2, 3, 4, 5):
+        p, w = quad.triangle_rule(q)
+        assert np.array_equal(p, g[f"tri{q}_p"]) and np.array_equal(w, g[f"tri{q}_w"])
+    for case in (quad.IDENTICAL, quad.SHARED_EDGE, quad.SHARED_VERTEX, quad.DISJOINT):
+        for q in (3, 4, 5):
+            r = quad.sauter_schwab_rule(case, q)
+            assert np.array_equal(r.points, g[f"ss_{case}_{q}_p"]), (case, q)
+            assert np.array_equal(r.weights, g[f"ss_{case}_{q}_w"]), (case, q)
+            assert len(r.weights) == quad.SUBDOMAINS[case] * q**4
+
+
+def test_classify_panel_pair():
+    assert quad.classify_panel_pair([0, 1, 2], [0, 1, 2])[0] == quad.IDENTICAL
+    case, pa, pb = quad.classify_panel_pair([5, 7, 9], [9, 7, 11])
+    assert case == quad.SHARED_EDGE and pa == (1, 2, 0) and pb == (1, 0, 2)
+    case, pa, pb = quad.classify_panel_pair([5, 7, 9], [1, 2, 9])
+    assert case == quad.SHARED_VERTEX and pa == (2, 0, 1) and pb == (2, 0, 1)
+    assert quad.classify_panel_pair([0, 1, 2], [3, 4, 5])[0] == quad.DISJOINT
+
+
+def test_gca_basis_bit_exact_cfg0():
+    g = golden("h2_cfg0.npz")
+    m = sphere(4)
+    t0, _ = trees(m, 32)
+    b = gca.build_basis(AssemblyContext(m), t0, gca.P0_SLP, 3, 1e-4, threads=4)
+    ranks = np.array([b.rank[u] for u in range(t0.n_nodes)])
+    piv = np.concatenate([b.pivots[u] for u in range(t0.n_nodes)])
+    assert np.array_equal(ranks, g["ranks"]) and np.array_equal(piv, g["pivots"])
+    V = np.concatenate([b.V[u].ravel() for u in t0.leaf_uids()])
+    E = np.concatenate([b.E[u].ravel() for u in range(t0.n_nodes) if u in b.E])
+    assert np.array_equal(V, g["V"]) and np.array_equal(E, g["E"])
+
+
+def test_gca_dlp_bases_bit_exact_level4():
+    g = golden("h2_dlp4.npz")
+    m = sphere(4)
+    t0, t1 = trees(m, 32)
+    ctx = AssemblyContext(m)
+    for prefix, tree, flavor in (("row_", t0, gca.P0_SLP), ("col_", t1, gca.P1_DLP)):
+        b = gca.build_basis(ctx, tree, flavor, 3, 1e-4, threads=4)
+        ranks = np.array([b.rank[u] for u in range(tree.n_nodes)])
+        piv = np.concatenate([b.pivots[u] for u in range(tree.n_nodes)])
+        assert np.array_equal(ranks, g[prefix + "ranks"]) and np.array_equal(piv, g[prefix + "pivots"])
+        V = np.concatenate([b.V[u].ravel() for u in tree.leaf_uids()])
+        assert np.abs(V - g[prefix + "V"]).max() <= 1e-12 * np.abs(g[prefix + "V"]).max()
+
+
+@pytest.mark.slow
+def test_gca_pivots_cfg1():
+    g = golden("h2_cfg1.npz")
+    m = sphere(6)
+    t0, _ = trees(m, 64)
+    b = gca.build_basis(AssemblyContext(m), t0, gca.P0_SLP, 4, 1e-4, threads=8)
+    ranks = np.array([b.rank[u] for u in range(t0.n_nodes)])
+    piv = np.concatenate([b.pivots[u] for u in range(t0.n_nodes)])
+    assert np.array_equal(ranks, g["ranks"]) and np.array_equal(piv, g["pivots"])
+
+
+def test_aca_inverse_core_properties(rng):
+    # reference tests/test_lowrank.py:94-127
+    u = rng.standard_normal(8)
+    v = rng.standard_normal(6)
+    tau, sigma, C, ok = aca_inverse_core(np.outer(u, v), 1e-12)
+    assert len(tau) == 1 and ok
+    A = rng.standard_normal((20, 5)) @ rng.standard_normal((5, 15))
+    tau, sigma, C, ok = aca_inverse_core(A, 1e-10)
+    R = A[:, sigma] @ C @ A[tau, :]
+    assert np.linalg.norm(R - A) <= 1e-8 * np.linalg.norm(A)
+    with pytest.raises(ValueError):
+        aca_inverse_core(np.array([[np.nan]]), 1e-3)
+    tau, sigma, C, ok = aca_inverse_core(np.zeros((3, 3)), 1e-3)
+    assert len(tau) == 0 and ok
+
+
+def test_green_quadrature_integrates_area():
+    gq = gca.green_quadrature(np.array([[0.0, 0, 0], [1.0, 2.0, 3.0]]), 3)
+    assert len(gq.weights) == 6 * 9
+    assert abs(gq.weights.sum() - 2 * (2 * 3 + 1 * 3 + 1 * 2)) < 1e-12
+
+
+def test_support_boxes_contain_dofs():
+    m = sphere(2)
+    b1 = S.DofSpace(S.P1, m).support_boxes()
+    assert (b1[:, 0, :] <= m.vertices).all() and (m.vertices <= b1[:, 1, :]).all()
+
+
+def test_library_exports_every_declared_symbol():
+    """libh2b.so loads without a GPU and exports what include/h2b.h declares."""
+    header = open(f"{ROOT}/include/h2b.h").read()
+    declared = set(re.findall(r"\bint\s+(h2b_\w+)\s*\(", header))
+    assert declared == set(_lib.EXPORTS)
+    L = _lib.lib()
+    for name in declared:
+        assert hasattr(L, name)
+    assert L.h2b_abi_version() == 1
+    # error plumbing works without a device
+    rc = L.h2b_cluster_tree(None, 0, 1, None, None, None, None, None, None, None, None)
+    assert rc == _lib.H2B_ERR_INVALID
+    with pytest.raises(ValueError, match="empty index set"):
+        _lib.check(rc)
+    assert "empty" in _lib.last_error()
+    rc = L.h2b_plan_create(None, ctypes.byref(ctypes.c_void_p()))
+    assert rc == _lib.H2B_ERR_INVALID
