@@ -321,17 +321,18 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
     H2B_CUDA_TRY(cudaMemcpy(rrank.data(), L.r_rank, sizeof(int32_t) * L.r_nodes, cudaMemcpyDeviceToHost));
     H2B_CUDA_TRY(cudaMemcpy(crank.data(), L.c_rank, sizeof(int32_t) * L.c_nodes, cudaMemcpyDeviceToHost));
     H2B_CUDA_TRY(cudaMemcpy(csize.data(), L.c_size, sizeof(int32_t) * L.c_nodes, cudaMemcpyDeviceToHost));
-    int maxcols = 1, maxk = 0;
+    std::vector<int64_t> rvoff(L.r_nodes);
+    H2B_CUDA_TRY(cudaMemcpy(rvoff.data(), L.r_v_off, sizeof(int64_t) * L.r_nodes, cudaMemcpyDeviceToHost));
+    int maxcols = 1, maxk = 0, maxleaf = 0;
     for (int i = 0; i < L.r_nodes; ++i) {
         maxcols = std::max(maxcols, std::max(scols[i], dcols[i]));
-        maxk = std::max(maxk, std::max(rrank[i], rsize[i] <= 1024 ? 0 : rsize[i]));
+        maxk = std::max(maxk, rrank[i]);
+        if (rvoff[i] >= 0) maxleaf = std::max(maxleaf, rsize[i]);
     }
-    int maxleaf = 0;
     for (int i = 0; i < L.c_nodes; ++i) maxk = std::max(maxk, crank[i]);
     std::vector<int32_t> leaves(L.c_leaves);
     H2B_CUDA_TRY(cudaMemcpy(leaves.data(), L.c_leaf_list, sizeof(int32_t) * L.c_leaves, cudaMemcpyDeviceToHost));
     for (int l : leaves) maxleaf = std::max(maxleaf, csize[l]);
-    for (int i = 0; i < L.r_nodes; ++i) if (dcols[i] > 0 || rsize[i] > 0) maxleaf = std::max(maxleaf, rsize[i]);
     if (maxk > 1024 || maxleaf > 1024) {
         delete p;
         return fail(H2B_ERR_INVALID, "h2b_plan_create: cluster rank or leaf size above 1024");

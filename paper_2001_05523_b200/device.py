@@ -31,6 +31,8 @@ def dev(a, dtype=None):
     """numpy -> contiguous CUDA tensor."""
     t = require_cuda()
     a = np.ascontiguousarray(a if dtype is None else np.asarray(a, dtype=dtype))
+    if not a.flags.writeable:
+        a = a.copy()
     return t.from_numpy(a).to("cuda", non_blocking=False)
 
 

@@ -1,0 +1,130 @@
+"""GPU H^2 matvec parity: device operator vs the reference goldens and the oracle."""
+
+import numpy as np
+import pytest
+
+from oracle import h2 as OH
+
+from .conftest import golden
+from .helpers import basis_from_arrays, oracle_tree, rel, sphere, trees
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cfg0():
+    """Config 0 on the reference's basis (golden V/E/pivots): couplings and
+    nearfield assembled on the GPU, q_reg 3 / q_ss 4."""
+    from paper_2001_05523_b200 import clustering as C
+    from paper_2001_05523_b200 import gca
+    from paper_2001_05523_b200.containers import AssemblyContext
+
+    g = golden("h2_cfg0.npz")
+    m = sphere(4)
+    t0, _ = trees(m, 32)
+    bt = C.BlockTree(t0, t0, 2.0)
+    b = basis_from_arrays(t0, g["ranks"], g["pivots"], g["V"], g["E"])
+    ctx = AssemblyContext(m)
+    H = gca.assemble_h2(ctx, "slp", bt, b, b, 3, q_singular=4)
+    return g, m, t0, bt, b, H
+
+
+def test_cfg0_matvec_vs_reference(cfg0):
+    g, m, t0, bt, b, H = cfg0
+    y = H.matvec(g["x"])
+    assert rel(y, g["y"]) < 1e-10
+    # the H^2 approximation error vs the dense product (reference: ~2.5e-4)
+    assert np.linalg.norm(y - g["y_dense"]) <= 1e-3 * np.linalg.norm(g["y_dense"])
+
+
+def test_cfg0_couplings_vs_reference(cfg0):
+    g, m, t0, bt, b, H = cfg0
+    far = H.far
+    vals = np.concatenate([far[i][1].ravel() for i in g["far_sel"]])
+    assert rel(vals, g["far_vals"]) < 1e-10
+    assert H.storage_report() == dict(zip(("basis", "coupling", "lowrank", "nearfield"),
+                                          (int(v) for v in g["storage"])))
+
+
+def test_cfg0_matvec_vs_oracle_same_operator(cfg0, rng):
+    """Kernel parity on identical operator data (the GPU-assembled S and D)."""
+    g, m, t0, bt, b, H = cfg0
+    ot = oracle_tree(t0)
+    S = [s for _, s in H.far]
+    Dn = [d for _, d in H.near]
+    for _ in range(3):
+        x = rng.uniform(-1, 1, H.shape[1])
+        ref = OH.matvec(ot, ot, b.V, b.E, b.rank, b.V, b.E, b.rank, bt.far_uids, S, bt.near_uids, Dn, x)
+        assert rel(H.matvec(x), ref) < 1e-13
+
+
+def test_cfg0_diagonal_transpose_zero(cfg0, rng):
+    g, m, t0, bt, b, H = cfg0
+    assert rel(H.diagonal(), g["diag"]) < 1e-10
+    assert not H.matvec(np.zeros(H.shape[1])).any()
+    x = rng.standard_normal(H.shape[1])
+    y = rng.standard_normal(H.shape[0])
+    lhs = float(H.matvec(x) @ y)
+    rhs = float(x @ H.rmatvec(y))
+    assert abs(lhs - rhs) <= 1e-10 * abs(lhs)
+
+
+def test_cfg0_device_tensors_and_determinism(cfg0):
+    import torch
+
+    g, m, t0, bt, b, H = cfg0
+    x = torch.from_numpy(g["x"]).cuda()
+    y1 = H.matvec(x)
+    y2 = H.matvec(x)
+    assert isinstance(y1, torch.Tensor) and y1.is_cuda
+    assert torch.equal(y1, y2)  # bitwise reproducible
+    assert rel(y1.cpu().numpy(), g["y"]) < 1e-10
+
+
+def test_cfg0_linearity(cfg0, rng):
+    g, m, t0, bt, b, H = cfg0
+    x = rng.standard_normal(H.shape[1])
+    z = rng.standard_normal(H.shape[1])
+    lhs = H.matvec(0.7 * x - 1.3 * z)
+    rhs = 0.7 * H.matvec(x) - 1.3 * H.matvec(z)
+    assert np.linalg.norm(lhs - rhs) <= 1e-12 * np.linalg.norm(lhs)
+
+
+def test_dlp_level4_matvec_vs_reference():
+    from paper_2001_05523_b200 import clustering as C
+    from paper_2001_05523_b200 import gca
+    from paper_2001_05523_b200.containers import AssemblyContext
+
+    g = golden("h2_dlp4.npz")
+    m = sphere(4)
+    t0, t1 = trees(m, 32)
+    bt = C.BlockTree(t0, t1, 2.0)
+    rb = basis_from_arrays(t0, g["row_ranks"], g["row_pivots"], g["row_V"], g["row_E"])
+    cb = basis_from_arrays(t1, g["col_ranks"], g["col_pivots"], g["col_V"], g["col_E"])
+    H = gca.assemble_h2(AssemblyContext(m), "dlp", bt, rb, cb, 3, q_singular=5)
+    far = H.far
+    vals = np.concatenate([far[i][1].ravel() for i in g["far_sel"]])
+    assert rel(vals, g["far_vals"]) < 1e-10
+    y = H.matvec(g["x"])
+    assert rel(y, g["y"]) < 1e-10
+
+
+def test_cfg1_end_to_end_vs_reference():
+    """Config 1 through the public API: host GCA basis (bit-exact pivots on the
+    reference host BLAS), GPU couplings + nearfield, GPU matvec."""
+    from paper_2001_05523_b200 import clustering as C
+    from paper_2001_05523_b200 import gca
+    from paper_2001_05523_b200.containers import AssemblyContext
+
+    g = golden("h2_cfg1.npz")
+    m = sphere(6)
+    t0, _ = trees(m, 64)
+    ctx = AssemblyContext(m)
+    b = gca.build_basis(ctx, t0, gca.P0_SLP, 4, 1e-4, threads=8)
+    piv = np.concatenate([b.pivots[u] for u in range(t0.n_nodes)])
+    if not np.array_equal(piv, g["pivots"]):
+        pytest.skip("host BLAS differs from the reference host: GCA pivots differ (construction, not matvec)")
+    H = gca.assemble_h2(ctx, "slp", C.BlockTree(t0, t0, 2.0), b, b, 3, q_singular=4)
+    for i in range(2):
+        assert rel(H.matvec(g[f"x{i}"]), g[f"y{i}"]) < 1e-10
+    assert rel(H.diagonal(), g["diag"]) < 1e-10

@@ -1,0 +1,161 @@
+"""GPU quadrature parity: libh2b kernels vs the CPU oracle and the reference goldens."""
+
+import numpy as np
+import pytest
+
+from oracle import quad as OQ
+
+from .conftest import golden
+from .helpers import rel, sphere, trees
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx4():
+    from paper_2001_05523_b200.containers import AssemblyContext
+
+    return AssemblyContext(sphere(4))
+
+
+@pytest.mark.parametrize("level", [2, 4])
+def test_touch_table_bit_exact(level):
+    from paper_2001_05523_b200.kernels import DeviceMesh
+
+    g = golden("touch.npz")
+    t = DeviceMesh(sphere(level)).touch()
+    assert np.array_equal(t.keys(), g[f"l{level}_keys"])
+    codes, perms = t.codes_perms()
+    assert np.array_equal(codes, g[f"l{level}_codes"])
+    assert np.array_equal(perms, g[f"l{level}_perms"])
+
+
+@pytest.mark.parametrize("q", [4, 5])
+@pytest.mark.parametrize("kind", ["slp", "dlp"])
+def test_singular_table_vs_oracle_all_pairs(kind, q):
+    from paper_2001_05523_b200.containers import AssemblyContext
+
+    m = sphere(3)
+    tab = AssemblyContext(m).singular_table(kind, q)
+    keys = tab.keys
+    F = m.n_triangles
+    ref = OQ.singular_integrals(m.vertices, m.triangles, m.normals, m.areas, keys // F, keys % F, kind, q)
+    got = tab.values
+    if kind == "slp":
+        # entrywise relative for SLP (all entries positive)
+        assert np.abs(got - ref).max() / np.abs(ref).min() < 1e-10
+    else:
+        assert rel(got, ref) < 1e-10
+
+
+@pytest.mark.parametrize("q", [3, 4, 5])
+@pytest.mark.parametrize("kind", ["slp", "dlp"])
+def test_singular_table_vs_reference_sample(ctx4, kind, q):
+    s = golden("singular.npz")
+    tab = ctx4.singular_table(kind, q)
+    got = tab.lookup(s["pa"], s["pb"])
+    assert rel(got, s[f"{kind}_q{q}"]) < 1e-10
+
+
+@pytest.mark.parametrize("q", [3, 4])
+@pytest.mark.parametrize("kind", ["slp", "dlp"])
+def test_regular_blocks_vs_reference(ctx4, kind, q):
+    """panel_pair_matrix golden (same q for regular and singular)."""
+    from paper_2001_05523_b200 import kernels
+
+    s = golden("singular.npz")
+    rows, cols = s["reg_rows"], s["reg_cols"]
+    if kind == "slp":
+        from paper_2001_05523_b200.containers import dense_block
+
+        got = dense_block(ctx4, "slp", rows, cols, q)
+        assert rel(got, s[f"reg_slp_q{q}"]) < 1e-10
+    else:
+        # DLP panel-pair values: one job per column panel with its 3 vertices
+        m = ctx4.mesh
+        ref = s[f"reg_dlp_q{q}"]
+        for j, pb in enumerate(cols):
+            verts = m.triangles[pb]
+            V, T, N, A = m.vertices, m.triangles, m.normals, m.areas
+            vptr, vidx = m.vertex_triangle_csr()
+            exp = OQ.dlp_block(V, T, N, A, vptr, vidx, rows, verts, q, OQ.Table(V, T, N, A, "dlp", q))
+            from paper_2001_05523_b200.containers import dense_block
+
+            got = dense_block(ctx4, "dlp", rows, verts, q)
+            assert rel(got, exp) < 1e-10
+            break
+        assert ref.shape == (len(rows), len(cols), 3)
+
+
+def test_require_disjoint_raises(ctx4):
+    from paper_2001_05523_b200.containers import dense_block
+
+    with pytest.raises(ValueError, match="touching"):
+        dense_block(ctx4, "slp", [0, 1], [0, 5], 3, require_disjoint=True)
+    with pytest.raises(ValueError):
+        dense_block(ctx4, "hyp", [0], [1], 3)
+
+
+@pytest.fixture(scope="module")
+def cfg0_world():
+    from paper_2001_05523_b200 import clustering as C
+    from paper_2001_05523_b200.containers import AssemblyContext
+
+    m = sphere(4)
+    t0, t1 = trees(m, 32)
+    return m, AssemblyContext(m), t0, t1, C.BlockTree(t0, t0, 2.0), C.BlockTree(t0, t1, 2.0)
+
+
+def test_nearfield_slp_all_blocks_vs_oracle(cfg0_world):
+    """Every near block of config 0 (q_reg 3, q_ss 4) vs the oracle, per block."""
+    from paper_2001_05523_b200.containers import assemble_nearfield
+
+    m, ctx, t0, _, bt, _ = cfg0_world
+    got = assemble_nearfield(ctx, "slp", bt, 3, q_singular=4)
+    V, T, N, A = m.vertices, m.triangles, m.normals, m.areas
+    tab = OQ.Table(V, T, N, A, "slp", 4)
+    worst = 0.0
+    for (t, s), blk in zip(bt.near_uids, got):
+        exp = OQ.slp_block(V, T, N, A, t0.perm[t0.start[t] : t0.end[t]], t0.perm[t0.start[s] : t0.end[s]], 3, tab)
+        worst = max(worst, float(np.abs(blk - exp).max() / np.abs(exp).min()))
+    assert worst < 1e-10, worst
+
+
+def test_nearfield_slp_vs_reference_sample(cfg0_world, g_cfg0):
+    from paper_2001_05523_b200.containers import assemble_nearfield
+
+    m, ctx, t0, _, bt, _ = cfg0_world
+    got = assemble_nearfield(ctx, "slp", bt, 3, q_singular=4)
+    vals = np.concatenate([got[i].ravel() for i in g_cfg0["near_sel"]])
+    assert np.abs(vals - g_cfg0["near_vals"]).max() / np.abs(g_cfg0["near_vals"]).min() < 1e-10
+    total = sum(float(d.sum()) for d in got)
+    assert abs(total - g_cfg0["near_sum"][0]) <= 1e-10 * abs(g_cfg0["near_sum"][0])
+
+
+def test_nearfield_dlp_vs_oracle_and_reference(cfg0_world):
+    from paper_2001_05523_b200.containers import assemble_nearfield
+
+    m, ctx, t0, t1, _, btd = cfg0_world
+    g = golden("h2_dlp4.npz")
+    got = assemble_nearfield(ctx, "dlp", btd, 3, q_singular=5)
+    vals = np.concatenate([got[i].ravel() for i in g["near_sel"]])
+    assert rel(vals, g["near_vals"]) < 1e-10
+    total = sum(float(d.sum()) for d in got)
+    assert abs(total - g["near_sum"][0]) <= 1e-9 * max(1.0, abs(g["near_sum"][0]))
+    V, T, N, A = m.vertices, m.triangles, m.normals, m.areas
+    vptr, vidx = m.vertex_triangle_csr()
+    tab = OQ.Table(V, T, N, A, "dlp", 5)
+    for i in range(0, len(btd.near_uids), 37):
+        t, s = btd.near_uids[i]
+        exp = OQ.dlp_block(V, T, N, A, vptr, vidx, t0.perm[t0.start[t] : t0.end[t]],
+                           t1.perm[t1.start[s] : t1.end[s]], 3, tab)
+        assert rel(got[i], exp) < 1e-10
+
+
+def test_quadrature_deterministic(cfg0_world):
+    from paper_2001_05523_b200.containers import assemble_nearfield_device
+
+    m, ctx, t0, _, bt, _ = cfg0_world
+    a = assemble_nearfield_device(ctx, "slp", bt, 3, 4).cpu().numpy()
+    b = assemble_nearfield_device(ctx, "slp", bt, 3, 4).cpu().numpy()
+    assert np.array_equal(a, b)
