@@ -1,0 +1,438 @@
+"""Benchmark: H^2-matvec DoF/s (+ nearfield quadrature pairs/s), fp64, B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 1]
+
+Workload (BASELINE.json configs[1], the metric's single-GPU configuration):
+sphere refined 6x (32 768 triangles), piecewise-constant single-layer
+operator, GCA H^2 with m = 4, eta = 2, leaf 64, eps_aca = 1e-4 (reference
+default), regular Gauss order 3, Sauter-Schwab order 4; x ~ N(0,1) seed 1.
+Synthetic mesh, no dataset.
+
+A step is one H^2 matvec y = A x of that operator (inputs resident in HBM).
+L2 is flushed (256 MiB write) between timed steps, so every step streams its
+operator (202 MB) from HBM; each step is bracketed by its own CUDA events and
+`value` = n x K / (sum of step times).  The nearfield assembly (Sauter-Schwab
+table + regular pair blocks) is timed in the same run and reported under
+`nearfield` (pairs/s, FP64 roofline).  `e2e` is the same matvec through the
+public API (H2Matrix.matvec on a pinned host numpy vector: H2D + kernels +
+D2H every step).
+
+--impl reference times the reference's CPU algorithm (the oracle port in
+oracle/, the reference itself cannot travel to the GPU box) on the same
+operator, on rank 0 only.
+
+Multi-GPU (torchrun, one rank per GPU): rows are sharded by contiguous
+row-leaf ranges (upper clusters redundant), x is all-gathered over NCCL
+once per matvec, each rank writes its own rows; strong scaling of the fixed
+config-1 problem; timing = max over ranks.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+
+CONFIGS = {
+    # name: level, leaf, eta, m, q_reg, q_ss, kind, seed, dist
+    "1": dict(level=6, leaf=64, eta=2.0, m=4, q_reg=3, q_ss=4, kind="slp", seed=1, dist="normal",
+              desc="sphere L6 (32768 tri) SLP P0, GCA m=4 eta=2 leaf=64 eps=1e-4, q 3/4"),
+    "0": dict(level=4, leaf=32, eta=2.0, m=3, q_reg=3, q_ss=4, kind="slp", seed=0, dist="uniform",
+              desc="sphere L4 (2048 tri) SLP P0, GCA m=3 eta=2 leaf=32 eps=1e-4, q 3/4"),
+    "2s": dict(level=8, leaf=64, eta=2.0, m=4, q_reg=3, q_ss=5, kind="slp", seed=2, dist="uniform",
+               desc="sphere L8 (524288 tri) SLP P0, GCA m=4 eta=2 leaf=64 eps=1e-4, q 3/5"),
+}
+EPS_ACA = 1e-4
+METRIC = "H2-matvec DoF/s (fp64), + nearfield quad pairs/s"
+
+
+def peaks():
+    p = {"hbm_gbs": None, "fp64_tflops": None, "hbm_src": None, "fp64_src": None}
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        p["hbm_gbs"], p["hbm_src"] = float(mp["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
+    except Exception:
+        p["hbm_gbs"], p["hbm_src"] = 6650.0, "B200_PROFILING.md fallback"
+    return p
+
+
+def measure_fp64_peak():
+    """DFMA-chain microbenchmark (tools/fp64_probe) run live on this GPU."""
+    exe = os.path.join(ROOT, "tools", "_bin", "fp64_probe")
+    if os.path.exists(exe):
+        try:
+            out = subprocess.run([exe], capture_output=True, text=True, timeout=60).stdout
+            return float(json.loads(out.strip().splitlines()[-1])["fp64_dfma_tflops"]), "tools/fp64_probe (measured live)"
+        except Exception:
+            pass
+    return 34.23, "profiles/r01_fp64_probe.json (measured earlier on this pool)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu_index=0):
+        self.proc = None
+        self.path = f"/tmp/h2b_clocks_{os.getpid()}.csv"
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={gpu_index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def build_problem(cfg, threads):
+    """Host setup (untimed): mesh, trees, block tree, GCA basis."""
+    from paper_2001_05523_b200 import clustering as C
+    from paper_2001_05523_b200 import gca, spaces
+    from paper_2001_05523_b200.containers import AssemblyContext
+    from paper_2001_05523_b200.mesh import sphere_mesh
+
+    mesh = sphere_mesh(cfg["level"])
+    ctx = AssemblyContext(mesh)
+    tree = C.build_cluster_tree(spaces.DofSpace(spaces.P0, mesh).support_boxes(), cfg["leaf"])
+    bt = C.BlockTree(tree, tree, cfg["eta"])
+    basis = gca.build_basis(ctx, tree, gca.P0_SLP, cfg["m"], EPS_ACA, threads=threads)
+    return mesh, ctx, tree, bt, basis
+
+
+def flop_counts(ctx, bt, cfg):
+    """Algorithmic nearfield work (SURVEY.md 8(d) convention)."""
+    from paper_2001_05523_b200.containers import near_layout
+
+    t = ctx.dmesh.touch()
+    n_id, n_edge, n_vert = (int(c) for c in t.case_counts)
+    q, qs = cfg["q_reg"], cfg["q_ss"]
+    entries = near_layout(bt).entries
+    regular = entries - t.n_pairs
+    ev_reg = regular * q**4
+    ev_sing = n_id * 6 * qs**4 + n_edge * 2 * 5 * qs**4 + n_vert * 2 * 2 * qs**4
+    return dict(pairs=entries, regular_pairs=regular, singular_pairs=t.n_pairs, reg_flops=12.0 * ev_reg,
+                sing_flops=36.0 * ev_sing, evals=ev_reg + ev_sing)
+
+
+def ev_time(torch, fn, reps=1):
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / 1e3 / reps
+
+
+def run_ours(args, cfg):
+    import torch
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    pg = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    from paper_2001_05523_b200 import gca, kernels
+    from paper_2001_05523_b200.containers import (H2Matrix, assemble_couplings, near_layout)
+    from paper_2001_05523_b200 import distributed as DD
+
+    threads = max(1, (os.cpu_count() or 8) // max(ws, 1))
+    t0 = time.time()
+    mesh, ctx, tree, bt, basis = build_problem(cfg, threads)
+    setup_s = time.time() - t0
+
+    # ---- nearfield assembly on the device (timed) --------------------------------
+    lay = near_layout(bt)
+    Dn = torch.zeros(max(lay.total, 1), dtype=torch.float64, device="cuda")
+    nu = bt.near_uids
+    jobs = np.stack([tree.start[nu[:, 0]], lay.blk_rows, tree.start[nu[:, 1]], lay.blk_cols, lay.blk_off,
+                     lay.blk_ld], axis=1)
+    clocks = Clocks(local)
+    t_touch = ev_time(torch, lambda: ctx.dmesh.touch())
+    slp_jobs = kernels.SlpJobs(ctx.dmesh, cfg["q_reg"], jobs, tree.perm.astype(np.int32), tree.perm.astype(np.int32))
+    table = kernels.SingularTable(ctx.dmesh, "slp", cfg["q_ss"], compute=False)
+    for _ in range(2):
+        table.compute()
+        slp_jobs.run(table, Dn)
+    nf_reps = 20
+    t_sing = ev_time(torch, table.compute, nf_reps)
+    t_reg = ev_time(torch, lambda: slp_jobs.run(table, Dn), nf_reps)
+    fc = flop_counts(ctx, bt, cfg)
+    S = assemble_couplings(ctx, "slp", bt, basis, basis, cfg["q_reg"])
+    H = H2Matrix.from_device(bt, basis, basis, S, Dn)
+    n = H.shape[0]
+
+    # ---- matvec ------------------------------------------------------------------
+    rng = np.random.default_rng(cfg["seed"])
+    x_host = rng.standard_normal(n) if cfg["dist"] == "normal" else rng.uniform(-1, 1, n)
+    if ws > 1:
+        op = DD.ShardedMatvec(H, rank, ws, pg)
+    else:
+        op = DD.LocalMatvec(H)
+    x = torch.from_numpy(x_host).cuda()
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+    for _ in range(max(args.warmup, 3)):
+        op.apply(x, y)
+    torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    K = args.steps
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    torch.cuda.synchronize()
+    for k in range(K):
+        flush.fill_(float(k))
+        starts[k].record()
+        op.apply(x, y)
+        ends[k].record()
+    torch.cuda.synchronize()
+    step_s = np.array([s.elapsed_time(e) / 1e3 for s, e in zip(starts, ends)])
+    clk = clocks.stop()
+    total = float(step_s.sum())
+    if pg:
+        tt = torch.tensor([total], dtype=torch.float64, device="cuda")
+        pg.all_reduce(tt, op=pg.ReduceOp.MAX)
+        total = float(tt.item())
+    mean_step = total / K
+    dofs_per_s = n * K / total
+
+    # ---- parity spot-check of this run against the oracle is in the test-suite;
+    # here: e2e through the public API with pinned host buffers ----------------------
+    e2e = None
+    if ws == 1:
+        xp = torch.from_numpy(x_host).pin_memory()
+        xh = xp.numpy()
+        for _ in range(3):
+            H.matvec(xh)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        ke = max(10, K)
+        for _ in range(ke):
+            yh = H.matvec(xh)
+        dt = time.perf_counter() - t1
+        e2e = {"value": n * ke / dt, "unit": "DoF/s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+               "timer": "host wall clock around H2Matrix.matvec(numpy) incl. H2D/D2H, synchronised"}
+        del yh
+
+    # ---- roofline ---------------------------------------------------------------
+    pk = peaks()
+    mv_bytes = H.matvec_bytes()
+    fp64_peak, fp64_src = measure_fp64_peak() if rank == 0 else (None, None)
+    nf_time = t_sing + t_reg
+    result = {
+        "metric": METRIC,
+        "value": dofs_per_s * (ws if False else 1),
+        "unit": "DoF/s",
+        "n_gpus": ws,
+        "steps": K,
+        "warmup": max(args.warmup, 3),
+        "ms_per_step": mean_step * 1e3,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (generated sphere mesh, x ~ N(0,1) seed 1)",
+        "config": {"workload": f"config {args.config}: {cfg['desc']}", "n_dofs": n,
+                   "matvec_bytes": mv_bytes, "l2": "flushed (256 MiB write) between timed steps",
+                   "parallelism": f"row-shard x{ws}" if ws > 1 else "single GPU"},
+        "gpu_launches": K,
+        "roofline": {"bound": "hbm", "kernel": "k_matvec (fused forward + coupling + backward + nearfield)",
+                     "achieved": mv_bytes / mean_step / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": mv_bytes / mean_step / 1e9 / pk["hbm_gbs"], "traffic": None,
+                     "algorithmic_bytes": mv_bytes, "kernel_ms": mean_step * 1e3, "peak_source": pk["hbm_src"]},
+        "nearfield": {
+            "pairs_per_s": fc["pairs"] / nf_time, "pairs": fc["pairs"], "ms": nf_time * 1e3,
+            "touch_classify_ms": t_touch * 1e3,
+            "singular": {"ms": t_sing * 1e3, "pairs": fc["singular_pairs"], "gflop": fc["sing_flops"] / 1e9,
+                         "tflops": fc["sing_flops"] / t_sing / 1e12,
+                         "frac": (fc["sing_flops"] / t_sing / 1e12 / fp64_peak) if fp64_peak else None},
+            "regular": {"ms": t_reg * 1e3, "pairs": fc["regular_pairs"], "gflop": fc["reg_flops"] / 1e9,
+                        "tflops": fc["reg_flops"] / t_reg / 1e12,
+                        "frac": (fc["reg_flops"] / t_reg / 1e12 / fp64_peak) if fp64_peak else None},
+            "roofline": {"bound": "fp64", "achieved": (fc["reg_flops"] + fc["sing_flops"]) / nf_time / 1e12,
+                         "peak": fp64_peak, "unit": "TFLOP/s",
+                         "frac": ((fc["reg_flops"] + fc["sing_flops"]) / nf_time / 1e12 / fp64_peak) if fp64_peak else None,
+                         "peak_source": fp64_src},
+        },
+        "e2e": e2e,
+        "clocks": clk,
+        "setup_s": setup_s,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(H, tree, bt, basis, x_host, budget_s=args.cpu_budget)
+    if pg:
+        pg.barrier()
+        pg.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result))
+
+
+def oracle_operator(H, tree, bt, basis):
+    from oracle import h2 as OH
+
+    ot = OH.Tree(tree.perm, tree.start, tree.end, tree.depth_of, tree.left, tree.right)
+    S = [s for _, s in H.far]
+    Dn = [d for _, d in H.near]
+    return ot, S, Dn
+
+
+def cpu_baseline(H, tree, bt, basis, x, budget_s=15.0):
+    """The oracle (numpy restatement of containers.py:254-270) on the same
+    operator, single thread, bounded sample of matvecs."""
+    from oracle import h2 as OH
+
+    ot, S, Dn = oracle_operator(H, tree, bt, basis)
+    n = H.shape[0]
+    OH.matvec(ot, ot, basis.V, basis.E, basis.rank, basis.V, basis.E, basis.rank, bt.far_uids, S, bt.near_uids, Dn, x)
+    t = time.perf_counter()
+    k = 0
+    while time.perf_counter() - t < budget_s:
+        OH.matvec(ot, ot, basis.V, basis.E, basis.rank, basis.V, basis.E, basis.rank, bt.far_uids, S, bt.near_uids,
+                  Dn, x)
+        k += 1
+    dt = time.perf_counter() - t
+    return {"value": n * k / dt, "unit": "DoF/s", "cores": 1, "kind": "port",
+            "sample": f"{k} oracle matvecs of the same config-1 operator ({dt:.1f} s, OPENBLAS_NUM_THREADS=1)"}
+
+
+def run_reference(args, cfg):
+    """Reference arm: the reference's CPU algorithm (oracle port) on rank 0."""
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    import torch  # noqa: F401  (device only used to assemble the operator values once? no: oracle assembly below)
+
+    from oracle import h2 as OH
+    from oracle import quad as OQ
+
+    threads = os.cpu_count() or 8
+    mesh, ctx, tree, bt, basis = build_problem(cfg, threads)
+    V, T, N, A = mesh.vertices, mesh.triangles, mesh.normals, mesh.areas
+    p = tree.perm
+    # operator values by the oracle (CPU quadrature), process pool over blocks
+    from concurrent.futures import ProcessPoolExecutor
+
+    t0 = time.time()
+    tab = OQ.Table(V, T, N, A, "slp", cfg["q_ss"])
+    near_jobs = [(p[tree.start[t] : tree.end[t]], p[tree.start[s] : tree.end[s]]) for t, s in bt.near_uids]
+    far_jobs = [(basis.pivots[t], basis.pivots[s]) for t, s in bt.far_uids]
+    global _REF_STATE
+    _REF_STATE = (V, T, N, A, tab, cfg["q_reg"])
+    with ProcessPoolExecutor(max_workers=threads) as ex:
+        Dn = list(ex.map(_ref_near, near_jobs, chunksize=64))
+        S = list(ex.map(_ref_far, far_jobs, chunksize=64))
+    t_asm = time.time() - t0
+    ot = OH.Tree(tree.perm, tree.start, tree.end, tree.depth_of, tree.left, tree.right)
+    n = len(tree.perm)
+    rng = np.random.default_rng(cfg["seed"])
+    x = rng.standard_normal(n) if cfg["dist"] == "normal" else rng.uniform(-1, 1, n)
+
+    def mv():
+        return OH.matvec(ot, ot, basis.V, basis.E, basis.rank, basis.V, basis.E, basis.rank, bt.far_uids, S,
+                         bt.near_uids, Dn, x)
+
+    for _ in range(max(args.warmup, 3)):
+        mv()
+    K = args.steps
+    t = time.perf_counter()
+    for _ in range(K):
+        mv()
+    dt = time.perf_counter() - t
+    val = n * K / dt
+    out = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "DoF/s", "n_gpus": ws, "steps": K,
+        "warmup": max(args.warmup, 3), "ms_per_step": dt / K * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (generated sphere mesh, x ~ N(0,1) seed 1)",
+        "config": {"workload": f"config {args.config}: {cfg['desc']}", "n_dofs": n},
+        "cpu_baseline": {"value": val, "unit": "DoF/s", "cores": 1, "kind": "port",
+                         "sample": f"{K} matvecs of the oracle port (containers.py:254-270 restated), "
+                                   f"operator assembled by the oracle quadrature in {t_asm:.0f} s on {threads} procs"},
+        "e2e": {"value": val, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+
+
+_REF_STATE = None
+
+
+def _ref_near(job):
+    from oracle import quad as OQ
+
+    V, T, N, A, tab, q = _REF_STATE
+    return OQ.slp_block(V, T, N, A, job[0], job[1], q, tab)
+
+
+def _ref_far(job):
+    from oracle import quad as OQ
+
+    V, T, N, A, tab, q = _REF_STATE
+    return OQ.slp_block(V, T, N, A, job[0], job[1], q, None)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="1", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -209,6 +209,14 @@ typedef struct {
     const int32_t* near_ptr;  /* n_rnodes+1 into near_col */
     const int32_t* near_col;  /* column uid per near block */
     const double* D;
+    /* right-hand-side gather indices: per row node, the x index of every
+     * column of its nearfield matrix (C_t entries at d_goff) and the x_hat
+     * index of every column of its coupling matrix (K_t entries at s_goff);
+     * padding columns point at index 0 (their matrix entries are zero) */
+    const int64_t* d_goff;
+    const int32_t* d_gidx;
+    const int64_t* s_goff;
+    const int32_t* s_gidx;
     /* which row nodes this rank processes (multi-GPU row sharding); all if NULL */
     int32_t n_owned;
     const int32_t* owned;     /* subset of r_order, still parents first */
@@ -222,6 +230,10 @@ int h2b_plan_destroy(h2b_plan* plan);
 int h2b_matvec(h2b_plan* plan, const double* d_x, double* d_y, void* stream);
 /* Same through host buffers: H2D copy of x, matvec, D2H copy of y, synchronised. */
 int h2b_matvec_host(h2b_plan* plan, const double* h_x, double* h_y, void* stream);
+/* Diagnostics: per-CTA timeline of the last matvec when the plan was created
+ * with the environment variable H2B_TRACE=1 (3 words per CTA ticket: start
+ * ns, end ns, SM id; then 5 words of ticket-range boundaries). */
+int h2b_plan_trace(h2b_plan* plan, unsigned long long* h_out, int64_t cap);
 /* Diagonal of the (square) operator from the nearfield, natural order. */
 int h2b_diagonal(h2b_plan* plan, double* d_diag, void* stream);
 

@@ -79,6 +79,7 @@ class Layout(ctypes.Structure):
         ("r_V", vp), ("r_E", vp), ("yhat_len", ctypes.c_int64),
         ("s_off", vp), ("s_cols", vp), ("far_ptr", vp), ("far_col", vp), ("S", vp),
         ("d_off", vp), ("d_cols", vp), ("near_ptr", vp), ("near_col", vp), ("D", vp),
+        ("d_goff", vp), ("d_gidx", vp), ("s_goff", vp), ("s_gidx", vp),
         ("n_owned", ctypes.c_int32), ("owned", vp),
     ]
 
@@ -87,7 +88,8 @@ class Layout(ctypes.Structure):
 EXPORTS = (
     "h2b_last_error", "h2b_abi_version", "h2b_cluster_tree", "h2b_block_tree", "h2b_panel_points",
     "h2b_touch_count", "h2b_touch_fill", "h2b_singular", "h2b_pair_blocks_slp", "h2b_pair_blocks_dlp",
-    "h2b_plan_create", "h2b_plan_destroy", "h2b_matvec", "h2b_matvec_host", "h2b_diagonal",
+    "h2b_plan_create", "h2b_plan_destroy", "h2b_matvec", "h2b_matvec_host",
+    "h2b_diagonal", "h2b_plan_trace",
 )
 
 _lib = None
@@ -123,6 +125,7 @@ def lib():
         L.h2b_matvec.argtypes = [vp, vp, vp, vp]
         L.h2b_matvec_host.argtypes = [vp, vp, vp, vp]
         L.h2b_diagonal.argtypes = [vp, vp, vp]
+        L.h2b_plan_trace.argtypes = [vp, vp, ctypes.c_int64]
         _lib = L
     return _lib
 

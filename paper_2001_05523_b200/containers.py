@@ -4,10 +4,10 @@ Device layout (HBM) of an H^2 operator, built once from the block tree and
 the bases:
 
   D  nearfield, one row-major |t| x C_t matrix per row leaf t whose columns are
-     its near blocks side by side (near-list order), C_t padded to even so rows
-     start 16-byte aligned;
+     its near blocks side by side (near-list order), C_t padded to a multiple of 4
+     so rows start 32-byte aligned (256-bit loads);
   S  couplings, one row-major k_t x K_t matrix per row cluster t, far blocks
-     side by side (far-list order), K_t padded to even;
+     side by side (far-list order), K_t padded to a multiple of 4;
   V  leaf bases |t| x k_t, E transfer matrices k_child x k_parent (row-major).
 
 The matvec streams D and S row by row (libh2b k_backward) and V/E once each
@@ -115,8 +115,10 @@ def assemble_dense(ctx, kind, q, cap=ORACLE_CAP, q_singular=None):
 # ---------------------------------------------------------------------------
 # packed layouts
 
-def _pad2(a):
-    return a + (a & 1)
+def _pad4(a):
+    """Round row lengths up to a multiple of 4 doubles (32-byte rows for the
+    256-bit streaming loads of the matvec)."""
+    return (a + 3) & ~3
 
 
 class NearLayout:
@@ -136,7 +138,7 @@ class NearLayout:
         np.cumsum(cnt, out=ptr[1:])
         wsum = np.zeros(nr_nodes + 1, dtype=np.int64)
         np.cumsum(np.bincount(rows, weights=width, minlength=nr_nodes).astype(np.int64), out=wsum[1:])
-        C = _pad2(np.diff(wsum))
+        C = _pad4(np.diff(wsum))
         # column offset of each block inside its row's matrix
         coloff = np.cumsum(width) - width - wsum[rows]
         height = rt.end - rt.start
@@ -145,6 +147,7 @@ class NearLayout:
         np.cumsum(size, out=off[1:])
         self.total = int(off[-1])
         self.C, self.off, self.ptr, self.col = C, off[:-1], ptr, cols
+        self.s_rows, self.s_width, self.s_coloff = rows, width, coloff
         # per block in reference near order
         inv = np.empty_like(order)
         inv[order] = np.arange(len(order))
@@ -171,13 +174,14 @@ class FarLayout:
         np.cumsum(cnt, out=ptr[1:])
         wsum = np.zeros(nr_nodes + 1, dtype=np.int64)
         np.cumsum(np.bincount(rows, weights=width, minlength=nr_nodes).astype(np.int64), out=wsum[1:])
-        K = _pad2(np.diff(wsum))
+        K = _pad4(np.diff(wsum))
         coloff = np.cumsum(width) - width - wsum[rows]
         size = rank_r * K
         off = np.zeros(nr_nodes + 1, dtype=np.int64)
         np.cumsum(size, out=off[1:])
         self.total = int(off[-1])
         self.K, self.off, self.ptr, self.col = K, off[:-1], ptr, cols
+        self.s_rows, self.s_width, self.s_coloff = rows, width, coloff
         inv = np.empty_like(order)
         inv[order] = np.arange(len(order))
         self.blk_off = (off[:-1][rows] + coloff)[inv] if len(fu) else np.zeros(0, dtype=np.int64)
@@ -315,7 +319,9 @@ class ClusterBasis:
         return _basis_transform(self, np.asarray(xp, dtype=float))
 
     def packed(self):
-        """(ranks, V flat, v_off, E flat, e_off, hat_off) in uid order; cached."""
+        """(ranks, V flat, v_off, E flat, e_off, hat_off) in uid order; cached.
+        Every block starts 16-byte aligned and is padded to an even number of
+        doubles, so the matvec can stage it with one TMA bulk copy."""
         if getattr(self, "_packed", None) is None:
             t = self.tree
             n = t.n_nodes
@@ -323,17 +329,24 @@ class ClusterBasis:
             v_off = np.full(n, -1, dtype=np.int64)
             e_off = np.full(n, -1, dtype=np.int64)
             vs, es = [], []
+            pad = np.zeros(1)
             pos = 0
             for u in t.leaf_uids():
                 v_off[u] = pos
                 vs.append(np.ascontiguousarray(self.V[u]).ravel())
                 pos += vs[-1].size
+                if pos & 1:
+                    vs.append(pad)
+                    pos += 1
             pos = 0
             for u in range(n):
                 if t.parent_of[u] >= 0:
                     e_off[u] = pos
                     es.append(np.ascontiguousarray(self.E[u]).ravel())
                     pos += es[-1].size
+                    if pos & 1:
+                        es.append(pad)
+                        pos += 1
             hat = np.zeros(n + 1, dtype=np.int64)
             np.cumsum(ranks, out=hat[1:])
             self._packed = (ranks, np.concatenate(vs) if vs else np.zeros(1), v_off,
@@ -479,10 +492,25 @@ def _scatter(flat, off, ld, block):
     view[...] = block
 
 
+def _gather_index(n_nodes, row_len, rows, width, coloff, first):
+    """Per-row-node gather lists: for every block (row node, width, column
+    offset inside the row's matrix) the `width` source indices first[b] + j.
+    Returns (offsets per node, flat int32 indices); padding columns -> 0."""
+    goff = np.zeros(n_nodes + 1, dtype=np.int64)
+    np.cumsum(row_len, out=goff[1:])
+    gidx = np.zeros(max(int(goff[-1]), 1), dtype=np.int64)
+    total = int(width.sum())
+    if total:
+        blk = np.repeat(np.arange(len(width)), width)
+        j = np.arange(total) - np.repeat(np.cumsum(width) - width, width)
+        gidx[goff[rows][blk] + coloff[blk] + j] = first[blk] + j
+    return goff[:-1], gidx
+
+
 class MatvecPlan:
     """Device layout + libh2b plan for y = A x."""
 
-    def __init__(self, bt, rb, cb, S, Dn, fl, nl, owned=None):
+    def __init__(self, bt, rb, cb, S, Dn, fl, nl, owned=None, col_perm=None, row_perm=None):
         t = D.require_cuda()
         rt, ct = bt.row_tree, bt.col_tree
         self.n_rows, self.n_cols = rt.n_dofs, ct.n_dofs
@@ -502,8 +530,8 @@ class MatvecPlan:
         r_vo = rbd.v_off.copy()
         lay = _lib.Layout()
         lay.n_rows, lay.n_cols = self.n_rows, self.n_cols
-        lay.col_perm = put("col_perm", ct.perm, np.int64)
-        lay.row_perm = put("row_perm", rt.perm, np.int64)
+        lay.col_perm = put("col_perm", ct.perm if col_perm is None else col_perm, np.int64)
+        lay.row_perm = put("row_perm", rt.perm if row_perm is None else row_perm, np.int64)
         lay.c_nodes, lay.c_leaves = ct.n_nodes, len(c_leaves)
         lay.c_parent = put("c_parent", ct.parent_of, i32)
         lay.c_child = put("c_child", c_child, i32)
@@ -537,6 +565,18 @@ class MatvecPlan:
         lay.near_ptr = put("near_ptr", nl.ptr, i32)
         lay.near_col = put("near_col", nl.col if len(nl.col) else np.zeros(1), i32)
         lay.D = Dn.data_ptr()
+        # right-hand-side gather lists (x for the nearfield, x_hat for couplings)
+        cperm = ct.perm if col_perm is None else np.asarray(col_perm)
+        nrow_len = np.where(rt.left < 0, nl.C, 0)
+        goff, gidx = _gather_index(rt.n_nodes, nrow_len, nl.s_rows, nl.s_width, nl.s_coloff, ct.start[nl.col])
+        gidx = cperm[gidx] if len(cperm) else gidx
+        if nl.total == 0:
+            gidx = np.zeros(1, dtype=np.int64)
+        lay.d_goff = put("d_goff", goff, np.int64)
+        lay.d_gidx = put("d_gidx", gidx, np.int32)
+        soff, sidx = _gather_index(rt.n_nodes, fl.K, fl.s_rows, fl.s_width, fl.s_coloff, cbd.hat[:-1][fl.col])
+        lay.s_goff = put("s_goff", soff, np.int64)
+        lay.s_gidx = put("s_gidx", sidx, np.int32)
         if owned is not None:
             lay.n_owned = len(owned)
             lay.owned = put("owned", owned, i32)

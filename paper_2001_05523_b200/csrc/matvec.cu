@@ -1,270 +1,563 @@
-// H^2-matrix-vector product y = A x (containers.py:254-270) in two launches.
+// H^2-matrix-vector product y = A x (containers.py:254-270) in ONE launch.
 //
-//   k_forward   one CTA per column leaf: gather x_p = x[col_perm] for the leaf,
-//               x_hat_t = V_t^T x_p|t, then climb the tree: the second child to
-//               arrive at a parent (arrival counter) computes
-//               x_hat_parent = sum_ch E_ch^T x_hat_ch in child order
-//               (ClusterBasis.forward, containers.py:201-212).  Deterministic:
-//               each sum has one fixed order regardless of arrival order.
-//   k_backward  one CTA per row cluster, parents first (dynamic tickets over a
-//               top-down order guarantee every parent CTA started before its
-//               children, so the flag wait below cannot deadlock):
-//                 y_hat_t = [S_b1 S_b2 ...] [x_hat_s1; x_hat_s2; ...]   (coupling, :259-264)
-//                 leaf: y_near = [D_b1 D_b2 ...] [x_p|s1; x_p|s2; ...]  (nearfield, :266-267)
-//                 wait for the parent, y_hat_t += E_t y_hat_parent     (backward, :214-228)
-//                 leaf: y[row_perm[i]] = y_near + V_t y_hat_t          (un-permute, :268-269)
+// Work is cut into CTA-sized tasks; every CTA takes a ticket (atomic counter)
+// that selects its task.  A task only ever waits for data produced by tasks
+// with smaller tickets that never wait on larger ones, so the launch cannot
+// deadlock for any grid size or residency.
 //
-// All products stream their matrices row-major and coalesced, one warp per
-// output row (lanes over columns, double2 loads, shuffle reduction), with the
-// gathered right-hand side staged in shared memory.  No atomics on values:
-// every output entry is produced by exactly one warp in a fixed order, so the
-// result is bitwise reproducible and independent of the number of GPUs.
+// Inter-CTA data travel in "LL" (low-latency) form: every double is stored as
+// two 8-byte units (32-bit payload | 32-bit launch epoch).  An 8-byte access
+// is single-copy atomic, so a reader that sees the current epoch in both units
+// has the value: data and flag arrive in the same transaction, with no
+// fences, no separate flag round trip and nothing to reset between launches
+// (the epoch advances every launch).  This is the idea of NCCL's LL protocol,
+// applied to the tree transforms.
+//
+// Every task starts from a host-built record (plan creation), so its first
+// memory round trip already yields all offsets it needs:
+//
+//   A forward   tickets [0, c_leaves) in leaf preorder: x_hat_t = V_t^T x|_t
+//               (V_t by TMA bulk copy, x gathered through col_perm).  Then the
+//               CTA climbs while its cluster is the RIGHT child: it reads the
+//               left sibling's coefficients (written by a smaller ticket),
+//               computes x_hat_p = E_c0^T x_hat_c0 + E_c1^T x_hat_c1
+//               (ClusterBasis.forward, containers.py:201-212; [E_c0; E_c1]
+//               staged by cp.async while it waits) and publishes x_hat_p.
+//   B near      one band of rows of a row leaf's nearfield matrix
+//               [D_b1 D_b2 ...] (contiguous in HBM; one TMA bulk copy lands
+//               while the right-hand side is gathered): y_near = D x|_cols
+//               (containers.py:266-267).  Never waits.
+//   C coupling  one band of rows of a row cluster's coupling matrix
+//               [S_b1 S_b2 ...] (TMA): y_cpl = S [x_hat_s ...]
+//               (containers.py:259-264), reading the x_hat in LL form.
+//               Bands are ticketed parents first; the LAST band of cluster t
+//               (an empty band if t has no couplings) also runs t's downward
+//               step v_t = y_cpl_t + E_t v_parent (ClusterBasis.backward,
+//               containers.py:214-228): inner clusters publish v_t, leaves
+//               write y[row_perm] = y_near + V_t v_t (containers.py:268-269).
+//               The downward chain thus advances while the remaining
+//               coupling bands stream.
+//
+// Every output value is produced by one warp or thread in a fixed order:
+// bitwise reproducible, no atomics on values, and independent of the number
+// of GPUs (row sharding keeps per-row order).  The last CTA to finish resets
+// the ticket counter and advances the epoch, so the launch is self-contained
+// and can be captured in a CUDA graph.
 
+#include <cstdlib>
 #include <vector>
 
 #include "device_common.cuh"
 
+namespace h2b {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxVec = 512;        // max rank / leaf size of the vectors kept in smem
+constexpr int kMaxDepth = 64;
+constexpr int kStageBytes = 32768;  // TMA staging buffer per CTA (one band)
+
+// record layouts (int64 words)
+constexpr int kBandWords = 24;  // src_off, cols, rows, gidx_off, out_off, is_last, has_cpl, kind, then the
+                                // downward-step record of the band's cluster (coupling bands):
+                                // k, parent y_hat offset (-1 root), k_parent, e_off, y_hat offset,
+                                // is_leaf, v_off, start (size = rows of a leaf)
+constexpr int kFwdHead = 6;     // start, size, k, v_off, xhat_off, n_climb
+constexpr int kFwdLevel = 6;    // k0, kp, e_off_c0, e_off_own, xhat_off_c0, xhat_off_parent
+
+}  // namespace
+}  // namespace h2b
+
 struct h2b_plan {
     h2b_layout L;
     int device;
-    double* xp;        // n_cols permuted input
-    double* xhat;      // xhat_len
-    double* yhat;      // yhat_len
-    int* arrive;       // c_nodes
-    int* flag;         // r_nodes
-    int* ticket;       // [0] backward ticket counter, [1] matvec epoch (device-resident: graph-safe)
-    int fwd_smem;      // bytes
-    int bwd_smem;
-    int n_bwd;
-    double* hx;        // pinned host staging for h2b_matvec_host
-    double* hy;
+    uint64_t* xhat;     // LL: 2 x xhat_len
+    uint64_t* ycpl;     // LL: 2 x yhat_len (coupling part of y_hat)
+    uint64_t* yfin;     // LL: 2 x yhat_len (final y_hat of inner clusters)
+    uint64_t* ynear;    // LL: 2 x n_rows (permuted order)
+    int* ctrl;          // [0] ticket, [1] epoch, [2] done counter
+    int64_t* rec;       // task records
+    int64_t* fwd_off;   // per column leaf: record offset
+    int64_t band_base;  // record offset of band 0
+    int64_t dgidx_bytes;
+    int n_near, n_cpl;
+    int max_cols;
+    int smem;
+    int64_t e_bytes_r;
     double* dx;
     double* dy;
+    unsigned long long* trace;  // optional per-CTA timeline (H2B_TRACE=1)
 };
 
 namespace h2b {
 namespace {
 
-constexpr int kFwdThreads = 128;
-constexpr int kBwdThreads = 256;
+// ---------------------------------------------------------------------------
+// PTX helpers
 
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// 1-D TMA bulk copy global -> shared (16-byte aligned, size % 16 == 0)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// LDGSTS: 8-byte asynchronous global -> shared copies; a thread can have many
+// in flight (no register staging).
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
+}
+
+__device__ __forceinline__ int arrive_acq_rel(int* f) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(f) : "memory");
+    return old;
+}
+
+// ---- LL form: double -> (lo32 | epoch), (hi32 | epoch) ---------------------
+__device__ __forceinline__ void ll_store(uint64_t* p, double v, uint32_t epoch) {
+    const uint64_t b = static_cast<uint64_t>(__double_as_longlong(v));
+    const uint64_t e = static_cast<uint64_t>(epoch) << 32;
+    const uint64_t u0 = (b & 0xffffffffull) | e, u1 = (b >> 32) | e;
+    asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(p), "l"(u0), "l"(u1) : "memory");
+}
+
+__device__ __forceinline__ bool ll_try(const uint64_t* p, uint32_t epoch, double& v) {
+    uint64_t u0, u1;
+    asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(u0), "=l"(u1) : "l"(p) : "memory");
+    if ((uint32_t)(u0 >> 32) != epoch || (uint32_t)(u1 >> 32) != epoch) return false;
+    v = __longlong_as_double(static_cast<long long>((u0 & 0xffffffffull) | (u1 << 32)));
+    return true;
+}
+
+__device__ __forceinline__ double ll_load(const uint64_t* p, uint32_t epoch) {
+    double v;
+    if (ll_try(p, epoch, v)) return v;
+    while (!ll_try(p, epoch, v)) __nanosleep(32);
     return v;
 }
 
-// out[i] (i < rows) = sum_c M[i*ld + c] * v[c] for c < cols, one warp per row.
-// M rows are read with coalesced loads; v is in shared memory.
-__device__ __forceinline__ double row_dot(const double* __restrict__ row, const double* __restrict__ v,
-                                          int cols, int lane) {
-    double acc = 0.0;
-    const bool al16 = ((reinterpret_cast<uintptr_t>(row) & 15) == 0);
-    if (al16) {
-        const double2* r2 = reinterpret_cast<const double2*>(row);
-        const int c2 = cols >> 1;
-        int c = lane;
-        for (; c + 32 < c2; c += 64) {
-            const double2 a = __ldcs(r2 + c);
-            const double2 b = __ldcs(r2 + c + 32);
-            acc = fma(a.x, v[2 * c], acc);
-            acc = fma(a.y, v[2 * c + 1], acc);
-            acc = fma(b.x, v[2 * c + 64], acc);
-            acc = fma(b.y, v[2 * c + 65], acc);
-        }
-        for (; c < c2; c += 32) {
-            const double2 a = __ldcs(r2 + c);
-            acc = fma(a.x, v[2 * c], acc);
-            acc = fma(a.y, v[2 * c + 1], acc);
-        }
-        if ((cols & 1) && lane == 0) acc = fma(__ldcs(row + cols - 1), v[cols - 1], acc);
-    } else {
-        for (int c = lane; c < cols; c += 32) acc = fma(__ldcs(row + c), v[c], acc);
+__device__ __forceinline__ void mark(unsigned long long* m, int i) {
+    if (m && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        m[i] = t;
     }
-    return warp_sum(acc);
 }
 
-// xhat (k) = M^T v for M (rows x k) row-major, all threads of the CTA.
-// Threads are split into groups over rows; partial sums reduced in smem.
-__device__ void transposed_product(const double* __restrict__ M, const double* __restrict__ v, int rows,
-                                   int k, double* __restrict__ red, double* __restrict__ out) {
-    const int nt = blockDim.x;
-    if (k <= 0) return;
-    const int kc = min(k, nt);
-    const int groups = max(1, nt / kc);
-    for (int c0 = 0; c0 < k; c0 += kc) {
-        const int tid = threadIdx.x;
-        const int c = tid % kc, g = tid / kc;
-        double acc = 0.0;
-        if (g < groups && c0 + c < k) {
-            for (int r = g; r < rows; r += groups) acc = fma(M[(int64_t)r * k + c0 + c], v[r], acc);
+// ---------------------------------------------------------------------------
+// dense building blocks (operands in shared memory unless noted)
+
+// out[i] = M[i*ld : i*ld+cols] . v, i < rows.  Few rows: one row per warp
+// (two partial sums per lane); many rows: each warp owns 4 rows at a time
+// (4 independent dot products, interleaved shuffle reductions).
+__device__ __forceinline__ void rows_dot(const double* M, int64_t ld, int rows, int cols, const double* v,
+                                         double* out) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (rows < 4 * kWarps) {
+        for (int r = warp; r < rows; r += kWarps) {
+            const double* row = M + (int64_t)r * ld;
+            double a0 = 0.0, a1 = 0.0;
+            int c = lane;
+            for (; c + 32 < cols; c += 64) {
+                a0 = fma(row[c], v[c], a0);
+                a1 = fma(row[c + 32], v[c + 32], a1);
+            }
+            if (c < cols) a0 = fma(row[c], v[c], a0);
+            double sum = a0 + a1;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            if (lane == 0) out[r] = sum;
         }
+        return;
+    }
+    for (int r0 = 4 * warp; r0 < rows; r0 += 4 * kWarps) {
+        const int nr = min(4, rows - r0);
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int c = lane; c < cols; c += 32) {
+            const double vc = v[c];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (i < nr) acc[i] = fma(M[(int64_t)(r0 + i) * ld + c], vc, acc[i]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+        if (lane < nr) {
+            double r = acc[0];
+#pragma unroll
+            for (int i = 1; i < 4; ++i)
+                if (lane == i) r = acc[i];
+            out[r0 + lane] = r;
+        }
+    }
+}
+
+// out[c] = sum_r M[r*k + c] v[r], c < k: warps split rows, lanes columns,
+// partials reduced through `red` (kWarps x 32).  Ends with __syncthreads().
+__device__ void cols_dot(const double* M, int rows, int k, const double* v, double* red, double* out) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int c0 = 0; c0 < k; c0 += 32) {
+        const int c = c0 + lane;
+        double a0 = 0.0, a1 = 0.0;
+        if (c < k) {
+            int r = warp;
+            for (; r + kWarps < rows; r += 2 * kWarps) {
+                a0 = fma(M[(int64_t)r * k + c], v[r], a0);
+                a1 = fma(M[(int64_t)(r + kWarps) * k + c], v[r + kWarps], a1);
+            }
+            if (r < rows) a0 = fma(M[(int64_t)r * k + c], v[r], a0);
+        }
+        red[warp * 32 + lane] = a0 + a1;
         __syncthreads();
-        if (g < groups) red[g * kc + c] = acc;
-        __syncthreads();
-        if (tid < kc && c0 + tid < k) {
+        if (warp == 0 && c < k) {
             double s = 0.0;
-            for (int gg = 0; gg < groups; ++gg) s += red[gg * kc + tid];
-            out[c0 + tid] = s;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) s += red[w * 32 + lane];
+            out[c] = s;
         }
         __syncthreads();
     }
 }
 
-__global__ void __launch_bounds__(kFwdThreads) k_forward(h2b_layout L, const double* __restrict__ x,
-                                                        double* __restrict__ xp, double* __restrict__ xhat,
-                                                        int* __restrict__ arrive, int* __restrict__ ticket) {
-    extern __shared__ double sm[];
-    __shared__ int s_last;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        ticket[0] = 0;  // backward's ticket counter
-        ticket[1] += 1; // epoch of this matvec (flags compare against it)
-    }
-    const int leaf = L.c_leaf_list[blockIdx.x];
-    const int start = L.c_start[leaf], size = L.c_size[leaf], k = L.c_rank[leaf];
-    double* xs = sm;                 // max leaf size
-    double* red = sm + 1024;         // reduction scratch (kFwdThreads)
-    double* tmp = red + kFwdThreads; // child-sum staging
-    for (int r = threadIdx.x; r < size; r += blockDim.x) {
-        const double v = x[L.col_perm[start + r]];
-        xs[r] = v;
-        xp[start + r] = v;
-    }
-    __syncthreads();
-    transposed_product(L.c_V + L.c_v_off[leaf], xs, size, k, red, xhat + L.c_xhat_off[leaf]);
-    int node = leaf;
-    while (true) {
-        const int parent = L.c_parent[node];
-        if (parent < 0) break;
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            const int old = atomicAdd(arrive + parent, 1);
-            s_last = (old == 1);
-            if (old == 1) arrive[parent] = 0;  // reset for the next matvec
+// Gather rhs[i] = src[idx[i]], i < n: all index loads, then all value loads.
+__device__ __forceinline__ void gather(double* rhs, const double* __restrict__ src, const int32_t* idx, int n) {
+    constexpr int kU = 4;
+    for (int base = 0; base < n; base += kU * kThreads) {
+        int ix[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int i = base + u * kThreads + (int)threadIdx.x;
+            ix[u] = i < n ? __ldg(idx + i) : -1;
         }
-        __syncthreads();
-        if (!s_last) break;
-        __threadfence();
-        const int kp = L.c_rank[parent];
-        double* out = xhat + L.c_xhat_off[parent];
-        // first child writes, second accumulates (child order, containers.py:209-211)
-        for (int ci = 0; ci < 2; ++ci) {
-            const int ch = L.c_child[2 * parent + ci];
-            const int kc = L.c_rank[ch];
-            const double* xc = xhat + L.c_xhat_off[ch];
-            for (int r = threadIdx.x; r < kc; r += blockDim.x) tmp[r] = __ldcg(xc + r);
-            __syncthreads();
-            transposed_product(L.c_E + L.c_e_off[ch], tmp, kc, kp, red, tmp + 1024);
-            for (int c = threadIdx.x; c < kp; c += blockDim.x) {
-                const double v = tmp[1024 + c];
-                out[c] = ci == 0 ? v : __ldcg(out + c) + v;
-            }
-            __syncthreads();
+        double v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) v[u] = ix[u] >= 0 ? __ldg(src + ix[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int i = base + u * kThreads + (int)threadIdx.x;
+            if (i < n) rhs[i] = v[u];
         }
-        node = parent;
     }
 }
 
-__global__ void __launch_bounds__(kBwdThreads) k_backward(h2b_layout L, const double* __restrict__ xp,
-                                                         const double* __restrict__ xhat,
-                                                         double* __restrict__ yhat, double* __restrict__ y,
-                                                         int* __restrict__ flag, int* __restrict__ ticket,
-                                                         int smem_cols) {
-    extern __shared__ double sm[];
-    __shared__ int s_node, s_epoch;
+// Gather from LL form: rhs[i] = LL[idx[i]] (spins until the producer's epoch).
+__device__ __forceinline__ void gather_ll(double* rhs, const uint64_t* ll, const int32_t* idx, int n,
+                                          uint32_t epoch) {
+    for (int i = threadIdx.x; i < n; i += kThreads) rhs[i] = ll_load(ll + 2 * (int64_t)__ldg(idx + i), epoch);
+}
+
+struct Shared {
+    unsigned long long* mark;  // trace slots of this CTA (5 phase marks) or null
+    uint64_t* bar;             // mbarrier of the staging buffer
+    char* stage;               // kStageBytes, 128-byte aligned
+    double* rhs;               // max_cols
+    double* va;                // kMaxVec
+    double* vb;                // kMaxVec
+    double* red;               // kWarps * 32
+    int64_t* rec;              // small record cache
+};
+
+// Thread 0 starts staging `bytes` (TMA bulk copy when it fits and is 16-byte
+// aligned; otherwise a plain arrive).  Returns where to read the data from.
+__device__ __forceinline__ const double* stage_issue(const Shared& s, const double* src, int64_t bytes) {
+    const bool fits = bytes > 0 && bytes <= kStageBytes && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+                      (bytes & 15) == 0;
     if (threadIdx.x == 0) {
-        const int tk = atomicAdd(ticket, 1);
-        s_node = L.owned ? L.owned[tk] : L.r_order[tk];
-        s_epoch = *reinterpret_cast<volatile int*>(ticket + 1);
-    }
-    __syncthreads();
-    const int node = s_node;
-    const int epoch = s_epoch;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    const int k = L.r_rank[node];
-    const int parent = L.r_parent[node];
-    const bool leaf = L.r_v_off[node] >= 0;
-    double* vg = sm;                       // gathered right-hand side (smem_cols)
-    double* yh = sm + smem_cols;           // y_hat_t (<= 1024)
-    double* yp = yh + 1024;                // y_hat_parent (<= 1024)
-    double* yn = yp + 1024;                // nearfield rows (<= 1024)
-
-    // 1. coupling y_hat_t = S_t [x_hat_s ...]
-    const int K = L.s_cols[node];
-    if (K > 0) {
-        int off = 0;
-        for (int f = L.far_ptr[node]; f < L.far_ptr[node + 1]; ++f) {
-            const int s = L.far_col[f];
-            const int ks = L.c_rank[s];
-            const double* src = xhat + L.c_xhat_off[s];
-            for (int c = threadIdx.x; c < ks; c += blockDim.x) vg[off + c] = src[c];
-            off += ks;
-        }
-        __syncthreads();
-        const double* S = L.S + L.s_off[node];
-        for (int i = warp; i < k; i += nw) {
-            const double v = row_dot(S + (int64_t)i * K, vg, K, lane);
-            if (lane == 0) yh[i] = v;
-        }
-    } else {
-        for (int i = threadIdx.x; i < k; i += blockDim.x) yh[i] = 0.0;
-    }
-    __syncthreads();
-    // 2. nearfield rows of a leaf (independent of the parent)
-    const int start = L.r_start[node], size = L.r_size[node];
-    if (leaf) {
-        const int C = L.d_cols[node];
-        if (C > 0) {
-            int off = 0;
-            for (int f = L.near_ptr[node]; f < L.near_ptr[node + 1]; ++f) {
-                const int s = L.near_col[f];
-                const int ss = L.c_start[s], sz = L.c_size[s];
-                for (int c = threadIdx.x; c < sz; c += blockDim.x) vg[off + c] = xp[ss + c];
-                off += sz;
-            }
-            __syncthreads();
-            const double* D = L.D + L.d_off[node];
-            for (int r = warp; r < size; r += nw) {
-                const double v = row_dot(D + (int64_t)r * C, vg, C, lane);
-                if (lane == 0) yn[r] = v;
-            }
+        if (fits) {
+            mbar_expect_tx(s.bar, (uint32_t)bytes);
+            bulk_g2s(s.stage, src, (uint32_t)bytes, s.bar);
         } else {
-            for (int r = threadIdx.x; r < size; r += blockDim.x) yn[r] = 0.0;
+            mbar_arrive(s.bar);
         }
     }
-    // 3. parent contribution
-    if (parent >= 0) {
-        if (threadIdx.x == 0) {
-            volatile int* fp = flag + parent;
-            while (*fp != epoch) __nanosleep(64);
-        }
+    return fits ? reinterpret_cast<const double*>(s.stage) : src;
+}
+
+__device__ void prefetch_slice(const double* base, int64_t bytes, int part, int parts) {
+    if (!base || bytes <= 0) return;
+    const int64_t lines = (bytes + 127) / 128;
+    const int64_t per = (lines + parts - 1) / parts;
+    const int64_t l0 = per * part, l1 = min(lines, l0 + per);
+    const char* b = reinterpret_cast<const char*>(base);
+    for (int64_t l = l0 + threadIdx.x; l < l1; l += blockDim.x) prefetch_l2(b + 128 * l);
+}
+
+// copy a record of n words into the shared record cache (one round trip)
+__device__ __forceinline__ void load_rec(const Shared& s, const int64_t* src, int n) {
+    for (int i = threadIdx.x; i < n; i += kThreads) s.rec[i] = __ldg(src + i);
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// A: forward transform of one column leaf; climb while the right child
+
+__device__ void task_forward(const h2b_layout& L, const int64_t* rec, const double* __restrict__ x,
+                             uint64_t* xhat, uint32_t epoch, const Shared& s) {
+    // header + climb levels in one load
+    const int n_climb_max = kMaxDepth;
+    {
+        const int n = kFwdHead + kFwdLevel * n_climb_max;
+        for (int i = threadIdx.x; i < kFwdHead; i += kThreads) s.rec[i] = __ldg(rec + i);
         __syncthreads();
-        __threadfence();
-        const int kp = L.r_rank[parent];
-        const double* src = yhat + L.r_yhat_off[parent];
-        for (int c = threadIdx.x; c < kp; c += blockDim.x) yp[c] = __ldcg(src + c);
-        __syncthreads();
-        const double* E = L.r_E + L.r_e_off[node];
-        for (int i = warp; i < k; i += nw) {
-            const double v = row_dot(E + (int64_t)i * kp, yp, kp, lane);
-            if (lane == 0) yh[i] += v;
+        const int nc = (int)s.rec[5];
+        for (int i = kFwdHead + threadIdx.x; i < kFwdHead + kFwdLevel * nc && i < n; i += kThreads)
+            s.rec[i] = __ldg(rec + i);
+    }
+    const int start = (int)s.rec[0], size = (int)s.rec[1], k = (int)s.rec[2];
+    const int64_t v_off = s.rec[3], xhat_off = s.rec[4];
+    const int n_climb = (int)s.rec[5];
+    const double* V = stage_issue(s, L.c_V + v_off, ((int64_t)size * k * 8 + 15) & ~int64_t(15));
+    for (int r = threadIdx.x; r < size; r += blockDim.x) s.va[r] = __ldg(x + L.col_perm[start + r]);
+    mbar_wait(s.bar, 0);
+    __syncthreads();
+    cols_dot(V, size, k, s.va, s.red, s.vb);  // own coefficients stay in s.vb
+    {
+        uint64_t* dst = xhat + 2 * xhat_off;
+        for (int c = threadIdx.x; c < k; c += blockDim.x) ll_store(dst + 2 * c, s.vb[c], epoch);
+    }
+    double* buf = reinterpret_cast<double*>(s.stage);  // [E_c0; E_own]
+    int k1 = k;
+    for (int j = 0; j < n_climb; ++j) {
+        const int64_t* lv = s.rec + kFwdHead + kFwdLevel * j;
+        const int k0 = (int)lv[0], kp = (int)lv[1];
+        const int n0 = k0 * kp, n1 = k1 * kp;
+        const bool in_smem = (n0 + n1) * 8 <= kStageBytes;
+        __syncthreads();  // previous users of buf / va are done
+        if (in_smem) {
+            const double* E0 = L.c_E + lv[2];
+            const double* E1 = L.c_E + lv[3];
+            for (int i = threadIdx.x; i < n0; i += kThreads) cp_async8(buf + i, E0 + i);
+            for (int i = threadIdx.x; i < n1; i += kThreads) cp_async8(buf + n0 + i, E1 + i);
         }
+        // v = [x_hat_c0; x_hat_own]: the left sibling's from LL (smaller ticket)
+        const uint64_t* xs = xhat + 2 * lv[4];
+        for (int r = threadIdx.x; r < k0; r += kThreads) s.va[r] = ll_load(xs + 2 * r, epoch);
+        for (int r = threadIdx.x; r < k1; r += kThreads) s.va[k0 + r] = s.vb[r];
+        cp_async_wait_all();
+        __syncthreads();
+        if (in_smem) {
+            cols_dot(buf, k0 + k1, kp, s.va, s.red, s.vb);
+        } else {
+            cols_dot(L.c_E + lv[2], k0, kp, s.va, s.red, s.vb);
+            for (int c = threadIdx.x; c < kp; c += kThreads) s.rhs[c] = s.vb[c];
+            __syncthreads();
+            cols_dot(L.c_E + lv[3], k1, kp, s.va + k0, s.red, s.vb);
+            for (int c = threadIdx.x; c < kp; c += kThreads) s.vb[c] += s.rhs[c];
+            __syncthreads();
+        }
+        uint64_t* dst = xhat + 2 * lv[5];
+        for (int c = threadIdx.x; c < kp; c += kThreads) ll_store(dst + 2 * c, s.vb[c], epoch);
+        k1 = kp;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// B / C: one band of a nearfield (x gathered) or coupling (x_hat, LL) matrix
+
+// Downward step of a row cluster t, run by the last coupling band of t (or by
+// an empty band when t has no couplings):  v_t = y_cpl_t + E_t v_parent
+// (ClusterBasis.backward, containers.py:214-228).  Inner clusters publish v_t
+// (LL); a leaf expands y[row_perm] = y_near + V_t v_t (containers.py:268-269).
+// Every value waited for is produced by a smaller ticket: the other bands of
+// t, the parent's last band (parents are ticketed first) and the near bands.
+__device__ void descent(const h2b_layout& L, const int64_t* d, const uint64_t* ycpl, uint64_t* yfin,
+                        const uint64_t* ynear, double* y, uint32_t epoch, bool has_cpl, const Shared& s) {
+    const int k = (int)d[0], kp = (int)d[2];
+    const int64_t par_off = d[1], e_off = d[3], yoff = d[4];
+    const bool leaf = d[5] != 0;
+    const int64_t v_off = d[6];
+    const int start = (int)d[7];
+    double* Es = reinterpret_cast<double*>(s.stage);
+    const bool e_smem = par_off >= 0 && k * kp <= kStageBytes / 8;
+    if (e_smem)
+        for (int i = threadIdx.x; i < k * kp; i += kThreads) cp_async8(Es + i, L.r_E + e_off + i);
+    const uint64_t* yc = ycpl + 2 * yoff;
+    for (int i = threadIdx.x; i < k; i += kThreads) s.va[i] = has_cpl ? ll_load(yc + 2 * i, epoch) : 0.0;
+    if (par_off >= 0) {
+        const uint64_t* yp = yfin + 2 * par_off;
+        for (int i = threadIdx.x; i < kp; i += kThreads) s.rhs[i] = ll_load(yp + 2 * i, epoch);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    mark(s.mark, 4);
+    if (par_off >= 0 && k > 0) {
+        rows_dot(e_smem ? Es : L.r_E + e_off, kp, k, kp, s.rhs, s.vb);
+        __syncthreads();
+        for (int i = threadIdx.x; i < k; i += kThreads) s.va[i] += s.vb[i];
+        __syncthreads();
+    }
+    if (!leaf) {
+        uint64_t* dst = yfin + 2 * yoff;
+        for (int i = threadIdx.x; i < k; i += kThreads) ll_store(dst + 2 * i, s.va[i], epoch);
+        return;
+    }
+    const int size = (int)d[8];
+    const int nv = size * k;
+    const bool v_smem = nv <= kStageBytes / 8;
+    const double* Vg = L.r_V + v_off;
+    if (v_smem) {
+        for (int i = threadIdx.x; i < nv; i += kThreads) cp_async8(Es + i, Vg + i);
+        cp_async_wait_all();
     }
     __syncthreads();
-    // 4. leaf: expand and un-permute; inner node: publish y_hat_t
-    if (leaf) {
-        const double* Vt = L.r_V + L.r_v_off[node];
-        for (int r = warp; r < size; r += nw) {
-            const double v = k > 0 ? row_dot(Vt + (int64_t)r * k, yh, k, lane) : 0.0;
-            if (lane == 0) y[L.row_perm[start + r]] = yn[r] + v;
-        }
-    } else {
-        double* dst = yhat + L.r_yhat_off[node];
-        for (int i = threadIdx.x; i < k; i += blockDim.x) dst[i] = yh[i];
-        __threadfence();
+    if (k > 0) rows_dot(v_smem ? Es : Vg, k, size, k, s.va, s.vb);
+    __syncthreads();
+    const uint64_t* yn = ynear + 2 * (int64_t)start;
+    for (int i = threadIdx.x; i < size; i += blockDim.x)
+        y[L.row_perm[start + i]] = ll_load(yn + 2 * i, epoch) + (k > 0 ? s.vb[i] : 0.0);
+}
+
+// The band record is already in s.rec (kind in word 7: 0 near, 1 coupling).
+template <bool kCoupling>
+__device__ void task_band(const h2b_layout& L, const double* __restrict__ x, const uint64_t* xhat, uint64_t* out,
+                          uint64_t* yfin, const uint64_t* ycpl, const uint64_t* ynear, double* y, uint32_t epoch,
+                          const Shared& s) {
+    const int64_t src_off = s.rec[0], gi_off = s.rec[3], out_off = s.rec[4];
+    const int cols = (int)s.rec[1], rows = (int)s.rec[2];
+    if (rows > 0) {
+        const double* base = kCoupling ? L.S : L.D;
+        const double* M = stage_issue(s, base + src_off, (int64_t)rows * cols * 8);
+        mark(s.mark, 0);
+        if (kCoupling)
+            gather_ll(s.rhs, xhat, L.s_gidx + gi_off, cols, epoch);
+        else
+            gather(s.rhs, x, L.d_gidx + gi_off, cols);
+        mark(s.mark, 1);
+        mbar_wait(s.bar, 0);
         __syncthreads();
-        if (threadIdx.x == 0) atomicExch(flag + node, epoch);
+        mark(s.mark, 2);
+        rows_dot(M, cols, rows, cols, s.rhs, s.va);
+        __syncthreads();
+        mark(s.mark, 3);
+        uint64_t* dst = out + 2 * out_off;
+        for (int i = threadIdx.x; i < rows; i += blockDim.x) ll_store(dst + 2 * i, s.va[i], epoch);
+    }
+    if (kCoupling && s.rec[5]) {
+        __syncthreads();
+        descent(L, s.rec + 8, ycpl, yfin, ynear, y, epoch, s.rec[6] != 0, s);
+    }
+}
+
+struct KArgs {
+    h2b_layout L;
+    const int64_t* rec;
+    const int64_t* fwd_off;
+    int64_t band_base, band_bytes, dgidx_bytes;
+    int n_near, n_cpl, n_near_a, n_inner_bands;
+    int max_cols;
+    int64_t e_bytes_r;
+    uint64_t *xhat, *ycpl, *yfin, *ynear;
+    int* ctrl;
+    unsigned long long* trace;
+};
+
+__global__ void __launch_bounds__(kThreads, 4) k_matvec(const KArgs a, const double* __restrict__ x,
+                                                       double* __restrict__ y) {
+    extern __shared__ __align__(128) char smraw[];
+    __shared__ int s_ticket;
+    __shared__ uint32_t s_epoch;
+    __shared__ int64_t s_rec[kFwdHead + kFwdLevel * kMaxDepth];
+    const h2b_layout& L = a.L;
+    Shared s;
+    s.bar = reinterpret_cast<uint64_t*>(smraw);
+    s.stage = smraw + 128;
+    s.rhs = reinterpret_cast<double*>(smraw + 128 + kStageBytes);
+    s.va = s.rhs + a.max_cols;
+    s.vb = s.va + kMaxVec;
+    s.red = s.vb + kMaxVec;
+    s.rec = s_rec;
+    if (threadIdx.x == 0) {
+        s_ticket = atomicAdd(a.ctrl, 1);
+        s_epoch = (uint32_t)(*reinterpret_cast<volatile int*>(a.ctrl + 1)) + 1u;
+        mbar_init(s.bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int ticket = s_ticket;
+    const uint32_t epoch = s_epoch;
+    unsigned long long t_begin = 0;
+    if (a.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
+    s.mark = a.trace ? a.trace + 8 * ticket + 3 : nullptr;
+    const int tB = L.c_leaves;
+
+    if (ticket < tB) {
+        // pull the band records, the nearfield gather lists and x into L2 for
+        // the streaming tasks that follow (fire-and-forget; LL needs no fences)
+        prefetch_slice(reinterpret_cast<const double*>(a.rec + a.band_base), a.band_bytes, ticket, L.c_leaves);
+        prefetch_slice(reinterpret_cast<const double*>(L.d_gidx), a.dgidx_bytes, ticket, L.c_leaves);
+        prefetch_slice(x, 8 * L.n_cols, ticket, L.c_leaves);
+        task_forward(L, a.rec + __ldg(a.fwd_off + ticket), x, a.xhat, epoch, s);
+    } else {
+        const int b = ticket - tB;
+        // the first bands pull the row-basis transfer matrices into L2
+        const int np = min(a.n_near + a.n_cpl, 512);
+        if (b < np) prefetch_slice(L.r_E, a.e_bytes_r, b, np);
+        const int64_t* rec = a.rec + a.band_base + (int64_t)kBandWords * b;
+        load_rec(s, rec, kBandWords);
+        if (s.rec[7] == 0)
+            task_band<false>(L, x, a.xhat, a.ynear, a.yfin, a.ycpl, a.ynear, y, epoch, s);
+        else
+            task_band<true>(L, x, a.xhat, a.ycpl, a.yfin, a.ycpl, a.ynear, y, epoch, s);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (a.trace) {
+            unsigned long long t_end;
+            unsigned smid;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            a.trace[8 * ticket] = t_begin;
+            a.trace[8 * ticket + 1] = t_end;
+            a.trace[8 * ticket + 2] = smid;
+        }
+        // last CTA out resets the ticket counter and advances the epoch (every
+        // CTA has taken its ticket and read the epoch before it counts itself)
+        const int done = arrive_acq_rel(a.ctrl + 2);
+        if (done == (int)gridDim.x - 1) {
+            a.ctrl[0] = 0;
+            a.ctrl[2] = 0;
+            atomicAdd(a.ctrl + 1, 1);
+        }
     }
 }
 
@@ -287,6 +580,12 @@ __global__ void k_diagonal(h2b_layout L, double* __restrict__ diag) {
     }
 }
 
+template <typename T>
+cudaError_t fetch(const T* d, int64_t n, std::vector<T>& h) {
+    h.resize((size_t)std::max<int64_t>(n, 0));
+    return n > 0 ? cudaMemcpy(h.data(), d, sizeof(T) * n, cudaMemcpyDeviceToHost) : cudaSuccess;
+}
+
 }  // namespace
 }  // namespace h2b
 
@@ -296,58 +595,174 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
     if (!layout || !out) return fail(H2B_ERR_INVALID, "h2b_plan_create: null pointer");
     const h2b_layout& L = *layout;
     if (L.c_nodes <= 0 || L.r_nodes <= 0 || L.c_leaves <= 0) return fail(H2B_ERR_INVALID, "h2b_plan_create: empty tree");
-    h2b_plan* p = new (std::nothrow) h2b_plan();
-    if (!p) return fail(H2B_ERR_INVALID, "h2b_plan_create: out of host memory");
-    p->L = L;
-    H2B_CUDA_TRY(cudaGetDevice(&p->device));
-    auto alloc = [&](void** ptr, size_t bytes) -> cudaError_t {
-        return cudaMalloc(ptr, bytes ? bytes : 8);
-    };
-    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->xp), sizeof(double) * L.n_cols));
-    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->xhat), sizeof(double) * L.xhat_len));
-    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->yhat), sizeof(double) * L.yhat_len));
-    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->arrive), sizeof(int) * L.c_nodes));
-    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->flag), sizeof(int) * L.r_nodes));
-    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->ticket), 2 * sizeof(int)));
-    H2B_CUDA_TRY(cudaMemset(p->arrive, 0, sizeof(int) * L.c_nodes));
-    H2B_CUDA_TRY(cudaMemset(p->flag, 0, sizeof(int) * L.r_nodes));
-    H2B_CUDA_TRY(cudaMemset(p->ticket, 0, 2 * sizeof(int)));
-    // shared memory: largest gathered right-hand side over coupling / nearfield rows
-    std::vector<int32_t> scols(L.r_nodes), dcols(L.r_nodes), rsize(L.r_nodes), rrank(L.r_nodes), crank(L.c_nodes),
-        csize(L.c_nodes);
-    H2B_CUDA_TRY(cudaMemcpy(scols.data(), L.s_cols, sizeof(int32_t) * L.r_nodes, cudaMemcpyDeviceToHost));
-    H2B_CUDA_TRY(cudaMemcpy(dcols.data(), L.d_cols, sizeof(int32_t) * L.r_nodes, cudaMemcpyDeviceToHost));
-    H2B_CUDA_TRY(cudaMemcpy(rsize.data(), L.r_size, sizeof(int32_t) * L.r_nodes, cudaMemcpyDeviceToHost));
-    H2B_CUDA_TRY(cudaMemcpy(rrank.data(), L.r_rank, sizeof(int32_t) * L.r_nodes, cudaMemcpyDeviceToHost));
-    H2B_CUDA_TRY(cudaMemcpy(crank.data(), L.c_rank, sizeof(int32_t) * L.c_nodes, cudaMemcpyDeviceToHost));
-    H2B_CUDA_TRY(cudaMemcpy(csize.data(), L.c_size, sizeof(int32_t) * L.c_nodes, cudaMemcpyDeviceToHost));
-    std::vector<int64_t> rvoff(L.r_nodes);
-    H2B_CUDA_TRY(cudaMemcpy(rvoff.data(), L.r_v_off, sizeof(int64_t) * L.r_nodes, cudaMemcpyDeviceToHost));
-    int maxcols = 1, maxk = 0, maxleaf = 0;
+    if (!L.d_gidx || !L.d_goff || !L.s_gidx || !L.s_goff)
+        return fail(H2B_ERR_INVALID, "h2b_plan_create: gather indices missing");
+    // host copies of the layout (plan creation only)
+    std::vector<int32_t> scols, dcols, rsize, rstart, rrank, rparent, crank, csize, cstart, cparent, cchild, order,
+        leaves;
+    std::vector<int64_t> rvoff, reoff, ryoff, soff, doff, sgoff, dgoff, cvoff, ceoff, cxoff;
+    H2B_CUDA_TRY(fetch(L.s_cols, L.r_nodes, scols));
+    H2B_CUDA_TRY(fetch(L.d_cols, L.r_nodes, dcols));
+    H2B_CUDA_TRY(fetch(L.r_size, L.r_nodes, rsize));
+    H2B_CUDA_TRY(fetch(L.r_start, L.r_nodes, rstart));
+    H2B_CUDA_TRY(fetch(L.r_rank, L.r_nodes, rrank));
+    H2B_CUDA_TRY(fetch(L.r_parent, L.r_nodes, rparent));
+    H2B_CUDA_TRY(fetch(L.c_rank, L.c_nodes, crank));
+    H2B_CUDA_TRY(fetch(L.c_size, L.c_nodes, csize));
+    H2B_CUDA_TRY(fetch(L.c_start, L.c_nodes, cstart));
+    H2B_CUDA_TRY(fetch(L.c_parent, L.c_nodes, cparent));
+    H2B_CUDA_TRY(fetch(L.c_child, 2 * (int64_t)L.c_nodes, cchild));
+    H2B_CUDA_TRY(fetch(L.c_leaf_list, L.c_leaves, leaves));
+    H2B_CUDA_TRY(fetch(L.r_v_off, L.r_nodes, rvoff));
+    H2B_CUDA_TRY(fetch(L.r_e_off, L.r_nodes, reoff));
+    H2B_CUDA_TRY(fetch(L.r_yhat_off, L.r_nodes, ryoff));
+    H2B_CUDA_TRY(fetch(L.s_off, L.r_nodes, soff));
+    H2B_CUDA_TRY(fetch(L.d_off, L.r_nodes, doff));
+    H2B_CUDA_TRY(fetch(L.s_goff, L.r_nodes, sgoff));
+    H2B_CUDA_TRY(fetch(L.d_goff, L.r_nodes, dgoff));
+    H2B_CUDA_TRY(fetch(L.c_v_off, L.c_nodes, cvoff));
+    H2B_CUDA_TRY(fetch(L.c_e_off, L.c_nodes, ceoff));
+    H2B_CUDA_TRY(fetch(L.c_xhat_off, L.c_nodes, cxoff));
+    if (L.owned) {
+        H2B_CUDA_TRY(fetch(L.owned, L.n_owned, order));
+    } else {
+        H2B_CUDA_TRY(fetch(L.r_order, L.r_nodes, order));
+    }
+    int maxcols = 2, maxk = 0, maxleaf = 0;
     for (int i = 0; i < L.r_nodes; ++i) {
         maxcols = std::max(maxcols, std::max(scols[i], dcols[i]));
         maxk = std::max(maxk, rrank[i]);
         if (rvoff[i] >= 0) maxleaf = std::max(maxleaf, rsize[i]);
     }
     for (int i = 0; i < L.c_nodes; ++i) maxk = std::max(maxk, crank[i]);
-    std::vector<int32_t> leaves(L.c_leaves);
-    H2B_CUDA_TRY(cudaMemcpy(leaves.data(), L.c_leaf_list, sizeof(int32_t) * L.c_leaves, cudaMemcpyDeviceToHost));
     for (int l : leaves) maxleaf = std::max(maxleaf, csize[l]);
-    if (maxk > 1024 || maxleaf > 1024) {
-        delete p;
-        return fail(H2B_ERR_INVALID, "h2b_plan_create: cluster rank or leaf size above 1024");
+    maxcols = std::max(maxcols, maxk);
+    if (maxk > kMaxVec || maxleaf > kMaxVec)
+        return fail(H2B_ERR_INVALID, "h2b_plan_create: cluster rank or leaf size above 512");
+    const int smem = 128 + kStageBytes + (int)sizeof(double) * (maxcols + 2 * kMaxVec + kWarps * 32);
+    if (smem > 227 * 1024) return fail(H2B_ERR_INVALID, "h2b_plan_create: gathered right-hand side exceeds shared memory");
+
+    std::vector<int64_t> rec, fwd_off(L.c_leaves);
+    // A: forward records (leaf, then the levels it climbs as the right child)
+    for (int i = 0; i < L.c_leaves; ++i) {
+        const int leaf = leaves[i];
+        fwd_off[i] = (int64_t)rec.size();
+        rec.insert(rec.end(), {cstart[leaf], csize[leaf], crank[leaf], cvoff[leaf], cxoff[leaf], 0});
+        const size_t hdr = rec.size() - kFwdHead;
+        int node = leaf, n = 0;
+        while (true) {
+            const int p = cparent[node];
+            if (p < 0 || cchild[2 * p + 1] != node) break;
+            const int c0 = cchild[2 * p];
+            if (n >= kMaxDepth) return fail(H2B_ERR_INVALID, "h2b_plan_create: tree deeper than 64 levels");
+            rec.insert(rec.end(), {crank[c0], crank[p], ceoff[c0], ceoff[node], cxoff[c0], cxoff[p]});
+            node = p;
+            ++n;
+        }
+        rec[hdr + 5] = n;
     }
-    p->bwd_smem = (int)sizeof(double) * (maxcols + 3 * 1024);
-    p->fwd_smem = (int)sizeof(double) * (1024 + kFwdThreads + 2048);
-    p->n_bwd = L.owned ? L.n_owned : L.r_nodes;
-    if (p->bwd_smem > 227 * 1024) {
-        delete p;
-        return fail(H2B_ERR_INVALID, "h2b_plan_create: gathered right-hand side exceeds shared memory");
+    // B/C: band records; rows per band so one band fits the TMA stage.  Near
+    // bands of the owned leaves, then coupling bands of the owned clusters
+    // parents first; the last band of a cluster (an empty one when it has no
+    // couplings) carries the cluster's downward-step record.
+    const int64_t band_base = (int64_t)rec.size();
+    auto add_bands = [&](int cols, int rows, int64_t src, int64_t gi, int64_t outo, int kind) {
+        const int per = std::max(1, (int)(kStageBytes / (8 * std::max(cols, 1))));
+        int n = 0;
+        for (int r0 = 0; r0 < rows; r0 += per, ++n) {
+            const int nr = std::min(per, rows - r0);
+            rec.insert(rec.end(), {src + (int64_t)r0 * cols, cols, nr, gi, outo + r0, 0, 0, kind});
+            rec.insert(rec.end(), kBandWords - 8, 0);
+        }
+        return n;
+    };
+    int n_cpl = 0;
+    auto add_cluster = [&](int u) {
+        const bool cpl = scols[u] > 0 && rrank[u] > 0;
+        int n = cpl ? add_bands(scols[u], rrank[u], soff[u], sgoff[u], ryoff[u], 1) : 0;
+        if (n == 0) {  // empty band: downward step only
+            rec.insert(rec.end(), {0, 0, 0, 0, 0, 0, 0, 1});
+            rec.insert(rec.end(), kBandWords - 8, 0);
+            n = 1;
+        }
+        n_cpl += n;
+        int64_t* last = rec.data() + rec.size() - kBandWords;
+        const int par = rparent[u];
+        const int64_t d[9] = {rrank[u], par >= 0 ? ryoff[par] : -1, par >= 0 ? rrank[par] : 0,
+                              par >= 0 ? reoff[u] : 0, ryoff[u], rvoff[u] >= 0 ? 1 : 0,
+                              rvoff[u] >= 0 ? rvoff[u] : 0, rstart[u], rsize[u]};
+        last[5] = 1;
+        last[6] = cpl ? 1 : 0;
+        for (int i = 0; i < 9; ++i) last[8 + i] = d[i];
+    };
+    // ticket order: near bands (first part) | inner-cluster coupling bands,
+    // parents first | near bands (rest) | leaf coupling bands.  The first near
+    // bands stream while the forward climb runs; the inner downward chain then
+    // advances while the remaining nearfield streams.
+    double split = 0.7;
+    if (const char* e = getenv("H2B_NEAR_SPLIT")) split = atof(e);
+    std::vector<int> owned_leaves;
+    for (int u : order)
+        if (rvoff[u] >= 0) owned_leaves.push_back(u);
+    const int n_leaf_a = (int)(split * owned_leaves.size());
+    int n_near = 0;
+    for (int i = 0; i < n_leaf_a; ++i) {
+        const int u = owned_leaves[i];
+        n_near += add_bands(dcols[u], rsize[u], doff[u], dgoff[u], rstart[u], 0);
     }
-    H2B_CUDA_TRY(cudaFuncSetAttribute(k_backward, cudaFuncAttributeMaxDynamicSharedMemorySize, p->bwd_smem));
-    H2B_CUDA_TRY(cudaFuncSetAttribute(k_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, p->fwd_smem));
-    H2B_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&p->hx), sizeof(double) * std::max<int64_t>(1, L.n_cols)));
-    H2B_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&p->hy), sizeof(double) * std::max<int64_t>(1, L.n_rows)));
+    for (int u : order)
+        if (rvoff[u] < 0) add_cluster(u);
+    for (size_t i = n_leaf_a; i < owned_leaves.size(); ++i) {
+        const int u = owned_leaves[i];
+        n_near += add_bands(dcols[u], rsize[u], doff[u], dgoff[u], rstart[u], 0);
+    }
+    for (int u : owned_leaves) add_cluster(u);
+    int64_t e_bytes_r = 0;
+    for (int i = 0; i < L.r_nodes; ++i)
+        if (rparent[i] >= 0 && reoff[i] >= 0)
+            e_bytes_r = std::max<int64_t>(e_bytes_r, 8 * (reoff[i] + (int64_t)rrank[i] * rrank[rparent[i]]));
+
+    h2b_plan* p = new (std::nothrow) h2b_plan();
+    if (!p) return fail(H2B_ERR_INVALID, "h2b_plan_create: out of host memory");
+    p->L = L;
+    p->n_near = n_near;
+    p->n_cpl = n_cpl;
+    p->band_base = band_base;
+    {
+        int64_t m = 0;
+        for (int i = 0; i < L.r_nodes; ++i)
+            if (rvoff[i] >= 0) m = std::max<int64_t>(m, 4 * (dgoff[i] + dcols[i]));
+        p->dgidx_bytes = m;
+    }
+    p->max_cols = maxcols;
+    p->smem = smem;
+    p->e_bytes_r = e_bytes_r;
+    H2B_CUDA_TRY(cudaGetDevice(&p->device));
+    auto alloc = [](void** ptr, size_t bytes) { return cudaMalloc(ptr, bytes ? bytes : 16); };
+    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->xhat), 16 * (size_t)L.xhat_len));
+    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->ycpl), 16 * (size_t)L.yhat_len));
+    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->yfin), 16 * (size_t)L.yhat_len));
+    H2B_CUDA_TRY(cudaMemset(p->yfin, 0, 16 * (size_t)L.yhat_len));
+    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->ynear), 16 * (size_t)L.n_rows));
+    H2B_CUDA_TRY(cudaMemset(p->xhat, 0, 16 * (size_t)L.xhat_len));
+    H2B_CUDA_TRY(cudaMemset(p->ycpl, 0, 16 * (size_t)L.yhat_len));
+    H2B_CUDA_TRY(cudaMemset(p->ynear, 0, 16 * (size_t)L.n_rows));
+    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->ctrl), 4 * sizeof(int)));
+    H2B_CUDA_TRY(cudaMemset(p->ctrl, 0, 4 * sizeof(int)));
+    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->rec), sizeof(int64_t) * std::max<size_t>(1, rec.size())));
+    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->fwd_off), sizeof(int64_t) * fwd_off.size()));
+    if (!rec.empty())
+        H2B_CUDA_TRY(cudaMemcpy(p->rec, rec.data(), sizeof(int64_t) * rec.size(), cudaMemcpyHostToDevice));
+    H2B_CUDA_TRY(cudaMemcpy(p->fwd_off, fwd_off.data(), sizeof(int64_t) * fwd_off.size(), cudaMemcpyHostToDevice));
+    H2B_CUDA_TRY(cudaFuncSetAttribute(k_matvec, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem));
+    p->trace = nullptr;
+    if (const char* tr = getenv("H2B_TRACE")) {
+        if (tr[0] == '1') {
+            const size_t n = (size_t)(L.c_leaves + n_near + n_cpl) * 8;
+            H2B_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&p->trace), n * sizeof(unsigned long long)));
+            H2B_CUDA_TRY(cudaMemset(p->trace, 0, n * sizeof(unsigned long long)));
+        }
+    }
     H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->dx), sizeof(double) * L.n_cols));
     H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->dy), sizeof(double) * L.n_rows));
     *out = p;
@@ -356,16 +771,9 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
 
 extern "C" int h2b_plan_destroy(h2b_plan* p) {
     if (!p) return ok();
-    cudaFree(p->xp);
-    cudaFree(p->xhat);
-    cudaFree(p->yhat);
-    cudaFree(p->arrive);
-    cudaFree(p->flag);
-    cudaFree(p->ticket);
-    cudaFree(p->dx);
-    cudaFree(p->dy);
-    cudaFreeHost(p->hx);
-    cudaFreeHost(p->hy);
+    void* bufs[] = {p->xhat, p->ycpl, p->yfin, p->ynear, p->ctrl, p->rec, p->fwd_off, p->dx, p->dy, p->trace};
+    for (void* q : bufs)
+        if (q) cudaFree(q);
     delete p;
     return ok();
 }
@@ -373,11 +781,25 @@ extern "C" int h2b_plan_destroy(h2b_plan* p) {
 extern "C" int h2b_matvec(h2b_plan* p, const double* d_x, double* d_y, void* stream) {
     if (!p || !d_x || !d_y) return fail(H2B_ERR_INVALID, "h2b_matvec: null pointer");
     cudaStream_t st = as_stream(stream);
-    k_forward<<<p->L.c_leaves, kFwdThreads, p->fwd_smem, st>>>(p->L, d_x, p->xp, p->xhat, p->arrive, p->ticket);
-    H2B_CUDA_TRY(cudaGetLastError());
-    int smem_cols = (p->bwd_smem / (int)sizeof(double)) - 3 * 1024;
-    k_backward<<<p->n_bwd, kBwdThreads, p->bwd_smem, st>>>(p->L, p->xp, p->xhat, p->yhat, d_y, p->flag,
-                                                          p->ticket, smem_cols);
+    KArgs a;
+    a.L = p->L;
+    a.rec = p->rec;
+    a.fwd_off = p->fwd_off;
+    a.band_base = p->band_base;
+    a.band_bytes = 8 * (int64_t)kBandWords * (p->n_near + p->n_cpl);
+    a.dgidx_bytes = p->dgidx_bytes;
+    a.n_near = p->n_near;
+    a.n_cpl = p->n_cpl;
+    a.max_cols = p->max_cols;
+    a.e_bytes_r = p->e_bytes_r;
+    a.xhat = p->xhat;
+    a.ycpl = p->ycpl;
+    a.yfin = p->yfin;
+    a.ynear = p->ynear;
+    a.ctrl = p->ctrl;
+    a.trace = p->trace;
+    const int grid = p->L.c_leaves + p->n_near + p->n_cpl;
+    k_matvec<<<grid, kThreads, p->smem, st>>>(a, d_x, d_y);
     H2B_CUDA_TRY(cudaGetLastError());
     return ok();
 }
@@ -389,6 +811,24 @@ extern "C" int h2b_matvec_host(h2b_plan* p, const double* h_x, double* h_y, void
     if (int rc = h2b_matvec(p, p->dx, p->dy, stream)) return rc;
     H2B_CUDA_TRY(cudaMemcpyAsync(h_y, p->dy, sizeof(double) * p->L.n_rows, cudaMemcpyDeviceToHost, st));
     H2B_CUDA_TRY(cudaStreamSynchronize(st));
+    return ok();
+}
+
+// Diagnostics: the per-CTA timeline of the last matvec when the plan was
+// created with H2B_TRACE=1: 8 words per ticket (start ns, end ns, SM id, 5
+// phase marks), then the task-range boundaries [near, coupling, leaf, total,
+// total].
+extern "C" int h2b_plan_trace(h2b_plan* p, unsigned long long* h_out, int64_t cap) {
+    if (!p || !h_out) return fail(H2B_ERR_INVALID, "h2b_plan_trace: null pointer");
+    if (!p->trace) return fail(H2B_ERR_INVALID, "h2b_plan_trace: plan created without H2B_TRACE=1");
+    const int64_t n = (int64_t)(p->L.c_leaves + p->n_near + p->n_cpl);
+    if (cap < 8 * n + 5) return fail(H2B_ERR_CAPACITY, "h2b_plan_trace: buffer too small");
+    H2B_CUDA_TRY(cudaMemcpy(h_out, p->trace, sizeof(unsigned long long) * 8 * n, cudaMemcpyDeviceToHost));
+    h_out[8 * n] = p->L.c_leaves;
+    h_out[8 * n + 1] = p->L.c_leaves + p->n_near;
+    h_out[8 * n + 2] = n;
+    h_out[8 * n + 3] = n;
+    h_out[8 * n + 4] = n;
     return ok();
 }
 

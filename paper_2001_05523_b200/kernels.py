@@ -122,25 +122,31 @@ class SingularTable:
     """Sauter-Schwab integrals of every touching pair at order q, on the device
     (reference: kernels.SingularTable, kernels.py:346-362)."""
 
-    def __init__(self, dmesh, kind, q):
-        L = _lib.lib()
+    def __init__(self, dmesh, kind, q, compute=True):
         self.kind = kind
         self.q = q
+        self.dmesh = dmesh
         self.touch = dmesh.touch()
         n = self.touch.n_pairs
         width = 3 if kind == DLP else 1
         self.values_dev = D.zeros((max(n, 1) * width,))
-        rules = (_lib.Rule * 3)()
+        self.rules = (_lib.Rule * 3)()
         self._keep = []
         for i, case in enumerate((quad.IDENTICAL, quad.SHARED_EDGE, quad.SHARED_VERTEX)):
             r = quad.sauter_schwab_rule(case, q)
             p, w = D.dev(r.points), D.dev(r.weights)
             self._keep += [p, w]
-            rules[i] = _lib.Rule(len(r.weights), p.data_ptr(), w.data_ptr())
-        _lib.check(L.h2b_singular(ctypes.byref(dmesh.c), ctypes.byref(self.touch.c), kind_code(kind), rules,
-                                  self.values_dev.data_ptr(), D.stream()))
+            self.rules[i] = _lib.Rule(len(r.weights), p.data_ptr(), w.data_ptr())
         self.n = dmesh.mesh.n_triangles
         self._keys = None
+        if compute:
+            self.compute()
+
+    def compute(self):
+        """(Re)evaluate every touching pair on the device (stream-ordered)."""
+        _lib.check(_lib.lib().h2b_singular(ctypes.byref(self.dmesh.c), ctypes.byref(self.touch.c),
+                                           kind_code(self.kind), self.rules, self.values_dev.data_ptr(),
+                                           D.stream()))
 
     @property
     def keys(self):
@@ -178,20 +184,35 @@ def tile_jobs(jobs):
     return np.array(out, dtype=np.int64).reshape(-1, 6)
 
 
+class SlpJobs:
+    """SLP pair-block jobs resident on the device (tiled to TILE x TILE)."""
+
+    def __init__(self, dmesh, q, jobs, row_idx, col_idx):
+        self.dmesh = dmesh
+        self.q = q
+        self.jobs = tile_jobs(jobs)
+        self.n = len(self.jobs)
+        self.pairs = int((self.jobs[:, 1] * self.jobs[:, 3]).sum()) if self.n else 0
+        if self.n == 0:
+            return
+        self.pp, self.Q, _ = dmesh.panel_points(q)
+        self.dj = D.dev(self.jobs, np.int64)
+        self.ri = row_idx if not isinstance(row_idx, np.ndarray) else D.dev(row_idx, np.int32)
+        self.ci = col_idx if not isinstance(col_idx, np.ndarray) else D.dev(col_idx, np.int32)
+        self.c = _lib.Jobs(self.n, self.dj.data_ptr(), self.ri.data_ptr(), self.ci.data_ptr())
+
+    def run(self, table, out):
+        if self.n == 0:
+            return
+        tptr = ctypes.byref(table.touch.c) if table is not None else None
+        tv = table.values_dev.data_ptr() if table is not None else None
+        _lib.check(_lib.lib().h2b_pair_blocks_slp(ctypes.byref(self.dmesh.c), self.pp.data_ptr(), self.Q,
+                                                  ctypes.byref(self.c), tptr, tv, out.data_ptr(), D.stream()))
+
+
 def run_slp_jobs(dmesh, q, jobs, row_idx, col_idx, table, out):
     """Device SLP pair blocks into `out` (device float64)."""
-    jobs = tile_jobs(jobs)
-    if len(jobs) == 0:
-        return
-    pp, Q, _ = dmesh.panel_points(q)
-    dj = D.dev(jobs, np.int64)
-    ri = row_idx if not isinstance(row_idx, np.ndarray) else D.dev(row_idx, np.int32)
-    ci = col_idx if not isinstance(col_idx, np.ndarray) else D.dev(col_idx, np.int32)
-    cj = _lib.Jobs(len(jobs), dj.data_ptr(), ri.data_ptr(), ci.data_ptr())
-    tptr = ctypes.byref(table.touch.c) if table is not None else None
-    tv = table.values_dev.data_ptr() if table is not None else None
-    _lib.check(_lib.lib().h2b_pair_blocks_slp(ctypes.byref(dmesh.c), pp.data_ptr(), Q, ctypes.byref(cj), tptr, tv,
-                                              out.data_ptr(), D.stream()))
+    SlpJobs(dmesh, q, jobs, row_idx, col_idx).run(table, out)
 
 
 def build_dlp_jobs(mesh, blocks):

@@ -1,0 +1,100 @@
+// HBM streaming microbenchmark for the matvec design: a CTA streams one or
+// more contiguous chunks and reduces them (dot with a vector in smem).
+//   mode 0: TMA bulk copy, nst stages of `chunk` bytes, loop over chunks
+//   mode 1: LDG.256 direct, 4 independent loads per lane per iteration
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t su(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__global__ void k_tma(const double* __restrict__ A, size_t n, int chunk, int per_cta, int nst, double* out) {
+    extern __shared__ __align__(128) char sm[];
+    uint64_t* bar = (uint64_t*)sm;
+    char* st = sm + 128;
+    const int nd = chunk / 8;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < nst; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su(bar + i)));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    __syncthreads();
+    const size_t c0 = (size_t)blockIdx.x * per_cta;
+    const size_t nchunks = n / nd;
+    double acc = 0;
+    auto issue = [&](int j) {
+        size_t c = c0 + j;
+        if (threadIdx.x == 0 && c < nchunks) {
+            int slot = j % nst;
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su(bar + slot)), "r"(chunk));
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(su(st + (size_t)slot * chunk)), "l"(A + c * nd), "r"(chunk), "r"(su(bar + slot)) : "memory");
+        }
+    };
+    for (int j = 0; j < nst - 1 && j < per_cta; ++j) issue(j);
+    for (int j = 0; j < per_cta; ++j) {
+        if (c0 + j >= nchunks) break;
+        if (j + nst - 1 < per_cta) issue(j + nst - 1);
+        int slot = j % nst;
+        uint32_t par = (j / nst) & 1;
+        asm volatile("{ .reg .pred p; W_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra W_%=; }" ::"r"(su(bar + slot)), "r"(par));
+        const double* d = (const double*)(st + (size_t)slot * chunk);
+        for (int i = threadIdx.x; i < nd; i += blockDim.x) acc += d[i];
+        __syncthreads();
+    }
+    if (acc == 12345.0) out[0] = acc;
+}
+
+struct d4 { double x, y, z, w; };
+__device__ __forceinline__ d4 ld4(const double* p) {
+    d4 r; asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w) : "l"(p)); return r;
+}
+__global__ void k_ldg(const double* __restrict__ A, size_t n, size_t per_cta, double* out) {
+    const size_t b0 = (size_t)blockIdx.x * per_cta, b1 = min(n, b0 + per_cta);
+    double acc = 0;
+    size_t i = b0 + 4 * threadIdx.x;
+    const size_t stride = 4 * blockDim.x;
+    for (; i + 3 * stride < b1; i += 4 * stride) {
+        d4 a = ld4(A + i), b = ld4(A + i + stride), c = ld4(A + i + 2 * stride), d = ld4(A + i + 3 * stride);
+        acc += a.x + a.y + a.z + a.w + b.x + b.y + b.z + b.w + c.x + c.y + c.z + c.w + d.x + d.y + d.z + d.w;
+    }
+    for (; i < b1; i += stride) { d4 a = ld4(A + i); acc += a.x + a.y + a.z + a.w; }
+    if (acc == 12345.0) out[0] = acc;
+}
+
+int main() {
+    const size_t bytes = 112ull << 20;
+    const size_t n = bytes / 8;
+    double *A, *out, *fl;
+    cudaMalloc(&A, bytes); cudaMemset(A, 0, bytes);
+    cudaMalloc(&out, 8);
+    cudaMalloc(&fl, 256 << 20);
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    auto run = [&](const char* name, auto launch) {
+        float best = 1e9;
+        for (int r = 0; r < 5; ++r) {
+            cudaMemset(fl, r, 256 << 20);
+            cudaEventRecord(e0); launch(); cudaEventRecord(e1); cudaEventSynchronize(e1);
+            float ms; cudaEventElapsedTime(&ms, e0, e1); best = fminf(best, ms);
+        }
+        printf("%-40s %8.2f us %8.1f GB/s  err=%s\n", name, best * 1e3, bytes / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+    };
+    for (int chunk : {16384, 24576, 32768, 49152}) {
+        for (int nst : {1, 2, 3, 4}) {
+            for (int per : {1, 4, 16}) {
+                int smem = 128 + nst * chunk;
+                if (smem > 220 * 1024) continue;
+                cudaFuncSetAttribute(k_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                size_t nch = n / (chunk / 8);
+                int grid = (int)((nch + per - 1) / per);
+                char nm[128]; snprintf(nm, 128, "tma chunk=%dK stages=%d per_cta=%d", chunk / 1024, nst, per);
+                run(nm, [&] { k_tma<<<grid, 256, smem>>>(A, n, chunk, per, nst, out); });
+            }
+        }
+    }
+    for (size_t per : {4096ul, 16384ul, 65536ul}) {
+        char nm[128]; snprintf(nm, 128, "ldg256 per_cta=%zu doubles", per);
+        int grid = (int)((n + per - 1) / per);
+        run(nm, [&] { k_ldg<<<grid, 256>>>(A, n, per, out); });
+    }
+    return 0;
+}
