@@ -20,14 +20,11 @@ import numpy as np
 from . import _lib
 
 
-def leaf_costs(H):
-    """Bytes streamed by k_backward per row leaf (nearfield + V + couplings of
-    the leaf itself); internal coupling work is charged to its first leaf."""
-    rt = H.row_tree
-    nl, fl = H.near_layout, H.far_layout
+def leaf_costs(rt, near_C, far_K, ranks):
+    """Bytes streamed per row leaf (nearfield rows + leaf basis + the leaf's
+    couplings); an inner cluster's coupling work is charged to its first leaf."""
     size = rt.end - rt.start
-    ranks = np.array([H.row_basis.rank[u] for u in range(rt.n_nodes)], dtype=np.int64)
-    cost = size * nl.C + size * ranks + ranks * fl.K
+    cost = size * near_C + size * ranks + ranks * far_K
     leaves = rt.leaf_uids()
     order = leaves[np.argsort(rt.start[leaves], kind="stable")]
     # charge each internal node's coupling to the leaf at its start
@@ -40,10 +37,11 @@ def leaf_costs(H):
     return order, np.array([lc[int(u)] for u in order])
 
 
-def partition_rows(H, world):
-    """Contiguous permuted row ranges [(lo, hi)] per rank, balanced by cost."""
-    rt = H.row_tree
-    order, cost = leaf_costs(H)
+def partition_rows(rt, near_C, far_K, ranks, world):
+    """Contiguous permuted row ranges [(lo, hi)] per rank, balanced by cost
+    (rt: row ClusterTree; near_C / far_K: per-node nearfield / coupling
+    matrix widths; ranks: per-node row-basis ranks)."""
+    order, cost = leaf_costs(rt, near_C, far_K, ranks)
     cum = np.cumsum(cost)
     total = cum[-1]
     bounds = [0]
@@ -66,6 +64,21 @@ def owned_nodes(tree, lo, hi):
     """Row clusters whose range intersects [lo, hi), parents first (by depth)."""
     hit = np.flatnonzero((tree.start < hi) & (tree.end > lo))
     return hit[np.argsort(tree.depth_of[hit], kind="stable")]
+
+
+def gather_layout(ranges, n):
+    """Equal-size all-gather chunks: (chunk, pad_index) with pad_index[p] the
+    position of permuted dof p in the gathered buffer of world * chunk."""
+    chunk = max(max(h - l for l, h in ranges), 1)
+    pad_index = np.empty(n, dtype=np.int64)
+    for r, (a, b) in enumerate(ranges):
+        pad_index[a:b] = r * chunk + np.arange(b - a)
+    return chunk, pad_index
+
+
+def operator_partition(H, world):
+    ranks = np.array([H.row_basis.rank[u] for u in range(H.row_tree.n_nodes)], dtype=np.int64)
+    return partition_rows(H.row_tree, H.near_layout.C, H.far_layout.K, ranks, world)
 
 
 class LocalMatvec:
@@ -94,14 +107,11 @@ class ShardedMatvec:
             raise ValueError("row sharding with the x all-gather needs a square operator")
         self.H, self.rank, self.world, self.dist = H, rank, world, dist
         rt = H.row_tree
-        self.ranges = partition_rows(H, world)
+        self.ranges = operator_partition(H, world)
         lo, hi = self.ranges[rank]
         self.lo, self.hi = lo, hi
-        self.chunk = max(h - l for l, h in self.ranges)
         # padded gather layout: permuted position p of rank r -> r*chunk + (p - lo_r)
-        pad_index = np.empty(rt.n_dofs, dtype=np.int64)
-        for r, (a, b) in enumerate(self.ranges):
-            pad_index[a:b] = r * self.chunk + np.arange(b - a)
+        self.chunk, pad_index = gather_layout(self.ranges, rt.n_dofs)
         row_local = np.arange(rt.n_dofs, dtype=np.int64) - lo  # only owned rows are written
         owned = owned_nodes(rt, lo, hi)
         self.plan = MatvecPlan(H.block_tree, H.row_basis, H.col_basis, H.S_dev, H.D_dev, H.far_layout,

@@ -128,3 +128,40 @@ def test_cfg1_end_to_end_vs_reference():
     for i in range(2):
         assert rel(H.matvec(g[f"x{i}"]), g[f"y{i}"]) < 1e-10
     assert rel(H.diagonal(), g["diag"]) < 1e-10
+
+
+class _FakeGather:
+    """Stands in for torch.distributed in a single process: the all-gather of
+    x returns every rank's padded permuted slice, computed from the full x."""
+
+    def __init__(self, full):
+        self.full = full
+
+    def all_gather_into_tensor(self, buf, loc):
+        buf.copy_(self.full)
+
+
+def test_row_sharded_plans_reproduce_single_gpu_bitwise(cfg0):
+    """Rank r's plan (owned clusters only, padded all-gather layout, local
+    row indices) evaluated for r = 0..W-1 on one GPU: the assembled rows equal
+    the single-GPU matvec bit for bit."""
+    import torch
+
+    from paper_2001_05523_b200 import distributed as DD
+
+    g, m, t0, bt, b, H = cfg0
+    n = H.shape[0]
+    x = torch.from_numpy(np.random.default_rng(5).uniform(-1, 1, n)).cuda()
+    y_ref = H.matvec(x)
+    for world in (2, 3):
+        ranges = DD.operator_partition(H, world)
+        chunk, pad = DD.gather_layout(ranges, n)
+        xp = x[torch.from_numpy(t0.perm).cuda()]
+        full = torch.zeros(world * chunk, dtype=torch.float64, device="cuda")
+        full[torch.from_numpy(pad).cuda()] = xp
+        y = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
+        for r in range(world):
+            op = DD.ShardedMatvec(H, r, world, _FakeGather(full))
+            op.apply(x, y)
+        assert not torch.isnan(y).any()
+        assert torch.equal(y, y_ref), world

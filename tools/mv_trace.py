@@ -46,8 +46,8 @@ b = buf[8 * tot : 8 * tot + 5].astype(np.int64)
 tr = buf[: 8 * tot].reshape(tot, 8).astype(np.int64)
 t0 = tr[:, 0].min()
 st, en, sm = (tr[:, 0] - t0) / 1e3, (tr[:, 1] - t0) / 1e3, tr[:, 2]
-names = ["forward", "near", "coupling", "-"]
-bounds = [0, int(b[0]), int(b[1]), int(b[2]), tot]
+names = ["forward", "bands", "-", "-"]
+bounds = [0, int(b[0]), tot, tot, tot]
 print(f"matvec span {en.max():.1f} us, CTAs {tot}")
 for i, nm in enumerate(names):
     a, z = bounds[i], bounds[i + 1]
@@ -72,3 +72,12 @@ for i, nm in enumerate(names):
         rel = (m[ok] - tr[a:z, 0][ok, None]) / 1e3
         rel[m[ok] == 0] = np.nan
         print(nm, "marks (us from start):", np.round(np.nanmean(np.where(np.isnan(rel), np.nan, rel), axis=0), 2).tolist())
+
+# concurrency / throughput timeline of band CTAs
+a, z = bounds[1], tot
+edges = np.arange(0, en.max() + 5, 5.0)
+for lo in edges[:-1]:
+    hi = lo + 5
+    act = ((st[a:z] < hi) & (en[a:z] > lo)).sum()
+    fin = ((en[a:z] >= lo) & (en[a:z] < hi)).sum()
+    print(f"[{lo:5.0f},{hi:5.0f}) bands active {act:4d} finished {fin:4d}")
