@@ -69,6 +69,17 @@ def build(force=False, verbose=False):
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
+    # measurement probes used by bench.py (FP64 peak) and tools/
+    tools = os.path.join(ROOT, "tools")
+    tbin = os.path.join(tools, "_bin")
+    os.makedirs(tbin, exist_ok=True)
+    for name in ("fp64_probe", "stream_probe"):
+        src = os.path.join(tools, name + ".cu")
+        exe = os.path.join(tbin, name)
+        if os.path.exists(src) and (force or _stale(exe, [src])):
+            res = subprocess.run([cc, "-O3", "-std=c++17", "-o", exe, src] + ARCH, capture_output=True, text=True)
+            if res.returncode != 0:
+                raise RuntimeError(f"nvcc failed for {name}:\n{res.stdout}\n{res.stderr}")
     if verbose:
         for src, text in logs:
             print(f"== {src}\n{text}")
