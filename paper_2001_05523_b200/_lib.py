@@ -99,12 +99,13 @@ def lib():
     """The loaded libh2b.so; raises if it has not been built."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
+        path = os.environ.get("H2B_LIB_PATH", LIB_PATH)  # tuning experiments only
+        if not os.path.exists(path):
             raise RuntimeError(
-                f"libh2b.so not found at {LIB_PATH}: build it with "
+                f"libh2b.so not found at {path}: build it with "
                 "`python -m paper_2001_05523_b200.build` (no CPU fallback exists)"
             )
-        L = ctypes.CDLL(LIB_PATH)
+        L = ctypes.CDLL(path)
         for name in EXPORTS:
             getattr(L, name).restype = ctypes.c_int
         L.h2b_last_error.argtypes = [ctypes.c_char_p, ctypes.c_size_t]

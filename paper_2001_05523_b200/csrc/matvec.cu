@@ -52,11 +52,20 @@
 namespace h2b {
 namespace {
 
+// rarely-run and multiply-used paths stay out of line: the kernel's hot
+// instruction footprint must fit the SM instruction caches
+#ifndef H2B_NOINL
+#define H2B_NOINL __forceinline__
+#endif
+
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxVec = 512;        // max rank / leaf size of the vectors kept in smem
 constexpr int kMaxDepth = 64;
-constexpr int kStageBytes = 32768;  // TMA staging buffer per CTA (one band)
+#ifndef H2B_STAGE_KB
+#define H2B_STAGE_KB 32
+#endif
+constexpr int kStageBytes = H2B_STAGE_KB * 1024;  // TMA staging buffer per CTA (one band)
 
 // record layouts (int64 words)
 constexpr int kBandWords = 24;  // src_off, cols, rows, gidx_off, out_off, is_last, has_cpl, kind, then the
@@ -187,22 +196,26 @@ __device__ __forceinline__ void mark(unsigned long long* m, int i) {
 // dense building blocks (operands in shared memory unless noted)
 
 // out[i] = M[i*ld : i*ld+cols] . v, i < rows.  Few rows: one row per warp
-// (two partial sums per lane); many rows: each warp owns 4 rows at a time
+// (four partial sums per lane); many rows: each warp owns 4 rows at a time
 // (4 independent dot products, interleaved shuffle reductions).
-__device__ __forceinline__ void rows_dot(const double* M, int64_t ld, int rows, int cols, const double* v,
+__device__ H2B_NOINL void rows_dot(const double* M, int64_t ld, int rows, int cols, const double* v,
                                          double* out) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (rows < 4 * kWarps) {
         for (int r = warp; r < rows; r += kWarps) {
             const double* row = M + (int64_t)r * ld;
-            double a0 = 0.0, a1 = 0.0;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
             int c = lane;
-            for (; c + 32 < cols; c += 64) {
-                a0 = fma(row[c], v[c], a0);
-                a1 = fma(row[c + 32], v[c + 32], a1);
+            for (; c + 96 < cols; c += 128) {
+                const double m0 = row[c], m1 = row[c + 32], m2 = row[c + 64], m3 = row[c + 96];
+                const double v0 = v[c], v1 = v[c + 32], v2 = v[c + 64], v3 = v[c + 96];
+                a0 = fma(m0, v0, a0);
+                a1 = fma(m1, v1, a1);
+                a2 = fma(m2, v2, a2);
+                a3 = fma(m3, v3, a3);
             }
-            if (c < cols) a0 = fma(row[c], v[c], a0);
-            double sum = a0 + a1;
+            for (; c < cols; c += 32) a0 = fma(row[c], v[c], a0);
+            double sum = (a0 + a1) + (a2 + a3);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
             if (lane == 0) out[r] = sum;
@@ -234,7 +247,7 @@ __device__ __forceinline__ void rows_dot(const double* M, int64_t ld, int rows, 
 
 // out[c] = sum_r M[r*k + c] v[r], c < k: warps split rows, lanes columns,
 // partials reduced through `red` (kWarps x 32).  Ends with __syncthreads().
-__device__ void cols_dot(const double* M, int rows, int k, const double* v, double* red, double* out) {
+__device__ H2B_NOINL void cols_dot(const double* M, int rows, int k, const double* v, double* red, double* out) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int c0 = 0; c0 < k; c0 += 32) {
         const int c = c0 + lane;
@@ -295,6 +308,8 @@ struct Shared {
     double* vb;                // kMaxVec
     double* red;               // kWarps * 32
     int64_t* rec;              // small record cache
+    uint32_t parity;           // mbarrier phase of the staging slot in use
+    bool issued;               // band bulk copy already issued by the caller
 };
 
 // Thread 0 starts staging `bytes` (TMA bulk copy when it fits and is 16-byte
@@ -313,7 +328,25 @@ __device__ __forceinline__ const double* stage_issue(const Shared& s, const doub
     return fits ? reinterpret_cast<const double*>(s.stage) : src;
 }
 
-__device__ void prefetch_slice(const double* base, int64_t bytes, int part, int parts) {
+__device__ __forceinline__ bool band_staged(int64_t bytes, const double* src) {
+    return bytes > 0 && bytes <= kStageBytes && (reinterpret_cast<uintptr_t>(src) & 15) == 0 && (bytes & 15) == 0;
+}
+
+// Thread 0 starts the TMA bulk copy of the band described by `rec` into
+// `stage` (a plain arrive when the band is empty or read from global memory).
+__device__ __forceinline__ void issue_band(const h2b_layout& L, const int64_t* rec, char* stage, uint64_t* bar) {
+    if (threadIdx.x != 0) return;
+    const int64_t bytes = rec[2] * rec[1] * 8;
+    const double* src = (rec[7] ? L.S : L.D) + rec[0];
+    if (band_staged(bytes, src)) {
+        mbar_expect_tx(bar, (uint32_t)bytes);
+        bulk_g2s(stage, src, (uint32_t)bytes, bar);
+    } else {
+        mbar_arrive(bar);
+    }
+}
+
+__device__ H2B_NOINL void prefetch_slice(const double* base, int64_t bytes, int part, int parts) {
     if (!base || bytes <= 0) return;
     const int64_t lines = (bytes + 127) / 128;
     const int64_t per = (lines + parts - 1) / parts;
@@ -331,7 +364,8 @@ __device__ __forceinline__ void load_rec(const Shared& s, const int64_t* src, in
 // ---------------------------------------------------------------------------
 // A: forward transform of one column leaf; climb while the right child
 
-__device__ void task_forward(const h2b_layout& L, const int64_t* rec, const double* __restrict__ x,
+__device__ H2B_NOINL void task_forward(const double* __restrict__ c_V, const double* __restrict__ c_E,
+                                       const int64_t* __restrict__ col_perm, const int64_t* rec, const double* __restrict__ x,
                              uint64_t* xhat, uint32_t epoch, const Shared& s) {
     // header + climb levels in one load
     const int n_climb_max = kMaxDepth;
@@ -346,9 +380,9 @@ __device__ void task_forward(const h2b_layout& L, const int64_t* rec, const doub
     const int start = (int)s.rec[0], size = (int)s.rec[1], k = (int)s.rec[2];
     const int64_t v_off = s.rec[3], xhat_off = s.rec[4];
     const int n_climb = (int)s.rec[5];
-    const double* V = stage_issue(s, L.c_V + v_off, ((int64_t)size * k * 8 + 15) & ~int64_t(15));
-    for (int r = threadIdx.x; r < size; r += blockDim.x) s.va[r] = __ldg(x + L.col_perm[start + r]);
-    mbar_wait(s.bar, 0);
+    const double* V = stage_issue(s, c_V + v_off, ((int64_t)size * k * 8 + 15) & ~int64_t(15));
+    for (int r = threadIdx.x; r < size; r += blockDim.x) s.va[r] = __ldg(x + col_perm[start + r]);
+    mbar_wait(s.bar, s.parity);
     __syncthreads();
     cols_dot(V, size, k, s.va, s.red, s.vb);  // own coefficients stay in s.vb
     {
@@ -364,8 +398,8 @@ __device__ void task_forward(const h2b_layout& L, const int64_t* rec, const doub
         const bool in_smem = (n0 + n1) * 8 <= kStageBytes;
         __syncthreads();  // previous users of buf / va are done
         if (in_smem) {
-            const double* E0 = L.c_E + lv[2];
-            const double* E1 = L.c_E + lv[3];
+            const double* E0 = c_E + lv[2];
+            const double* E1 = c_E + lv[3];
             for (int i = threadIdx.x; i < n0; i += kThreads) cp_async8(buf + i, E0 + i);
             for (int i = threadIdx.x; i < n1; i += kThreads) cp_async8(buf + n0 + i, E1 + i);
         }
@@ -378,10 +412,10 @@ __device__ void task_forward(const h2b_layout& L, const int64_t* rec, const doub
         if (in_smem) {
             cols_dot(buf, k0 + k1, kp, s.va, s.red, s.vb);
         } else {
-            cols_dot(L.c_E + lv[2], k0, kp, s.va, s.red, s.vb);
+            cols_dot(c_E + lv[2], k0, kp, s.va, s.red, s.vb);
             for (int c = threadIdx.x; c < kp; c += kThreads) s.rhs[c] = s.vb[c];
             __syncthreads();
-            cols_dot(L.c_E + lv[3], k1, kp, s.va + k0, s.red, s.vb);
+            cols_dot(c_E + lv[3], k1, kp, s.va + k0, s.red, s.vb);
             for (int c = threadIdx.x; c < kp; c += kThreads) s.vb[c] += s.rhs[c];
             __syncthreads();
         }
@@ -400,7 +434,8 @@ __device__ void task_forward(const h2b_layout& L, const int64_t* rec, const doub
 // (LL); a leaf expands y[row_perm] = y_near + V_t v_t (containers.py:268-269).
 // Every value waited for is produced by a smaller ticket: the other bands of
 // t, the parent's last band (parents are ticketed first) and the near bands.
-__device__ void descent(const h2b_layout& L, const int64_t* d, const uint64_t* ycpl, uint64_t* yfin,
+__device__ H2B_NOINL void descent(const double* __restrict__ r_E, const double* __restrict__ r_V,
+                                  const int64_t* __restrict__ row_perm, const int64_t* d, const uint64_t* ycpl, uint64_t* yfin,
                         const uint64_t* ynear, double* y, uint32_t epoch, bool has_cpl, const Shared& s) {
     const int k = (int)d[0], kp = (int)d[2];
     const int64_t par_off = d[1], e_off = d[3], yoff = d[4];
@@ -410,7 +445,7 @@ __device__ void descent(const h2b_layout& L, const int64_t* d, const uint64_t* y
     double* Es = reinterpret_cast<double*>(s.stage);
     const bool e_smem = par_off >= 0 && k * kp <= kStageBytes / 8;
     if (e_smem)
-        for (int i = threadIdx.x; i < k * kp; i += kThreads) cp_async8(Es + i, L.r_E + e_off + i);
+        for (int i = threadIdx.x; i < k * kp; i += kThreads) cp_async8(Es + i, r_E + e_off + i);
     const uint64_t* yc = ycpl + 2 * yoff;
     for (int i = threadIdx.x; i < k; i += kThreads) s.va[i] = has_cpl ? ll_load(yc + 2 * i, epoch) : 0.0;
     if (par_off >= 0) {
@@ -421,7 +456,7 @@ __device__ void descent(const h2b_layout& L, const int64_t* d, const uint64_t* y
     __syncthreads();
     mark(s.mark, 4);
     if (par_off >= 0 && k > 0) {
-        rows_dot(e_smem ? Es : L.r_E + e_off, kp, k, kp, s.rhs, s.vb);
+        rows_dot(e_smem ? Es : r_E + e_off, kp, k, kp, s.rhs, s.vb);
         __syncthreads();
         for (int i = threadIdx.x; i < k; i += kThreads) s.va[i] += s.vb[i];
         __syncthreads();
@@ -434,7 +469,7 @@ __device__ void descent(const h2b_layout& L, const int64_t* d, const uint64_t* y
     const int size = (int)d[8];
     const int nv = size * k;
     const bool v_smem = nv <= kStageBytes / 8;
-    const double* Vg = L.r_V + v_off;
+    const double* Vg = r_V + v_off;
     if (v_smem) {
         for (int i = threadIdx.x; i < nv; i += kThreads) cp_async8(Es + i, Vg + i);
         cp_async_wait_all();
@@ -444,7 +479,102 @@ __device__ void descent(const h2b_layout& L, const int64_t* d, const uint64_t* y
     __syncthreads();
     const uint64_t* yn = ynear + 2 * (int64_t)start;
     for (int i = threadIdx.x; i < size; i += blockDim.x)
-        y[L.row_perm[start + i]] = ll_load(yn + 2 * i, epoch) + (k > 0 ? s.vb[i] : 0.0);
+        y[row_perm[start + i]] = ll_load(yn + 2 * i, epoch) + (k > 0 ? s.vb[i] : 0.0);
+}
+
+#ifndef H2B_REGCOLS
+#define H2B_REGCOLS 0
+#endif
+constexpr int kRegCols = H2B_REGCOLS > 0 ? H2B_REGCOLS : 1;  // right-hand-side values held in registers per thread
+
+// Sum of 8 per-lane values over the warp with 9 shuffles (recursive halving):
+// returns the total of value index ri(lane) = 4*b4 + 2*b3 + b2 (bits of lane).
+__device__ __forceinline__ double warp_sum8(double (&a)[8], int lane) {
+    {
+        const bool up = lane & 16;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const double send = up ? a[i] : a[i + 4], keep = up ? a[i + 4] : a[i];
+            a[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        }
+    }
+    {
+        const bool up = lane & 8;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const double send = up ? a[i] : a[i + 2], keep = up ? a[i + 2] : a[i];
+            a[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
+    }
+    {
+        const bool up = lane & 4;
+        const double send = up ? a[0] : a[1], keep = up ? a[1] : a[0];
+        a[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    double v = a[0];
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    return v;
+}
+
+// One band, right-hand side gathered straight into registers (thread t owns
+// columns t, t + 256, ...; cols <= kRegCols * kThreads): out = M v with M
+// (rows x cols, row major) staged by the bulk copy on s.bar.  Each thread
+// reads every staged element once, the shared memory carries no vector
+// traffic, and rows are reduced 8 at a time (shuffle halving, then across
+// warps through s.red), stored in LL form.
+template <bool kLL>
+__device__ __forceinline__ void band_dot(const double* M, int rows, int cols, const double* __restrict__ x,
+                                         const uint64_t* ll, const int32_t* __restrict__ gidx, uint32_t epoch,
+                                         uint64_t* dst, const Shared& s) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    double v[kRegCols];
+    {
+        int ix[kRegCols];
+#pragma unroll
+        for (int j = 0; j < kRegCols; ++j) {
+            const int c = tid + j * kThreads;
+            ix[j] = c < cols ? __ldg(gidx + c) : -1;
+        }
+#pragma unroll
+        for (int j = 0; j < kRegCols; ++j) {
+            if (kLL)
+                v[j] = ix[j] >= 0 ? ll_load(ll + 2 * (int64_t)ix[j], epoch) : 0.0;
+            else
+                v[j] = ix[j] >= 0 ? __ldg(x + ix[j]) : 0.0;
+        }
+    }
+    mark(s.mark, 1);
+    mbar_wait(s.bar, s.parity);
+    mark(s.mark, 2);
+    const int ri = ((lane >> 2) & 4) | ((lane >> 2) & 2) | ((lane >> 2) & 1);
+    for (int r32 = 0; r32 < rows; r32 += 32) {
+        const int n32 = min(32, rows - r32);
+        for (int r8 = 0; r8 < n32; r8 += 8) {
+            const int r0 = r32 + r8;
+            double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int j = 0; j < kRegCols; ++j) {
+                const int c = tid + j * kThreads;
+                if (j * kThreads < cols && c < cols) {
+                    const double* m = M + (int64_t)r0 * cols + c;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        if (r0 + i < rows) acc[i] = fma(m[(int64_t)i * cols], v[j], acc[i]);
+                }
+            }
+            const double sum = warp_sum8(acc, lane);
+            if ((lane & 3) == 0) s.red[warp * 32 + r8 + ri] = sum;
+        }
+        __syncthreads();
+        if (tid < n32) {
+            double t = 0.0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) t += s.red[w * 32 + tid];
+            ll_store(dst + 2 * (r32 + tid), t, epoch);
+        }
+        __syncthreads();
+    }
 }
 
 // The band record is already in s.rec (kind in word 7: 0 near, 1 coupling).
@@ -456,14 +586,22 @@ __device__ void task_band(const h2b_layout& L, const double* __restrict__ x, con
     const int cols = (int)s.rec[1], rows = (int)s.rec[2];
     if (rows > 0) {
         const double* base = kCoupling ? L.S : L.D;
-        const double* M = stage_issue(s, base + src_off, (int64_t)rows * cols * 8);
+        const int64_t bytes = (int64_t)rows * cols * 8;
+        const double* M = s.issued ? (band_staged(bytes, base + src_off) ? reinterpret_cast<const double*>(s.stage)
+                                                                         : base + src_off)
+                                   : stage_issue(s, base + src_off, bytes);
         mark(s.mark, 0);
+        if (H2B_REGCOLS > 0 && cols <= kRegCols * kThreads) {
+            band_dot<kCoupling>(M, rows, cols, x, xhat, kCoupling ? L.s_gidx + gi_off : L.d_gidx + gi_off, epoch,
+                                out + 2 * out_off, s);
+            mark(s.mark, 3);
+        } else {
         if (kCoupling)
             gather_ll(s.rhs, xhat, L.s_gidx + gi_off, cols, epoch);
         else
             gather(s.rhs, x, L.d_gidx + gi_off, cols);
         mark(s.mark, 1);
-        mbar_wait(s.bar, 0);
+        mbar_wait(s.bar, s.parity);
         __syncthreads();
         mark(s.mark, 2);
         rows_dot(M, cols, rows, cols, s.rhs, s.va);
@@ -471,10 +609,13 @@ __device__ void task_band(const h2b_layout& L, const double* __restrict__ x, con
         mark(s.mark, 3);
         uint64_t* dst = out + 2 * out_off;
         for (int i = threadIdx.x; i < rows; i += blockDim.x) ll_store(dst + 2 * i, s.va[i], epoch);
+        }
+    } else if (s.issued) {
+        mbar_wait(s.bar, s.parity);  // the plain arrive of an empty band
     }
     if (kCoupling && s.rec[5]) {
         __syncthreads();
-        descent(L, s.rec + 8, ycpl, yfin, ynear, y, epoch, s.rec[6] != 0, s);
+        descent(L.r_E, L.r_V, L.row_perm, s.rec + 8, ycpl, yfin, ynear, y, epoch, s.rec[6] != 0, s);
     }
 }
 
@@ -491,7 +632,11 @@ struct KArgs {
     unsigned long long* trace;
 };
 
-__global__ void __launch_bounds__(kThreads, 4) k_matvec(const KArgs a, const double* __restrict__ x,
+#ifndef H2B_MINB
+#define H2B_MINB 4
+#endif
+
+__global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, const double* __restrict__ x,
                                                        double* __restrict__ y) {
     extern __shared__ __align__(128) char smraw[];
     __shared__ int s_ticket;
@@ -506,6 +651,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_matvec(const KArgs a, const dou
     s.vb = s.va + kMaxVec;
     s.red = s.vb + kMaxVec;
     s.rec = s_rec;
+    s.parity = 0;
+    s.issued = false;
     if (threadIdx.x == 0) {
         s_ticket = atomicAdd(a.ctrl, 1);
         s_epoch = (uint32_t)(*reinterpret_cast<volatile int*>(a.ctrl + 1)) + 1u;
@@ -526,7 +673,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_matvec(const KArgs a, const dou
         prefetch_slice(reinterpret_cast<const double*>(a.rec + a.band_base), a.band_bytes, ticket, L.c_leaves);
         prefetch_slice(reinterpret_cast<const double*>(L.d_gidx), a.dgidx_bytes, ticket, L.c_leaves);
         prefetch_slice(x, 8 * L.n_cols, ticket, L.c_leaves);
-        task_forward(L, a.rec + __ldg(a.fwd_off + ticket), x, a.xhat, epoch, s);
+        task_forward(L.c_V, L.c_E, L.col_perm, a.rec + __ldg(a.fwd_off + ticket), x, a.xhat, epoch, s);
     } else {
         const int b = ticket - tB;
         // the first bands pull the row-basis transfer matrices into L2
@@ -560,6 +707,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_matvec(const KArgs a, const dou
         }
     }
 }
+
 
 __global__ void k_diagonal(h2b_layout L, double* __restrict__ diag) {
     const int node = blockIdx.x * blockDim.x + threadIdx.x;

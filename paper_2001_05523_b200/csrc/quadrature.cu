@@ -16,6 +16,8 @@
 // reference's _dist2, kernels.py:75-85, without its cancellation because both
 // point sets are shifted to a block-local origin first).
 
+#include <cstdlib>
+
 #include <cub/device/device_scan.cuh>
 
 #include "device_common.cuh"
@@ -375,12 +377,12 @@ __device__ __forceinline__ int64_t touch_find(const int64_t* __restrict__ row_pt
     return -1;
 }
 
-// constant factor of the folded Newton step: with g = -r^2/2 and t ~ rsqrt(-g),
-// 1/(4 pi r) = t (3 + g t^2) / (8 sqrt(2) pi)
+// constant factor of the folded Newton step: with p = r^2/2 and t ~ rsqrt(p),
+// 1/(4 pi r) = t (3 - p t^2) / (8 sqrt(2) pi)
 constexpr double kSlpFold = 1.0 / (8.0 * 1.4142135623730950488016887 * kPi);
 
-template <int Q, int JC>
-__global__ void __launch_bounds__(256) k_blocks_slp(const double* __restrict__ P, int64_t F,
+template <int Q, int JC, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_blocks_slp(const double* __restrict__ P, int64_t F,
                                                    const int32_t* __restrict__ T,
                                                    const int64_t* __restrict__ jobs,
                                                    const int32_t* __restrict__ row_idx,
@@ -415,10 +417,10 @@ __global__ void __launch_bounds__(256) k_blocks_slp(const double* __restrict__ P
         const int64_t g = (int64_t)pnl * Q + i;
         const double x = P[g] - ox, y = P[FQ + g] - oy, z = P[2 * FQ + g] - oz;
         const int s = i * kTile + r;
-        rx[s] = x;
-        rx[Q * kTile + s] = y;
-        rx[2 * Q * kTile + s] = z;
-        rx[3 * Q * kTile + s] = -0.5 * fma(z, z, fma(y, y, x * x));
+        rx[s] = -x;  // negated: r^2/2 = |x'|^2/2 + |y'|^2/2 + (-x').y'
+        rx[Q * kTile + s] = -y;
+        rx[2 * Q * kTile + s] = -z;
+        rx[3 * Q * kTile + s] = 0.5 * fma(z, z, fma(y, y, x * x));
         rx[4 * Q * kTile + s] = P[3 * FQ + g];
         if (i == 0) {
             rp[r] = pnl;
@@ -436,7 +438,7 @@ __global__ void __launch_bounds__(256) k_blocks_slp(const double* __restrict__ P
         cx[s] = x;
         cx[Q * kTile + s] = y;
         cx[2 * Q * kTile + s] = z;
-        cx[3 * Q * kTile + s] = -0.5 * fma(z, z, fma(y, y, x * x));
+        cx[3 * Q * kTile + s] = 0.5 * fma(z, z, fma(y, y, x * x));
         cx[4 * Q * kTile + s] = P[3 * FQ + g] * kSlpFold;
         if (j == 0) {
             cp[c] = pnl;
@@ -472,28 +474,42 @@ __global__ void __launch_bounds__(256) k_blocks_slp(const double* __restrict__ P
                 double y0[JC], y1[JC], y2[JC], yh[JC], yw[JC];
 #pragma unroll
                 for (int j = 0; j < JC; ++j) {
-                    const int s = (j0 + j) * kTile + b;
-                    y0[j] = cx[s];
-                    y1[j] = cx[Q * kTile + s];
-                    y2[j] = cx[2 * Q * kTile + s];
-                    yh[j] = cx[3 * Q * kTile + s];
-                    yw[j] = cx[4 * Q * kTile + s];
+                    if (j0 + j < Q) {
+                        const int s = (j0 + j) * kTile + b;
+                        y0[j] = cx[s];
+                        y1[j] = cx[Q * kTile + s];
+                        y2[j] = cx[2 * Q * kTile + s];
+                        yh[j] = cx[3 * Q * kTile + s];
+                        yw[j] = cx[4 * Q * kTile + s];
+                    }
                 }
+                // two row points per step: two independent accumulation chains
 #pragma unroll
-                for (int i = 0; i < Q; ++i) {
-                    const int s = i * kTile + a;
-                    const double x0 = rx[s], x1 = rx[Q * kTile + s], x2 = rx[2 * Q * kTile + s];
-                    const double xh = rx[3 * Q * kTile + s], xw = rx[4 * Q * kTile + s];
-                    double acc = 0.0;
+                for (int i = 0; i < Q; i += 2) {
+                    const bool two = (i + 1 < Q);
+                    const int sa = i * kTile + a, sb = two ? sa + kTile : sa;
+                    const double a0 = rx[sa], a1 = rx[Q * kTile + sa], a2 = rx[2 * Q * kTile + sa];
+                    const double ah = rx[3 * Q * kTile + sa], aw = rx[4 * Q * kTile + sa];
+                    const double b0 = rx[sb], b1 = rx[Q * kTile + sb], b2 = rx[2 * Q * kTile + sb];
+                    const double bh = rx[3 * Q * kTile + sb], bw = rx[4 * Q * kTile + sb];
+                    double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
                     for (int j = 0; j < JC; ++j) {
-                        // g = x'.y' - |x'|^2/2 - |y'|^2/2 = -r^2/2
-                        const double g = fma(x0, y0[j], fma(x1, y1[j], fma(x2, y2[j], xh + yh[j])));
-                        const double t = rsqrt_seed(-g);
-                        const double c = fma(g, t * t, 3.0);
-                        acc = fma(yw[j] * t, c, acc);
+                        if (j0 + j < Q) {
+                            // p = |x'|^2/2 + |y'|^2/2 - x'.y' = r^2/2, t ~ rsqrt(p);
+                            // one Newton step folded: 1/r ~ t (3 - p t^2) / (2 sqrt 2)
+                            const double pa = fma(a0, y0[j], fma(a1, y1[j], fma(a2, y2[j], ah + yh[j])));
+                            const double ta = rsqrt_seed(pa);
+                            acc0 = fma(yw[j] * ta, fma(-pa, ta * ta, 3.0), acc0);
+                            if (two) {
+                                const double pb = fma(b0, y0[j], fma(b1, y1[j], fma(b2, y2[j], bh + yh[j])));
+                                const double tb = rsqrt_seed(pb);
+                                acc1 = fma(yw[j] * tb, fma(-pb, tb * tb, 3.0), acc1);
+                            }
+                        }
                     }
-                    tot = fma(xw, acc, tot);
+                    tot = fma(aw, acc0, tot);
+                    if (two) tot = fma(bw, acc1, tot);
                 }
             }
             val = tot;
@@ -701,11 +717,11 @@ int alloc_flags(int** d, cudaStream_t st) {
     return ok();
 }
 
-template <int Q, int JC>
+template <int Q, int JC, int MINB = 2>
 int launch_slp(const h2b_mesh* m, const double* P, const h2b_jobs* jobs, const h2b_touch* t,
                const double* tv, double* out, int* flags, cudaStream_t st) {
     const size_t sm = (size_t)10 * Q * kTile * sizeof(double) + (size_t)8 * kTile * sizeof(int);
-    auto kern = k_blocks_slp<Q, JC>;
+    auto kern = k_blocks_slp<Q, JC, MINB>;
     H2B_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     const int64_t nj = jobs->n_jobs;
     for (int64_t j0 = 0; j0 < nj; j0 += 2147483647LL) {
@@ -865,7 +881,7 @@ extern "C" int h2b_pair_blocks_slp(const h2b_mesh* m, const double* d_panel_poin
     switch (Q) {
         case 1: rc = launch_slp<1, 1>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
         case 4: rc = launch_slp<4, 4>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
-        case 9: rc = launch_slp<9, 9>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
+        case 9: rc = launch_slp<9, 9, 2>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
         case 16: rc = launch_slp<16, 8>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
         case 25: rc = launch_slp<25, 5>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
         default: rc = fail(H2B_ERR_INVALID, "h2b_pair_blocks_slp: supported regular orders q = 1..5");
