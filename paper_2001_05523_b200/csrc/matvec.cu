@@ -52,12 +52,6 @@
 namespace h2b {
 namespace {
 
-// rarely-run and multiply-used paths stay out of line: the kernel's hot
-// instruction footprint must fit the SM instruction caches
-#ifndef H2B_NOINL
-#define H2B_NOINL __forceinline__
-#endif
-
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxVec = 512;        // max rank / leaf size of the vectors kept in smem
@@ -73,7 +67,10 @@ constexpr int kBandWords = 24;  // src_off, cols, rows, gidx_off, out_off, is_la
                                 // k, parent y_hat offset (-1 root), k_parent, e_off, y_hat offset,
                                 // is_leaf, v_off, start (size = rows of a leaf)
 constexpr int kFwdHead = 6;     // start, size, k, v_off, xhat_off, n_climb
-constexpr int kFwdLevel = 6;    // k0, kp, e_off_c0, e_off_own, xhat_off_c0, xhat_off_parent
+constexpr int kFwdLevel = 6;
+constexpr int kKindNear = 0, kKindCpl = 1, kKindDescent = 3;  // band record kinds (word 7)
+constexpr int kSpecWin = 16;   // speculatively fetched band records per CTA
+constexpr int kSpecLead = 4;   // ... starting this many tickets before blockIdx.x    // k0, kp, e_off_c0, e_off_own, xhat_off_c0, xhat_off_parent
 
 }  // namespace
 }  // namespace h2b
@@ -85,7 +82,7 @@ struct h2b_plan {
     uint64_t* ycpl;     // LL: 2 x yhat_len (coupling part of y_hat)
     uint64_t* yfin;     // LL: 2 x yhat_len (final y_hat of inner clusters)
     uint64_t* ynear;    // LL: 2 x n_rows (permuted order)
-    int* ctrl;          // [0] ticket, [1] epoch, [2] done counter
+    unsigned long long* ctrl;  // ticket counter (monotonic over launches)
     int64_t* rec;       // task records
     int64_t* fwd_off;   // per column leaf: record offset
     int64_t band_base;  // record offset of band 0
@@ -147,19 +144,12 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
     asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
 }
 
-__device__ __forceinline__ int arrive_acq_rel(int* f) {
-    int old;
-    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(f) : "memory");
-    return old;
-}
 
 // ---- LL form: double -> (lo32 | epoch), (hi32 | epoch) ---------------------
 __device__ __forceinline__ void ll_store(uint64_t* p, double v, uint32_t epoch) {
@@ -198,7 +188,7 @@ __device__ __forceinline__ void mark(unsigned long long* m, int i) {
 // out[i] = M[i*ld : i*ld+cols] . v, i < rows.  Few rows: one row per warp
 // (four partial sums per lane); many rows: each warp owns 4 rows at a time
 // (4 independent dot products, interleaved shuffle reductions).
-__device__ H2B_NOINL void rows_dot(const double* M, int64_t ld, int rows, int cols, const double* v,
+__device__ void rows_dot(const double* M, int64_t ld, int rows, int cols, const double* v,
                                          double* out) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (rows < 4 * kWarps) {
@@ -247,7 +237,7 @@ __device__ H2B_NOINL void rows_dot(const double* M, int64_t ld, int rows, int co
 
 // out[c] = sum_r M[r*k + c] v[r], c < k: warps split rows, lanes columns,
 // partials reduced through `red` (kWarps x 32).  Ends with __syncthreads().
-__device__ H2B_NOINL void cols_dot(const double* M, int rows, int k, const double* v, double* red, double* out) {
+__device__ void cols_dot(const double* M, int rows, int k, const double* v, double* red, double* out) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int c0 = 0; c0 < k; c0 += 32) {
         const int c = c0 + lane;
@@ -346,7 +336,7 @@ __device__ __forceinline__ void issue_band(const h2b_layout& L, const int64_t* r
     }
 }
 
-__device__ H2B_NOINL void prefetch_slice(const double* base, int64_t bytes, int part, int parts) {
+__device__ void prefetch_slice(const double* base, int64_t bytes, int part, int parts) {
     if (!base || bytes <= 0) return;
     const int64_t lines = (bytes + 127) / 128;
     const int64_t per = (lines + parts - 1) / parts;
@@ -364,7 +354,7 @@ __device__ __forceinline__ void load_rec(const Shared& s, const int64_t* src, in
 // ---------------------------------------------------------------------------
 // A: forward transform of one column leaf; climb while the right child
 
-__device__ H2B_NOINL void task_forward(const double* __restrict__ c_V, const double* __restrict__ c_E,
+__device__ void task_forward(const double* __restrict__ c_V, const double* __restrict__ c_E,
                                        const int64_t* __restrict__ col_perm, const int64_t* rec, const double* __restrict__ x,
                              uint64_t* xhat, uint32_t epoch, const Shared& s) {
     // header + climb levels in one load
@@ -434,7 +424,7 @@ __device__ H2B_NOINL void task_forward(const double* __restrict__ c_V, const dou
 // (LL); a leaf expands y[row_perm] = y_near + V_t v_t (containers.py:268-269).
 // Every value waited for is produced by a smaller ticket: the other bands of
 // t, the parent's last band (parents are ticketed first) and the near bands.
-__device__ H2B_NOINL void descent(const double* __restrict__ r_E, const double* __restrict__ r_V,
+__device__ void descent(const double* __restrict__ r_E, const double* __restrict__ r_V,
                                   const int64_t* __restrict__ row_perm, const int64_t* d, const uint64_t* ycpl, uint64_t* yfin,
                         const uint64_t* ynear, double* y, uint32_t epoch, bool has_cpl, const Shared& s) {
     const int k = (int)d[0], kp = (int)d[2];
@@ -482,101 +472,6 @@ __device__ H2B_NOINL void descent(const double* __restrict__ r_E, const double* 
         y[row_perm[start + i]] = ll_load(yn + 2 * i, epoch) + (k > 0 ? s.vb[i] : 0.0);
 }
 
-#ifndef H2B_REGCOLS
-#define H2B_REGCOLS 0
-#endif
-constexpr int kRegCols = H2B_REGCOLS > 0 ? H2B_REGCOLS : 1;  // right-hand-side values held in registers per thread
-
-// Sum of 8 per-lane values over the warp with 9 shuffles (recursive halving):
-// returns the total of value index ri(lane) = 4*b4 + 2*b3 + b2 (bits of lane).
-__device__ __forceinline__ double warp_sum8(double (&a)[8], int lane) {
-    {
-        const bool up = lane & 16;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const double send = up ? a[i] : a[i + 4], keep = up ? a[i + 4] : a[i];
-            a[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-        }
-    }
-    {
-        const bool up = lane & 8;
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const double send = up ? a[i] : a[i + 2], keep = up ? a[i + 2] : a[i];
-            a[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-        }
-    }
-    {
-        const bool up = lane & 4;
-        const double send = up ? a[0] : a[1], keep = up ? a[1] : a[0];
-        a[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-    double v = a[0];
-    v += __shfl_xor_sync(0xffffffffu, v, 2);
-    v += __shfl_xor_sync(0xffffffffu, v, 1);
-    return v;
-}
-
-// One band, right-hand side gathered straight into registers (thread t owns
-// columns t, t + 256, ...; cols <= kRegCols * kThreads): out = M v with M
-// (rows x cols, row major) staged by the bulk copy on s.bar.  Each thread
-// reads every staged element once, the shared memory carries no vector
-// traffic, and rows are reduced 8 at a time (shuffle halving, then across
-// warps through s.red), stored in LL form.
-template <bool kLL>
-__device__ __forceinline__ void band_dot(const double* M, int rows, int cols, const double* __restrict__ x,
-                                         const uint64_t* ll, const int32_t* __restrict__ gidx, uint32_t epoch,
-                                         uint64_t* dst, const Shared& s) {
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    double v[kRegCols];
-    {
-        int ix[kRegCols];
-#pragma unroll
-        for (int j = 0; j < kRegCols; ++j) {
-            const int c = tid + j * kThreads;
-            ix[j] = c < cols ? __ldg(gidx + c) : -1;
-        }
-#pragma unroll
-        for (int j = 0; j < kRegCols; ++j) {
-            if (kLL)
-                v[j] = ix[j] >= 0 ? ll_load(ll + 2 * (int64_t)ix[j], epoch) : 0.0;
-            else
-                v[j] = ix[j] >= 0 ? __ldg(x + ix[j]) : 0.0;
-        }
-    }
-    mark(s.mark, 1);
-    mbar_wait(s.bar, s.parity);
-    mark(s.mark, 2);
-    const int ri = ((lane >> 2) & 4) | ((lane >> 2) & 2) | ((lane >> 2) & 1);
-    for (int r32 = 0; r32 < rows; r32 += 32) {
-        const int n32 = min(32, rows - r32);
-        for (int r8 = 0; r8 < n32; r8 += 8) {
-            const int r0 = r32 + r8;
-            double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-            for (int j = 0; j < kRegCols; ++j) {
-                const int c = tid + j * kThreads;
-                if (j * kThreads < cols && c < cols) {
-                    const double* m = M + (int64_t)r0 * cols + c;
-#pragma unroll
-                    for (int i = 0; i < 8; ++i)
-                        if (r0 + i < rows) acc[i] = fma(m[(int64_t)i * cols], v[j], acc[i]);
-                }
-            }
-            const double sum = warp_sum8(acc, lane);
-            if ((lane & 3) == 0) s.red[warp * 32 + r8 + ri] = sum;
-        }
-        __syncthreads();
-        if (tid < n32) {
-            double t = 0.0;
-#pragma unroll
-            for (int w = 0; w < kWarps; ++w) t += s.red[w * 32 + tid];
-            ll_store(dst + 2 * (r32 + tid), t, epoch);
-        }
-        __syncthreads();
-    }
-}
-
 // The band record is already in s.rec (kind in word 7: 0 near, 1 coupling).
 template <bool kCoupling>
 __device__ void task_band(const h2b_layout& L, const double* __restrict__ x, const uint64_t* xhat, uint64_t* out,
@@ -591,11 +486,6 @@ __device__ void task_band(const h2b_layout& L, const double* __restrict__ x, con
                                                                          : base + src_off)
                                    : stage_issue(s, base + src_off, bytes);
         mark(s.mark, 0);
-        if (H2B_REGCOLS > 0 && cols <= kRegCols * kThreads) {
-            band_dot<kCoupling>(M, rows, cols, x, xhat, kCoupling ? L.s_gidx + gi_off : L.d_gidx + gi_off, epoch,
-                                out + 2 * out_off, s);
-            mark(s.mark, 3);
-        } else {
         if (kCoupling)
             gather_ll(s.rhs, xhat, L.s_gidx + gi_off, cols, epoch);
         else
@@ -609,7 +499,6 @@ __device__ void task_band(const h2b_layout& L, const double* __restrict__ x, con
         mark(s.mark, 3);
         uint64_t* dst = out + 2 * out_off;
         for (int i = threadIdx.x; i < rows; i += blockDim.x) ll_store(dst + 2 * i, s.va[i], epoch);
-        }
     } else if (s.issued) {
         mbar_wait(s.bar, s.parity);  // the plain arrive of an empty band
     }
@@ -628,7 +517,7 @@ struct KArgs {
     int max_cols;
     int64_t e_bytes_r;
     uint64_t *xhat, *ycpl, *yfin, *ynear;
-    int* ctrl;
+    unsigned long long* ctrl;
     unsigned long long* trace;
 };
 
@@ -641,7 +530,8 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
     extern __shared__ __align__(128) char smraw[];
     __shared__ int s_ticket;
     __shared__ uint32_t s_epoch;
-    __shared__ int64_t s_rec[kFwdHead + kFwdLevel * kMaxDepth];
+    __shared__ int64_t s_rec[kSpecWin * kBandWords > kFwdHead + kFwdLevel * kMaxDepth ? kSpecWin * kBandWords
+                                                                                : kFwdHead + kFwdLevel * kMaxDepth];
     const h2b_layout& L = a.L;
     Shared s;
     s.bar = reinterpret_cast<uint64_t*>(smraw);
@@ -654,10 +544,22 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
     s.parity = 0;
     s.issued = false;
     if (threadIdx.x == 0) {
-        s_ticket = atomicAdd(a.ctrl, 1);
-        s_epoch = (uint32_t)(*reinterpret_cast<volatile int*>(a.ctrl + 1)) + 1u;
+        // tickets count on across launches: launch = t / grid (every CTA of a
+        // launch takes exactly one ticket before the next launch starts)
+        const unsigned long long t = atomicAdd(a.ctrl, 1ull);
+        s_ticket = (int)(t % gridDim.x);
+        s_epoch = (uint32_t)(t / gridDim.x) + 1u;
         mbar_init(s.bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // While the ticket is in flight, fetch the band records of the tickets
+    // near blockIdx.x (CTAs mostly take tickets in launch order): a hit saves
+    // the dependent record round trip.
+    const int spec0 = (int)blockIdx.x - kSpecLead;
+    for (int i = threadIdx.x; i < kSpecWin * kBandWords; i += kThreads) {
+        const int tk = spec0 + i / kBandWords;
+        if (tk >= L.c_leaves && tk < (int)gridDim.x)
+            s_rec[i] = __ldg(a.rec + a.band_base + (int64_t)kBandWords * (tk - L.c_leaves) + i % kBandWords);
     }
     __syncthreads();
     const int ticket = s_ticket;
@@ -679,12 +581,18 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
         // the first bands pull the row-basis transfer matrices into L2
         const int np = min(a.n_near + a.n_cpl, 512);
         if (b < np) prefetch_slice(L.r_E, a.e_bytes_r, b, np);
-        const int64_t* rec = a.rec + a.band_base + (int64_t)kBandWords * b;
-        load_rec(s, rec, kBandWords);
-        if (s.rec[7] == 0)
+        if (ticket >= spec0 && ticket < spec0 + kSpecWin) {
+            s.rec = s_rec + kBandWords * (ticket - spec0);
+        } else {
+            load_rec(s, a.rec + a.band_base + (int64_t)kBandWords * b, kBandWords);
+        }
+        const int kind = (int)s.rec[7];
+        if (kind == kKindNear)
             task_band<false>(L, x, a.xhat, a.ynear, a.yfin, a.ycpl, a.ynear, y, epoch, s);
-        else
+        else if (kind == kKindCpl)
             task_band<true>(L, x, a.xhat, a.ycpl, a.yfin, a.ycpl, a.ynear, y, epoch, s);
+        else
+            descent(L.r_E, L.r_V, L.row_perm, s.rec + 8, a.ycpl, a.yfin, a.ynear, y, epoch, s.rec[6] != 0, s);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -695,15 +603,10 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
             asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
             a.trace[8 * ticket] = t_begin;
             a.trace[8 * ticket + 1] = t_end;
-            a.trace[8 * ticket + 2] = smid;
-        }
-        // last CTA out resets the ticket counter and advances the epoch (every
-        // CTA has taken its ticket and read the epoch before it counts itself)
-        const int done = arrive_acq_rel(a.ctrl + 2);
-        if (done == (int)gridDim.x - 1) {
-            a.ctrl[0] = 0;
-            a.ctrl[2] = 0;
-            atomicAdd(a.ctrl + 1, 1);
+            const int kd = ticket < L.c_leaves ? 2 : (int)s.rec[7];
+            const bool hit = ticket >= spec0 && ticket < spec0 + kSpecWin;
+            a.trace[8 * ticket + 2] = smid | ((unsigned long long)kd << 16) | ((unsigned long long)hit << 40) |
+                                      (kd == 2 ? (unsigned long long)s.rec[5] << 24 : 0ull);
         }
     }
 }
@@ -858,13 +761,16 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
         const int u = owned_leaves[i];
         n_near += add_bands(dcols[u], rsize[u], doff[u], dgoff[u], rstart[u], 0);
     }
-    for (int u : order)
-        if (rvoff[u] < 0) add_cluster(u);
+    const bool diag_near = getenv("H2B_DIAG_NEAR_ONLY") && getenv("H2B_DIAG_NEAR_ONLY")[0] == '1';
+    if (!diag_near)
+        for (int u : order)
+            if (rvoff[u] < 0) add_cluster(u);
     for (size_t i = n_leaf_a; i < owned_leaves.size(); ++i) {
         const int u = owned_leaves[i];
         n_near += add_bands(dcols[u], rsize[u], doff[u], dgoff[u], rstart[u], 0);
     }
-    for (int u : owned_leaves) add_cluster(u);
+    if (!diag_near)
+        for (int u : owned_leaves) add_cluster(u);
     int64_t e_bytes_r = 0;
     for (int i = 0; i < L.r_nodes; ++i)
         if (rparent[i] >= 0 && reoff[i] >= 0)
@@ -895,8 +801,8 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
     H2B_CUDA_TRY(cudaMemset(p->xhat, 0, 16 * (size_t)L.xhat_len));
     H2B_CUDA_TRY(cudaMemset(p->ycpl, 0, 16 * (size_t)L.yhat_len));
     H2B_CUDA_TRY(cudaMemset(p->ynear, 0, 16 * (size_t)L.n_rows));
-    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->ctrl), 4 * sizeof(int)));
-    H2B_CUDA_TRY(cudaMemset(p->ctrl, 0, 4 * sizeof(int)));
+    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->ctrl), sizeof(unsigned long long)));
+    H2B_CUDA_TRY(cudaMemset(p->ctrl, 0, sizeof(unsigned long long)));
     H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->rec), sizeof(int64_t) * std::max<size_t>(1, rec.size())));
     H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->fwd_off), sizeof(int64_t) * fwd_off.size()));
     if (!rec.empty())

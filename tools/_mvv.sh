@@ -1,7 +1,3 @@
 cd $GRAFT_REPO_ROOT
-for v in ${VARS:-a b d e f}; do
-  echo -n "$v "; H2B_LIB_PATH=paper_2001_05523_b200/_lib/variants/$v.so python bench.py --steps 300 --warmup 5 --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['roofline']['frac'])"
-done
-for v in ${TRACE:-a}; do
-H2B_LIB_PATH=paper_2001_05523_b200/_lib/variants/$v.so python tools/mv_trace.py 2>&1 | grep -E "span|forward|bands |marks"
-done
+timeout 300 python -m pytest tests/test_gpu_matvec.py -q -x 2>&1 | tail -2
+for v in 0.7 0.8 0.6; do echo -n "split=$v: "; H2B_NEAR_SPLIT=$v timeout 300 python tools/mv_time.py 2>&1 | tail -1; done

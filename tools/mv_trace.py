@@ -42,42 +42,35 @@ for cand in range(1, n // 8):
     if 8 * cand + 4 < n and buf[8 * cand + 3] == cand and buf[8 * cand + 4] == cand and buf[8 * cand] == nfwd:
         tot = cand
         break
-b = buf[8 * tot : 8 * tot + 5].astype(np.int64)
 tr = buf[: 8 * tot].reshape(tot, 8).astype(np.int64)
 t0 = tr[:, 0].min()
-st, en, sm = (tr[:, 0] - t0) / 1e3, (tr[:, 1] - t0) / 1e3, tr[:, 2]
-names = ["forward", "bands", "-", "-"]
-bounds = [0, int(b[0]), tot, tot, tot]
-print(f"matvec span {en.max():.1f} us, CTAs {tot}")
-for i, nm in enumerate(names):
-    a, z = bounds[i], bounds[i + 1]
-    if z <= a:
+st, en = (tr[:, 0] - t0) / 1e3, (tr[:, 1] - t0) / 1e3
+kind = (tr[:, 2] >> 16) & 0xff
+nclimb = (tr[:, 2] >> 24) & 0xff
+hit = (tr[:, 2] >> 40) & 1
+print('record speculation hit rate (bands):', hit[kind != 2].mean().round(3))
+print(f"matvec span {en.max():.1f} us, tasks {tot}")
+for kd, nm in ((2, "forward"), (0, "near"), (1, "coupling"), (3, "descent")):
+    sel = kind == kd
+    if not sel.any():
         continue
-    d = en[a:z] - st[a:z]
-    print(f"{nm:8s} n={z-a:5d} start [{st[a:z].min():6.1f},{st[a:z].max():6.1f}] end [{en[a:z].min():6.1f},{en[a:z].max():6.1f}] dur mean {d.mean():6.2f} max {d.max():6.2f} sum {d.sum():8.1f}")
-# concurrency profile
-grid = np.linspace(0, en.max(), 40)
-for g in grid[::4]:
-    act = [(int(((st[a:z] <= g) & (en[a:z] > g)).sum())) for a, z in zip(bounds[:-1], bounds[1:])]
-    print(f"t={g:6.1f} active fwd/near/cpl/desc = {act}")
-
-# phase marks (relative to CTA start), means per role
-for i, nm in enumerate(names):
-    a, z = bounds[i], bounds[i + 1]
-    if z <= a:
-        continue
-    m = tr[a:z, 3:8]
-    ok = m[:, 0] > 0
-    if ok.any():
-        rel = (m[ok] - tr[a:z, 0][ok, None]) / 1e3
-        rel[m[ok] == 0] = np.nan
-        print(nm, "marks (us from start):", np.round(np.nanmean(np.where(np.isnan(rel), np.nan, rel), axis=0), 2).tolist())
-
-# concurrency / throughput timeline of band CTAs
-a, z = bounds[1], tot
+    d = en[sel] - st[sel]
+    print(f"{nm:8s} n={sel.sum():5d} start [{st[sel].min():6.1f},{st[sel].max():6.1f}] end [{en[sel].min():6.1f},{en[sel].max():6.1f}] dur mean {d.mean():6.2f} max {d.max():6.2f}")
+    m = tr[sel, 3:8].astype(np.float64)
+    m[m == 0] = np.nan
+    dm = np.diff(np.concatenate([tr[sel, 0:1].astype(np.float64), m], axis=1), axis=1)
+    with np.errstate(all="ignore"):
+        print(f"{'':8s} phase ns (start->m0->..->m4):", np.round(np.nanmean(dm, axis=0), 0).tolist())
+sel = kind == 2
+for c in range(int(nclimb[sel].max()) + 1 if sel.any() else 0):
+    m = sel & (nclimb == c)
+    if m.any():
+        print(f"forward climb {c:2d}: n={m.sum():4d} dur mean {(en[m]-st[m]).mean():6.2f} us, end max {en[m].max():6.1f}")
 edges = np.arange(0, en.max() + 5, 5.0)
 for lo in edges[:-1]:
     hi = lo + 5
-    act = ((st[a:z] < hi) & (en[a:z] > lo)).sum()
-    fin = ((en[a:z] >= lo) & (en[a:z] < hi)).sum()
-    print(f"[{lo:5.0f},{hi:5.0f}) bands active {act:4d} finished {fin:4d}")
+    row = []
+    for kd in (2, 0, 1, 3):
+        sel = kind == kd
+        row.append(int(((en[sel] >= lo) & (en[sel] < hi)).sum()))
+    print(f"[{lo:5.0f},{hi:5.0f}) finished fwd/near/cpl/desc {row}")

@@ -11,7 +11,7 @@ NVCC=/usr/local/cuda/bin/nvcc
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 while [ $# -ge 2 ]; do
   name=$1; flags=$2; shift 2
-  $NVCC -c paper_2001_05523_b200/csrc/matvec.cu -o $OUT/$name.o -O3 -std=c++17 -Xcompiler -fPIC -I include \
+  $NVCC -c ${SRC:-paper_2001_05523_b200/csrc/matvec.cu} -o $OUT/$name.o -O3 -std=c++17 -Xcompiler -fPIC -I include \
     $ARCH -lineinfo --expt-relaxed-constexpr $flags
   $NVCC -shared -o $OUT/$name.so $OBJ/errors.cpp.o $OBJ/structure.cpp.o $OBJ/quadrature.cu.o $OUT/$name.o $ARCH \
     -lcudart_static -lrt -ldl -lpthread
