@@ -52,12 +52,15 @@
 namespace h2b {
 namespace {
 
-constexpr int kThreads = 256;
+#ifndef H2B_THREADS
+#define H2B_THREADS 128
+#endif
+constexpr int kThreads = H2B_THREADS;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxVec = 512;        // max rank / leaf size of the vectors kept in smem
-constexpr int kMaxDepth = 64;
+constexpr int kMaxDepth = 32;
 #ifndef H2B_STAGE_KB
-#define H2B_STAGE_KB 32
+#define H2B_STAGE_KB 24
 #endif
 constexpr int kStageBytes = H2B_STAGE_KB * 1024;  // TMA staging buffer per CTA (one band)
 
@@ -67,10 +70,8 @@ constexpr int kBandWords = 24;  // src_off, cols, rows, gidx_off, out_off, is_la
                                 // k, parent y_hat offset (-1 root), k_parent, e_off, y_hat offset,
                                 // is_leaf, v_off, start (size = rows of a leaf)
 constexpr int kFwdHead = 6;     // start, size, k, v_off, xhat_off, n_climb
-constexpr int kFwdLevel = 6;
+constexpr int kFwdLevel = 6;    // k0, kp, e_off_c0, e_off_own, xhat_off_c0, xhat_off_parent
 constexpr int kKindNear = 0, kKindCpl = 1, kKindDescent = 3;  // band record kinds (word 7)
-constexpr int kSpecWin = 16;   // speculatively fetched band records per CTA
-constexpr int kSpecLead = 4;   // ... starting this many tickets before blockIdx.x    // k0, kp, e_off_c0, e_off_own, xhat_off_c0, xhat_off_parent
 
 }  // namespace
 }  // namespace h2b
@@ -88,7 +89,7 @@ struct h2b_plan {
     int64_t band_base;  // record offset of band 0
     int64_t dgidx_bytes;
     int n_near, n_cpl;
-    int max_cols;
+    int max_cols, vec_len;
     int smem;
     int64_t e_bytes_r;
     double* dx;
@@ -185,15 +186,73 @@ __device__ __forceinline__ void mark(unsigned long long* m, int i) {
 // ---------------------------------------------------------------------------
 // dense building blocks (operands in shared memory unless noted)
 
+#ifndef H2B_ROWBLOCK
+#define H2B_ROWBLOCK 4
+#endif
+constexpr int kRowBlock = H2B_ROWBLOCK;  // rows per warp in rows_dot's many-rows mode
+
+__host__ __device__ constexpr int log2c(int n) { return n <= 1 ? 0 : 1 + log2c(n / 2); }
+
+// Sum over the warp of N per-lane values by recursive halving (N - 1 + 5 -
+// log2 N shuffles); lane l ends with the total of value ri(l), whose bit
+// (log2 N - 1 - j) is lane bit (4 - j).
+template <int N>
+__device__ __forceinline__ double warp_sum(double (&a)[N], int lane) {
+    int o = 16;
+#pragma unroll
+    for (int h = N / 2; h >= 1; h >>= 1, o >>= 1) {
+        const bool up = lane & o;
+#pragma unroll
+        for (int i = 0; i < h; ++i) {
+            const double send = up ? a[i] : a[i + h], keep = up ? a[i + h] : a[i];
+            a[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    double v = a[0];
+#pragma unroll
+    for (; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// One warp: out[r0 + i] = M[(r0 + i) * ld : ...] . v, i < nr <= R.  Lanes
+// stride the columns; every lane keeps R independent FMA chains and reads
+// v[c] once for all R rows.  Rows past nr re-read the last row (branch-free
+// loads, results dropped).
+template <int R>
+__device__ __forceinline__ void rows_warp(const double* M, int64_t ld, int r0, int nr, int cols, const double* v,
+                                          double* out, int lane) {
+    if (nr <= 0) return;
+    const double* m[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) m[i] = M + (int64_t)(r0 + min(i, nr - 1)) * ld;
+    double acc[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) acc[i] = 0.0;
+    for (int c = lane; c < cols; c += 32) {
+        const double vc = v[c];
+        double e[R];
+#pragma unroll
+        for (int i = 0; i < R; ++i) e[i] = m[i][c];
+#pragma unroll
+        for (int i = 0; i < R; ++i) acc[i] = fma(e[i], vc, acc[i]);
+    }
+    const double sum = warp_sum<R>(acc, lane);
+    constexpr int lg = log2c(R), sh = 5 - lg;
+    int ri = 0;
+#pragma unroll
+    for (int j = 0; j < lg; ++j) ri |= ((lane >> (4 - j)) & 1) << (lg - 1 - j);
+    if ((lane & ((1 << sh) - 1)) == 0 && ri < nr) out[r0 + ri] = sum;
+}
+
 // out[i] = M[i*ld : i*ld+cols] . v, i < rows.  Few rows: one row per warp
 // (four partial sums per lane); many rows: each warp owns 4 rows at a time
 // (4 independent dot products, interleaved shuffle reductions).
 __device__ void rows_dot(const double* M, int64_t ld, int rows, int cols, const double* v,
                                          double* out) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (rows < 4 * kWarps) {
-        for (int r = warp; r < rows; r += kWarps) {
-            const double* row = M + (int64_t)r * ld;
+    if (rows <= kWarps) {
+        if (warp < rows) {
+            const double* row = M + (int64_t)warp * ld;
             double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
             int c = lane;
             for (; c + 96 < cols; c += 128) {
@@ -208,31 +267,16 @@ __device__ void rows_dot(const double* M, int64_t ld, int rows, int cols, const 
             double sum = (a0 + a1) + (a2 + a3);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-            if (lane == 0) out[r] = sum;
+            if (lane == 0) out[warp] = sum;
         }
         return;
     }
-    for (int r0 = 4 * warp; r0 < rows; r0 += 4 * kWarps) {
-        const int nr = min(4, rows - r0);
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int c = lane; c < cols; c += 32) {
-            const double vc = v[c];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-                if (i < nr) acc[i] = fma(M[(int64_t)(r0 + i) * ld + c], vc, acc[i]);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
-        if (lane < nr) {
-            double r = acc[0];
-#pragma unroll
-            for (int i = 1; i < 4; ++i)
-                if (lane == i) r = acc[i];
-            out[r0 + lane] = r;
-        }
+    if (rows <= 2 * kWarps) {
+        rows_warp<2>(M, ld, 2 * warp, min(2, rows - 2 * warp), cols, v, out, lane);
+        return;
     }
+    for (int r0 = kRowBlock * warp; r0 < rows; r0 += kRowBlock * kWarps)
+        rows_warp<kRowBlock>(M, ld, r0, min(kRowBlock, rows - r0), cols, v, out, lane);
 }
 
 // out[c] = sum_r M[r*k + c] v[r], c < k: warps split rows, lanes columns,
@@ -284,9 +328,38 @@ __device__ __forceinline__ void gather(double* rhs, const double* __restrict__ s
 }
 
 // Gather from LL form: rhs[i] = LL[idx[i]] (spins until the producer's epoch).
+// (all index loads, then all LL loads in flight at once; spin only on the
+// entries whose producer has not published yet)
 __device__ __forceinline__ void gather_ll(double* rhs, const uint64_t* ll, const int32_t* idx, int n,
                                           uint32_t epoch) {
-    for (int i = threadIdx.x; i < n; i += kThreads) rhs[i] = ll_load(ll + 2 * (int64_t)__ldg(idx + i), epoch);
+    constexpr int kU = 1024 / kThreads;
+    for (int base = 0; base < n; base += kU * kThreads) {
+        int ix[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int i = base + u * kThreads + (int)threadIdx.x;
+            ix[u] = i < n ? __ldg(idx + i) : -1;
+        }
+        uint64_t w0[kU], w1[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            w0[u] = w1[u] = 0;
+            if (ix[u] >= 0)
+                asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];"
+                             : "=l"(w0[u]), "=l"(w1[u])
+                             : "l"(ll + 2 * (int64_t)ix[u]));
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            if (ix[u] < 0) continue;
+            double v;
+            if ((uint32_t)(w0[u] >> 32) == epoch && (uint32_t)(w1[u] >> 32) == epoch)
+                v = __longlong_as_double(static_cast<long long>((w0[u] & 0xffffffffull) | (w1[u] << 32)));
+            else
+                v = ll_load(ll + 2 * (int64_t)ix[u], epoch);
+            rhs[base + u * kThreads + (int)threadIdx.x] = v;
+        }
+    }
 }
 
 struct Shared {
@@ -294,8 +367,8 @@ struct Shared {
     uint64_t* bar;             // mbarrier of the staging buffer
     char* stage;               // kStageBytes, 128-byte aligned
     double* rhs;               // max_cols
-    double* va;                // kMaxVec
-    double* vb;                // kMaxVec
+    double* va;                // 2 vec_len ([x_hat_c0; x_hat_c1] in the climb)
+    double* vb;                // vec_len (vec_len = max rank / leaf size)
     double* red;               // kWarps * 32
     int64_t* rec;              // small record cache
     uint32_t parity;           // mbarrier phase of the staging slot in use
@@ -514,7 +587,7 @@ struct KArgs {
     const int64_t* fwd_off;
     int64_t band_base, band_bytes, dgidx_bytes;
     int n_near, n_cpl, n_near_a, n_inner_bands;
-    int max_cols;
+    int max_cols, vec_len;
     int64_t e_bytes_r;
     uint64_t *xhat, *ycpl, *yfin, *ynear;
     unsigned long long* ctrl;
@@ -522,7 +595,7 @@ struct KArgs {
 };
 
 #ifndef H2B_MINB
-#define H2B_MINB 4
+#define H2B_MINB 6
 #endif
 
 __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, const double* __restrict__ x,
@@ -530,16 +603,15 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
     extern __shared__ __align__(128) char smraw[];
     __shared__ int s_ticket;
     __shared__ uint32_t s_epoch;
-    __shared__ int64_t s_rec[kSpecWin * kBandWords > kFwdHead + kFwdLevel * kMaxDepth ? kSpecWin * kBandWords
-                                                                                : kFwdHead + kFwdLevel * kMaxDepth];
+    __shared__ int64_t s_rec[kFwdHead + kFwdLevel * kMaxDepth];
     const h2b_layout& L = a.L;
     Shared s;
     s.bar = reinterpret_cast<uint64_t*>(smraw);
     s.stage = smraw + 128;
     s.rhs = reinterpret_cast<double*>(smraw + 128 + kStageBytes);
     s.va = s.rhs + a.max_cols;
-    s.vb = s.va + kMaxVec;
-    s.red = s.vb + kMaxVec;
+    s.vb = s.va + 2 * a.vec_len;
+    s.red = s.vb + a.vec_len;
     s.rec = s_rec;
     s.parity = 0;
     s.issued = false;
@@ -551,15 +623,6 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
         s_epoch = (uint32_t)(t / gridDim.x) + 1u;
         mbar_init(s.bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    // While the ticket is in flight, fetch the band records of the tickets
-    // near blockIdx.x (CTAs mostly take tickets in launch order): a hit saves
-    // the dependent record round trip.
-    const int spec0 = (int)blockIdx.x - kSpecLead;
-    for (int i = threadIdx.x; i < kSpecWin * kBandWords; i += kThreads) {
-        const int tk = spec0 + i / kBandWords;
-        if (tk >= L.c_leaves && tk < (int)gridDim.x)
-            s_rec[i] = __ldg(a.rec + a.band_base + (int64_t)kBandWords * (tk - L.c_leaves) + i % kBandWords);
     }
     __syncthreads();
     const int ticket = s_ticket;
@@ -581,11 +644,7 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
         // the first bands pull the row-basis transfer matrices into L2
         const int np = min(a.n_near + a.n_cpl, 512);
         if (b < np) prefetch_slice(L.r_E, a.e_bytes_r, b, np);
-        if (ticket >= spec0 && ticket < spec0 + kSpecWin) {
-            s.rec = s_rec + kBandWords * (ticket - spec0);
-        } else {
-            load_rec(s, a.rec + a.band_base + (int64_t)kBandWords * b, kBandWords);
-        }
+        load_rec(s, a.rec + a.band_base + (int64_t)kBandWords * b, kBandWords);
         const int kind = (int)s.rec[7];
         if (kind == kKindNear)
             task_band<false>(L, x, a.xhat, a.ynear, a.yfin, a.ycpl, a.ynear, y, epoch, s);
@@ -604,8 +663,7 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
             a.trace[8 * ticket] = t_begin;
             a.trace[8 * ticket + 1] = t_end;
             const int kd = ticket < L.c_leaves ? 2 : (int)s.rec[7];
-            const bool hit = ticket >= spec0 && ticket < spec0 + kSpecWin;
-            a.trace[8 * ticket + 2] = smid | ((unsigned long long)kd << 16) | ((unsigned long long)hit << 40) |
+            a.trace[8 * ticket + 2] = smid | ((unsigned long long)kd << 16) |
                                       (kd == 2 ? (unsigned long long)s.rec[5] << 24 : 0ull);
         }
     }
@@ -690,7 +748,8 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
     maxcols = std::max(maxcols, maxk);
     if (maxk > kMaxVec || maxleaf > kMaxVec)
         return fail(H2B_ERR_INVALID, "h2b_plan_create: cluster rank or leaf size above 512");
-    const int smem = 128 + kStageBytes + (int)sizeof(double) * (maxcols + 2 * kMaxVec + kWarps * 32);
+    const int vec_len = (std::max(maxk, maxleaf) + 1) & ~1;
+    const int smem = 128 + kStageBytes + (int)sizeof(double) * (maxcols + 3 * vec_len + kWarps * 32);
     if (smem > 227 * 1024) return fail(H2B_ERR_INVALID, "h2b_plan_create: gathered right-hand side exceeds shared memory");
 
     std::vector<int64_t> rec, fwd_off(L.c_leaves);
@@ -705,7 +764,7 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
             const int p = cparent[node];
             if (p < 0 || cchild[2 * p + 1] != node) break;
             const int c0 = cchild[2 * p];
-            if (n >= kMaxDepth) return fail(H2B_ERR_INVALID, "h2b_plan_create: tree deeper than 64 levels");
+            if (n >= kMaxDepth) return fail(H2B_ERR_INVALID, "h2b_plan_create: tree deeper than 32 levels");
             rec.insert(rec.end(), {crank[c0], crank[p], ceoff[c0], ceoff[node], cxoff[c0], cxoff[p]});
             node = p;
             ++n;
@@ -789,6 +848,7 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
         p->dgidx_bytes = m;
     }
     p->max_cols = maxcols;
+    p->vec_len = vec_len;
     p->smem = smem;
     p->e_bytes_r = e_bytes_r;
     H2B_CUDA_TRY(cudaGetDevice(&p->device));
@@ -845,6 +905,7 @@ extern "C" int h2b_matvec(h2b_plan* p, const double* d_x, double* d_y, void* str
     a.n_near = p->n_near;
     a.n_cpl = p->n_cpl;
     a.max_cols = p->max_cols;
+    a.vec_len = p->vec_len;
     a.e_bytes_r = p->e_bytes_r;
     a.xhat = p->xhat;
     a.ycpl = p->ycpl;

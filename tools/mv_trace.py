@@ -47,8 +47,6 @@ t0 = tr[:, 0].min()
 st, en = (tr[:, 0] - t0) / 1e3, (tr[:, 1] - t0) / 1e3
 kind = (tr[:, 2] >> 16) & 0xff
 nclimb = (tr[:, 2] >> 24) & 0xff
-hit = (tr[:, 2] >> 40) & 1
-print('record speculation hit rate (bands):', hit[kind != 2].mean().round(3))
 print(f"matvec span {en.max():.1f} us, tasks {tot}")
 for kd, nm in ((2, "forward"), (0, "near"), (1, "coupling"), (3, "descent")):
     sel = kind == kd
