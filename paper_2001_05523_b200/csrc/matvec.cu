@@ -306,6 +306,43 @@ __device__ void cols_dot(const double* M, int rows, int k, const double* v, doub
     }
 }
 
+// Small dense products (transfer matrices, leaf bases: at most a few hundred
+// columns), one thread per output: no reductions, no barriers inside; four
+// interleaved partial sums per thread; operands in shared or global memory.
+// out[r] = M[r*ld : r*ld+cols] . v, r < rows
+__device__ __forceinline__ void small_rows_dot(const double* M, int64_t ld, int rows, int cols, const double* v,
+                                               double* out) {
+    for (int r = threadIdx.x; r < rows; r += kThreads) {
+        const double* m = M + (int64_t)r * ld;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int c = 0;
+        for (; c + 3 < cols; c += 4) {
+            a0 = fma(m[c], v[c], a0);
+            a1 = fma(m[c + 1], v[c + 1], a1);
+            a2 = fma(m[c + 2], v[c + 2], a2);
+            a3 = fma(m[c + 3], v[c + 3], a3);
+        }
+        for (; c < cols; ++c) a0 = fma(m[c], v[c], a0);
+        out[r] = (a0 + a1) + (a2 + a3);
+    }
+}
+
+// out[c] = sum_r M[r*k + c] v[r], c < k
+__device__ __forceinline__ void small_cols_dot(const double* M, int rows, int k, const double* v, double* out) {
+    for (int c = threadIdx.x; c < k; c += kThreads) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int r = 0;
+        for (; r + 3 < rows; r += 4) {
+            a0 = fma(M[(int64_t)r * k + c], v[r], a0);
+            a1 = fma(M[(int64_t)(r + 1) * k + c], v[r + 1], a1);
+            a2 = fma(M[(int64_t)(r + 2) * k + c], v[r + 2], a2);
+            a3 = fma(M[(int64_t)(r + 3) * k + c], v[r + 3], a3);
+        }
+        for (; r < rows; ++r) a0 = fma(M[(int64_t)r * k + c], v[r], a0);
+        out[c] = (a0 + a1) + (a2 + a3);
+    }
+}
+
 // Gather rhs[i] = src[idx[i]], i < n: all index loads, then all value loads.
 __device__ __forceinline__ void gather(double* rhs, const double* __restrict__ src, const int32_t* idx, int n) {
     constexpr int kU = 4;
@@ -447,7 +484,9 @@ __device__ void task_forward(const double* __restrict__ c_V, const double* __res
     for (int r = threadIdx.x; r < size; r += blockDim.x) s.va[r] = __ldg(x + col_perm[start + r]);
     mbar_wait(s.bar, s.parity);
     __syncthreads();
-    cols_dot(V, size, k, s.va, s.red, s.vb);  // own coefficients stay in s.vb
+    small_cols_dot(V, size, k, s.va, s.vb);  // own coefficients stay in s.vb
+    __syncthreads();
+    mark(s.mark, 0);
     {
         uint64_t* dst = xhat + 2 * xhat_off;
         for (int c = threadIdx.x; c < k; c += blockDim.x) ll_store(dst + 2 * c, s.vb[c], epoch);
@@ -472,8 +511,10 @@ __device__ void task_forward(const double* __restrict__ c_V, const double* __res
         for (int r = threadIdx.x; r < k1; r += kThreads) s.va[k0 + r] = s.vb[r];
         cp_async_wait_all();
         __syncthreads();
+        if (j < 2) mark(s.mark, 1 + 2 * j);
         if (in_smem) {
-            cols_dot(buf, k0 + k1, kp, s.va, s.red, s.vb);
+            small_cols_dot(buf, k0 + k1, kp, s.va, s.vb);
+            __syncthreads();
         } else {
             cols_dot(c_E + lv[2], k0, kp, s.va, s.red, s.vb);
             for (int c = threadIdx.x; c < kp; c += kThreads) s.rhs[c] = s.vb[c];
@@ -484,6 +525,7 @@ __device__ void task_forward(const double* __restrict__ c_V, const double* __res
         }
         uint64_t* dst = xhat + 2 * lv[5];
         for (int c = threadIdx.x; c < kp; c += kThreads) ll_store(dst + 2 * c, s.vb[c], epoch);
+        if (j < 2) mark(s.mark, 2 + 2 * j);
         k1 = kp;
     }
 }
@@ -507,10 +549,17 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
     const int start = (int)d[7];
     double* Es = reinterpret_cast<double*>(s.stage);
     const bool e_smem = par_off >= 0 && k * kp <= kStageBytes / 8;
+    // transfer / leaf basis matrices are staged TRANSPOSED, so that the
+    // thread-per-row products below read consecutive words (no bank conflicts)
     if (e_smem)
-        for (int i = threadIdx.x; i < k * kp; i += kThreads) cp_async8(Es + i, r_E + e_off + i);
+        for (int i = threadIdx.x; i < k * kp; i += kThreads) {
+            const int r = i / kp, c = i - r * kp;
+            cp_async8(Es + c * k + r, r_E + e_off + i);
+        }
     const uint64_t* yc = ycpl + 2 * yoff;
     for (int i = threadIdx.x; i < k; i += kThreads) s.va[i] = has_cpl ? ll_load(yc + 2 * i, epoch) : 0.0;
+    __syncthreads();
+    mark(s.mark, 0);
     if (par_off >= 0) {
         const uint64_t* yp = yfin + 2 * par_off;
         for (int i = threadIdx.x; i < kp; i += kThreads) s.rhs[i] = ll_load(yp + 2 * i, epoch);
@@ -519,14 +568,19 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
     __syncthreads();
     mark(s.mark, 4);
     if (par_off >= 0 && k > 0) {
-        rows_dot(e_smem ? Es : r_E + e_off, kp, k, kp, s.rhs, s.vb);
+        if (e_smem)
+            small_cols_dot(Es, kp, k, s.rhs, s.vb);  // E^T staged: out[r] = sum_c Es[c*k + r] v[c]
+        else
+            small_rows_dot(r_E + e_off, kp, k, kp, s.rhs, s.vb);
         __syncthreads();
         for (int i = threadIdx.x; i < k; i += kThreads) s.va[i] += s.vb[i];
         __syncthreads();
     }
+    mark(s.mark, 1);
     if (!leaf) {
         uint64_t* dst = yfin + 2 * yoff;
         for (int i = threadIdx.x; i < k; i += kThreads) ll_store(dst + 2 * i, s.va[i], epoch);
+        mark(s.mark, 2);
         return;
     }
     const int size = (int)d[8];
@@ -534,11 +588,19 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
     const bool v_smem = nv <= kStageBytes / 8;
     const double* Vg = r_V + v_off;
     if (v_smem) {
-        for (int i = threadIdx.x; i < nv; i += kThreads) cp_async8(Es + i, Vg + i);
+        for (int i = threadIdx.x; i < nv; i += kThreads) {
+            const int r = i / k, c = i - r * k;
+            cp_async8(Es + c * size + r, Vg + i);
+        }
         cp_async_wait_all();
     }
     __syncthreads();
-    if (k > 0) rows_dot(v_smem ? Es : Vg, k, size, k, s.va, s.vb);
+    if (k > 0) {
+        if (v_smem)
+            small_cols_dot(Es, k, size, s.va, s.vb);  // V^T staged
+        else
+            small_rows_dot(Vg, k, size, k, s.va, s.vb);
+    }
     __syncthreads();
     const uint64_t* yn = ynear + 2 * (int64_t)start;
     for (int i = threadIdx.x; i < size; i += blockDim.x)
@@ -664,7 +726,8 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
             a.trace[8 * ticket + 1] = t_end;
             const int kd = ticket < L.c_leaves ? 2 : (int)s.rec[7];
             a.trace[8 * ticket + 2] = smid | ((unsigned long long)kd << 16) |
-                                      (kd == 2 ? (unsigned long long)s.rec[5] << 24 : 0ull);
+                                      (kd == 2 ? (unsigned long long)s.rec[5] << 24 : 0ull) |
+                                      ((kd == 1 && s.rec[5]) || kd == 3 ? (1ull << 41) | ((unsigned long long)s.rec[17] << 32) : 0ull);
         }
     }
 }
@@ -776,27 +839,32 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
     // parents first; the last band of a cluster (an empty one when it has no
     // couplings) carries the cluster's downward-step record.
     const int64_t band_base = (int64_t)rec.size();
-    auto add_bands = [&](int cols, int rows, int64_t src, int64_t gi, int64_t outo, int kind) {
+    auto bands_to = [&](std::vector<int64_t>& out, int cols, int rows, int64_t src, int64_t gi, int64_t outo,
+                        int kind) {
         const int per = std::max(1, (int)(kStageBytes / (8 * std::max(cols, 1))));
         int n = 0;
         for (int r0 = 0; r0 < rows; r0 += per, ++n) {
             const int nr = std::min(per, rows - r0);
-            rec.insert(rec.end(), {src + (int64_t)r0 * cols, cols, nr, gi, outo + r0, 0, 0, kind});
-            rec.insert(rec.end(), kBandWords - 8, 0);
+            out.insert(out.end(), {src + (int64_t)r0 * cols, cols, nr, gi, outo + r0, 0, 0, kind});
+            out.insert(out.end(), kBandWords - 8, 0);
         }
         return n;
     };
     int n_cpl = 0;
-    auto add_cluster = [&](int u) {
+    // Coupling bands of cluster u: all but the last to `early`; the last one
+    // (an empty band when u has no couplings) runs u's downward step and goes
+    // to `late`.
+    auto cluster_to = [&](std::vector<int64_t>& early, std::vector<int64_t>& late, int u) {
         const bool cpl = scols[u] > 0 && rrank[u] > 0;
-        int n = cpl ? add_bands(scols[u], rrank[u], soff[u], sgoff[u], ryoff[u], 1) : 0;
+        std::vector<int64_t> tmp;
+        int n = cpl ? bands_to(tmp, scols[u], rrank[u], soff[u], sgoff[u], ryoff[u], kKindCpl) : 0;
         if (n == 0) {  // empty band: downward step only
-            rec.insert(rec.end(), {0, 0, 0, 0, 0, 0, 0, 1});
-            rec.insert(rec.end(), kBandWords - 8, 0);
+            tmp.insert(tmp.end(), {0, 0, 0, 0, 0, 0, 0, kKindCpl});
+            tmp.insert(tmp.end(), kBandWords - 8, 0);
             n = 1;
         }
         n_cpl += n;
-        int64_t* last = rec.data() + rec.size() - kBandWords;
+        int64_t* last = tmp.data() + tmp.size() - kBandWords;
         const int par = rparent[u];
         const int64_t d[9] = {rrank[u], par >= 0 ? ryoff[par] : -1, par >= 0 ? rrank[par] : 0,
                               par >= 0 ? reoff[u] : 0, ryoff[u], rvoff[u] >= 0 ? 1 : 0,
@@ -804,32 +872,57 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
         last[5] = 1;
         last[6] = cpl ? 1 : 0;
         for (int i = 0; i < 9; ++i) last[8 + i] = d[i];
+        int dd = 0;
+        for (int q = rparent[u]; q >= 0; q = rparent[q]) ++dd;
+        last[17] = dd;  // depth (diagnostics: trace)
+        early.insert(early.end(), tmp.begin(), tmp.end() - kBandWords);
+        late.insert(late.end(), tmp.end() - kBandWords, tmp.end());
     };
-    // ticket order: near bands (first part) | inner-cluster coupling bands,
-    // parents first | near bands (rest) | leaf coupling bands.  The first near
-    // bands stream while the forward climb runs; the inner downward chain then
-    // advances while the remaining nearfield streams.
-    double split = 0.7;
-    if (const char* e = getenv("H2B_NEAR_SPLIT")) split = atof(e);
+    // append `xs` with the bands of `fill` spread evenly among them
+    auto interleave = [&](const std::vector<int64_t>& xs, const std::vector<int64_t>& fill) {
+        const int64_t nx = (int64_t)xs.size() / kBandWords, nf = (int64_t)fill.size() / kBandWords;
+        int64_t f = 0;
+        for (int64_t i = 0; i < nx; ++i) {
+            rec.insert(rec.end(), xs.begin() + kBandWords * i, xs.begin() + kBandWords * (i + 1));
+            for (const int64_t until = (nf * (i + 1)) / nx; f < until; ++f)
+                rec.insert(rec.end(), fill.begin() + kBandWords * f, fill.begin() + kBandWords * (f + 1));
+        }
+        rec.insert(rec.end(), fill.begin() + kBandWords * f, fill.end());
+    };
+    // Ticket order after the forward tasks (a task waits only on smaller
+    // tickets; near bands never wait):
+    //   near A1 | the leaf coupling bands except each leaf's last one (they
+    //   need leaf-level x_hat only) spread over near A2 | inner-cluster
+    //   coupling bands, parents first (each cluster's last band runs its
+    //   downward step) spread over near B | the last band of every leaf (leaf
+    //   downward step; needs every near band of its leaf).
+    // The nearfield streams while the forward climb and the downward chain
+    // advance.
+    double fa1 = 0.2, fa2 = 0.5;
+    if (const char* e = getenv("H2B_NEAR_A1")) fa1 = atof(e);
+    if (const char* e = getenv("H2B_NEAR_A2")) fa2 = atof(e);
     std::vector<int> owned_leaves;
     for (int u : order)
         if (rvoff[u] >= 0) owned_leaves.push_back(u);
-    const int n_leaf_a = (int)(split * owned_leaves.size());
+    const int nl = (int)owned_leaves.size();
+    const int c1 = std::min(nl, (int)(fa1 * nl)), c2 = std::min(nl, c1 + (int)(fa2 * nl));
+    std::vector<int64_t> na1, na2, nb, leaf_early, leaf_late, inner;
     int n_near = 0;
-    for (int i = 0; i < n_leaf_a; ++i) {
+    for (int i = 0; i < nl; ++i) {
         const int u = owned_leaves[i];
-        n_near += add_bands(dcols[u], rsize[u], doff[u], dgoff[u], rstart[u], 0);
+        n_near += bands_to(i < c1 ? na1 : i < c2 ? na2 : nb, dcols[u], rsize[u], doff[u], dgoff[u], rstart[u],
+                           kKindNear);
     }
     const bool diag_near = getenv("H2B_DIAG_NEAR_ONLY") && getenv("H2B_DIAG_NEAR_ONLY")[0] == '1';
-    if (!diag_near)
+    if (!diag_near) {
         for (int u : order)
-            if (rvoff[u] < 0) add_cluster(u);
-    for (size_t i = n_leaf_a; i < owned_leaves.size(); ++i) {
-        const int u = owned_leaves[i];
-        n_near += add_bands(dcols[u], rsize[u], doff[u], dgoff[u], rstart[u], 0);
+            if (rvoff[u] < 0) cluster_to(inner, inner, u);
+        for (int u : owned_leaves) cluster_to(leaf_early, leaf_late, u);
     }
-    if (!diag_near)
-        for (int u : owned_leaves) add_cluster(u);
+    rec.insert(rec.end(), na1.begin(), na1.end());
+    interleave(leaf_early, na2);
+    interleave(inner, nb);
+    rec.insert(rec.end(), leaf_late.begin(), leaf_late.end());
     int64_t e_bytes_r = 0;
     for (int i = 0; i < L.r_nodes; ++i)
         if (rparent[i] >= 0 && reoff[i] >= 0)

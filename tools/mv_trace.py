@@ -64,6 +64,17 @@ for c in range(int(nclimb[sel].max()) + 1 if sel.any() else 0):
     m = sel & (nclimb == c)
     if m.any():
         print(f"forward climb {c:2d}: n={m.sum():4d} dur mean {(en[m]-st[m]).mean():6.2f} us, end max {en[m].max():6.1f}")
+is_last = (tr[:, 2] >> 41) & 1
+ddepth = (tr[:, 2] >> 32) & 0xff
+sel = ((kind == 1) | (kind == 3)) & (is_last == 1)
+for dd in range(int(ddepth[sel].max()) + 1 if sel.any() else 0):
+    m = sel & (ddepth == dd)
+    if m.any():
+        mk = tr[m, 3:8].astype(np.float64)
+        mk[mk == 0] = np.nan
+        with np.errstate(all="ignore"):
+            ph = np.round(np.nanmean(mk - tr[m, 0:1], axis=0) / 1e3, 2).tolist()
+        print(f"descent depth {dd:2d}: n={m.sum():4d} start [{st[m].min():6.1f},{st[m].max():6.1f}] end [{en[m].min():6.1f},{en[m].max():6.1f}] dur mean {(en[m]-st[m]).mean():5.2f} marks(us from start: ycpl, E-step, store, -, parent) {ph}")
 edges = np.arange(0, en.max() + 5, 5.0)
 for lo in edges[:-1]:
     hi = lo + 5
