@@ -327,8 +327,33 @@ __device__ __forceinline__ void small_rows_dot(const double* M, int64_t ld, int 
     }
 }
 
-// out[c] = sum_r M[r*k + c] v[r], c < k
-__device__ __forceinline__ void small_cols_dot(const double* M, int rows, int k, const double* v, double* out) {
+// out[c] = sum_r M[r*k + c] v[r], c < k.  With at most 32 outputs, the warps
+// split the rows (interleaved) and the partials are summed in a fixed order
+// through red (kWarps x 32): ends with __syncthreads() in that case.
+__device__ __forceinline__ void small_cols_dot(const double* M, int rows, int k, const double* v, double* out,
+                                               double* red) {
+    if (k <= 32 && red) {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        if (lane < k) {
+            double a0 = 0.0, a1 = 0.0;
+            int r = warp;
+            for (; r + kWarps < rows; r += 2 * kWarps) {
+                a0 = fma(M[(int64_t)r * k + lane], v[r], a0);
+                a1 = fma(M[(int64_t)(r + kWarps) * k + lane], v[r + kWarps], a1);
+            }
+            if (r < rows) a0 = fma(M[(int64_t)r * k + lane], v[r], a0);
+            red[warp * 32 + lane] = a0 + a1;
+        }
+        __syncthreads();
+        if (warp == 0 && lane < k) {
+            double t = 0.0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) t += red[w * 32 + lane];
+            out[lane] = t;
+        }
+        __syncthreads();
+        return;
+    }
     for (int c = threadIdx.x; c < k; c += kThreads) {
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         int r = 0;
@@ -483,8 +508,23 @@ __device__ void task_forward(const double* __restrict__ c_V, const double* __res
     const double* V = stage_issue(s, c_V + v_off, ((int64_t)size * k * 8 + 15) & ~int64_t(15));
     for (int r = threadIdx.x; r < size; r += blockDim.x) s.va[r] = __ldg(x + col_perm[start + r]);
     mbar_wait(s.bar, s.parity);
-    __syncthreads();
-    small_cols_dot(V, size, k, s.va, s.vb);  // own coefficients stay in s.vb
+    __syncthreads();  // (also: the climb levels are in s.rec)
+    {
+        // pull every climb level's [E_c0; E_own] into L2 now (the copies into
+        // shared memory at each level then hit L2)
+        int kk = k;
+        for (int j = 0; j < n_climb; ++j) {
+            const int64_t* lv = s.rec + kFwdHead + kFwdLevel * j;
+            const int kp = (int)lv[1];
+            const int64_t b0 = 8 * (int64_t)lv[0] * kp, b1 = 8 * (int64_t)kk * kp;
+            const char* e0 = reinterpret_cast<const char*>(c_E + lv[2]);
+            const char* e1 = reinterpret_cast<const char*>(c_E + lv[3]);
+            for (int64_t o = 128 * threadIdx.x; o < b0; o += 128 * kThreads) prefetch_l2(e0 + o);
+            for (int64_t o = 128 * threadIdx.x; o < b1; o += 128 * kThreads) prefetch_l2(e1 + o);
+            kk = kp;
+        }
+    }
+    small_cols_dot(V, size, k, s.va, s.vb, s.red);  // own coefficients stay in s.vb
     __syncthreads();
     mark(s.mark, 0);
     {
@@ -513,7 +553,7 @@ __device__ void task_forward(const double* __restrict__ c_V, const double* __res
         __syncthreads();
         if (j < 2) mark(s.mark, 1 + 2 * j);
         if (in_smem) {
-            small_cols_dot(buf, k0 + k1, kp, s.va, s.vb);
+            small_cols_dot(buf, k0 + k1, kp, s.va, s.vb, s.red);
             __syncthreads();
         } else {
             cols_dot(c_E + lv[2], k0, kp, s.va, s.red, s.vb);
@@ -569,7 +609,7 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
     mark(s.mark, 4);
     if (par_off >= 0 && k > 0) {
         if (e_smem)
-            small_cols_dot(Es, kp, k, s.rhs, s.vb);  // E^T staged: out[r] = sum_c Es[c*k + r] v[c]
+            small_cols_dot(Es, kp, k, s.rhs, s.vb, s.red);  // E^T staged: out[r] = sum_c Es[c*k + r] v[c]
         else
             small_rows_dot(r_E + e_off, kp, k, kp, s.rhs, s.vb);
         __syncthreads();
@@ -597,7 +637,7 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
     __syncthreads();
     if (k > 0) {
         if (v_smem)
-            small_cols_dot(Es, k, size, s.va, s.vb);  // V^T staged
+            small_cols_dot(Es, k, size, s.va, s.vb, nullptr);  // V^T staged
         else
             small_rows_dot(Vg, k, size, k, s.va, s.vb);
     }
@@ -919,10 +959,14 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
             if (rvoff[u] < 0) cluster_to(inner, inner, u);
         for (int u : owned_leaves) cluster_to(leaf_early, leaf_late, u);
     }
-    rec.insert(rec.end(), na1.begin(), na1.end());
-    interleave(leaf_early, na2);
-    interleave(inner, nb);
-    rec.insert(rec.end(), leaf_late.begin(), leaf_late.end());
+    if (!(getenv("H2B_DIAG_FWD_ONLY") && getenv("H2B_DIAG_FWD_ONLY")[0] == '1')) {  // diagnostics: forward alone
+        rec.insert(rec.end(), na1.begin(), na1.end());
+        interleave(leaf_early, na2);
+        interleave(inner, nb);
+        rec.insert(rec.end(), leaf_late.begin(), leaf_late.end());
+    } else {
+        n_near = n_cpl = 0;
+    }
     int64_t e_bytes_r = 0;
     for (int i = 0; i < L.r_nodes; ++i)
         if (rparent[i] >= 0 && reoff[i] >= 0)
