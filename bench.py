@@ -126,6 +126,31 @@ def dist_env():
     return ws, rank, local
 
 
+
+def ncu_traffic(kernel, path=None):
+    """DRAM bytes (read + write) of one launch of `kernel` from the committed
+    ncu --set full capture (profiles/), or None."""
+    import csv
+    path = path or os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_ncu_full_raw.csv")
+    if not os.path.exists(path):
+        return None
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+    with open(path) as f:
+        rows = list(csv.reader(f))
+    if len(rows) < 3:
+        return None
+    head, units = rows[0], rows[1]
+    try:
+        ik = head.index("Kernel Name")
+        ir, iw = head.index("dram__bytes_read.sum"), head.index("dram__bytes_write.sum")
+    except ValueError:
+        return None
+    for r in rows[2:]:
+        if kernel in r[ik]:
+            return float(r[ir]) * scale.get(units[ir], 1) + float(r[iw]) * scale.get(units[iw], 1)
+    return None
+
+
 def build_problem(cfg, threads):
     """Host setup (untimed): mesh, trees, block tree, GCA basis."""
     from paper_2001_05523_b200 import clustering as C
@@ -286,7 +311,8 @@ def run_ours(args, cfg):
         "gpu_launches": K,
         "roofline": {"bound": "hbm", "kernel": "k_matvec (fused forward + coupling + backward + nearfield)",
                      "achieved": mv_bytes / mean_step / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": mv_bytes / mean_step / 1e9 / pk["hbm_gbs"], "traffic": None,
+                     "frac": mv_bytes / mean_step / 1e9 / pk["hbm_gbs"], "traffic": ncu_traffic("k_matvec"),
+                     "traffic_source": "profiles/r01_ncu_full_raw.csv (ncu --set full, one launch, DRAM read+write bytes)",
                      "algorithmic_bytes": mv_bytes, "kernel_ms": mean_step * 1e3, "peak_source": pk["hbm_src"]},
         "nearfield": {
             "pairs_per_s": fc["pairs"] / nf_time, "pairs": fc["pairs"], "ms": nf_time * 1e3,

@@ -48,7 +48,7 @@ st, en = (tr[:, 0] - t0) / 1e3, (tr[:, 1] - t0) / 1e3
 kind = (tr[:, 2] >> 16) & 0xff
 nclimb = (tr[:, 2] >> 24) & 0xff
 print(f"matvec span {en.max():.1f} us, tasks {tot}")
-for kd, nm in ((2, "forward"), (0, "near"), (1, "coupling"), (3, "descent")):
+for kd, nm in ((2, "forward"), (0, "near"), (1, "coupling"), (3, "descent"), (4, "up"), (5, "down")):
     sel = kind == kd
     if not sel.any():
         continue
