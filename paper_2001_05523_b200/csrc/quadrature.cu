@@ -22,6 +22,12 @@
 
 #include "device_common.cuh"
 
+// tuning knobs of the regular SLP kernel (see launch_slp)
+#ifndef H2B_SLP_UNROLL_OUTER
+#define H2B_SLP_UNROLL_OUTER 16
+#endif
+constexpr int kSlpUnroll = H2B_SLP_UNROLL_OUTER;
+
 namespace h2b {
 namespace {
 
@@ -381,7 +387,7 @@ __device__ __forceinline__ int64_t touch_find(const int64_t* __restrict__ row_pt
 // 1/(4 pi r) = t (3 - p t^2) / (8 sqrt(2) pi)
 constexpr double kSlpFold = 1.0 / (8.0 * 1.4142135623730950488016887 * kPi);
 
-template <int Q, int JC, int MINB>
+template <int Q, int JC, int MINB, int R>
 __global__ void __launch_bounds__(256, MINB) k_blocks_slp(const double* __restrict__ P, int64_t F,
                                                    const int32_t* __restrict__ T,
                                                    const int64_t* __restrict__ jobs,
@@ -469,7 +475,7 @@ __global__ void __launch_bounds__(256, MINB) k_blocks_slp(const double* __restri
             }
         } else {
             double tot = 0.0;
-#pragma unroll
+#pragma unroll kSlpUnroll
             for (int j0 = 0; j0 < Q; j0 += JC) {
                 double y0[JC], y1[JC], y2[JC], yh[JC], yw[JC];
 #pragma unroll
@@ -483,33 +489,36 @@ __global__ void __launch_bounds__(256, MINB) k_blocks_slp(const double* __restri
                         yw[j] = cx[4 * Q * kTile + s];
                     }
                 }
-                // two row points per step: two independent accumulation chains
+                // R row points per step: R independent accumulation chains
+#pragma unroll kSlpUnroll
+                for (int i0 = 0; i0 < Q; i0 += R) {
+                    double xa[R][5], acc[R];
 #pragma unroll
-                for (int i = 0; i < Q; i += 2) {
-                    const bool two = (i + 1 < Q);
-                    const int sa = i * kTile + a, sb = two ? sa + kTile : sa;
-                    const double a0 = rx[sa], a1 = rx[Q * kTile + sa], a2 = rx[2 * Q * kTile + sa];
-                    const double ah = rx[3 * Q * kTile + sa], aw = rx[4 * Q * kTile + sa];
-                    const double b0 = rx[sb], b1 = rx[Q * kTile + sb], b2 = rx[2 * Q * kTile + sb];
-                    const double bh = rx[3 * Q * kTile + sb], bw = rx[4 * Q * kTile + sb];
-                    double acc0 = 0.0, acc1 = 0.0;
+                    for (int r = 0; r < R; ++r) {
+                        const int si = (i0 + r < Q ? i0 + r : Q - 1) * kTile + a;
+#pragma unroll
+                        for (int f = 0; f < 5; ++f) xa[r][f] = rx[f * Q * kTile + si];
+                        acc[r] = 0.0;
+                    }
 #pragma unroll
                     for (int j = 0; j < JC; ++j) {
                         if (j0 + j < Q) {
-                            // p = |x'|^2/2 + |y'|^2/2 - x'.y' = r^2/2, t ~ rsqrt(p);
-                            // one Newton step folded: 1/r ~ t (3 - p t^2) / (2 sqrt 2)
-                            const double pa = fma(a0, y0[j], fma(a1, y1[j], fma(a2, y2[j], ah + yh[j])));
-                            const double ta = rsqrt_seed(pa);
-                            acc0 = fma(yw[j] * ta, fma(-pa, ta * ta, 3.0), acc0);
-                            if (two) {
-                                const double pb = fma(b0, y0[j], fma(b1, y1[j], fma(b2, y2[j], bh + yh[j])));
-                                const double tb = rsqrt_seed(pb);
-                                acc1 = fma(yw[j] * tb, fma(-pb, tb * tb, 3.0), acc1);
+#pragma unroll
+                            for (int r = 0; r < R; ++r) {
+                                if (i0 + r < Q) {
+                                    // p = |x'|^2/2 + |y'|^2/2 - x'.y' = r^2/2, t ~ rsqrt(p);
+                                    // one Newton step folded: 1/r ~ t (3 - p t^2) / (2 sqrt 2)
+                                    const double pa = fma(xa[r][0], y0[j], fma(xa[r][1], y1[j],
+                                                                             fma(xa[r][2], y2[j], xa[r][3] + yh[j])));
+                                    const double ta = rsqrt_seed(pa);
+                                    acc[r] = fma(yw[j] * ta, fma(-pa, ta * ta, 3.0), acc[r]);
+                                }
                             }
                         }
                     }
-                    tot = fma(aw, acc0, tot);
-                    if (two) tot = fma(bw, acc1, tot);
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+                        if (i0 + r < Q) tot = fma(xa[r][4], acc[r], tot);
                 }
             }
             val = tot;
@@ -717,11 +726,21 @@ int alloc_flags(int** d, cudaStream_t st) {
     return ok();
 }
 
-template <int Q, int JC, int MINB = 2>
+#ifndef H2B_SLP9_JC
+#define H2B_SLP9_JC 9
+#endif
+#ifndef H2B_SLP9_MINB
+#define H2B_SLP9_MINB 2
+#endif
+#ifndef H2B_SLP9_R
+#define H2B_SLP9_R 2
+#endif
+
+template <int Q, int JC, int MINB = 2, int R = 2>
 int launch_slp(const h2b_mesh* m, const double* P, const h2b_jobs* jobs, const h2b_touch* t,
                const double* tv, double* out, int* flags, cudaStream_t st) {
     const size_t sm = (size_t)10 * Q * kTile * sizeof(double) + (size_t)8 * kTile * sizeof(int);
-    auto kern = k_blocks_slp<Q, JC, MINB>;
+    auto kern = k_blocks_slp<Q, JC, MINB, R>;
     H2B_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     const int64_t nj = jobs->n_jobs;
     for (int64_t j0 = 0; j0 < nj; j0 += 2147483647LL) {
@@ -881,7 +900,9 @@ extern "C" int h2b_pair_blocks_slp(const h2b_mesh* m, const double* d_panel_poin
     switch (Q) {
         case 1: rc = launch_slp<1, 1>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
         case 4: rc = launch_slp<4, 4>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
-        case 9: rc = launch_slp<9, 9, 2>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
+        case 9: rc = launch_slp<9, H2B_SLP9_JC, H2B_SLP9_MINB, H2B_SLP9_R>(m, d_panel_points, jobs, t, d_touch_values, d_out,
+                                                                        flags, st);
+            break;
         case 16: rc = launch_slp<16, 8>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
         case 25: rc = launch_slp<25, 5>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
         default: rc = fail(H2B_ERR_INVALID, "h2b_pair_blocks_slp: supported regular orders q = 1..5");
