@@ -495,7 +495,10 @@ def _scatter(flat, off, ld, block):
 def _gather_index(n_nodes, row_len, rows, width, coloff, first):
     """Per-row-node gather lists: for every block (row node, width, column
     offset inside the row's matrix) the `width` source indices first[b] + j.
-    Returns (offsets per node, flat int32 indices); padding columns -> 0."""
+    Returns (offsets per node, flat int32 indices).  Padding columns (zero
+    matrix columns) repeat the row's first index: a gather never touches a
+    value nobody produces (the matvec skips x_hat of clusters without far
+    blocks above them)."""
     goff = np.zeros(n_nodes + 1, dtype=np.int64)
     np.cumsum(row_len, out=goff[1:])
     gidx = np.zeros(max(int(goff[-1]), 1), dtype=np.int64)
@@ -504,6 +507,13 @@ def _gather_index(n_nodes, row_len, rows, width, coloff, first):
         blk = np.repeat(np.arange(len(width)), width)
         j = np.arange(total) - np.repeat(np.cumsum(width) - width, width)
         gidx[goff[rows][blk] + coloff[blk] + j] = first[blk] + j
+        real = np.bincount(rows, weights=width, minlength=n_nodes).astype(np.int64)
+        pad = np.asarray(row_len, dtype=np.int64) - real
+        has = np.nonzero((pad > 0) & (real > 0))[0]
+        if len(has):
+            pos = np.repeat(goff[has] + real[has], pad[has]) + (np.arange(int(pad[has].sum())) -
+                                                                 np.repeat(np.cumsum(pad[has]) - pad[has], pad[has]))
+            gidx[pos] = np.repeat(gidx[goff[has]], pad[has])
     return goff[:-1], gidx
 
 

@@ -44,6 +44,8 @@
 // the ticket counter and advances the epoch, so the launch is self-contained
 // and can be captured in a CUDA graph.
 
+#include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -170,10 +172,25 @@ __device__ __forceinline__ bool ll_try(const uint64_t* p, uint32_t epoch, double
     return true;
 }
 
+#ifdef H2B_LL_TIMEOUT
+__device__ unsigned long long g_ll_stuck[4];  // debugging: address / epoch of an abandoned wait
+#endif
 __device__ __forceinline__ double ll_load(const uint64_t* p, uint32_t epoch) {
     double v;
     if (ll_try(p, epoch, v)) return v;
+#ifdef H2B_LL_TIMEOUT
+    for (long long it = 0; !ll_try(p, epoch, v); ++it) {
+        __nanosleep(32);
+        if (it > (1ll << 22)) {
+            g_ll_stuck[0] = reinterpret_cast<unsigned long long>(p);
+            g_ll_stuck[1] = epoch;
+            g_ll_stuck[2] = blockIdx.x;
+            return 0.0;
+        }
+    }
+#else
     while (!ll_try(p, epoch, v)) __nanosleep(32);
+#endif
     return v;
 }
 
@@ -858,6 +875,40 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
     if (smem > 227 * 1024) return fail(H2B_ERR_INVALID, "h2b_plan_create: gathered right-hand side exceeds shared memory");
 
     std::vector<int64_t> rec, fwd_off(L.c_leaves);
+    // Skip the zero work at the top of the trees: x_hat_u is needed only if u
+    // or an ancestor is the column cluster of a far block; v_t is non-zero only
+    // if t or an ancestor has couplings (for the reference geometries the top
+    // levels are all nearfield, e.g. depths 0-3 at config 1).  The forward climb
+    // stops below the first needed level and the downward chain starts there.
+    std::vector<char> need_c(L.c_nodes, 0), hasv(L.r_nodes, 0);
+    {
+        std::vector<int32_t> fptr, fcol;
+        H2B_CUDA_TRY(fetch(L.far_ptr, (int64_t)L.r_nodes + 1, fptr));
+        H2B_CUDA_TRY(fetch(L.far_col, std::max<int64_t>(fptr[L.r_nodes], 0), fcol));
+        for (int32_t c : fcol) need_c[c] = 1;
+        auto top_down = [](int n, const std::vector<int32_t>& parent, std::vector<char>& flag) {
+            std::vector<int> depth(n, -1), idx(n);
+            for (int u = 0; u < n; ++u) {
+                int d = 0;
+                for (int q = parent[u]; q >= 0; q = parent[q]) ++d;
+                depth[u] = d;
+                idx[u] = u;
+            }
+            std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return depth[a] < depth[b]; });
+            for (int u : idx)
+                if (parent[u] >= 0 && flag[parent[u]]) flag[u] = 1;
+        };
+        top_down(L.c_nodes, cparent, need_c);
+        for (int u = 0; u < L.r_nodes; ++u) hasv[u] = (scols[u] > 0 && rrank[u] > 0) ? 1 : 0;
+        top_down(L.r_nodes, rparent, hasv);
+        if (getenv("H2B_DEBUG_PLAN")) {
+            int nc = 0, nv = 0;
+            for (char c : need_c) nc += c;
+            for (char c : hasv) nv += c;
+            fprintf(stderr, "plan: far blocks %d, x_hat needed %d / %d, v_t nonzero %d / %d\n", (int)fcol.size(), nc,
+                    L.c_nodes, nv, L.r_nodes);
+        }
+    }
     // A: forward records (leaf, then the levels it climbs as the right child)
     for (int i = 0; i < L.c_leaves; ++i) {
         const int leaf = leaves[i];
@@ -867,7 +918,7 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
         int node = leaf, n = 0;
         while (true) {
             const int p = cparent[node];
-            if (p < 0 || cchild[2 * p + 1] != node) break;
+            if (p < 0 || cchild[2 * p + 1] != node || !need_c[p]) break;
             const int c0 = cchild[2 * p];
             if (n >= kMaxDepth) return fail(H2B_ERR_INVALID, "h2b_plan_create: tree deeper than 32 levels");
             rec.insert(rec.end(), {crank[c0], crank[p], ceoff[c0], ceoff[node], cxoff[c0], cxoff[p]});
@@ -897,6 +948,7 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
     // (an empty band when u has no couplings) runs u's downward step and goes
     // to `late`.
     auto cluster_to = [&](std::vector<int64_t>& early, std::vector<int64_t>& late, int u) {
+        if (rvoff[u] < 0 && !hasv[u]) return;  // inner cluster with v_t == 0: nothing to do
         const bool cpl = scols[u] > 0 && rrank[u] > 0;
         std::vector<int64_t> tmp;
         int n = cpl ? bands_to(tmp, scols[u], rrank[u], soff[u], sgoff[u], ryoff[u], kKindCpl) : 0;
@@ -907,7 +959,7 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
         }
         n_cpl += n;
         int64_t* last = tmp.data() + tmp.size() - kBandWords;
-        const int par = rparent[u];
+        const int par = (rparent[u] >= 0 && hasv[rparent[u]]) ? rparent[u] : -1;  // v_parent == 0: as a root
         const int64_t d[9] = {rrank[u], par >= 0 ? ryoff[par] : -1, par >= 0 ? rrank[par] : 0,
                               par >= 0 ? reoff[u] : 0, ryoff[u], rvoff[u] >= 0 ? 1 : 0,
                               rvoff[u] >= 0 ? rvoff[u] : 0, rstart[u], rsize[u]};
@@ -1022,6 +1074,21 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
     *out = p;
     return ok();
 }
+
+#ifdef H2B_LL_TIMEOUT
+extern "C" int h2b_debug_stuck(h2b_plan* p, unsigned long long* out) {
+    unsigned long long h[4];
+    H2B_CUDA_TRY(cudaMemcpyFromSymbol(h, g_ll_stuck, sizeof(h)));
+    out[0] = h[0];
+    out[1] = h[1];
+    out[2] = h[2];
+    out[3] = reinterpret_cast<unsigned long long>(p->xhat);
+    out[4] = reinterpret_cast<unsigned long long>(p->ycpl);
+    out[5] = reinterpret_cast<unsigned long long>(p->yfin);
+    out[6] = reinterpret_cast<unsigned long long>(p->ynear);
+    return 0;
+}
+#endif
 
 extern "C" int h2b_plan_destroy(h2b_plan* p) {
     if (!p) return ok();
