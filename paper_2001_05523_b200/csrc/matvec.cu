@@ -72,7 +72,7 @@ constexpr int kBandWords = 24;  // src_off, cols, rows, gidx_off, out_off, is_la
                                 // downward-step record of the band's cluster (coupling bands):
                                 // k, parent y_hat offset (-1 root), k_parent, e_off, y_hat offset,
                                 // is_leaf, v_off, start (size = rows of a leaf)
-constexpr int kFwdHead = 6;     // start, size, k, v_off, xhat_off, n_climb
+constexpr int kFwdHead = 7;     // start, size, k, v_off, xhat_off, n_climb, warp_ok
 constexpr int kFwdLevel = 6;    // k0, kp, e_off_c0, e_off_own, xhat_off_c0, xhat_off_parent
 constexpr int kKindNear = 0, kKindCpl = 1, kKindDescent = 3;  // band record kinds (word 7)
 
@@ -452,6 +452,7 @@ struct Shared {
     double* vb;                // vec_len (vec_len = max rank / leaf size)
     double* red;               // kWarps * 32
     int64_t* rec;              // small record cache
+    const int64_t* rec_src;    // the forward task's record in global memory
     uint32_t parity;           // mbarrier phase of the staging slot in use
     bool issued;               // band bulk copy already issued by the caller
 };
@@ -505,25 +506,103 @@ __device__ __forceinline__ void load_rec(const Shared& s, const int64_t* src, in
     __syncthreads();
 }
 
+// Forward task on one warp (chain latency: no block barriers).  Lane c owns
+// output coefficient c (ranks <= 32), the leaf has <= 64 rows; operands in
+// shared memory, the climb's transfer matrices copied by the warp (cp.async)
+// while the sibling's coefficients are awaited.
+__device__ void forward_warp(const double* __restrict__ c_V, const double* __restrict__ c_E,
+                             const int64_t* __restrict__ col_perm, const double* __restrict__ x, uint64_t* xhat,
+                             uint32_t epoch, const Shared& s) {
+    const int lane = threadIdx.x;
+    const int start = (int)s.rec[0], size = (int)s.rec[1], k = (int)s.rec[2];
+    const int64_t v_off = s.rec[3], xhat_off = s.rec[4];
+    const int n_climb = (int)s.rec[5];
+    const double* V = stage_issue(s, c_V + v_off, ((int64_t)size * k * 8 + 15) & ~int64_t(15));
+    for (int i = kFwdHead + lane; i < kFwdHead + kFwdLevel * n_climb; i += 32) s.rec[i] = __ldg(s.rec_src + i);
+    for (int r = lane; r < size; r += 32) s.va[r] = __ldg(x + __ldg(col_perm + start + r));
+    __syncwarp();
+    {
+        int kk = k;  // pull the climb's transfer matrices into L2
+        for (int j = 0; j < n_climb; ++j) {
+            const int64_t* lv = s.rec + kFwdHead + kFwdLevel * j;
+            const int kp = (int)lv[1];
+            const int64_t b0 = 8 * (int64_t)lv[0] * kp, b1 = 8 * (int64_t)kk * kp;
+            const char* e0 = reinterpret_cast<const char*>(c_E + lv[2]);
+            const char* e1 = reinterpret_cast<const char*>(c_E + lv[3]);
+            for (int64_t o = 128 * lane; o < b0; o += 128 * 32) prefetch_l2(e0 + o);
+            for (int64_t o = 128 * lane; o < b1; o += 128 * 32) prefetch_l2(e1 + o);
+            kk = kp;
+        }
+    }
+    mbar_wait(s.bar, s.parity);
+    double own = 0.0;
+    if (lane < k) {
+        double a0 = 0.0, a1 = 0.0;
+        int r = 0;
+        for (; r + 1 < size; r += 2) {
+            a0 = fma(V[(int64_t)r * k + lane], s.va[r], a0);
+            a1 = fma(V[(int64_t)(r + 1) * k + lane], s.va[r + 1], a1);
+        }
+        if (r < size) a0 = fma(V[(int64_t)r * k + lane], s.va[r], a0);
+        own = a0 + a1;
+        ll_store(xhat + 2 * (xhat_off + lane), own, epoch);
+    }
+    mark(s.mark, 0);
+    double* buf = reinterpret_cast<double*>(s.stage);
+    int k1 = k;
+    for (int j = 0; j < n_climb; ++j) {
+        const int64_t* lv = s.rec + kFwdHead + kFwdLevel * j;
+        const int k0 = (int)lv[0], kp = (int)lv[1];
+        const int n0 = k0 * kp, n1 = k1 * kp;
+        __syncwarp();  // buf / va free
+        const double* E0 = c_E + lv[2];
+        const double* E1 = c_E + lv[3];
+        for (int i = lane; i < n0; i += 32) cp_async8(buf + i, E0 + i);
+        for (int i = lane; i < n1; i += 32) cp_async8(buf + n0 + i, E1 + i);
+        if (lane < k1) s.va[k0 + lane] = own;
+        if (lane < k0) s.va[lane] = ll_load(xhat + 2 * (lv[4] + lane), epoch);
+        cp_async_wait_all();
+        __syncwarp();
+        if (j < 2) mark(s.mark, 1 + 2 * j);
+        own = 0.0;
+        if (lane < kp) {
+            double a0 = 0.0, a1 = 0.0;
+            const int rows = k0 + k1;
+            int r = 0;
+            for (; r + 1 < rows; r += 2) {
+                a0 = fma(buf[r * kp + lane], s.va[r], a0);
+                a1 = fma(buf[(r + 1) * kp + lane], s.va[r + 1], a1);
+            }
+            if (r < rows) a0 = fma(buf[r * kp + lane], s.va[r], a0);
+            own = a0 + a1;
+            ll_store(xhat + 2 * (lv[5] + lane), own, epoch);
+        }
+        if (j < 2) mark(s.mark, 2 + 2 * j);
+        k1 = kp;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // A: forward transform of one column leaf; climb while the right child
 
 __device__ void task_forward(const double* __restrict__ c_V, const double* __restrict__ c_E,
                                        const int64_t* __restrict__ col_perm, const int64_t* rec, const double* __restrict__ x,
                              uint64_t* xhat, uint32_t epoch, const Shared& s) {
-    // header + climb levels in one load
-    const int n_climb_max = kMaxDepth;
-    {
-        const int n = kFwdHead + kFwdLevel * n_climb_max;
-        for (int i = threadIdx.x; i < kFwdHead; i += kThreads) s.rec[i] = __ldg(rec + i);
-        __syncthreads();
+    // header, then (block path) the climb levels
+    for (int i = threadIdx.x; i < kFwdHead; i += kThreads) s.rec[i] = __ldg(rec + i);
+    __syncthreads();
+    const_cast<Shared&>(s).rec_src = rec;
+    if (!s.rec[6]) {
         const int nc = (int)s.rec[5];
-        for (int i = kFwdHead + threadIdx.x; i < kFwdHead + kFwdLevel * nc && i < n; i += kThreads)
-            s.rec[i] = __ldg(rec + i);
+        for (int i = kFwdHead + threadIdx.x; i < kFwdHead + kFwdLevel * nc; i += kThreads) s.rec[i] = __ldg(rec + i);
     }
     const int start = (int)s.rec[0], size = (int)s.rec[1], k = (int)s.rec[2];
     const int64_t v_off = s.rec[3], xhat_off = s.rec[4];
     const int n_climb = (int)s.rec[5];
+    if (s.rec[6]) {  // every rank <= 32 and the leaf <= 64 rows: one warp, no block barriers
+        if (threadIdx.x < 32) forward_warp(c_V, c_E, col_perm, x, xhat, epoch, s);
+        return;
+    }
     const double* V = stage_issue(s, c_V + v_off, ((int64_t)size * k * 8 + 15) & ~int64_t(15));
     for (int r = threadIdx.x; r < size; r += blockDim.x) s.va[r] = __ldg(x + col_perm[start + r]);
     mbar_wait(s.bar, s.parity);
@@ -607,6 +686,56 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
     const int64_t v_off = d[6];
     const int start = (int)d[7];
     double* Es = reinterpret_cast<double*>(s.stage);
+    if (d[10]) {  // (record word 18) ranks <= 32, leaf <= 64 rows: one warp, no block barriers
+        if (threadIdx.x >= 32) return;
+        const int lane = threadIdx.x;
+        const int size = leaf ? (int)d[8] : 0;
+        double* Vt = Es + ((k * kp + 1) & ~1);
+        // E_t^T and V_t^T staged by the warp while the inputs are awaited
+        if (par_off >= 0)
+            for (int i = lane; i < k * kp; i += 32) {
+                const int r = i / kp, c = i - r * kp;
+                cp_async8(Es + c * k + r, r_E + e_off + i);
+            }
+        if (leaf)
+            for (int i = lane; i < size * k; i += 32) {
+                const int r = i / k, c = i - r * k;
+                cp_async8(Vt + c * size + r, r_V + v_off + i);
+            }
+        double v = (has_cpl && lane < k) ? ll_load(ycpl + 2 * (yoff + lane), epoch) : 0.0;
+        if (par_off >= 0 && lane < kp) s.rhs[lane] = ll_load(yfin + 2 * (par_off + lane), epoch);
+        cp_async_wait_all();
+        __syncwarp();
+        mark(s.mark, 4);
+        if (par_off >= 0 && lane < k) {
+            double a0 = 0.0, a1 = 0.0;
+            int c = 0;
+            for (; c + 1 < kp; c += 2) {
+                a0 = fma(Es[c * k + lane], s.rhs[c], a0);
+                a1 = fma(Es[(c + 1) * k + lane], s.rhs[c + 1], a1);
+            }
+            if (c < kp) a0 = fma(Es[c * k + lane], s.rhs[c], a0);
+            v += a0 + a1;
+        }
+        mark(s.mark, 1);
+        if (!leaf) {
+            if (lane < k) ll_store(yfin + 2 * (yoff + lane), v, epoch);
+            return;
+        }
+        if (lane < k) s.vb[lane] = v;
+        __syncwarp();
+        for (int i = lane; i < size; i += 32) {
+            double a0 = 0.0, a1 = 0.0;
+            int r = 0;
+            for (; r + 1 < k; r += 2) {
+                a0 = fma(Vt[r * size + i], s.vb[r], a0);
+                a1 = fma(Vt[(r + 1) * size + i], s.vb[r + 1], a1);
+            }
+            if (r < k) a0 = fma(Vt[r * size + i], s.vb[r], a0);
+            y[__ldg(row_perm + start + i)] = ll_load(ynear + 2 * ((int64_t)start + i), epoch) + (a0 + a1);
+        }
+        return;
+    }
     const bool e_smem = par_off >= 0 && k * kp <= kStageBytes / 8;
     // transfer / leaf basis matrices are staged TRANSPOSED, so that the
     // thread-per-row products below read consecutive words (no bank conflicts)
@@ -913,8 +1042,10 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
     for (int i = 0; i < L.c_leaves; ++i) {
         const int leaf = leaves[i];
         fwd_off[i] = (int64_t)rec.size();
-        rec.insert(rec.end(), {cstart[leaf], csize[leaf], crank[leaf], cvoff[leaf], cxoff[leaf], 0});
+        rec.insert(rec.end(), {cstart[leaf], csize[leaf], crank[leaf], cvoff[leaf], cxoff[leaf], 0, 0});
         const size_t hdr = rec.size() - kFwdHead;
+        bool warp_ok = crank[leaf] <= 32 && csize[leaf] <= 64 &&
+                       (int64_t)csize[leaf] * crank[leaf] * 8 <= kStageBytes;
         int node = leaf, n = 0;
         while (true) {
             const int p = cparent[node];
@@ -922,10 +1053,13 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
             const int c0 = cchild[2 * p];
             if (n >= kMaxDepth) return fail(H2B_ERR_INVALID, "h2b_plan_create: tree deeper than 32 levels");
             rec.insert(rec.end(), {crank[c0], crank[p], ceoff[c0], ceoff[node], cxoff[c0], cxoff[p]});
+            warp_ok = warp_ok && crank[c0] <= 32 && crank[p] <= 32 &&
+                      (int64_t)(crank[c0] + crank[node]) * crank[p] * 8 <= kStageBytes;
             node = p;
             ++n;
         }
         rec[hdr + 5] = n;
+        rec[hdr + 6] = warp_ok ? 1 : 0;
     }
     // B/C: band records; rows per band so one band fits the TMA stage.  Near
     // bands of the owned leaves, then coupling bands of the owned clusters
@@ -969,6 +1103,13 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
         int dd = 0;
         for (int q = rparent[u]; q >= 0; q = rparent[q]) ++dd;
         last[17] = dd;  // depth (diagnostics: trace)
+        {
+            const int kk = rrank[u], kq = par >= 0 ? rrank[par] : 0;
+            const bool lf = rvoff[u] >= 0;
+            last[18] = (kk <= 32 && kq <= 32 && (!lf || rsize[u] <= 64) &&
+                        8 * ((((int64_t)kk * kq + 1) & ~int64_t(1)) + (lf ? (int64_t)rsize[u] * kk : 0)) <= kStageBytes)
+                           ? 1 : 0;  // one-warp downward step
+        }
         early.insert(early.end(), tmp.begin(), tmp.end() - kBandWords);
         late.insert(late.end(), tmp.end() - kBandWords, tmp.end());
     };
@@ -993,6 +1134,8 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
     // The nearfield streams while the forward climb and the downward chain
     // advance.
     double fa1 = 0.2, fa2 = 0.5;
+    // (H2B_EARLY_INNER=1: also move the inner clusters' non-last bands forward; measured neutral)
+    const bool early_inner = getenv("H2B_EARLY_INNER") && getenv("H2B_EARLY_INNER")[0] == '1';
     if (const char* e = getenv("H2B_NEAR_A1")) fa1 = atof(e);
     if (const char* e = getenv("H2B_NEAR_A2")) fa2 = atof(e);
     std::vector<int> owned_leaves;
@@ -1000,7 +1143,7 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
         if (rvoff[u] >= 0) owned_leaves.push_back(u);
     const int nl = (int)owned_leaves.size();
     const int c1 = std::min(nl, (int)(fa1 * nl)), c2 = std::min(nl, c1 + (int)(fa2 * nl));
-    std::vector<int64_t> na1, na2, nb, leaf_early, leaf_late, inner;
+    std::vector<int64_t> na1, na2, nb, leaf_early, leaf_late, inner, inner_early;
     int n_near = 0;
     for (int i = 0; i < nl; ++i) {
         const int u = owned_leaves[i];
@@ -1010,12 +1153,16 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
     const bool diag_near = getenv("H2B_DIAG_NEAR_ONLY") && getenv("H2B_DIAG_NEAR_ONLY")[0] == '1';
     if (!diag_near) {
         for (int u : order)
-            if (rvoff[u] < 0) cluster_to(inner, inner, u);
+            if (rvoff[u] < 0) cluster_to(early_inner ? inner_early : inner, inner, u);
         for (int u : owned_leaves) cluster_to(leaf_early, leaf_late, u);
     }
     if (!(getenv("H2B_DIAG_FWD_ONLY") && getenv("H2B_DIAG_FWD_ONLY")[0] == '1')) {  // diagnostics: forward alone
         rec.insert(rec.end(), na1.begin(), na1.end());
-        interleave(leaf_early, na2);
+        {
+            std::vector<int64_t> prod(leaf_early);  // leaf products first (their x_hat are ready first)
+            prod.insert(prod.end(), inner_early.begin(), inner_early.end());
+            interleave(prod, na2);
+        }
         interleave(inner, nb);
         rec.insert(rec.end(), leaf_late.begin(), leaf_late.end());
     } else {
