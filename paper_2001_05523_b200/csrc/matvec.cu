@@ -1081,11 +1081,40 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
     // Coupling bands of cluster u: all but the last to `early`; the last one
     // (an empty band when u has no couplings) runs u's downward step and goes
     // to `late`.
+    // H2B_DESC_TASKS=1: every coupling band is a pure product and the downward
+    // step of each cluster is its own task (kind kKindDescent)
+    const bool desc_tasks = getenv("H2B_DESC_TASKS") && getenv("H2B_DESC_TASKS")[0] == '1';
     auto cluster_to = [&](std::vector<int64_t>& early, std::vector<int64_t>& late, int u) {
         if (rvoff[u] < 0 && !hasv[u]) return;  // inner cluster with v_t == 0: nothing to do
         const bool cpl = scols[u] > 0 && rrank[u] > 0;
+        const int par = (rparent[u] >= 0 && hasv[rparent[u]]) ? rparent[u] : -1;  // v_parent == 0: as a root
+        int64_t dw[kBandWords] = {0};  // downward-step words 5..18 of a record
+        {
+            const int64_t d[9] = {rrank[u], par >= 0 ? ryoff[par] : -1, par >= 0 ? rrank[par] : 0,
+                                  par >= 0 ? reoff[u] : 0, ryoff[u], rvoff[u] >= 0 ? 1 : 0,
+                                  rvoff[u] >= 0 ? rvoff[u] : 0, rstart[u], rsize[u]};
+            dw[5] = 1;
+            dw[6] = cpl ? 1 : 0;
+            for (int i = 0; i < 9; ++i) dw[8 + i] = d[i];
+            int dd = 0;
+            for (int q = rparent[u]; q >= 0; q = rparent[q]) ++dd;
+            dw[17] = dd;  // depth (diagnostics: trace)
+            const int kk = rrank[u], kq = par >= 0 ? rrank[par] : 0;
+            const bool lf = rvoff[u] >= 0;
+            dw[18] = (kk <= 32 && kq <= 32 && (!lf || rsize[u] <= 64) &&
+                      8 * ((((int64_t)kk * kq + 1) & ~int64_t(1)) + (lf ? (int64_t)rsize[u] * kk : 0)) <= kStageBytes)
+                         ? 1 : 0;  // one-warp downward step
+        }
         std::vector<int64_t> tmp;
         int n = cpl ? bands_to(tmp, scols[u], rrank[u], soff[u], sgoff[u], ryoff[u], kKindCpl) : 0;
+        if (desc_tasks) {
+            early.insert(early.end(), tmp.begin(), tmp.end());
+            std::vector<int64_t> t(dw, dw + kBandWords);
+            t[7] = kKindDescent;
+            late.insert(late.end(), t.begin(), t.end());
+            n_cpl += n + 1;
+            return;
+        }
         if (n == 0) {  // empty band: downward step only
             tmp.insert(tmp.end(), {0, 0, 0, 0, 0, 0, 0, kKindCpl});
             tmp.insert(tmp.end(), kBandWords - 8, 0);
@@ -1093,23 +1122,8 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
         }
         n_cpl += n;
         int64_t* last = tmp.data() + tmp.size() - kBandWords;
-        const int par = (rparent[u] >= 0 && hasv[rparent[u]]) ? rparent[u] : -1;  // v_parent == 0: as a root
-        const int64_t d[9] = {rrank[u], par >= 0 ? ryoff[par] : -1, par >= 0 ? rrank[par] : 0,
-                              par >= 0 ? reoff[u] : 0, ryoff[u], rvoff[u] >= 0 ? 1 : 0,
-                              rvoff[u] >= 0 ? rvoff[u] : 0, rstart[u], rsize[u]};
-        last[5] = 1;
-        last[6] = cpl ? 1 : 0;
-        for (int i = 0; i < 9; ++i) last[8 + i] = d[i];
-        int dd = 0;
-        for (int q = rparent[u]; q >= 0; q = rparent[q]) ++dd;
-        last[17] = dd;  // depth (diagnostics: trace)
-        {
-            const int kk = rrank[u], kq = par >= 0 ? rrank[par] : 0;
-            const bool lf = rvoff[u] >= 0;
-            last[18] = (kk <= 32 && kq <= 32 && (!lf || rsize[u] <= 64) &&
-                        8 * ((((int64_t)kk * kq + 1) & ~int64_t(1)) + (lf ? (int64_t)rsize[u] * kk : 0)) <= kStageBytes)
-                           ? 1 : 0;  // one-warp downward step
-        }
+        for (int i = 5; i < kBandWords; ++i)
+            if (i != 7) last[i] = dw[i];
         early.insert(early.end(), tmp.begin(), tmp.end() - kBandWords);
         late.insert(late.end(), tmp.end() - kBandWords, tmp.end());
     };
@@ -1153,7 +1167,7 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
     const bool diag_near = getenv("H2B_DIAG_NEAR_ONLY") && getenv("H2B_DIAG_NEAR_ONLY")[0] == '1';
     if (!diag_near) {
         for (int u : order)
-            if (rvoff[u] < 0) cluster_to(early_inner ? inner_early : inner, inner, u);
+            if (rvoff[u] < 0) cluster_to(early_inner || desc_tasks ? inner_early : inner, inner, u);
         for (int u : owned_leaves) cluster_to(leaf_early, leaf_late, u);
     }
     if (!(getenv("H2B_DIAG_FWD_ONLY") && getenv("H2B_DIAG_FWD_ONLY")[0] == '1')) {  // diagnostics: forward alone
@@ -1163,7 +1177,24 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
             prod.insert(prod.end(), inner_early.begin(), inner_early.end());
             interleave(prod, na2);
         }
-        interleave(inner, nb);
+        if (const char* e = getenv("H2B_CHAIN_GAP")) {
+            // the downward-chain tasks by depth, a fixed number of near bands
+            // between consecutive depths, the rest of near B after the chain
+            const int64_t gap = atoll(e);
+            const int64_t nt = (int64_t)inner.size() / kBandWords, nn = (int64_t)nb.size() / kBandWords;
+            int64_t f = 0;
+            for (int64_t i = 0; i < nt; ++i) {
+                const int64_t* t = inner.data() + kBandWords * i;
+                rec.insert(rec.end(), t, t + kBandWords);
+                const bool depth_end = i + 1 == nt || inner[kBandWords * (i + 1) + 17] != t[17];
+                if (depth_end)
+                    for (int64_t g = 0; g < gap && f < nn; ++g, ++f)
+                        rec.insert(rec.end(), nb.begin() + kBandWords * f, nb.begin() + kBandWords * (f + 1));
+            }
+            rec.insert(rec.end(), nb.begin() + kBandWords * f, nb.end());
+        } else {
+            interleave(inner, nb);
+        }
         rec.insert(rec.end(), leaf_late.begin(), leaf_late.end());
     } else {
         n_near = n_cpl = 0;
