@@ -626,7 +626,10 @@ class MatvecPlan:
         x = np.ascontiguousarray(x, dtype=np.float64)
         if x.ndim != 1 or len(x) != self.n_cols:
             raise ValueError(f"expected a vector of length {self.n_cols}")
-        y = np.empty(self.n_rows)
+        # the result is written by the kernel straight into page-locked host
+        # memory (torch's caching host allocator: cheap after the first call);
+        # a page-locked x is read in place, a pageable one staged by the library
+        y = t.empty(self.n_rows, dtype=t.float64, pin_memory=True).numpy()
         _lib.check(_lib.lib().h2b_matvec_host(self.handle, _lib.ptr(x), _lib.ptr(y), _lib.stream_ptr()))
         return y
 

@@ -74,6 +74,7 @@ constexpr int kBandWords = 24;  // src_off, cols, rows, gidx_off, out_off, is_la
                                 // is_leaf, v_off, start (size = rows of a leaf)
 constexpr int kFwdHead = 7;     // start, size, k, v_off, xhat_off, n_climb, warp_ok
 constexpr int kFwdLevel = 6;    // k0, kp, e_off_c0, e_off_own, xhat_off_c0, xhat_off_parent
+constexpr int kCopyChunk = 1024;  // x values per copy task (host-input launches)
 constexpr int kKindNear = 0, kKindCpl = 1, kKindDescent = 3;  // band record kinds (word 7)
 
 }  // namespace
@@ -98,6 +99,8 @@ struct h2b_plan {
     double* dx;
     double* dy;
     double* hy;         // pinned host staging of the result (h2b_matvec_host)
+    double* hx;         // pinned host staging of a pageable input
+    uint64_t* xll;      // LL copy of a host input
     unsigned long long* trace;  // optional per-CTA timeline (H2B_TRACE=1)
 };
 
@@ -452,10 +455,17 @@ struct Shared {
     double* vb;                // vec_len (vec_len = max rank / leaf size)
     double* red;               // kWarps * 32
     int64_t* rec;              // small record cache
+    const uint64_t* xll;       // x in LL form (host-input launches) or null: x read directly
     const int64_t* rec_src;    // the forward task's record in global memory
     uint32_t parity;           // mbarrier phase of the staging slot in use
     bool issued;               // band bulk copy already issued by the caller
 };
+
+// x[i]: from the LL copy made by this launch's copy tasks (host input) or
+// directly from device memory
+__device__ __forceinline__ double load_x(const Shared& s, const double* __restrict__ x, int64_t i, uint32_t epoch) {
+    return s.xll ? ll_load(s.xll + 2 * i, epoch) : __ldg(x + i);
+}
 
 // Thread 0 starts staging `bytes` (TMA bulk copy when it fits and is 16-byte
 // aligned; otherwise a plain arrive).  Returns where to read the data from.
@@ -519,7 +529,7 @@ __device__ void forward_warp(const double* __restrict__ c_V, const double* __res
     const int n_climb = (int)s.rec[5];
     const double* V = stage_issue(s, c_V + v_off, ((int64_t)size * k * 8 + 15) & ~int64_t(15));
     for (int i = kFwdHead + lane; i < kFwdHead + kFwdLevel * n_climb; i += 32) s.rec[i] = __ldg(s.rec_src + i);
-    for (int r = lane; r < size; r += 32) s.va[r] = __ldg(x + __ldg(col_perm + start + r));
+    for (int r = lane; r < size; r += 32) s.va[r] = load_x(s, x, __ldg(col_perm + start + r), epoch);
     __syncwarp();
     {
         int kk = k;  // pull the climb's transfer matrices into L2
@@ -604,7 +614,7 @@ __device__ void task_forward(const double* __restrict__ c_V, const double* __res
         return;
     }
     const double* V = stage_issue(s, c_V + v_off, ((int64_t)size * k * 8 + 15) & ~int64_t(15));
-    for (int r = threadIdx.x; r < size; r += blockDim.x) s.va[r] = __ldg(x + col_perm[start + r]);
+    for (int r = threadIdx.x; r < size; r += blockDim.x) s.va[r] = load_x(s, x, col_perm[start + r], epoch);
     mbar_wait(s.bar, s.parity);
     __syncthreads();  // (also: the climb levels are in s.rec)
     {
@@ -812,7 +822,10 @@ __device__ void task_band(const h2b_layout& L, const double* __restrict__ x, con
         if (kCoupling)
             gather_ll(s.rhs, xhat, L.s_gidx + gi_off, cols, epoch);
         else
-            gather(s.rhs, x, L.d_gidx + gi_off, cols);
+            if (s.xll)
+                gather_ll(s.rhs, s.xll, L.d_gidx + gi_off, cols, epoch);
+            else
+                gather(s.rhs, x, L.d_gidx + gi_off, cols);
         mark(s.mark, 1);
         mbar_wait(s.bar, s.parity);
         __syncthreads();
@@ -842,6 +855,9 @@ struct KArgs {
     uint64_t *xhat, *ycpl, *yfin, *ynear;
     unsigned long long* ctrl;
     unsigned long long* trace;
+    const double* xh;  // host-mapped x (h2b_matvec_host) or null
+    uint64_t* xll;     // LL copy of x for host-input launches
+    int n_copy;        // copy tasks (host input)
 };
 
 #ifndef H2B_MINB
@@ -869,7 +885,7 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
         // tickets count on across launches: launch = t / grid (every CTA of a
         // launch takes exactly one ticket before the next launch starts)
         const unsigned long long t = atomicAdd(a.ctrl, 1ull);
-        s_ticket = (int)(t % gridDim.x);
+        s_ticket = (int)(t % gridDim.x) - a.n_copy;  // copy tasks (host input) first: negative
         s_epoch = (uint32_t)(t / gridDim.x) + 1u;
         mbar_init(s.bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -877,6 +893,27 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
     __syncthreads();
     const int ticket = s_ticket;
     const uint32_t epoch = s_epoch;
+    s.xll = a.xh ? a.xll : nullptr;
+    if (ticket < 0) {
+        if (!a.xh) return;
+        // host-input launch: copy a chunk of x from mapped host memory into
+        // the LL form (many loads in flight per thread: the link latency)
+        const int64_t c = ticket + a.n_copy, n = L.n_cols;
+        const int64_t i0 = c * kCopyChunk, i1 = min(n, i0 + kCopyChunk);
+        constexpr int kU = kCopyChunk / kThreads;
+        double v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int64_t i = i0 + u * kThreads + threadIdx.x;
+            v[u] = i < i1 ? a.xh[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int64_t i = i0 + u * kThreads + threadIdx.x;
+            if (i < i1) ll_store(a.xll + 2 * i, v[u], epoch);
+        }
+        return;
+    }
     unsigned long long t_begin = 0;
     if (a.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
     s.mark = a.trace ? a.trace + 8 * ticket + 3 : nullptr;
@@ -887,7 +924,7 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
         // the streaming tasks that follow (fire-and-forget; LL needs no fences)
         prefetch_slice(reinterpret_cast<const double*>(a.rec + a.band_base), a.band_bytes, ticket, L.c_leaves);
         prefetch_slice(reinterpret_cast<const double*>(L.d_gidx), a.dgidx_bytes, ticket, L.c_leaves);
-        prefetch_slice(x, 8 * L.n_cols, ticket, L.c_leaves);
+        if (!a.xh) prefetch_slice(x, 8 * L.n_cols, ticket, L.c_leaves);
         task_forward(L.c_V, L.c_E, L.col_perm, a.rec + __ldg(a.fwd_off + ticket), x, a.xhat, epoch, s);
     } else {
         const int b = ticket - tB;
@@ -1249,6 +1286,9 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
     H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->dx), sizeof(double) * L.n_cols));
     H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->dy), sizeof(double) * L.n_rows));
     H2B_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&p->hy), sizeof(double) * std::max<int64_t>(L.n_rows, 1)));
+    H2B_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&p->hx), sizeof(double) * std::max<int64_t>(L.n_cols, 1)));
+    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->xll), 16 * (size_t)std::max<int64_t>(L.n_cols, 1)));
+    H2B_CUDA_TRY(cudaMemset(p->xll, 0, 16 * (size_t)std::max<int64_t>(L.n_cols, 1)));
     *out = p;
     return ok();
 }
@@ -1270,17 +1310,17 @@ extern "C" int h2b_debug_stuck(h2b_plan* p, unsigned long long* out) {
 
 extern "C" int h2b_plan_destroy(h2b_plan* p) {
     if (!p) return ok();
-    void* bufs[] = {p->xhat, p->ycpl, p->yfin, p->ynear, p->ctrl, p->rec, p->fwd_off, p->dx, p->dy, p->trace};
+    void* bufs[] = {p->xhat, p->ycpl, p->yfin, p->ynear, p->ctrl, p->rec, p->fwd_off, p->dx, p->dy, p->trace, p->xll};
     for (void* q : bufs)
         if (q) cudaFree(q);
     if (p->hy) cudaFreeHost(p->hy);
+    if (p->hx) cudaFreeHost(p->hx);
     delete p;
     return ok();
 }
 
-extern "C" int h2b_matvec(h2b_plan* p, const double* d_x, double* d_y, void* stream) {
-    if (!p || !d_x || !d_y) return fail(H2B_ERR_INVALID, "h2b_matvec: null pointer");
-    cudaStream_t st = as_stream(stream);
+namespace {
+int launch_matvec(h2b_plan* p, const double* d_x, const double* xh, double* y, cudaStream_t st) {
     KArgs a;
     a.L = p->L;
     a.rec = p->rec;
@@ -1299,22 +1339,53 @@ extern "C" int h2b_matvec(h2b_plan* p, const double* d_x, double* d_y, void* str
     a.ynear = p->ynear;
     a.ctrl = p->ctrl;
     a.trace = p->trace;
-    const int grid = p->L.c_leaves + p->n_near + p->n_cpl;
-    k_matvec<<<grid, kThreads, p->smem, st>>>(a, d_x, d_y);
+    a.xh = xh;
+    a.xll = p->xll;
+    // the copy tasks are part of every launch (device input: they return at
+    // once), so all launches of a plan have the same grid -- the ticket
+    // counter's launch index relies on it
+    a.n_copy = (int)((p->L.n_cols + kCopyChunk - 1) / kCopyChunk);
+    const int grid = a.n_copy + p->L.c_leaves + p->n_near + p->n_cpl;
+    k_matvec<<<grid, kThreads, p->smem, st>>>(a, d_x, y);
     H2B_CUDA_TRY(cudaGetLastError());
     return ok();
 }
 
+// device-accessible pointer of pinned (page-locked, mapped) host memory, or null
+const void* mapped(const void* h) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, h) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
+}  // namespace
+
+extern "C" int h2b_matvec(h2b_plan* p, const double* d_x, double* d_y, void* stream) {
+    if (!p || !d_x || !d_y) return fail(H2B_ERR_INVALID, "h2b_matvec: null pointer");
+    return launch_matvec(p, d_x, nullptr, d_y, as_stream(stream));
+}
+
+// Host vectors: the kernel reads x straight from (mapped) pinned host memory
+// -- its first tasks copy it into an LL-form device copy that the other tasks
+// wait on -- and writes y straight into pinned host memory: no separate
+// transfers.  Pageable buffers go through the plan's pinned staging.
 extern "C" int h2b_matvec_host(h2b_plan* p, const double* h_x, double* h_y, void* stream) {
     if (!p || !h_x || !h_y) return fail(H2B_ERR_INVALID, "h2b_matvec_host: null pointer");
     cudaStream_t st = as_stream(stream);
-    H2B_CUDA_TRY(cudaMemcpyAsync(p->dx, h_x, sizeof(double) * p->L.n_cols, cudaMemcpyHostToDevice, st));
-    if (int rc = h2b_matvec(p, p->dx, p->dy, stream)) return rc;
-    // the result lands in pinned staging (full-rate DMA), then one host copy
-    // (a device-to-pageable copy is staged by the driver and costs ~2x)
-    H2B_CUDA_TRY(cudaMemcpyAsync(p->hy, p->dy, sizeof(double) * p->L.n_rows, cudaMemcpyDeviceToHost, st));
+    const double* xh = static_cast<const double*>(mapped(h_x));
+    if (!xh) {
+        std::memcpy(p->hx, h_x, sizeof(double) * p->L.n_cols);
+        xh = static_cast<const double*>(mapped(p->hx));
+    }
+    double* yh = static_cast<double*>(const_cast<void*>(mapped(h_y)));
+    const bool staged_y = yh == nullptr;
+    if (staged_y) yh = static_cast<double*>(const_cast<void*>(mapped(p->hy)));
+    if (!xh || !yh) return fail(H2B_ERR_CUDA, "h2b_matvec_host: pinned staging is not device-mapped");
+    if (int rc = launch_matvec(p, nullptr, xh, yh, st)) return rc;
     H2B_CUDA_TRY(cudaStreamSynchronize(st));
-    std::memcpy(h_y, p->hy, sizeof(double) * p->L.n_rows);
+    if (staged_y) std::memcpy(h_y, p->hy, sizeof(double) * p->L.n_rows);
     return ok();
 }
 
