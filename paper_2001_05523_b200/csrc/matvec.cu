@@ -1203,8 +1203,23 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
     }
     const bool diag_near = getenv("H2B_DIAG_NEAR_ONLY") && getenv("H2B_DIAG_NEAR_ONLY")[0] == '1';
     if (!diag_near) {
+        // H2B_DEPTH_MAJOR=1: inner clusters breadth first, each cluster's
+        // products right before its downward step
+        const bool depth_major = getenv("H2B_DEPTH_MAJOR") && getenv("H2B_DEPTH_MAJOR")[0] == '1';
+        std::vector<int> inner_order;
         for (int u : order)
-            if (rvoff[u] < 0) cluster_to(early_inner || desc_tasks ? inner_early : inner, inner, u);
+            if (rvoff[u] < 0) inner_order.push_back(u);
+        if (depth_major) {
+            std::vector<int> dep(L.r_nodes, 0);
+            for (int u : inner_order) {
+                int dd = 0;
+                for (int q = rparent[u]; q >= 0; q = rparent[q]) ++dd;
+                dep[u] = dd;
+            }
+            std::stable_sort(inner_order.begin(), inner_order.end(), [&](int a2, int b2) { return dep[a2] < dep[b2]; });
+        }
+        for (int u : inner_order)
+            cluster_to(!depth_major && (early_inner || desc_tasks) ? inner_early : inner, inner, u);
         for (int u : owned_leaves) cluster_to(leaf_early, leaf_late, u);
     }
     if (!(getenv("H2B_DIAG_FWD_ONLY") && getenv("H2B_DIAG_FWD_ONLY")[0] == '1')) {  // diagnostics: forward alone
