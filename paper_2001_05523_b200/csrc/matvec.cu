@@ -87,7 +87,7 @@ struct h2b_plan {
     uint64_t* ycpl;     // LL: 2 x yhat_len (coupling part of y_hat)
     uint64_t* yfin;     // LL: 2 x yhat_len (final y_hat of inner clusters)
     uint64_t* ynear;    // LL: 2 x n_rows (permuted order)
-    unsigned long long* ctrl;  // ticket counter (monotonic over launches)
+    unsigned long long* ctrl;  // ticket counters (device / host input), monotonic over launches
     int64_t* rec;       // task records
     int64_t* fwd_off;   // per column leaf: record offset
     int64_t band_base;  // record offset of band 0
@@ -884,9 +884,12 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
     if (threadIdx.x == 0) {
         // tickets count on across launches: launch = t / grid (every CTA of a
         // launch takes exactly one ticket before the next launch starts)
-        const unsigned long long t = atomicAdd(a.ctrl, 1ull);
+        // device- and host-input launches count on separate counters (their
+        // grids differ by the copy tasks); epochs stay unique: odd / even
+        const int host = a.xh != nullptr;
+        const unsigned long long t = atomicAdd(a.ctrl + host, 1ull);
         s_ticket = (int)(t % gridDim.x) - a.n_copy;  // copy tasks (host input) first: negative
-        s_epoch = (uint32_t)(t / gridDim.x) + 1u;
+        s_epoch = 2u * (uint32_t)(t / gridDim.x) + 1u + (uint32_t)host;
         mbar_init(s.bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -1282,8 +1285,8 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
     H2B_CUDA_TRY(cudaMemset(p->xhat, 0, 16 * (size_t)L.xhat_len));
     H2B_CUDA_TRY(cudaMemset(p->ycpl, 0, 16 * (size_t)L.yhat_len));
     H2B_CUDA_TRY(cudaMemset(p->ynear, 0, 16 * (size_t)L.n_rows));
-    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->ctrl), sizeof(unsigned long long)));
-    H2B_CUDA_TRY(cudaMemset(p->ctrl, 0, sizeof(unsigned long long)));
+    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->ctrl), 2 * sizeof(unsigned long long)));
+    H2B_CUDA_TRY(cudaMemset(p->ctrl, 0, 2 * sizeof(unsigned long long)));
     H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->rec), sizeof(int64_t) * std::max<size_t>(1, rec.size())));
     H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->fwd_off), sizeof(int64_t) * fwd_off.size()));
     if (!rec.empty())
@@ -1356,10 +1359,7 @@ int launch_matvec(h2b_plan* p, const double* d_x, const double* xh, double* y, c
     a.trace = p->trace;
     a.xh = xh;
     a.xll = p->xll;
-    // the copy tasks are part of every launch (device input: they return at
-    // once), so all launches of a plan have the same grid -- the ticket
-    // counter's launch index relies on it
-    a.n_copy = (int)((p->L.n_cols + kCopyChunk - 1) / kCopyChunk);
+    a.n_copy = xh ? (int)((p->L.n_cols + kCopyChunk - 1) / kCopyChunk) : 0;
     const int grid = a.n_copy + p->L.c_leaves + p->n_near + p->n_cpl;
     k_matvec<<<grid, kThreads, p->smem, st>>>(a, d_x, y);
     H2B_CUDA_TRY(cudaGetLastError());

@@ -165,3 +165,21 @@ def test_row_sharded_plans_reproduce_single_gpu_bitwise(cfg0):
             op.apply(x, y)
         assert not torch.isnan(y).any()
         assert torch.equal(y, y_ref), world
+
+
+def test_host_vectors_pinned_pageable_device_agree(cfg0):
+    """h2b_matvec_host reads x in place when it is page-locked (else through
+    the plan's staging) and writes y into page-locked memory: all paths give
+    the device result bit for bit, in any interleaving of launches."""
+    import torch
+
+    g, m, t0, bt, b, H = cfg0
+    x = np.random.default_rng(11).standard_normal(H.shape[1])
+    xp = torch.from_numpy(x.copy()).pin_memory().numpy()
+    y_dev = H.matvec(torch.from_numpy(x).cuda()).cpu().numpy()
+    for _ in range(2):
+        y_page = H.matvec(x)
+        y_pin = H.matvec(xp)
+        assert isinstance(y_page, np.ndarray) and isinstance(y_pin, np.ndarray)
+        assert np.array_equal(y_page, y_dev) and np.array_equal(y_pin, y_dev)
+        assert np.array_equal(H.matvec(torch.from_numpy(x).cuda()).cpu().numpy(), y_dev)
