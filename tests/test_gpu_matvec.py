@@ -183,3 +183,53 @@ def test_host_vectors_pinned_pageable_device_agree(cfg0):
         assert isinstance(y_page, np.ndarray) and isinstance(y_pin, np.ndarray)
         assert np.array_equal(y_page, y_dev) and np.array_equal(y_pin, y_dev)
         assert np.array_equal(H.matvec(torch.from_numpy(x).cuda()).cpu().numpy(), y_dev)
+
+
+def _h2_on(level, leaf, eta=2.0, m=3, kind="slp"):
+    from paper_2001_05523_b200 import clustering as C
+    from paper_2001_05523_b200 import gca
+    from paper_2001_05523_b200.containers import AssemblyContext
+
+    mesh = sphere(level)
+    t0, t1 = trees(mesh, leaf)
+    ctx = AssemblyContext(mesh)
+    if kind == "slp":
+        b = gca.build_basis(ctx, t0, gca.P0_SLP, m, 1e-4, threads=4)
+        bt = C.BlockTree(t0, t0, eta)
+        return bt, b, b, gca.assemble_h2(ctx, "slp", bt, b, b, 3, q_singular=4)
+    rb = gca.build_basis(ctx, t0, gca.P0_SLP, m, 1e-4, threads=4)
+    cb = gca.build_basis(ctx, t1, gca.P1_DLP, m, 1e-4, threads=4)
+    bt = C.BlockTree(t0, t1, eta)
+    return bt, rb, cb, gca.assemble_h2(ctx, "dlp", bt, rb, cb, 3, q_singular=4)
+
+
+def _vs_oracle(bt, rb, cb, H, rng):
+    ot_r, ot_c = oracle_tree(bt.row_tree), oracle_tree(bt.col_tree)
+    S = [s for _, s in H.far]
+    Dn = [d for _, d in H.near]
+    for _ in range(2):
+        x = rng.uniform(-1, 1, H.shape[1])
+        ref = OH.matvec(ot_r, ot_c, rb.V, rb.E, rb.rank, cb.V, cb.E, cb.rank, bt.far_uids, S, bt.near_uids, Dn, x)
+        assert rel(H.matvec(x), ref) < 1e-13
+
+
+def test_all_nearfield_operator(rng):
+    """Edge case: one leaf, no far blocks (every transform level pruned):
+    y = D x exactly."""
+    bt, rb, cb, H = _h2_on(1, 64)
+    assert len(bt.far_uids) == 0
+    _vs_oracle(bt, rb, cb, H, rng)
+
+
+def test_deep_ragged_tree(rng):
+    """Edge case: tiny leaves (deep, ragged cluster tree) -- long forward climbs
+    and downward chains, clusters of every size."""
+    bt, rb, cb, H = _h2_on(4, 5, eta=1.5)
+    assert len(bt.far_uids) > 0
+    _vs_oracle(bt, rb, cb, H, rng)
+
+
+def test_dlp_distinct_row_column_trees(rng):
+    """P0 rows x P1 columns: different row and column trees, separately pruned."""
+    bt, rb, cb, H = _h2_on(3, 16, kind="dlp")
+    _vs_oracle(bt, rb, cb, H, rng)
