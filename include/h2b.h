@@ -157,6 +157,22 @@ int h2b_pair_blocks_dlp(const h2b_mesh* m, const double* d_panel_points, const d
                         int32_t Q, const h2b_dlp_jobs* jobs, const h2b_touch* t,
                         const double* d_touch_values, double* d_out, void* stream);
 
+/* Host-side DLP job builder for h2b_pair_blocks_dlp (replaces the Python
+ * construction of the column-panel sets of kernels.py:448-468; identical
+ * output).  Blocks: rows[row_ptr[b]:row_ptr[b+1]] (panel ids),
+ * cols[col_ptr[b]:col_ptr[b+1]] (vertex ids), out_off[b], ld[b]; mesh
+ * vertex->triangle CSR (vptr, vidx) and triangles (n x 3).  The result is
+ * read with h2b_dlp_jobs_sizes / h2b_dlp_jobs_copy and released with
+ * h2b_dlp_jobs_free. */
+typedef struct h2b_dlp_build h2b_dlp_build;
+int h2b_dlp_jobs_build(int64_t n_verts, const int64_t* vptr, const int64_t* vidx, const int64_t* tris,
+                       int64_t n_blocks, const int64_t* row_ptr, const int64_t* rows, const int64_t* col_ptr,
+                       const int64_t* cols, const int64_t* out_off, const int64_t* ld, h2b_dlp_build** out);
+int h2b_dlp_jobs_sizes(const h2b_dlp_build* b, int64_t* sizes);
+int h2b_dlp_jobs_copy(const h2b_dlp_build* b, int64_t* jobs, int32_t* row_idx, int32_t* pan_idx, int32_t* inc_ptr,
+                      int32_t* inc, int64_t* inc_base);
+int h2b_dlp_jobs_free(h2b_dlp_build* b);
+
 /* ============================ H^2 matvec (device) ========================== */
 
 /* Packed operator layout (all device pointers; int32 unless noted).

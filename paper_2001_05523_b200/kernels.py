@@ -216,6 +216,48 @@ def run_slp_jobs(dmesh, q, jobs, row_idx, col_idx, table, out):
 
 
 def build_dlp_jobs(mesh, blocks):
+    """DLP jobs for dense blocks (row panels, column vertices, out_off, ld),
+    built natively (h2b_dlp_jobs_build); same output as _build_dlp_jobs_py."""
+    blocks = list(blocks)
+    if not blocks:
+        return None
+    vptr, vidx = mesh.vertex_triangle_csr()
+    tris = np.ascontiguousarray(mesh.triangles, dtype=np.int64)
+    rows = [np.asarray(b[0], dtype=np.int64) for b in blocks]
+    cols = [np.asarray(b[1], dtype=np.int64) for b in blocks]
+    row_ptr = np.zeros(len(blocks) + 1, dtype=np.int64)
+    np.cumsum([len(r) for r in rows], out=row_ptr[1:])
+    col_ptr = np.zeros(len(blocks) + 1, dtype=np.int64)
+    np.cumsum([len(c) for c in cols], out=col_ptr[1:])
+    R = np.concatenate(rows) if row_ptr[-1] else np.zeros(1, dtype=np.int64)
+    Cc = np.concatenate(cols) if col_ptr[-1] else np.zeros(1, dtype=np.int64)
+    off = np.array([b[2] for b in blocks], dtype=np.int64)
+    ld = np.array([b[3] for b in blocks], dtype=np.int64)
+    vptr = np.ascontiguousarray(vptr, dtype=np.int64)
+    vidx = np.ascontiguousarray(vidx, dtype=np.int64)
+    L = _lib.lib()
+    h = ctypes.c_void_p()
+    _lib.check(L.h2b_dlp_jobs_build(mesh.n_vertices, _lib.ptr(vptr), _lib.ptr(vidx), _lib.ptr(tris), len(blocks),
+                                    _lib.ptr(row_ptr), _lib.ptr(R), _lib.ptr(col_ptr), _lib.ptr(Cc), _lib.ptr(off),
+                                    _lib.ptr(ld), ctypes.byref(h)))
+    try:
+        sz = np.zeros(6, dtype=np.int64)
+        _lib.check(L.h2b_dlp_jobs_sizes(h, _lib.ptr(sz)))
+        if sz[0] == 0:
+            return None
+        out = dict(jobs=np.empty((sz[0], 8), dtype=np.int64), row_idx=np.empty(sz[1], dtype=np.int32),
+                   pan_idx=np.empty(sz[2], dtype=np.int32), inc_ptr=np.empty(sz[3], dtype=np.int32),
+                   inc=np.empty(max(sz[4], 1), dtype=np.int32), inc_base=np.empty(sz[5], dtype=np.int64))
+        if sz[4] == 0:
+            out["inc"][:] = 0
+        _lib.check(L.h2b_dlp_jobs_copy(h, *(_lib.ptr(out[k]) for k in
+                                            ("jobs", "row_idx", "pan_idx", "inc_ptr", "inc", "inc_base"))))
+        return out
+    finally:
+        L.h2b_dlp_jobs_free(h)
+
+
+def _build_dlp_jobs_py(mesh, blocks):
     """DLP jobs for dense blocks (row panels, column vertices, out_off, ld):
     the column-panel set of each job is the sorted union of the panels incident
     to its column vertices (kernels.py:454), tiled so that a job holds at most

@@ -124,3 +124,31 @@ def test_library_exports_every_declared_symbol():
     assert "empty" in _lib.last_error()
     rc = L.h2b_plan_create(None, ctypes.byref(ctypes.c_void_p()))
     assert rc == _lib.H2B_ERR_INVALID
+
+
+def test_native_dlp_job_builder_matches_restatement():
+    """h2b_dlp_jobs_build (C++) == the Python restatement of the column-panel
+    tiling, element for element: near blocks of a P0 x P1 block tree plus
+    ragged and single-vertex blocks."""
+    import numpy as np
+
+    from paper_2001_05523_b200 import clustering as C, kernels, spaces
+    from paper_2001_05523_b200.containers import near_layout
+    from paper_2001_05523_b200.mesh import sphere_mesh
+
+    m = sphere_mesh(4)
+    t_r = C.build_cluster_tree(spaces.DofSpace(spaces.P0, m).support_boxes(), 32)
+    t_c = C.build_cluster_tree(spaces.DofSpace(spaces.P1, m).support_boxes(), 32)
+    bt = C.BlockTree(t_r, t_c, 2.0)
+    nl = near_layout(bt)
+    blocks = [(t_r.perm[t_r.start[t] : t_r.end[t]], t_c.perm[t_c.start[s] : t_c.end[s]], int(nl.blk_off[i]),
+               int(nl.blk_ld[i])) for i, (t, s) in enumerate(bt.near_uids)]
+    rng = np.random.default_rng(0)
+    blocks.append((np.arange(70), rng.permutation(m.n_vertices)[:130], 5, 130))  # > one tile both ways
+    blocks.append((np.array([3]), np.array([7]), 0, 1))
+    a = kernels.build_dlp_jobs(m, blocks)
+    b = kernels._build_dlp_jobs_py(m, blocks)
+    assert set(a) == set(b)
+    for k in a:
+        assert a[k].dtype == b[k].dtype and np.array_equal(a[k], b[k]), k
+    assert kernels.build_dlp_jobs(m, []) is None
