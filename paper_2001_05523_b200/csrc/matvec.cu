@@ -559,32 +559,43 @@ __device__ void forward_warp(const double* __restrict__ c_V, const double* __res
     }
     mark(s.mark, 0);
     double* buf = reinterpret_cast<double*>(s.stage);
+    uint32_t par = s.parity ^ 1u;  // the staging barrier's next phase (V used one)
     int k1 = k;
     for (int j = 0; j < n_climb; ++j) {
         const int64_t* lv = s.rec + kFwdHead + kFwdLevel * j;
         const int k0 = (int)lv[0], kp = (int)lv[1];
-        const int n0 = k0 * kp, n1 = k1 * kp;
+        // E_c0 and E_own by two TMA bulk copies (blocks are 16-byte aligned and
+        // padded to an even length; the warp path is taken only when both fit)
+        const int p0 = (k0 * kp + 1) & ~1, p1 = (k1 * kp + 1) & ~1;
         __syncwarp();  // buf / va free
-        const double* E0 = c_E + lv[2];
-        const double* E1 = c_E + lv[3];
-        for (int i = lane; i < n0; i += 32) cp_async8(buf + i, E0 + i);
-        for (int i = lane; i < n1; i += 32) cp_async8(buf + n0 + i, E1 + i);
+        if (lane == 0) {
+            mbar_expect_tx(s.bar, (uint32_t)(8 * (p0 + p1)));
+            bulk_g2s(buf, c_E + lv[2], (uint32_t)(8 * p0), s.bar);
+            bulk_g2s(buf + p0, c_E + lv[3], (uint32_t)(8 * p1), s.bar);
+        }
         if (lane < k1) s.va[k0 + lane] = own;
         if (lane < k0) s.va[lane] = ll_load(xhat + 2 * (lv[4] + lane), epoch);
-        cp_async_wait_all();
+        mbar_wait(s.bar, par);
+        par ^= 1u;
         __syncwarp();
         if (j < 2) mark(s.mark, 1 + 2 * j);
         own = 0.0;
         if (lane < kp) {
-            double a0 = 0.0, a1 = 0.0;
-            const int rows = k0 + k1;
+            const double* e1 = buf + p0;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
             int r = 0;
-            for (; r + 1 < rows; r += 2) {
+            for (; r + 1 < k0; r += 2) {
                 a0 = fma(buf[r * kp + lane], s.va[r], a0);
                 a1 = fma(buf[(r + 1) * kp + lane], s.va[r + 1], a1);
             }
-            if (r < rows) a0 = fma(buf[r * kp + lane], s.va[r], a0);
-            own = a0 + a1;
+            if (r < k0) a0 = fma(buf[r * kp + lane], s.va[r], a0);
+            r = 0;
+            for (; r + 1 < k1; r += 2) {
+                a2 = fma(e1[r * kp + lane], s.va[k0 + r], a2);
+                a3 = fma(e1[(r + 1) * kp + lane], s.va[k0 + r + 1], a3);
+            }
+            if (r < k1) a2 = fma(e1[r * kp + lane], s.va[k0 + r], a2);
+            own = (a0 + a1) + (a2 + a3);
             ll_store(xhat + 2 * (lv[5] + lane), own, epoch);
         }
         if (j < 2) mark(s.mark, 2 + 2 * j);
@@ -1094,7 +1105,8 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
             if (n >= kMaxDepth) return fail(H2B_ERR_INVALID, "h2b_plan_create: tree deeper than 32 levels");
             rec.insert(rec.end(), {crank[c0], crank[p], ceoff[c0], ceoff[node], cxoff[c0], cxoff[p]});
             warp_ok = warp_ok && crank[c0] <= 32 && crank[p] <= 32 &&
-                      (int64_t)(crank[c0] + crank[node]) * crank[p] * 8 <= kStageBytes;
+                      8 * ((((int64_t)crank[c0] * crank[p] + 1) & ~int64_t(1)) +
+                           (((int64_t)crank[node] * crank[p] + 1) & ~int64_t(1))) <= kStageBytes;
             node = p;
             ++n;
         }
