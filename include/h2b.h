@@ -104,6 +104,10 @@ typedef struct {
     const int32_t* d_info;    /* code | perm_a << 2 | perm_b << 8 (2 bits/idx) */
     const int32_t* d_case_list; /* n_pairs pair ids grouped by case          */
     const int64_t* h_case_off;  /* 4: start of identical/edge/vertex/end in case_list */
+    /* optional (NULL if absent, see h2b_touch_half): one pair id per unordered
+     * touching pair {a, b} (a < b; identical pairs once), grouped by case */
+    const int32_t* d_half_list;
+    const int64_t* h_half_off;  /* 4: segment starts in d_half_list + end */
 } h2b_touch;
 
 /* Pass 1: per row panel touching count -> exclusive scan in d_row_ptr (F+1),
@@ -114,6 +118,13 @@ int h2b_touch_count(const h2b_mesh* m, int64_t* d_row_ptr, int64_t* h_case_count
 int h2b_touch_fill(const h2b_mesh* m, const int64_t* d_row_ptr, const int64_t* h_case_count,
                    int32_t* d_col, int32_t* d_info, int32_t* d_case_list, void* stream);
 
+/* Pass 3 (optional): the unordered-pair list of the symmetric single-layer
+ * table.  Every touching relation is symmetric, so the edge and vertex
+ * segments hold exactly half of the ordered pairs (checked; H2B_ERR_INVALID
+ * otherwise).  d_half_list: n_identical + (n_edge + n_vertex) / 2 entries,
+ * h_half_off[4] receives its segment offsets.  Synchronises. */
+int h2b_touch_half(const h2b_touch* t, int32_t* d_half_list, int64_t* h_half_off, void* stream);
+
 typedef struct {
     int64_t n;         /* number of rule points */
     const double* d_p; /* n x 4: (u1, v1, u2, v2) */
@@ -122,18 +133,26 @@ typedef struct {
 
 /* Sauter-Schwab integrals of every touching pair.  rules[0..2] = identical,
  * edge, vertex rules (quadrature.sauter_schwab_rule).  values: n_pairs (SLP)
- * or n_pairs x 3 (DLP, original local vertex order of the column panel). */
+ * or n_pairs x 3 (DLP, original local vertex order of the column panel).
+ * SLP with t->d_half_list set: each unordered pair is integrated once (the
+ * reference symmetrises edge/vertex pairs over both orientations,
+ * kernels.py:303-309, so G(a,b) = G(b,a)) and written to both ordered ids. */
 int h2b_singular(const h2b_mesh* m, const h2b_touch* t, int kind, const h2b_rule* rules,
                  double* d_values, void* stream);
 
 typedef struct {
     int64_t n_jobs;
-    const int64_t* d_jobs;    /* n_jobs x 6: row_off, n_rows, col_off, n_cols, out_off, out_ld */
+    const int64_t* d_jobs;    /* n_jobs x 8: row_off, n_rows, col_off, n_cols, out_off, out_ld,
+                               * mirror_off, mirror_ld (mirror_off = -1: none) */
     const int32_t* d_row_idx; /* row panels */
     const int32_t* d_col_idx; /* column panels (SLP) */
 } h2b_jobs;
 
 /* Dense SLP blocks out[out_off + r*ld + c] = G(row_idx[row_off+r], col_idx[col_off+c]).
+ * Mirrored jobs (symmetric single-layer matrix, G(a,b) = G(b,a)) also write
+ * out[mirror_off + c*mirror_ld + r]; a job whose mirror_off == out_off is a
+ * diagonal tile (same rows and columns) and only its upper triangle is
+ * integrated.
  * Regular pairs: tensor rule with Q points per panel (panel_points).  Touching
  * pairs: value from the singular table (t != NULL) or, when t == NULL
  * (require_disjoint), the call fails with H2B_ERR_TOUCHING.  Synchronises. */

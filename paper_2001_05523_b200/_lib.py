@@ -47,6 +47,7 @@ class Touch(ctypes.Structure):
     _fields_ = [
         ("n_panels", ctypes.c_int64), ("n_pairs", ctypes.c_int64),
         ("d_row_ptr", vp), ("d_col", vp), ("d_info", vp), ("d_case_list", vp), ("h_case_off", vp),
+        ("d_half_list", vp), ("h_half_off", vp),
     ]
 
 
@@ -87,7 +88,7 @@ class Layout(ctypes.Structure):
 # every symbol include/h2b.h declares (checked by the CPU test-suite)
 EXPORTS = (
     "h2b_last_error", "h2b_abi_version", "h2b_cluster_tree", "h2b_block_tree", "h2b_panel_points",
-    "h2b_touch_count", "h2b_touch_fill", "h2b_singular", "h2b_pair_blocks_slp", "h2b_pair_blocks_dlp",
+    "h2b_touch_count", "h2b_touch_fill", "h2b_touch_half", "h2b_singular", "h2b_pair_blocks_slp", "h2b_pair_blocks_dlp",
     "h2b_plan_create", "h2b_plan_destroy", "h2b_matvec", "h2b_matvec_host",
     "h2b_diagonal", "h2b_plan_trace", "h2b_dlp_jobs_build", "h2b_dlp_jobs_sizes", "h2b_dlp_jobs_copy",
     "h2b_dlp_jobs_free",
@@ -116,6 +117,7 @@ def lib():
         L.h2b_panel_points.argtypes = [ctypes.POINTER(Mesh), vp, vp, ctypes.c_int32, vp, vp]
         L.h2b_touch_count.argtypes = [ctypes.POINTER(Mesh), vp, vp, vp]
         L.h2b_touch_fill.argtypes = [ctypes.POINTER(Mesh), vp, vp, vp, vp, vp, vp]
+        L.h2b_touch_half.argtypes = [ctypes.POINTER(Touch), vp, vp, vp]
         L.h2b_singular.argtypes = [ctypes.POINTER(Mesh), ctypes.POINTER(Touch), ctypes.c_int,
                                    ctypes.POINTER(Rule), vp, vp]
         L.h2b_pair_blocks_slp.argtypes = [ctypes.POINTER(Mesh), vp, ctypes.c_int32, ctypes.POINTER(Jobs),

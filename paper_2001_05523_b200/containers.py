@@ -205,6 +205,26 @@ def _near_blocks(bt, lay):
     ]
 
 
+def _symmetric_trees(bt):
+    rt, ct = bt.row_tree, bt.col_tree
+    return rt is ct or (np.array_equal(rt.perm, ct.perm) and np.array_equal(rt.start, ct.start)
+                        and np.array_equal(rt.end, ct.end))
+
+
+def near_slp_jobs(bt):
+    """Pair-block jobs of the single-layer nearfield.  With one tree on both
+    sides the matrix is symmetric (G(a,b) = G(b,a) for P0 x P0, and the
+    Sauter-Schwab values are symmetrised, kernels.py:303-309): block (s, t) is
+    written as the mirror of block (t, s) and diagonal blocks integrate their
+    upper triangle only."""
+    lay = near_layout(bt)
+    rt, ct = bt.row_tree, bt.col_tree
+    nu = bt.near_uids
+    jobs = np.stack([rt.start[nu[:, 0]], lay.blk_rows, ct.start[nu[:, 1]], lay.blk_cols, lay.blk_off, lay.blk_ld],
+                    axis=1)
+    return kernels.mirror_jobs(jobs, nu) if _symmetric_trees(bt) else jobs
+
+
 def assemble_nearfield_device(ctx, kind, bt, q, q_singular=None, cache=None):
     """Packed device nearfield D (see module docstring)."""
     qs = q if q_singular is None else q_singular
@@ -215,9 +235,7 @@ def assemble_nearfield_device(ctx, kind, bt, q, q_singular=None, cache=None):
     out = D.zeros((max(lay.total, 1),))
     if kind == kernels.SLP:
         rt, ct = bt.row_tree, bt.col_tree
-        nu = bt.near_uids
-        jobs = np.stack([rt.start[nu[:, 0]], lay.blk_rows, ct.start[nu[:, 1]], lay.blk_cols, lay.blk_off,
-                         lay.blk_ld], axis=1)
+        jobs = near_slp_jobs(bt)
         kernels.run_slp_jobs(ctx.dmesh, q, jobs, rt.perm.astype(np.int32), ct.perm.astype(np.int32),
                              ctx.singular_table(kind, qs), out)
     else:
@@ -263,6 +281,9 @@ def assemble_couplings(ctx, kind, bt, row_basis, col_basis, q):
         if kind == kernels.SLP:
             jobs = np.stack([roff[fu[:, 0]], lay.blk_rows, coff[fu[:, 1]], lay.blk_cols, lay.blk_off, lay.blk_ld],
                             axis=1)
+            if row_basis is col_basis and _symmetric_trees(bt):
+                # S_(s,t) = G[piv_s, piv_t] = S_(t,s)^T: one job per block pair
+                jobs = kernels.mirror_jobs(jobs, fu)
             kernels.run_slp_jobs(ctx.dmesh, q, jobs, rpiv.astype(np.int32), cpiv.astype(np.int32), None, out)
         else:
             blocks = [(rpiv[roff[t] : roff[t + 1]], cpiv[coff[s] : coff[s + 1]], int(lay.blk_off[i]),

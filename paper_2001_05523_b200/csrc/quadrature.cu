@@ -191,6 +191,12 @@ __global__ void k_touch_fill(const int32_t* __restrict__ T, int64_t F,
     }
 }
 
+// unordered touching pairs (a < b) of the edge and vertex segments
+__global__ void k_touch_half(const int64_t* __restrict__ row_ptr, int64_t F, const int32_t* __restrict__ col,
+                             const int32_t* __restrict__ info, const int32_t* __restrict__ case_list,
+                             int64_t lo, int64_t hi, int32_t* __restrict__ half,
+                             unsigned long long* __restrict__ cursor);
+
 // ----------------------------------------------------------------------------
 // Sauter-Schwab integrals
 struct SegDesc {
@@ -225,7 +231,7 @@ __global__ void __launch_bounds__(128) k_singular(const double* __restrict__ V, 
                                                  const int64_t* __restrict__ row_ptr, int64_t F,
                                                  const int32_t* __restrict__ col, const int32_t* __restrict__ info,
                                                  const int32_t* __restrict__ case_list, SegSet segs,
-                                                 double* __restrict__ values) {
+                                                 double* __restrict__ values, int mirror) {
     __shared__ double srule[kRuleChunk * kRuleStride];
     int si = 0;
     while (si + 1 < segs.nseg && (int)blockIdx.x >= segs.s[si + 1].first_block) ++si;
@@ -237,12 +243,12 @@ __global__ void __launch_bounds__(128) k_singular(const double* __restrict__ V, 
     double base[3] = {0, 0, 0}, ea1[3] = {0, 0, 0}, ea2[3] = {0, 0, 0}, eb1[3] = {0, 0, 0},
            eb2[3] = {0, 0, 0}, nb[3] = {0, 0, 0};
     double scale = 0.0;
-    int64_t pid = 0;
-    int inf = 0;
+    int64_t pid = 0, a = 0;
+    int inf = 0, b = 0;
     if (active) {
         pid = case_list[sd.list_off + local];
-        const int64_t a = find_row(row_ptr, F, pid);
-        const int b = col[pid];
+        a = find_row(row_ptr, F, pid);
+        b = col[pid];
         inf = info[pid];
         int pa[3] = {(inf >> 2) & 3, (inf >> 4) & 3, (inf >> 6) & 3};
         int pb[3] = {(inf >> 8) & 3, (inf >> 10) & 3, (inf >> 12) & 3};
@@ -350,7 +356,13 @@ __global__ void __launch_bounds__(128) k_singular(const double* __restrict__ V, 
     if (KIND == H2B_SLP) {
         // 1/r = t (3 - r^2 t^2) / 2; symmetrised pairs average both orientations
         double v = sym ? 0.25 * (acc0 + acc1) : 0.5 * acc0;
-        values[pid] = v * kInv4Pi * scale;
+        v *= kInv4Pi * scale;
+        values[pid] = v;
+        if (mirror && kase != H2B_IDENTICAL) {
+            // unordered pair {a, b}: the same value for (b, a) (symmetric SLP)
+            for (int64_t q = row_ptr[b]; q < row_ptr[b + 1]; ++q)
+                if (col[q] == (int32_t)a) values[q] = v;
+        }
     } else {
         // 1/r^3 = 1.5 t^3 (5/3 - r^2 t^2); scatter back to original local vertices
         const double f = 1.5 * kInv4Pi * scale;
@@ -363,6 +375,19 @@ __global__ void __launch_bounds__(128) k_singular(const double* __restrict__ V, 
         values[3 * pid + 1] = out[1];
         values[3 * pid + 2] = out[2];
     }
+}
+
+__global__ void k_touch_half(const int64_t* __restrict__ row_ptr, int64_t F, const int32_t* __restrict__ col,
+                             const int32_t* __restrict__ info, const int32_t* __restrict__ case_list,
+                             int64_t lo, int64_t hi, int32_t* __restrict__ half,
+                             unsigned long long* __restrict__ cursor) {
+    const int64_t e = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= hi) return;
+    const int32_t pid = case_list[e];
+    const int64_t a = find_row(row_ptr, F, pid);
+    if (a >= col[pid]) return;
+    const int seg = (info[pid] & 3) == H2B_EDGE ? 0 : 1;
+    half[atomicAdd(&cursor[seg], 1ull)] = pid;
 }
 
 // ----------------------------------------------------------------------------
@@ -405,9 +430,12 @@ __global__ void __launch_bounds__(256, MINB) k_blocks_slp(const double* __restri
     int* rp = cv + 3 * kTile;
     int* cp = rp + kTile;
 
-    const int64_t* jb = jobs + 6 * (int64_t)blockIdx.x;
+    const int64_t* jb = jobs + 8 * (int64_t)blockIdx.x;
     const int64_t row_off = jb[0], col_off = jb[2], out_off = jb[4], ld = jb[5];
+    const int64_t m_off = jb[6], m_ld = jb[7];
     const int nr = (int)jb[1], nc = (int)jb[3];
+    // diagonal tile of a symmetric block: upper triangle only, mirrored
+    const bool tri = m_off == out_off;
     if (nr > kTile || nc > kTile) {
         if (threadIdx.x == 0) atomicOr(flags, kFlagShape);
         return;
@@ -456,9 +484,19 @@ __global__ void __launch_bounds__(256, MINB) k_blocks_slp(const double* __restri
     __syncthreads();
 
     int lflags = 0;
-    const int np = nr * nc;
+    const int np = tri ? nc * (nc + 1) / 2 : nr * nc;
     for (int p = threadIdx.x; p < np; p += blockDim.x) {
-        const int a = p / nc, b = p - a * nc;
+        int a, b;
+        if (tri) {
+            // p = b (b + 1) / 2 + a, 0 <= a <= b
+            b = (int)((sqrt(8.0 * p + 1.0) - 1.0) * 0.5);
+            if ((b + 1) * (b + 2) / 2 <= p) ++b;
+            if (b * (b + 1) / 2 > p) --b;
+            a = p - b * (b + 1) / 2;
+        } else {
+            a = p / nc;
+            b = p - a * nc;
+        }
         double val;
         if (shares_vertex(rv + 3 * a, cv + 3 * b)) {
             if (t_row_ptr == nullptr) {
@@ -525,6 +563,7 @@ __global__ void __launch_bounds__(256, MINB) k_blocks_slp(const double* __restri
         }
         if (!isfinite(val)) lflags |= kFlagNonFinite;
         out[out_off + (int64_t)a * ld + b] = val;
+        if (m_off >= 0 && !(tri && a == b)) out[m_off + (int64_t)b * m_ld + a] = val;
     }
     if (lflags) atomicOr(flags, lflags);
 }
@@ -745,7 +784,7 @@ int launch_slp(const h2b_mesh* m, const double* P, const h2b_jobs* jobs, const h
     const int64_t nj = jobs->n_jobs;
     for (int64_t j0 = 0; j0 < nj; j0 += 2147483647LL) {
         const unsigned g = (unsigned)std::min<int64_t>(nj - j0, 2147483647LL);
-        kern<<<g, 256, sm, st>>>(P, m->n_triangles, m->d_triangles, jobs->d_jobs + 6 * j0, jobs->d_row_idx,
+        kern<<<g, 256, sm, st>>>(P, m->n_triangles, m->d_triangles, jobs->d_jobs + 8 * j0, jobs->d_row_idx,
                                  jobs->d_col_idx, t ? t->d_row_ptr : nullptr, t ? t->d_col : nullptr, tv,
                                  out, flags);
     }
@@ -842,6 +881,34 @@ extern "C" int h2b_touch_fill(const h2b_mesh* m, const int64_t* d_row_ptr, const
     return check_flags(flags, st);
 }
 
+extern "C" int h2b_touch_half(const h2b_touch* t, int32_t* d_half_list, int64_t* h_half_off, void* stream) {
+    if (!t || !d_half_list || !h_half_off || !t->h_case_off) return fail(H2B_ERR_INVALID, "h2b_touch_half: bad argument");
+    cudaStream_t st = as_stream(stream);
+    const int64_t* co = t->h_case_off;
+    const int64_t n_id = co[1] - co[0], n_edge = co[2] - co[1], n_vert = co[3] - co[2];
+    if ((n_edge & 1) || (n_vert & 1)) return fail(H2B_ERR_INVALID, "h2b_touch_half: touching relation not symmetric");
+    const int64_t off[4] = {0, n_id, n_id + n_edge / 2, n_id + n_edge / 2 + n_vert / 2};
+    if (n_id > 0)
+        H2B_CUDA_TRY(cudaMemcpyAsync(d_half_list, t->d_case_list + co[0], n_id * sizeof(int32_t),
+                                     cudaMemcpyDeviceToDevice, st));
+    unsigned long long hcur[2] = {(unsigned long long)off[1], (unsigned long long)off[2]}, hend[2];
+    unsigned long long* cur;
+    H2B_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&cur), sizeof(hcur), st));
+    H2B_CUDA_TRY(cudaMemcpyAsync(cur, hcur, sizeof(hcur), cudaMemcpyHostToDevice, st));
+    const int64_t n = co[3] - co[1];
+    if (n > 0)
+        k_touch_half<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(t->d_row_ptr, t->n_panels, t->d_col, t->d_info,
+                                                                 t->d_case_list, co[1], co[3], d_half_list, cur);
+    H2B_CUDA_TRY(cudaGetLastError());
+    H2B_CUDA_TRY(cudaMemcpyAsync(hend, cur, sizeof(hend), cudaMemcpyDeviceToHost, st));
+    H2B_CUDA_TRY(cudaFreeAsync(cur, st));
+    H2B_CUDA_TRY(cudaStreamSynchronize(st));
+    if ((int64_t)hend[0] != off[2] || (int64_t)hend[1] != off[3])
+        return fail(H2B_ERR_INVALID, "h2b_touch_half: touching relation not symmetric");
+    for (int i = 0; i < 4; ++i) h_half_off[i] = off[i];
+    return ok();
+}
+
 extern "C" int h2b_singular(const h2b_mesh* m, const h2b_touch* t, int kind, const h2b_rule* rules,
                             double* d_values, void* stream) {
     if (!m || !t || !rules || !d_values || !t->h_case_off) return fail(H2B_ERR_INVALID, "h2b_singular: bad argument");
@@ -851,6 +918,10 @@ extern "C" int h2b_singular(const h2b_mesh* m, const h2b_touch* t, int kind, con
         // identical flat panels: <x - y, n> = 0 identically (kernels.py:278-279)
         H2B_CUDA_TRY(cudaMemsetAsync(d_values, 0, 3 * sizeof(double) * t->n_pairs, st));
     }
+    // symmetric single-layer table: one thread per unordered pair
+    const bool half = kind == H2B_SLP && t->d_half_list && t->h_half_off;
+    const int64_t* segoff = half ? t->h_half_off : t->h_case_off;
+    const int32_t* list = half ? t->d_half_list : t->d_case_list;
     SegSet ss;
     ss.nseg = 0;
     int32_t block = 0;
@@ -860,10 +931,10 @@ extern "C" int h2b_singular(const h2b_mesh* m, const h2b_touch* t, int kind, con
     for (int oi = 0; oi < 3; ++oi) {
         const int c = order[oi];
         if (kind == H2B_DLP && c == 0) continue;
-        const int64_t cnt = t->h_case_off[c + 1] - t->h_case_off[c];
+        const int64_t cnt = segoff[c + 1] - segoff[c];
         if (cnt <= 0) continue;
         SegDesc& sd = ss.s[ss.nseg++];
-        sd.list_off = t->h_case_off[c];
+        sd.list_off = segoff[c];
         sd.count = cnt;
         sd.first_block = block;
         sd.n_blocks = (int32_t)((cnt + 127) / 128);
@@ -877,11 +948,11 @@ extern "C" int h2b_singular(const h2b_mesh* m, const h2b_touch* t, int kind, con
         if (kind == H2B_SLP)
             k_singular<H2B_SLP><<<block, 128, 0, st>>>(m->d_vertices, m->d_triangles, m->d_normals, m->d_areas,
                                                        t->d_row_ptr, t->n_panels, t->d_col, t->d_info,
-                                                       t->d_case_list, ss, d_values);
+                                                       list, ss, d_values, half ? 1 : 0);
         else
             k_singular<H2B_DLP><<<block, 128, 0, st>>>(m->d_vertices, m->d_triangles, m->d_normals, m->d_areas,
                                                        t->d_row_ptr, t->n_panels, t->d_col, t->d_info,
-                                                       t->d_case_list, ss, d_values);
+                                                       list, ss, d_values, 0);
         H2B_CUDA_TRY(cudaGetLastError());
     }
     return ok();

@@ -102,7 +102,21 @@ class TouchTable:
                                     D.stream()))
         self.case_off = np.array([0, counts[0], counts[0] + counts[1], n], dtype=np.int64)
         self.c = _lib.Touch(F, n, self.row_ptr.data_ptr(), self.col.data_ptr(), self.info.data_ptr(),
-                            self.case_list.data_ptr(), _lib.ptr(self.case_off))
+                            self.case_list.data_ptr(), _lib.ptr(self.case_off), None, None)
+        self.half_list = None
+
+    def ensure_half(self):
+        """Unordered-pair list (a < b) for the symmetric single-layer table."""
+        if self.half_list is None:
+            counts = self.case_counts
+            nh = int(counts[0] + (counts[1] + counts[2]) // 2)
+            self.half_list = D.empty((max(nh, 1),), "int32")
+            self.half_off = np.zeros(4, dtype=np.int64)
+            _lib.check(_lib.lib().h2b_touch_half(ctypes.byref(self.c), self.half_list.data_ptr(),
+                                                 _lib.ptr(self.half_off), D.stream()))
+            self.c.d_half_list = self.half_list.data_ptr()
+            self.c.h_half_off = _lib.ptr(self.half_off)
+        return self.half_list
 
     def keys(self):
         """Sorted int64 keys pa * F + pb (reference SingularTable.keys)."""
@@ -143,7 +157,10 @@ class SingularTable:
             self.compute()
 
     def compute(self):
-        """(Re)evaluate every touching pair on the device (stream-ordered)."""
+        """(Re)evaluate every touching pair on the device (stream-ordered).
+        Single layer: one evaluation per unordered pair (symmetric table)."""
+        if self.kind == SLP:
+            self.touch.ensure_half()
         _lib.check(_lib.lib().h2b_singular(ctypes.byref(self.dmesh.c), ctypes.byref(self.touch.c),
                                            kind_code(self.kind), self.rules, self.values_dev.data_ptr(),
                                            D.stream()))
@@ -171,17 +188,62 @@ class SingularTable:
 # ---------------------------------------------------------------------------
 # job packing
 
+def _as_job8(jobs):
+    jobs = np.asarray(jobs, dtype=np.int64)
+    if jobs.size == 0:
+        return np.zeros((0, 8), dtype=np.int64)
+    if jobs.ndim == 2 and jobs.shape[1] == 8:
+        return jobs
+    jobs = jobs.reshape(-1, 6)
+    pad = np.zeros((len(jobs), 2), dtype=np.int64)
+    pad[:, 0] = -1
+    return np.hstack([jobs, pad])
+
+
 def tile_jobs(jobs):
-    """Split (row_off, nr, col_off, nc, out_off, ld) jobs into <= TILE x TILE tiles."""
-    jobs = np.asarray(jobs, dtype=np.int64).reshape(-1, 6)
+    """Split (row_off, nr, col_off, nc, out_off, ld[, mirror_off, mirror_ld])
+    jobs into <= TILE x TILE tiles (8-word jobs out).  A mirrored tile also
+    writes its transpose at mirror_off; a diagonal job (mirror_off == out_off)
+    keeps its upper-triangle tiles only."""
+    jobs = _as_job8(jobs)
     if len(jobs) == 0 or (jobs[:, 1].max() <= TILE and jobs[:, 3].max() <= TILE):
         return jobs
     out = []
-    for r0, nr, c0, nc, o, ld in jobs:
+    for r0, nr, c0, nc, o, ld, mo, mld in jobs:
+        diag = mo == o and mo >= 0
         for i in range(0, max(nr, 1), TILE):
             for j in range(0, max(nc, 1), TILE):
-                out.append((r0 + i, min(TILE, nr - i), c0 + j, min(TILE, nc - j), o + i * ld + j, ld))
-    return np.array(out, dtype=np.int64).reshape(-1, 6)
+                if diag and i > j:
+                    continue
+                m = mo + j * mld + i if mo >= 0 else -1
+                out.append((r0 + i, min(TILE, nr - i), c0 + j, min(TILE, nc - j), o + i * ld + j, ld, m, mld))
+    return np.array(out, dtype=np.int64).reshape(-1, 8)
+
+
+def mirror_jobs(jobs, uids):
+    """Symmetric single-layer blocks (same tree and basis on both sides, so
+    block (s, t) = block (t, s)^T): keep one job per block pair {(t, s), (s, t)}
+    with the other written as its mirror; a diagonal block (t, t) keeps its
+    upper triangle.  jobs: (n, 6) in the order of uids (n, 2)."""
+    jobs = np.asarray(jobs, dtype=np.int64).reshape(-1, 6)
+    uids = np.asarray(uids, dtype=np.int64).reshape(-1, 2)
+    n = len(jobs)
+    out = _as_job8(jobs).copy()
+    if n == 0:
+        return out
+    key = uids[:, 0] * (uids.max() + 1) + uids[:, 1]
+    tkey = uids[:, 1] * (uids.max() + 1) + uids[:, 0]
+    order = np.argsort(key, kind="stable")
+    pos = np.searchsorted(key[order], tkey)
+    pos = np.minimum(pos, n - 1)
+    has = key[order][pos] == tkey
+    partner = np.where(has, order[pos], -1)
+    t, s = uids[:, 0], uids[:, 1]
+    keep = (partner < 0) | (t <= s)
+    m = keep & (partner >= 0)
+    out[m, 6] = jobs[partner[m], 4]
+    out[m, 7] = jobs[partner[m], 5]
+    return out[keep]
 
 
 class SlpJobs:
@@ -192,7 +254,15 @@ class SlpJobs:
         self.q = q
         self.jobs = tile_jobs(jobs)
         self.n = len(self.jobs)
-        self.pairs = int((self.jobs[:, 1] * self.jobs[:, 3]).sum()) if self.n else 0
+        if self.n:
+            tri = self.jobs[:, 6] == self.jobs[:, 4]
+            full = self.jobs[:, 1] * self.jobs[:, 3]
+            mult = np.where(self.jobs[:, 6] >= 0, 2, 1)
+            # pairs integrated / pairs of the matrix written
+            self.evaluated = int(np.where(tri, self.jobs[:, 3] * (self.jobs[:, 3] + 1) // 2, full).sum())
+            self.pairs = int(np.where(tri, full, full * mult).sum())
+        else:
+            self.evaluated = self.pairs = 0
         if self.n == 0:
             return
         self.pp, self.Q, _ = dmesh.panel_points(q)

@@ -159,3 +159,34 @@ def test_quadrature_deterministic(cfg0_world):
     a = assemble_nearfield_device(ctx, "slp", bt, 3, 4).cpu().numpy()
     b = assemble_nearfield_device(ctx, "slp", bt, 3, 4).cpu().numpy()
     assert np.array_equal(a, b)
+
+
+def test_symmetric_nearfield_equals_full_integration(cfg0_world):
+    """Mirrored single-layer jobs (one integration per entry pair, diagonal
+    blocks by upper triangle) vs integrating every entry; the symmetric
+    singular table is exactly symmetric."""
+    import torch
+
+    from paper_2001_05523_b200 import kernels
+    from paper_2001_05523_b200.containers import near_layout, near_slp_jobs
+
+    m, ctx, t0, _, bt, _ = cfg0_world
+    lay = near_layout(bt)
+    tab = ctx.singular_table("slp", 4)
+    nu = bt.near_uids
+    full = np.stack([t0.start[nu[:, 0]], lay.blk_rows, t0.start[nu[:, 1]], lay.blk_cols, lay.blk_off, lay.blk_ld], 1)
+    mirrored = near_slp_jobs(bt)
+    assert mirrored.shape[1] == 8 and len(mirrored) < len(full)
+    perm = t0.perm.astype(np.int32)
+    a = torch.zeros(lay.total, dtype=torch.float64, device="cuda")
+    b = torch.zeros(lay.total, dtype=torch.float64, device="cuda")
+    kernels.run_slp_jobs(ctx.dmesh, 3, full, perm, perm, tab, a)
+    sj = kernels.SlpJobs(ctx.dmesh, 3, mirrored, perm, perm)
+    sj.run(tab, b)
+    assert sj.pairs == lay.entries and sj.evaluated < 0.55 * lay.entries
+    a, b = a.cpu().numpy(), b.cpu().numpy()
+    assert np.abs(a - b).max() <= 1e-13 * np.abs(a).max()
+    keys, vals = tab.keys, tab.values
+    F = m.n_triangles
+    tk = (keys % F) * F + keys // F
+    assert np.array_equal(vals[np.searchsorted(keys, tk)], vals)

@@ -152,3 +152,33 @@ def test_native_dlp_job_builder_matches_restatement():
     for k in a:
         assert a[k].dtype == b[k].dtype and np.array_equal(a[k], b[k]), k
     assert kernels.build_dlp_jobs(m, []) is None
+
+
+def test_mirror_and_tile_jobs_cover_every_entry_once():
+    """Host job logic of the symmetric single-layer assembly: every entry of
+    every block is written exactly once (directly or as a mirror), diagonal
+    blocks larger than a tile keep their upper-triangle tiles only."""
+    from paper_2001_05523_b200 import kernels
+
+    sizes = {0: 100, 1: 40, 2: 70}
+    uids = np.array([(0, 0), (0, 1), (1, 0), (1, 1), (2, 0), (0, 2), (1, 2), (2, 2)])
+    off, jobs, start = 0, [], {0: 0, 1: 100, 2: 140}
+    blocks = {}
+    for t, s in uids:
+        nr, nc = sizes[t], sizes[s]
+        jobs.append((start[t], nr, start[s], nc, off, nc))
+        blocks[(t, s)] = (off, nc, nr)
+        off += nr * nc
+    jobs = kernels.tile_jobs(kernels.mirror_jobs(np.array(jobs), uids[:, ::-1][:, ::-1]))
+    hits = np.zeros(off, dtype=np.int64)
+    for r0, nr, c0, nc, o, ld, mo, mld in jobs:
+        assert nr <= kernels.TILE and nc <= kernels.TILE
+        tri = mo == o
+        for a in range(nr):
+            for b in range(nc):
+                if tri and a > b:
+                    continue
+                hits[o + a * ld + b] += 1
+                if mo >= 0 and not (tri and a == b):
+                    hits[mo + b * mld + a] += 1
+    assert (hits == 1).all()

@@ -5,6 +5,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
 import ctypes
 import numpy as np
+from paper_2001_05523_b200.containers import near_slp_jobs
 import torch
 import bench
 from paper_2001_05523_b200 import kernels, _lib
@@ -15,7 +16,7 @@ mesh, ctx, tree, bt, basis = bench.build_problem(cfg, os.cpu_count() or 8)
 lay = near_layout(bt)
 Dn = torch.zeros(max(lay.total, 1), dtype=torch.float64, device="cuda")
 nu = bt.near_uids
-jobs = np.stack([tree.start[nu[:, 0]], lay.blk_rows, tree.start[nu[:, 1]], lay.blk_cols, lay.blk_off, lay.blk_ld], 1)
+jobs = near_slp_jobs(bt)
 sj = kernels.SlpJobs(ctx.dmesh, cfg["q_reg"], jobs, tree.perm.astype(np.int32), tree.perm.astype(np.int32))
 tab = kernels.SingularTable(ctx.dmesh, "slp", cfg["q_ss"])
 sj.run(tab, Dn)

@@ -2,7 +2,8 @@
 import os, sys, subprocess, json
 if len(sys.argv) > 1 and sys.argv[1] == "child":
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    import numpy as np, torch, bench
+    import numpy as np
+from paper_2001_05523_b200.containers import near_slp_jobs, torch, bench
     from paper_2001_05523_b200 import kernels, clustering as C, spaces
     from paper_2001_05523_b200.containers import AssemblyContext, near_layout
     from paper_2001_05523_b200.mesh import sphere_mesh
@@ -10,7 +11,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     tree = C.build_cluster_tree(spaces.DofSpace(spaces.P0, m).support_boxes(), 64)
     bt = C.BlockTree(tree, tree, 2.0); lay = near_layout(bt)
     Dn = torch.zeros(lay.total, dtype=torch.float64, device="cuda"); nu = bt.near_uids
-    jobs = np.stack([tree.start[nu[:, 0]], lay.blk_rows, tree.start[nu[:, 1]], lay.blk_cols, lay.blk_off, lay.blk_ld], 1)
+    jobs = near_slp_jobs(bt)
     sj = kernels.SlpJobs(ctx.dmesh, 3, jobs, tree.perm.astype(np.int32), tree.perm.astype(np.int32))
     tab = kernels.SingularTable(ctx.dmesh, "slp", 4)
     for _ in range(2): sj.run(tab, Dn)
