@@ -24,6 +24,9 @@
  *   h2b_matvec           <- containers.H2Matrix.matvec             containers.py:254-270
  *                           (ClusterBasis.forward/backward          containers.py:201-228)
  *   h2b_diagonal         <- containers.H2Matrix.diagonal           containers.py:290-301
+ *   h2b_gca_columns /
+ *   h2b_gca_aca          <- gca.build_basis (green_columns, cross_interpolate) gca.py:149-179,
+ *                           lowrank.aca_inverse_core               lowrank.py:154-184
  */
 #ifndef H2B_H
 #define H2B_H
@@ -191,6 +194,44 @@ int h2b_dlp_jobs_sizes(const h2b_dlp_build* b, int64_t* sizes);
 int h2b_dlp_jobs_copy(const h2b_dlp_build* b, int64_t* jobs, int32_t* row_idx, int32_t* pan_idx, int32_t* inc_ptr,
                       int32_t* inc, int64_t* inc_base);
 int h2b_dlp_jobs_free(h2b_dlp_build* b);
+
+/* ================= GCA cluster-basis construction (device) ================= */
+
+/* Basis flavors (gca.P0_SLP / gca.P1_DLP): P0 rows are panels (potentials
+ * K_VALUE | K_DN_Z), P1 rows are vertices (hat functions, K_DN_X | K_DN_X_DN_Z). */
+#define H2B_GCA_P0_SLP 0
+#define H2B_GCA_P1_DLP 1
+
+/* One tree level of clusters (independent).  Cluster c has rows
+ * d_rows[d_row_ptr[c] : d_row_ptr[c+1]] (leaf: its dofs; inner: its children's
+ * pivots), n_green = 6 m^2 Green points (x, y, z, sqrt(w), nx, ny, nz, 0) at
+ * d_green + 8 n_green c, and a slot at d_l_off[c] of rows x 2 n_green doubles
+ * in the L, scratch and V buffers.  max_rows = largest row count. */
+typedef struct {
+    int64_t n_clusters;
+    const int64_t* d_row_ptr;
+    const int32_t* d_rows;
+    int32_t n_green;
+    int32_t max_rows;
+    const double* d_green;
+    const int64_t* d_l_off;
+} h2b_gca_batch;
+
+/* Green-quadrature columns L (rows x 2k, row-major) of every cluster
+ * (gca.green_columns <- src/gca.py; panel_potentials / p1_potentials
+ * src/kernels.py:97-196), regular rule with Q points per panel
+ * (h2b_panel_points), d_lam = Q x 3 barycentrics (P1 only).  Non-finite
+ * entries -> H2B_ERR_INVALID.  Synchronises. */
+int h2b_gca_columns(const h2b_mesh* m, const double* d_panel_points, int32_t Q, const double* d_lam, int flavor,
+                    const h2b_gca_batch* b, double* d_L, void* stream);
+/* Fully pivoted ACA with inverse core on every L (lowrank.aca_inverse_core,
+ * src/lowrank.py:154-184) and the interpolation matrix V = L[:, sigma]
+ * inv(L[tau, sigma]) (gca.cross_interpolate).  Outputs: d_rank[c], local pivot
+ * rows d_tau[c * tau_cap + i] (tau_cap >= 2 n_green), V (rows x rank,
+ * row-major) at d_V + d_l_off[c].  d_scratch (same size as d_L) holds the
+ * residuals that do not fit in shared memory. */
+int h2b_gca_aca(const h2b_gca_batch* b, double eps, const double* d_L, double* d_scratch, int32_t* d_rank,
+                int32_t* d_tau, int32_t tau_cap, double* d_V, void* stream);
 
 /* ============================ H^2 matvec (device) ========================== */
 

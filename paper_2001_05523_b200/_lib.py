@@ -66,6 +66,13 @@ class DlpJobs(ctypes.Structure):
     ]
 
 
+class GcaBatch(ctypes.Structure):
+    _fields_ = [
+        ("n_clusters", ctypes.c_int64), ("d_row_ptr", vp), ("d_rows", vp), ("n_green", ctypes.c_int32),
+        ("max_rows", ctypes.c_int32), ("d_green", vp), ("d_l_off", vp),
+    ]
+
+
 class Layout(ctypes.Structure):
     _fields_ = [
         ("n_rows", ctypes.c_int64), ("n_cols", ctypes.c_int64),
@@ -91,7 +98,7 @@ EXPORTS = (
     "h2b_touch_count", "h2b_touch_fill", "h2b_touch_half", "h2b_singular", "h2b_pair_blocks_slp", "h2b_pair_blocks_dlp",
     "h2b_plan_create", "h2b_plan_destroy", "h2b_matvec", "h2b_matvec_host",
     "h2b_diagonal", "h2b_plan_trace", "h2b_dlp_jobs_build", "h2b_dlp_jobs_sizes", "h2b_dlp_jobs_copy",
-    "h2b_dlp_jobs_free",
+    "h2b_dlp_jobs_free", "h2b_gca_columns", "h2b_gca_aca",
 )
 
 _lib = None
@@ -135,6 +142,9 @@ def lib():
         L.h2b_dlp_jobs_sizes.argtypes = [vp, vp]
         L.h2b_dlp_jobs_copy.argtypes = [vp, vp, vp, vp, vp, vp, vp]
         L.h2b_dlp_jobs_free.argtypes = [vp]
+        L.h2b_gca_columns.argtypes = [ctypes.POINTER(Mesh), vp, ctypes.c_int32, vp, ctypes.c_int,
+                                      ctypes.POINTER(GcaBatch), vp, vp]
+        L.h2b_gca_aca.argtypes = [ctypes.POINTER(GcaBatch), ctypes.c_double, vp, vp, vp, vp, ctypes.c_int32, vp, vp]
         _lib = L
     return _lib
 

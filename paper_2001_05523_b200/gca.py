@@ -212,14 +212,126 @@ def gca_nested(ctx, flavor, child_pivots, box, m, eps_aca, q_single):
     return rows[tau], Vhat
 
 
-def build_basis(ctx, tree, flavor, m, eps_aca, q_single=None, threads=1):
+def green_points_batch(boxes, m):
+    """Green points of many clusters at once: (n, 6 m^2, 8) = x, y, z,
+    sqrt(w), nx, ny, nz, 0 -- the same floating-point operations as
+    green_quadrature(green_box(box), m) per cluster, vectorised."""
+    boxes = np.asarray(boxes, dtype=float).reshape(-1, 2, 3).copy()
+    n = len(boxes)
+    ext = boxes[:, 1] - boxes[:, 0]
+    pad = DEGENERATE_WIDTH * np.maximum(ext.max(axis=1), 1.0)
+    for d in range(3):
+        flat = ext[:, d] < pad
+        mid = 0.5 * (boxes[:, 0, d] + boxes[:, 1, d])
+        boxes[:, 0, d] = np.where(flat, mid - 0.5 * pad, boxes[:, 0, d])
+        boxes[:, 1, d] = np.where(flat, mid + 0.5 * pad, boxes[:, 1, d])
+    delta = (boxes[:, 1] - boxes[:, 0]).max(axis=1)
+    gb = np.stack([boxes[:, 0] - delta[:, None], boxes[:, 1] + delta[:, None]], axis=1)
+    g = gauss_legendre(m)
+    mm = m * m
+    out = np.zeros((n, 6 * mm, 8))
+    f = 0
+    for axis in range(3):
+        u, v = (axis + 1) % 3, (axis + 2) % 3
+        lu = gb[:, 1, u] - gb[:, 0, u]
+        lv = gb[:, 1, v] - gb[:, 0, v]
+        cu = gb[:, 0, u][:, None] + lu[:, None] * g.points[None, :]
+        cv = gb[:, 0, v][:, None] + lv[:, None] * g.points[None, :]
+        wface = ((lu[:, None] * g.weights[None, :])[:, :, None] * (lv[:, None] * g.weights[None, :])[:, None, :])
+        wface = wface.reshape(n, mm)
+        for side in (0, 1):
+            blk = out[:, f * mm : (f + 1) * mm]
+            blk[:, :, axis] = gb[:, side, axis][:, None]
+            blk[:, :, u] = np.repeat(cu, m, axis=1)
+            blk[:, :, v] = np.tile(cv, (1, m))
+            blk[:, :, 3] = np.sqrt(wface)
+            blk[:, :, 4 + axis] = 1.0 if side else -1.0
+            f += 1
+    return out
+
+
+_GCA_FLAVOR_CODE = {P0_SLP: 0, P1_DLP: 1}
+
+
+def build_basis_device(ctx, tree, flavor, m, eps_aca, q_single=None):
+    """GCA basis on the GPU (libh2b h2b_gca_columns + h2b_gca_aca), one tree
+    level per call, leaves first.  Same algorithm as build_basis; the Green
+    columns are evaluated with device arithmetic, so a pivot can differ from
+    the host path where two residual entries tie to rounding (tests measure
+    the agreement)."""
+    import ctypes
+
+    from . import _lib
+    from . import device as D
+    from .containers import ClusterBasis
+
+    if flavor not in _GCA_FLAVOR_CODE:
+        raise ValueError(f"unknown basis flavor {flavor!r}")
+    if q_single is None:
+        q_single = max(2, m)
+    L_ = _lib.lib()
+    pp, Q, lam = ctx.dmesh.panel_points(q_single)
+    basis = ClusterBasis(tree)
+    depth = tree.depth_of
+    k = 6 * m * m
+    ncol = 2 * k
+    for d in range(int(depth.max()), -1, -1):
+        level = np.flatnonzero(depth == d)
+        rows, boxes = [], []
+        for u in level:
+            c = tree.nodes[int(u)]
+            rows.append(np.asarray(tree.dofs(c), dtype=np.int64) if c.is_leaf
+                        else np.concatenate([basis.pivots[ch.uid] for ch in c.children]))
+            boxes.append(c.box)
+        nr = np.array([len(r) for r in rows], dtype=np.int64)
+        ptr = np.zeros(len(level) + 1, dtype=np.int64)
+        np.cumsum(nr, out=ptr[1:])
+        l_off = ptr[:-1] * ncol
+        total = int(ptr[-1]) * ncol
+        d_ptr, d_rows = D.dev(ptr), D.dev(np.concatenate(rows), np.int32)
+        d_green, d_loff = D.dev(green_points_batch(boxes, m)), D.dev(l_off)
+        b = _lib.GcaBatch(len(level), d_ptr.data_ptr(), d_rows.data_ptr(), k, int(nr.max()), d_green.data_ptr(),
+                          d_loff.data_ptr())
+        Lm, scratch, Vm = D.empty((total,)), D.empty((total,)), D.empty((total,))
+        rank = D.empty((len(level),), "int32")
+        tau = D.empty((len(level) * ncol,), "int32")
+        _lib.check(L_.h2b_gca_columns(ctypes.byref(ctx.dmesh.c), pp.data_ptr(), Q, lam.data_ptr(),
+                                      _GCA_FLAVOR_CODE[flavor], ctypes.byref(b), Lm.data_ptr(), D.stream()))
+        _lib.check(L_.h2b_gca_aca(ctypes.byref(b), float(eps_aca), Lm.data_ptr(), scratch.data_ptr(),
+                                  rank.data_ptr(), tau.data_ptr(), ncol, Vm.data_ptr(), D.stream()))
+        rk, tu, Vh = D.host(rank).astype(np.int64), D.host(tau).reshape(-1, ncol), D.host(Vm)
+        del Lm, scratch, Vm
+        for i, u in enumerate(level):
+            u = int(u)
+            c = tree.nodes[u]
+            kk = int(rk[i])
+            V = Vh[l_off[i] : l_off[i] + nr[i] * kk].reshape(nr[i], kk).copy()
+            piv = rows[i][tu[i, :kk].astype(np.int64)]
+            if c.is_leaf:
+                basis.V[u] = V
+            else:
+                off = 0
+                for ch in c.children:
+                    kc = basis.rank[ch.uid]
+                    basis.E[ch.uid] = V[off : off + kc, :]
+                    off += kc
+            basis.pivots[u] = piv
+            basis.rank[u] = kk
+    return basis
+
+
+def build_basis(ctx, tree, flavor, m, eps_aca, q_single=None, threads=1, device=False):
     """Nested cluster basis from the leaves up (gca.py:149-179): at each depth
     all clusters are independent; transfer matrices are the row blocks of the
-    parent's interpolation matrix in child order."""
+    parent's interpolation matrix in child order.  device=True builds it on
+    the GPU (build_basis_device); the default host path reproduces the
+    reference's pivots bit for bit."""
     from threadpoolctl import threadpool_limits
 
     from .containers import ClusterBasis
 
+    if device:
+        return build_basis_device(ctx, tree, flavor, m, eps_aca, q_single)
     if q_single is None:
         q_single = max(2, m)
     basis = ClusterBasis(tree)

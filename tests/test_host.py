@@ -182,3 +182,20 @@ def test_mirror_and_tile_jobs_cover_every_entry_once():
                 if mo >= 0 and not (tri and a == b):
                     hits[mo + b * mld + a] += 1
     assert (hits == 1).all()
+
+
+def test_green_points_batch_matches_per_cluster_bits():
+    from paper_2001_05523_b200 import gca
+
+    rng = np.random.default_rng(5)
+    lo = rng.uniform(-1, 1, (40, 3))
+    ext = rng.uniform(0, 0.5, (40, 3))
+    ext[::7, 1] = 0.0  # flat boxes are widened
+    boxes = np.stack([lo, lo + ext], axis=1)
+    for m in (3, 4, 5):
+        got = gca.green_points_batch(boxes, m)
+        for i, box in enumerate(boxes):
+            gq = gca.green_quadrature(gca.green_box(box), m)
+            assert np.array_equal(got[i, :, :3], gq.points)
+            assert np.array_equal(got[i, :, 3], np.sqrt(gq.weights))
+            assert np.array_equal(got[i, :, 4:7], gq.normals)
