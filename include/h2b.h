@@ -24,6 +24,7 @@
  *   h2b_matvec           <- containers.H2Matrix.matvec             containers.py:254-270
  *                           (ClusterBasis.forward/backward          containers.py:201-228)
  *   h2b_diagonal         <- containers.H2Matrix.diagonal           containers.py:290-301
+ *   h2b_cg_*             <- solver.cg (vector updates, dots)      solver.py:22-59
  *   h2b_gca_columns /
  *   h2b_gca_aca          <- gca.build_basis (green_columns, cross_interpolate) gca.py:149-179,
  *                           lowrank.aca_inverse_core               lowrank.py:154-184
@@ -232,6 +233,24 @@ int h2b_gca_columns(const h2b_mesh* m, const double* d_panel_points, int32_t Q, 
  * residuals that do not fit in shared memory. */
 int h2b_gca_aca(const h2b_gca_batch* b, double eps, const double* d_L, double* d_scratch, int32_t* d_rank,
                 int32_t* d_tau, int32_t tau_cap, double* d_V, void* stream);
+
+/* ====================== CG vector kernels (device) ========================= */
+
+/* Fused passes of the Jacobi-preconditioned CG iteration (solver.cg,
+ * src/solver.py:22-59) with deterministic reductions (fixed grid, per-CTA
+ * partials summed in index order).  Scalars live on the device in
+ * scal = (rz, pAp, rz_new, r.r); with row-sharded vectors the caller
+ * all-reduces the scalars a call writes before the next call.  d_work: a
+ * zero-initialised workspace of h2b_cg_workspace_size bytes (one per stream). */
+int h2b_cg_workspace_size(int64_t* bytes);
+/* d_out[0] = a . b */
+int h2b_cg_dot(const double* d_a, const double* d_b, int64_t n, void* d_work, double* d_out, void* stream);
+/* alpha = scal[0] / scal[1]; x += alpha p; r -= alpha Ap; z = r * inv_diag
+ * (z unused when inv_diag is NULL: then z is r); d_out[0..1] = (r.z, r.r). */
+int h2b_cg_step(int64_t n, const double* d_scal, double* d_x, double* d_r, const double* d_p, const double* d_Ap,
+                const double* d_inv_diag, double* d_z, void* d_work, double* d_out, void* stream);
+/* p = z + (scal[2] / scal[0]) p */
+int h2b_cg_direction(int64_t n, const double* d_scal, const double* d_z, double* d_p, void* stream);
 
 /* ============================ H^2 matvec (device) ========================== */
 

@@ -64,10 +64,36 @@ def cg(apply_a, b, eps, max_it, precond_diag=None):
     return CGResult(x, max_it, False, float(np.linalg.norm(b - apply_a(x))) / norm_b)
 
 
-def _cg_torch(apply_a, b, eps, max_it, precond_diag):
+def _cg_torch(apply_a, b, eps, max_it, precond_diag, allreduce=None):
+    """Device-resident CG on CUDA float64 tensors: fused libh2b vector passes
+    (h2b_cg_dot / h2b_cg_step / h2b_cg_direction), scalars kept on the device
+    and one 4-double read-back per iteration for the breakdown and stopping
+    tests.  `allreduce(t)` (row-sharded vectors) sums a small device tensor
+    over the ranks in place."""
+    import ctypes
+
     import torch
 
-    norm_b = float(torch.linalg.vector_norm(b))
+    from . import _lib
+
+    L = _lib.lib()
+    st = _lib.stream_ptr()
+    n = b.numel()
+    b = b.contiguous()
+    ws = ctypes.c_int64()
+    _lib.check(L.h2b_cg_workspace_size(ctypes.byref(ws)))
+    work = torch.zeros(ws.value, dtype=torch.uint8, device=b.device)
+    sc = torch.zeros(4, dtype=torch.float64, device=b.device)  # rz, pAp, rz_new, r.r
+    host = torch.zeros(4, dtype=torch.float64).pin_memory()
+
+    def dot(a, c, out):
+        _lib.check(L.h2b_cg_dot(a.data_ptr(), c.data_ptr(), n, work.data_ptr(), out.data_ptr(), st))
+        if allreduce is not None:
+            allreduce(out)
+
+    nb = torch.zeros(1, dtype=torch.float64, device=b.device)
+    dot(b, b, nb)
+    norm_b = float(nb.sqrt())
     if norm_b == 0.0:
         return CGResult(torch.zeros_like(b), 0, True, 0.0)
     inv_d = None
@@ -75,25 +101,31 @@ def _cg_torch(apply_a, b, eps, max_it, precond_diag):
         d = torch.as_tensor(precond_diag, dtype=b.dtype, device=b.device)
         if bool((d <= 0.0).any()):
             raise SolverBreakdown("Jacobi preconditioner requires a positive diagonal")
-        inv_d = 1.0 / d
+        inv_d = (1.0 / d).contiguous()
     x = torch.zeros_like(b)
     r = b.clone()
     z = r * inv_d if inv_d is not None else r
     p = z.clone()
-    rz = torch.dot(r, z)
+    dot(r, z, sc[0:1])
+    z_ptr = z.data_ptr() if inv_d is not None else None
     for it in range(1, max_it + 1):
         Ap = apply_a(p)
-        pAp = torch.dot(p, Ap)
-        if float(pAp) <= 0.0:
-            raise SolverBreakdown(f"non-positive curvature p^T A p = {float(pAp):.3e} at iteration {it}")
-        alpha = rz / pAp
-        x.add_(alpha * p)
-        r.sub_(alpha * Ap)
-        res = float(torch.linalg.vector_norm(r)) / norm_b
+        dot(p, Ap, sc[1:2])
+        _lib.check(L.h2b_cg_step(n, sc.data_ptr(), x.data_ptr(), r.data_ptr(), p.data_ptr(), Ap.data_ptr(),
+                                 inv_d.data_ptr() if inv_d is not None else None, z_ptr, work.data_ptr(),
+                                 sc[2:4].data_ptr(), st))
+        if allreduce is not None:
+            allreduce(sc[2:4])
+        host.copy_(sc)
+        pAp, rr = float(host[1]), float(host[3])
+        if pAp <= 0.0:
+            raise SolverBreakdown(f"non-positive curvature p^T A p = {pAp:.3e} at iteration {it}")
+        res = float(np.sqrt(rr)) / norm_b
         if res <= eps:
             return CGResult(x, it, True, res)
-        z = r * inv_d if inv_d is not None else r
-        rz_new = torch.dot(r, z)
-        p = z + (rz_new / rz) * p
-        rz = rz_new
-    return CGResult(x, max_it, False, float(torch.linalg.vector_norm(b - apply_a(x))) / norm_b)
+        _lib.check(L.h2b_cg_direction(n, sc.data_ptr(), (z if inv_d is not None else r).data_ptr(), p.data_ptr(),
+                                      st))
+        sc[0:1].copy_(sc[2:3])
+    res_vec = b - apply_a(x)
+    dot(res_vec, res_vec, nb)
+    return CGResult(x, max_it, False, float(nb.sqrt()) / norm_b)
