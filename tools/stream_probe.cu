@@ -3,6 +3,7 @@
 //   mode 0: TMA bulk copy, nst stages of `chunk` bytes, loop over chunks
 //   mode 1: LDG.256 direct, 4 independent loads per lane per iteration
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -61,8 +62,9 @@ __global__ void k_ldg(const double* __restrict__ A, size_t n, size_t per_cta, do
     if (acc == 12345.0) out[0] = acc;
 }
 
-int main() {
-    const size_t bytes = 112ull << 20;
+int main(int argc, char** argv) {
+    // streamed size in MiB (default 112: the config-1 nearfield)
+    const size_t bytes = (argc > 1 ? (size_t)atoll(argv[1]) : 112ull) << 20;
     const size_t n = bytes / 8;
     double *A, *out, *fl;
     cudaMalloc(&A, bytes); cudaMemset(A, 0, bytes);
@@ -91,7 +93,7 @@ int main() {
             }
         }
     }
-    for (size_t per : {4096ul, 16384ul, 65536ul}) {
+    for (size_t per : {4096ul, 16384ul, 65536ul, 262144ul}) {
         char nm[128]; snprintf(nm, 128, "ldg256 per_cta=%zu doubles", per);
         int grid = (int)((n + per - 1) / per);
         run(nm, [&] { k_ldg<<<grid, 256>>>(A, n, per, out); });
