@@ -131,7 +131,7 @@ def ncu_traffic(kernel, path=None):
     """DRAM bytes (read + write) of one launch of `kernel` from the committed
     ncu --set full capture (profiles/), or None."""
     import csv
-    path = path or os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_ncu_full_raw.csv")
+    path = path or os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01s2_ncu_full_raw.csv")
     if not os.path.exists(path):
         return None
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
@@ -295,6 +295,35 @@ def run_ours(args, cfg):
                "timer": "host wall clock around H2Matrix.matvec(numpy) incl. H2D/D2H, synchronised"}
         del yh
 
+    # ---- the rest of the pipeline on the device (reported, untimed by the metric) ----
+    extra = {}
+    if ws == 1:
+        from paper_2001_05523_b200 import solver, spaces
+
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        bdev = gca.build_basis(ctx, tree, gca.P0_SLP, cfg["m"], EPS_ACA, device=True)
+        torch.cuda.synchronize()
+        t_gca = time.perf_counter() - t1
+        same = np.mean([basis.rank[u] == bdev.rank[u] and np.array_equal(basis.pivots[u], bdev.pivots[u])
+                        for u in range(tree.n_nodes)])
+        extra["gca_basis"] = {"device_s": t_gca, "host_s": setup_s, "host_threads": threads,
+                              "pivots_identical_to_host_frac": float(same),
+                              "note": "host_s = whole host setup (mesh, trees, reference-identical GCA basis)"}
+        b = spaces.load_vector(spaces.DofSpace(spaces.P0, mesh), lambda X, tt: X[..., 0] ** 2 - X[..., 1] ** 2)
+        bd = torch.from_numpy(b).cuda()
+        diag = H.diagonal()
+        plan = H.plan()
+        solver.cg(lambda v: plan.apply_device(v), bd, EPS_ACA / 10.0, 2000, precond_diag=diag)  # warm
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        res = solver.cg(lambda v: plan.apply_device(v), bd, EPS_ACA / 10.0, 2000, precond_diag=diag)
+        torch.cuda.synchronize()
+        t_cg = time.perf_counter() - t1
+        extra["cg"] = {"iterations": res.iterations, "converged": res.converged, "residual": res.residual,
+                       "ms": t_cg * 1e3, "ms_per_iteration": t_cg * 1e3 / max(res.iterations, 1),
+                       "rhs": "P0 load of x1^2 - x2^2, Jacobi, eps_solver = eps_aca / 10 (solver.cg)"}
+
     # ---- roofline ---------------------------------------------------------------
     pk = peaks()
     mv_bytes = H.matvec_bytes()
@@ -320,7 +349,7 @@ def run_ours(args, cfg):
         "roofline": {"bound": "hbm", "kernel": "k_matvec (fused forward + coupling + backward + nearfield)",
                      "achieved": mv_bytes / mean_step / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": mv_bytes / mean_step / 1e9 / pk["hbm_gbs"], "traffic": ncu_traffic("k_matvec"),
-                     "traffic_source": "profiles/r01_ncu_full_raw.csv (ncu --set full, one launch, DRAM read+write bytes)",
+                     "traffic_source": "profiles/r01s2_ncu_full_raw.csv (ncu --set full, one launch, DRAM read+write bytes)",
                      "algorithmic_bytes": mv_bytes, "kernel_ms": mean_step * 1e3, "peak_source": pk["hbm_src"]},
         "nearfield": {
             "pairs_per_s": fc["pairs"] / nf_time, "pairs": fc["pairs"], "ms": nf_time * 1e3,
@@ -339,6 +368,7 @@ def run_ours(args, cfg):
                          "peak_source": fp64_src},
         },
         "e2e": e2e,
+        **extra,
         "clocks": clk,
         "setup_s": setup_s,
     }
