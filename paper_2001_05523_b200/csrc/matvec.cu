@@ -127,7 +127,29 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+#ifdef H2B_LL_TIMEOUT
+__device__ unsigned long long g_mbar_stuck[2];
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef H2B_LL_TIMEOUT
+    // debug builds: an abandoned wait is recorded instead of hanging the GPU
+    for (long long it = 0;; ++it) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (it > (1ll << 20)) {
+            g_mbar_stuck[0] = blockIdx.x + 1;
+            g_mbar_stuck[1] = parity;
+            return;
+        }
+    }
+#endif
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "WAIT_%=:\n\t"
@@ -184,10 +206,14 @@ __device__ __forceinline__ double ll_load(const uint64_t* p, uint32_t epoch) {
 #ifdef H2B_LL_TIMEOUT
     for (long long it = 0; !ll_try(p, epoch, v); ++it) {
         __nanosleep(32);
-        if (it > (1ll << 22)) {
+#ifndef H2B_LL_TIMEOUT_ITERS
+#define H2B_LL_TIMEOUT_ITERS (1ll << 22)
+#endif
+        if (it > H2B_LL_TIMEOUT_ITERS) {
             g_ll_stuck[0] = reinterpret_cast<unsigned long long>(p);
             g_ll_stuck[1] = epoch;
             g_ll_stuck[2] = blockIdx.x;
+            g_ll_stuck[3] = *reinterpret_cast<const volatile unsigned long long*>(p);
             return 0.0;
         }
     }
@@ -1334,6 +1360,11 @@ extern "C" int h2b_debug_stuck(h2b_plan* p, unsigned long long* out) {
     out[4] = reinterpret_cast<unsigned long long>(p->ycpl);
     out[5] = reinterpret_cast<unsigned long long>(p->yfin);
     out[6] = reinterpret_cast<unsigned long long>(p->ynear);
+    out[7] = h[3];  // the word found at the abandoned address
+    unsigned long long mb[2];
+    H2B_CUDA_TRY(cudaMemcpyFromSymbol(mb, g_mbar_stuck, sizeof(mb)));
+    out[8] = mb[0];
+    out[9] = mb[1];
     return 0;
 }
 #endif
