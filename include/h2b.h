@@ -24,6 +24,7 @@
  *   h2b_matvec           <- containers.H2Matrix.matvec             containers.py:254-270
  *                           (ClusterBasis.forward/backward          containers.py:201-228)
  *   h2b_diagonal         <- containers.H2Matrix.diagonal           containers.py:290-301
+ *   h2b_matmat           <- (no reference counterpart: H2Matrix.matvec per column, containers.py:254-270)
  *   h2b_cg_*             <- solver.cg (vector updates, dots)      solver.py:22-59
  *   h2b_gca_columns /
  *   h2b_gca_aca          <- gca.build_basis (green_columns, cross_interpolate) gca.py:149-179,
@@ -329,6 +330,17 @@ int h2b_matvec_host(h2b_plan* plan, const double* h_x, double* h_y, void* stream
  * with the environment variable H2B_TRACE=1 (3 words per CTA ticket: start
  * ns, end ns, SM id; then 5 words of ticket-range boundaries). */
 int h2b_plan_trace(h2b_plan* plan, unsigned long long* h_out, int64_t cap);
+/* Multi-right-hand-side product Y = A X for 1 <= nrhs <= 16 device vectors
+ * (X: n_cols x nrhs, Y: n_rows x nrhs, row-major, natural dof order) over the
+ * same packed operator as a matvec plan (single-GPU layouts).  The reference
+ * has no block product; each column equals H2Matrix.matvec of that column
+ * (containers.py:254-270) to rounding.  Dense products on the FP64 tensor
+ * cores (mma.sync m8n8k4.f64); level-synchronous launches on `stream`. */
+typedef struct h2b_mmplan h2b_mmplan;
+int h2b_matmat_create(const h2b_layout* layout, h2b_mmplan** out);
+int h2b_matmat_destroy(h2b_mmplan* plan);
+int h2b_matmat(h2b_mmplan* plan, const double* d_X, double* d_Y, int32_t nrhs, void* stream);
+
 /* Diagonal of the (square) operator from the nearfield, natural order. */
 int h2b_diagonal(h2b_plan* plan, double* d_diag, void* stream);
 

@@ -99,7 +99,7 @@ EXPORTS = (
     "h2b_plan_create", "h2b_plan_destroy", "h2b_matvec", "h2b_matvec_host",
     "h2b_diagonal", "h2b_plan_trace", "h2b_dlp_jobs_build", "h2b_dlp_jobs_sizes", "h2b_dlp_jobs_copy",
     "h2b_dlp_jobs_free", "h2b_gca_columns", "h2b_gca_aca", "h2b_cg_workspace_size", "h2b_cg_dot", "h2b_cg_step",
-    "h2b_cg_direction",
+    "h2b_cg_direction", "h2b_matmat_create", "h2b_matmat_destroy", "h2b_matmat",
 )
 
 _lib = None
@@ -145,6 +145,9 @@ def lib():
         L.h2b_dlp_jobs_free.argtypes = [vp]
         L.h2b_gca_columns.argtypes = [ctypes.POINTER(Mesh), vp, ctypes.c_int32, vp, ctypes.c_int,
                                       ctypes.POINTER(GcaBatch), vp, vp]
+        L.h2b_matmat_create.argtypes = [ctypes.POINTER(Layout), ctypes.POINTER(vp)]
+        L.h2b_matmat_destroy.argtypes = [vp]
+        L.h2b_matmat.argtypes = [vp, vp, vp, ctypes.c_int32, vp]
         L.h2b_cg_workspace_size.argtypes = [vp]
         L.h2b_cg_dot.argtypes = [vp, vp, ctypes.c_int64, vp, vp, vp]
         L.h2b_cg_step.argtypes = [ctypes.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]

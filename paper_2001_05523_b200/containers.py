@@ -469,6 +469,14 @@ class H2Matrix:
             self._tplan = _transposed_plan(self)
         return self._tplan.apply(x)
 
+    def matmat(self, X):
+        """Y = A X for a block of right-hand sides X (n_cols x nrhs): numpy in ->
+        numpy out, CUDA tensor -> tensor.  Not in the reference (its matvec is
+        single-vector); column j equals matvec(X[:, j]) to rounding."""
+        if getattr(self, "_mmplan", None) is None:
+            self._mmplan = MatmatPlan(self.plan())
+        return self._mmplan.apply(X)
+
     def diagonal(self):
         assert self.shape[0] == self.shape[1], "diagonal extraction requires a square operator"
         return self.plan().diagonal()
@@ -658,6 +666,58 @@ class MatvecPlan:
         d = D.zeros((self.n_rows,))
         _lib.check(_lib.lib().h2b_diagonal(self.handle, d.data_ptr(), _lib.stream_ptr()))
         return D.host(d)
+
+
+class MatmatPlan:
+    """libh2b block product (h2b_matmat) over a matvec plan's device layout."""
+
+    MAX_RHS = 16
+
+    def __init__(self, mv_plan):
+        self._mv = mv_plan  # owns the layout arrays the block plan points into
+        self.n_rows, self.n_cols = mv_plan.n_rows, mv_plan.n_cols
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().h2b_matmat_create(ctypes.byref(mv_plan.layout), ctypes.byref(h)))
+        self.handle = h
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                _lib.lib().h2b_matmat_destroy(h)
+            except Exception:
+                pass
+
+    def apply_device(self, X, Y=None, stream=None):
+        """Y (n_rows x nrhs) = A X for a CUDA float64 tensor X (n_cols x nrhs),
+        in slices of at most 16 columns (stream-ordered)."""
+        t = D.torch()
+        if X.ndim != 2 or X.shape[0] != self.n_cols:
+            raise ValueError(f"expected a ({self.n_cols}, nrhs) block")
+        nrhs = X.shape[1]
+        if Y is None:
+            Y = t.empty((self.n_rows, nrhs), dtype=t.float64, device=X.device)
+        L = _lib.lib()
+        for j0 in range(0, nrhs, self.MAX_RHS):
+            j1 = min(nrhs, j0 + self.MAX_RHS)
+            xs = X[:, j0:j1].contiguous() if (j0 > 0 or j1 < nrhs or not X.is_contiguous()) else X
+            ys = Y if (j0 == 0 and j1 == nrhs and Y.is_contiguous()) else t.empty((self.n_rows, j1 - j0),
+                                                                                   dtype=t.float64, device=X.device)
+            _lib.check(L.h2b_matmat(self.handle, xs.data_ptr(), ys.data_ptr(), j1 - j0, _lib.stream_ptr(stream)))
+            if ys is not Y:
+                Y[:, j0:j1] = ys
+        return Y
+
+    def apply(self, X):
+        t = D.torch()
+        if isinstance(X, t.Tensor):
+            if X.dtype != t.float64 or not X.is_cuda:
+                raise ValueError("expected a CUDA float64 tensor")
+            return self.apply_device(X)
+        X = np.asarray(X, dtype=np.float64)
+        if X.ndim == 1:
+            return D.host(self.apply_device(D.dev(X[:, None])))[:, 0]
+        return D.host(self.apply_device(D.dev(np.ascontiguousarray(X))))
 
 
 def _transposed_plan(H):
