@@ -36,10 +36,12 @@ namespace {
 
 constexpr int kMmThreads = 256;
 constexpr int kMmWarps = kMmThreads / 32;
-constexpr int kChunk = 128;  // staged B rows per chunk (gathered right-hand sides)
+constexpr int kChunk = 256;  // staged B rows per chunk (gathered right-hand sides)
 
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+    // not volatile: a pure function of its operands, so the compiler may hoist
+    // the operand loads of later steps above it
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                  : "+d"(d[0]), "+d"(d[1])
                  : "d"(a), "d"(b));
 }
@@ -62,6 +64,7 @@ __device__ __forceinline__ void warp_mma(double (&acc)[NT][2], int m0, int M, in
 #pragma unroll
             for (int t = 0; t < NT; ++t) dmma(acc[t], a[u], Bs[(k + 4 * u + q - kb) * R + 8 * t + g]);
     }
+#pragma unroll 4
     for (; k < k1; k += 4) {
         const int kk = k + q;
         const double a = (rowok && kk < k1) ? fa(m0 + g, kk) : 0.0;
@@ -70,11 +73,77 @@ __device__ __forceinline__ void warp_mma(double (&acc)[NT][2], int m0, int M, in
     }
 }
 
+struct d4 {
+    double x, y, z, w;
+};
+// 32-byte streaming load (LDG.256), read once: no L1 allocation
+__device__ __forceinline__ d4 ld_stream4(const double* p) {
+    d4 r;
+    asm("ld.global.nc.L1::no_allocate.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+// acc += A[m0:m0+8, k0:k1] B for a row-major streamed A (32-byte aligned rows,
+// k0 16-aligned): lane (g, q) loads A[m0+g][k + 4q .. k + 4q + 3] with one
+// 32-byte load and feeds them to four mma steps whose k index q stands for
+// column k + 4q + j (the contraction order is free) -- a quarter of the load
+// instructions of the fragment-order loads.  Columns past the last full group
+// of 16 take the scalar path.
+template <int NT>
+__device__ __forceinline__ void warp_mma_stream(double (&acc)[NT][2], int m0, int M, int k0, int k1, int kb,
+                                                const double* A, int64_t ld, const double* Bs);
+
 // streaming operand loads (read once): no L1 allocation
 __device__ __forceinline__ double ld_stream(const double* p) {
     double v;
-    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
     return v;
+}
+
+template <int NT>
+__device__ __forceinline__ void warp_mma_stream(double (&acc)[NT][2], int m0, int M, int k0, int k1, int kb,
+                                                const double* A, int64_t ld, const double* Bs) {
+    constexpr int R = 8 * NT;
+    const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+    const bool rowok = m0 + g < M;
+    const double* row = A + (int64_t)(rowok ? m0 + g : m0) * ld;
+    int k = k0;
+    for (; k + 64 <= k1; k += 64) {
+        d4 a[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) a[u] = rowok ? ld_stream4(row + k + 16 * u + 4 * q) : d4{0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const double* b = Bs + (k + 16 * u + 4 * q - kb) * R + g;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                dmma(acc[t], a[u].x, b[8 * t]);
+                dmma(acc[t], a[u].y, b[R + 8 * t]);
+                dmma(acc[t], a[u].z, b[2 * R + 8 * t]);
+                dmma(acc[t], a[u].w, b[3 * R + 8 * t]);
+            }
+        }
+    }
+    for (; k + 16 <= k1; k += 16) {
+        const d4 a = rowok ? ld_stream4(row + k + 4 * q) : d4{0.0, 0.0, 0.0, 0.0};
+        const double* b = Bs + (k + 4 * q - kb) * R + g;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            dmma(acc[t], a.x, b[8 * t]);
+            dmma(acc[t], a.y, b[R + 8 * t]);
+            dmma(acc[t], a.z, b[2 * R + 8 * t]);
+            dmma(acc[t], a.w, b[3 * R + 8 * t]);
+        }
+    }
+#pragma unroll 4
+    for (; k < k1; k += 4) {
+        const int kk = k + q;
+        const double a = (rowok && kk < k1) ? ld_stream(row + kk) : 0.0;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) dmma(acc[t], a, kk < k1 ? Bs[(kk - kb) * R + 8 * t + g] : 0.0);
+    }
 }
 
 template <int NT>
@@ -95,156 +164,236 @@ __device__ __forceinline__ void warp_store(const double (&acc)[NT][2], int m0, i
     }
 }
 
-// ---- forward transform ------------------------------------------------------
+// ---- work split over the CTA's warps -------------------------------------------
+// Row tiles of 8; with fewer tiles than warps the K range of each tile is split
+// over nsplit warps and the partial sums are added in split order (fixed:
+// deterministic).  Every warp runs the same number of rounds (block barriers).
+struct Split {
+    int tiles, nsplit, per_round, rounds;
+};
 
+__device__ __forceinline__ Split make_split(int M) {
+    Split s;
+    s.tiles = (M + 7) / 8;
+    s.nsplit = s.tiles >= kMmWarps ? 1 : kMmWarps / max(s.tiles, 1);
+    s.per_round = kMmWarps / s.nsplit;
+    s.rounds = (s.tiles + s.per_round - 1) / s.per_round;
+    return s;
+}
+
+// [lo, hi) of split `sp` inside [a, b) (4-aligned pieces)
+__device__ __forceinline__ void split_range(int a, int b, int nsplit, int sp, int& lo, int& hi, int align = 4) {
+    const int per = (((b - a) + nsplit - 1) / nsplit + align - 1) / align * align;
+    lo = min(b, a + sp * per);
+    hi = min(b, lo + per);
+}
+
+// add the split partials (split 0 keeps the sum); all warps call it
 template <int NT>
-__global__ void __launch_bounds__(kMmThreads) k_mm_fwd_leaf(h2b_layout L, const int32_t* __restrict__ leaves,
-                                                            const double* __restrict__ X, int nrhs,
-                                                            double* __restrict__ xhat) {
-    constexpr int R = 8 * NT;
-    extern __shared__ double Bs[];
-    const int t = leaves[blockIdx.x];
-    const int start = L.c_start[t], size = L.c_size[t], k = L.c_rank[t];
-    const double* V = L.c_V + L.c_v_off[t];
-    for (int e = threadIdx.x; e < size * R; e += kMmThreads) {
-        const int i = e / R, r = e - i * R;
-        Bs[e] = r < nrhs ? X[L.col_perm[start + i] * nrhs + r] : 0.0;
-    }
+__device__ __forceinline__ void reduce_splits(double (&acc)[NT][2], const Split& s, double* red) {
+    if (s.nsplit == 1) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sp = warp / s.per_round;
+    double* mine = red + ((size_t)warp * 32 + lane) * 2 * NT;
     __syncthreads();
-    double* out = xhat + L.c_xhat_off[t] * R;
+    if (sp > 0)
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            mine[2 * t] = acc[t][0];
+            mine[2 * t + 1] = acc[t][1];
+        }
+    __syncthreads();
+    if (sp == 0)
+        for (int q = 1; q < s.nsplit; ++q) {
+            const double* o = red + ((size_t)(warp + q * s.per_round) * 32 + lane) * 2 * NT;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                acc[t][0] += o[2 * t];
+                acc[t][1] += o[2 * t + 1];
+            }
+        }
+}
+
+// C (M x R) = A (M x K) B with B (K x R) fully staged in Bs; out(m, n, value)
+template <int NT, class FA, class FO>
+__device__ void cta_product(int M, int K, FA fa, const double* Bs, double* red, FO out) {
+    const Split s = make_split(M);
     const int warp = threadIdx.x >> 5;
-    for (int m0 = 8 * warp; m0 < k; m0 += 8 * kMmWarps) {
+    const int sp = warp / s.per_round;
+    for (int rd = 0; rd < s.rounds; ++rd) {
+        const int tile = rd * s.per_round + warp % s.per_round;
         double acc[NT][2];
         zero(acc);
-        warp_mma<NT>(acc, m0, k, 0, size, 0, [&](int m, int kk) { return V[(int64_t)kk * k + m]; }, Bs);
-        warp_store<NT>(acc, m0, k, [&](int m, int n, double v) { out[m * R + n] = v; });
+        int lo, hi;
+        split_range(0, K, s.nsplit, sp, lo, hi);
+        if (tile < s.tiles && lo < hi) warp_mma<NT>(acc, 8 * tile, M, lo, hi, 0, fa, Bs);
+        reduce_splits<NT>(acc, s, red);
+        if (tile < s.tiles && sp == 0) warp_store<NT>(acc, 8 * tile, M, out);
+    }
+}
+
+// C (M x R) = A (M x K, row-major, ld, streamed once) B with B row kk =
+// src[idx[kk]] (src_w wide, first nrhs columns), staged kChunk rows at a time;
+// then C += A2 (M x K2) B2 with B2 (K2 x R) contiguous at src2 (leaf expansion);
+// out(m, n, value)
+template <int NT, class FA2, class FO>
+__device__ void cta_streamed(int M, const double* A, int64_t ld, int K, const int32_t* idx, const double* src,
+                             int src_w, int nrhs, int K2, FA2 fa2, const double* src2, double* Bs, double* red,
+                             FO out) {
+    constexpr int R = 8 * NT;
+    const Split s = make_split(M);
+    const int warp = threadIdx.x >> 5;
+    const int sp = warp / s.per_round;
+    for (int rd = 0; rd < s.rounds; ++rd) {
+        const int tile = rd * s.per_round + warp % s.per_round;
+        const bool act = tile < s.tiles;
+        double acc[NT][2];
+        zero(acc);
+        for (int kc = 0; kc < K; kc += kChunk) {
+            const int kn = min(kChunk, K - kc);
+            __syncthreads();
+            for (int e = threadIdx.x; e < kn * R; e += kMmThreads) {
+                const int i = e / R, r = e - i * R;
+                Bs[e] = r < nrhs ? src[(int64_t)idx[kc + i] * src_w + r] : 0.0;
+            }
+            __syncthreads();
+            int lo, hi;
+            split_range(kc, kc + kn, s.nsplit, sp, lo, hi, 16);
+            if (act && lo < hi) warp_mma_stream<NT>(acc, 8 * tile, M, lo, hi, kc, A, ld, Bs);
+        }
+        if (K2 > 0) {
+            __syncthreads();
+            for (int e = threadIdx.x; e < K2 * R; e += kMmThreads) Bs[e] = src2[e];
+            __syncthreads();
+            int lo, hi;
+            split_range(0, K2, s.nsplit, sp, lo, hi);
+            if (act && lo < hi) warp_mma<NT>(acc, 8 * tile, M, lo, hi, 0, fa2, Bs);
+        }
+        reduce_splits<NT>(acc, s, red);
+        if (act && sp == 0) warp_store<NT>(acc, 8 * tile, M, out);
+    }
+}
+
+// ---- tree transforms: one warp per cluster ---------------------------------------
+// The per-cluster products are small (ranks ~25-50): a warp stages its B in a
+// private shared-memory slice and runs all row tiles itself, so a CTA keeps
+// kMmWarps clusters in flight without block barriers.
+
+// all row tiles of C (M x R) = A (M x K) B, B staged at Bw; out(m, n, value)
+template <int NT, class FA, class FO>
+__device__ __forceinline__ void warp_product(int M, int K, FA fa, const double* Bw, FO out) {
+    for (int m0 = 0; m0 < M; m0 += 8) {
+        double acc[NT][2];
+        zero(acc);
+        warp_mma<NT>(acc, m0, M, 0, K, 0, fa, Bw);
+        warp_store<NT>(acc, m0, M, out);
     }
 }
 
 template <int NT>
-__global__ void __launch_bounds__(kMmThreads) k_mm_fwd_level(h2b_layout L, const int32_t* __restrict__ nodes,
-                                                             double* __restrict__ xhat) {
+__global__ void __launch_bounds__(kMmThreads) k_mm_fwd_leaf(h2b_layout L, const int32_t* __restrict__ leaves, int n,
+                                                            const double* __restrict__ X, int nrhs,
+                                                            double* __restrict__ xhat, int slice) {
     constexpr int R = 8 * NT;
     extern __shared__ double Bs[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i = blockIdx.x * kMmWarps + warp;
+    if (i >= n) return;
+    double* Bw = Bs + (size_t)warp * slice;
+    const int t = leaves[i];
+    const int start = L.c_start[t], size = L.c_size[t], k = L.c_rank[t];
+    const double* V = L.c_V + L.c_v_off[t];
+    for (int e = lane; e < size * R; e += 32) {
+        const int r = e % R;
+        Bw[e] = r < nrhs ? X[L.col_perm[start + e / R] * nrhs + r] : 0.0;
+    }
+    __syncwarp();
+    double* out = xhat + L.c_xhat_off[t] * R;
+    warp_product<NT>(k, size, [&](int m, int kk) { return V[(int64_t)kk * k + m]; }, Bw,
+                     [&](int m, int c, double v) { out[m * R + c] = v; });
+}
+
+// inner levels: one CTA per cluster (split-K over the warps measured faster
+// than a warp per cluster for the transfer products)
+template <int NT>
+__global__ void __launch_bounds__(kMmThreads) k_mm_fwd_level(h2b_layout L, const int32_t* __restrict__ nodes,
+                                                             double* __restrict__ xhat, int bs_doubles) {
+    constexpr int R = 8 * NT;
+    extern __shared__ double Bs[];
+    double* red = Bs + bs_doubles;
     const int p = nodes[blockIdx.x];
     const int kp = L.c_rank[p];
     const int c0 = L.c_child[2 * p], c1 = L.c_child[2 * p + 1];
     const int k0 = L.c_rank[c0], k1 = L.c_rank[c1];
     // B = [x_hat_c0; x_hat_c1] ((k0 + k1) x R), A = [E_c0^T, E_c1^T] (kp x (k0 + k1))
-    for (int e = threadIdx.x; e < (k0 + k1) * R; e += kMmThreads) {
-        const int i = e / R, r = e - i * R;
-        Bs[e] = i < k0 ? xhat[(L.c_xhat_off[c0] + i) * R + r] : xhat[(L.c_xhat_off[c1] + i - k0) * R + r];
-    }
+    const double* x0 = xhat + L.c_xhat_off[c0] * R;
+    const double* x1 = xhat + L.c_xhat_off[c1] * R;
+    for (int e = threadIdx.x; e < (k0 + k1) * R; e += kMmThreads) Bs[e] = e < k0 * R ? x0[e] : x1[e - k0 * R];
     __syncthreads();
     const double* E0 = L.c_E + L.c_e_off[c0];
     const double* E1 = L.c_E + L.c_e_off[c1];
     double* out = xhat + L.c_xhat_off[p] * R;
-    const int warp = threadIdx.x >> 5;
-    for (int m0 = 8 * warp; m0 < kp; m0 += 8 * kMmWarps) {
-        double acc[NT][2];
-        zero(acc);
-        warp_mma<NT>(acc, m0, kp, 0, k0, 0, [&](int m, int kk) { return E0[(int64_t)kk * kp + m]; }, Bs);
-        warp_mma<NT>(acc, m0, kp, k0, k0 + k1, 0,
-                     [&](int m, int kk) { return E1[(int64_t)(kk - k0) * kp + m]; }, Bs);
-        warp_store<NT>(acc, m0, kp, [&](int m, int n, double v) { out[m * R + n] = v; });
-    }
-}
-
-// ---- streamed products: couplings and nearfield -------------------------------
-// C (M x R) = A (M x K, row-major, ld) B where B row kk = src[idx[kk]] (R wide,
-// or nrhs wide from X when x_src); K staged in chunks of kChunk rows.
-template <int NT>
-__device__ void streamed_rows(double (&acc)[NT][2], int m0, int M, const double* A, int64_t ld, int K,
-                              const int32_t* idx, const double* src, int src_w, int nrhs, double* Bs) {
-    constexpr int R = 8 * NT;
-    for (int kc = 0; kc < K; kc += kChunk) {
-        const int kn = min(kChunk, K - kc);
-        __syncthreads();
-        for (int e = threadIdx.x; e < kn * R; e += kMmThreads) {
-            const int i = e / R, r = e - i * R;
-            Bs[e] = r < nrhs ? src[(int64_t)idx[kc + i] * src_w + r] : 0.0;
-        }
-        __syncthreads();
-        if (m0 < M)
-            warp_mma<NT>(acc, m0, M, kc, kc + kn, kc, [&](int m, int kk) { return ld_stream(A + (int64_t)m * ld + kk); },
-                         Bs);
-    }
-}
-
-template <int NT>
-__global__ void __launch_bounds__(kMmThreads) k_mm_cpl(h2b_layout L, const int32_t* __restrict__ nodes,
-                                                       const double* __restrict__ xhat, double* __restrict__ ycpl) {
-    constexpr int R = 8 * NT;
-    extern __shared__ double Bs[];
-    const int t = nodes[blockIdx.x];
-    const int k = L.r_rank[t], K = L.s_cols[t];
-    const double* S = L.S + L.s_off[t];
-    const int32_t* idx = L.s_gidx + L.s_goff[t];
-    double* out = ycpl + L.r_yhat_off[t] * R;
-    const int warp = threadIdx.x >> 5;
-    // every warp takes part in the staging: loop over the same number of tiles
-    const int tiles = (k + 7) / 8, rounds = (tiles + kMmWarps - 1) / kMmWarps;
-    for (int rd = 0; rd < rounds; ++rd) {
-        const int m0 = 8 * (rd * kMmWarps + warp);
-        double acc[NT][2];
-        zero(acc);
-        streamed_rows<NT>(acc, m0, k, S, K, K, idx, xhat, R, R, Bs);
-        if (m0 < k) warp_store<NT>(acc, m0, k, [&](int m, int n, double v) { out[m * R + n] = v; });
-    }
+    cta_product<NT>(kp, k0 + k1,
+                    [&](int m, int kk) { return kk < k0 ? E0[(int64_t)kk * kp + m] : E1[(int64_t)(kk - k0) * kp + m]; },
+                    Bs, red, [&](int m, int n, double v) { out[m * R + n] = v; });
 }
 
 template <int NT>
 __global__ void __launch_bounds__(kMmThreads) k_mm_bwd_level(h2b_layout L, const int32_t* __restrict__ nodes,
-                                                             const double* __restrict__ ycpl, double* __restrict__ v) {
+                                                             const double* __restrict__ ycpl, double* __restrict__ v,
+                                                             int bs_doubles) {
     constexpr int R = 8 * NT;
     extern __shared__ double Bs[];
+    double* red = Bs + bs_doubles;
     const int t = nodes[blockIdx.x];
     const int k = L.r_rank[t], p = L.r_parent[t];
     const bool cpl = L.s_cols[t] > 0;
     const int kp = p >= 0 ? L.r_rank[p] : 0;
-    for (int e = threadIdx.x; e < kp * R; e += kMmThreads) Bs[e] = v[L.r_yhat_off[p] * R + e];
+    if (kp > 0) {
+        const double* vp = v + L.r_yhat_off[p] * R;
+        for (int e = threadIdx.x; e < kp * R; e += kMmThreads) Bs[e] = vp[e];
+    }
     __syncthreads();
     const double* E = L.r_E + (p >= 0 ? L.r_e_off[t] : 0);
     const double* yc = ycpl + L.r_yhat_off[t] * R;
     double* out = v + L.r_yhat_off[t] * R;
-    const int warp = threadIdx.x >> 5;
-    for (int m0 = 8 * warp; m0 < k; m0 += 8 * kMmWarps) {
-        double acc[NT][2];
-        zero(acc);
-        if (kp > 0) warp_mma<NT>(acc, m0, k, 0, kp, 0, [&](int m, int kk) { return E[(int64_t)m * kp + kk]; }, Bs);
-        warp_store<NT>(acc, m0, k, [&](int m, int n, double val) { out[m * R + n] = val + (cpl ? yc[m * R + n] : 0.0); });
-    }
+    cta_product<NT>(k, kp, [&](int m, int kk) { return E[(int64_t)m * kp + kk]; }, Bs, red,
+                    [&](int m, int n, double val) { out[m * R + n] = val + (cpl ? yc[m * R + n] : 0.0); });
+}
+
+// ---- couplings, downward transform, nearfield ------------------------------------
+
+template <int NT>
+__global__ void __launch_bounds__(kMmThreads) k_mm_cpl(h2b_layout L, const int32_t* __restrict__ nodes,
+                                                       const double* __restrict__ xhat, double* __restrict__ ycpl,
+                                                       int bs_doubles) {
+    constexpr int R = 8 * NT;
+    extern __shared__ double Bs[];
+    double* red = Bs + bs_doubles;
+    const int t = nodes[blockIdx.x];
+    const int k = L.r_rank[t], K = L.s_cols[t];
+    double* out = ycpl + L.r_yhat_off[t] * R;
+    cta_streamed<NT>(k, L.S + L.s_off[t], K, K, L.s_gidx + L.s_goff[t], xhat, R, R, 0,
+                     [](int, int) { return 0.0; }, nullptr, Bs, red,
+                     [&](int m, int n, double v) { out[m * R + n] = v; });
 }
 
 template <int NT>
 __global__ void __launch_bounds__(kMmThreads) k_mm_leaf(h2b_layout L, const int32_t* __restrict__ leaves,
                                                         const double* __restrict__ X, int nrhs,
-                                                        const double* __restrict__ v, double* __restrict__ Y) {
+                                                        const double* __restrict__ v, double* __restrict__ Y,
+                                                        int bs_doubles) {
     constexpr int R = 8 * NT;
     extern __shared__ double Bs[];
+    double* red = Bs + bs_doubles;
     const int t = leaves[blockIdx.x];
     const int start = L.r_start[t], size = L.r_size[t], k = L.r_rank[t], C = L.d_cols[t];
-    const double* Dm = L.D + L.d_off[t];
-    const int32_t* idx = L.d_gidx + L.d_goff[t];
     const double* V = L.r_V + L.r_v_off[t];
-    const int warp = threadIdx.x >> 5;
-    const int tiles = (size + 7) / 8, rounds = (tiles + kMmWarps - 1) / kMmWarps;
-    for (int rd = 0; rd < rounds; ++rd) {
-        const int m0 = 8 * (rd * kMmWarps + warp);
-        double acc[NT][2];
-        zero(acc);
-        streamed_rows<NT>(acc, m0, size, Dm, C, C, idx, X, nrhs, nrhs, Bs);
-        // + V_t v_t
-        __syncthreads();
-        for (int e = threadIdx.x; e < k * R; e += kMmThreads) Bs[e] = v[L.r_yhat_off[t] * R + e];
-        __syncthreads();
-        if (m0 < size) {
-            if (k > 0) warp_mma<NT>(acc, m0, size, 0, k, 0, [&](int m, int kk) { return V[(int64_t)m * k + kk]; }, Bs);
-            warp_store<NT>(acc, m0, size, [&](int m, int n, double val) {
-                if (n < nrhs) Y[L.row_perm[start + m] * nrhs + n] = val;
-            });
-        }
-    }
+    cta_streamed<NT>(size, L.D + L.d_off[t], C, C, L.d_gidx + L.d_goff[t], X, nrhs, nrhs, k,
+                     [&](int m, int kk) { return V[(int64_t)m * k + kk]; }, v + L.r_yhat_off[t] * R, Bs, red,
+                     [&](int m, int n, double val) {
+                         if (n < nrhs) Y[L.row_perm[start + m] * nrhs + n] = val;
+                     });
 }
 
 template <typename T>
@@ -258,30 +407,36 @@ int run_mm(h2b_mmplan* p, const double* X, int nrhs, double* Y, cudaStream_t st)
     constexpr int R = 8 * NT;
     const h2b_layout& L = p->L;
     const int32_t* lists = p->d_lists;
-    const size_t sm_small = (size_t)std::max(64, p->max_c_node) * R * sizeof(double);
-    const size_t sm_chunk = (size_t)std::max(kChunk, 64) * R * sizeof(double);
-    const size_t sm_leaf = std::max(sm_chunk, (size_t)512 * R * sizeof(double));
-    for (auto* f : {(const void*)k_mm_fwd_leaf<NT>, (const void*)k_mm_fwd_level<NT>, (const void*)k_mm_cpl<NT>,
-                    (const void*)k_mm_bwd_level<NT>, (const void*)k_mm_leaf<NT>})
-        H2B_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_leaf + (int)sm_small));
+    // streamed products: a chunk of gathered rows (or a leaf's ranks) + the
+    // split-reduction buffer; tree transforms: one B slice per warp
+    const int bs = std::max(std::max(kChunk, p->max_c_node), 64) * R;
+    const size_t sm = (size_t)(bs + kMmWarps * 32 * 2 * NT) * sizeof(double);
+    const int slice = std::max(p->max_c_node, 64) * R;
+    const size_t sm_tree = (size_t)kMmWarps * slice * sizeof(double);
+    for (auto* f : {(const void*)k_mm_cpl<NT>, (const void*)k_mm_leaf<NT>, (const void*)k_mm_fwd_level<NT>,
+                    (const void*)k_mm_bwd_level<NT>})
+        H2B_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    for (auto* f : {(const void*)k_mm_fwd_leaf<NT>})
+        H2B_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_tree));
+    auto blocks = [](int64_t n) { return (unsigned)((n + kMmWarps - 1) / kMmWarps); };
     if (p->n_leaf_c > 0)
-        k_mm_fwd_leaf<NT><<<(unsigned)p->n_leaf_c, kMmThreads, sm_small, st>>>(L, lists + p->off_leaf_c, X, nrhs,
-                                                                              p->xhat);
+        k_mm_fwd_leaf<NT><<<blocks(p->n_leaf_c), kMmThreads, sm_tree, st>>>(L, lists + p->off_leaf_c,
+                                                                           (int)p->n_leaf_c, X, nrhs, p->xhat, slice);
     for (int lv = 0; lv + 1 < (int)p->fwd_level_off.size(); ++lv) {
         const int64_t a = p->fwd_level_off[lv], b = p->fwd_level_off[lv + 1];
         if (b > a)
-            k_mm_fwd_level<NT><<<(unsigned)(b - a), kMmThreads, sm_small, st>>>(L, lists + p->off_fwd + a, p->xhat);
+            k_mm_fwd_level<NT><<<(unsigned)(b - a), kMmThreads, sm, st>>>(L, lists + p->off_fwd + a, p->xhat, bs);
     }
     if (p->n_cpl > 0)
-        k_mm_cpl<NT><<<(unsigned)p->n_cpl, kMmThreads, sm_chunk, st>>>(L, lists + p->off_cpl, p->xhat, p->ycpl);
+        k_mm_cpl<NT><<<(unsigned)p->n_cpl, kMmThreads, sm, st>>>(L, lists + p->off_cpl, p->xhat, p->ycpl, bs);
     for (int lv = 0; lv + 1 < (int)p->bwd_level_off.size(); ++lv) {
         const int64_t a = p->bwd_level_off[lv], b = p->bwd_level_off[lv + 1];
         if (b > a)
-            k_mm_bwd_level<NT><<<(unsigned)(b - a), kMmThreads, sm_small, st>>>(L, lists + p->off_bwd + a, p->ycpl,
-                                                                               p->v);
+            k_mm_bwd_level<NT><<<(unsigned)(b - a), kMmThreads, sm, st>>>(L, lists + p->off_bwd + a, p->ycpl, p->v,
+                                                                         bs);
     }
     if (p->n_leaf_r > 0)
-        k_mm_leaf<NT><<<(unsigned)p->n_leaf_r, kMmThreads, sm_leaf, st>>>(L, lists + p->off_leaf_r, X, nrhs, p->v, Y);
+        k_mm_leaf<NT><<<(unsigned)p->n_leaf_r, kMmThreads, sm, st>>>(L, lists + p->off_leaf_r, X, nrhs, p->v, Y, bs);
     H2B_CUDA_TRY(cudaGetLastError());
     return ok();
 }
