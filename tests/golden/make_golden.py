@@ -21,6 +21,9 @@ What is pinned (all produced by the reference's own public functions):
   h2_cfg0.npz      full GCA basis + sampled couplings + matvec x/y of config 0
   h2_cfg1.npz      pivots/ranks digests + matvec x/y of config 1
   h2_dlp4.npz      level-4 double-layer H^2 (P0 x P1) matvec x/y + basis
+  cube4.npz        config-4 geometry at n=4 (this repo's cube_shell_mesh arrays fed
+                   to the reference): trees + block trees (grid-aligned: exact
+                   ties in the splits), SLP/DLP GCA H^2 matvec x/y, SLP basis
 """
 
 import argparse
@@ -337,6 +340,40 @@ def gen_h2_dlp4():
     np.savez_compressed(os.path.join(HERE, "h2_dlp4.npz"), **out)
 
 
+def gen_cube():
+    """Config 4 geometry (3x3x3 unit cubes minus the centre, merged surface) at
+    n=4: 1920 flat panels on a lattice -- the split coordinates tie exactly."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from paper_2001_05523_b200.mesh import cube_shell_mesh  # the input geometry only
+    from h2bem.mesh import SurfaceMesh
+
+    ours = cube_shell_mesh(4)
+    mesh = SurfaceMesh(ours.vertices, ours.triangles)
+    ctx = AssemblyContext(mesh)
+    out = {"vertices": mesh.vertices, "triangles": mesh.triangles}
+    t0 = build_cluster_tree(spaces.DofSpace(spaces.P0, mesh).support_boxes(), 32)
+    t1 = build_cluster_tree(spaces.DofSpace(spaces.P1, mesh).support_boxes(), 32)
+    for name, t in (("p0", t0), ("p1", t1)):
+        for k, v in tree_arrays(t).items():
+            out[f"{name}_{k}"] = v
+    bs, bd = BlockTree(t0, t0, 2.0), BlockTree(t0, t1, 2.0)
+    out["slp_far"], out["slp_near"] = block_arrays(bs)
+    out["dlp_far"], out["dlp_near"] = block_arrays(bd)
+    rb = gca.build_basis(ctx, t0, gca.P0_SLP, 3, 1e-4, threads=THREADS)
+    cb = gca.build_basis(ctx, t1, gca.P1_DLP, 3, 1e-4, threads=THREADS)
+    log("cube bases")
+    ba = basis_arrays("", rb, t0)
+    out["slp_ranks"], out["slp_pivots"] = ba["ranks"], ba["pivots"]
+    rng = np.random.default_rng(4)
+    Hs = split_h2(ctx, kernels.SLP, bs, rb, rb, 3, 4)
+    out["x_slp"] = rng.uniform(-1.0, 1.0, Hs.shape[1])
+    out["y_slp"] = Hs.matvec(out["x_slp"])
+    Hd = split_h2(ctx, kernels.DLP, bd, rb, cb, 3, 4)
+    out["x_dlp"] = rng.uniform(-1.0, 1.0, Hd.shape[1])
+    out["y_dlp"] = Hd.matvec(out["x_dlp"])
+    np.savez_compressed(os.path.join(HERE, "cube4.npz"), **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-large", action="store_true")
@@ -351,6 +388,7 @@ def main():
         ("h2_cfg0", gen_h2_cfg0),
         ("h2_dlp4", gen_h2_dlp4),
         ("h2_cfg1", gen_h2_cfg1),
+        ("cube", gen_cube),
     ]
     if not args.skip_large:
         steps.append(("struct_large", gen_structure_large))

@@ -199,3 +199,16 @@ def test_green_points_batch_matches_per_cluster_bits():
             assert np.array_equal(got[i, :, :3], gq.points)
             assert np.array_equal(got[i, :, 3], np.sqrt(gq.weights))
             assert np.array_equal(got[i, :, 4:7], gq.normals)
+
+
+def test_gca_pivots_bit_exact_cube_shell():
+    """Host GCA basis on the config-4 geometry: ranks and pivots bit-exact."""
+    from paper_2001_05523_b200 import clustering as C
+    from paper_2001_05523_b200.mesh import cube_shell_mesh
+
+    g = golden("cube4.npz")
+    m = cube_shell_mesh(4)
+    t0 = C.build_cluster_tree(S.DofSpace(S.P0, m).support_boxes(), 32)
+    b = gca.build_basis(AssemblyContext(m), t0, gca.P0_SLP, 3, 1e-4, threads=4)
+    assert np.array_equal(np.array([b.rank[u] for u in range(t0.n_nodes)]), g["slp_ranks"])
+    assert np.array_equal(np.concatenate([b.pivots[u] for u in range(t0.n_nodes)]), g["slp_pivots"])

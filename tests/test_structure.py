@@ -128,3 +128,23 @@ def test_cube_shell_mesh():
     assert m.n_triangles == 60 * 2 * 4
     # outer volume 27 minus the cavity 1
     assert abs(m.signed_volume() - 26.0) < 1e-12
+
+
+def test_cube_shell_structure_exact():
+    """Config-4 geometry (grid-aligned flat panels: split coordinates tie
+    exactly) -- trees and block trees bit-exact vs the reference run on the
+    same mesh arrays (tests/golden/make_golden.py gen_cube)."""
+    g = golden("cube4.npz")
+    m = M.cube_shell_mesh(4)
+    assert np.array_equal(m.vertices, g["vertices"]) and np.array_equal(m.triangles, g["triangles"])
+    trees = {}
+    for sp, kind in (("p0", S.P0), ("p1", S.P1)):
+        t = C.build_cluster_tree(S.DofSpace(kind, m).support_boxes(), 32)
+        for a in ("perm", "start", "end", "left", "right", "boxes"):
+            assert np.array_equal(getattr(t, a), g[f"{sp}_{a}"]), (sp, a)
+        assert np.array_equal(t.depth_of, g[f"{sp}_depth"])
+        trees[sp] = t
+    bt = C.BlockTree(trees["p0"], trees["p0"], 2.0)
+    assert np.array_equal(bt.far_uids, g["slp_far"]) and np.array_equal(bt.near_uids, g["slp_near"])
+    bt = C.BlockTree(trees["p0"], trees["p1"], 2.0)
+    assert np.array_equal(bt.far_uids, g["dlp_far"]) and np.array_equal(bt.near_uids, g["dlp_near"])
