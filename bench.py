@@ -239,6 +239,9 @@ def run_ours(args, cfg):
     t_reg = ev_time(torch, lambda: slp_jobs.run(table, Dn), nf_reps)
     fc = flop_counts(ctx, bt, cfg, slp_jobs)
     S = assemble_couplings(ctx, "slp", bt, basis, basis, cfg["q_reg"])
+    # coupling matrices S_b = G[pivots_t, pivots_s] (gca.assemble_h2), host job list + device quadrature
+    t_cpl = ev_time(torch, lambda: assemble_couplings(ctx, "slp", bt, basis, basis, cfg["q_reg"]), 3)
+    n_cpl_pairs = int(sum(basis.rank[int(t)] * basis.rank[int(u)] for t, u in bt.far_uids))
     H = H2Matrix.from_device(bt, basis, basis, S, Dn)
     n = H.shape[0]
 
@@ -354,6 +357,8 @@ def run_ours(args, cfg):
         "nearfield": {
             "pairs_per_s": fc["pairs"] / nf_time, "pairs": fc["pairs"], "ms": nf_time * 1e3,
             "touch_classify_ms": t_touch * 1e3,
+            "couplings": {"ms": t_cpl * 1e3, "pairs": n_cpl_pairs, "pairs_per_s": n_cpl_pairs / t_cpl,
+                          "note": "assemble_couplings end to end (host job list + k_blocks_slp, symmetric)"},
             "singular": {"ms": t_sing * 1e3, "pairs": fc["singular_pairs"], "evaluated": fc["singular_evaluated"],
                          "gflop": fc["sing_flops"] / 1e9,
                          "tflops": fc["sing_flops"] / t_sing / 1e12,
