@@ -42,7 +42,8 @@ class ProblemSetup:
         if key not in self._bases:
             tree = self.tree_p0 if tree_name == "p0" else self.tree_p1
             p = self.params
-            self._bases[key] = gca.build_basis(self.ctx, tree, flavor, p.order, p.eps_aca, threads=p.threads)
+            self._bases[key] = gca.build_basis(self.ctx, tree, flavor, p.order, p.eps_aca, threads=p.threads,
+                                               device=getattr(p, "gca_device", False))
         return self._bases[key]
 
     def operator(self, kind, method=None):
