@@ -579,8 +579,9 @@ __constant__ double c_lam[64 * 3];  // barycentrics of the regular rule, Q <= 64
 // 1/r^3 = 1.5 (1/2)^(3/2) t^3 (5/3 + g t^2) with g = -r^2/2, t ~ rsqrt(-g)
 constexpr double kDlpFold = 1.5 * 0.35355339059327376220042218 / (4.0 * kPi);
 
-template <int Q>
-__global__ void __launch_bounds__(256) k_blocks_dlp(const double* __restrict__ P, int64_t F,
+// JC column points per register chunk (fewer registers -> more resident CTAs)
+template <int Q, int JC = Q, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_blocks_dlp(const double* __restrict__ P, int64_t F,
                                                    const int32_t* __restrict__ T,
                                                    const double* __restrict__ Nrm,
                                                    const int64_t* __restrict__ jobs,
@@ -684,39 +685,46 @@ __global__ void __launch_bounds__(256) k_blocks_dlp(const double* __restrict__ P
                 }
             } else {
                 const double n0 = pn[b], n1 = pn[PT + b], n2 = pn[2 * PT + b];
-                double y0[Q], y1[Q], y2[Q], yh[Q], yw[Q], yn[Q];
-#pragma unroll
-                for (int j = 0; j < Q; ++j) {
-                    const int s = j * PT + b;
-                    y0[j] = px[s];
-                    y1[j] = px[Q * PT + s];
-                    y2[j] = px[2 * Q * PT + s];
-                    yh[j] = px[3 * Q * PT + s];
-                    yw[j] = px[4 * Q * PT + s];
-                    yn[j] = px[5 * Q * PT + s];
-                }
                 double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+#pragma unroll 1
+                for (int j0 = 0; j0 < Q; j0 += JC) {
+                    double y0[JC], y1[JC], y2[JC], yh[JC], yw[JC], yn[JC];
 #pragma unroll
-                for (int i = 0; i < Q; ++i) {
-                    const int s = i * RT + a;
-                    const double x0 = rx[s], x1 = rx[Q * RT + s], x2 = rx[2 * Q * RT + s];
-                    const double xh = rx[3 * Q * RT + s], xw = rx[4 * Q * RT + s];
-                    const double xn = fma(x2, n2, fma(x1, n1, x0 * n0));
-                    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-#pragma unroll
-                    for (int j = 0; j < Q; ++j) {
-                        const double g = fma(x0, y0[j], fma(x1, y1[j], fma(x2, y2[j], xh + yh[j])));
-                        const double t = rsqrt_seed(-g);
-                        const double s2 = t * t;
-                        const double c3 = fma(g, s2, 5.0 / 3.0);
-                        const double k = ((xn - yn[j]) * c3) * ((s2 * t) * yw[j]);
-                        a0 = fma(k, c_lam[3 * j], a0);
-                        a1 = fma(k, c_lam[3 * j + 1], a1);
-                        a2 = fma(k, c_lam[3 * j + 2], a2);
+                    for (int j = 0; j < JC; ++j) {
+                        if (j0 + j < Q) {
+                            const int s = (j0 + j) * PT + b;
+                            y0[j] = px[s];
+                            y1[j] = px[Q * PT + s];
+                            y2[j] = px[2 * Q * PT + s];
+                            yh[j] = px[3 * Q * PT + s];
+                            yw[j] = px[4 * Q * PT + s];
+                            yn[j] = px[5 * Q * PT + s];
+                        }
                     }
-                    t0 = fma(xw, a0, t0);
-                    t1 = fma(xw, a1, t1);
-                    t2 = fma(xw, a2, t2);
+#pragma unroll(JC < Q ? 1 : Q)
+                    for (int i = 0; i < Q; ++i) {
+                        const int s = i * RT + a;
+                        const double x0 = rx[s], x1 = rx[Q * RT + s], x2 = rx[2 * Q * RT + s];
+                        const double xh = rx[3 * Q * RT + s], xw = rx[4 * Q * RT + s];
+                        const double xn = fma(x2, n2, fma(x1, n1, x0 * n0));
+                        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll
+                        for (int j = 0; j < JC; ++j) {
+                            if (j0 + j < Q) {
+                                const double g = fma(x0, y0[j], fma(x1, y1[j], fma(x2, y2[j], xh + yh[j])));
+                                const double t = rsqrt_seed(-g);
+                                const double s2 = t * t;
+                                const double c3 = fma(g, s2, 5.0 / 3.0);
+                                const double k = ((xn - yn[j]) * c3) * ((s2 * t) * yw[j]);
+                                a0 = fma(k, c_lam[3 * (j0 + j)], a0);
+                                a1 = fma(k, c_lam[3 * (j0 + j) + 1], a1);
+                                a2 = fma(k, c_lam[3 * (j0 + j) + 2], a2);
+                            }
+                        }
+                        t0 = fma(xw, a0, t0);
+                        t1 = fma(xw, a1, t1);
+                        t2 = fma(xw, a2, t2);
+                    }
                 }
                 v0 = t0;
                 v1 = t1;
@@ -792,13 +800,20 @@ int launch_slp(const h2b_mesh* m, const double* P, const h2b_jobs* jobs, const h
     return ok();
 }
 
-template <int Q>
+#ifndef H2B_DLP9_JC
+#define H2B_DLP9_JC 3  // measured: 5.0 -> 4.3 ms at config 1 (114 registers, 2 CTAs/SM)
+#endif
+#ifndef H2B_DLP9_MINB
+#define H2B_DLP9_MINB 1
+#endif
+
+template <int Q, int JC = Q, int MINB = 1>
 int launch_dlp(const h2b_mesh* m, const double* P, const h2b_dlp_jobs* jobs, const h2b_touch* t,
                const double* tv, double* out, int* flags, cudaStream_t st) {
     const size_t sm = (size_t)(5 * Q * kTile + 6 * Q * kDlpMaxPanels + 3 * kDlpMaxPanels +
                                kDlpRowChunk * kDlpMaxPanels * 3) * sizeof(double) +
                       (size_t)(4 * kTile + 4 * kDlpMaxPanels) * sizeof(int);
-    auto kern = k_blocks_dlp<Q>;
+    auto kern = k_blocks_dlp<Q, JC, MINB>;
     H2B_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     if (jobs->n_jobs > 0)
         kern<<<(unsigned)jobs->n_jobs, 256, sm, st>>>(P, m->n_triangles, m->d_triangles, m->d_normals,
@@ -997,8 +1012,10 @@ extern "C" int h2b_pair_blocks_dlp(const h2b_mesh* m, const double* d_panel_poin
     switch (Q) {
         case 1: rc = launch_dlp<1>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
         case 4: rc = launch_dlp<4>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
-        case 9: rc = launch_dlp<9>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
-        case 16: rc = launch_dlp<16>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
+        case 9:
+            rc = launch_dlp<9, H2B_DLP9_JC, H2B_DLP9_MINB>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st);
+            break;
+        case 16: rc = launch_dlp<16, 4>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
         default: rc = fail(H2B_ERR_INVALID, "h2b_pair_blocks_dlp: supported regular orders q = 1..4");
     }
     if (rc) return rc;

@@ -40,7 +40,40 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     t_ev = ctx.dmesh.touch()
     n_touch_eval = int(t_ev.case_counts[0] + (t_ev.case_counts[1] + t_ev.case_counts[2]) // 2)
     fl = (sj.evaluated - n_touch_eval) * 81 * 12
-    print(json.dumps({"ms": t * 1e3, "tflops": fl / t / 1e12, "err_vs_first": err}))
+    res = {"slp_ms": t * 1e3, "slp_tflops": fl / t / 1e12, "err_vs_first": err}
+    # double layer (P0 rows x P1 columns): the regular pair-block kernel with the vertex scatter
+    import ctypes
+
+    from paper_2001_05523_b200 import _lib
+    from paper_2001_05523_b200 import device as D
+    from paper_2001_05523_b200.containers import _near_blocks
+
+    t1 = C.build_cluster_tree(spaces.DofSpace(spaces.P1, m).support_boxes(), 64)
+    btd = C.BlockTree(tree, t1, 2.0)
+    layd = near_layout(btd)
+    packed = kernels.build_dlp_jobs(m, _near_blocks(btd, layd))
+    tabd = kernels.SingularTable(ctx.dmesh, "dlp", 4)
+    pp, Qd, lam = ctx.dmesh.panel_points(3)
+    tt = {k: D.dev(v) for k, v in packed.items()}
+    cj = _lib.DlpJobs(len(packed["jobs"]), tt["jobs"].data_ptr(), tt["row_idx"].data_ptr(), tt["pan_idx"].data_ptr(),
+                      tt["inc_ptr"].data_ptr(), tt["inc"].data_ptr(), tt["inc_base"].data_ptr())
+    Dd = torch.zeros(layd.total, dtype=torch.float64, device="cuda")
+
+    def dlp():
+        _lib.check(_lib.lib().h2b_pair_blocks_dlp(ctypes.byref(ctx.dmesh.c), pp.data_ptr(), lam.data_ptr(), Qd,
+                                                  ctypes.byref(cj), ctypes.byref(tabd.touch.c),
+                                                  tabd.values_dev.data_ptr(), Dd.data_ptr(), D.stream()))
+
+    dlp()
+    td = bench.ev_time(torch, dlp, 10)
+    hd = Dd.cpu().numpy()
+    if not os.path.exists("/tmp/nf_ref_dlp.npy"):
+        np.save("/tmp/nf_ref_dlp.npy", hd)
+    rd = np.load("/tmp/nf_ref_dlp.npy")
+    pairs = int((packed["jobs"][:, 1] * packed["jobs"][:, 3]).sum())
+    res.update(dlp_ms=td * 1e3, dlp_tflops=25.0 * pairs * 81 / td / 1e12,
+               dlp_err_vs_first=float(np.abs(hd - rd).max() / np.abs(rd).max()))
+    print(json.dumps(res))
 else:
     for v in sys.argv[1:]:
         path = os.path.join(ROOT, "paper_2001_05523_b200", "_lib", "variants", v + ".so")
