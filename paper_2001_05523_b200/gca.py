@@ -299,13 +299,28 @@ def build_basis_device(ctx, tree, flavor, m, eps_aca, q_single=None):
                                       _GCA_FLAVOR_CODE[flavor], ctypes.byref(b), Lm.data_ptr(), D.stream()))
         _lib.check(L_.h2b_gca_aca(ctypes.byref(b), float(eps_aca), Lm.data_ptr(), scratch.data_ptr(),
                                   rank.data_ptr(), tau.data_ptr(), ncol, Vm.data_ptr(), D.stream()))
-        rk, tu, Vh = D.host(rank).astype(np.int64), D.host(tau).reshape(-1, ncol), D.host(Vm)
+        # download only the used part of every V slot (rows x rank of rows x 2k):
+        # compact on the device first
+        rk = D.host(rank).astype(np.int64)
+        tu = D.host(tau).reshape(-1, ncol)
+        sizes = nr * rk
+        coff = np.zeros(len(level) + 1, dtype=np.int64)
+        np.cumsum(sizes, out=coff[1:])
+        t = D.torch()
+        if coff[-1] > 0:
+            sz = t.from_numpy(sizes).cuda()
+            starts = t.from_numpy(l_off - coff[:-1]).cuda()
+            src = t.arange(int(coff[-1]), device="cuda", dtype=t.int64) + t.repeat_interleave(starts, sz)
+            Vh = D.host(Vm[src])
+            del src, sz, starts
+        else:
+            Vh = np.zeros(0)
         del Lm, scratch, Vm
         for i, u in enumerate(level):
             u = int(u)
             c = tree.nodes[u]
             kk = int(rk[i])
-            V = Vh[l_off[i] : l_off[i] + nr[i] * kk].reshape(nr[i], kk).copy()
+            V = Vh[coff[i] : coff[i + 1]].reshape(nr[i], kk)
             piv = rows[i][tu[i, :kk].astype(np.int64)]
             if c.is_leaf:
                 basis.V[u] = V
