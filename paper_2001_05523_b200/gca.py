@@ -250,6 +250,46 @@ def green_points_batch(boxes, m):
     return out
 
 
+def green_points_batch_device(boxes, m):
+    """green_points_batch with torch on the GPU: the same elementwise IEEE
+    operations in the same order (no contractions), so the same bits."""
+    t = __import__("torch")
+    b = t.as_tensor(np.asarray(boxes, dtype=float).reshape(-1, 2, 3), device="cuda").clone()
+    n = b.shape[0]
+    ext = b[:, 1] - b[:, 0]
+    pad = DEGENERATE_WIDTH * t.clamp(ext.max(dim=1).values, min=1.0)
+    for d in range(3):
+        flat = ext[:, d] < pad
+        mid = 0.5 * (b[:, 0, d] + b[:, 1, d])
+        lo = t.where(flat, mid - 0.5 * pad, b[:, 0, d])
+        hi = t.where(flat, mid + 0.5 * pad, b[:, 1, d])
+        b[:, 0, d], b[:, 1, d] = lo, hi
+    delta = (b[:, 1] - b[:, 0]).max(dim=1).values
+    gb = t.stack([b[:, 0] - delta[:, None], b[:, 1] + delta[:, None]], dim=1)
+    g = gauss_legendre(m)
+    gp = t.as_tensor(g.points, device="cuda")
+    gw = t.as_tensor(g.weights, device="cuda")
+    mm = m * m
+    out = t.zeros((n, 6 * mm, 8), dtype=t.float64, device="cuda")
+    f = 0
+    for axis in range(3):
+        u, v = (axis + 1) % 3, (axis + 2) % 3
+        lu = gb[:, 1, u] - gb[:, 0, u]
+        lv = gb[:, 1, v] - gb[:, 0, v]
+        cu = gb[:, 0, u][:, None] + lu[:, None] * gp[None, :]
+        cv = gb[:, 0, v][:, None] + lv[:, None] * gp[None, :]
+        wface = ((lu[:, None] * gw[None, :])[:, :, None] * (lv[:, None] * gw[None, :])[:, None, :]).reshape(n, mm)
+        for side in (0, 1):
+            blk = out[:, f * mm : (f + 1) * mm]
+            blk[:, :, axis] = gb[:, side, axis][:, None]
+            blk[:, :, u] = cu.repeat_interleave(m, dim=1)
+            blk[:, :, v] = cv.repeat(1, m)
+            blk[:, :, 3] = t.sqrt(wface)
+            blk[:, :, 4 + axis] = 1.0 if side else -1.0
+            f += 1
+    return out
+
+
 _GCA_FLAVOR_CODE = {P0_SLP: 0, P1_DLP: 1}
 
 
@@ -289,7 +329,7 @@ def build_basis_device(ctx, tree, flavor, m, eps_aca, q_single=None):
         l_off = ptr[:-1] * ncol
         total = int(ptr[-1]) * ncol
         d_ptr, d_rows = D.dev(ptr), D.dev(np.concatenate(rows), np.int32)
-        d_green, d_loff = D.dev(green_points_batch(boxes, m)), D.dev(l_off)
+        d_green, d_loff = green_points_batch_device(np.stack(boxes), m), D.dev(l_off)
         b = _lib.GcaBatch(len(level), d_ptr.data_ptr(), d_rows.data_ptr(), k, int(nr.max()), d_green.data_ptr(),
                           d_loff.data_ptr())
         Lm, scratch, Vm = D.empty((total,)), D.empty((total,)), D.empty((total,))

@@ -85,3 +85,15 @@ def test_problem_setup_with_device_basis():
     ref = G @ x
     assert np.linalg.norm(yd - ref) / np.linalg.norm(ref) < 1e-3
     assert np.linalg.norm(yd - yh) / np.linalg.norm(yh) < 1e-3
+
+
+def test_green_points_device_bit_identical():
+    from paper_2001_05523_b200 import gca
+
+    rng = np.random.default_rng(5)
+    lo = rng.uniform(-1, 1, (64, 3))
+    ext = rng.uniform(0, 0.5, (64, 3))
+    ext[::7, 2] = 0.0
+    boxes = np.stack([lo, lo + ext], axis=1)
+    for m in (3, 4, 5):
+        assert np.array_equal(gca.green_points_batch_device(boxes, m).cpu().numpy(), gca.green_points_batch(boxes, m))
