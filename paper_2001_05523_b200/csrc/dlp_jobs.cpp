@@ -8,6 +8,8 @@
 #include <algorithm>
 #include <cstring>
 #include <new>
+#include <string>
+#include <thread>
 #include <vector>
 
 #include "h2b_internal.h"
@@ -25,14 +27,13 @@ struct h2b_dlp_build {
 
 using namespace h2b;
 
-extern "C" int h2b_dlp_jobs_build(int64_t n_verts, const int64_t* vptr, const int64_t* vidx, const int64_t* tris,
-                                  int64_t n_blocks, const int64_t* row_ptr, const int64_t* rows,
-                                  const int64_t* col_ptr, const int64_t* cols, const int64_t* out_off,
-                                  const int64_t* ld, h2b_dlp_build** out) {
-    if (!out || (n_blocks > 0 && (!vptr || !vidx || !tris || !row_ptr || !rows || !col_ptr || !cols || !out_off || !ld)))
-        return fail(H2B_ERR_INVALID, "h2b_dlp_jobs_build: null pointer");
-    h2b_dlp_build* b = new (std::nothrow) h2b_dlp_build();
-    if (!b) return fail(H2B_ERR_INVALID, "h2b_dlp_jobs_build: out of host memory");
+namespace {
+// Jobs of blocks [b0, b1) with offsets local to this range (0-based row_idx,
+// pan_idx, inc and incidence-pointer lists); merged in block order below.
+int build_range(int64_t n_verts, const int64_t* vptr, const int64_t* vidx, const int64_t* tris, int64_t b0,
+                int64_t b1, const int64_t* row_ptr, const int64_t* rows, const int64_t* col_ptr,
+                const int64_t* cols, const int64_t* out_off, const int64_t* ld, h2b_dlp_build* b,
+                std::string& err) {
     std::vector<int32_t> vpos((size_t)std::max<int64_t>(n_verts, 0), -1);
     std::vector<int64_t> pans;
     struct Trip {
@@ -40,7 +41,7 @@ extern "C" int h2b_dlp_jobs_build(int64_t n_verts, const int64_t* vptr, const in
     };
     std::vector<Trip> trip;
     int64_t nrow = 0, npan = 0, ninc = 0, nptr = 0;
-    for (int64_t bk = 0; bk < n_blocks; ++bk) {
+    for (int64_t bk = b0; bk < b1; ++bk) {
         const int64_t* R = rows + row_ptr[bk];
         const int64_t nr = row_ptr[bk + 1] - row_ptr[bk];
         const int64_t* Cc = cols + col_ptr[bk];
@@ -53,8 +54,8 @@ extern "C" int h2b_dlp_jobs_build(int64_t n_verts, const int64_t* vptr, const in
                 for (int64_t c = c0; c < c1; ++c) {
                     const int64_t v = Cc[c];
                     if (v < 0 || v >= n_verts) {
-                        delete b;
-                        return fail(H2B_ERR_INVALID, "h2b_dlp_jobs_build: column vertex out of range");
+                        err = "h2b_dlp_jobs_build: column vertex out of range";
+                        return H2B_ERR_INVALID;
                     }
                     pans.insert(pans.end(), vidx + vptr[v], vidx + vptr[v + 1]);
                 }
@@ -64,8 +65,8 @@ extern "C" int h2b_dlp_jobs_build(int64_t n_verts, const int64_t* vptr, const in
                 c1 = c0 + std::max<int64_t>(1, (c1 - c0) / 2);
             }
             if ((int64_t)pans.size() > kMaxPanels) {
-                delete b;
-                return fail(H2B_ERR_INVALID, "vertex valence too large for the DLP panel tile");
+                err = "vertex valence too large for the DLP panel tile";
+                return H2B_ERR_INVALID;
             }
             const int64_t nsel = c1 - c0;
             for (int64_t c = c0; c < c1; ++c) vpos[Cc[c]] = (int32_t)(c - c0);
@@ -102,6 +103,63 @@ extern "C" int h2b_dlp_jobs_build(int64_t n_verts, const int64_t* vptr, const in
             ninc += (int64_t)trip.size();
             c0 = c1;
         }
+    }
+    return H2B_OK;
+}
+}  // namespace
+
+extern "C" int h2b_dlp_jobs_build(int64_t n_verts, const int64_t* vptr, const int64_t* vidx, const int64_t* tris,
+                                  int64_t n_blocks, const int64_t* row_ptr, const int64_t* rows,
+                                  const int64_t* col_ptr, const int64_t* cols, const int64_t* out_off,
+                                  const int64_t* ld, h2b_dlp_build** out) {
+    if (!out || (n_blocks > 0 && (!vptr || !vidx || !tris || !row_ptr || !rows || !col_ptr || !cols || !out_off || !ld)))
+        return fail(H2B_ERR_INVALID, "h2b_dlp_jobs_build: null pointer");
+    h2b_dlp_build* b = new (std::nothrow) h2b_dlp_build();
+    if (!b) return fail(H2B_ERR_INVALID, "h2b_dlp_jobs_build: out of host memory");
+    // block ranges built in parallel (independent), then concatenated in block
+    // order with the offsets shifted: identical to one sequential pass
+    const int64_t hw = std::max<int64_t>(1, (int64_t)std::thread::hardware_concurrency());
+    const int64_t nt = std::max<int64_t>(1, std::min<int64_t>(hw, n_blocks / 256));
+    std::vector<h2b_dlp_build> part((size_t)nt);
+    std::vector<int> rc((size_t)nt, H2B_OK);
+    std::vector<std::string> err((size_t)nt);
+    {
+        std::vector<std::thread> th;
+        for (int64_t t = 0; t < nt; ++t) {
+            const int64_t b0 = n_blocks * t / nt, b1 = n_blocks * (t + 1) / nt;
+            auto job = [&, t, b0, b1] {
+                rc[(size_t)t] = build_range(n_verts, vptr, vidx, tris, b0, b1, row_ptr, rows, col_ptr, cols, out_off,
+                                            ld, &part[(size_t)t], err[(size_t)t]);
+            };
+            if (nt == 1)
+                job();
+            else
+                th.emplace_back(job);
+        }
+        for (auto& x : th) x.join();
+    }
+    for (int64_t t = 0; t < nt; ++t)
+        if (rc[(size_t)t] != H2B_OK) {
+            delete b;
+            return fail(rc[(size_t)t], err[(size_t)t]);
+        }
+    int64_t nrow = 0, npan = 0, ninc = 0, nptr = 0;
+    for (int64_t t = 0; t < nt; ++t) {
+        const h2b_dlp_build& q = part[(size_t)t];
+        for (size_t j = 0; j < q.jobs.size(); j += 8) {
+            b->jobs.insert(b->jobs.end(), q.jobs.begin() + j, q.jobs.begin() + j + 8);
+            b->jobs[b->jobs.size() - 8] += nrow;
+            b->jobs[b->jobs.size() - 6] += npan;
+        }
+        for (int32_t v : q.inc_ptr) b->inc_ptr.push_back((int32_t)(v + ninc));
+        for (int64_t v : q.inc_base) b->inc_base.push_back(v + nptr);
+        b->row_idx.insert(b->row_idx.end(), q.row_idx.begin(), q.row_idx.end());
+        b->pan_idx.insert(b->pan_idx.end(), q.pan_idx.begin(), q.pan_idx.end());
+        b->inc.insert(b->inc.end(), q.inc.begin(), q.inc.end());
+        nrow += (int64_t)q.row_idx.size();
+        npan += (int64_t)q.pan_idx.size();
+        ninc += (int64_t)q.inc.size();
+        nptr += (int64_t)q.inc_ptr.size();
     }
     *out = b;
     return ok();
