@@ -276,6 +276,7 @@ __device__ __forceinline__ void rows_warp(const double* M, int64_t ld, int r0, i
     double acc[R];
 #pragma unroll
     for (int i = 0; i < R; ++i) acc[i] = 0.0;
+#pragma unroll 4
     for (int c = lane; c < cols; c += 32) {
         const double vc = v[c];
         double e[R];
