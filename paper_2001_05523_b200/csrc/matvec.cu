@@ -45,6 +45,7 @@
 // and can be captured in a CUDA graph.
 
 #include <algorithm>
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -95,6 +96,7 @@ struct h2b_plan {
     int n_near, n_cpl;
     int max_cols, vec_len;
     int smem;
+    int loop_grid;      // > 0: persistent k_matvec_loop with this many CTAs (H2B_LOOP=1)
     int64_t e_bytes_r;
     double* dx;
     double* dy;
@@ -902,39 +904,11 @@ struct KArgs {
 #define H2B_MINB 6
 #endif
 
-__global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, const double* __restrict__ x,
-                                                       double* __restrict__ y) {
-    extern __shared__ __align__(128) char smraw[];
-    __shared__ int s_ticket;
-    __shared__ uint32_t s_epoch;
-    __shared__ int64_t s_rec[kFwdHead + kFwdLevel * kMaxDepth];
+// One task (ticket < 0: host-input copy task; [0, c_leaves): forward; then
+// band / descent records).  Ends with a block barrier.
+__device__ __forceinline__ void run_task(const KArgs& a, const double* __restrict__ x, double* __restrict__ y,
+                                         const int ticket, const uint32_t epoch, Shared& s) {
     const h2b_layout& L = a.L;
-    Shared s;
-    s.bar = reinterpret_cast<uint64_t*>(smraw);
-    s.stage = smraw + 128;
-    s.rhs = reinterpret_cast<double*>(smraw + 128 + kStageBytes);
-    s.va = s.rhs + a.max_cols;
-    s.vb = s.va + 2 * a.vec_len;
-    s.red = s.vb + a.vec_len;
-    s.rec = s_rec;
-    s.parity = 0;
-    s.issued = false;
-    if (threadIdx.x == 0) {
-        // tickets count on across launches: launch = t / grid (every CTA of a
-        // launch takes exactly one ticket before the next launch starts)
-        // device- and host-input launches count on separate counters (their
-        // grids differ by the copy tasks); epochs stay unique: odd / even
-        const int host = a.xh != nullptr;
-        const unsigned long long t = atomicAdd(a.ctrl + host, 1ull);
-        s_ticket = (int)(t % gridDim.x) - a.n_copy;  // copy tasks (host input) first: negative
-        s_epoch = 2u * (uint32_t)(t / gridDim.x) + 1u + (uint32_t)host;
-        mbar_init(s.bar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    const int ticket = s_ticket;
-    const uint32_t epoch = s_epoch;
-    s.xll = a.xh ? a.xll : nullptr;
     if (ticket < 0) {
         if (!a.xh) return;
         // host-input launch: copy a chunk of x from mapped host memory into
@@ -998,6 +972,89 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
     }
 }
 
+
+
+__global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, const double* __restrict__ x,
+                                                       double* __restrict__ y) {
+    extern __shared__ __align__(128) char smraw[];
+    __shared__ int s_ticket;
+    __shared__ uint32_t s_epoch;
+    __shared__ int64_t s_rec[kFwdHead + kFwdLevel * kMaxDepth];
+    const h2b_layout& L = a.L;
+    Shared s;
+    s.bar = reinterpret_cast<uint64_t*>(smraw);
+    s.stage = smraw + 128;
+    s.rhs = reinterpret_cast<double*>(smraw + 128 + kStageBytes);
+    s.va = s.rhs + a.max_cols;
+    s.vb = s.va + 2 * a.vec_len;
+    s.red = s.vb + a.vec_len;
+    s.rec = s_rec;
+    s.parity = 0;
+    s.issued = false;
+    if (threadIdx.x == 0) {
+        // tickets count on across launches: launch = t / grid (every CTA of a
+        // launch takes exactly one ticket before the next launch starts)
+        // device- and host-input launches count on separate counters (their
+        // grids differ by the copy tasks); epochs stay unique: odd / even
+        const int host = a.xh != nullptr;
+        const unsigned long long t = atomicAdd(a.ctrl + host, 1ull);
+        s_ticket = (int)(t % gridDim.x) - a.n_copy;  // copy tasks (host input) first: negative
+        s_epoch = 2u * (uint32_t)(t / gridDim.x) + 1u + (uint32_t)host;
+        mbar_init(s.bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int ticket = s_ticket;
+    const uint32_t epoch = s_epoch;
+    s.xll = a.xh ? a.xll : nullptr;
+    run_task(a, x, y, ticket, epoch, s);
+}
+
+// Persistent variant (H2B_LOOP=1): gridDim CTAs (one wave) each loop
+// take-ticket / run-task, so no CTA is relaunched per task.  A CTA holds one
+// ticket at a time, exactly as the one-task-per-CTA kernel, so the same
+// smallest-ticket argument rules out deadlock; a launch consumes n_tasks +
+// gridDim tickets (every CTA stops at its first ticket past the end).
+__global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec_loop(const KArgs a, const double* __restrict__ x,
+                                                            double* __restrict__ y) {
+    extern __shared__ __align__(128) char smraw[];
+    __shared__ int s_ticket;
+    __shared__ uint32_t s_epoch;
+    __shared__ int64_t s_rec[kFwdHead + kFwdLevel * kMaxDepth];
+    const h2b_layout& L = a.L;
+    const int host = a.xh != nullptr;
+    const int n_total = a.n_copy + L.c_leaves + a.n_near + a.n_cpl;
+    const unsigned long long per_launch = (unsigned long long)n_total + gridDim.x;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smraw);
+    for (int it = 0;; ++it) {
+        if (threadIdx.x == 0) {
+            const unsigned long long t = atomicAdd(a.ctrl + host, 1ull);
+            const int idx = (int)(t % per_launch);
+            s_ticket = idx < n_total ? idx - a.n_copy : INT_MIN;
+            s_epoch = 2u * (uint32_t)(t / per_launch) + 1u + (uint32_t)host;
+            // the previous task waited on every phase it armed: re-arm
+            if (it > 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+            mbar_init(bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        const int ticket = s_ticket;
+        if (ticket == INT_MIN) return;
+        Shared s;
+        s.bar = bar;
+        s.stage = smraw + 128;
+        s.rhs = reinterpret_cast<double*>(smraw + 128 + kStageBytes);
+        s.va = s.rhs + a.max_cols;
+        s.vb = s.va + 2 * a.vec_len;
+        s.red = s.vb + a.vec_len;
+        s.rec = s_rec;
+        s.parity = 0;
+        s.issued = false;
+        s.xll = a.xh ? a.xll : nullptr;
+        run_task(a, x, y, ticket, s_epoch, s);
+        __syncthreads();
+    }
+}
 
 __global__ void k_diagonal(h2b_layout L, double* __restrict__ diag) {
     const int node = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1332,6 +1389,16 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
         H2B_CUDA_TRY(cudaMemcpy(p->rec, rec.data(), sizeof(int64_t) * rec.size(), cudaMemcpyHostToDevice));
     H2B_CUDA_TRY(cudaMemcpy(p->fwd_off, fwd_off.data(), sizeof(int64_t) * fwd_off.size(), cudaMemcpyHostToDevice));
     H2B_CUDA_TRY(cudaFuncSetAttribute(k_matvec, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem));
+    p->loop_grid = 0;
+    if (const char* e = getenv("H2B_LOOP")) {
+        if (atoi(e) > 0) {
+            H2B_CUDA_TRY(cudaFuncSetAttribute(k_matvec_loop, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem));
+            int nb = 0, sms = 0;
+            H2B_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_matvec_loop, kThreads, p->smem));
+            H2B_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
+            p->loop_grid = std::max(1, nb * sms);
+        }
+    }
     p->trace = nullptr;
     if (const char* tr = getenv("H2B_TRACE")) {
         if (tr[0] == '1') {
@@ -1405,7 +1472,10 @@ int launch_matvec(h2b_plan* p, const double* d_x, const double* xh, double* y, c
     a.xll = p->xll;
     a.n_copy = xh ? (int)((p->L.n_cols + kCopyChunk - 1) / kCopyChunk) : 0;
     const int grid = a.n_copy + p->L.c_leaves + p->n_near + p->n_cpl;
-    k_matvec<<<grid, kThreads, p->smem, st>>>(a, d_x, y);
+    if (p->loop_grid > 0)
+        k_matvec_loop<<<std::min(grid, p->loop_grid), kThreads, p->smem, st>>>(a, d_x, y);
+    else
+        k_matvec<<<grid, kThreads, p->smem, st>>>(a, d_x, y);
     H2B_CUDA_TRY(cudaGetLastError());
     return ok();
 }
