@@ -206,12 +206,20 @@ def run_ours(args, cfg):
     import torch
 
     ws, rank, local = dist_env()
+    # H2B_DIST_BACKEND=gloo: functional check of the N-rank orchestration on
+    # fewer GPUs (ranks share a device; not a measurement)
+    backend = os.environ.get("H2B_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     pg = None
     if ws > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
         pg = dist
     from paper_2001_05523_b200 import gca, kernels
     from paper_2001_05523_b200.containers import (H2Matrix, assemble_couplings, near_layout, near_slp_jobs)
