@@ -516,20 +516,6 @@ __device__ __forceinline__ bool band_staged(int64_t bytes, const double* src) {
     return bytes > 0 && bytes <= kStageBytes && (reinterpret_cast<uintptr_t>(src) & 15) == 0 && (bytes & 15) == 0;
 }
 
-// Thread 0 starts the TMA bulk copy of the band described by `rec` into
-// `stage` (a plain arrive when the band is empty or read from global memory).
-__device__ __forceinline__ void issue_band(const h2b_layout& L, const int64_t* rec, char* stage, uint64_t* bar) {
-    if (threadIdx.x != 0) return;
-    const int64_t bytes = rec[2] * rec[1] * 8;
-    const double* src = (rec[7] ? L.S : L.D) + rec[0];
-    if (band_staged(bytes, src)) {
-        mbar_expect_tx(bar, (uint32_t)bytes);
-        bulk_g2s(stage, src, (uint32_t)bytes, bar);
-    } else {
-        mbar_arrive(bar);
-    }
-}
-
 __device__ void prefetch_slice(const double* base, int64_t bytes, int part, int parts) {
     if (!base || bytes <= 0) return;
     const int64_t lines = (bytes + 127) / 128;
@@ -980,7 +966,6 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
     __shared__ int s_ticket;
     __shared__ uint32_t s_epoch;
     __shared__ int64_t s_rec[kFwdHead + kFwdLevel * kMaxDepth];
-    const h2b_layout& L = a.L;
     Shared s;
     s.bar = reinterpret_cast<uint64_t*>(smraw);
     s.stage = smraw + 128;
