@@ -283,14 +283,24 @@ __global__ void __launch_bounds__(128) k_singular(const double* __restrict__ V, 
             const double* p = sd.p + 4 * (c0 + e);
             const double w = sd.w[c0 + e];
             double* d = srule + e * kRuleStride;
-            d[0] = p[0];
-            d[1] = p[1];
-            d[2] = p[2];
-            d[3] = p[3];
-            d[4] = w;
-            d[5] = w * (1.0 - p[2]);
-            d[6] = w * (p[2] - p[3]);
-            d[7] = w * p[3];
+            if (KIND == H2B_SLP) {
+                // sums and differences of the two charts' coordinates: both
+                // orientations of a symmetrised pair share the sum terms
+                d[0] = p[0] + p[2];
+                d[1] = p[1] + p[3];
+                d[2] = p[0] - p[2];
+                d[3] = p[1] - p[3];
+                d[4] = w;
+            } else {
+                d[0] = p[0];
+                d[1] = p[1];
+                d[2] = p[2];
+                d[3] = p[3];
+                d[4] = w;
+                d[5] = w * (1.0 - p[2]);
+                d[6] = w * (p[2] - p[3]);
+                d[7] = w * p[3];
+            }
         }
         __syncthreads();
         if (!active) continue;
@@ -300,7 +310,7 @@ __global__ void __launch_bounds__(128) k_singular(const double* __restrict__ V, 
 #pragma unroll 4
                 for (int e = 0; e < cn; ++e) {
                     const double* d = srule + e * kRuleStride;
-                    const double du = d[0] - d[2], dv = d[1] - d[3];
+                    const double du = d[2], dv = d[3];  // u1 - u2, v1 - v2
                     const double dx = fma(dv, ea2[0], du * ea1[0]);
                     const double dy = fma(dv, ea2[1], du * ea1[1]);
                     const double dz = fma(dv, ea2[2], du * ea1[2]);
@@ -311,27 +321,42 @@ __global__ void __launch_bounds__(128) k_singular(const double* __restrict__ V, 
                     acc0 = fma(d[4] * t, c, acc0);
                 }
             } else {
+                // shared vertex first in both charts, so base = 0 and
+                //   d  = u1 E_a1 + v1 E_a2 + u2 E_b1 + v2 E_b2      (E_b negated)
+                //   d' = u2 E_a1 + v2 E_a2 + u1 E_b1 + v1 E_b2      (swapped rule)
+                // = c +- e with c = s P + s' Q, e = m M + m' N over the sums
+                // s = u1 + u2, s' = v1 + v2 and differences m = u1 - u2, m' = v1 - v2
+                double P[3], M[3], Qv[3], N[3];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    P[k] = 0.5 * (ea1[k] + eb1[k]);
+                    M[k] = 0.5 * (ea1[k] - eb1[k]);
+                    Qv[k] = 0.5 * (ea2[k] + eb2[k]);
+                    N[k] = 0.5 * (ea2[k] - eb2[k]);
+                }
 #pragma unroll 2
                 for (int e = 0; e < cn; ++e) {
                     const double* d = srule + e * kRuleStride;
-                    const double u1 = d[0], v1 = d[1], u2 = d[2], v2 = d[3], w = d[4];
-                    double dx = fma(v2, eb2[0], fma(u2, eb1[0], fma(v1, ea2[0], fma(u1, ea1[0], base[0]))));
-                    double dy = fma(v2, eb2[1], fma(u2, eb1[1], fma(v1, ea2[1], fma(u1, ea1[1], base[1]))));
-                    double dz = fma(v2, eb2[2], fma(u2, eb1[2], fma(v1, ea2[2], fma(u1, ea1[2], base[2]))));
-                    double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+                    const double su = d[0], sv = d[1], mu = d[2], mv = d[3], w = d[4];
+                    double dp[3], dm[3];
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        const double c = fma(sv, Qv[k], su * P[k]);
+                        const double ee = fma(mv, N[k], mu * M[k]);
+                        dp[k] = c + ee;
+                        dm[k] = c - ee;
+                    }
+                    double r2 = fma(dp[2], dp[2], fma(dp[1], dp[1], dp[0] * dp[0]));
                     double t = rsqrt_seed(r2);
-                    double s = t * t;
-                    double c = fma(-r2, s, 3.0);
-                    acc0 = fma(w * t, c, acc0);
+                    double sq = t * t;
+                    double cc = fma(-r2, sq, 3.0);
+                    acc0 = fma(w * t, cc, acc0);
                     // orientation-swapped rule (kernels.py:303-309)
-                    dx = fma(v1, eb2[0], fma(u1, eb1[0], fma(v2, ea2[0], fma(u2, ea1[0], base[0]))));
-                    dy = fma(v1, eb2[1], fma(u1, eb1[1], fma(v2, ea2[1], fma(u2, ea1[1], base[1]))));
-                    dz = fma(v1, eb2[2], fma(u1, eb1[2], fma(v2, ea2[2], fma(u2, ea1[2], base[2]))));
-                    r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+                    r2 = fma(dm[2], dm[2], fma(dm[1], dm[1], dm[0] * dm[0]));
                     t = rsqrt_seed(r2);
-                    s = t * t;
-                    c = fma(-r2, s, 3.0);
-                    acc1 = fma(w * t, c, acc1);
+                    sq = t * t;
+                    cc = fma(-r2, sq, 3.0);
+                    acc1 = fma(w * t, cc, acc1);
                 }
             }
         } else {
