@@ -625,7 +625,7 @@ __global__ void __launch_bounds__(256, MINB) k_blocks_dlp(const double* __restri
     extern __shared__ double smem[];
     constexpr int RT = kTile, PT = kDlpMaxPanels;
     double* rx = smem;                  // [5][Q][RT]
-    double* px = rx + 5 * Q * RT;       // [6][Q][PT]: y', -|y'|^2/2, W, y'.n
+    double* px = rx + 5 * Q * RT;       // [6][Q][PT]: y', -|y'|^2/2, W, (y'.n) W
     double* pn = px + 6 * Q * PT;       // [3][PT]
     double* scr = pn + 3 * PT;          // [kDlpRowChunk][PT][3]
     int* rv = reinterpret_cast<int*>(scr + kDlpRowChunk * PT * 3);
@@ -675,8 +675,9 @@ __global__ void __launch_bounds__(256, MINB) k_blocks_dlp(const double* __restri
         px[Q * PT + s] = y;
         px[2 * Q * PT + s] = z;
         px[3 * Q * PT + s] = -0.5 * fma(z, z, fma(y, y, x * x));
-        px[4 * Q * PT + s] = P[3 * FQ + g] * kDlpFold;
-        px[5 * Q * PT + s] = fma(z, n2, fma(y, n1, x * n0));
+        const double wf = P[3 * FQ + g] * kDlpFold;
+        px[4 * Q * PT + s] = wf;
+        px[5 * Q * PT + s] = fma(z, n2, fma(y, n1, x * n0)) * wf;  // (y'.n) w: folds a product per evaluation
         if (j == 0) {
             pp[c] = pnl;
             pn[c] = n0;
@@ -743,7 +744,8 @@ __global__ void __launch_bounds__(256, MINB) k_blocks_dlp(const double* __restri
                                 const double t = rsqrt_seed(-g);
                                 const double s2 = t * t;
                                 const double c3 = fma(g, s2, 5.0 / 3.0);
-                                const double k = ((xn - yn[j]) * c3) * ((s2 * t) * yw[j]);
+                                // (x' - y').n w = x'.n w - (y'.n) w
+                                const double k = (fma(xn, yw[j], -yn[j]) * c3) * (s2 * t);
                                 a0 = fma(k, c_lam[3 * (j0 + j)], a0);
                                 a1 = fma(k, c_lam[3 * (j0 + j) + 1], a1);
                                 a2 = fma(k, c_lam[3 * (j0 + j) + 2], a2);
