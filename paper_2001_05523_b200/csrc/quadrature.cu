@@ -360,19 +360,24 @@ __global__ void __launch_bounds__(128) k_singular(const double* __restrict__ V, 
                 }
             }
         } else {
-            // DLP: <x - y, n_b> / r^3 weighted by the column chart barycentrics
+            // DLP: <x - y, n_b> / r^3 weighted by the column chart barycentrics.
+            // The shared vertex comes first in both charts (base = 0) and E_b1,
+            // E_b2 lie in panel b's plane, so <x - y, n_b> = u1 <E_a1, n_b> +
+            // v1 <E_a2, n_b> (the E_b terms are rounding noise)
+            const double al = fma(ea1[2], nb[2], fma(ea1[1], nb[1], ea1[0] * nb[0]));
+            const double be = fma(ea2[2], nb[2], fma(ea2[1], nb[1], ea2[0] * nb[0]));
 #pragma unroll 2
             for (int e = 0; e < cn; ++e) {
                 const double* d = srule + e * kRuleStride;
                 const double u1 = d[0], v1 = d[1], u2 = d[2], v2 = d[3];
-                const double dx = fma(v2, eb2[0], fma(u2, eb1[0], fma(v1, ea2[0], fma(u1, ea1[0], base[0]))));
-                const double dy = fma(v2, eb2[1], fma(u2, eb1[1], fma(v1, ea2[1], fma(u1, ea1[1], base[1]))));
-                const double dz = fma(v2, eb2[2], fma(u2, eb1[2], fma(v1, ea2[2], fma(u1, ea1[2], base[2]))));
+                const double dx = fma(v2, eb2[0], fma(u2, eb1[0], fma(v1, ea2[0], u1 * ea1[0])));
+                const double dy = fma(v2, eb2[1], fma(u2, eb1[1], fma(v1, ea2[1], u1 * ea1[1])));
+                const double dz = fma(v2, eb2[2], fma(u2, eb1[2], fma(v1, ea2[2], u1 * ea1[2])));
                 const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
                 const double t = rsqrt_seed(r2);
                 const double s = t * t;
                 const double c3 = fma(-r2, s, 5.0 / 3.0);
-                const double num = fma(dz, nb[2], fma(dy, nb[1], dx * nb[0]));
+                const double num = fma(v1, be, u1 * al);
                 const double k = (num * c3) * (s * t);
                 acc0 = fma(k, d[5], acc0);
                 acc1 = fma(k, d[6], acc1);
