@@ -306,15 +306,16 @@ __global__ void __launch_bounds__(128) k_singular(const double* __restrict__ V, 
         if (!active) continue;
         if (KIND == H2B_SLP) {
             if (kase == H2B_IDENTICAL) {
-                // same panel: d = (u1-u2) E1 + (v1-v2) E2 (base = 0)
+                // same panel: d = (u1-u2) E1 + (v1-v2) E2 (base = 0), so
+                // r^2 = du (du |E1|^2 + 2 dv E1.E2) + dv^2 |E2|^2 (a 2x2 Gram form)
+                const double g11 = fma(ea1[2], ea1[2], fma(ea1[1], ea1[1], ea1[0] * ea1[0]));
+                const double g12 = 2.0 * fma(ea1[2], ea2[2], fma(ea1[1], ea2[1], ea1[0] * ea2[0]));
+                const double g22 = fma(ea2[2], ea2[2], fma(ea2[1], ea2[1], ea2[0] * ea2[0]));
 #pragma unroll 4
                 for (int e = 0; e < cn; ++e) {
                     const double* d = srule + e * kRuleStride;
                     const double du = d[2], dv = d[3];  // u1 - u2, v1 - v2
-                    const double dx = fma(dv, ea2[0], du * ea1[0]);
-                    const double dy = fma(dv, ea2[1], du * ea1[1]);
-                    const double dz = fma(dv, ea2[2], du * ea1[2]);
-                    const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+                    const double r2 = fma(du, fma(du, g11, dv * g12), (dv * dv) * g22);
                     const double t = rsqrt_seed(r2);
                     const double s = t * t;
                     const double c = fma(-r2, s, 3.0);
