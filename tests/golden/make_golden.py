@@ -21,6 +21,9 @@ What is pinned (all produced by the reference's own public functions):
   h2_cfg0.npz      full GCA basis + sampled couplings + matvec x/y of config 0
   h2_cfg1.npz      pivots/ranks digests + matvec x/y of config 1
   h2_dlp4.npz      level-4 double-layer H^2 (P0 x P1) matvec x/y + basis
+  sample_l8.npz    config-2 size (sphere level 8): a seeded sample of single- and
+                   double-layer near blocks with the split orders (regular 3,
+                   Sauter-Schwab 5) and of touching-pair integrals
   cube4.npz        config-4 geometry at n=4 (this repo's cube_shell_mesh arrays fed
                    to the reference): trees + block trees (grid-aligned: exact
                    ties in the splits), SLP/DLP GCA H^2 matvec x/y, SLP basis
@@ -340,6 +343,55 @@ def gen_h2_dlp4():
     np.savez_compressed(os.path.join(HERE, "h2_dlp4.npz"), **out)
 
 
+class _OnDemandTable:
+    """Stands in for kernels.SingularTable on a sampled block: the reference's
+    panel_pair_matrix looks touching pairs up through .lookup, answered by the
+    reference's own pair_integrals at the Sauter-Schwab order."""
+
+    def __init__(self, mesh, kind, q):
+        self.mesh, self.kind, self.q = mesh, kind, q
+
+    def lookup(self, pa, pb):
+        return kernels.pair_integrals(self.mesh, np.asarray(pa), np.asarray(pb), self.kind, self.q)
+
+
+def gen_sample_l8():
+    """Config-2 size parity sample (the full reference nearfield takes hours)."""
+    mesh = sphere_mesh(8)
+    ctx = AssemblyContext(mesh)
+    t0 = build_cluster_tree(spaces.DofSpace(spaces.P0, mesh).support_boxes(), 64)
+    t1 = build_cluster_tree(spaces.DofSpace(spaces.P1, mesh).support_boxes(), 64)
+    bs, bd = BlockTree(t0, t0, 2.0), BlockTree(t0, t1, 2.0)
+    log("l8 structure")
+    rng = np.random.default_rng(8)
+    pq = ctx.panel_quad(3)
+    vt = mesh.vertex_triangles()
+    out = {}
+    for name, bt, n_sel in (("slp", bs, 40), ("dlp", bd, 24)):
+        sel = np.sort(rng.choice(len(bt.near), n_sel, replace=False))
+        vals = []
+        for i in sel:
+            b = bt.near[i]
+            rows = t0.perm[b.row.start : b.row.end]
+            cols = bt.col_tree.perm[b.col.start : b.col.end]
+            if name == "slp":
+                blk = kernels.slp_block(mesh, rows, cols, 3, pq=pq, singular=_OnDemandTable(mesh, kernels.SLP, 5))
+            else:
+                blk = kernels.dlp_block(mesh, rows, cols, 3, vertex_tris=vt, pq=pq,
+                                        singular=_OnDemandTable(mesh, kernels.DLP, 5))
+            vals.append(blk.ravel())
+        out[f"{name}_sel"] = sel
+        out[f"{name}_vals"] = np.concatenate(vals)
+        log(f"l8 {name} blocks")
+    keys = kernels.touching_pairs(mesh, vt)
+    pick = np.sort(rng.choice(len(keys), 5000, replace=False))
+    pa, pb = keys[pick] // mesh.n_triangles, keys[pick] % mesh.n_triangles
+    out["pa"], out["pb"] = pa, pb
+    out["slp_pairs"] = kernels.pair_integrals(mesh, pa, pb, kernels.SLP, 5)
+    out["dlp_pairs"] = kernels.pair_integrals(mesh, pa, pb, kernels.DLP, 5)
+    np.savez_compressed(os.path.join(HERE, "sample_l8.npz"), **out)
+
+
 def gen_cube():
     """Config 4 geometry (3x3x3 unit cubes minus the centre, merged surface) at
     n=4: 1920 flat panels on a lattice -- the split coordinates tie exactly."""
@@ -389,6 +441,7 @@ def main():
         ("h2_dlp4", gen_h2_dlp4),
         ("h2_cfg1", gen_h2_cfg1),
         ("cube", gen_cube),
+        ("sample_l8", gen_sample_l8),
     ]
     if not args.skip_large:
         steps.append(("struct_large", gen_structure_large))

@@ -1,0 +1,59 @@
+"""Parity at configuration-2 size (sphere level 8: 524 288 panels, 262 146
+vertices), where the reference's full nearfield takes hours: a seeded sample
+of single- and double-layer near blocks (regular order 3, Sauter-Schwab
+order 5) and of touching-pair integrals, produced by the reference itself
+(tests/golden/make_golden.py gen_sample_l8), against the device assembly."""
+
+import numpy as np
+import pytest
+
+from .conftest import golden
+from .helpers import rel, sphere, trees
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def world8():
+    from paper_2001_05523_b200 import clustering as C
+    from paper_2001_05523_b200.containers import AssemblyContext
+
+    m = sphere(8)
+    t0, t1 = trees(m, 64)
+    return m, AssemblyContext(m), C.BlockTree(t0, t0, 2.0), C.BlockTree(t0, t1, 2.0)
+
+
+def _blocks(out, lay, sel):
+    """Sampled blocks of a packed device nearfield, row-major, concatenated."""
+    import torch
+
+    idx = []
+    for i in sel:
+        off, ld = int(lay.blk_off[i]), int(lay.blk_ld[i])
+        r, c = int(lay.blk_rows[i]), int(lay.blk_cols[i])
+        idx.append((off + np.arange(r)[:, None] * ld + np.arange(c)[None, :]).ravel())
+    return out[torch.from_numpy(np.concatenate(idx)).cuda()].cpu().numpy()
+
+
+@pytest.mark.parametrize("kind", ["slp", "dlp"])
+def test_level8_near_blocks_vs_reference(world8, kind):
+    from paper_2001_05523_b200.containers import assemble_nearfield_device, near_layout
+
+    g = golden("sample_l8.npz")
+    m, ctx, bs, bd = world8
+    bt = bs if kind == "slp" else bd
+    out = assemble_nearfield_device(ctx, kind, bt, 3, 5)
+    got = _blocks(out, near_layout(bt), g[f"{kind}_sel"])
+    ref = g[f"{kind}_vals"]
+    assert got.shape == ref.shape
+    assert rel(got, ref) < 1e-10
+    if kind == "slp":  # all single-layer entries are positive: entrywise
+        assert np.abs(got - ref).max() / np.abs(ref).min() < 1e-10
+
+
+@pytest.mark.parametrize("kind", ["slp", "dlp"])
+def test_level8_touching_pairs_vs_reference(world8, kind):
+    g = golden("sample_l8.npz")
+    m, ctx, _, _ = world8
+    got = ctx.singular_table(kind, 5).lookup(g["pa"], g["pb"])
+    assert rel(got, g[f"{kind}_pairs"]) < 1e-10
