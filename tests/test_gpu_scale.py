@@ -57,3 +57,31 @@ def test_level8_touching_pairs_vs_reference(world8, kind):
     m, ctx, _, _ = world8
     got = ctx.singular_table(kind, 5).lookup(g["pa"], g["pb"])
     assert rel(got, g[f"{kind}_pairs"]) < 1e-10
+
+
+def test_level8_operator_properties(world8):
+    """Size-independent checks of the level-8 single-layer H^2 operator
+    (device GCA basis, device assembly): symmetry x.Ay = y.Ax of the
+    symmetric Galerkin matrix, linearity, bitwise repeatability, and the
+    block product against the matvec."""
+    import torch
+
+    from paper_2001_05523_b200 import gca
+
+    m, ctx, bs, _ = world8
+    t0 = bs.row_tree
+    b = gca.build_basis(ctx, t0, gca.P0_SLP, 4, 1e-4, device=True)
+    H = gca.assemble_h2(ctx, "slp", bs, b, b, 3, q_singular=5)
+    n = H.shape[0]
+    gen = torch.Generator(device="cuda").manual_seed(8)
+    X = torch.randn((n, 3), dtype=torch.float64, device="cuda", generator=gen)
+    x, z = X[:, 0].contiguous(), X[:, 1].contiguous()
+    ax, az = H.matvec(x), H.matvec(z)
+    assert abs(float(z @ ax - x @ az)) <= 1e-12 * abs(float(z @ ax)) + 1e-12 * float(ax.norm() * z.norm())
+    lin = H.matvec(0.7 * x - 1.3 * z) - (0.7 * ax - 1.3 * az)
+    assert float(lin.norm()) <= 1e-13 * float(ax.norm())
+    assert torch.equal(H.matvec(x), ax)
+    Y = H.matmat(X)
+    for j in range(3):
+        yj = H.matvec(X[:, j].contiguous())
+        assert float((Y[:, j] - yj).abs().max()) <= 1e-13 * float(yj.abs().max())
