@@ -267,7 +267,7 @@ def green_points_batch_device(boxes, m):
     delta = (b[:, 1] - b[:, 0]).max(dim=1).values
     gb = t.stack([b[:, 0] - delta[:, None], b[:, 1] + delta[:, None]], dim=1)
     g = gauss_legendre(m)
-    gp = t.as_tensor(g.points, device="cuda")
+    gp = t.as_tensor(np.array(g.points), device="cuda")
     gw = t.as_tensor(g.weights, device="cuda")
     mm = m * m
     out = t.zeros((n, 6 * mm, 8), dtype=t.float64, device="cuda")
