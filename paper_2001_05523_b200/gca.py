@@ -268,7 +268,7 @@ def green_points_batch_device(boxes, m):
     gb = t.stack([b[:, 0] - delta[:, None], b[:, 1] + delta[:, None]], dim=1)
     g = gauss_legendre(m)
     gp = t.as_tensor(np.array(g.points), device="cuda")
-    gw = t.as_tensor(g.weights, device="cuda")
+    gw = t.as_tensor(np.array(g.weights), device="cuda")
     mm = m * m
     out = t.zeros((n, 6 * mm, 8), dtype=t.float64, device="cuda")
     f = 0
