@@ -15,6 +15,7 @@
 //   k_mm_leaf        Y|_t = D_t X|near(t) + V_t v_t       (nearfield loop + leaf expansion)
 // Each output entry is produced by one lane in a fixed order: deterministic.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "device_common.cuh"
@@ -29,6 +30,8 @@ struct h2b_mmplan {
     double* xhat;    // xhat_len x 16
     double* ycpl;    // yhat_len x 16
     double* v;       // yhat_len x 16
+    uint32_t* flags;  // per column node (forward) then per row node (backward): launch epoch when done
+    unsigned long long* ctr;  // ticket counters of the fused forward / backward launches
 };
 
 namespace h2b {
@@ -361,6 +364,130 @@ __global__ void __launch_bounds__(kMmThreads) k_mm_bwd_level(h2b_layout L, const
                     [&](int m, int n, double val) { out[m * R + n] = val + (cpl ? yc[m * R + n] : 0.0); });
 }
 
+// ---- fused tree transforms (one launch each) --------------------------------------
+// Tasks are ticketed (atomic counter, monotonic over launches: epoch = t / n + 1)
+// in dependency order -- leaves, then inner clusters deepest first (forward);
+// parents first (backward) -- and a task waits only on flags of smaller
+// tickets, so any residency makes progress.  A finished cluster publishes its
+// coefficients with a release store of the epoch into its flag.
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void wait_flag(const uint32_t* f, uint32_t ep) {
+    while (ld_acquire_u32(f) != ep) __nanosleep(64);
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kMmThreads) k_mm_fwd_fused(h2b_layout L, const int32_t* __restrict__ leaves,
+                                                             int n_leaves, const int32_t* __restrict__ inner,
+                                                             int n_inner, const double* __restrict__ X, int nrhs,
+                                                             double* xhat, uint32_t* flags,
+                                                             unsigned long long* ctr, int bs_doubles) {
+    constexpr int R = 8 * NT;
+    extern __shared__ double Bs[];
+    double* red = Bs + bs_doubles;
+    __shared__ int s_task;
+    __shared__ uint32_t s_ep;
+    const int n = n_leaves + n_inner;
+    if (threadIdx.x == 0) {
+        const unsigned long long t = atomicAdd(ctr, 1ull);
+        s_task = (int)(t % (unsigned long long)n);
+        s_ep = (uint32_t)(t / (unsigned long long)n) + 1u;
+    }
+    __syncthreads();
+    const int task = s_task;
+    const uint32_t ep = s_ep;
+    int node;
+    if (task < n_leaves) {
+        node = leaves[task];
+        const int start = L.c_start[node], size = L.c_size[node], k = L.c_rank[node];
+        const double* V = L.c_V + L.c_v_off[node];
+        for (int e = threadIdx.x; e < size * R; e += kMmThreads) {
+            const int r = e % R;
+            Bs[e] = r < nrhs ? X[L.col_perm[start + e / R] * nrhs + r] : 0.0;
+        }
+        __syncthreads();
+        double* out = xhat + L.c_xhat_off[node] * R;
+        cta_product<NT>(k, size, [&](int m, int kk) { return V[(int64_t)kk * k + m]; }, Bs, red,
+                        [&](int m, int c, double v) { out[m * R + c] = v; });
+    } else {
+        node = inner[task - n_leaves];
+        const int kp = L.c_rank[node];
+        const int c0 = L.c_child[2 * node], c1 = L.c_child[2 * node + 1];
+        const int k0 = L.c_rank[c0], k1 = L.c_rank[c1];
+        if (threadIdx.x == 0) {
+            wait_flag(flags + c0, ep);
+            wait_flag(flags + c1, ep);
+        }
+        __syncthreads();
+        const double* x0 = xhat + L.c_xhat_off[c0] * R;
+        const double* x1 = xhat + L.c_xhat_off[c1] * R;
+        for (int e = threadIdx.x; e < (k0 + k1) * R; e += kMmThreads)
+            Bs[e] = e < k0 * R ? __ldcg(x0 + e) : __ldcg(x1 + e - k0 * R);
+        __syncthreads();
+        const double* E0 = L.c_E + L.c_e_off[c0];
+        const double* E1 = L.c_E + L.c_e_off[c1];
+        double* out = xhat + L.c_xhat_off[node] * R;
+        cta_product<NT>(kp, k0 + k1,
+                        [&](int m, int kk) {
+                            return kk < k0 ? E0[(int64_t)kk * kp + m] : E1[(int64_t)(kk - k0) * kp + m];
+                        },
+                        Bs, red, [&](int m, int c, double v) { out[m * R + c] = v; });
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        st_release_u32(flags + node, ep);
+    }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kMmThreads) k_mm_bwd_fused(h2b_layout L, const int32_t* __restrict__ nodes, int n,
+                                                             const double* __restrict__ ycpl, double* v,
+                                                             uint32_t* flags, unsigned long long* ctr,
+                                                             int bs_doubles) {
+    constexpr int R = 8 * NT;
+    extern __shared__ double Bs[];
+    double* red = Bs + bs_doubles;
+    __shared__ int s_task;
+    __shared__ uint32_t s_ep;
+    if (threadIdx.x == 0) {
+        const unsigned long long t = atomicAdd(ctr, 1ull);
+        s_task = (int)(t % (unsigned long long)n);
+        s_ep = (uint32_t)(t / (unsigned long long)n) + 1u;
+    }
+    __syncthreads();
+    const int t = nodes[s_task];
+    const uint32_t ep = s_ep;
+    const int k = L.r_rank[t], p = L.r_parent[t];
+    const bool cpl = L.s_cols[t] > 0;
+    const int kp = p >= 0 ? L.r_rank[p] : 0;
+    if (kp > 0) {
+        if (threadIdx.x == 0) wait_flag(flags + p, ep);
+        __syncthreads();
+        const double* vp = v + L.r_yhat_off[p] * R;
+        for (int e = threadIdx.x; e < kp * R; e += kMmThreads) Bs[e] = __ldcg(vp + e);
+    }
+    __syncthreads();
+    const double* E = L.r_E + (p >= 0 ? L.r_e_off[t] : 0);
+    const double* yc = ycpl + L.r_yhat_off[t] * R;
+    double* out = v + L.r_yhat_off[t] * R;
+    cta_product<NT>(k, kp, [&](int m, int kk) { return E[(int64_t)m * kp + kk]; }, Bs, red,
+                    [&](int m, int c, double val) { out[m * R + c] = val + (cpl ? yc[m * R + c] : 0.0); });
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        st_release_u32(flags + t, ep);
+    }
+}
+
 // ---- couplings, downward transform, nearfield ------------------------------------
 
 template <int NT>
@@ -419,6 +546,26 @@ int run_mm(h2b_mmplan* p, const double* X, int nrhs, double* Y, cudaStream_t st)
     for (auto* f : {(const void*)k_mm_fwd_leaf<NT>})
         H2B_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_tree));
     auto blocks = [](int64_t n) { return (unsigned)((n + kMmWarps - 1) / kMmWarps); };
+    // fused tree launches pay off where launches dominate (config 1: 0.26 -> 0.21 ms
+    // for 8 RHS); on large trees the waiting tasks cost more than the level
+    // launches (sphere L8: 1.44 vs 1.52 ms), so the level kernels are kept there
+    // (H2B_MM_LEVELS=0/1 forces either)
+    const int64_t n_inner = p->fwd_level_off.back(), n_bwd = p->bwd_level_off.back();
+    const char* lv_env = getenv("H2B_MM_LEVELS");
+    const bool levels = lv_env ? lv_env[0] == '1' : (p->n_leaf_c + n_inner > 8192);
+    if (!levels) {
+        for (auto* f : {(const void*)k_mm_fwd_fused<NT>, (const void*)k_mm_bwd_fused<NT>})
+            H2B_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        if (p->n_leaf_c + n_inner > 0)
+            k_mm_fwd_fused<NT><<<(unsigned)(p->n_leaf_c + n_inner), kMmThreads, sm, st>>>(
+                L, lists + p->off_leaf_c, (int)p->n_leaf_c, lists + p->off_fwd, (int)n_inner, X, nrhs, p->xhat,
+                p->flags, p->ctr, bs);
+        if (p->n_cpl > 0)
+            k_mm_cpl<NT><<<(unsigned)p->n_cpl, kMmThreads, sm, st>>>(L, lists + p->off_cpl, p->xhat, p->ycpl, bs);
+        if (n_bwd > 0)
+            k_mm_bwd_fused<NT><<<(unsigned)n_bwd, kMmThreads, sm, st>>>(L, lists + p->off_bwd, (int)n_bwd, p->ycpl,
+                                                                       p->v, p->flags + L.c_nodes, p->ctr + 1, bs);
+    } else {
     if (p->n_leaf_c > 0)
         k_mm_fwd_leaf<NT><<<blocks(p->n_leaf_c), kMmThreads, sm_tree, st>>>(L, lists + p->off_leaf_c,
                                                                            (int)p->n_leaf_c, X, nrhs, p->xhat, slice);
@@ -434,6 +581,7 @@ int run_mm(h2b_mmplan* p, const double* X, int nrhs, double* Y, cudaStream_t st)
         if (b > a)
             k_mm_bwd_level<NT><<<(unsigned)(b - a), kMmThreads, sm, st>>>(L, lists + p->off_bwd + a, p->ycpl, p->v,
                                                                          bs);
+    }
     }
     if (p->n_leaf_r > 0)
         k_mm_leaf<NT><<<(unsigned)p->n_leaf_r, kMmThreads, sm, st>>>(L, lists + p->off_leaf_r, X, nrhs, p->v, Y, bs);
@@ -523,13 +671,17 @@ extern "C" int h2b_matmat_create(const h2b_layout* layout, h2b_mmplan** out) {
     H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->ycpl), sizeof(double) * 16 * (size_t)L.yhat_len));
     H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->v), sizeof(double) * 16 * (size_t)L.yhat_len));
     H2B_CUDA_TRY(cudaMemset(p->ycpl, 0, sizeof(double) * 16 * (size_t)L.yhat_len));
+    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->flags), sizeof(uint32_t) * ((size_t)L.c_nodes + L.r_nodes)));
+    H2B_CUDA_TRY(cudaMemset(p->flags, 0, sizeof(uint32_t) * ((size_t)L.c_nodes + L.r_nodes)));
+    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->ctr), 2 * sizeof(unsigned long long)));
+    H2B_CUDA_TRY(cudaMemset(p->ctr, 0, 2 * sizeof(unsigned long long)));
     *out = p;
     return ok();
 }
 
 extern "C" int h2b_matmat_destroy(h2b_mmplan* p) {
     if (!p) return ok();
-    for (void* q : {(void*)p->d_lists, (void*)p->xhat, (void*)p->ycpl, (void*)p->v})
+    for (void* q : {(void*)p->d_lists, (void*)p->xhat, (void*)p->ycpl, (void*)p->v, (void*)p->flags, (void*)p->ctr})
         if (q) cudaFree(q);
     delete p;
     return ok();
