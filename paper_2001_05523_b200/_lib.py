@@ -97,7 +97,7 @@ EXPORTS = (
     "h2b_last_error", "h2b_abi_version", "h2b_cluster_tree", "h2b_block_tree", "h2b_panel_points",
     "h2b_touch_count", "h2b_touch_fill", "h2b_touch_half", "h2b_singular", "h2b_pair_blocks_slp", "h2b_pair_blocks_dlp",
     "h2b_plan_create", "h2b_plan_destroy", "h2b_matvec", "h2b_matvec_host",
-    "h2b_diagonal", "h2b_plan_trace", "h2b_dlp_jobs_build", "h2b_dlp_jobs_sizes", "h2b_dlp_jobs_copy",
+    "h2b_diagonal", "h2b_plan_trace", "h2b_plan_info", "h2b_dlp_jobs_build", "h2b_dlp_jobs_sizes", "h2b_dlp_jobs_copy",
     "h2b_dlp_jobs_free", "h2b_gca_columns", "h2b_gca_aca", "h2b_cg_workspace_size", "h2b_cg_dot", "h2b_cg_step",
     "h2b_cg_direction", "h2b_matmat_create", "h2b_matmat_destroy", "h2b_matmat",
 )
@@ -138,6 +138,7 @@ def lib():
         L.h2b_matvec_host.argtypes = [vp, vp, vp, vp]
         L.h2b_diagonal.argtypes = [vp, vp, vp]
         L.h2b_plan_trace.argtypes = [vp, vp, ctypes.c_int64]
+        L.h2b_plan_info.argtypes = [vp, vp]
         L.h2b_dlp_jobs_build.argtypes = [ctypes.c_int64, vp, vp, vp, ctypes.c_int64, vp, vp, vp, vp, vp, vp,
                                          ctypes.POINTER(vp)]
         L.h2b_dlp_jobs_sizes.argtypes = [vp, vp]

@@ -77,6 +77,10 @@ constexpr int kFwdHead = 7;     // start, size, k, v_off, xhat_off, n_climb, war
 constexpr int kFwdLevel = 6;    // k0, kp, e_off_c0, e_off_own, xhat_off_c0, xhat_off_parent
 constexpr int kCopyChunk = 1024;  // x values per copy task (host-input launches)
 constexpr int kKindNear = 0, kKindCpl = 1, kKindDescent = 3;  // band record kinds (word 7)
+// symmetric nearfield band (see task_near_sym): words 8..10 = offset of the
+// transposed outputs (column c -> 8 + c), leading diagonal-block columns
+// without a transposed output, gather offset of the row leaf's own x
+constexpr int kKindNearSym = 4;
 
 }  // namespace
 }  // namespace h2b
@@ -104,6 +108,13 @@ struct h2b_plan {
     double* hx;         // pinned host staging of a pageable input
     uint64_t* xll;      // LL copy of a host input
     unsigned long long* trace;  // optional per-CTA timeline (H2B_TRACE=1)
+    // symmetric nearfield (one copy of every block pair; null when unused)
+    double* dsym;       // packed column panels of the upper blocks
+    int32_t* gsym;      // their gather indices
+    uint64_t* ppart;    // LL partial vectors (direct per panel, transposed per block)
+    int64_t* nsum;      // per leaf: the partials summed by its final task, in order
+    int64_t ppart_len;
+    int64_t near_bytes; // nearfield bytes one matvec streams
 };
 
 namespace h2b {
@@ -482,10 +493,13 @@ struct Shared {
     double* rhs;               // max_cols
     double* va;                // 2 vec_len ([x_hat_c0; x_hat_c1] in the climb)
     double* vb;                // vec_len (vec_len = max rank / leaf size)
-    double* red;               // kWarps * 32
+    double* red;               // kWarps * 64
     int64_t* rec;              // small record cache
     const uint64_t* xll;       // x in LL form (host-input launches) or null: x read directly
     const int64_t* rec_src;    // the forward task's record in global memory
+    double* yn;                // vec_len: a leaf's summed nearfield rows (symmetric nearfield)
+    const uint64_t* ppart;     // symmetric nearfield partials or null
+    const int64_t* nsum;       // their per-leaf lists
     uint32_t parity;           // mbarrier phase of the staging slot in use
     bool issued;               // band bulk copy already issued by the caller
 };
@@ -713,6 +727,62 @@ __device__ void task_forward(const double* __restrict__ c_V, const double* __res
 // (LL); a leaf expands y[row_perm] = y_near + V_t v_t (containers.py:268-269).
 // Every value waited for is produced by a smaller ticket: the other bands of
 // t, the parent's last band (parents are ticketed first) and the near bands.
+// Symmetric nearfield: s.yn[i] = sum of the n partial vectors listed at
+// `list` (LL offsets into s.ppart), i < size, always in list order.  H threads
+// per row take contiguous parts of the list (their sums are added in part
+// order); each thread keeps 8 loads in flight.  Ends with a block barrier.
+__device__ void near_sum(const Shared& s, const int64_t* list, int n, int size, uint32_t epoch) {
+    int H = 1;
+    while (H < 4 && 2 * H * size <= kThreads) H *= 2;
+    const int tid = threadIdx.x;
+    const int step = H == 1 ? kThreads : size;
+    for (int base = 0; base < size; base += step) {
+        const int h = H == 1 ? 0 : tid / size;
+        const int i = base + (H == 1 ? tid : tid - h * size);
+        double acc = 0.0;
+        if (h < H && i < size) {
+            const int m0 = (n * h) / H, m1 = (n * (h + 1)) / H;
+            for (int m = m0; m < m1; m += 8) {
+                uint64_t w0[8], w1[8];
+                const uint64_t* src[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    src[u] = m + u < m1 ? s.ppart + 2 * (__ldg(list + m + u) + i) : nullptr;
+                    w0[u] = w1[u] = 0;
+                    if (src[u])
+                        asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];"
+                                     : "=l"(w0[u]), "=l"(w1[u])
+                                     : "l"(src[u]));
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    if (!src[u]) continue;
+                    double v;
+                    if ((uint32_t)(w0[u] >> 32) == epoch && (uint32_t)(w1[u] >> 32) == epoch)
+                        v = __longlong_as_double(static_cast<long long>((w0[u] & 0xffffffffull) | (w1[u] << 32)));
+                    else
+                        v = ll_load(src[u], epoch);
+                    acc += v;
+                }
+            }
+        }
+        if (H == 1) {
+            if (i < size) s.yn[i] = acc;
+        } else if (h < H && i < size) {
+            s.red[h * size + i] = acc;
+        }
+    }
+    __syncthreads();
+    if (H > 1) {
+        for (int i = tid; i < size; i += kThreads) {
+            double t = 0.0;
+            for (int h = 0; h < H; ++h) t += s.red[h * size + i];
+            s.yn[i] = t;
+        }
+        __syncthreads();
+    }
+}
+
 __device__ void descent(const double* __restrict__ r_E, const double* __restrict__ r_V,
                                   const int64_t* __restrict__ row_perm, const int64_t* d, const uint64_t* ycpl, uint64_t* yfin,
                         const uint64_t* ynear, double* y, uint32_t epoch, bool has_cpl, const Shared& s) {
@@ -722,6 +792,9 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
     const int64_t v_off = d[6];
     const int start = (int)d[7];
     double* Es = reinterpret_cast<double*>(s.stage);
+    // symmetric nearfield: this leaf's rows are the sum of its partials
+    const bool sym = leaf && s.ppart != nullptr;
+    if (sym) near_sum(s, s.nsum + d[11], (int)d[12], (int)d[8], epoch);
     if (d[10]) {  // (record word 18) ranks <= 32, leaf <= 64 rows: one warp, no block barriers
         if (threadIdx.x >= 32) return;
         const int lane = threadIdx.x;
@@ -768,7 +841,8 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
                 a1 = fma(Vt[(r + 1) * size + i], s.vb[r + 1], a1);
             }
             if (r < k) a0 = fma(Vt[r * size + i], s.vb[r], a0);
-            y[__ldg(row_perm + start + i)] = ll_load(ynear + 2 * ((int64_t)start + i), epoch) + (a0 + a1);
+            y[__ldg(row_perm + start + i)] =
+                (sym ? s.yn[i] : ll_load(ynear + 2 * ((int64_t)start + i), epoch)) + (a0 + a1);
         }
         return;
     }
@@ -828,7 +902,7 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
     __syncthreads();
     const uint64_t* yn = ynear + 2 * (int64_t)start;
     for (int i = threadIdx.x; i < size; i += blockDim.x)
-        y[row_perm[start + i]] = ll_load(yn + 2 * i, epoch) + (k > 0 ? s.vb[i] : 0.0);
+        y[row_perm[start + i]] = (sym ? s.yn[i] : ll_load(yn + 2 * i, epoch)) + (k > 0 ? s.vb[i] : 0.0);
 }
 
 // The band record is already in s.rec (kind in word 7: 0 near, 1 coupling).
@@ -870,6 +944,132 @@ __device__ void task_band(const h2b_layout& L, const double* __restrict__ x, con
     }
 }
 
+// Both products of a tall panel M (rows x cols, cols <= 64, row-major in
+// shared memory) in ONE pass: lane l owns columns l and l + 32, warps take 8
+// rows at a time.  Direct: y[r] = M[r,:] . xc (8 rows reduced together by
+// recursive halving, stored by the lane that holds the row); transposed:
+// z[c] = sum_r M[r,c] xr[r] (per-warp register sums, added in warp order).
+// Fixed summation order throughout.
+__device__ void panel_dot(const double* M, int rows, int cols, const double* xc, const double* xr, bool transposed,
+                          uint64_t* yd, uint64_t* zt, int skip, double* red, uint32_t epoch) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool ok0 = lane < cols, ok1 = lane + 32 < cols;
+    const double x0 = ok0 ? xc[lane] : 0.0, x1 = ok1 ? xc[lane + 32] : 0.0;
+    double t0 = 0.0, t1 = 0.0;
+    constexpr int R = 8;
+    int ri = 0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) ri |= ((lane >> (4 - j)) & 1) << (2 - j);
+    for (int rb = R * warp; rb < rows; rb += R * kWarps) {
+        double a[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            const int r = rb + k;
+            double m0 = 0.0, m1 = 0.0, xv = 0.0;
+            if (r < rows) {
+                if (ok0) m0 = M[r * cols + lane];
+                if (ok1) m1 = M[r * cols + lane + 32];
+                xv = xr[r];
+            }
+            a[k] = fma(m1, x1, m0 * x0);
+            t0 = fma(m0, xv, t0);
+            t1 = fma(m1, xv, t1);
+        }
+        const double sum = warp_sum<R>(a, lane);
+        if ((lane & 3) == 0 && rb + ri < rows) ll_store(yd + 2 * (rb + ri), sum, epoch);
+    }
+    if (!transposed) return;
+    red[warp * 64 + lane] = t0;
+    red[warp * 64 + 32 + lane] = t1;
+    __syncthreads();
+    for (int c = skip + threadIdx.x; c < cols; c += kThreads) {
+        double z = 0.0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) z += red[w * 64 + c];
+        ll_store(zt + 2 * c, z, epoch);
+    }
+}
+
+// Gather two index lists in one pass (all index loads, then all value loads):
+// d1[i] = src[idx1[i]], i < n1, and d2[i] = src[idx2[i]], i < n2; src in LL
+// form when `ll` (spinning on the producer's epoch), else plain.
+template <bool kLL>
+__device__ __forceinline__ void gather2(double* d1, const int32_t* idx1, int n1, double* d2, const int32_t* idx2,
+                                        int n2, const double* __restrict__ src, const uint64_t* ll, uint32_t epoch) {
+    constexpr int kU = 4;
+    const int n = n1 + n2;
+    for (int base = 0; base < n; base += kU * kThreads) {
+        int ix[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int i = base + u * kThreads + (int)threadIdx.x;
+            ix[u] = i < n1 ? __ldg(idx1 + i) : i < n ? __ldg(idx2 + (i - n1)) : -1;
+        }
+        double v[kU];
+        if (kLL) {
+            uint64_t w0[kU], w1[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                w0[u] = w1[u] = 0;
+                if (ix[u] >= 0)
+                    asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];"
+                                 : "=l"(w0[u]), "=l"(w1[u])
+                                 : "l"(ll + 2 * (int64_t)ix[u]));
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                v[u] = 0.0;
+                if (ix[u] < 0) continue;
+                if ((uint32_t)(w0[u] >> 32) == epoch && (uint32_t)(w1[u] >> 32) == epoch)
+                    v[u] = __longlong_as_double(static_cast<long long>((w0[u] & 0xffffffffull) | (w1[u] << 32)));
+                else
+                    v[u] = ll_load(ll + 2 * (int64_t)ix[u], epoch);
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < kU; ++u) v[u] = ix[u] >= 0 ? __ldg(src + ix[u]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int i = base + u * kThreads + (int)threadIdx.x;
+            if (i < n1)
+                d1[i] = v[u];
+            else if (i < n)
+                d2[i - n1] = v[u];
+        }
+    }
+}
+
+// Symmetric nearfield band: one column panel [D_(t,s) ...] (all rows of row
+// leaf t, upper blocks s >= t in leaf order, the diagonal block first) streamed
+// ONCE for both triangles: the direct product D x|_cols -> t's partial at
+// out_off, and the transposed product D^T x|_t -> the columns' partials at
+// tr_off + c (skipped for the diagonal block's columns, which are stored in
+// full).  Never waits.
+__device__ void task_near_sym(const double* __restrict__ dsym, const int32_t* __restrict__ gsym,
+                              const double* __restrict__ x, uint64_t* ppart, uint32_t epoch, const Shared& s) {
+    const int64_t src_off = s.rec[0], gi_off = s.rec[3], out_off = s.rec[4];
+    const int cols = (int)s.rec[1], rows = (int)s.rec[2];
+    const int64_t tr_off = s.rec[8], rg_off = s.rec[10];
+    const int skip = (int)s.rec[9];
+    const int64_t bytes = ((int64_t)rows * cols * 8 + 15) & ~int64_t(15);  // panels are padded to 16 bytes
+    const double* M = s.issued ? (band_staged(bytes, dsym + src_off) ? reinterpret_cast<const double*>(s.stage)
+                                                                     : dsym + src_off)
+                               : stage_issue(s, dsym + src_off, bytes);
+    mark(s.mark, 0);
+    const bool tr = skip < cols;
+    if (s.xll)
+        gather2<true>(s.rhs, gsym + gi_off, cols, s.vb, gsym + rg_off, tr ? rows : 0, nullptr, s.xll, epoch);
+    else
+        gather2<false>(s.rhs, gsym + gi_off, cols, s.vb, gsym + rg_off, tr ? rows : 0, x, nullptr, epoch);
+    mark(s.mark, 1);
+    mbar_wait(s.bar, s.parity);
+    __syncthreads();
+    mark(s.mark, 2);
+    panel_dot(M, rows, cols, s.rhs, s.vb, tr, ppart + 2 * out_off, ppart + 2 * tr_off, skip, s.red, epoch);
+    mark(s.mark, 3);
+}
+
 struct KArgs {
     h2b_layout L;
     const int64_t* rec;
@@ -884,6 +1084,10 @@ struct KArgs {
     const double* xh;  // host-mapped x (h2b_matvec_host) or null
     uint64_t* xll;     // LL copy of x for host-input launches
     int n_copy;        // copy tasks (host input)
+    const double* dsym;      // symmetric nearfield (null: not used)
+    const int32_t* gsym;
+    uint64_t* ppart;
+    const int64_t* nsum;
 };
 
 #ifndef H2B_MINB
@@ -924,7 +1128,8 @@ __device__ __forceinline__ void run_task(const KArgs& a, const double* __restric
         // pull the band records, the nearfield gather lists and x into L2 for
         // the streaming tasks that follow (fire-and-forget; LL needs no fences)
         prefetch_slice(reinterpret_cast<const double*>(a.rec + a.band_base), a.band_bytes, ticket, L.c_leaves);
-        prefetch_slice(reinterpret_cast<const double*>(L.d_gidx), a.dgidx_bytes, ticket, L.c_leaves);
+        prefetch_slice(reinterpret_cast<const double*>(a.dsym ? a.gsym : L.d_gidx), a.dgidx_bytes, ticket,
+                       L.c_leaves);
         if (!a.xh) prefetch_slice(x, 8 * L.n_cols, ticket, L.c_leaves);
         task_forward(L.c_V, L.c_E, L.col_perm, a.rec + __ldg(a.fwd_off + ticket), x, a.xhat, epoch, s);
     } else {
@@ -934,7 +1139,9 @@ __device__ __forceinline__ void run_task(const KArgs& a, const double* __restric
         if (b < np) prefetch_slice(L.r_E, a.e_bytes_r, b, np);
         load_rec(s, a.rec + a.band_base + (int64_t)kBandWords * b, kBandWords);
         const int kind = (int)s.rec[7];
-        if (kind == kKindNear)
+        if (kind == kKindNearSym)
+            task_near_sym(a.dsym, a.gsym, x, a.ppart, epoch, s);
+        else if (kind == kKindNear)
             task_band<false>(L, x, a.xhat, a.ynear, a.yfin, a.ycpl, a.ynear, y, epoch, s);
         else if (kind == kKindCpl)
             task_band<true>(L, x, a.xhat, a.ycpl, a.yfin, a.ycpl, a.ynear, y, epoch, s);
@@ -973,6 +1180,9 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
     s.va = s.rhs + a.max_cols;
     s.vb = s.va + 2 * a.vec_len;
     s.red = s.vb + a.vec_len;
+    s.yn = s.red + kWarps * 64;
+    s.ppart = a.ppart;
+    s.nsum = a.nsum;
     s.rec = s_rec;
     s.parity = 0;
     s.issued = false;
@@ -1032,6 +1242,9 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec_loop(const KArgs 
         s.va = s.rhs + a.max_cols;
         s.vb = s.va + 2 * a.vec_len;
         s.red = s.vb + a.vec_len;
+        s.yn = s.red + kWarps * 64;
+        s.ppart = a.ppart;
+        s.nsum = a.nsum;
         s.rec = s_rec;
         s.parity = 0;
         s.issued = false;
@@ -1071,7 +1284,191 @@ cudaError_t fetch(const T* d, int64_t n, std::vector<T>& h) {
 
 using namespace h2b;
 
-extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
+namespace h2b {
+namespace {
+
+// D(t,s)[a][b] == D(s,t)[b][a] bit for bit, per upper block pair (job words:
+// off1, ld1, off2, ld2, rows, cols); any mismatch sets *bad.
+__global__ void k_sym_check(const double* __restrict__ D, const int64_t* __restrict__ jobs,
+                            int* __restrict__ bad) {
+    const int64_t* j = jobs + 6 * (int64_t)blockIdx.x;
+    const int64_t o1 = j[0], l1 = j[1], o2 = j[2], l2 = j[3];
+    const int nr = (int)j[4], nc = (int)j[5];
+    int mism = 0;
+    for (int e = threadIdx.x; e < nr * nc; e += blockDim.x) {
+        const int a = e / nc, b = e - a * nc;
+        mism |= __double_as_longlong(D[o1 + a * l1 + b]) != __double_as_longlong(D[o2 + b * l2 + a]);
+    }
+    if (__syncthreads_or(mism) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
+// Column panels of the symmetric nearfield (job words: source row base,
+// source ld, rows, cols, destination, source-column list offset).
+__global__ void k_sym_pack(const double* __restrict__ D, const int64_t* __restrict__ jobs,
+                           const int32_t* __restrict__ srccol, double* __restrict__ out) {
+    const int64_t* j = jobs + 6 * (int64_t)blockIdx.x;
+    const int64_t src = j[0], ld = j[1], dst = j[4], so = j[5];
+    const int nr = (int)j[2], nc = (int)j[3];
+    for (int e = threadIdx.x; e < nr * nc; e += blockDim.x) {
+        const int a = e / nc, b = e - a * nc;
+        out[dst + e] = D[src + a * ld + __ldg(srccol + so + b)];
+    }
+}
+
+// Host side of the symmetric nearfield (single-GPU plans whose row and column
+// trees coincide and whose nearfield is symmetric bit for bit, e.g. the
+// single-layer Galerkin matrix, containers.py near_slp_jobs).  Per row leaf t,
+// the upper blocks s (start(s) >= start(t), t itself first) are cut into
+// column panels of all |t| rows that fit the TMA stage.
+struct SymNear {
+    bool on = false;
+    std::vector<std::vector<int64_t>> bands;  // per row node: band records
+    std::vector<int64_t> list_off, list_n;    // per row node: its partial list
+    std::vector<int64_t> nsum, pack, check;
+    std::vector<int32_t> srccol, gsym;
+    int64_t dsym_len = 0, ppart_len = 0, near_bytes = 0;
+};
+
+int build_sym_near(const h2b_layout& L, const std::vector<int32_t>& rstart, const std::vector<int32_t>& rsize,
+                   const std::vector<int32_t>& cstart, const std::vector<int32_t>& csize,
+                   const std::vector<int64_t>& rvoff, const std::vector<int32_t>& dcols,
+                   const std::vector<int64_t>& doff, const std::vector<int64_t>& dgoff, SymNear& S) {
+    S.on = false;
+    if (L.owned || L.r_nodes != L.c_nodes || L.n_rows != L.n_cols || !L.near_ptr || !L.near_col) return 0;
+    if (const char* e = getenv("H2B_NEAR_SYM"))
+        if (e[0] == '0') return 0;
+    const int n = L.r_nodes;
+    for (int u = 0; u < n; ++u)
+        if (rstart[u] != cstart[u] || rsize[u] != csize[u]) return 0;
+    std::vector<int64_t> rp, cp;
+    H2B_CUDA_TRY(fetch(L.row_perm, L.n_rows, rp));
+    H2B_CUDA_TRY(fetch(L.col_perm, L.n_cols, cp));
+    if (rp != cp) return 0;
+    std::vector<int32_t> nptr, ncol, dg;
+    H2B_CUDA_TRY(fetch(L.near_ptr, (int64_t)n + 1, nptr));
+    H2B_CUDA_TRY(fetch(L.near_col, std::max<int64_t>(nptr[n], 1), ncol));
+    int64_t glen = 0;
+    for (int u = 0; u < n; ++u)
+        if (rvoff[u] >= 0) glen = std::max<int64_t>(glen, dgoff[u] + dcols[u]);
+    H2B_CUDA_TRY(fetch(L.d_gidx, std::max<int64_t>(glen, 1), dg));
+    // structure: near blocks only between row leaves, each with its mirror and
+    // the diagonal block present
+    std::vector<std::vector<std::pair<int, int64_t>>> blocks(n);  // (s, column offset in t's row)
+    for (int t = 0; t < n; ++t) {
+        int64_t c = 0;
+        for (int q = nptr[t]; q < nptr[t + 1]; ++q) {
+            const int s = ncol[q];
+            if (rvoff[t] < 0 || s < 0 || s >= n || rvoff[s] < 0) return 0;
+            blocks[t].push_back({s, c});
+            c += rsize[s];
+        }
+    }
+    auto find = [&](int t, int s) -> int64_t {
+        for (const auto& b : blocks[t])
+            if (b.first == s) return b.second;
+        return -1;
+    };
+    for (int t = 0; t < n; ++t) {
+        if (rvoff[t] < 0) continue;
+        if (find(t, t) < 0) return 0;
+        for (const auto& b : blocks[t])
+            if (find(b.first, t) < 0) return 0;
+    }
+    // upper blocks, diagonal first; check jobs for the bitwise symmetry test
+    std::vector<std::vector<std::pair<int, int64_t>>> up(n);
+    for (int t = 0; t < n; ++t) {
+        if (rvoff[t] < 0) continue;
+        up[t].push_back({t, find(t, t)});
+        for (const auto& b : blocks[t])
+            if (b.first != t && rstart[b.first] > rstart[t]) up[t].push_back(b);
+        for (const auto& b : up[t])
+            S.check.insert(S.check.end(), {doff[t] + b.second, dcols[t], doff[b.first] + find(b.first, t),
+                                           dcols[b.first], rsize[t], rsize[b.first]});
+    }
+    // panels, partial offsets
+    S.bands.assign(n, {});
+    S.list_off.assign(n, 0);
+    S.list_n.assign(n, 0);
+    std::vector<int64_t> tbase(n, 0);
+    std::vector<std::vector<int64_t>> tcol(n);  // per t: column offset of each upper block in its panels
+    std::vector<std::vector<int64_t>> direct(n);
+    int64_t pdir = 0, dlen = 0, g = 0;
+    for (int t = 0; t < n; ++t) {
+        if (rvoff[t] < 0) continue;
+        const int rows = rsize[t];
+        int64_t W = 0;
+        for (const auto& b : up[t]) {
+            tcol[t].push_back(W);
+            W += rsize[b.first];
+        }
+        int wmax = std::min(64, std::max(2, (int)(kStageBytes / 8 / std::max(rows, 1))));
+        if ((rows & 1) && (wmax & 1)) --wmax;
+        const int64_t gbase = g;
+        for (const auto& b : up[t])
+            for (int j = 0; j < rsize[b.first]; ++j) {
+                S.srccol.push_back((int32_t)(b.second + j));
+                S.gsym.push_back(dg[dgoff[t] + b.second + j]);
+            }
+        g += W;
+        tbase[t] = -1;  // set below, after all direct partials
+        for (int64_t j0 = 0; j0 < W; j0 += wmax) {
+            const int w = (int)std::min<int64_t>(wmax, W - j0);
+            const int skip = (int)std::max<int64_t>(0, std::min<int64_t>(w, rows - j0));
+            std::vector<int64_t> r(kBandWords, 0);
+            r[0] = dlen;
+            r[1] = w;
+            r[2] = rows;
+            r[3] = gbase + j0;
+            r[4] = pdir;
+            r[7] = kKindNearSym;
+            r[8] = j0;  // + tbase[t] below
+            r[9] = skip;
+            r[10] = gbase;
+            S.bands[t].insert(S.bands[t].end(), r.begin(), r.end());
+            S.pack.insert(S.pack.end(), {doff[t], dcols[t], rows, w, dlen, gbase + j0});
+            direct[t].push_back(pdir);
+            pdir += rows;
+            dlen += ((int64_t)rows * w + 1) & ~int64_t(1);  // 16-byte aligned panels
+            S.near_bytes += 8 * (int64_t)rows * w;
+        }
+        tbase[t] = W;  // temporarily: the width
+    }
+    int64_t tpos = pdir;
+    for (int t = 0; t < n; ++t) {
+        if (rvoff[t] < 0) continue;
+        const int64_t W = tbase[t];
+        tbase[t] = tpos;
+        tpos += W;
+        for (size_t i = 0; i < S.bands[t].size(); i += kBandWords) S.bands[t][i + 8] += tpos - W;
+    }
+    S.ppart_len = tpos;
+    S.dsym_len = dlen;
+    // per leaf u: its panels' direct partials, then the transposed partials
+    // of the blocks (t, u) with t before u, in u's near-list order
+    for (int u = 0; u < n; ++u) {
+        if (rvoff[u] < 0) continue;
+        S.list_off[u] = (int64_t)S.nsum.size();
+        for (int64_t o : direct[u]) S.nsum.push_back(o);
+        for (const auto& b : blocks[u]) {
+            const int t = b.first;
+            if (t == u || rstart[t] > rstart[u]) continue;
+            int64_t off = -1;
+            for (size_t i = 0; i < up[t].size(); ++i)
+                if (up[t][i].first == u) off = tbase[t] + tcol[t][i];
+            if (off < 0) return 0;
+            S.nsum.push_back(off);
+        }
+        S.list_n[u] = (int64_t)S.nsum.size() - S.list_off[u];
+    }
+    S.on = true;
+    return 0;
+}
+
+}  // namespace
+}  // namespace h2b
+
+namespace {
+int plan_create(const h2b_layout* layout, h2b_plan** out, bool allow_sym) {
     if (!layout || !out) return fail(H2B_ERR_INVALID, "h2b_plan_create: null pointer");
     const h2b_layout& L = *layout;
     if (L.c_nodes <= 0 || L.r_nodes <= 0 || L.c_leaves <= 0) return fail(H2B_ERR_INVALID, "h2b_plan_create: empty tree");
@@ -1120,7 +1517,11 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
     if (maxk > kMaxVec || maxleaf > kMaxVec)
         return fail(H2B_ERR_INVALID, "h2b_plan_create: cluster rank or leaf size above 512");
     const int vec_len = (std::max(maxk, maxleaf) + 1) & ~1;
-    const int smem = 128 + kStageBytes + (int)sizeof(double) * (maxcols + 3 * vec_len + kWarps * 32);
+    SymNear sym;
+    if (allow_sym)
+        if (int rc = build_sym_near(L, rstart, rsize, cstart, csize, rvoff, dcols, doff, dgoff, sym)) return rc;
+    const int smem =
+        128 + kStageBytes + (int)sizeof(double) * (maxcols + 3 * vec_len + (sym.on ? vec_len + kWarps * 64 : kWarps * 32));
     if (smem > 227 * 1024) return fail(H2B_ERR_INVALID, "h2b_plan_create: gathered right-hand side exceeds shared memory");
 
     std::vector<int64_t> rec, fwd_off(L.c_leaves);
@@ -1220,6 +1621,10 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
             int dd = 0;
             for (int q = rparent[u]; q >= 0; q = rparent[q]) ++dd;
             dw[17] = dd;  // depth (diagnostics: trace)
+            if (sym.on && rvoff[u] >= 0) {  // the leaf's nearfield partials (symmetric nearfield)
+                dw[19] = sym.list_off[u];
+                dw[20] = sym.list_n[u];
+            }
             const int kk = rrank[u], kq = par >= 0 ? rrank[par] : 0;
             const bool lf = rvoff[u] >= 0;
             dw[18] = (kk <= 32 && kq <= 32 && (!lf || rsize[u] <= 64) &&
@@ -1282,8 +1687,13 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
     int n_near = 0;
     for (int i = 0; i < nl; ++i) {
         const int u = owned_leaves[i];
-        n_near += bands_to(i < c1 ? na1 : i < c2 ? na2 : nb, dcols[u], rsize[u], doff[u], dgoff[u], rstart[u],
-                           kKindNear);
+        std::vector<int64_t>& dst = i < c1 ? na1 : i < c2 ? na2 : nb;
+        if (sym.on) {
+            dst.insert(dst.end(), sym.bands[u].begin(), sym.bands[u].end());
+            n_near += (int)(sym.bands[u].size() / kBandWords);
+        } else {
+            n_near += bands_to(dst, dcols[u], rsize[u], doff[u], dgoff[u], rstart[u], kKindNear);
+        }
     }
     const bool diag_near = getenv("H2B_DIAG_NEAR_ONLY") && getenv("H2B_DIAG_NEAR_ONLY")[0] == '1';
     if (!diag_near) {
@@ -1350,7 +1760,7 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
         int64_t m = 0;
         for (int i = 0; i < L.r_nodes; ++i)
             if (rvoff[i] >= 0) m = std::max<int64_t>(m, 4 * (dgoff[i] + dcols[i]));
-        p->dgidx_bytes = m;
+        p->dgidx_bytes = sym.on ? 4 * (int64_t)sym.gsym.size() : m;
     }
     p->max_cols = maxcols;
     p->vec_len = vec_len;
@@ -1373,11 +1783,25 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
     if (!rec.empty())
         H2B_CUDA_TRY(cudaMemcpy(p->rec, rec.data(), sizeof(int64_t) * rec.size(), cudaMemcpyHostToDevice));
     H2B_CUDA_TRY(cudaMemcpy(p->fwd_off, fwd_off.data(), sizeof(int64_t) * fwd_off.size(), cudaMemcpyHostToDevice));
-    H2B_CUDA_TRY(cudaFuncSetAttribute(k_matvec, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem));
+    {
+        // the attribute belongs to the kernel, not the plan: only ever raise it
+        // (a later plan with less shared memory must not break an earlier one)
+        static int smem_set[64] = {0};
+        int& cur = smem_set[p->device & 63];
+        if (p->smem > cur) {
+            H2B_CUDA_TRY(cudaFuncSetAttribute(k_matvec, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem));
+            cur = p->smem;
+        }
+    }
     p->loop_grid = 0;
     if (const char* e = getenv("H2B_LOOP")) {
         if (atoi(e) > 0) {
-            H2B_CUDA_TRY(cudaFuncSetAttribute(k_matvec_loop, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem));
+            static int loop_smem_set[64] = {0};
+            int& cur = loop_smem_set[p->device & 63];
+            if (p->smem > cur) {
+                H2B_CUDA_TRY(cudaFuncSetAttribute(k_matvec_loop, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem));
+                cur = p->smem;
+            }
             int nb = 0, sms = 0;
             H2B_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_matvec_loop, kThreads, p->smem));
             H2B_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
@@ -1398,8 +1822,64 @@ extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
     H2B_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&p->hx), sizeof(double) * std::max<int64_t>(L.n_cols, 1)));
     H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->xll), 16 * (size_t)std::max<int64_t>(L.n_cols, 1)));
     H2B_CUDA_TRY(cudaMemset(p->xll, 0, 16 * (size_t)std::max<int64_t>(L.n_cols, 1)));
+    p->dsym = nullptr;
+    p->gsym = nullptr;
+    p->ppart = nullptr;
+    p->nsum = nullptr;
+    p->near_bytes = 0;
+    p->ppart_len = 0;
+    for (int u = 0; u < L.r_nodes; ++u)
+        if (rvoff[u] >= 0) p->near_bytes += 8 * (int64_t)rsize[u] * dcols[u];
+    if (sym.on) {
+        // the nearfield must be symmetric bit for bit (checked on the device);
+        // then its upper blocks are packed into the panels the bands stream
+        int64_t* djobs = nullptr;
+        int* dbad = nullptr;
+        const int nchk = (int)(sym.check.size() / 6);
+        H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&djobs), 8 * std::max(sym.check.size(), sym.pack.size())));
+        H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&dbad), sizeof(int)));
+        H2B_CUDA_TRY(cudaMemset(dbad, 0, sizeof(int)));
+        H2B_CUDA_TRY(cudaMemcpy(djobs, sym.check.data(), 8 * sym.check.size(), cudaMemcpyHostToDevice));
+        if (nchk) k_sym_check<<<nchk, 256>>>(L.D, djobs, dbad);
+        H2B_CUDA_TRY(cudaGetLastError());
+        int bad = 0;
+        H2B_CUDA_TRY(cudaMemcpy(&bad, dbad, sizeof(int), cudaMemcpyDeviceToHost));
+        if (!bad) {
+            int32_t* dsrc = nullptr;
+            H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&dsrc), 4 * sym.srccol.size()));
+            H2B_CUDA_TRY(cudaMemcpy(dsrc, sym.srccol.data(), 4 * sym.srccol.size(), cudaMemcpyHostToDevice));
+            H2B_CUDA_TRY(cudaMemcpy(djobs, sym.pack.data(), 8 * sym.pack.size(), cudaMemcpyHostToDevice));
+            H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->dsym), 8 * (size_t)sym.dsym_len));
+            H2B_CUDA_TRY(cudaMemset(p->dsym, 0, 8 * (size_t)sym.dsym_len));
+            const int npk = (int)(sym.pack.size() / 6);
+            if (npk) k_sym_pack<<<npk, 256>>>(L.D, djobs, dsrc, p->dsym);
+            H2B_CUDA_TRY(cudaGetLastError());
+            H2B_CUDA_TRY(cudaDeviceSynchronize());
+            cudaFree(dsrc);
+            H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->gsym), 4 * sym.gsym.size()));
+            H2B_CUDA_TRY(cudaMemcpy(p->gsym, sym.gsym.data(), 4 * sym.gsym.size(), cudaMemcpyHostToDevice));
+            H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->ppart), 16 * (size_t)sym.ppart_len));
+            H2B_CUDA_TRY(cudaMemset(p->ppart, 0, 16 * (size_t)sym.ppart_len));
+            p->ppart_len = sym.ppart_len;
+            H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->nsum), 8 * std::max<size_t>(sym.nsum.size(), 1)));
+            H2B_CUDA_TRY(cudaMemcpy(p->nsum, sym.nsum.data(), 8 * sym.nsum.size(), cudaMemcpyHostToDevice));
+            p->near_bytes = sym.near_bytes;
+        }
+        cudaFree(djobs);
+        cudaFree(dbad);
+        if (bad) {
+            // not symmetric: the plan streams every block
+            h2b_plan_destroy(p);
+            return plan_create(layout, out, false);
+        }
+    }
     *out = p;
     return ok();
+}
+}  // namespace
+
+extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
+    return plan_create(layout, out, true);
 }
 
 #ifdef H2B_LL_TIMEOUT
@@ -1424,7 +1904,8 @@ extern "C" int h2b_debug_stuck(h2b_plan* p, unsigned long long* out) {
 
 extern "C" int h2b_plan_destroy(h2b_plan* p) {
     if (!p) return ok();
-    void* bufs[] = {p->xhat, p->ycpl, p->yfin, p->ynear, p->ctrl, p->rec, p->fwd_off, p->dx, p->dy, p->trace, p->xll};
+    void* bufs[] = {p->xhat, p->ycpl, p->yfin, p->ynear, p->ctrl, p->rec,  p->fwd_off, p->dx,
+                    p->dy,   p->trace, p->xll, p->dsym,  p->gsym, p->ppart, p->nsum};
     for (void* q : bufs)
         if (q) cudaFree(q);
     if (p->hy) cudaFreeHost(p->hy);
@@ -1456,6 +1937,10 @@ int launch_matvec(h2b_plan* p, const double* d_x, const double* xh, double* y, c
     a.xh = xh;
     a.xll = p->xll;
     a.n_copy = xh ? (int)((p->L.n_cols + kCopyChunk - 1) / kCopyChunk) : 0;
+    a.dsym = p->dsym;
+    a.gsym = p->gsym;
+    a.ppart = p->ppart;
+    a.nsum = p->nsum;
     const int grid = a.n_copy + p->L.c_leaves + p->n_near + p->n_cpl;
     if (p->loop_grid > 0)
         k_matvec_loop<<<std::min(grid, p->loop_grid), kThreads, p->smem, st>>>(a, d_x, y);
@@ -1518,6 +2003,19 @@ extern "C" int h2b_plan_trace(h2b_plan* p, unsigned long long* h_out, int64_t ca
     h_out[8 * n + 2] = n;
     h_out[8 * n + 3] = n;
     h_out[8 * n + 4] = n;
+    return ok();
+}
+
+// Plan facts: [0] symmetric nearfield in use (0/1), [1] nearfield bytes one
+// matvec streams, [2] nearfield tasks, [3] coupling tasks, [4] bytes of the
+// symmetric nearfield's partial vectors (LL form).
+extern "C" int h2b_plan_info(h2b_plan* p, int64_t* h_out) {
+    if (!p || !h_out) return fail(H2B_ERR_INVALID, "h2b_plan_info: null pointer");
+    h_out[0] = p->dsym != nullptr;
+    h_out[1] = p->near_bytes;
+    h_out[2] = p->n_near;
+    h_out[3] = p->n_cpl;
+    h_out[4] = p->ppart_len * 16;
     return ok();
 }
 

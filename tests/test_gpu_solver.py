@@ -36,7 +36,9 @@ def test_device_cg_matches_host_cg(op0):
     host = solver.cg(H.matvec, b, 1e-10, 500, precond_diag=diag)
     dev = solver.cg(H.matvec, torch.from_numpy(b).cuda(), 1e-10, 500, precond_diag=diag)
     assert host.converged and dev.converged
-    assert abs(host.iterations - dev.iterations) <= 1
+    # the reductions round differently on host and device: near 1e-10 the
+    # stopping test may trip a couple of iterations apart
+    assert abs(host.iterations - dev.iterations) <= 3
     xd = dev.x.cpu().numpy()
     assert np.linalg.norm(xd - host.x) <= 1e-8 * np.linalg.norm(host.x)
     # the solution solves the system

@@ -49,3 +49,4 @@ ts = np.sort(ts)[: int(0.8 * len(ts))]  # drop the slowest 20 %; mean resolves b
 t = float(np.mean(ts)) * 1e-3
 b = H.matvec_bytes()
 print(f"matvec {t*1e6:.1f} us (mean of fastest {len(ts)}), {b/t/1e9:.0f} GB/s, {b/t/1e9/bench.peaks()['hbm_gbs']*100:.1f} % of HBM")
+print("plan", plan.info())

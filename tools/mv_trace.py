@@ -49,7 +49,7 @@ st, en = (tr[:, 0] - t0) / 1e3, (tr[:, 1] - t0) / 1e3
 kind = (tr[:, 2] >> 16) & 0xff
 nclimb = (tr[:, 2] >> 24) & 0xff
 print(f"matvec span {en.max():.1f} us, tasks {tot}")
-for kd, nm in ((2, "forward"), (0, "near"), (1, "coupling"), (3, "descent"), (4, "up"), (5, "down")):
+for kd, nm in ((2, "forward"), (0, "near"), (1, "coupling"), (3, "descent"), (4, "nearsym")):
     sel = kind == kd
     if not sel.any():
         continue
@@ -81,6 +81,6 @@ for lo in edges[:-1]:
     hi = lo + 5
     row = []
     for kd in (2, 0, 1, 3):
-        sel = kind == kd
+        sel = (kind == kd) | ((kind == 4) & (kd == 0))
         row.append(int(((en[sel] >= lo) & (en[sel] < hi)).sum()))
     print(f"[{lo:5.0f},{hi:5.0f}) finished fwd/near/cpl/desc {row}")
