@@ -330,9 +330,10 @@ int h2b_matvec_host(h2b_plan* plan, const double* h_x, double* h_y, void* stream
  * with the environment variable H2B_TRACE=1 (3 words per CTA ticket: start
  * ns, end ns, SM id; then 5 words of ticket-range boundaries). */
 int h2b_plan_trace(h2b_plan* plan, unsigned long long* h_out, int64_t cap);
-/* Plan facts (5 words): symmetric nearfield in use (0/1; single-GPU plans whose
+/* Plan facts (7 words): symmetric nearfield in use (0/1; single-GPU plans whose
  * nearfield is symmetric bit for bit stream each block pair once), nearfield
- * bytes per matvec, nearfield tasks, coupling tasks, partial-vector bytes. */
+ * bytes per matvec, nearfield tasks, coupling tasks, partial-vector bytes,
+ * symmetric couplings in use (0/1; same rule for S), coupling bytes per matvec. */
 int h2b_plan_info(h2b_plan* plan, int64_t* h_out);
 /* Multi-right-hand-side product Y = A X for 1 <= nrhs <= 16 device vectors
  * (X: n_cols x nrhs, Y: n_rows x nrhs, row-major, natural dof order) over the

@@ -507,15 +507,17 @@ class H2Matrix:
     def matvec_bytes(self):
         """Algorithmic HBM bytes of one matvec: every operator
         entry once, each basis in both roles, plus x and y.  A symmetric
-        nearfield is stored and streamed once per block pair (MatvecPlan.info):
-        its bytes are the upper blocks only."""
+        nearfield (or coupling set) is stored and streamed once per block pair
+        (MatvecPlan.info): its bytes are the upper blocks only."""
         basis_r = self.row_basis.storage_floats()
         basis_c = self.col_basis.storage_floats()
-        near = 8 * self.near_layout.entries
+        near, cpl = 8 * self.near_layout.entries, 8 * self.far_layout.entries
         info = self.plan().info()
         if info["near_symmetric"]:
             near = info["near_bytes"]
-        return near + 8 * (self.far_layout.entries + basis_r + basis_c + self.shape[0] + self.shape[1])
+        if info["coupling_symmetric"]:
+            cpl = info["coupling_bytes"]
+        return near + cpl + 8 * (basis_r + basis_c + self.shape[0] + self.shape[1])
 
 
 def _scatter(flat, off, ld, block):
@@ -676,10 +678,11 @@ class MatvecPlan:
         """Plan facts (h2b_plan_info): whether the nearfield is streamed once
         per block pair (single-GPU plans of a bitwise symmetric nearfield), the
         nearfield bytes one matvec streams, task counts."""
-        out = (ctypes.c_int64 * 5)()
+        out = (ctypes.c_int64 * 7)()
         _lib.check(_lib.lib().h2b_plan_info(self.handle, out))
         return {"near_symmetric": bool(out[0]), "near_bytes": int(out[1]), "near_tasks": int(out[2]),
-                "coupling_tasks": int(out[3]), "partial_bytes": int(out[4])}
+                "coupling_tasks": int(out[3]), "partial_bytes": int(out[4]), "coupling_symmetric": bool(out[5]),
+                "coupling_bytes": int(out[6])}
 
 
 class MatmatPlan:

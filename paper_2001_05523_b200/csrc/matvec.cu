@@ -77,10 +77,11 @@ constexpr int kFwdHead = 7;     // start, size, k, v_off, xhat_off, n_climb, war
 constexpr int kFwdLevel = 6;    // k0, kp, e_off_c0, e_off_own, xhat_off_c0, xhat_off_parent
 constexpr int kCopyChunk = 1024;  // x values per copy task (host-input launches)
 constexpr int kKindNear = 0, kKindCpl = 1, kKindDescent = 3;  // band record kinds (word 7)
-// symmetric nearfield band (see task_near_sym): words 8..10 = offset of the
+// symmetric nearfield band (see task_panel): words 8..10 = offset of the
 // transposed outputs (column c -> 8 + c), leading diagonal-block columns
 // without a transposed output, gather offset of the row leaf's own x
 constexpr int kKindNearSym = 4;
+constexpr int kKindCplSym = 5;  // symmetric coupling panel (same words as kKindNearSym)
 
 }  // namespace
 }  // namespace h2b
@@ -115,6 +116,9 @@ struct h2b_plan {
     int64_t* nsum;      // per leaf: the partials summed by its final task, in order
     int64_t ppart_len;
     int64_t near_bytes; // nearfield bytes one matvec streams
+    double* ssym;       // packed column panels of the upper coupling blocks (null when unused)
+    int32_t* gsym_c;    // their x_hat gather indices
+    int64_t cpl_bytes;  // coupling bytes one matvec streams
 };
 
 namespace h2b {
@@ -500,6 +504,9 @@ struct Shared {
     double* yn;                // vec_len: a leaf's summed nearfield rows (symmetric nearfield)
     const uint64_t* ppart;     // symmetric nearfield partials or null
     const int64_t* nsum;       // their per-leaf lists
+    double* yc;                // vec_len: a cluster's summed coupling partials (symmetric couplings)
+    bool cpl_sym;              // couplings as symmetric column panels
+    bool near_sym;             // nearfield as symmetric column panels
     uint32_t parity;           // mbarrier phase of the staging slot in use
     bool issued;               // band bulk copy already issued by the caller
 };
@@ -731,7 +738,7 @@ __device__ void task_forward(const double* __restrict__ c_V, const double* __res
 // `list` (LL offsets into s.ppart), i < size, always in list order.  H threads
 // per row take contiguous parts of the list (their sums are added in part
 // order); each thread keeps 8 loads in flight.  Ends with a block barrier.
-__device__ void near_sum(const Shared& s, const int64_t* list, int n, int size, uint32_t epoch) {
+__device__ void near_sum(const Shared& s, const int64_t* list, int n, int size, uint32_t epoch, double* out) {
     int H = 1;
     while (H < 4 && 2 * H * size <= kThreads) H *= 2;
     const int tid = threadIdx.x;
@@ -767,7 +774,7 @@ __device__ void near_sum(const Shared& s, const int64_t* list, int n, int size, 
             }
         }
         if (H == 1) {
-            if (i < size) s.yn[i] = acc;
+            if (i < size) out[i] = acc;
         } else if (h < H && i < size) {
             s.red[h * size + i] = acc;
         }
@@ -777,7 +784,7 @@ __device__ void near_sum(const Shared& s, const int64_t* list, int n, int size, 
         for (int i = tid; i < size; i += kThreads) {
             double t = 0.0;
             for (int h = 0; h < H; ++h) t += s.red[h * size + i];
-            s.yn[i] = t;
+            out[i] = t;
         }
         __syncthreads();
     }
@@ -793,8 +800,14 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
     const int start = (int)d[7];
     double* Es = reinterpret_cast<double*>(s.stage);
     // symmetric nearfield: this leaf's rows are the sum of its partials
-    const bool sym = leaf && s.ppart != nullptr;
-    if (sym) near_sum(s, s.nsum + d[11], (int)d[12], (int)d[8], epoch);
+    const bool sym = leaf && s.near_sym;
+    if (sym) near_sum(s, s.nsum + d[11], (int)d[12], (int)d[8], epoch, s.yn);
+    // symmetric couplings: y_cpl of this cluster = the sum of its partials
+    const bool csym = s.cpl_sym;
+    if (csym) {
+        has_cpl = d[14] > 0;
+        if (has_cpl) near_sum(s, s.nsum + d[13], (int)d[14], k, epoch, s.yc);
+    }
     if (d[10]) {  // (record word 18) ranks <= 32, leaf <= 64 rows: one warp, no block barriers
         if (threadIdx.x >= 32) return;
         const int lane = threadIdx.x;
@@ -811,7 +824,7 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
                 const int r = i / k, c = i - r * k;
                 cp_async8(Vt + c * size + r, r_V + v_off + i);
             }
-        double v = (has_cpl && lane < k) ? ll_load(ycpl + 2 * (yoff + lane), epoch) : 0.0;
+        double v = (has_cpl && lane < k) ? (csym ? s.yc[lane] : ll_load(ycpl + 2 * (yoff + lane), epoch)) : 0.0;
         if (par_off >= 0 && lane < kp) s.rhs[lane] = ll_load(yfin + 2 * (par_off + lane), epoch);
         cp_async_wait_all();
         __syncwarp();
@@ -855,7 +868,8 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
             cp_async8(Es + c * k + r, r_E + e_off + i);
         }
     const uint64_t* yc = ycpl + 2 * yoff;
-    for (int i = threadIdx.x; i < k; i += kThreads) s.va[i] = has_cpl ? ll_load(yc + 2 * i, epoch) : 0.0;
+    for (int i = threadIdx.x; i < k; i += kThreads)
+        s.va[i] = has_cpl ? (csym ? s.yc[i] : ll_load(yc + 2 * i, epoch)) : 0.0;
     __syncthreads();
     mark(s.mark, 0);
     if (par_off >= 0) {
@@ -1045,23 +1059,28 @@ __device__ __forceinline__ void gather2(double* d1, const int32_t* idx1, int n1,
 // ONCE for both triangles: the direct product D x|_cols -> t's partial at
 // out_off, and the transposed product D^T x|_t -> the columns' partials at
 // tr_off + c (skipped for the diagonal block's columns, which are stored in
-// full).  Never waits.
-__device__ void task_near_sym(const double* __restrict__ dsym, const int32_t* __restrict__ gsym,
-                              const double* __restrict__ x, uint64_t* ppart, uint32_t epoch, const Shared& s) {
+// full).  Never waits.  Coupling panels (kCpl, symmetric couplings) do the
+// same on S with x_hat in LL form (they wait on the forward tasks); they have
+// no diagonal block.
+template <bool kCpl>
+__device__ void task_panel(const double* __restrict__ base, const int32_t* __restrict__ gl,
+                           const double* __restrict__ x, const uint64_t* xhat, uint64_t* ppart, uint32_t epoch,
+                           const Shared& s) {
     const int64_t src_off = s.rec[0], gi_off = s.rec[3], out_off = s.rec[4];
     const int cols = (int)s.rec[1], rows = (int)s.rec[2];
     const int64_t tr_off = s.rec[8], rg_off = s.rec[10];
     const int skip = (int)s.rec[9];
     const int64_t bytes = ((int64_t)rows * cols * 8 + 15) & ~int64_t(15);  // panels are padded to 16 bytes
-    const double* M = s.issued ? (band_staged(bytes, dsym + src_off) ? reinterpret_cast<const double*>(s.stage)
-                                                                     : dsym + src_off)
-                               : stage_issue(s, dsym + src_off, bytes);
+    const double* M = s.issued ? (band_staged(bytes, base + src_off) ? reinterpret_cast<const double*>(s.stage)
+                                                                     : base + src_off)
+                               : stage_issue(s, base + src_off, bytes);
     mark(s.mark, 0);
     const bool tr = skip < cols;
-    if (s.xll)
-        gather2<true>(s.rhs, gsym + gi_off, cols, s.vb, gsym + rg_off, tr ? rows : 0, nullptr, s.xll, epoch);
+    if (kCpl || s.xll)
+        gather2<true>(s.rhs, gl + gi_off, cols, s.vb, gl + rg_off, tr ? rows : 0, nullptr, kCpl ? xhat : s.xll,
+                      epoch);
     else
-        gather2<false>(s.rhs, gsym + gi_off, cols, s.vb, gsym + rg_off, tr ? rows : 0, x, nullptr, epoch);
+        gather2<false>(s.rhs, gl + gi_off, cols, s.vb, gl + rg_off, tr ? rows : 0, x, nullptr, epoch);
     mark(s.mark, 1);
     mbar_wait(s.bar, s.parity);
     __syncthreads();
@@ -1088,6 +1107,8 @@ struct KArgs {
     const int32_t* gsym;
     uint64_t* ppart;
     const int64_t* nsum;
+    const double* ssym;      // symmetric couplings (null: not used)
+    const int32_t* gsym_c;
 };
 
 #ifndef H2B_MINB
@@ -1140,7 +1161,9 @@ __device__ __forceinline__ void run_task(const KArgs& a, const double* __restric
         load_rec(s, a.rec + a.band_base + (int64_t)kBandWords * b, kBandWords);
         const int kind = (int)s.rec[7];
         if (kind == kKindNearSym)
-            task_near_sym(a.dsym, a.gsym, x, a.ppart, epoch, s);
+            task_panel<false>(a.dsym, a.gsym, x, nullptr, a.ppart, epoch, s);
+        else if (kind == kKindCplSym)
+            task_panel<true>(a.ssym, a.gsym_c, x, a.xhat, a.ppart, epoch, s);
         else if (kind == kKindNear)
             task_band<false>(L, x, a.xhat, a.ynear, a.yfin, a.ycpl, a.ynear, y, epoch, s);
         else if (kind == kKindCpl)
@@ -1181,6 +1204,9 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
     s.vb = s.va + 2 * a.vec_len;
     s.red = s.vb + a.vec_len;
     s.yn = s.red + kWarps * 64;
+    s.yc = s.yn + a.vec_len;
+    s.near_sym = a.dsym != nullptr;
+    s.cpl_sym = a.ssym != nullptr;
     s.ppart = a.ppart;
     s.nsum = a.nsum;
     s.rec = s_rec;
@@ -1243,6 +1269,9 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec_loop(const KArgs 
         s.vb = s.va + 2 * a.vec_len;
         s.red = s.vb + a.vec_len;
         s.yn = s.red + kWarps * 64;
+        s.yc = s.yn + a.vec_len;
+        s.near_sym = a.dsym != nullptr;
+        s.cpl_sym = a.ssym != nullptr;
         s.ppart = a.ppart;
         s.nsum = a.nsum;
         s.rec = s_rec;
@@ -1464,11 +1493,149 @@ int build_sym_near(const h2b_layout& L, const std::vector<int32_t>& rstart, cons
     return 0;
 }
 
+
+// Symmetric couplings: S_(t,s) == S_(s,t)^T bit for bit (containers.py
+// assemble_couplings mirrors them).  Per row cluster t, the blocks (t, s) with
+// s > t are cut into column panels of all k_t rows; the transposed product of
+// a panel goes to s.  Partials follow the nearfield's in the same buffer.
+struct SymCpl {
+    bool on = false;
+    std::vector<std::vector<int64_t>> bands;
+    std::vector<int64_t> list_off, list_n;
+    std::vector<int64_t> nsum, pack, check;
+    std::vector<int32_t> srccol, gsym;
+    std::vector<std::vector<int>> producers;  // per cluster u: the t < u whose panels hold (t, u)
+    int64_t ssym_len = 0, ppart_len = 0, bytes = 0;
+};
+
+int build_sym_cpl(const h2b_layout& L, const std::vector<int32_t>& rstart, const std::vector<int32_t>& rsize,
+                  const std::vector<int32_t>& cstart, const std::vector<int32_t>& csize,
+                  const std::vector<int32_t>& rrank, const std::vector<int32_t>& crank,
+                  const std::vector<int32_t>& scols, const std::vector<int64_t>& soff,
+                  const std::vector<int64_t>& cxoff, int64_t ppart_base, int64_t nsum_base, SymCpl& S) {
+    S.on = false;
+    if (L.owned || L.r_nodes != L.c_nodes || !L.far_ptr || !L.far_col) return 0;
+    // opt-in (H2B_CPL_SYM=1): measured slower than the row bands at configs 1
+    // and 2 (62.9 vs 57.2 us, 884 vs 774 us): the separate downward-step tasks
+    // and their partial sums lengthen the downward chain more than the halved
+    // coupling bytes save
+    {
+        const char* e = getenv("H2B_CPL_SYM");
+        if (!e || e[0] != '1') return 0;
+    }
+    const int n = L.r_nodes;
+    for (int u = 0; u < n; ++u)
+        if (rstart[u] != cstart[u] || rsize[u] != csize[u] || rrank[u] != crank[u]) return 0;
+    std::vector<int32_t> fptr, fcol;
+    H2B_CUDA_TRY(fetch(L.far_ptr, (int64_t)n + 1, fptr));
+    H2B_CUDA_TRY(fetch(L.far_col, std::max<int64_t>(fptr[n], 1), fcol));
+    std::vector<std::vector<std::pair<int, int64_t>>> blocks(n);
+    for (int t = 0; t < n; ++t) {
+        int64_t c = 0;
+        for (int q = fptr[t]; q < fptr[t + 1]; ++q) {
+            const int s = fcol[q];
+            if (s < 0 || s >= n || s == t) return 0;
+            blocks[t].push_back({s, c});
+            c += crank[s];
+        }
+        if (c > (int64_t)scols[t] || scols[t] - c >= 4) return 0;  // (rows padded to 4 columns)
+    }
+    auto find = [&](int t, int s) -> int64_t {
+        for (const auto& b : blocks[t])
+            if (b.first == s) return b.second;
+        return -1;
+    };
+    std::vector<std::vector<std::pair<int, int64_t>>> up(n);
+    for (int t = 0; t < n; ++t)
+        for (const auto& b : blocks[t]) {
+            const int64_t m = find(b.first, t);
+            if (m < 0) return 0;
+            if (b.first > t && rrank[t] > 0 && crank[b.first] > 0) {
+                up[t].push_back(b);
+                S.check.insert(S.check.end(), {soff[t] + b.second, scols[t], soff[b.first] + m, scols[b.first],
+                                               rrank[t], rrank[b.first]});
+            }
+        }
+    S.bands.assign(n, {});
+    S.list_off.assign(n, 0);
+    S.list_n.assign(n, 0);
+    S.producers.assign(n, {});
+    std::vector<int64_t> width(n, 0), tbase(n, 0);
+    std::vector<std::vector<int64_t>> tcol(n), direct(n);
+    int64_t pdir = ppart_base, dlen = 0, g = 0;
+    for (int t = 0; t < n; ++t) {
+        const int rows = rrank[t];
+        if (up[t].empty()) continue;
+        int64_t W = 0;
+        for (const auto& b : up[t]) {
+            tcol[t].push_back(W);
+            W += crank[b.first];
+        }
+        width[t] = W;
+        int wmax = std::min(64, std::max(2, (int)(kStageBytes / 8 / rows)));
+        if ((rows & 1) && (wmax & 1)) --wmax;
+        const int64_t gbase = g, sbase = (int64_t)S.srccol.size();
+        for (int a = 0; a < rows; ++a) S.gsym.push_back((int32_t)(cxoff[t] + a));  // the cluster's own x_hat
+        for (const auto& b : up[t])
+            for (int j = 0; j < crank[b.first]; ++j) {
+                S.srccol.push_back((int32_t)(b.second + j));
+                S.gsym.push_back((int32_t)(cxoff[b.first] + j));
+            }
+        g += rows + W;
+        for (int64_t j0 = 0; j0 < W; j0 += wmax) {
+            const int w = (int)std::min<int64_t>(wmax, W - j0);
+            std::vector<int64_t> r(kBandWords, 0);
+            r[0] = dlen;
+            r[1] = w;
+            r[2] = rows;
+            r[3] = gbase + rows + j0;
+            r[4] = pdir;
+            r[7] = kKindCplSym;
+            r[8] = j0;  // + the transposed base, below
+            r[9] = 0;
+            r[10] = gbase;
+            S.bands[t].insert(S.bands[t].end(), r.begin(), r.end());
+            S.pack.insert(S.pack.end(), {soff[t], scols[t], rows, w, dlen, sbase + j0});
+            direct[t].push_back(pdir);
+            pdir += rows;
+            dlen += ((int64_t)rows * w + 1) & ~int64_t(1);
+            S.bytes += 8 * (int64_t)rows * w;
+        }
+    }
+    int64_t tpos = pdir;
+    for (int t = 0; t < n; ++t) {
+        tbase[t] = tpos;
+        tpos += width[t];
+        for (size_t i = 0; i < S.bands[t].size(); i += kBandWords) S.bands[t][i + 8] += tbase[t];
+    }
+    S.ppart_len = tpos - ppart_base;
+    S.ssym_len = dlen;
+    for (int u = 0; u < n; ++u) {
+        S.list_off[u] = nsum_base + (int64_t)S.nsum.size();
+        if (rrank[u] > 0) {
+            for (int64_t o : direct[u]) S.nsum.push_back(o);
+            for (const auto& b : blocks[u]) {
+                const int t = b.first;
+                if (t > u || rrank[t] == 0 || crank[u] == 0) continue;
+                int64_t off = -1;
+                for (size_t i = 0; i < up[t].size(); ++i)
+                    if (up[t][i].first == u) off = tbase[t] + tcol[t][i];
+                if (off < 0) return 0;
+                S.nsum.push_back(off);
+                S.producers[u].push_back(t);
+            }
+        }
+        S.list_n[u] = nsum_base + (int64_t)S.nsum.size() - S.list_off[u];
+    }
+    S.on = true;
+    return 0;
+}
 }  // namespace
 }  // namespace h2b
 
 namespace {
-int plan_create(const h2b_layout* layout, h2b_plan** out, bool allow_sym) {
+constexpr int kSymNear = 1, kSymCpl = 2;
+int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
     if (!layout || !out) return fail(H2B_ERR_INVALID, "h2b_plan_create: null pointer");
     const h2b_layout& L = *layout;
     if (L.c_nodes <= 0 || L.r_nodes <= 0 || L.c_leaves <= 0) return fail(H2B_ERR_INVALID, "h2b_plan_create: empty tree");
@@ -1518,10 +1685,16 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, bool allow_sym) {
         return fail(H2B_ERR_INVALID, "h2b_plan_create: cluster rank or leaf size above 512");
     const int vec_len = (std::max(maxk, maxleaf) + 1) & ~1;
     SymNear sym;
-    if (allow_sym)
+    if (sym_flags & kSymNear)
         if (int rc = build_sym_near(L, rstart, rsize, cstart, csize, rvoff, dcols, doff, dgoff, sym)) return rc;
+    SymCpl csym;
+    if (sym_flags & kSymCpl)
+        if (int rc = build_sym_cpl(L, rstart, rsize, cstart, csize, rrank, crank, scols, soff, cxoff, sym.ppart_len,
+                                   (int64_t)sym.nsum.size(), csym))
+            return rc;
     const int smem =
-        128 + kStageBytes + (int)sizeof(double) * (maxcols + 3 * vec_len + (sym.on ? vec_len + kWarps * 64 : kWarps * 32));
+        128 + kStageBytes +
+        (int)sizeof(double) * (maxcols + 3 * vec_len + (sym.on || csym.on ? 2 * vec_len + kWarps * 64 : kWarps * 32));
     if (smem > 227 * 1024) return fail(H2B_ERR_INVALID, "h2b_plan_create: gathered right-hand side exceeds shared memory");
 
     std::vector<int64_t> rec, fwd_off(L.c_leaves);
@@ -1625,11 +1798,23 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, bool allow_sym) {
                 dw[19] = sym.list_off[u];
                 dw[20] = sym.list_n[u];
             }
+            if (csym.on) {  // the cluster's coupling partials (symmetric couplings)
+                dw[21] = csym.list_off[u];
+                dw[22] = csym.list_n[u];
+            }
+            dw[23] = u;  // (plan building only)
             const int kk = rrank[u], kq = par >= 0 ? rrank[par] : 0;
             const bool lf = rvoff[u] >= 0;
             dw[18] = (kk <= 32 && kq <= 32 && (!lf || rsize[u] <= 64) &&
                       8 * ((((int64_t)kk * kq + 1) & ~int64_t(1)) + (lf ? (int64_t)rsize[u] * kk : 0)) <= kStageBytes)
                          ? 1 : 0;  // one-warp downward step
+        }
+        if (csym.on) {  // products are the panel tasks (all ticketed before any downward step)
+            std::vector<int64_t> t(dw, dw + kBandWords);
+            t[7] = kKindDescent;
+            late.insert(late.end(), t.begin(), t.end());
+            n_cpl += 1;
+            return;
         }
         std::vector<int64_t> tmp;
         int n = cpl ? bands_to(tmp, scols[u], rrank[u], soff[u], sgoff[u], ryoff[u], kKindCpl) : 0;
@@ -1715,6 +1900,30 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, bool allow_sym) {
         for (int u : inner_order)
             cluster_to(!depth_major && (early_inner || desc_tasks) ? inner_early : inner, inner, u);
         for (int u : owned_leaves) cluster_to(leaf_early, leaf_late, u);
+        if (csym.on) {
+            // symmetric coupling panels: leaf clusters' panels early (their
+            // x_hat are ready first); each inner cluster's downward step right
+            // after the panels it needs (its own and those of the t < u that
+            // hold (t, u)), parents first: every task waits on smaller tickets
+            std::vector<char> done(L.r_nodes, 0);
+            auto emit = [&](std::vector<int64_t>& dst, int t) {
+                if (done[t]) return;
+                done[t] = 1;
+                dst.insert(dst.end(), csym.bands[t].begin(), csym.bands[t].end());
+                n_cpl += (int)(csym.bands[t].size() / kBandWords);
+            };
+            for (int u : owned_leaves) emit(leaf_early, u);
+            std::vector<int64_t> seq;
+            for (size_t i = 0; i < inner.size(); i += kBandWords) {
+                // inner holds the downward steps of the inner clusters, parents first
+                const int u = (int)inner[i + 23];
+                for (int t : csym.producers[u]) emit(seq, t);
+                emit(seq, u);
+                seq.insert(seq.end(), inner.begin() + i, inner.begin() + i + kBandWords);
+            }
+            for (int u = 0; u < L.r_nodes; ++u) emit(inner_early, u);  // the rest (no downward step needs them)
+            inner.swap(seq);
+        }
     }
     if (!(getenv("H2B_DIAG_FWD_ONLY") && getenv("H2B_DIAG_FWD_ONLY")[0] == '1')) {  // diagnostics: forward alone
         rec.insert(rec.end(), na1.begin(), na1.end());
@@ -1826,52 +2035,82 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, bool allow_sym) {
     p->gsym = nullptr;
     p->ppart = nullptr;
     p->nsum = nullptr;
+    p->ssym = nullptr;
+    p->gsym_c = nullptr;
     p->near_bytes = 0;
+    p->cpl_bytes = 0;
     p->ppart_len = 0;
-    for (int u = 0; u < L.r_nodes; ++u)
+    for (int u = 0; u < L.r_nodes; ++u) {
         if (rvoff[u] >= 0) p->near_bytes += 8 * (int64_t)rsize[u] * dcols[u];
-    if (sym.on) {
-        // the nearfield must be symmetric bit for bit (checked on the device);
-        // then its upper blocks are packed into the panels the bands stream
-        int64_t* djobs = nullptr;
-        int* dbad = nullptr;
-        const int nchk = (int)(sym.check.size() / 6);
-        H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&djobs), 8 * std::max(sym.check.size(), sym.pack.size())));
-        H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&dbad), sizeof(int)));
-        H2B_CUDA_TRY(cudaMemset(dbad, 0, sizeof(int)));
-        H2B_CUDA_TRY(cudaMemcpy(djobs, sym.check.data(), 8 * sym.check.size(), cudaMemcpyHostToDevice));
-        if (nchk) k_sym_check<<<nchk, 256>>>(L.D, djobs, dbad);
-        H2B_CUDA_TRY(cudaGetLastError());
-        int bad = 0;
-        H2B_CUDA_TRY(cudaMemcpy(&bad, dbad, sizeof(int), cudaMemcpyDeviceToHost));
-        if (!bad) {
-            int32_t* dsrc = nullptr;
-            H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&dsrc), 4 * sym.srccol.size()));
-            H2B_CUDA_TRY(cudaMemcpy(dsrc, sym.srccol.data(), 4 * sym.srccol.size(), cudaMemcpyHostToDevice));
-            H2B_CUDA_TRY(cudaMemcpy(djobs, sym.pack.data(), 8 * sym.pack.size(), cudaMemcpyHostToDevice));
-            H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->dsym), 8 * (size_t)sym.dsym_len));
-            H2B_CUDA_TRY(cudaMemset(p->dsym, 0, 8 * (size_t)sym.dsym_len));
-            const int npk = (int)(sym.pack.size() / 6);
-            if (npk) k_sym_pack<<<npk, 256>>>(L.D, djobs, dsrc, p->dsym);
+        p->cpl_bytes += 8 * (int64_t)rrank[u] * scols[u];
+    }
+    if (sym.on || csym.on) {
+        // symmetric storage needs the operator's blocks symmetric bit for bit
+        // (checked on the device); then the upper blocks are packed into the
+        // column panels the tasks stream
+        auto check = [&](const double* base, const std::vector<int64_t>& jobs, int& bad) -> int {
+            int64_t* dj = nullptr;
+            int* db = nullptr;
+            H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&dj), 8 * std::max<size_t>(jobs.size(), 1)));
+            H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&db), sizeof(int)));
+            H2B_CUDA_TRY(cudaMemset(db, 0, sizeof(int)));
+            H2B_CUDA_TRY(cudaMemcpy(dj, jobs.data(), 8 * jobs.size(), cudaMemcpyHostToDevice));
+            if (!jobs.empty()) k_sym_check<<<(unsigned)(jobs.size() / 6), 256>>>(base, dj, db);
+            H2B_CUDA_TRY(cudaGetLastError());
+            H2B_CUDA_TRY(cudaMemcpy(&bad, db, sizeof(int), cudaMemcpyDeviceToHost));
+            cudaFree(dj);
+            cudaFree(db);
+            return 0;
+        };
+        auto pack = [&](const double* base, const std::vector<int64_t>& jobs, const std::vector<int32_t>& srccol,
+                        int64_t len, double** dst) -> int {
+            int64_t* dj = nullptr;
+            int32_t* ds = nullptr;
+            H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&dj), 8 * std::max<size_t>(jobs.size(), 1)));
+            H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&ds), 4 * std::max<size_t>(srccol.size(), 1)));
+            H2B_CUDA_TRY(cudaMemcpy(dj, jobs.data(), 8 * jobs.size(), cudaMemcpyHostToDevice));
+            H2B_CUDA_TRY(cudaMemcpy(ds, srccol.data(), 4 * srccol.size(), cudaMemcpyHostToDevice));
+            H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(dst), 8 * (size_t)std::max<int64_t>(len, 2)));
+            H2B_CUDA_TRY(cudaMemset(*dst, 0, 8 * (size_t)std::max<int64_t>(len, 2)));
+            if (!jobs.empty()) k_sym_pack<<<(unsigned)(jobs.size() / 6), 256>>>(base, dj, ds, *dst);
             H2B_CUDA_TRY(cudaGetLastError());
             H2B_CUDA_TRY(cudaDeviceSynchronize());
-            cudaFree(dsrc);
-            H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->gsym), 4 * sym.gsym.size()));
-            H2B_CUDA_TRY(cudaMemcpy(p->gsym, sym.gsym.data(), 4 * sym.gsym.size(), cudaMemcpyHostToDevice));
-            H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->ppart), 16 * (size_t)sym.ppart_len));
-            H2B_CUDA_TRY(cudaMemset(p->ppart, 0, 16 * (size_t)sym.ppart_len));
-            p->ppart_len = sym.ppart_len;
-            H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->nsum), 8 * std::max<size_t>(sym.nsum.size(), 1)));
-            H2B_CUDA_TRY(cudaMemcpy(p->nsum, sym.nsum.data(), 8 * sym.nsum.size(), cudaMemcpyHostToDevice));
+            cudaFree(dj);
+            cudaFree(ds);
+            return 0;
+        };
+        auto upload = [&](const auto& v, auto** dst) -> int {
+            using T = typename std::decay_t<decltype(v)>::value_type;
+            H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(dst), sizeof(T) * std::max<size_t>(v.size(), 1)));
+            if (!v.empty()) H2B_CUDA_TRY(cudaMemcpy(*dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+            return 0;
+        };
+        int bad_near = 0, bad_cpl = 0;
+        if (sym.on)
+            if (int rc = check(L.D, sym.check, bad_near)) return rc;
+        if (csym.on)
+            if (int rc = check(L.S, csym.check, bad_cpl)) return rc;
+        if (bad_near || bad_cpl) {
+            // not symmetric: stream every block of that part
+            h2b_plan_destroy(p);
+            return plan_create(layout, out, sym_flags & ~(bad_near ? kSymNear : 0) & ~(bad_cpl ? kSymCpl : 0));
+        }
+        if (sym.on) {
+            if (int rc = pack(L.D, sym.pack, sym.srccol, sym.dsym_len, &p->dsym)) return rc;
+            if (int rc = upload(sym.gsym, &p->gsym)) return rc;
             p->near_bytes = sym.near_bytes;
         }
-        cudaFree(djobs);
-        cudaFree(dbad);
-        if (bad) {
-            // not symmetric: the plan streams every block
-            h2b_plan_destroy(p);
-            return plan_create(layout, out, false);
+        if (csym.on) {
+            if (int rc = pack(L.S, csym.pack, csym.srccol, csym.ssym_len, &p->ssym)) return rc;
+            if (int rc = upload(csym.gsym, &p->gsym_c)) return rc;
+            p->cpl_bytes = csym.bytes;
         }
+        p->ppart_len = sym.ppart_len + csym.ppart_len;
+        H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->ppart), 16 * (size_t)std::max<int64_t>(p->ppart_len, 1)));
+        H2B_CUDA_TRY(cudaMemset(p->ppart, 0, 16 * (size_t)std::max<int64_t>(p->ppart_len, 1)));
+        std::vector<int64_t> lists(sym.nsum);
+        lists.insert(lists.end(), csym.nsum.begin(), csym.nsum.end());
+        if (int rc = upload(lists, &p->nsum)) return rc;
     }
     *out = p;
     return ok();
@@ -1879,7 +2118,7 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, bool allow_sym) {
 }  // namespace
 
 extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
-    return plan_create(layout, out, true);
+    return plan_create(layout, out, kSymNear | kSymCpl);
 }
 
 #ifdef H2B_LL_TIMEOUT
@@ -1905,7 +2144,7 @@ extern "C" int h2b_debug_stuck(h2b_plan* p, unsigned long long* out) {
 extern "C" int h2b_plan_destroy(h2b_plan* p) {
     if (!p) return ok();
     void* bufs[] = {p->xhat, p->ycpl, p->yfin, p->ynear, p->ctrl, p->rec,  p->fwd_off, p->dx,
-                    p->dy,   p->trace, p->xll, p->dsym,  p->gsym, p->ppart, p->nsum};
+                    p->dy,   p->trace, p->xll, p->dsym,  p->gsym, p->ppart, p->nsum, p->ssym, p->gsym_c};
     for (void* q : bufs)
         if (q) cudaFree(q);
     if (p->hy) cudaFreeHost(p->hy);
@@ -1941,6 +2180,8 @@ int launch_matvec(h2b_plan* p, const double* d_x, const double* xh, double* y, c
     a.gsym = p->gsym;
     a.ppart = p->ppart;
     a.nsum = p->nsum;
+    a.ssym = p->ssym;
+    a.gsym_c = p->gsym_c;
     const int grid = a.n_copy + p->L.c_leaves + p->n_near + p->n_cpl;
     if (p->loop_grid > 0)
         k_matvec_loop<<<std::min(grid, p->loop_grid), kThreads, p->smem, st>>>(a, d_x, y);
@@ -2008,7 +2249,8 @@ extern "C" int h2b_plan_trace(h2b_plan* p, unsigned long long* h_out, int64_t ca
 
 // Plan facts: [0] symmetric nearfield in use (0/1), [1] nearfield bytes one
 // matvec streams, [2] nearfield tasks, [3] coupling tasks, [4] bytes of the
-// symmetric nearfield's partial vectors (LL form).
+// symmetric partial vectors (LL form), [5] symmetric couplings in use (0/1),
+// [6] coupling bytes one matvec streams.
 extern "C" int h2b_plan_info(h2b_plan* p, int64_t* h_out) {
     if (!p || !h_out) return fail(H2B_ERR_INVALID, "h2b_plan_info: null pointer");
     h_out[0] = p->dsym != nullptr;
@@ -2016,6 +2258,8 @@ extern "C" int h2b_plan_info(h2b_plan* p, int64_t* h_out) {
     h_out[2] = p->n_near;
     h_out[3] = p->n_cpl;
     h_out[4] = p->ppart_len * 16;
+    h_out[5] = p->ssym != nullptr;
+    h_out[6] = p->cpl_bytes;
     return ok();
 }
 
