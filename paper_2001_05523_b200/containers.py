@@ -636,6 +636,7 @@ class MatvecPlan:
         _lib.check(_lib.lib().h2b_plan_create(ctypes.byref(lay), ctypes.byref(h)))
         self.handle = h
         self._torch = t
+        self._host_fn = _lib.lib().h2b_matvec_host
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -655,6 +656,16 @@ class MatvecPlan:
 
     def apply(self, x):
         t = self._torch
+        if type(x) is np.ndarray and x.dtype == np.float64 and x.ndim == 1 and x.flags.c_contiguous:
+            # fast path of the common host call (numpy in, numpy out)
+            if len(x) != self.n_cols:
+                raise ValueError(f"expected a vector of length {self.n_cols}")
+            y = t.empty(self.n_rows, dtype=t.float64, pin_memory=True).numpy()
+            rc = self._host_fn(self.handle, x.__array_interface__["data"][0], y.__array_interface__["data"][0],
+                               t.cuda.current_stream().cuda_stream)
+            if rc:
+                _lib.check(rc)
+            return y
         if isinstance(x, t.Tensor):
             if x.dtype != t.float64 or not x.is_cuda:
                 raise ValueError("expected a CUDA float64 tensor")

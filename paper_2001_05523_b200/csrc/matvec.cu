@@ -115,6 +115,7 @@ struct h2b_plan {
     uint64_t* ppart;    // LL partial vectors (direct per panel, transposed per block)
     int64_t* nsum;      // per leaf: the partials summed by its final task, in order
     int64_t ppart_len;
+    int n_leaf;         // leaf downward-step tasks per launch
     int64_t near_bytes; // nearfield bytes one matvec streams
     double* ssym;       // packed column panels of the upper coupling blocks (null when unused)
     int32_t* gsym_c;    // their x_hat gather indices
@@ -1101,6 +1102,10 @@ struct KArgs {
     unsigned long long* ctrl;
     unsigned long long* trace;
     const double* xh;  // host-mapped x (h2b_matvec_host) or null
+    double* yh;        // host-mapped y (h2b_matvec_host) or null: y is then a device copy
+    int n_out;         // copy-out tasks (host output): the last tickets
+    int n_leaf;        // leaf downward steps per launch
+    unsigned long long* ydone;  // leaf downward steps finished (host-output launches, monotonic)
     uint64_t* xll;     // LL copy of x for host-input launches
     int n_copy;        // copy tasks (host input)
     const double* dsym;      // symmetric nearfield (null: not used)
@@ -1140,6 +1145,37 @@ __device__ __forceinline__ void run_task(const KArgs& a, const double* __restric
         }
         return;
     }
+    if (ticket >= L.c_leaves + a.n_near + a.n_cpl) {
+        // host-output launch: once every leaf has written its rows of y (in
+        // HBM, natural order), copy a chunk to the mapped host buffer with
+        // coalesced stores (scattered 8-byte stores over the host link cost
+        // one transaction each)
+        if (threadIdx.x == 0) {
+            const unsigned long long target = (unsigned long long)((epoch - 2) / 2 + 1) * (unsigned long long)a.n_leaf;
+            unsigned long long v;
+            while (true) {
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.ydone) : "memory");
+                if (v >= target) break;
+                __nanosleep(64);
+            }
+        }
+        __syncthreads();
+        const int64_t c = ticket - (L.c_leaves + a.n_near + a.n_cpl), n = L.n_rows;
+        const int64_t i0 = c * kCopyChunk, i1 = min(n, i0 + kCopyChunk);
+        constexpr int kU = kCopyChunk / kThreads;
+        double v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int64_t i = i0 + u * kThreads + threadIdx.x;
+            v[u] = i < i1 ? __ldcg(y + i) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int64_t i = i0 + u * kThreads + threadIdx.x;
+            if (i < i1) a.yh[i] = v[u];
+        }
+        return;
+    }
     unsigned long long t_begin = 0;
     if (a.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
     s.mark = a.trace ? a.trace + 8 * ticket + 3 : nullptr;
@@ -1172,6 +1208,13 @@ __device__ __forceinline__ void run_task(const KArgs& a, const double* __restric
             descent(L.r_E, L.r_V, L.row_perm, s.rec + 8, a.ycpl, a.yfin, a.ynear, y, epoch, s.rec[6] != 0, s);
     }
     __syncthreads();
+    if (a.yh && threadIdx.x == 0 && ticket >= tB) {
+        const int kind = (int)s.rec[7];
+        if (((kind == kKindCpl && s.rec[5]) || kind == kKindDescent) && s.rec[13]) {  // a leaf's rows of y are out
+            __threadfence();
+            atomicAdd(a.ydone, 1ull);
+        }
+    }
     if (threadIdx.x == 0) {
         if (a.trace) {
             unsigned long long t_end;
@@ -1244,7 +1287,7 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec_loop(const KArgs 
     __shared__ int64_t s_rec[kFwdHead + kFwdLevel * kMaxDepth];
     const h2b_layout& L = a.L;
     const int host = a.xh != nullptr;
-    const int n_total = a.n_copy + L.c_leaves + a.n_near + a.n_cpl;
+    const int n_total = a.n_copy + L.c_leaves + a.n_near + a.n_cpl + a.n_out;
     const unsigned long long per_launch = (unsigned long long)n_total + gridDim.x;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smraw);
     for (int it = 0;; ++it) {
@@ -1964,6 +2007,11 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
     p->L = L;
     p->n_near = n_near;
     p->n_cpl = n_cpl;
+    p->n_leaf = 0;
+    for (int64_t b = 0; b < (int64_t)(n_near + n_cpl); ++b) {
+        const int64_t* r = rec.data() + band_base + kBandWords * b;
+        if (((r[7] == kKindCpl && r[5]) || r[7] == kKindDescent) && r[13]) ++p->n_leaf;
+    }
     p->band_base = band_base;
     {
         int64_t m = 0;
@@ -1985,8 +2033,8 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
     H2B_CUDA_TRY(cudaMemset(p->xhat, 0, 16 * (size_t)L.xhat_len));
     H2B_CUDA_TRY(cudaMemset(p->ycpl, 0, 16 * (size_t)L.yhat_len));
     H2B_CUDA_TRY(cudaMemset(p->ynear, 0, 16 * (size_t)L.n_rows));
-    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->ctrl), 2 * sizeof(unsigned long long)));
-    H2B_CUDA_TRY(cudaMemset(p->ctrl, 0, 2 * sizeof(unsigned long long)));
+    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->ctrl), 3 * sizeof(unsigned long long)));
+    H2B_CUDA_TRY(cudaMemset(p->ctrl, 0, 3 * sizeof(unsigned long long)));
     H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->rec), sizeof(int64_t) * std::max<size_t>(1, rec.size())));
     H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->fwd_off), sizeof(int64_t) * fwd_off.size()));
     if (!rec.empty())
@@ -2154,7 +2202,8 @@ extern "C" int h2b_plan_destroy(h2b_plan* p) {
 }
 
 namespace {
-int launch_matvec(h2b_plan* p, const double* d_x, const double* xh, double* y, cudaStream_t st) {
+int launch_matvec(h2b_plan* p, const double* d_x, const double* xh, double* y, cudaStream_t st,
+                  double* yh = nullptr) {
     KArgs a;
     a.L = p->L;
     a.rec = p->rec;
@@ -2182,7 +2231,11 @@ int launch_matvec(h2b_plan* p, const double* d_x, const double* xh, double* y, c
     a.nsum = p->nsum;
     a.ssym = p->ssym;
     a.gsym_c = p->gsym_c;
-    const int grid = a.n_copy + p->L.c_leaves + p->n_near + p->n_cpl;
+    a.yh = yh;
+    a.n_out = yh ? (int)((p->L.n_rows + kCopyChunk - 1) / kCopyChunk) : 0;
+    a.n_leaf = p->n_leaf;
+    a.ydone = p->ctrl + 2;
+    const int grid = a.n_copy + p->L.c_leaves + p->n_near + p->n_cpl + a.n_out;
     if (p->loop_grid > 0)
         k_matvec_loop<<<std::min(grid, p->loop_grid), kThreads, p->smem, st>>>(a, d_x, y);
     else
@@ -2223,7 +2276,7 @@ extern "C" int h2b_matvec_host(h2b_plan* p, const double* h_x, double* h_y, void
     const bool staged_y = yh == nullptr;
     if (staged_y) yh = static_cast<double*>(const_cast<void*>(mapped(p->hy)));
     if (!xh || !yh) return fail(H2B_ERR_CUDA, "h2b_matvec_host: pinned staging is not device-mapped");
-    if (int rc = launch_matvec(p, nullptr, xh, yh, st)) return rc;
+    if (int rc = launch_matvec(p, nullptr, xh, p->dy, st, yh)) return rc;
     H2B_CUDA_TRY(cudaStreamSynchronize(st));
     if (staged_y) std::memcpy(h_y, p->hy, sizeof(double) * p->L.n_rows);
     return ok();

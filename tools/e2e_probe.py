@@ -1,40 +1,57 @@
-"""Breakdown of the end-to-end matvec call (host numpy in/out) on config 1."""
+"""Where the end-to-end (numpy in / numpy out) matvec time goes at config 1."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
 import numpy as np
 import torch
 import bench
+from paper_2001_05523_b200 import _lib
 from paper_2001_05523_b200.containers import H2Matrix, assemble_couplings, near_layout
 
 cfg = bench.CONFIGS["1"]
 mesh, ctx, tree, bt, basis = bench.build_problem(cfg, os.cpu_count() or 8)
 lay = near_layout(bt)
 Dn = torch.zeros(max(lay.total, 1), dtype=torch.float64, device="cuda")
-S = assemble_couplings(ctx, "slp", bt, basis, basis, cfg["q_reg"])
+S = assemble_couplings(ctx, "slp", bt, basis, basis, 3)
 H = H2Matrix.from_device(bt, basis, basis, S, Dn)
+n = H.shape[1]
 plan = H.plan()
-n = H.shape[0]
-xh = torch.from_numpy(np.random.default_rng(1).standard_normal(n)).pin_memory().numpy()
+xh = torch.randn(n, dtype=torch.float64).pin_memory().numpy()
+yh = torch.empty(n, dtype=torch.float64).pin_memory().numpy()
 xd = torch.from_numpy(xh).cuda()
-yd = torch.empty(n, dtype=torch.float64, device="cuda")
-yp = torch.empty(n, dtype=torch.float64).pin_memory()
+L = _lib.lib()
 
 
-def wall(f, k=200):
-    for _ in range(5):
-        f()
+def wall(fn, reps=300):
+    for _ in range(10):
+        fn()
     torch.cuda.synchronize()
-    t = time.perf_counter()
-    for _ in range(k):
-        f()
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+    ts = np.sort(ts)
+    return f"median {np.median(ts)*1e6:.1f} us, p10 {ts[len(ts)//10]*1e6:.1f} us"
+
+
+def dev():
+    plan.apply_device(xd)
     torch.cuda.synchronize()
-    return (time.perf_counter() - t) / k * 1e6
 
 
-print(f"H.matvec(numpy)           {wall(lambda: H.matvec(xh)):7.1f} us")
-print(f"plan.apply(numpy)         {wall(lambda: plan.apply(xh)):7.1f} us")
-print(f"kernel (apply_device)+sync {wall(lambda: (plan.apply_device(xd, yd), torch.cuda.synchronize())):7.1f} us")
-print(f"H2D pinned 262KB + sync    {wall(lambda: (xd.copy_(torch.from_numpy(xh), non_blocking=True), torch.cuda.synchronize())):7.1f} us")
-print(f"D2H pinned + sync          {wall(lambda: (yp.copy_(yd, non_blocking=True), torch.cuda.synchronize())):7.1f} us")
-print(f"np.empty + D2H pageable    {wall(lambda: torch.from_numpy(np.empty(n)).copy_(yd)):7.1f} us")
+print("H.matvec(numpy)            ", wall(lambda: H.matvec(xh)))
+print("raw h2b_matvec_host         ", wall(lambda: L.h2b_matvec_host(plan.handle, _lib.ptr(xh), _lib.ptr(yh), None)))
+print("device in/out + sync        ", wall(dev))
+print("pinned alloc                ", wall(lambda: torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()))
+print("pageable x (staged)         ", wall(lambda: L.h2b_matvec_host(plan.handle, _lib.ptr(np.array(xh)), _lib.ptr(yh), None)))
+
+
+def copies():
+    xd.copy_(torch.from_numpy(xh), non_blocking=True)
+    y = plan.apply_device(xd)
+    torch.from_numpy(yh).copy_(y, non_blocking=True)
+    torch.cuda.synchronize()
+
+
+print("H2D + device + D2H (torch)  ", wall(copies))
