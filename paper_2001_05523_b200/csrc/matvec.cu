@@ -82,6 +82,9 @@ constexpr int kKindNear = 0, kKindCpl = 1, kKindDescent = 3;  // band record kin
 // without a transposed output, gather offset of the row leaf's own x
 constexpr int kKindNearSym = 4;
 constexpr int kKindCplSym = 5;  // symmetric coupling panel (same words as kKindNearSym)
+// a leaf's nearfield rows summed from its partials into y_near (symmetric
+// nearfield): words 0 list offset, 1 list length, 2 rows, 3 first row
+constexpr int kKindNearSum = 6;
 
 }  // namespace
 }  // namespace h2b
@@ -801,7 +804,7 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
     const int start = (int)d[7];
     double* Es = reinterpret_cast<double*>(s.stage);
     // symmetric nearfield: this leaf's rows are the sum of its partials
-    const bool sym = leaf && s.near_sym;
+    const bool sym = leaf && s.near_sym && d[12] > 0;  // (else a near-sum task filled y_near)
     if (sym) near_sum(s, s.nsum + d[11], (int)d[12], (int)d[8], epoch, s.yn);
     // symmetric couplings: y_cpl of this cluster = the sum of its partials
     const bool csym = s.cpl_sym;
@@ -1196,9 +1199,14 @@ __device__ __forceinline__ void run_task(const KArgs& a, const double* __restric
         if (b < np) prefetch_slice(L.r_E, a.e_bytes_r, b, np);
         load_rec(s, a.rec + a.band_base + (int64_t)kBandWords * b, kBandWords);
         const int kind = (int)s.rec[7];
-        if (kind == kKindNearSym)
+        if (kind == kKindNearSym) {
             task_panel<false>(a.dsym, a.gsym, x, nullptr, a.ppart, epoch, s);
-        else if (kind == kKindCplSym)
+        } else if (kind == kKindNearSum) {
+            const int rows = (int)s.rec[2];
+            near_sum(s, a.nsum + s.rec[0], (int)s.rec[1], rows, epoch, s.yn);
+            uint64_t* dst = a.ynear + 2 * s.rec[3];
+            for (int i = threadIdx.x; i < rows; i += kThreads) ll_store(dst + 2 * i, s.yn[i], epoch);
+        } else if (kind == kKindCplSym)
             task_panel<true>(a.ssym, a.gsym_c, x, a.xhat, a.ppart, epoch, s);
         else if (kind == kKindNear)
             task_band<false>(L, x, a.xhat, a.ynear, a.yfin, a.ycpl, a.ynear, y, epoch, s);
@@ -1398,6 +1406,7 @@ struct SymNear {
     std::vector<int64_t> list_off, list_n;    // per row node: its partial list
     std::vector<int64_t> nsum, pack, check;
     std::vector<int32_t> srccol, gsym;
+    std::vector<std::vector<int>> producers;  // per leaf u: the leaves t whose panels hold (t, u)
     int64_t dsym_len = 0, ppart_len = 0, near_bytes = 0;
 };
 
@@ -1461,6 +1470,7 @@ int build_sym_near(const h2b_layout& L, const std::vector<int32_t>& rstart, cons
     S.bands.assign(n, {});
     S.list_off.assign(n, 0);
     S.list_n.assign(n, 0);
+    S.producers.assign(n, {});
     std::vector<int64_t> tbase(n, 0);
     std::vector<std::vector<int64_t>> tcol(n);  // per t: column offset of each upper block in its panels
     std::vector<std::vector<int64_t>> direct(n);
@@ -1529,6 +1539,7 @@ int build_sym_near(const h2b_layout& L, const std::vector<int32_t>& rstart, cons
                 if (up[t][i].first == u) off = tbase[t] + tcol[t][i];
             if (off < 0) return 0;
             S.nsum.push_back(off);
+            S.producers[u].push_back(t);
         }
         S.list_n[u] = (int64_t)S.nsum.size() - S.list_off[u];
     }
@@ -1727,6 +1738,11 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
     if (maxk > kMaxVec || maxleaf > kMaxVec)
         return fail(H2B_ERR_INVALID, "h2b_plan_create: cluster rank or leaf size above 512");
     const int vec_len = (std::max(maxk, maxleaf) + 1) & ~1;
+    // symmetric nearfield: leaf partial sums in the leaf's final task, or as
+    // separate tasks in the nearfield stream (H2B_NEAR_SUM_TASKS=1; measured
+    // slower: config 1 67.0 vs 59.4 us, sphere L8 920 vs 827 us, sphere L9
+    // m=5 4.47 vs 4.12 ms -- the extra tasks cost more than the shorter tail)
+    const bool near_sum_tasks = getenv("H2B_NEAR_SUM_TASKS") && getenv("H2B_NEAR_SUM_TASKS")[0] == '1';
     SymNear sym;
     if (sym_flags & kSymNear)
         if (int rc = build_sym_near(L, rstart, rsize, cstart, csize, rvoff, dcols, doff, dgoff, sym)) return rc;
@@ -1837,7 +1853,7 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
             int dd = 0;
             for (int q = rparent[u]; q >= 0; q = rparent[q]) ++dd;
             dw[17] = dd;  // depth (diagnostics: trace)
-            if (sym.on && rvoff[u] >= 0) {  // the leaf's nearfield partials (symmetric nearfield)
+            if (sym.on && !near_sum_tasks && rvoff[u] >= 0) {  // the leaf's nearfield partials (symmetric nearfield)
                 dw[19] = sym.list_off[u];
                 dw[20] = sym.list_n[u];
             }
@@ -1913,12 +1929,36 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
     const int c1 = std::min(nl, (int)(fa1 * nl)), c2 = std::min(nl, c1 + (int)(fa2 * nl));
     std::vector<int64_t> na1, na2, nb, leaf_early, leaf_late, inner, inner_early;
     int n_near = 0;
+    // symmetric nearfield: each leaf's partials are summed by a near-sum task
+    // placed `lag` leaves after the last of its producers (so they are done)
+    std::vector<std::vector<int64_t>> sums_after(nl);
+    if (sym.on && near_sum_tasks) {
+        int lag = 16;
+        if (const char* e = getenv("H2B_NEAR_SUM_LAG")) lag = atoi(e);
+        std::vector<int> pos(L.r_nodes, 0);
+        for (int i = 0; i < nl; ++i) pos[owned_leaves[i]] = i;
+        for (int i = 0; i < nl; ++i) {
+            const int u = owned_leaves[i];
+            int last = i;
+            for (int t : sym.producers[u]) last = std::max(last, pos[t]);
+            std::vector<int64_t> r(kBandWords, 0);
+            r[0] = sym.list_off[u];
+            r[1] = sym.list_n[u];
+            r[2] = rsize[u];
+            r[3] = rstart[u];
+            r[7] = kKindNearSum;
+            auto& dst = sums_after[std::min(nl - 1, last + lag)];
+            dst.insert(dst.end(), r.begin(), r.end());
+        }
+    }
     for (int i = 0; i < nl; ++i) {
         const int u = owned_leaves[i];
         std::vector<int64_t>& dst = i < c1 ? na1 : i < c2 ? na2 : nb;
         if (sym.on) {
             dst.insert(dst.end(), sym.bands[u].begin(), sym.bands[u].end());
             n_near += (int)(sym.bands[u].size() / kBandWords);
+            dst.insert(dst.end(), sums_after[i].begin(), sums_after[i].end());
+            n_near += (int)(sums_after[i].size() / kBandWords);
         } else {
             n_near += bands_to(dst, dcols[u], rsize[u], doff[u], dgoff[u], rstart[u], kKindNear);
         }

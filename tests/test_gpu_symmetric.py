@@ -124,3 +124,18 @@ def test_nonsymmetric_couplings_stream_every_block():
     x = np.random.default_rng(2).standard_normal(H.shape[1])
     assert rel(H2.matvec(x), ref.apply(x)) < 1e-14
     assert rel(H2.matvec(x), H.matvec(x)) > 1e-12
+
+
+def test_near_sum_tasks_variant_matches():
+    """Opt-in H2B_NEAR_SUM_TASKS=1: the leaf partial sums run as separate
+    tasks in the nearfield stream (same sums, same order)."""
+    from paper_2001_05523_b200.containers import MatvecPlan
+
+    H = _slp(4, 32)
+    os.environ["H2B_NEAR_SUM_TASKS"] = "1"
+    try:
+        p = MatvecPlan(H.block_tree, H.row_basis, H.col_basis, H.S_dev, H.D_dev, H.far_layout, H.near_layout)
+    finally:
+        del os.environ["H2B_NEAR_SUM_TASKS"]
+    x = np.random.default_rng(3).standard_normal(H.shape[1])
+    assert np.array_equal(p.apply(x), H.matvec(x))
