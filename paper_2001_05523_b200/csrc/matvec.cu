@@ -974,10 +974,14 @@ __device__ void panel_dot(const double* M, int rows, int cols, const double* xc,
     const bool ok0 = lane < cols, ok1 = lane + 32 < cols;
     const double x0 = ok0 ? xc[lane] : 0.0, x1 = ok1 ? xc[lane + 32] : 0.0;
     double t0 = 0.0, t1 = 0.0;
-    constexpr int R = 8;
+#ifndef H2B_PANEL_R
+#define H2B_PANEL_R 8
+#endif
+    constexpr int R = H2B_PANEL_R;
+    constexpr int lg = log2c(R);
     int ri = 0;
 #pragma unroll
-    for (int j = 0; j < 3; ++j) ri |= ((lane >> (4 - j)) & 1) << (2 - j);
+    for (int j = 0; j < lg; ++j) ri |= ((lane >> (4 - j)) & 1) << (lg - 1 - j);
     for (int rb = R * warp; rb < rows; rb += R * kWarps) {
         double a[R];
 #pragma unroll
@@ -994,7 +998,7 @@ __device__ void panel_dot(const double* M, int rows, int cols, const double* xc,
             t1 = fma(m1, xv, t1);
         }
         const double sum = warp_sum<R>(a, lane);
-        if ((lane & 3) == 0 && rb + ri < rows) ll_store(yd + 2 * (rb + ri), sum, epoch);
+        if ((lane & ((32 / R) - 1)) == 0 && rb + ri < rows) ll_store(yd + 2 * (rb + ri), sum, epoch);
     }
     if (!transposed) return;
     red[warp * 64 + lane] = t0;
