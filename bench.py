@@ -365,7 +365,7 @@ def run_ours(args, cfg):
 
     # ---- roofline ---------------------------------------------------------------
     pk = peaks()
-    mv_bytes = H.matvec_bytes()
+    mv_bytes = H.matvec_bytes(stored_once=ws == 1)  # sharded plans stream every block
     fp64_peak, fp64_src = measure_fp64_peak() if rank == 0 else (None, None)
     nf_time = t_sing + t_reg
     result = {

@@ -504,15 +504,16 @@ class H2Matrix:
         return {"basis": 8 * basis, "coupling": 8 * self.far_layout.entries, "lowrank": 0,
                 "nearfield": 8 * self.near_layout.entries}
 
-    def matvec_bytes(self):
+    def matvec_bytes(self, stored_once=True):
         """Algorithmic HBM bytes of one matvec: every operator
         entry once, each basis in both roles, plus x and y.  A symmetric
         nearfield (or coupling set) is stored and streamed once per block pair
-        (MatvecPlan.info): its bytes are the upper blocks only."""
+        (MatvecPlan.info): its bytes are the upper blocks only.  Row-sharded
+        plans stream every block (stored_once=False)."""
         basis_r = self.row_basis.storage_floats()
         basis_c = self.col_basis.storage_floats()
         near, cpl = 8 * self.near_layout.entries, 8 * self.far_layout.entries
-        info = self.plan().info()
+        info = self.plan().info() if stored_once else {"near_symmetric": False, "coupling_symmetric": False}
         if info["near_symmetric"]:
             near = info["near_bytes"]
         if info["coupling_symmetric"]:
