@@ -62,8 +62,9 @@ def test_level8_touching_pairs_vs_reference(world8, kind):
 def test_level8_operator_properties(world8):
     """Size-independent checks of the level-8 single-layer H^2 operator
     (device GCA basis, device assembly): symmetry x.Ay = y.Ax of the
-    symmetric Galerkin matrix, linearity, bitwise repeatability, and the
-    block product against the matvec."""
+    symmetric Galerkin matrix, linearity, bitwise repeatability, the block
+    product against the matvec, and the symmetric-nearfield plan against the
+    one-sided one."""
     import torch
 
     from paper_2001_05523_b200 import gca
@@ -85,3 +86,16 @@ def test_level8_operator_properties(world8):
     for j in range(3):
         yj = H.matvec(X[:, j].contiguous())
         assert float((Y[:, j] - yj).abs().max()) <= 1e-13 * float(yj.abs().max())
+    # the symmetric nearfield (streamed once per block pair) against the
+    # one-sided plan at full size
+    import os
+
+    from paper_2001_05523_b200.containers import MatvecPlan
+
+    assert H.plan().info()["near_symmetric"]
+    os.environ["H2B_NEAR_SYM"] = "0"
+    try:
+        one = MatvecPlan(H.block_tree, H.row_basis, H.col_basis, H.S_dev, H.D_dev, H.far_layout, H.near_layout)
+    finally:
+        del os.environ["H2B_NEAR_SYM"]
+    assert float((one.apply(x) - ax).norm()) <= 1e-14 * float(ax.norm())
