@@ -504,21 +504,22 @@ class H2Matrix:
         return {"basis": 8 * basis, "coupling": 8 * self.far_layout.entries, "lowrank": 0,
                 "nearfield": 8 * self.near_layout.entries}
 
-    def matvec_bytes(self, stored_once=True):
+    def matvec_bytes(self):
         """Algorithmic HBM bytes of one matvec: every operator
-        entry once, each basis in both roles, plus x and y.  A symmetric
-        nearfield (or coupling set) is stored and streamed once per block pair
-        (MatvecPlan.info): its bytes are the upper blocks only.  Row-sharded
-        plans stream every block (stored_once=False)."""
+        entry once, each basis in both roles, plus x and y."""
         basis_r = self.row_basis.storage_floats()
         basis_c = self.col_basis.storage_floats()
-        near, cpl = 8 * self.near_layout.entries, 8 * self.far_layout.entries
-        info = self.plan().info() if stored_once else {"near_symmetric": False, "coupling_symmetric": False}
-        if info["near_symmetric"]:
-            near = info["near_bytes"]
-        if info["coupling_symmetric"]:
-            cpl = info["coupling_bytes"]
-        return near + cpl + 8 * (basis_r + basis_c + self.shape[0] + self.shape[1])
+        return 8 * (self.near_layout.entries + self.far_layout.entries + basis_r + basis_c + self.shape[0]
+                    + self.shape[1])
+
+    def streamed_bytes(self):
+        """Bytes the single-GPU plan actually streams per matvec: a symmetric
+        nearfield (or coupling set) is stored once per block pair
+        (MatvecPlan.info), i.e. below matvec_bytes()."""
+        info = self.plan().info()
+        near = info["near_bytes"] if info["near_symmetric"] else 8 * self.near_layout.entries
+        cpl = info["coupling_bytes"] if info["coupling_symmetric"] else 8 * self.far_layout.entries
+        return self.matvec_bytes() - 8 * (self.near_layout.entries + self.far_layout.entries) + near + cpl
 
 
 def _scatter(flat, off, ld, block):

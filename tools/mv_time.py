@@ -48,5 +48,7 @@ for k in range(105):
 ts = np.sort(ts)[: int(0.8 * len(ts))]  # drop the slowest 20 %; mean resolves below the 2 us event tick
 t = float(np.mean(ts)) * 1e-3
 b = H.matvec_bytes()
-print(f"matvec {t*1e6:.1f} us (mean of fastest {len(ts)}), {b/t/1e9:.0f} GB/s, {b/t/1e9/bench.peaks()['hbm_gbs']*100:.1f} % of HBM")
+sb = H.streamed_bytes()
+print(f"matvec {t*1e6:.1f} us (mean of fastest {len(ts)}), {b/t/1e9:.0f} GB/s algorithmic = "
+      f"{b/t/1e9/bench.peaks()['hbm_gbs']*100:.1f} % of HBM; streamed {sb/1e6:.1f} MB = {sb/t/1e9:.0f} GB/s")
 print("plan", plan.info())
