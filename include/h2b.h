@@ -320,6 +320,14 @@ typedef struct {
 
 typedef struct h2b_plan h2b_plan;
 
+/* Builds the task records of the fused matvec from the layout (the arrays stay
+ * owned by the caller and must outlive the plan).  A single-GPU plan (owned ==
+ * NULL) whose row and column trees coincide and whose nearfield blocks satisfy
+ * D_(t,s) == D_(s,t)^T bit for bit (checked on the device) packs a copy of the
+ * upper blocks and streams each block pair once; later changes to D are not
+ * seen by such a plan (create a new one).  Environment knobs read here:
+ * H2B_NEAR_SYM=0 (stream every block), H2B_CPL_SYM=1 (also the couplings),
+ * H2B_LOOP=1 (persistent variant), H2B_TRACE=1 (timeline). */
 int h2b_plan_create(const h2b_layout* layout, h2b_plan** out);
 int h2b_plan_destroy(h2b_plan* plan);
 /* y = A x for device vectors in natural dof order (x: n_cols, y: n_rows). */
