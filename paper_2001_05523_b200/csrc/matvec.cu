@@ -1755,6 +1755,14 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
         if (int rc = build_sym_cpl(L, rstart, rsize, cstart, csize, rrank, crank, scols, soff, cxoff, sym.ppart_len,
                                    (int64_t)sym.nsum.size(), csym))
             return rc;
+    // gathered right-hand side per task: a panel (<= 64 columns) where the
+    // symmetric layouts are used, else the widest row of D / S
+    maxcols = std::max(2, maxk);
+    for (int i = 0; i < L.r_nodes; ++i) {
+        maxcols = std::max(maxcols, sym.on ? std::min<int>(dcols[i], 64) : dcols[i]);
+        maxcols = std::max(maxcols, csym.on ? std::min<int>(scols[i], 64) : scols[i]);
+    }
+    maxcols = (maxcols + 1) & ~1;
     const int smem =
         128 + kStageBytes +
         (int)sizeof(double) * (maxcols + 3 * vec_len + (sym.on || csym.on ? 2 * vec_len + kWarps * 64 : kWarps * 32));
