@@ -742,11 +742,14 @@ __device__ void task_forward(const double* __restrict__ c_V, const double* __res
 // `list` (LL offsets into s.ppart), i < size, always in list order.  H threads
 // per row take contiguous parts of the list (their sums are added in part
 // order); each thread keeps 8 loads in flight.  Ends with a block barrier.
-__device__ void near_sum(const Shared& s, const int64_t* list, int n, int size, uint32_t epoch, double* out) {
+// Threads [t0, t0 + nt) take part; bar_id 0 = block barrier, else a named
+// barrier over those nt threads.
+__device__ void near_sum(const Shared& s, const int64_t* list, int n, int size, uint32_t epoch, double* out,
+                         int t0 = 0, int nt = kThreads, int bar_id = 0) {
     int H = 1;
-    while (H < 4 && 2 * H * size <= kThreads) H *= 2;
-    const int tid = threadIdx.x;
-    const int step = H == 1 ? kThreads : size;
+    while (H < 4 && 2 * H * size <= nt) H *= 2;
+    const int tid = (int)threadIdx.x - t0;
+    const int step = H == 1 ? nt : size;
     for (int base = 0; base < size; base += step) {
         const int h = H == 1 ? 0 : tid / size;
         const int i = base + (H == 1 ? tid : tid - h * size);
@@ -783,14 +786,20 @@ __device__ void near_sum(const Shared& s, const int64_t* list, int n, int size, 
             s.red[h * size + i] = acc;
         }
     }
-    __syncthreads();
+    auto sync = [&]() {
+        if (bar_id == 0)
+            __syncthreads();
+        else
+            asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nt) : "memory");
+    };
+    sync();
     if (H > 1) {
-        for (int i = tid; i < size; i += kThreads) {
+        for (int i = tid; i < size; i += nt) {
             double t = 0.0;
             for (int h = 0; h < H; ++h) t += s.red[h * size + i];
             out[i] = t;
         }
-        __syncthreads();
+        sync();
     }
 }
 
@@ -805,7 +814,8 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
     double* Es = reinterpret_cast<double*>(s.stage);
     // symmetric nearfield: this leaf's rows are the sum of its partials
     const bool sym = leaf && s.near_sym && d[12] > 0;  // (else a near-sum task filled y_near)
-    if (sym) near_sum(s, s.nsum + d[11], (int)d[12], (int)d[8], epoch, s.yn);
+    // (one-warp downward step: warps 1..3 sum the partials meanwhile, below)
+    if (sym && !d[10]) near_sum(s, s.nsum + d[11], (int)d[12], (int)d[8], epoch, s.yn);
     // symmetric couplings: y_cpl of this cluster = the sum of its partials
     const bool csym = s.cpl_sym;
     if (csym) {
@@ -813,7 +823,14 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
         if (has_cpl) near_sum(s, s.nsum + d[13], (int)d[14], k, epoch, s.yc);
     }
     if (d[10]) {  // (record word 18) ranks <= 32, leaf <= 64 rows: one warp, no block barriers
-        if (threadIdx.x >= 32) return;
+        if (threadIdx.x >= 32) {
+            if (sym) {
+                // the leaf's nearfield rows, while warp 0 waits for its inputs
+                near_sum(s, s.nsum + d[11], (int)d[12], (int)d[8], epoch, s.yn, 32, kThreads - 32, 1);
+                __syncthreads();  // s.yn -> warp 0
+            }
+            return;
+        }
         const int lane = threadIdx.x;
         const int size = leaf ? (int)d[8] : 0;
         double* Vt = Es + ((k * kp + 1) & ~1);
@@ -849,7 +866,10 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
             return;
         }
         if (lane < k) s.vb[lane] = v;
-        __syncwarp();
+        if (sym)
+            __syncthreads();  // s.yn from warps 1..3
+        else
+            __syncwarp();
         for (int i = lane; i < size; i += 32) {
             double a0 = 0.0, a1 = 0.0;
             int r = 0;

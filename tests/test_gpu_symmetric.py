@@ -128,7 +128,8 @@ def test_nonsymmetric_couplings_stream_every_block():
 
 def test_near_sum_tasks_variant_matches():
     """Opt-in H2B_NEAR_SUM_TASKS=1: the leaf partial sums run as separate
-    tasks in the nearfield stream (same sums, same order)."""
+    tasks in the nearfield stream (same partials and list order; the threads
+    split the list differently, so the association, not the values, differs)."""
     from paper_2001_05523_b200.containers import MatvecPlan
 
     H = _slp(4, 32)
@@ -138,4 +139,6 @@ def test_near_sum_tasks_variant_matches():
     finally:
         del os.environ["H2B_NEAR_SUM_TASKS"]
     x = np.random.default_rng(3).standard_normal(H.shape[1])
-    assert np.array_equal(p.apply(x), H.matvec(x))
+    y = p.apply(x)
+    assert rel(y, H.matvec(x)) < 1e-14
+    assert np.array_equal(y, p.apply(x))
