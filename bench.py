@@ -131,7 +131,7 @@ def ncu_traffic(kernel, path=None):
     """DRAM bytes (read + write) of one launch of `kernel` from the committed
     ncu --set full capture (profiles/), or None."""
     import csv
-    path = path or os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01s5_ncu_full_raw.csv")
+    path = path or os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01s8_ncu_full_raw.csv")
     if not os.path.exists(path):
         return None
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
@@ -390,7 +390,7 @@ def run_ours(args, cfg):
         "roofline": {"bound": "hbm", "kernel": "k_matvec (fused forward + coupling + backward + nearfield)",
                      "achieved": mv_bytes / mean_step / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": mv_bytes / mean_step / 1e9 / pk["hbm_gbs"], "traffic": ncu_traffic("k_matvec"),
-                     "traffic_source": "profiles/r01s5_ncu_full_raw.csv (ncu --set full, one launch, DRAM read+write bytes)",
+                     "traffic_source": "profiles/r01s8_ncu_full_raw.csv (ncu --set full, one launch, DRAM read+write bytes)",
                      "algorithmic_bytes": mv_bytes, "kernel_ms": mean_step * 1e3, "peak_source": pk["hbm_src"],
                      "streamed_bytes": st_bytes, "streamed_frac": st_bytes / mean_step / 1e9 / pk["hbm_gbs"],
                      "note": "algorithmic = SURVEY 8(d) (every operator entry once); the plan streams the "
