@@ -17,13 +17,16 @@
  *   h2b_panel_points     <- quadrature.triangle_points             quadrature.py:71-87
  *   h2b_touch_count/fill <- kernels.touching_pairs/_classify_pairs  kernels.py:246-254,333-343
  *                           + quadrature.classify_panel_pair        quadrature.py:90-118
- *   h2b_singular         <- kernels.pair_integrals / SingularTable kernels.py:260-362
+ *   h2b_singular         <- kernels.SingularTable (all touching pairs) kernels.py:346-362
+ *   h2b_pair_integrals   <- kernels.pair_integrals (any pair list)  kernels.py:260-319
  *   h2b_pair_blocks_slp  <- kernels.panel_pair_matrix(SLP)+slp_block kernels.py:365-445
  *   h2b_pair_blocks_dlp  <- kernels.panel_pair_matrix(DLP)+dlp_block kernels.py:365-434,448-468
  *   h2b_plan_create /
  *   h2b_matvec           <- containers.H2Matrix.matvec             containers.py:254-270
  *                           (ClusterBasis.forward/backward          containers.py:201-228)
  *   h2b_diagonal         <- containers.H2Matrix.diagonal           containers.py:290-301
+ *   h2b_basis_forward /
+ *   h2b_basis_backward   <- containers.ClusterBasis.forward/backward containers.py:201-228
  *   h2b_matmat           <- (no reference counterpart: H2Matrix.matvec per column, containers.py:254-270)
  *   h2b_cg_*             <- solver.cg (vector updates, dots)      solver.py:22-59
  *   h2b_gca_columns /
@@ -145,6 +148,16 @@ typedef struct {
 int h2b_singular(const h2b_mesh* m, const h2b_touch* t, int kind, const h2b_rule* rules,
                  double* d_values, void* stream);
 
+/* kernels.pair_integrals (kernels.py:260-319) on an arbitrary list of n
+ * panel pairs (d_pa[i], d_pb[i]): each pair is classified on the device
+ * (quadrature.classify_panel_pair) and integrated with the Sauter-Schwab rule
+ * of its case, rules[0..3] = identical, edge, vertex, disjoint
+ * (quadrature.sauter_schwab_rule).  values: n (SLP; edge/vertex pairs
+ * averaged over both orientations) or n x 3 (DLP, original local vertex
+ * order of the column panel; identical pairs 0).  Synchronises. */
+int h2b_pair_integrals(const h2b_mesh* m, int64_t n, const int32_t* d_pa, const int32_t* d_pb, int kind,
+                       const h2b_rule* rules, double* d_values, void* stream);
+
 typedef struct {
     int64_t n_jobs;
     const int64_t* d_jobs;    /* n_jobs x 8: row_off, n_rows, col_off, n_cols, out_off, out_ld,
@@ -234,6 +247,40 @@ int h2b_gca_columns(const h2b_mesh* m, const double* d_panel_points, int32_t Q, 
  * residuals that do not fit in shared memory. */
 int h2b_gca_aca(const h2b_gca_batch* b, double eps, const double* d_L, double* d_scratch, int32_t* d_rank,
                 int32_t* d_tau, int32_t tau_cap, double* d_V, void* stream);
+
+/* ================= cluster-basis transforms (device) ====================== */
+
+/* A nested cluster basis (ClusterBasis, containers.py:189-238) on the device:
+ * per uid child uids (-1 for leaves), permuted start and size, rank k_t and the
+ * offsets of V_t (leaves, |t| x k_t row-major), E_t (non-root, k_t x k_parent)
+ * and of the cluster's coefficients in a packed coefficient vector; clusters
+ * listed level by level (root level first): level l = d_level_nodes
+ * [h_level_off[l], h_level_off[l+1]). */
+typedef struct {
+    int64_t n_nodes;
+    const int32_t* d_left;
+    const int32_t* d_right;
+    const int32_t* d_start;
+    const int32_t* d_size;
+    const int32_t* d_rank;
+    const int64_t* d_v_off;
+    const int64_t* d_e_off;
+    const int64_t* d_hat_off;
+    const double* d_V;
+    const double* d_E;
+    int32_t n_levels;
+    const int64_t* h_level_off; /* host, n_levels + 1 */
+    const int32_t* d_level_nodes;
+} h2b_basis;
+
+/* ClusterBasis.forward (containers.py:201-212): x_hat of every cluster from the
+ * permuted vector xp (leaves V_t^T xp|_t, parents sum over children of
+ * E_ch^T x_hat_ch).  d_xhat: packed coefficients (d_hat_off). */
+int h2b_basis_forward(const h2b_basis* b, const double* d_xp, double* d_xhat, void* stream);
+/* ClusterBasis.backward (containers.py:214-228): top down y_hat_ch += E_ch
+ * y_hat_t, then leaves yp|_t += V_t y_hat_t.  d_yhat (packed) is updated in
+ * place; d_yp is accumulated into. */
+int h2b_basis_backward(const h2b_basis* b, double* d_yhat, double* d_yp, void* stream);
 
 /* ====================== CG vector kernels (device) ========================= */
 
@@ -325,9 +372,14 @@ typedef struct h2b_plan h2b_plan;
  * NULL) whose row and column trees coincide and whose nearfield blocks satisfy
  * D_(t,s) == D_(s,t)^T bit for bit (checked on the device) packs a copy of the
  * upper blocks and streams each block pair once; later changes to D are not
- * seen by such a plan (create a new one).  Environment knobs read here:
- * H2B_NEAR_SYM=0 (stream every block), H2B_CPL_SYM=1 (also the couplings),
- * H2B_LOOP=1 (persistent variant), H2B_TRACE=1 (timeline). */
+ * seen by such a plan (create a new one).  Environment knobs read here (test
+ * and diagnostics only): H2B_NEAR_SYM=0 (stream every block, one-sided),
+ * H2B_TRACE=1 (per-task timeline).
+ * A plan owns one ticket counter and one set of inter-CTA scratch buffers, so
+ * its launches are serialised: calls from several host threads take a
+ * per-plan lock, and a launch on a different stream than the plan's previous
+ * launch first waits for that launch (event).  Different plans run
+ * concurrently. */
 int h2b_plan_create(const h2b_layout* layout, h2b_plan** out);
 int h2b_plan_destroy(h2b_plan* plan);
 /* y = A x for device vectors in natural dof order (x: n_cols, y: n_rows). */

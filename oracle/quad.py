@@ -76,7 +76,8 @@ def _chart(c, u, v):
 
 
 def singular_integrals(V, T, N, A, pa, pb, kind, q, chunk=200_000):
-    """Sauter-Schwab integrals of touching pairs -- kernels.py:260-319.
+    """Regularised pair integrals -- kernels.py:260-319 (pair_integrals): any
+    case, disjoint pairs by the tensor rule of quadrature.py:171-180.
     SLP: (B,); edge/vertex averaged with the orientation-swapped rule.
     DLP: (B, 3) per ORIGINAL local vertex of the column panel; identical -> 0."""
     pa = np.asarray(pa, dtype=np.int64)
@@ -86,7 +87,7 @@ def singular_integrals(V, T, N, A, pa, pb, kind, q, chunk=200_000):
     if B == 0:
         return out
     code, perm_a, perm_b = classify(T[pa], T[pb], pa == pb)
-    for c, case in ((3, "identical"), (2, "edge"), (1, "vertex")):
+    for c, case in ((3, "identical"), (2, "edge"), (1, "vertex"), (0, "disjoint")):
         idx = np.flatnonzero(code == c)
         if len(idx) == 0 or (kind == "dlp" and case == "identical"):
             continue
@@ -103,7 +104,7 @@ def singular_integrals(V, T, N, A, pa, pb, kind, q, chunk=200_000):
             r = np.sqrt(np.einsum("bnk,bnk->bn", d, d))
             if kind == "slp":
                 val = (INV4PI / r) @ w
-                if case != "identical":
+                if case in ("edge", "vertex"):
                     d2 = _chart(ca, P[:, 2], P[:, 3]) - _chart(cb, P[:, 0], P[:, 1])
                     r2 = np.sqrt(np.einsum("bnk,bnk->bn", d2, d2))
                     val = 0.5 * (val + (INV4PI / r2) @ w)

@@ -32,7 +32,7 @@ def _tensor4(q):
 
 
 def ss_rule(case, q):
-    """Sauter-Schwab rule for case in {'identical', 'edge', 'vertex'}:
+    """Sauter-Schwab rule for case in {'identical', 'edge', 'vertex', 'disjoint'}:
     (points (N, 4) = u1, v1, u2, v2, weights) -- quadrature.py:121-190."""
     (e1, e2, e3, xi), W = _tensor4(q)
     if case == "identical":
@@ -58,6 +58,14 @@ def ss_rule(case, q):
             ((xi * (1 - e1 * e2 * e3), xi * e1 * (1 - e2 * e3)), (xi, xi * e1 * e2)),
         ]
         jac = [ja, jb, jb, jb, jb]
+    elif case == "disjoint":
+        # quadrature.py:171-180: the tensor product of two Duffy rules in chart
+        # coordinates (u, v) = (s, s t), weight w_s w_t w_s' w_t' s s'
+        x, w = gauss01(q)
+        G = np.array(np.meshgrid(x, x, x, x, indexing="ij")).reshape(4, -1)
+        Wg = np.array(np.meshgrid(w, w, w, w, indexing="ij")).reshape(4, -1)
+        P = np.column_stack([G[0], G[0] * G[1], G[2], G[2] * G[3]])
+        return P, Wg[0] * Wg[1] * Wg[2] * Wg[3] * G[0] * G[2]
     elif case == "vertex":
         # quadrature.py:156-160
         j = xi**3 * e2

@@ -73,6 +73,14 @@ class GcaBatch(ctypes.Structure):
     ]
 
 
+class Basis(ctypes.Structure):
+    _fields_ = [
+        ("n_nodes", ctypes.c_int64), ("d_left", vp), ("d_right", vp), ("d_start", vp), ("d_size", vp),
+        ("d_rank", vp), ("d_v_off", vp), ("d_e_off", vp), ("d_hat_off", vp), ("d_V", vp), ("d_E", vp),
+        ("n_levels", ctypes.c_int32), ("h_level_off", vp), ("d_level_nodes", vp),
+    ]
+
+
 class Layout(ctypes.Structure):
     _fields_ = [
         ("n_rows", ctypes.c_int64), ("n_cols", ctypes.c_int64),
@@ -99,7 +107,8 @@ EXPORTS = (
     "h2b_plan_create", "h2b_plan_destroy", "h2b_matvec", "h2b_matvec_host",
     "h2b_diagonal", "h2b_plan_trace", "h2b_plan_info", "h2b_dlp_jobs_build", "h2b_dlp_jobs_sizes", "h2b_dlp_jobs_copy",
     "h2b_dlp_jobs_free", "h2b_gca_columns", "h2b_gca_aca", "h2b_cg_workspace_size", "h2b_cg_dot", "h2b_cg_step",
-    "h2b_cg_direction", "h2b_matmat_create", "h2b_matmat_destroy", "h2b_matmat",
+    "h2b_cg_direction", "h2b_matmat_create", "h2b_matmat_destroy", "h2b_matmat", "h2b_pair_integrals",
+    "h2b_basis_forward", "h2b_basis_backward",
 )
 
 _lib = None
@@ -153,6 +162,10 @@ def lib():
         L.h2b_cg_dot.argtypes = [vp, vp, ctypes.c_int64, vp, vp, vp]
         L.h2b_cg_step.argtypes = [ctypes.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         L.h2b_cg_direction.argtypes = [ctypes.c_int64, vp, vp, vp, vp]
+        L.h2b_pair_integrals.argtypes = [ctypes.POINTER(Mesh), ctypes.c_int64, vp, vp, ctypes.c_int,
+                                         ctypes.POINTER(Rule), vp, vp]
+        L.h2b_basis_forward.argtypes = [ctypes.POINTER(Basis), vp, vp, vp]
+        L.h2b_basis_backward.argtypes = [ctypes.POINTER(Basis), vp, vp, vp]
         L.h2b_gca_aca.argtypes = [ctypes.POINTER(GcaBatch), ctypes.c_double, vp, vp, vp, vp, ctypes.c_int32, vp, vp]
         _lib = L
     return _lib

@@ -40,7 +40,7 @@ class AssemblyContext:
     @property
     def dmesh(self):
         if self._dmesh is None:
-            self._dmesh = kernels.DeviceMesh(self.mesh)
+            self._dmesh = kernels.device_mesh(self.mesh)
         return self._dmesh
 
     @property
@@ -336,8 +336,68 @@ class ClusterBasis:
         return sum(v.size for v in self.V.values()) + sum(e.size for e in self.E.values())
 
     def forward(self, xp):
-        """x_hat_t = V_t^T x|_t for every cluster, on the device (permuted input)."""
-        return _basis_transform(self, np.asarray(xp, dtype=float))
+        """x_hat_t for every cluster from the permuted vector xp
+        (containers.py:201-212): leaves V_t^T xp|_t, parents the sum over
+        their children of E_ch^T x_hat_ch.  Runs on the device
+        (h2b_basis_forward); returns {uid: (k_t,) array} like the reference
+        (CUDA tensors in -> CUDA tensor values out)."""
+        t = D.require_cuda()
+        dev_in = isinstance(xp, t.Tensor)
+        n = self.tree.n_dofs
+        x = xp.contiguous() if dev_in else D.dev(np.asarray(xp, dtype=np.float64))
+        if x.dtype != t.float64 or x.ndim != 1 or x.numel() != n:
+            raise ValueError(f"expected a float64 vector of length {n}")
+        db = self._device()
+        xhat = t.empty(max(int(db.hat[-1]), 1), dtype=t.float64, device="cuda")
+        _lib.check(_lib.lib().h2b_basis_forward(ctypes.byref(db.c), x.data_ptr(), xhat.data_ptr(), D.stream()))
+        out = xhat if dev_in else D.host(xhat)
+        return {u: out[db.hat[u] : db.hat[u + 1]] for u in range(self.tree.n_nodes)}
+
+    def backward(self, yhat, yp):
+        """Accumulate sum_t V_t y_hat_t into the permuted vector yp
+        (containers.py:214-228): top down y_hat_ch += E_ch y_hat_t, then the
+        leaves.  Clusters without an entry in yhat contribute nothing; yhat
+        receives the propagated coefficients of every cluster below an entry,
+        as in the reference.  Runs on the device (h2b_basis_backward); yp is
+        updated in place (numpy array or CUDA tensor)."""
+        t = D.require_cuda()
+        db = self._device()
+        n = self.tree.n_dofs
+        dense = np.zeros(max(int(db.hat[-1]), 1))
+        for u, v in yhat.items():
+            v = D.host(v) if isinstance(v, t.Tensor) else np.asarray(v, dtype=np.float64)
+            dense[db.hat[u] : db.hat[u + 1]] = v
+        yd = D.dev(dense)
+        dev_out = isinstance(yp, t.Tensor)
+        if dev_out:
+            if yp.dtype != t.float64 or yp.numel() != n or not yp.is_contiguous():
+                raise ValueError(f"expected a contiguous float64 vector of length {n}")
+            y = yp
+        else:
+            if np.shape(yp) != (n,):
+                raise ValueError(f"expected a vector of length {n}")
+            y = D.dev(np.asarray(yp, dtype=np.float64))
+        _lib.check(_lib.lib().h2b_basis_backward(ctypes.byref(db.c), yd.data_ptr(), y.data_ptr(), D.stream()))
+        if not dev_out:
+            yp[...] = D.host(y)
+        # the reference leaves the propagated coefficients in yhat
+        reached = np.zeros(self.tree.n_nodes, dtype=bool)
+        reached[list(yhat.keys())] = True
+        for u in np.argsort(self.tree.depth_of, kind="stable"):
+            p = self.tree.parent_of[u]
+            if p >= 0 and reached[p]:
+                reached[u] = True
+        h = D.host(yd)
+        for u in np.flatnonzero(reached):
+            v = h[db.hat[u] : db.hat[u + 1]].copy()
+            yhat[int(u)] = D.dev(v) if dev_out else v
+        return yp
+
+    def _device(self):
+        """Device copy of the packed basis + the h2b_basis descriptor (cached)."""
+        if getattr(self, "_dev", None) is None:
+            self._dev = _BasisTransforms(self)
+        return self._dev
 
     def packed(self):
         """(ranks, V flat, v_off, E flat, e_off, hat_off) in uid order; cached.
@@ -375,10 +435,25 @@ class ClusterBasis:
         return self._packed
 
 
-def _basis_transform(basis, xp):
-    """Forward transform via a matvec plan with no far/near blocks reading out
-    x_hat (device path; used by the reference-API ClusterBasis.forward)."""
-    raise NotImplementedError("ClusterBasis.forward: use H2Matrix.forward_coefficients (device)")
+class _BasisTransforms:
+    """h2b_basis descriptor of a ClusterBasis: packed V / E on the device and
+    the clusters listed level by level (root first)."""
+
+    def __init__(self, basis):
+        t = basis.tree
+        ranks, V, v_off, E, e_off, hat = basis.packed()
+        order = np.argsort(t.depth_of, kind="stable")
+        depth = t.depth_of[order]
+        level_off = np.searchsorted(depth, np.arange(int(depth.max()) + 2)).astype(np.int64)
+        self.hat = hat
+        self._keep = [D.dev(a, dt) for a, dt in (
+            (t.left, np.int32), (t.right, np.int32), (t.start, np.int32), (t.end - t.start, np.int32),
+            (ranks, np.int32), (np.maximum(v_off, 0), np.int64), (np.maximum(e_off, 0), np.int64),
+            (hat[:-1], np.int64), (V, np.float64), (E, np.float64), (order, np.int32))]
+        k = self._keep
+        self._level_off = level_off
+        self.c = _lib.Basis(t.n_nodes, *(a.data_ptr() for a in k[:10]), len(level_off) - 1, _lib.ptr(level_off),
+                            k[10].data_ptr())
 
 
 class _DeviceBasis:

@@ -49,6 +49,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "device_common.cuh"
@@ -76,15 +77,11 @@ constexpr int kBandWords = 24;  // src_off, cols, rows, gidx_off, out_off, is_la
 constexpr int kFwdHead = 7;     // start, size, k, v_off, xhat_off, n_climb, warp_ok
 constexpr int kFwdLevel = 6;    // k0, kp, e_off_c0, e_off_own, xhat_off_c0, xhat_off_parent
 constexpr int kCopyChunk = 1024;  // x values per copy task (host-input launches)
-constexpr int kKindNear = 0, kKindCpl = 1, kKindDescent = 3;  // band record kinds (word 7)
+constexpr int kKindNear = 0, kKindCpl = 1;  // band record kinds (word 7)
 // symmetric nearfield band (see task_panel): words 8..10 = offset of the
 // transposed outputs (column c -> 8 + c), leading diagonal-block columns
 // without a transposed output, gather offset of the row leaf's own x
 constexpr int kKindNearSym = 4;
-constexpr int kKindCplSym = 5;  // symmetric coupling panel (same words as kKindNearSym)
-// a leaf's nearfield rows summed from its partials into y_near (symmetric
-// nearfield): words 0 list offset, 1 list length, 2 rows, 3 first row
-constexpr int kKindNearSum = 6;
 
 }  // namespace
 }  // namespace h2b
@@ -104,7 +101,6 @@ struct h2b_plan {
     int n_near, n_cpl;
     int max_cols, vec_len;
     int smem;
-    int loop_grid;      // > 0: persistent k_matvec_loop with this many CTAs (H2B_LOOP=1)
     int64_t e_bytes_r;
     double* dx;
     double* dy;
@@ -120,9 +116,15 @@ struct h2b_plan {
     int64_t ppart_len;
     int n_leaf;         // leaf downward-step tasks per launch
     int64_t near_bytes; // nearfield bytes one matvec streams
-    double* ssym;       // packed column panels of the upper coupling blocks (null when unused)
-    int32_t* gsym_c;    // their x_hat gather indices
     int64_t cpl_bytes;  // coupling bytes one matvec streams
+    // Launches of one plan must run one after another (one ticket counter and
+    // one set of LL scratch buffers per plan): a host mutex serialises callers,
+    // and a launch on a different stream than the previous one first waits
+    // for it (event), so stream-ordered use from any stream is safe.
+    std::mutex mu;
+    cudaEvent_t done = nullptr;
+    cudaStream_t last = nullptr;
+    bool launched = false;
 };
 
 namespace h2b {
@@ -508,8 +510,6 @@ struct Shared {
     double* yn;                // vec_len: a leaf's summed nearfield rows (symmetric nearfield)
     const uint64_t* ppart;     // symmetric nearfield partials or null
     const int64_t* nsum;       // their per-leaf lists
-    double* yc;                // vec_len: a cluster's summed coupling partials (symmetric couplings)
-    bool cpl_sym;              // couplings as symmetric column panels
     bool near_sym;             // nearfield as symmetric column panels
     uint32_t parity;           // mbarrier phase of the staging slot in use
     bool issued;               // band bulk copy already issued by the caller
@@ -813,21 +813,16 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
     const int start = (int)d[7];
     double* Es = reinterpret_cast<double*>(s.stage);
     // symmetric nearfield: this leaf's rows are the sum of its partials
-    const bool sym = leaf && s.near_sym && d[12] > 0;  // (else a near-sum task filled y_near)
+    const bool sym = leaf && s.near_sym && d[12] > 0;
     // (one-warp downward step: warps 1..3 sum the partials meanwhile, below)
     if (sym && !d[10]) near_sum(s, s.nsum + d[11], (int)d[12], (int)d[8], epoch, s.yn);
-    // symmetric couplings: y_cpl of this cluster = the sum of its partials
-    const bool csym = s.cpl_sym;
-    if (csym) {
-        has_cpl = d[14] > 0;
-        if (has_cpl) near_sum(s, s.nsum + d[13], (int)d[14], k, epoch, s.yc);
-    }
     if (d[10]) {  // (record word 18) ranks <= 32, leaf <= 64 rows: one warp, no block barriers
         if (threadIdx.x >= 32) {
             if (sym) {
-                // the leaf's nearfield rows, while warp 0 waits for its inputs
+                // the leaf's nearfield rows, while warp 0 waits for its inputs;
+                // named barrier 2 (all 128 threads) hands s.yn over to warp 0
                 near_sum(s, s.nsum + d[11], (int)d[12], (int)d[8], epoch, s.yn, 32, kThreads - 32, 1);
-                __syncthreads();  // s.yn -> warp 0
+                asm volatile("bar.sync 2, %0;" ::"r"(kThreads) : "memory");
             }
             return;
         }
@@ -845,7 +840,7 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
                 const int r = i / k, c = i - r * k;
                 cp_async8(Vt + c * size + r, r_V + v_off + i);
             }
-        double v = (has_cpl && lane < k) ? (csym ? s.yc[lane] : ll_load(ycpl + 2 * (yoff + lane), epoch)) : 0.0;
+        double v = (has_cpl && lane < k) ? ll_load(ycpl + 2 * (yoff + lane), epoch) : 0.0;
         if (par_off >= 0 && lane < kp) s.rhs[lane] = ll_load(yfin + 2 * (par_off + lane), epoch);
         cp_async_wait_all();
         __syncwarp();
@@ -867,7 +862,7 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
         }
         if (lane < k) s.vb[lane] = v;
         if (sym)
-            __syncthreads();  // s.yn from warps 1..3
+            asm volatile("bar.sync 2, %0;" ::"r"(kThreads) : "memory");  // s.yn from warps 1..3
         else
             __syncwarp();
         for (int i = lane; i < size; i += 32) {
@@ -893,7 +888,7 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
         }
     const uint64_t* yc = ycpl + 2 * yoff;
     for (int i = threadIdx.x; i < k; i += kThreads)
-        s.va[i] = has_cpl ? (csym ? s.yc[i] : ll_load(yc + 2 * i, epoch)) : 0.0;
+        s.va[i] = has_cpl ? ll_load(yc + 2 * i, epoch) : 0.0;
     __syncthreads();
     mark(s.mark, 0);
     if (par_off >= 0) {
@@ -1087,13 +1082,9 @@ __device__ __forceinline__ void gather2(double* d1, const int32_t* idx1, int n1,
 // ONCE for both triangles: the direct product D x|_cols -> t's partial at
 // out_off, and the transposed product D^T x|_t -> the columns' partials at
 // tr_off + c (skipped for the diagonal block's columns, which are stored in
-// full).  Never waits.  Coupling panels (kCpl, symmetric couplings) do the
-// same on S with x_hat in LL form (they wait on the forward tasks); they have
-// no diagonal block.
-template <bool kCpl>
+// full).  Never waits.
 __device__ void task_panel(const double* __restrict__ base, const int32_t* __restrict__ gl,
-                           const double* __restrict__ x, const uint64_t* xhat, uint64_t* ppart, uint32_t epoch,
-                           const Shared& s) {
+                           const double* __restrict__ x, uint64_t* ppart, uint32_t epoch, const Shared& s) {
     const int64_t src_off = s.rec[0], gi_off = s.rec[3], out_off = s.rec[4];
     const int cols = (int)s.rec[1], rows = (int)s.rec[2];
     const int64_t tr_off = s.rec[8], rg_off = s.rec[10];
@@ -1104,9 +1095,8 @@ __device__ void task_panel(const double* __restrict__ base, const int32_t* __res
                                : stage_issue(s, base + src_off, bytes);
     mark(s.mark, 0);
     const bool tr = skip < cols;
-    if (kCpl || s.xll)
-        gather2<true>(s.rhs, gl + gi_off, cols, s.vb, gl + rg_off, tr ? rows : 0, nullptr, kCpl ? xhat : s.xll,
-                      epoch);
+    if (s.xll)
+        gather2<true>(s.rhs, gl + gi_off, cols, s.vb, gl + rg_off, tr ? rows : 0, nullptr, s.xll, epoch);
     else
         gather2<false>(s.rhs, gl + gi_off, cols, s.vb, gl + rg_off, tr ? rows : 0, x, nullptr, epoch);
     mark(s.mark, 1);
@@ -1139,8 +1129,6 @@ struct KArgs {
     const int32_t* gsym;
     uint64_t* ppart;
     const int64_t* nsum;
-    const double* ssym;      // symmetric couplings (null: not used)
-    const int32_t* gsym_c;
 };
 
 #ifndef H2B_MINB
@@ -1223,26 +1211,17 @@ __device__ __forceinline__ void run_task(const KArgs& a, const double* __restric
         if (b < np) prefetch_slice(L.r_E, a.e_bytes_r, b, np);
         load_rec(s, a.rec + a.band_base + (int64_t)kBandWords * b, kBandWords);
         const int kind = (int)s.rec[7];
-        if (kind == kKindNearSym) {
-            task_panel<false>(a.dsym, a.gsym, x, nullptr, a.ppart, epoch, s);
-        } else if (kind == kKindNearSum) {
-            const int rows = (int)s.rec[2];
-            near_sum(s, a.nsum + s.rec[0], (int)s.rec[1], rows, epoch, s.yn);
-            uint64_t* dst = a.ynear + 2 * s.rec[3];
-            for (int i = threadIdx.x; i < rows; i += kThreads) ll_store(dst + 2 * i, s.yn[i], epoch);
-        } else if (kind == kKindCplSym)
-            task_panel<true>(a.ssym, a.gsym_c, x, a.xhat, a.ppart, epoch, s);
+        if (kind == kKindNearSym)
+            task_panel(a.dsym, a.gsym, x, a.ppart, epoch, s);
         else if (kind == kKindNear)
             task_band<false>(L, x, a.xhat, a.ynear, a.yfin, a.ycpl, a.ynear, y, epoch, s);
-        else if (kind == kKindCpl)
-            task_band<true>(L, x, a.xhat, a.ycpl, a.yfin, a.ycpl, a.ynear, y, epoch, s);
         else
-            descent(L.r_E, L.r_V, L.row_perm, s.rec + 8, a.ycpl, a.yfin, a.ynear, y, epoch, s.rec[6] != 0, s);
+            task_band<true>(L, x, a.xhat, a.ycpl, a.yfin, a.ycpl, a.ynear, y, epoch, s);
     }
     __syncthreads();
     if (a.yh && threadIdx.x == 0 && ticket >= tB) {
         const int kind = (int)s.rec[7];
-        if (((kind == kKindCpl && s.rec[5]) || kind == kKindDescent) && s.rec[13]) {  // a leaf's rows of y are out
+        if (kind == kKindCpl && s.rec[5] && s.rec[13]) {  // a leaf's rows of y are out
             __threadfence();
             atomicAdd(a.ydone, 1ull);
         }
@@ -1258,7 +1237,7 @@ __device__ __forceinline__ void run_task(const KArgs& a, const double* __restric
             const int kd = ticket < L.c_leaves ? 2 : (int)s.rec[7];
             a.trace[8 * ticket + 2] = smid | ((unsigned long long)kd << 16) |
                                       (kd == 2 ? (unsigned long long)s.rec[5] << 24 : 0ull) |
-                                      ((kd == 1 && s.rec[5]) || kd == 3 ? (1ull << 41) | ((unsigned long long)s.rec[17] << 32) : 0ull);
+                                      (kd == 1 && s.rec[5] ? (1ull << 41) | ((unsigned long long)s.rec[17] << 32) : 0ull);
         }
     }
 }
@@ -1279,9 +1258,7 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
     s.vb = s.va + 2 * a.vec_len;
     s.red = s.vb + a.vec_len;
     s.yn = s.red + kWarps * 64;
-    s.yc = s.yn + a.vec_len;
     s.near_sym = a.dsym != nullptr;
-    s.cpl_sym = a.ssym != nullptr;
     s.ppart = a.ppart;
     s.nsum = a.nsum;
     s.rec = s_rec;
@@ -1304,58 +1281,6 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
     const uint32_t epoch = s_epoch;
     s.xll = a.xh ? a.xll : nullptr;
     run_task(a, x, y, ticket, epoch, s);
-}
-
-// Persistent variant (H2B_LOOP=1): gridDim CTAs (one wave) each loop
-// take-ticket / run-task, so no CTA is relaunched per task.  A CTA holds one
-// ticket at a time, exactly as the one-task-per-CTA kernel, so the same
-// smallest-ticket argument rules out deadlock; a launch consumes n_tasks +
-// gridDim tickets (every CTA stops at its first ticket past the end).
-__global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec_loop(const KArgs a, const double* __restrict__ x,
-                                                            double* __restrict__ y) {
-    extern __shared__ __align__(128) char smraw[];
-    __shared__ int s_ticket;
-    __shared__ uint32_t s_epoch;
-    __shared__ int64_t s_rec[kFwdHead + kFwdLevel * kMaxDepth];
-    const h2b_layout& L = a.L;
-    const int host = a.xh != nullptr;
-    const int n_total = a.n_copy + L.c_leaves + a.n_near + a.n_cpl + a.n_out;
-    const unsigned long long per_launch = (unsigned long long)n_total + gridDim.x;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smraw);
-    for (int it = 0;; ++it) {
-        if (threadIdx.x == 0) {
-            const unsigned long long t = atomicAdd(a.ctrl + host, 1ull);
-            const int idx = (int)(t % per_launch);
-            s_ticket = idx < n_total ? idx - a.n_copy : INT_MIN;
-            s_epoch = 2u * (uint32_t)(t / per_launch) + 1u + (uint32_t)host;
-            // the previous task waited on every phase it armed: re-arm
-            if (it > 0) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-            mbar_init(bar, 1);
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-        __syncthreads();
-        const int ticket = s_ticket;
-        if (ticket == INT_MIN) return;
-        Shared s;
-        s.bar = bar;
-        s.stage = smraw + 128;
-        s.rhs = reinterpret_cast<double*>(smraw + 128 + kStageBytes);
-        s.va = s.rhs + a.max_cols;
-        s.vb = s.va + 2 * a.vec_len;
-        s.red = s.vb + a.vec_len;
-        s.yn = s.red + kWarps * 64;
-        s.yc = s.yn + a.vec_len;
-        s.near_sym = a.dsym != nullptr;
-        s.cpl_sym = a.ssym != nullptr;
-        s.ppart = a.ppart;
-        s.nsum = a.nsum;
-        s.rec = s_rec;
-        s.parity = 0;
-        s.issued = false;
-        s.xll = a.xh ? a.xll : nullptr;
-        run_task(a, x, y, ticket, s_epoch, s);
-        __syncthreads();
-    }
 }
 
 __global__ void k_diagonal(h2b_layout L, double* __restrict__ diag) {
@@ -1572,147 +1497,11 @@ int build_sym_near(const h2b_layout& L, const std::vector<int32_t>& rstart, cons
 }
 
 
-// Symmetric couplings: S_(t,s) == S_(s,t)^T bit for bit (containers.py
-// assemble_couplings mirrors them).  Per row cluster t, the blocks (t, s) with
-// s > t are cut into column panels of all k_t rows; the transposed product of
-// a panel goes to s.  Partials follow the nearfield's in the same buffer.
-struct SymCpl {
-    bool on = false;
-    std::vector<std::vector<int64_t>> bands;
-    std::vector<int64_t> list_off, list_n;
-    std::vector<int64_t> nsum, pack, check;
-    std::vector<int32_t> srccol, gsym;
-    std::vector<std::vector<int>> producers;  // per cluster u: the t < u whose panels hold (t, u)
-    int64_t ssym_len = 0, ppart_len = 0, bytes = 0;
-};
-
-int build_sym_cpl(const h2b_layout& L, const std::vector<int32_t>& rstart, const std::vector<int32_t>& rsize,
-                  const std::vector<int32_t>& cstart, const std::vector<int32_t>& csize,
-                  const std::vector<int32_t>& rrank, const std::vector<int32_t>& crank,
-                  const std::vector<int32_t>& scols, const std::vector<int64_t>& soff,
-                  const std::vector<int64_t>& cxoff, int64_t ppart_base, int64_t nsum_base, SymCpl& S) {
-    S.on = false;
-    if (L.owned || L.r_nodes != L.c_nodes || !L.far_ptr || !L.far_col) return 0;
-    // opt-in (H2B_CPL_SYM=1): measured slower than the row bands at configs 1
-    // and 2 (62.9 vs 57.2 us, 884 vs 774 us): the separate downward-step tasks
-    // and their partial sums lengthen the downward chain more than the halved
-    // coupling bytes save
-    {
-        const char* e = getenv("H2B_CPL_SYM");
-        if (!e || e[0] != '1') return 0;
-    }
-    const int n = L.r_nodes;
-    for (int u = 0; u < n; ++u)
-        if (rstart[u] != cstart[u] || rsize[u] != csize[u] || rrank[u] != crank[u]) return 0;
-    std::vector<int32_t> fptr, fcol;
-    H2B_CUDA_TRY(fetch(L.far_ptr, (int64_t)n + 1, fptr));
-    H2B_CUDA_TRY(fetch(L.far_col, std::max<int64_t>(fptr[n], 1), fcol));
-    std::vector<std::vector<std::pair<int, int64_t>>> blocks(n);
-    for (int t = 0; t < n; ++t) {
-        int64_t c = 0;
-        for (int q = fptr[t]; q < fptr[t + 1]; ++q) {
-            const int s = fcol[q];
-            if (s < 0 || s >= n || s == t) return 0;
-            blocks[t].push_back({s, c});
-            c += crank[s];
-        }
-        if (c > (int64_t)scols[t] || scols[t] - c >= 4) return 0;  // (rows padded to 4 columns)
-    }
-    auto find = [&](int t, int s) -> int64_t {
-        for (const auto& b : blocks[t])
-            if (b.first == s) return b.second;
-        return -1;
-    };
-    std::vector<std::vector<std::pair<int, int64_t>>> up(n);
-    for (int t = 0; t < n; ++t)
-        for (const auto& b : blocks[t]) {
-            const int64_t m = find(b.first, t);
-            if (m < 0) return 0;
-            if (b.first > t && rrank[t] > 0 && crank[b.first] > 0) {
-                up[t].push_back(b);
-                S.check.insert(S.check.end(), {soff[t] + b.second, scols[t], soff[b.first] + m, scols[b.first],
-                                               rrank[t], rrank[b.first]});
-            }
-        }
-    S.bands.assign(n, {});
-    S.list_off.assign(n, 0);
-    S.list_n.assign(n, 0);
-    S.producers.assign(n, {});
-    std::vector<int64_t> width(n, 0), tbase(n, 0);
-    std::vector<std::vector<int64_t>> tcol(n), direct(n);
-    int64_t pdir = ppart_base, dlen = 0, g = 0;
-    for (int t = 0; t < n; ++t) {
-        const int rows = rrank[t];
-        if (up[t].empty()) continue;
-        int64_t W = 0;
-        for (const auto& b : up[t]) {
-            tcol[t].push_back(W);
-            W += crank[b.first];
-        }
-        width[t] = W;
-        int wmax = std::min(64, std::max(2, (int)(kStageBytes / 8 / rows)));
-        if ((rows & 1) && (wmax & 1)) --wmax;
-        const int64_t gbase = g, sbase = (int64_t)S.srccol.size();
-        for (int a = 0; a < rows; ++a) S.gsym.push_back((int32_t)(cxoff[t] + a));  // the cluster's own x_hat
-        for (const auto& b : up[t])
-            for (int j = 0; j < crank[b.first]; ++j) {
-                S.srccol.push_back((int32_t)(b.second + j));
-                S.gsym.push_back((int32_t)(cxoff[b.first] + j));
-            }
-        g += rows + W;
-        for (int64_t j0 = 0; j0 < W; j0 += wmax) {
-            const int w = (int)std::min<int64_t>(wmax, W - j0);
-            std::vector<int64_t> r(kBandWords, 0);
-            r[0] = dlen;
-            r[1] = w;
-            r[2] = rows;
-            r[3] = gbase + rows + j0;
-            r[4] = pdir;
-            r[7] = kKindCplSym;
-            r[8] = j0;  // + the transposed base, below
-            r[9] = 0;
-            r[10] = gbase;
-            S.bands[t].insert(S.bands[t].end(), r.begin(), r.end());
-            S.pack.insert(S.pack.end(), {soff[t], scols[t], rows, w, dlen, sbase + j0});
-            direct[t].push_back(pdir);
-            pdir += rows;
-            dlen += ((int64_t)rows * w + 1) & ~int64_t(1);
-            S.bytes += 8 * (int64_t)rows * w;
-        }
-    }
-    int64_t tpos = pdir;
-    for (int t = 0; t < n; ++t) {
-        tbase[t] = tpos;
-        tpos += width[t];
-        for (size_t i = 0; i < S.bands[t].size(); i += kBandWords) S.bands[t][i + 8] += tbase[t];
-    }
-    S.ppart_len = tpos - ppart_base;
-    S.ssym_len = dlen;
-    for (int u = 0; u < n; ++u) {
-        S.list_off[u] = nsum_base + (int64_t)S.nsum.size();
-        if (rrank[u] > 0) {
-            for (int64_t o : direct[u]) S.nsum.push_back(o);
-            for (const auto& b : blocks[u]) {
-                const int t = b.first;
-                if (t > u || rrank[t] == 0 || crank[u] == 0) continue;
-                int64_t off = -1;
-                for (size_t i = 0; i < up[t].size(); ++i)
-                    if (up[t][i].first == u) off = tbase[t] + tcol[t][i];
-                if (off < 0) return 0;
-                S.nsum.push_back(off);
-                S.producers[u].push_back(t);
-            }
-        }
-        S.list_n[u] = nsum_base + (int64_t)S.nsum.size() - S.list_off[u];
-    }
-    S.on = true;
-    return 0;
-}
 }  // namespace
 }  // namespace h2b
 
 namespace {
-constexpr int kSymNear = 1, kSymCpl = 2;
+constexpr int kSymNear = 1;
 int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
     if (!layout || !out) return fail(H2B_ERR_INVALID, "h2b_plan_create: null pointer");
     const h2b_layout& L = *layout;
@@ -1762,30 +1551,22 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
     if (maxk > kMaxVec || maxleaf > kMaxVec)
         return fail(H2B_ERR_INVALID, "h2b_plan_create: cluster rank or leaf size above 512");
     const int vec_len = (std::max(maxk, maxleaf) + 1) & ~1;
-    // symmetric nearfield: leaf partial sums in the leaf's final task, or as
-    // separate tasks in the nearfield stream (H2B_NEAR_SUM_TASKS=1; measured
-    // slower: config 1 67.0 vs 59.4 us, sphere L8 920 vs 827 us, sphere L9
-    // m=5 4.47 vs 4.12 ms -- the extra tasks cost more than the shorter tail)
-    const bool near_sum_tasks = getenv("H2B_NEAR_SUM_TASKS") && getenv("H2B_NEAR_SUM_TASKS")[0] == '1';
+    // symmetric nearfield: each leaf's partials are summed in the leaf's final
+    // task (separate sum tasks in the nearfield stream measured slower)
     SymNear sym;
     if (sym_flags & kSymNear)
         if (int rc = build_sym_near(L, rstart, rsize, cstart, csize, rvoff, dcols, doff, dgoff, sym)) return rc;
-    SymCpl csym;
-    if (sym_flags & kSymCpl)
-        if (int rc = build_sym_cpl(L, rstart, rsize, cstart, csize, rrank, crank, scols, soff, cxoff, sym.ppart_len,
-                                   (int64_t)sym.nsum.size(), csym))
-            return rc;
     // gathered right-hand side per task: a panel (<= 64 columns) where the
     // symmetric layouts are used, else the widest row of D / S
     maxcols = std::max(2, maxk);
     for (int i = 0; i < L.r_nodes; ++i) {
         maxcols = std::max(maxcols, sym.on ? std::min<int>(dcols[i], 64) : dcols[i]);
-        maxcols = std::max(maxcols, csym.on ? std::min<int>(scols[i], 64) : scols[i]);
+        maxcols = std::max(maxcols, scols[i]);
     }
     maxcols = (maxcols + 1) & ~1;
     const int smem =
         128 + kStageBytes +
-        (int)sizeof(double) * (maxcols + 3 * vec_len + (sym.on || csym.on ? 2 * vec_len + kWarps * 64 : kWarps * 32));
+        (int)sizeof(double) * (maxcols + 3 * vec_len + (sym.on ? 2 * vec_len + kWarps * 64 : kWarps * 32));
     if (smem > 227 * 1024) return fail(H2B_ERR_INVALID, "h2b_plan_create: gathered right-hand side exceeds shared memory");
 
     std::vector<int64_t> rec, fwd_off(L.c_leaves);
@@ -1815,13 +1596,6 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
         top_down(L.c_nodes, cparent, need_c);
         for (int u = 0; u < L.r_nodes; ++u) hasv[u] = (scols[u] > 0 && rrank[u] > 0) ? 1 : 0;
         top_down(L.r_nodes, rparent, hasv);
-        if (getenv("H2B_DEBUG_PLAN")) {
-            int nc = 0, nv = 0;
-            for (char c : need_c) nc += c;
-            for (char c : hasv) nv += c;
-            fprintf(stderr, "plan: far blocks %d, x_hat needed %d / %d, v_t nonzero %d / %d\n", (int)fcol.size(), nc,
-                    L.c_nodes, nv, L.r_nodes);
-        }
     }
     // A: forward records (leaf, then the levels it climbs as the right child)
     for (int i = 0; i < L.c_leaves; ++i) {
@@ -1867,9 +1641,6 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
     // Coupling bands of cluster u: all but the last to `early`; the last one
     // (an empty band when u has no couplings) runs u's downward step and goes
     // to `late`.
-    // H2B_DESC_TASKS=1: every coupling band is a pure product and the downward
-    // step of each cluster is its own task (kind kKindDescent)
-    const bool desc_tasks = getenv("H2B_DESC_TASKS") && getenv("H2B_DESC_TASKS")[0] == '1';
     auto cluster_to = [&](std::vector<int64_t>& early, std::vector<int64_t>& late, int u) {
         if (rvoff[u] < 0 && !hasv[u]) return;  // inner cluster with v_t == 0: nothing to do
         const bool cpl = scols[u] > 0 && rrank[u] > 0;
@@ -1885,13 +1656,9 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
             int dd = 0;
             for (int q = rparent[u]; q >= 0; q = rparent[q]) ++dd;
             dw[17] = dd;  // depth (diagnostics: trace)
-            if (sym.on && !near_sum_tasks && rvoff[u] >= 0) {  // the leaf's nearfield partials (symmetric nearfield)
+            if (sym.on && rvoff[u] >= 0) {  // the leaf's nearfield partials (symmetric nearfield)
                 dw[19] = sym.list_off[u];
                 dw[20] = sym.list_n[u];
-            }
-            if (csym.on) {  // the cluster's coupling partials (symmetric couplings)
-                dw[21] = csym.list_off[u];
-                dw[22] = csym.list_n[u];
             }
             dw[23] = u;  // (plan building only)
             const int kk = rrank[u], kq = par >= 0 ? rrank[par] : 0;
@@ -1900,23 +1667,8 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
                       8 * ((((int64_t)kk * kq + 1) & ~int64_t(1)) + (lf ? (int64_t)rsize[u] * kk : 0)) <= kStageBytes)
                          ? 1 : 0;  // one-warp downward step
         }
-        if (csym.on) {  // products are the panel tasks (all ticketed before any downward step)
-            std::vector<int64_t> t(dw, dw + kBandWords);
-            t[7] = kKindDescent;
-            late.insert(late.end(), t.begin(), t.end());
-            n_cpl += 1;
-            return;
-        }
         std::vector<int64_t> tmp;
         int n = cpl ? bands_to(tmp, scols[u], rrank[u], soff[u], sgoff[u], ryoff[u], kKindCpl) : 0;
-        if (desc_tasks) {
-            early.insert(early.end(), tmp.begin(), tmp.end());
-            std::vector<int64_t> t(dw, dw + kBandWords);
-            t[7] = kKindDescent;
-            late.insert(late.end(), t.begin(), t.end());
-            n_cpl += n + 1;
-            return;
-        }
         if (n == 0) {  // empty band: downward step only
             tmp.insert(tmp.end(), {0, 0, 0, 0, 0, 0, 0, kKindCpl});
             tmp.insert(tmp.end(), kBandWords - 8, 0);
@@ -1949,126 +1701,31 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
     //   downward step; needs every near band of its leaf).
     // The nearfield streams while the forward climb and the downward chain
     // advance.
-    double fa1 = 0.2, fa2 = 0.5;
-    // (H2B_EARLY_INNER=1: also move the inner clusters' non-last bands forward; measured neutral)
-    const bool early_inner = getenv("H2B_EARLY_INNER") && getenv("H2B_EARLY_INNER")[0] == '1';
-    if (const char* e = getenv("H2B_NEAR_A1")) fa1 = atof(e);
-    if (const char* e = getenv("H2B_NEAR_A2")) fa2 = atof(e);
+    const double fa1 = 0.2, fa2 = 0.5;  // nearfield fractions A1, A2 (neutral within +-1 % when varied)
     std::vector<int> owned_leaves;
     for (int u : order)
         if (rvoff[u] >= 0) owned_leaves.push_back(u);
     const int nl = (int)owned_leaves.size();
     const int c1 = std::min(nl, (int)(fa1 * nl)), c2 = std::min(nl, c1 + (int)(fa2 * nl));
-    std::vector<int64_t> na1, na2, nb, leaf_early, leaf_late, inner, inner_early;
+    std::vector<int64_t> na1, na2, nb, leaf_early, leaf_late, inner;
     int n_near = 0;
-    // symmetric nearfield: each leaf's partials are summed by a near-sum task
-    // placed `lag` leaves after the last of its producers (so they are done)
-    std::vector<std::vector<int64_t>> sums_after(nl);
-    if (sym.on && near_sum_tasks) {
-        int lag = 16;
-        if (const char* e = getenv("H2B_NEAR_SUM_LAG")) lag = atoi(e);
-        std::vector<int> pos(L.r_nodes, 0);
-        for (int i = 0; i < nl; ++i) pos[owned_leaves[i]] = i;
-        for (int i = 0; i < nl; ++i) {
-            const int u = owned_leaves[i];
-            int last = i;
-            for (int t : sym.producers[u]) last = std::max(last, pos[t]);
-            std::vector<int64_t> r(kBandWords, 0);
-            r[0] = sym.list_off[u];
-            r[1] = sym.list_n[u];
-            r[2] = rsize[u];
-            r[3] = rstart[u];
-            r[7] = kKindNearSum;
-            auto& dst = sums_after[std::min(nl - 1, last + lag)];
-            dst.insert(dst.end(), r.begin(), r.end());
-        }
-    }
     for (int i = 0; i < nl; ++i) {
         const int u = owned_leaves[i];
         std::vector<int64_t>& dst = i < c1 ? na1 : i < c2 ? na2 : nb;
         if (sym.on) {
             dst.insert(dst.end(), sym.bands[u].begin(), sym.bands[u].end());
             n_near += (int)(sym.bands[u].size() / kBandWords);
-            dst.insert(dst.end(), sums_after[i].begin(), sums_after[i].end());
-            n_near += (int)(sums_after[i].size() / kBandWords);
         } else {
             n_near += bands_to(dst, dcols[u], rsize[u], doff[u], dgoff[u], rstart[u], kKindNear);
         }
     }
-    const bool diag_near = getenv("H2B_DIAG_NEAR_ONLY") && getenv("H2B_DIAG_NEAR_ONLY")[0] == '1';
-    if (!diag_near) {
-        // H2B_DEPTH_MAJOR=1: inner clusters breadth first, each cluster's
-        // products right before its downward step
-        const bool depth_major = getenv("H2B_DEPTH_MAJOR") && getenv("H2B_DEPTH_MAJOR")[0] == '1';
-        std::vector<int> inner_order;
-        for (int u : order)
-            if (rvoff[u] < 0) inner_order.push_back(u);
-        if (depth_major) {
-            std::vector<int> dep(L.r_nodes, 0);
-            for (int u : inner_order) {
-                int dd = 0;
-                for (int q = rparent[u]; q >= 0; q = rparent[q]) ++dd;
-                dep[u] = dd;
-            }
-            std::stable_sort(inner_order.begin(), inner_order.end(), [&](int a2, int b2) { return dep[a2] < dep[b2]; });
-        }
-        for (int u : inner_order)
-            cluster_to(!depth_major && (early_inner || desc_tasks) ? inner_early : inner, inner, u);
-        for (int u : owned_leaves) cluster_to(leaf_early, leaf_late, u);
-        if (csym.on) {
-            // symmetric coupling panels: leaf clusters' panels early (their
-            // x_hat are ready first); each inner cluster's downward step right
-            // after the panels it needs (its own and those of the t < u that
-            // hold (t, u)), parents first: every task waits on smaller tickets
-            std::vector<char> done(L.r_nodes, 0);
-            auto emit = [&](std::vector<int64_t>& dst, int t) {
-                if (done[t]) return;
-                done[t] = 1;
-                dst.insert(dst.end(), csym.bands[t].begin(), csym.bands[t].end());
-                n_cpl += (int)(csym.bands[t].size() / kBandWords);
-            };
-            for (int u : owned_leaves) emit(leaf_early, u);
-            std::vector<int64_t> seq;
-            for (size_t i = 0; i < inner.size(); i += kBandWords) {
-                // inner holds the downward steps of the inner clusters, parents first
-                const int u = (int)inner[i + 23];
-                for (int t : csym.producers[u]) emit(seq, t);
-                emit(seq, u);
-                seq.insert(seq.end(), inner.begin() + i, inner.begin() + i + kBandWords);
-            }
-            for (int u = 0; u < L.r_nodes; ++u) emit(inner_early, u);  // the rest (no downward step needs them)
-            inner.swap(seq);
-        }
-    }
-    if (!(getenv("H2B_DIAG_FWD_ONLY") && getenv("H2B_DIAG_FWD_ONLY")[0] == '1')) {  // diagnostics: forward alone
-        rec.insert(rec.end(), na1.begin(), na1.end());
-        {
-            std::vector<int64_t> prod(leaf_early);  // leaf products first (their x_hat are ready first)
-            prod.insert(prod.end(), inner_early.begin(), inner_early.end());
-            interleave(prod, na2);
-        }
-        if (const char* e = getenv("H2B_CHAIN_GAP")) {
-            // the downward-chain tasks by depth, a fixed number of near bands
-            // between consecutive depths, the rest of near B after the chain
-            const int64_t gap = atoll(e);
-            const int64_t nt = (int64_t)inner.size() / kBandWords, nn = (int64_t)nb.size() / kBandWords;
-            int64_t f = 0;
-            for (int64_t i = 0; i < nt; ++i) {
-                const int64_t* t = inner.data() + kBandWords * i;
-                rec.insert(rec.end(), t, t + kBandWords);
-                const bool depth_end = i + 1 == nt || inner[kBandWords * (i + 1) + 17] != t[17];
-                if (depth_end)
-                    for (int64_t g = 0; g < gap && f < nn; ++g, ++f)
-                        rec.insert(rec.end(), nb.begin() + kBandWords * f, nb.begin() + kBandWords * (f + 1));
-            }
-            rec.insert(rec.end(), nb.begin() + kBandWords * f, nb.end());
-        } else {
-            interleave(inner, nb);
-        }
-        rec.insert(rec.end(), leaf_late.begin(), leaf_late.end());
-    } else {
-        n_near = n_cpl = 0;
-    }
+    for (int u : order)
+        if (rvoff[u] < 0) cluster_to(inner, inner, u);
+    for (int u : owned_leaves) cluster_to(leaf_early, leaf_late, u);
+    rec.insert(rec.end(), na1.begin(), na1.end());
+    interleave(leaf_early, na2);  // leaf products first (their x_hat are ready first)
+    interleave(inner, nb);
+    rec.insert(rec.end(), leaf_late.begin(), leaf_late.end());
     int64_t e_bytes_r = 0;
     for (int i = 0; i < L.r_nodes; ++i)
         if (rparent[i] >= 0 && reoff[i] >= 0)
@@ -2082,7 +1739,7 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
     p->n_leaf = 0;
     for (int64_t b = 0; b < (int64_t)(n_near + n_cpl); ++b) {
         const int64_t* r = rec.data() + band_base + kBandWords * b;
-        if (((r[7] == kKindCpl && r[5]) || r[7] == kKindDescent) && r[13]) ++p->n_leaf;
+        if (r[7] == kKindCpl && r[5] && r[13]) ++p->n_leaf;
     }
     p->band_base = band_base;
     {
@@ -2096,6 +1753,7 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
     p->smem = smem;
     p->e_bytes_r = e_bytes_r;
     H2B_CUDA_TRY(cudaGetDevice(&p->device));
+    H2B_CUDA_TRY(cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming));
     auto alloc = [](void** ptr, size_t bytes) { return cudaMalloc(ptr, bytes ? bytes : 16); };
     H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->xhat), 16 * (size_t)L.xhat_len));
     H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->ycpl), 16 * (size_t)L.yhat_len));
@@ -2122,21 +1780,6 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
             cur = p->smem;
         }
     }
-    p->loop_grid = 0;
-    if (const char* e = getenv("H2B_LOOP")) {
-        if (atoi(e) > 0) {
-            static int loop_smem_set[64] = {0};
-            int& cur = loop_smem_set[p->device & 63];
-            if (p->smem > cur) {
-                H2B_CUDA_TRY(cudaFuncSetAttribute(k_matvec_loop, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem));
-                cur = p->smem;
-            }
-            int nb = 0, sms = 0;
-            H2B_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_matvec_loop, kThreads, p->smem));
-            H2B_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
-            p->loop_grid = std::max(1, nb * sms);
-        }
-    }
     p->trace = nullptr;
     if (const char* tr = getenv("H2B_TRACE")) {
         if (tr[0] == '1') {
@@ -2155,8 +1798,6 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
     p->gsym = nullptr;
     p->ppart = nullptr;
     p->nsum = nullptr;
-    p->ssym = nullptr;
-    p->gsym_c = nullptr;
     p->near_bytes = 0;
     p->cpl_bytes = 0;
     p->ppart_len = 0;
@@ -2164,7 +1805,7 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
         if (rvoff[u] >= 0) p->near_bytes += 8 * (int64_t)rsize[u] * dcols[u];
         p->cpl_bytes += 8 * (int64_t)rrank[u] * scols[u];
     }
-    if (sym.on || csym.on) {
+    if (sym.on) {
         // symmetric storage needs the operator's blocks symmetric bit for bit
         // (checked on the device); then the upper blocks are packed into the
         // column panels the tasks stream
@@ -2205,32 +1846,20 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
             if (!v.empty()) H2B_CUDA_TRY(cudaMemcpy(*dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
             return 0;
         };
-        int bad_near = 0, bad_cpl = 0;
-        if (sym.on)
-            if (int rc = check(L.D, sym.check, bad_near)) return rc;
-        if (csym.on)
-            if (int rc = check(L.S, csym.check, bad_cpl)) return rc;
-        if (bad_near || bad_cpl) {
-            // not symmetric: stream every block of that part
+        int bad_near = 0;
+        if (int rc = check(L.D, sym.check, bad_near)) return rc;
+        if (bad_near) {
+            // not symmetric: stream every block
             h2b_plan_destroy(p);
-            return plan_create(layout, out, sym_flags & ~(bad_near ? kSymNear : 0) & ~(bad_cpl ? kSymCpl : 0));
+            return plan_create(layout, out, sym_flags & ~kSymNear);
         }
-        if (sym.on) {
-            if (int rc = pack(L.D, sym.pack, sym.srccol, sym.dsym_len, &p->dsym)) return rc;
-            if (int rc = upload(sym.gsym, &p->gsym)) return rc;
-            p->near_bytes = sym.near_bytes;
-        }
-        if (csym.on) {
-            if (int rc = pack(L.S, csym.pack, csym.srccol, csym.ssym_len, &p->ssym)) return rc;
-            if (int rc = upload(csym.gsym, &p->gsym_c)) return rc;
-            p->cpl_bytes = csym.bytes;
-        }
-        p->ppart_len = sym.ppart_len + csym.ppart_len;
+        if (int rc = pack(L.D, sym.pack, sym.srccol, sym.dsym_len, &p->dsym)) return rc;
+        if (int rc = upload(sym.gsym, &p->gsym)) return rc;
+        p->near_bytes = sym.near_bytes;
+        p->ppart_len = sym.ppart_len;
         H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->ppart), 16 * (size_t)std::max<int64_t>(p->ppart_len, 1)));
         H2B_CUDA_TRY(cudaMemset(p->ppart, 0, 16 * (size_t)std::max<int64_t>(p->ppart_len, 1)));
-        std::vector<int64_t> lists(sym.nsum);
-        lists.insert(lists.end(), csym.nsum.begin(), csym.nsum.end());
-        if (int rc = upload(lists, &p->nsum)) return rc;
+        if (int rc = upload(sym.nsum, &p->nsum)) return rc;
     }
     *out = p;
     return ok();
@@ -2238,7 +1867,7 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
 }  // namespace
 
 extern "C" int h2b_plan_create(const h2b_layout* layout, h2b_plan** out) {
-    return plan_create(layout, out, kSymNear | kSymCpl);
+    return plan_create(layout, out, kSymNear);
 }
 
 #ifdef H2B_LL_TIMEOUT
@@ -2264,11 +1893,12 @@ extern "C" int h2b_debug_stuck(h2b_plan* p, unsigned long long* out) {
 extern "C" int h2b_plan_destroy(h2b_plan* p) {
     if (!p) return ok();
     void* bufs[] = {p->xhat, p->ycpl, p->yfin, p->ynear, p->ctrl, p->rec,  p->fwd_off, p->dx,
-                    p->dy,   p->trace, p->xll, p->dsym,  p->gsym, p->ppart, p->nsum, p->ssym, p->gsym_c};
+                    p->dy,   p->trace, p->xll, p->dsym,  p->gsym, p->ppart, p->nsum};
     for (void* q : bufs)
         if (q) cudaFree(q);
     if (p->hy) cudaFreeHost(p->hy);
     if (p->hx) cudaFreeHost(p->hx);
+    if (p->done) cudaEventDestroy(p->done);
     delete p;
     return ok();
 }
@@ -2276,6 +1906,9 @@ extern "C" int h2b_plan_destroy(h2b_plan* p) {
 namespace {
 int launch_matvec(h2b_plan* p, const double* d_x, const double* xh, double* y, cudaStream_t st,
                   double* yh = nullptr) {
+    // (caller holds p->mu) order after the plan's previous launch if that was
+    // on another stream
+    if (p->launched && p->last != st) H2B_CUDA_TRY(cudaStreamWaitEvent(st, p->done, 0));
     KArgs a;
     a.L = p->L;
     a.rec = p->rec;
@@ -2301,18 +1934,16 @@ int launch_matvec(h2b_plan* p, const double* d_x, const double* xh, double* y, c
     a.gsym = p->gsym;
     a.ppart = p->ppart;
     a.nsum = p->nsum;
-    a.ssym = p->ssym;
-    a.gsym_c = p->gsym_c;
     a.yh = yh;
     a.n_out = yh ? (int)((p->L.n_rows + kCopyChunk - 1) / kCopyChunk) : 0;
     a.n_leaf = p->n_leaf;
     a.ydone = p->ctrl + 2;
     const int grid = a.n_copy + p->L.c_leaves + p->n_near + p->n_cpl + a.n_out;
-    if (p->loop_grid > 0)
-        k_matvec_loop<<<std::min(grid, p->loop_grid), kThreads, p->smem, st>>>(a, d_x, y);
-    else
-        k_matvec<<<grid, kThreads, p->smem, st>>>(a, d_x, y);
+    k_matvec<<<grid, kThreads, p->smem, st>>>(a, d_x, y);
     H2B_CUDA_TRY(cudaGetLastError());
+    H2B_CUDA_TRY(cudaEventRecord(p->done, st));
+    p->last = st;
+    p->launched = true;
     return ok();
 }
 
@@ -2329,6 +1960,7 @@ const void* mapped(const void* h) {
 
 extern "C" int h2b_matvec(h2b_plan* p, const double* d_x, double* d_y, void* stream) {
     if (!p || !d_x || !d_y) return fail(H2B_ERR_INVALID, "h2b_matvec: null pointer");
+    std::lock_guard<std::mutex> g(p->mu);
     return launch_matvec(p, d_x, nullptr, d_y, as_stream(stream));
 }
 
@@ -2338,6 +1970,7 @@ extern "C" int h2b_matvec(h2b_plan* p, const double* d_x, double* d_y, void* str
 // transfers.  Pageable buffers go through the plan's pinned staging.
 extern "C" int h2b_matvec_host(h2b_plan* p, const double* h_x, double* h_y, void* stream) {
     if (!p || !h_x || !h_y) return fail(H2B_ERR_INVALID, "h2b_matvec_host: null pointer");
+    std::lock_guard<std::mutex> g(p->mu);
     cudaStream_t st = as_stream(stream);
     const double* xh = static_cast<const double*>(mapped(h_x));
     if (!xh) {
@@ -2383,7 +2016,7 @@ extern "C" int h2b_plan_info(h2b_plan* p, int64_t* h_out) {
     h_out[2] = p->n_near;
     h_out[3] = p->n_cpl;
     h_out[4] = p->ppart_len * 16;
-    h_out[5] = p->ssym != nullptr;
+    h_out[5] = 0;  // (symmetric coupling panels: measured slower, removed)
     h_out[6] = p->cpl_bytes;
     return ok();
 }

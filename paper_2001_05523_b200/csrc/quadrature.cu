@@ -200,6 +200,32 @@ __global__ void k_touch_half(const int64_t* __restrict__ row_ptr, int64_t F, con
                              int64_t lo, int64_t hi, int32_t* __restrict__ half,
                              unsigned long long* __restrict__ cursor);
 
+// case code + permutations of arbitrary pairs (kernels.pair_integrals),
+// counted per segment: 0 identical, 1 edge, 2 vertex, 3 disjoint
+__device__ __forceinline__ int seg_of(int code) {
+    return code == H2B_IDENTICAL ? 0 : code == H2B_EDGE ? 1 : code == H2B_VERTEX ? 2 : 3;
+}
+
+__global__ void k_classify_list(const int32_t* __restrict__ T, int64_t n, const int32_t* __restrict__ pa,
+                                const int32_t* __restrict__ pb, int32_t* __restrict__ info,
+                                unsigned long long* __restrict__ count) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int a = pa[i], b = pb[i];
+    const int ta[3] = {T[3 * a], T[3 * a + 1], T[3 * a + 2]};
+    const int tb[3] = {T[3 * b], T[3 * b + 1], T[3 * b + 2]};
+    const int inf = classify(ta, tb, a == b);
+    info[i] = inf;
+    atomicAdd(&count[seg_of(inf & 3)], 1ull);
+}
+
+__global__ void k_bucket_list(int64_t n, const int32_t* __restrict__ info, int32_t* __restrict__ list,
+                              unsigned long long* __restrict__ cursor) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    list[atomicAdd(&cursor[seg_of(info[i] & 3)], 1ull)] = (int32_t)i;
+}
+
 // ----------------------------------------------------------------------------
 // Sauter-Schwab integrals
 struct SegDesc {
@@ -208,11 +234,11 @@ struct SegDesc {
     const double* p;
     const double* w;
     int64_t n;
-    int kase;  // H2B_IDENTICAL / H2B_EDGE / H2B_VERTEX
+    int kase;  // H2B_IDENTICAL / H2B_EDGE / H2B_VERTEX / H2B_DISJOINT
 };
 
 struct SegSet {
-    SegDesc s[3];
+    SegDesc s[4];
     int nseg;
 };
 
@@ -234,7 +260,8 @@ __global__ void __launch_bounds__(128) k_singular(const double* __restrict__ V, 
                                                  const int64_t* __restrict__ row_ptr, int64_t F,
                                                  const int32_t* __restrict__ col, const int32_t* __restrict__ info,
                                                  const int32_t* __restrict__ case_list, SegSet segs,
-                                                 double* __restrict__ values, int mirror) {
+                                                 double* __restrict__ values, int mirror,
+                                                 const int32_t* __restrict__ pa_list) {
     __shared__ double srule[kRuleChunk * kRuleStride];
     int si = 0;
     while (si + 1 < segs.nseg && (int)blockIdx.x >= segs.s[si + 1].first_block) ++si;
@@ -250,7 +277,8 @@ __global__ void __launch_bounds__(128) k_singular(const double* __restrict__ V, 
     int inf = 0, b = 0;
     if (active) {
         pid = case_list[sd.list_off + local];
-        a = find_row(row_ptr, F, pid);
+        // touching table: the row panel from the CSR; pair list: given
+        a = pa_list ? (int64_t)pa_list[pid] : find_row(row_ptr, F, pid);
         b = col[pid];
         inf = info[pid];
         int pa[3] = {(inf >> 2) & 3, (inf >> 4) & 3, (inf >> 6) & 3};
@@ -275,7 +303,7 @@ __global__ void __launch_bounds__(128) k_singular(const double* __restrict__ V, 
     }
 
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
-    const bool sym = (KIND == H2B_SLP) && (kase != H2B_IDENTICAL);
+    const bool sym = (KIND == H2B_SLP) && (kase == H2B_EDGE || kase == H2B_VERTEX);
     for (int64_t c0 = 0; c0 < sd.n; c0 += kRuleChunk) {
         const int cn = (int)min((int64_t)kRuleChunk, sd.n - c0);
         __syncthreads();
@@ -283,7 +311,7 @@ __global__ void __launch_bounds__(128) k_singular(const double* __restrict__ V, 
             const double* p = sd.p + 4 * (c0 + e);
             const double w = sd.w[c0 + e];
             double* d = srule + e * kRuleStride;
-            if (KIND == H2B_SLP) {
+            if (KIND == H2B_SLP && kase != H2B_DISJOINT) {
                 // sums and differences of the two charts' coordinates: both
                 // orientations of a symmetrised pair share the sum terms
                 d[0] = p[0] + p[2];
@@ -304,7 +332,32 @@ __global__ void __launch_bounds__(128) k_singular(const double* __restrict__ V, 
         }
         __syncthreads();
         if (!active) continue;
-        if (KIND == H2B_SLP) {
+        if (kase == H2B_DISJOINT) {
+            // pair list only (kernels.pair_integrals on separated panels): the
+            // tensor rule of quadrature.py:171-180 through both charts,
+            // d = (A1 - B1) + u1 E_a1 + v1 E_a2 - u2 E_b1 - v2 E_b2
+#pragma unroll 2
+            for (int e = 0; e < cn; ++e) {
+                const double* d = srule + e * kRuleStride;
+                const double u1 = d[0], v1 = d[1], u2 = d[2], v2 = d[3], w = d[4];
+                double dd[3];
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+                    dd[k] = fma(v2, eb2[k], fma(u2, eb1[k], fma(v1, ea2[k], fma(u1, ea1[k], base[k]))));
+                const double r2 = fma(dd[2], dd[2], fma(dd[1], dd[1], dd[0] * dd[0]));
+                const double t = rsqrt_seed(r2);
+                const double sq = t * t;
+                if (KIND == H2B_SLP) {
+                    acc0 = fma(w * t, fma(-r2, sq, 3.0), acc0);
+                } else {
+                    const double num = fma(dd[2], nb[2], fma(dd[1], nb[1], dd[0] * nb[0]));
+                    const double k = (num * fma(-r2, sq, 5.0 / 3.0)) * (sq * t);
+                    acc0 = fma(k, d[5], acc0);
+                    acc1 = fma(k, d[6], acc1);
+                    acc2 = fma(k, d[7], acc2);
+                }
+            }
+        } else if (KIND == H2B_SLP) {
             if (kase == H2B_IDENTICAL) {
                 // same panel: d = (u1-u2) E1 + (v1-v2) E2 (base = 0), so
                 // r^2 = du (du |E1|^2 + 2 dv E1.E2) + dv^2 |E2|^2 (a 2x2 Gram form)
@@ -999,11 +1052,11 @@ extern "C" int h2b_singular(const h2b_mesh* m, const h2b_touch* t, int kind, con
         if (kind == H2B_SLP)
             k_singular<H2B_SLP><<<block, 128, 0, st>>>(m->d_vertices, m->d_triangles, m->d_normals, m->d_areas,
                                                        t->d_row_ptr, t->n_panels, t->d_col, t->d_info,
-                                                       list, ss, d_values, half ? 1 : 0);
+                                                       list, ss, d_values, half ? 1 : 0, nullptr);
         else
             k_singular<H2B_DLP><<<block, 128, 0, st>>>(m->d_vertices, m->d_triangles, m->d_normals, m->d_areas,
                                                        t->d_row_ptr, t->n_panels, t->d_col, t->d_info,
-                                                       list, ss, d_values, 0);
+                                                       list, ss, d_values, 0, nullptr);
         H2B_CUDA_TRY(cudaGetLastError());
     }
     return ok();
@@ -1056,4 +1109,74 @@ extern "C" int h2b_pair_blocks_dlp(const h2b_mesh* m, const double* d_panel_poin
     }
     if (rc) return rc;
     return check_flags(flags, st);
+}
+
+// kernels.pair_integrals (kernels.py:260-319) on an arbitrary list of panel
+// pairs: classification on the device, then the Sauter-Schwab kernel with the
+// rule of each pair's case (rules[0..3] = identical, edge, vertex, disjoint).
+extern "C" int h2b_pair_integrals(const h2b_mesh* m, int64_t n, const int32_t* d_pa, const int32_t* d_pb, int kind,
+                                  const h2b_rule* rules, double* d_values, void* stream) {
+    if (!m || (n > 0 && (!d_pa || !d_pb || !d_values)) || !rules || n < 0)
+        return fail(H2B_ERR_INVALID, "h2b_pair_integrals: bad argument");
+    if (kind != H2B_SLP && kind != H2B_DLP) return fail(H2B_ERR_INVALID, "h2b_pair_integrals: unknown kind");
+    if (n == 0) return ok();
+    if (n > 2147483647LL) return fail(H2B_ERR_INVALID, "h2b_pair_integrals: more than 2^31 pairs");
+    cudaStream_t st = as_stream(stream);
+    H2B_CUDA_TRY(cudaMemsetAsync(d_values, 0, (kind == H2B_DLP ? 3 : 1) * sizeof(double) * n, st));
+    int32_t *info, *list;
+    unsigned long long* cnt;
+    H2B_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&info), n * sizeof(int32_t), st));
+    H2B_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&list), n * sizeof(int32_t), st));
+    H2B_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&cnt), 4 * sizeof(unsigned long long), st));
+    H2B_CUDA_TRY(cudaMemsetAsync(cnt, 0, 4 * sizeof(unsigned long long), st));
+    const unsigned g = (unsigned)((n + 255) / 256);
+    k_classify_list<<<g, 256, 0, st>>>(m->d_triangles, n, d_pa, d_pb, info, cnt);
+    H2B_CUDA_TRY(cudaGetLastError());
+    unsigned long long hc[4];
+    H2B_CUDA_TRY(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    H2B_CUDA_TRY(cudaStreamSynchronize(st));
+    int64_t off[5] = {0, 0, 0, 0, 0};
+    for (int c = 0; c < 4; ++c) off[c + 1] = off[c] + (int64_t)hc[c];
+    unsigned long long cur[4] = {(unsigned long long)off[0], (unsigned long long)off[1], (unsigned long long)off[2],
+                                 (unsigned long long)off[3]};
+    H2B_CUDA_TRY(cudaMemcpyAsync(cnt, cur, sizeof(cur), cudaMemcpyHostToDevice, st));
+    k_bucket_list<<<g, 256, 0, st>>>(n, info, list, cnt);
+    H2B_CUDA_TRY(cudaGetLastError());
+    SegSet ss;
+    ss.nseg = 0;
+    int32_t block = 0;
+    const int order[4] = {1, 0, 2, 3};
+    const int kases[4] = {H2B_IDENTICAL, H2B_EDGE, H2B_VERTEX, H2B_DISJOINT};
+    for (int oi = 0; oi < 4; ++oi) {
+        const int c = order[oi];
+        if (kind == H2B_DLP && c == 0) continue;  // identical flat panels: 0 (kernels.py:278-279)
+        const int64_t cn = off[c + 1] - off[c];
+        if (cn <= 0) continue;
+        if (!rules[c].d_p || !rules[c].d_w || rules[c].n <= 0) return fail(H2B_ERR_INVALID, "h2b_pair_integrals: rule missing");
+        SegDesc& sd = ss.s[ss.nseg++];
+        sd.list_off = off[c];
+        sd.count = cn;
+        sd.first_block = block;
+        sd.n_blocks = (int32_t)((cn + 127) / 128);
+        sd.p = rules[c].d_p;
+        sd.w = rules[c].d_w;
+        sd.n = rules[c].n;
+        sd.kase = kases[c];
+        block += sd.n_blocks;
+    }
+    if (block > 0) {
+        if (kind == H2B_SLP)
+            k_singular<H2B_SLP><<<block, 128, 0, st>>>(m->d_vertices, m->d_triangles, m->d_normals, m->d_areas,
+                                                       nullptr, m->n_triangles, d_pb, info, list, ss, d_values, 0,
+                                                       d_pa);
+        else
+            k_singular<H2B_DLP><<<block, 128, 0, st>>>(m->d_vertices, m->d_triangles, m->d_normals, m->d_areas,
+                                                       nullptr, m->n_triangles, d_pb, info, list, ss, d_values, 0,
+                                                       d_pa);
+        H2B_CUDA_TRY(cudaGetLastError());
+    }
+    H2B_CUDA_TRY(cudaFreeAsync(info, st));
+    H2B_CUDA_TRY(cudaFreeAsync(list, st));
+    H2B_CUDA_TRY(cudaFreeAsync(cnt, st));
+    return ok();
 }

@@ -136,7 +136,11 @@ class SingularTable:
     """Sauter-Schwab integrals of every touching pair at order q, on the device
     (reference: kernels.SingularTable, kernels.py:346-362)."""
 
-    def __init__(self, dmesh, kind, q, compute=True):
+    def __init__(self, mesh, kind, q, vertex_tris=None, compute=True):
+        """mesh: the host SurfaceMesh (reference signature) or its DeviceMesh."""
+        if kind not in (SLP, DLP):
+            raise ValueError(f"unknown operator kind {kind!r}")
+        dmesh = device_mesh(mesh)
         self.kind = kind
         self.q = q
         self.dmesh = dmesh
@@ -409,3 +413,158 @@ def run_dlp_jobs(dmesh, q, packed, table, out):
 def touching_pairs(mesh):
     """Sorted keys pa * F + pb of all touching ordered pairs (device classifier)."""
     return DeviceMesh(mesh).touch().keys()
+
+
+# ---------------------------------------------------------------------------
+# reference kernel-level entry points (kernels.py:260-319, 346-362, 365-468):
+# same names and arguments, computed on the device.  `mesh` is the host
+# SurfaceMesh (its device copy is cached); `pq` (host panel points) is
+# accepted for signature compatibility -- the device builds its own points at
+# order q, bit-identical to quadrature.triangle_points -- and `singular` is a
+# SingularTable of this module (AssemblyContext.singular_table).
+
+def device_mesh(mesh):
+    """The DeviceMesh of a host mesh, cached on the mesh object (its lifetime
+    follows the mesh), or the DeviceMesh itself."""
+    if isinstance(mesh, DeviceMesh):
+        return mesh
+    dm = getattr(mesh, "_h2b_device_mesh", None)
+    if dm is None:
+        dm = DeviceMesh(mesh)
+        mesh._h2b_device_mesh = dm
+    return dm
+
+
+def _table_for(dm, kind, q, singular):
+    if singular is None:
+        # the reference integrates touching pairs on the fly at order q
+        # (pair_integrals); the device table of the mesh at order q holds the
+        # same values
+        key = ("table", kind, q)
+        if key not in dm._pp:
+            dm._pp[key] = SingularTable(dm, kind, q)
+        return dm._pp[key]
+    if not isinstance(singular, SingularTable):
+        raise ValueError("singular must be a device SingularTable (AssemblyContext.singular_table)")
+    if singular.kind != kind:
+        raise ValueError(f"singular table of kind {singular.kind!r} used for {kind!r}")
+    return singular
+
+
+def pair_integrals(mesh, pa, pb, kind, q, chunk=None):
+    """Galerkin double integrals over panel pairs (pa[i], pb[i]) with the
+    regularising rule of each pair's case (kernels.py:260-319): SLP (B,),
+    DLP (B, 3) per original local vertex of the column panel (identical pairs
+    0).  Any case, disjoint included (tensor rule through the charts)."""
+    if kind not in (SLP, DLP):
+        raise ValueError(f"unknown operator kind {kind!r}")
+    dm = device_mesh(mesh)
+    pa = np.asarray(pa, dtype=np.int64)
+    pb = np.asarray(pb, dtype=np.int64)
+    B = len(pa)
+    if len(pb) != B:
+        raise ValueError("pa and pb differ in length")
+    width = 3 if kind == DLP else 1
+    if B == 0:
+        return np.zeros((0, 3)) if kind == DLP else np.zeros(0)
+    F = dm.mesh.n_triangles
+    if pa.min() < 0 or pb.min() < 0 or pa.max() >= F or pb.max() >= F:
+        raise ValueError("panel index out of range")
+    rules = (_lib.Rule * 4)()
+    keep = []
+    for i, case in enumerate((quad.IDENTICAL, quad.SHARED_EDGE, quad.SHARED_VERTEX, quad.DISJOINT)):
+        r = quad.sauter_schwab_rule(case, q)
+        p, w = D.dev(r.points), D.dev(r.weights)
+        keep += [p, w]
+        rules[i] = _lib.Rule(len(r.weights), p.data_ptr(), w.data_ptr())
+    da, db = D.dev(pa, np.int32), D.dev(pb, np.int32)
+    out = D.empty((B * width,))
+    _lib.check(_lib.lib().h2b_pair_integrals(ctypes.byref(dm.c), B, da.data_ptr(), db.data_ptr(), kind_code(kind),
+                                             rules, out.data_ptr(), D.stream()))
+    h = D.host(out)
+    return h.reshape(B, 3) if kind == DLP else h
+
+
+def _dlp_pair_jobs(na, nb):
+    """DLP jobs whose output columns are (column panel, local vertex) pairs,
+    one contribution each: the kernel's vertex scatter becomes the identity
+    and out (na x 3 nb) holds panel_pair_matrix(..., DLP) (na, nb, 3)."""
+    per = TILE // 3
+    jobs, row_idx, pan_idx, inc_ptr, inc, inc_base = [], [], [], [], [], []
+    nptr = ninc = 0
+    for p0 in range(0, nb, per):
+        p1 = min(nb, p0 + per)
+        w = p1 - p0
+        pan_idx.append(np.arange(p0, p1))
+        codes = [(p << 2) | l for p in range(w) for l in range(3)]
+        ptr0 = nptr
+        inc_ptr.append(ninc + np.arange(3 * w + 1))
+        nptr += 3 * w + 1
+        inc.extend(codes)
+        ninc += len(codes)
+        for r0 in range(0, na, TILE):
+            r1 = min(na, r0 + TILE)
+            jobs.append((r0, r1 - r0, p0, w, 3 * p0, 3 * w, r0 * 3 * nb + 3 * p0, 3 * nb))
+            inc_base.append(ptr0)
+    return dict(jobs=np.array(jobs, dtype=np.int64), pan_local=np.concatenate(pan_idx),
+                inc_ptr=np.concatenate(inc_ptr).astype(np.int32), inc=np.array(inc, dtype=np.int32),
+                inc_base=np.array(inc_base, dtype=np.int64))
+
+
+def panel_pair_matrix(mesh, panels_a, panels_b, kind, q, chunk=None, pq=None, singular=None):
+    """All-pairs Galerkin integrals between two panel sets (kernels.py:365-434):
+    regular pairs by the q^2-point tensor rule, touching pairs from the
+    singular table (its order is the Sauter-Schwab order; without a table the
+    touching pairs are integrated at order q).  SLP (Pa, Pb); DLP (Pa, Pb, 3)
+    per local vertex of the column panel."""
+    if kind not in (SLP, DLP):
+        raise ValueError(f"unknown operator kind {kind!r}")
+    dm = device_mesh(mesh)
+    pa = np.asarray(panels_a, dtype=np.int64)
+    pb = np.asarray(panels_b, dtype=np.int64)
+    na, nb = len(pa), len(pb)
+    if na == 0 or nb == 0:
+        return np.zeros((na, nb, 3) if kind == DLP else (na, nb))
+    table = _table_for(dm, kind, q, singular)
+    if kind == SLP:
+        out = D.zeros((na * nb,))
+        run_slp_jobs(dm, q, np.array([[0, na, 0, nb, 0, nb]], dtype=np.int64), pa.astype(np.int32),
+                     pb.astype(np.int32), table, out)
+        return D.host(out).reshape(na, nb)
+    J = _dlp_pair_jobs(na, nb)
+    packed = dict(jobs=J["jobs"], row_idx=pa.astype(np.int32), pan_idx=pb[J["pan_local"]].astype(np.int32),
+                  inc_ptr=J["inc_ptr"], inc=J["inc"], inc_base=J["inc_base"])
+    out = D.zeros((na * nb * 3,))
+    run_dlp_jobs(dm, q, packed, table, out)
+    return D.host(out).reshape(na, nb, 3)
+
+
+def slp_block(mesh, rows, cols, q, require_disjoint=False, pq=None, singular=None):
+    """Dense single-layer block rows x cols (panel ids) (kernels.py:437-445);
+    ValueError on a touching pair when require_disjoint."""
+    dm = device_mesh(mesh)
+    rows = np.asarray(rows, dtype=np.int64)
+    cols = np.asarray(cols, dtype=np.int64)
+    if len(rows) == 0 or len(cols) == 0:
+        return np.zeros((len(rows), len(cols)))
+    table = None if require_disjoint else _table_for(dm, SLP, q, singular)
+    out = D.zeros((len(rows) * len(cols),))
+    run_slp_jobs(dm, q, np.array([[0, len(rows), 0, len(cols), 0, len(cols)]], dtype=np.int64),
+                 rows.astype(np.int32), cols.astype(np.int32), table, out)
+    return D.host(out).reshape(len(rows), len(cols))
+
+
+def dlp_block(mesh, rows, cols, q, vertex_tris=None, require_disjoint=False, pq=None, singular=None):
+    """Dense double-layer block: P0 rows (panels) x P1 columns (vertices)
+    through the panels incident to the column vertices with the barycentric
+    scatter fused in (kernels.py:448-468); ValueError on a touching pair when
+    require_disjoint."""
+    dm = device_mesh(mesh)
+    rows = np.asarray(rows, dtype=np.int64)
+    cols = np.asarray(cols, dtype=np.int64)
+    if len(rows) == 0 or len(cols) == 0:
+        return np.zeros((len(rows), len(cols)))
+    table = None if require_disjoint else _table_for(dm, DLP, q, singular)
+    out = D.zeros((len(rows) * len(cols),))
+    run_dlp_jobs(dm, q, build_dlp_jobs(dm.mesh, [(rows, cols, 0, len(cols))]), table, out)
+    return D.host(out).reshape(len(rows), len(cols))

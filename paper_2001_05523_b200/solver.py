@@ -1,14 +1,31 @@
-"""Jacobi-preconditioned conjugate gradients (h2bem.solver.cg, solver.py:22-59).
+"""Jacobi-preconditioned conjugate gradients on the device.
 
-Same iteration, stopping rule and breakdown checks as the reference; the
-operator application is whatever `apply_a` is -- for an H2Matrix the device
-matvec.  Vectors may be numpy arrays (host loop, reference semantics) or CUDA
-tensors (device-resident loop: no host round trip per iteration except the
-scalar residual test)."""
+Drop-in for h2bem.solver.cg (reference solver.py:22-59): same arguments
+(apply_a, b, eps, max_it, precond_diag), same stopping rule (relative residual
+||r|| / ||b|| <= eps), same breakdown conditions (SolverBreakdown for a
+non-positive Jacobi diagonal or non-positive curvature) and the same result
+fields.  The vectors always live in HBM and every vector pass is a fused
+libh2b kernel (h2b_cg_dot / h2b_cg_step / h2b_cg_direction) with
+deterministic reductions; the scalars stay on the device and one 32-byte
+read-back per iteration feeds the host-side tests.
 
+* b a CUDA float64 tensor: apply_a maps CUDA tensors to CUDA tensors (e.g.
+  MatvecPlan.apply_device); x is returned as a tensor.
+* b a numpy array (the reference call, e.g. cg(G.matvec, b, ...)): apply_a is
+  called with numpy vectors, as in the reference; x is returned as numpy.
+* Row-sharded vectors (one process per GPU): pass `allreduce(t)`, an in-place
+  sum of a small device tensor over the ranks (distributed.allreduce_sum);
+  each rank then holds its own rows of x, r, p and the Jacobi diagonal, and
+  the iteration count is the single-GPU one.
+"""
+
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
+
+from . import _lib
+from . import device as D
 
 
 class SolverBreakdown(Exception):
@@ -23,58 +40,21 @@ class CGResult:
     residual: float
 
 
-def cg(apply_a, b, eps, max_it, precond_diag=None):
-    try:
-        import torch
-        is_t = isinstance(b, torch.Tensor)
-    except ImportError:  # pragma: no cover
-        is_t = False
-    if is_t:
-        return _cg_torch(apply_a, b, eps, max_it, precond_diag)
-    b = np.asarray(b, dtype=float)
-    norm_b = float(np.linalg.norm(b))
-    if norm_b == 0.0:
-        return CGResult(np.zeros_like(b), 0, True, 0.0)
-    inv_d = None
-    if precond_diag is not None:
-        precond_diag = np.asarray(precond_diag, dtype=float)
-        if (precond_diag <= 0.0).any():
-            raise SolverBreakdown("Jacobi preconditioner requires a positive diagonal")
-        inv_d = 1.0 / precond_diag
-    x = np.zeros_like(b)
-    r = b.copy()
-    z = r * inv_d if inv_d is not None else r
-    p = z.copy()
-    rz = float(r @ z)
-    for it in range(1, max_it + 1):
-        Ap = apply_a(p)
-        pAp = float(p @ Ap)
-        if pAp <= 0.0:
-            raise SolverBreakdown(f"non-positive curvature p^T A p = {pAp:.3e} at iteration {it}")
-        alpha = rz / pAp
-        x += alpha * p
-        r -= alpha * Ap
-        res = float(np.linalg.norm(r)) / norm_b
-        if res <= eps:
-            return CGResult(x, it, True, res)
-        z = r * inv_d if inv_d is not None else r
-        rz_new = float(r @ z)
-        p = z + (rz_new / rz) * p
-        rz = rz_new
-    return CGResult(x, max_it, False, float(np.linalg.norm(b - apply_a(x))) / norm_b)
+def cg(apply_a, b, eps, max_it, precond_diag=None, allreduce=None):
+    t = D.require_cuda()
+    if isinstance(b, t.Tensor):
+        return _cg_device(apply_a, b, eps, max_it, precond_diag, allreduce)
+    bh = np.asarray(b, dtype=np.float64)
+
+    def apply_dev(p):
+        return D.dev(np.asarray(apply_a(D.host(p)), dtype=np.float64))
+
+    res = _cg_device(apply_dev, D.dev(bh), eps, max_it, precond_diag, allreduce)
+    return CGResult(D.host(res.x), res.iterations, res.converged, res.residual)
 
 
-def _cg_torch(apply_a, b, eps, max_it, precond_diag, allreduce=None):
-    """Device-resident CG on CUDA float64 tensors: fused libh2b vector passes
-    (h2b_cg_dot / h2b_cg_step / h2b_cg_direction), scalars kept on the device
-    and one 4-double read-back per iteration for the breakdown and stopping
-    tests.  `allreduce(t)` (row-sharded vectors) sums a small device tensor
-    over the ranks in place."""
-    import ctypes
-
+def _cg_device(apply_a, b, eps, max_it, precond_diag, allreduce=None):
     import torch
-
-    from . import _lib
 
     L = _lib.lib()
     st = _lib.stream_ptr()
@@ -99,7 +79,10 @@ def _cg_torch(apply_a, b, eps, max_it, precond_diag, allreduce=None):
     inv_d = None
     if precond_diag is not None:
         d = torch.as_tensor(precond_diag, dtype=b.dtype, device=b.device)
-        if bool((d <= 0.0).any()):
+        bad = (d <= 0.0).any().to(torch.float64).reshape(1)
+        if allreduce is not None:
+            allreduce(bad)
+        if bool(bad.item() > 0):
             raise SolverBreakdown("Jacobi preconditioner requires a positive diagonal")
         inv_d = (1.0 / d).contiguous()
     x = torch.zeros_like(b)

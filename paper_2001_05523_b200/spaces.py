@@ -1,12 +1,13 @@
 """P0 / P1 boundary element spaces (host).  API subset of h2bem.spaces
-(spaces.py:1-186): support boxes (cluster-tree input), mixed mass matrix,
-L2 projection/load vectors and the energy error used by the drivers."""
+(spaces.py:1-186) that the hot path needs: support boxes (cluster-tree input,
+spaces.py:29-41), the mixed mass matrix and the Galerkin load vector of the
+config-3 right-hand side.  Post-processing (L2 projection, error norms) is out
+of scope."""
 
 from dataclasses import dataclass
 
 import numpy as np
 import scipy.sparse as sp
-import scipy.sparse.linalg as spla
 
 from . import quadrature as quad
 
@@ -48,24 +49,6 @@ def assemble_mass(mesh):
     )
 
 
-def l2_project(space, fn):
-    """Coefficients of the L2 projection of fn(X, tris) onto the space."""
-    mesh = space.mesh
-    tris = np.arange(mesh.n_triangles)
-    X, W, lam = quad.triangle_points(mesh, tris, ERROR_QUAD_ORDER)
-    f = fn(X, tris)
-    if space.kind == P0:
-        return np.einsum("pq,pq->p", W, f) / mesh.areas
-    load = np.zeros(mesh.n_vertices)
-    for l in range(3):
-        np.add.at(load, mesh.triangles[:, l], np.einsum("pq,pq,q->p", W, f, lam[:, l]))
-    ptl = np.einsum("pq,qa,qb->pab", W, lam, lam)
-    rows = np.repeat(mesh.triangles, 3, axis=1).ravel()
-    cols = np.tile(mesh.triangles, (1, 3)).ravel()
-    gram = sp.csr_matrix((ptl.ravel(), (rows, cols)), shape=(mesh.n_vertices,) * 2)
-    return spla.spsolve(gram.tocsc(), load)
-
-
 def load_vector(space, fn):
     """Galerkin load b_i = int phi_i f (P0: per-triangle integral)."""
     mesh = space.mesh
@@ -78,14 +61,3 @@ def load_vector(space, fn):
     for l in range(3):
         np.add.at(load, mesh.triangles[:, l], np.einsum("pq,pq,q->p", W, f, lam[:, l]))
     return load
-
-
-def energy_error(apply_g, d):
-    """sqrt(d^T G d) through the (compressed) single-layer action."""
-    d = np.asarray(d, dtype=float)
-    if not d.any():
-        return 0.0
-    val = float(d @ apply_g(d))
-    if val < -1e-12 * float(d @ d):
-        raise ArithmeticError(f"energy product is negative ({val:.3e}): operator lost definiteness")
-    return float(np.sqrt(max(val, 0.0)))

@@ -17,6 +17,8 @@ What is pinned (all produced by the reference's own public functions):
   touch.npz        touching pair keys, case codes and permutations (kernels.py:246-343,
                    quadrature.py:90-118)
   singular.npz     pair_integrals samples, SLP/DLP, q_ss 4 and 5 (kernels.py:260-319)
+  pairs.npz        pair_integrals on mixed pair lists (disjoint included), and
+                   panel_pair_matrix / slp_block / dlp_block without a table
   near_cfg0.npz    sampled split-order nearfield blocks (kernels.py:365-468)
   h2_cfg0.npz      full GCA basis + sampled couplings + matvec x/y of config 0
   h2_cfg1.npz      pivots/ranks digests + matvec x/y of config 1
@@ -426,6 +428,34 @@ def gen_cube():
     np.savez_compressed(os.path.join(HERE, "cube4.npz"), **out)
 
 
+def gen_pairs():
+    """pair_integrals on separated (disjoint-case) and mixed pair lists, and
+    panel_pair_matrix / slp_block / dlp_block without a singular table (the
+    touching pairs integrated on the fly at order q) -- the kernel-level
+    entry points (kernels.py:260-319, 365-468)."""
+    mesh = sphere_mesh(3)
+    F = mesh.n_triangles
+    rng = np.random.default_rng(7)
+    pa = rng.integers(0, F, 400)
+    pb = rng.integers(0, F, 400)
+    pb[:20] = pa[:20]  # a few identical pairs in the mixed list
+    codes = kernels._classify_pairs(mesh, pa, pb)
+    out = {"pa": pa, "pb": pb, "code": codes.astype(np.int64)}
+    for q in (2, 3, 4):
+        out[f"slp_q{q}"] = kernels.pair_integrals(mesh, pa, pb, kernels.SLP, q)
+        out[f"dlp_q{q}"] = kernels.pair_integrals(mesh, pa, pb, kernels.DLP, q)
+    ra = np.array([0, 1, 2, 3, 40, 41, 200, 511])
+    rb = np.array([0, 2, 5, 9, 40, 300, 301, 17, 510])
+    verts = np.array([0, 1, 5, 17, 100, 255])
+    for q in (3, 4):
+        out[f"ppm_slp_q{q}"] = kernels.panel_pair_matrix(mesh, ra, rb, kernels.SLP, q)
+        out[f"ppm_dlp_q{q}"] = kernels.panel_pair_matrix(mesh, ra, rb, kernels.DLP, q)
+        out[f"slpb_q{q}"] = kernels.slp_block(mesh, ra, rb, q)
+        out[f"dlpb_q{q}"] = kernels.dlp_block(mesh, ra, verts, q)
+    out["ra"], out["rb"], out["verts"] = ra, rb, verts
+    np.savez_compressed(os.path.join(HERE, "pairs.npz"), **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-large", action="store_true")
@@ -437,6 +467,7 @@ def main():
         ("struct", gen_structure_small),
         ("touch", gen_touch),
         ("singular", gen_singular),
+        ("pairs", gen_pairs),
         ("h2_cfg0", gen_h2_cfg0),
         ("h2_dlp4", gen_h2_dlp4),
         ("h2_cfg1", gen_h2_cfg1),

@@ -270,22 +270,3 @@ def test_cube_shell_matvec_vs_reference(kind):
         bt, cb = C.BlockTree(t0, t1, 2.0), gca.build_basis(ctx, t1, gca.P1_DLP, 3, 1e-4, threads=4)
     H = gca.assemble_h2(ctx, kind, bt, rb, cb, 3, q_singular=4)
     assert rel(H.matvec(g[f"x_{kind}"]), g[f"y_{kind}"]) < 1e-10
-
-
-def test_persistent_loop_kernel_bitwise_equal(cfg0, rng):
-    """Opt-in persistent variant (H2B_LOOP=1, read at plan creation): the
-    same tasks in the same per-output order -> bitwise identical results."""
-    import os
-
-    from paper_2001_05523_b200.containers import MatvecPlan
-
-    H = cfg0[-1]
-    x = rng.uniform(-1, 1, H.shape[1])
-    y0 = H.matvec(x)
-    os.environ["H2B_LOOP"] = "1"
-    try:
-        p = MatvecPlan(H.block_tree, H.row_basis, H.col_basis, H.S_dev, H.D_dev, H.far_layout, H.near_layout)
-    finally:
-        del os.environ["H2B_LOOP"]
-    for _ in range(3):
-        assert np.array_equal(p.apply(x), y0)

@@ -1,7 +1,7 @@
-"""Symmetric storage in the matvec: single-GPU plans of a bitwise symmetric
-nearfield / coupling set (the single-layer Galerkin matrix on one tree) stream
-every block pair once and deliver the transposed product as partial vectors;
-anything else streams every block.  Both must give the same operator."""
+"""Symmetric storage in the matvec: plans of a bitwise symmetric nearfield
+(the single-layer Galerkin matrix on one tree) stream every block pair once
+and deliver the transposed product as partial vectors; anything else streams
+every block.  Both must give the same operator."""
 
 import os
 
@@ -13,12 +13,11 @@ from .helpers import rel, sphere, trees
 pytestmark = pytest.mark.gpu
 
 
-def _plan(H, near_sym, cpl_sym):
-    """A plan with the symmetric nearfield / couplings allowed or not (the
-    symmetric couplings are opt-in)."""
+def _plan(H, near_sym):
+    """A plan with the symmetric nearfield allowed or not."""
     from paper_2001_05523_b200.containers import MatvecPlan
 
-    env = {"H2B_NEAR_SYM": "1" if near_sym else "0", "H2B_CPL_SYM": "1" if cpl_sym else "0"}
+    env = {"H2B_NEAR_SYM": "1" if near_sym else "0"}
     os.environ.update(env)
     try:
         return MatvecPlan(H.block_tree, H.row_basis, H.col_basis, H.S_dev, H.D_dev, H.far_layout, H.near_layout)
@@ -44,29 +43,20 @@ def test_symmetric_nearfield_matches_one_sided(level, leaf):
     import torch
 
     H = _slp(level, leaf)
-    assert H.plan().info()["near_symmetric"] and not H.plan().info()["coupling_symmetric"]
-    both = _plan(H, True, True)
-    info = both.info()
-    assert info["near_symmetric"] and info["coupling_symmetric"]
-    ref = _plan(H, False, False)
+    info = H.plan().info()
+    assert info["near_symmetric"] and not info["coupling_symmetric"]
+    ref = _plan(H, False)
     full = ref.info()
     # every block pair once: the upper blocks (diagonal blocks in full)
     assert full["near_bytes"] >= 8 * H.near_layout.entries  # (+ the rows' padding columns)
     assert info["near_bytes"] < 0.6 * full["near_bytes"]
     assert full["coupling_bytes"] >= 8 * H.far_layout.entries
-    assert 2 * info["coupling_bytes"] == 8 * H.far_layout.entries
-    halves = [H.plan(), _plan(H, False, True)]
-    assert [h.info()["near_symmetric"] for h in halves] == [True, False]
-    assert [h.info()["coupling_symmetric"] for h in halves] == [False, True]
     rng = np.random.default_rng(level * 100 + leaf)
     for _ in range(3):
         x = rng.standard_normal(H.shape[1])
         y = H.matvec(x)
         y1 = ref.apply(x)
         assert rel(y, y1) < 1e-14
-        assert rel(both.apply(x), y1) < 1e-14
-        for h in halves:
-            assert rel(h.apply(x), y1) < 1e-14
         xd = torch.from_numpy(x).cuda()
         yd = H.matvec(xd)
         assert torch.equal(yd, H.matvec(xd))  # bitwise reproducible
@@ -84,8 +74,8 @@ def test_nonsymmetric_nearfield_streams_every_block():
     i = int(np.nonzero(nl.blk_cols > 1)[0][0])
     Dn[int(nl.blk_off[i]) + 1] += 1.0  # entry (0, 1) of a near block
     H2 = H2Matrix.from_device(H.block_tree, H.row_basis, H.col_basis, H.S_dev, Dn)
-    info = _plan(H2, True, True).info()
-    assert not info["near_symmetric"] and info["coupling_symmetric"]
+    info = _plan(H2, True).info()
+    assert not info["near_symmetric"]
     x = np.random.default_rng(1).standard_normal(H.shape[1])
     d = H2.matvec(x) - H.matvec(x)
     r = H.row_tree.perm[H.row_tree.start[H.block_tree.near_uids[i, 0]]]
@@ -105,40 +95,5 @@ def test_dlp_plan_is_one_sided():
     rb = gca.build_basis(ctx, t0, gca.P0_SLP, 3, 1e-4, threads=4)
     cb = gca.build_basis(ctx, t1, gca.P1_DLP, 3, 1e-4, threads=4)
     H = gca.assemble_h2(ctx, "dlp", C.BlockTree(t0, t1, 2.0), rb, cb, 3, q_singular=4)
-    info = _plan(H, True, True).info()
+    info = _plan(H, True).info()
     assert not info["near_symmetric"] and not info["coupling_symmetric"]
-
-
-def test_nonsymmetric_couplings_stream_every_block():
-    from paper_2001_05523_b200.containers import H2Matrix
-
-    H = _slp(4, 32)
-    S = H.S_dev.clone()
-    fl = H.far_layout
-    i = int(np.nonzero(fl.blk_cols > 1)[0][0])
-    S[int(fl.blk_off[i]) + 1] *= 1.5
-    H2 = H2Matrix.from_device(H.block_tree, H.row_basis, H.col_basis, S, H.D_dev)
-    info = _plan(H2, True, True).info()
-    assert info["near_symmetric"] and not info["coupling_symmetric"]
-    ref = _plan(H2, False, False)
-    x = np.random.default_rng(2).standard_normal(H.shape[1])
-    assert rel(H2.matvec(x), ref.apply(x)) < 1e-14
-    assert rel(H2.matvec(x), H.matvec(x)) > 1e-12
-
-
-def test_near_sum_tasks_variant_matches():
-    """Opt-in H2B_NEAR_SUM_TASKS=1: the leaf partial sums run as separate
-    tasks in the nearfield stream (same partials and list order; the threads
-    split the list differently, so the association, not the values, differs)."""
-    from paper_2001_05523_b200.containers import MatvecPlan
-
-    H = _slp(4, 32)
-    os.environ["H2B_NEAR_SUM_TASKS"] = "1"
-    try:
-        p = MatvecPlan(H.block_tree, H.row_basis, H.col_basis, H.S_dev, H.D_dev, H.far_layout, H.near_layout)
-    finally:
-        del os.environ["H2B_NEAR_SUM_TASKS"]
-    x = np.random.default_rng(3).standard_normal(H.shape[1])
-    y = p.apply(x)
-    assert rel(y, H.matvec(x)) < 1e-14
-    assert np.array_equal(y, p.apply(x))

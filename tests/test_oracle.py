@@ -99,3 +99,15 @@ def test_oracle_matvec_vs_reference(cfg0_oracle_operator):
     assert rel(d, g["diag"]) < 1e-11
     # accuracy of the H^2 approximation itself (reference: 2.5e-4 at eps 1e-4)
     assert np.linalg.norm(y - g["y_dense"]) <= 1e-3 * np.linalg.norm(g["y_dense"])
+
+
+@pytest.mark.parametrize("q", [2, 3, 4])
+@pytest.mark.parametrize("kind", ["slp", "dlp"])
+def test_pair_integrals_any_case(kind, q):
+    """kernels.pair_integrals on a mixed list (mostly separated panels: the
+    disjoint-case tensor rule of quadrature.py:171-180)."""
+    g = golden("pairs.npz")
+    m = sphere(3)
+    assert (g["code"] == 0).sum() > 300
+    v = OQ.singular_integrals(m.vertices, m.triangles, m.normals, m.areas, g["pa"], g["pb"], kind, q)
+    assert rel(v, g[f"{kind}_q{q}"]) < 1e-12
