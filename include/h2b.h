@@ -170,7 +170,9 @@ typedef struct {
  * Mirrored jobs (symmetric single-layer matrix, G(a,b) = G(b,a)) also write
  * out[mirror_off + c*mirror_ld + r]; a job whose mirror_off == out_off is a
  * diagonal tile (same rows and columns) and only its upper triangle is
- * integrated.
+ * integrated.  out_off = -1 writes the mirror only (row-sharded assembly:
+ * the pair is integrated in the orientation of the single-GPU job, so both
+ * give the same bits).
  * Regular pairs: tensor rule with Q points per panel (panel_points).  Touching
  * pairs: value from the singular table (t != NULL) or, when t == NULL
  * (require_disjoint), the call fails with H2B_ERR_TOUCHING.  Synchronises. */

@@ -70,9 +70,10 @@ class AssemblyContext:
         return np.unique(np.concatenate([idx[ptr[v] : ptr[v + 1]] for v in verts]))
 
 
-def _blocks_to_device(ctx, kind, blocks, q, q_singular, require_disjoint, out):
+def _blocks_to_device(ctx, kind, blocks, q, q_singular, require_disjoint, out, table=None):
     """Run (row dofs, col dofs, out_off, ld) dense blocks through the kernels."""
-    table = None if require_disjoint else ctx.singular_table(kind, q_singular)
+    if table is None and not require_disjoint:
+        table = ctx.singular_table(kind, q_singular)
     if kind == kernels.SLP:
         ri = np.concatenate([np.asarray(b[0], dtype=np.int64) for b in blocks]) if blocks else np.zeros(0)
         ci = np.concatenate([np.asarray(b[1], dtype=np.int64) for b in blocks]) if blocks else np.zeros(0)
@@ -245,6 +246,56 @@ def assemble_nearfield_device(ctx, kind, bt, q, q_singular=None, cache=None):
     return out
 
 
+def _sharded_table(ctx, kind, q, own_panels):
+    """The singular table of one rank: only the touching pairs its blocks look
+    up are integrated (SingularTable.compute(own_panels))."""
+    key = ("sharded", kind, q)
+    tab = ctx._singular.get(key)
+    if tab is None:
+        tab = kernels.SingularTable(ctx.dmesh, kind, q, compute=False)
+        ctx._singular[key] = tab
+    tab.compute(own_panels)
+    return tab
+
+
+def _dst_map(n_full, index, off, ld):
+    """(n_full,) destination offset / leading dimension of every block of the
+    full list in a rank's packed layout (-1: stored by another rank)."""
+    d_off = np.full(n_full, -1, dtype=np.int64)
+    d_ld = np.zeros(n_full, dtype=np.int64)
+    d_off[index] = off
+    d_ld[index] = ld
+    return d_off, d_ld
+
+
+def assemble_nearfield_sharded(ctx, kind, view, q, q_singular=None, own_panels=None):
+    """Packed nearfield of one rank of a row-sharded operator (`view`: the
+    rank's BlockTreeView, distributed.py): only the rank's near blocks are
+    integrated and stored, and only the touching pairs they need.  For the
+    single layer the block pairs are integrated in the orientation of the
+    single-GPU job list (mirror_jobs_owned), so every stored entry has the
+    same bits as the single-GPU assembly."""
+    qs = q if q_singular is None else q_singular
+    lay = near_layout(view)
+    out = D.zeros((max(lay.total, 1),))
+    if lay.n_blocks == 0:
+        return out
+    full = view.full
+    rt, ct = full.row_tree, full.col_tree
+    table = _sharded_table(ctx, kind, qs, own_panels)
+    if kind == kernels.SLP and _symmetric_trees(full):
+        nu = full.near_uids
+        geom = np.stack([rt.start[nu[:, 0]], rt.end[nu[:, 0]] - rt.start[nu[:, 0]], ct.start[nu[:, 1]],
+                         ct.end[nu[:, 1]] - ct.start[nu[:, 1]], np.zeros(len(nu), dtype=np.int64),
+                         np.zeros(len(nu), dtype=np.int64)], axis=1)
+        d_off, d_ld = _dst_map(len(nu), view.near_index, lay.blk_off, lay.blk_ld)
+        jobs = kernels.mirror_jobs_owned(geom, nu, d_off, d_ld)
+        kernels.run_slp_jobs(ctx.dmesh, q, jobs, rt.perm.astype(np.int32), ct.perm.astype(np.int32), table, out)
+    else:
+        _blocks_to_device(ctx, kind, _near_blocks(view, lay), q, qs, False, out, table=table)
+    return out
+
+
 def assemble_nearfield(ctx, kind, block_tree, q, cache=None, threads=1, q_singular=None):
     """Dense nearfield payloads in block order (containers.py:79-98); computed
     on the device, returned as host arrays.  Raises FloatingPointError on a
@@ -271,19 +322,31 @@ def _pivots_concat(basis, n_nodes):
 
 
 def assemble_couplings(ctx, kind, bt, row_basis, col_basis, q):
-    """Packed device couplings S_b = G[pivots_t, pivots_s] (gca.py:198-203)."""
+    """Packed device couplings S_b = G[pivots_t, pivots_s] (gca.py:198-203).
+    `bt` may be a rank's BlockTreeView (row sharding): then only the rank's
+    far blocks are integrated and stored, the symmetric pairs in the
+    single-GPU orientation (same bits)."""
     rr, roff, rpiv = _pivots_concat(row_basis, bt.row_tree.n_nodes)
     cr, coff, cpiv = _pivots_concat(col_basis, bt.col_tree.n_nodes)
     lay = FarLayout(bt, rr, cr)
     out = D.zeros((max(lay.total, 1),))
     fu = bt.far_uids
+    full = getattr(bt, "full", None)
     if len(fu):
         if kind == kernels.SLP:
-            jobs = np.stack([roff[fu[:, 0]], lay.blk_rows, coff[fu[:, 1]], lay.blk_cols, lay.blk_off, lay.blk_ld],
-                            axis=1)
-            if row_basis is col_basis and _symmetric_trees(bt):
-                # S_(s,t) = G[piv_s, piv_t] = S_(t,s)^T: one job per block pair
-                jobs = kernels.mirror_jobs(jobs, fu)
+            sym = row_basis is col_basis and _symmetric_trees(bt)
+            if full is not None and sym:
+                ff = full.far_uids
+                geom = np.stack([roff[ff[:, 0]], rr[ff[:, 0]], coff[ff[:, 1]], cr[ff[:, 1]],
+                                 np.zeros(len(ff), dtype=np.int64), np.zeros(len(ff), dtype=np.int64)], axis=1)
+                d_off, d_ld = _dst_map(len(ff), bt.far_index, lay.blk_off, lay.blk_ld)
+                jobs = kernels.mirror_jobs_owned(geom, ff, d_off, d_ld)
+            else:
+                jobs = np.stack([roff[fu[:, 0]], lay.blk_rows, coff[fu[:, 1]], lay.blk_cols, lay.blk_off,
+                                 lay.blk_ld], axis=1)
+                if sym:
+                    # S_(s,t) = G[piv_s, piv_t] = S_(t,s)^T: one job per block pair
+                    jobs = kernels.mirror_jobs(jobs, fu)
             kernels.run_slp_jobs(ctx.dmesh, q, jobs, rpiv.astype(np.int32), cpiv.astype(np.int32), None, out)
         else:
             blocks = [(rpiv[roff[t] : roff[t + 1]], cpiv[coff[s] : coff[s + 1]], int(lay.blk_off[i]),

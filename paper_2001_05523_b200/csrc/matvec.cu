@@ -1284,8 +1284,12 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
 }
 
 __global__ void k_diagonal(h2b_layout L, double* __restrict__ diag) {
-    const int node = blockIdx.x * blockDim.x + threadIdx.x;
-    if (node >= L.r_nodes || L.r_v_off[node] < 0) return;
+    // row-sharded plans: only the rank's own leaves (row_perm maps its rows)
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (L.owned ? L.n_owned : L.r_nodes)) return;
+    const int node = L.owned ? L.owned[i] : i;
+    if (L.r_v_off[node] < 0) return;
+    if (L.owned && (L.r_start[node] + L.r_size[node] > L.n_rows || L.row_perm[L.r_start[node]] < 0)) return;
     const int ts = L.r_start[node], te = ts + L.r_size[node];
     const int C = L.d_cols[node];
     const double* D = L.D + L.d_off[node];
@@ -1344,11 +1348,17 @@ __global__ void k_sym_pack(const double* __restrict__ D, const int64_t* __restri
     }
 }
 
-// Host side of the symmetric nearfield (single-GPU plans whose row and column
-// trees coincide and whose nearfield is symmetric bit for bit, e.g. the
+// Host side of the symmetric nearfield (plans whose row and column trees
+// coincide and whose nearfield is symmetric bit for bit, e.g. the
 // single-layer Galerkin matrix, containers.py near_slp_jobs).  Per row leaf t,
-// the upper blocks s (start(s) >= start(t), t itself first) are cut into
-// column panels of all |t| rows that fit the TMA stage.
+// the blocks it streams are cut into column panels of all |t| rows that fit
+// the TMA stage, in the column order
+//   [ diagonal block | one-sided blocks | upper paired blocks ]
+// where "paired" blocks (t, s) have their mirror (s, t) held by the same plan
+// and start(s) > start(t): their transposed product is s's contribution from
+// this panel.  The first `skip` columns have no transposed output.  Single-GPU
+// plans pair every block; a row-sharded plan (L.owned) holds only its own
+// leaves' blocks, so blocks towards another rank's leaves are one-sided.
 struct SymNear {
     bool on = false;
     std::vector<std::vector<int64_t>> bands;  // per row node: band records
@@ -1364,16 +1374,20 @@ int build_sym_near(const h2b_layout& L, const std::vector<int32_t>& rstart, cons
                    const std::vector<int64_t>& rvoff, const std::vector<int32_t>& dcols,
                    const std::vector<int64_t>& doff, const std::vector<int64_t>& dgoff, SymNear& S) {
     S.on = false;
-    if (L.owned || L.r_nodes != L.c_nodes || L.n_rows != L.n_cols || !L.near_ptr || !L.near_col) return 0;
+    if (L.r_nodes != L.c_nodes || L.n_rows != L.n_cols || !L.near_ptr || !L.near_col) return 0;
     if (const char* e = getenv("H2B_NEAR_SYM"))
         if (e[0] == '0') return 0;
     const int n = L.r_nodes;
     for (int u = 0; u < n; ++u)
         if (rstart[u] != cstart[u] || rsize[u] != csize[u]) return 0;
-    std::vector<int64_t> rp, cp;
-    H2B_CUDA_TRY(fetch(L.row_perm, L.n_rows, rp));
-    H2B_CUDA_TRY(fetch(L.col_perm, L.n_cols, cp));
-    if (rp != cp) return 0;
+    if (!L.owned) {
+        // (row-sharded plans map rows and columns to different index spaces;
+        // there the trees are checked by the structure above)
+        std::vector<int64_t> rp, cp;
+        H2B_CUDA_TRY(fetch(L.row_perm, L.n_rows, rp));
+        H2B_CUDA_TRY(fetch(L.col_perm, L.n_cols, cp));
+        if (rp != cp) return 0;
+    }
     std::vector<int32_t> nptr, ncol, dg;
     H2B_CUDA_TRY(fetch(L.near_ptr, (int64_t)n + 1, nptr));
     H2B_CUDA_TRY(fetch(L.near_col, std::max<int64_t>(nptr[n], 1), ncol));
@@ -1381,8 +1395,16 @@ int build_sym_near(const h2b_layout& L, const std::vector<int32_t>& rstart, cons
     for (int u = 0; u < n; ++u)
         if (rvoff[u] >= 0) glen = std::max<int64_t>(glen, dgoff[u] + dcols[u]);
     H2B_CUDA_TRY(fetch(L.d_gidx, std::max<int64_t>(glen, 1), dg));
-    // structure: near blocks only between row leaves, each with its mirror and
-    // the diagonal block present
+    // leaves whose tasks this plan runs (all leaves on one GPU; a rank's own)
+    std::vector<char> mine(n, 1);
+    if (L.owned) {
+        std::vector<int32_t> own;
+        H2B_CUDA_TRY(fetch(L.owned, L.n_owned, own));
+        std::fill(mine.begin(), mine.end(), 0);
+        for (int u : own)
+            if (u >= 0 && u < n) mine[u] = 1;
+    }
+    std::vector<char> has(n, 0);
     std::vector<std::vector<std::pair<int, int64_t>>> blocks(n);  // (s, column offset in t's row)
     for (int t = 0; t < n; ++t) {
         int64_t c = 0;
@@ -1392,6 +1414,7 @@ int build_sym_near(const h2b_layout& L, const std::vector<int32_t>& rstart, cons
             blocks[t].push_back({s, c});
             c += rsize[s];
         }
+        has[t] = mine[t] && nptr[t + 1] > nptr[t];
     }
     auto find = [&](int t, int s) -> int64_t {
         for (const auto& b : blocks[t])
@@ -1400,20 +1423,34 @@ int build_sym_near(const h2b_layout& L, const std::vector<int32_t>& rstart, cons
     };
     for (int t = 0; t < n; ++t) {
         if (rvoff[t] < 0) continue;
+        if (!has[t]) {
+            if (!L.owned) return 0;  // one GPU: every leaf has its diagonal block
+            continue;
+        }
         if (find(t, t) < 0) return 0;
         for (const auto& b : blocks[t])
-            if (find(b.first, t) < 0) return 0;
+            if (has[b.first] && find(b.first, t) < 0) return 0;  // a held leaf must hold the mirror
+            else if (!has[b.first] && !L.owned) return 0;
     }
-    // upper blocks, diagonal first; check jobs for the bitwise symmetry test
+    // per leaf: diagonal, one-sided, then upper paired blocks; check jobs for
+    // the bitwise symmetry test of the paired (and diagonal) blocks
     std::vector<std::vector<std::pair<int, int64_t>>> up(n);
+    std::vector<int64_t> skip_w(n, 0);  // columns without a transposed output
     for (int t = 0; t < n; ++t) {
-        if (rvoff[t] < 0) continue;
+        if (rvoff[t] < 0 || !has[t]) continue;
         up[t].push_back({t, find(t, t)});
+        skip_w[t] = rsize[t];
         for (const auto& b : blocks[t])
-            if (b.first != t && rstart[b.first] > rstart[t]) up[t].push_back(b);
+            if (b.first != t && !has[b.first]) {
+                up[t].push_back(b);
+                skip_w[t] += rsize[b.first];
+            }
+        for (const auto& b : blocks[t])
+            if (b.first != t && has[b.first] && rstart[b.first] > rstart[t]) up[t].push_back(b);
         for (const auto& b : up[t])
-            S.check.insert(S.check.end(), {doff[t] + b.second, dcols[t], doff[b.first] + find(b.first, t),
-                                           dcols[b.first], rsize[t], rsize[b.first]});
+            if (has[b.first])
+                S.check.insert(S.check.end(), {doff[t] + b.second, dcols[t], doff[b.first] + find(b.first, t),
+                                               dcols[b.first], rsize[t], rsize[b.first]});
     }
     // panels, partial offsets
     S.bands.assign(n, {});
@@ -1421,11 +1458,11 @@ int build_sym_near(const h2b_layout& L, const std::vector<int32_t>& rstart, cons
     S.list_n.assign(n, 0);
     S.producers.assign(n, {});
     std::vector<int64_t> tbase(n, 0);
-    std::vector<std::vector<int64_t>> tcol(n);  // per t: column offset of each upper block in its panels
+    std::vector<std::vector<int64_t>> tcol(n);  // per t: column offset of each streamed block in its panels
     std::vector<std::vector<int64_t>> direct(n);
     int64_t pdir = 0, dlen = 0, g = 0;
     for (int t = 0; t < n; ++t) {
-        if (rvoff[t] < 0) continue;
+        if (rvoff[t] < 0 || !has[t]) continue;
         const int rows = rsize[t];
         int64_t W = 0;
         for (const auto& b : up[t]) {
@@ -1441,10 +1478,9 @@ int build_sym_near(const h2b_layout& L, const std::vector<int32_t>& rstart, cons
                 S.gsym.push_back(dg[dgoff[t] + b.second + j]);
             }
         g += W;
-        tbase[t] = -1;  // set below, after all direct partials
         for (int64_t j0 = 0; j0 < W; j0 += wmax) {
             const int w = (int)std::min<int64_t>(wmax, W - j0);
-            const int skip = (int)std::max<int64_t>(0, std::min<int64_t>(w, rows - j0));
+            const int skip = (int)std::max<int64_t>(0, std::min<int64_t>(w, skip_w[t] - j0));
             std::vector<int64_t> r(kBandWords, 0);
             r[0] = dlen;
             r[1] = w;
@@ -1454,7 +1490,7 @@ int build_sym_near(const h2b_layout& L, const std::vector<int32_t>& rstart, cons
             r[7] = kKindNearSym;
             r[8] = j0;  // + tbase[t] below
             r[9] = skip;
-            r[10] = gbase;
+            r[10] = gbase;  // t's own x: the diagonal block's columns come first
             S.bands[t].insert(S.bands[t].end(), r.begin(), r.end());
             S.pack.insert(S.pack.end(), {doff[t], dcols[t], rows, w, dlen, gbase + j0});
             direct[t].push_back(pdir);
@@ -1466,7 +1502,7 @@ int build_sym_near(const h2b_layout& L, const std::vector<int32_t>& rstart, cons
     }
     int64_t tpos = pdir;
     for (int t = 0; t < n; ++t) {
-        if (rvoff[t] < 0) continue;
+        if (rvoff[t] < 0 || !has[t]) continue;
         const int64_t W = tbase[t];
         tbase[t] = tpos;
         tpos += W;
@@ -1475,14 +1511,14 @@ int build_sym_near(const h2b_layout& L, const std::vector<int32_t>& rstart, cons
     S.ppart_len = tpos;
     S.dsym_len = dlen;
     // per leaf u: its panels' direct partials, then the transposed partials
-    // of the blocks (t, u) with t before u, in u's near-list order
+    // of the paired blocks (t, u) with t before u, in u's near-list order
     for (int u = 0; u < n; ++u) {
-        if (rvoff[u] < 0) continue;
+        if (rvoff[u] < 0 || !has[u]) continue;
         S.list_off[u] = (int64_t)S.nsum.size();
         for (int64_t o : direct[u]) S.nsum.push_back(o);
         for (const auto& b : blocks[u]) {
             const int t = b.first;
-            if (t == u || rstart[t] > rstart[u]) continue;
+            if (t == u || !has[t] || rstart[t] > rstart[u]) continue;
             int64_t off = -1;
             for (size_t i = 0; i < up[t].size(); ++i)
                 if (up[t][i].first == u) off = tbase[t] + tcol[t][i];
@@ -1495,7 +1531,6 @@ int build_sym_near(const h2b_layout& L, const std::vector<int32_t>& rstart, cons
     S.on = true;
     return 0;
 }
-
 
 }  // namespace
 }  // namespace h2b
@@ -2025,7 +2060,8 @@ extern "C" int h2b_diagonal(h2b_plan* p, double* d_diag, void* stream) {
     if (!p || !d_diag) return fail(H2B_ERR_INVALID, "h2b_diagonal: null pointer");
     if (p->L.n_rows != p->L.n_cols) return fail(H2B_ERR_INVALID, "diagonal extraction requires a square operator");
     cudaStream_t st = as_stream(stream);
-    k_diagonal<<<(p->L.r_nodes + 127) / 128, 128, 0, st>>>(p->L, d_diag);
+    const int n = p->L.owned ? p->L.n_owned : p->L.r_nodes;
+    if (n > 0) k_diagonal<<<(n + 127) / 128, 128, 0, st>>>(p->L, d_diag);
     H2B_CUDA_TRY(cudaGetLastError());
     return ok();
 }

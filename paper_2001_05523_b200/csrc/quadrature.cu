@@ -649,7 +649,9 @@ __global__ void __launch_bounds__(H2B_SLP_THREADS, MINB) k_blocks_slp(const doub
             val = tot;
         }
         if (!isfinite(val)) lflags |= kFlagNonFinite;
-        out[out_off + (int64_t)a * ld + b] = val;
+        // out_off < 0: mirror-only job (a sharded rank integrates a block pair
+        // in the orientation one GPU uses and keeps only the transposed copy)
+        if (out_off >= 0) out[out_off + (int64_t)a * ld + b] = val;
         if (m_off >= 0 && !(tri && a == b)) out[m_off + (int64_t)b * m_ld + a] = val;
     }
     if (lflags) atomicOr(flags, lflags);

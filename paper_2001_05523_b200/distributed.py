@@ -1,18 +1,32 @@
-"""Row-sharded multi-GPU H^2 matvec (one process per GPU, torch.distributed).
+"""Row-sharded multi-GPU H^2 operator (one process per GPU, torch.distributed).
 
 Partition: the row leaves, in permuted (tree) order, are cut
 into `world` contiguous ranges balanced by streamed bytes (nearfield rows x
 C_t + leaf basis + coupling rows of the leaf).  Rank r owns permuted rows
-[lo_r, hi_r) and every row cluster whose index range intersects it; clusters
-above the cut are evaluated redundantly by each rank that shares them, and
-each rank's backward pass only descends into its own subtrees.  No value is
-reduced across ranks: each rank writes its own rows of y.
+[lo_r, hi_r), every row leaf inside that range and every row cluster whose
+index range intersects it; clusters above the cut (spanning several ranks)
+are processed redundantly by each rank that shares them, and each rank's
+backward pass only descends into its own subtrees.
+
+Assembly is sharded too (reference work split: containers.py:79-98 nearfield,
+gca.py:194-205 couplings): a rank integrates and stores only the near blocks
+of its row leaves, the far blocks of its row clusters and the touching pairs
+those blocks look up (RowShard.assemble).  Single-layer block pairs are
+integrated in the orientation the single-GPU job list uses, so the stored
+entries are the same bits as a single-GPU assembly.
 
 Per matvec the only exchange is one all-gather of x (permuted order, padded
-to equal chunks) over NCCL; every rank then runs the full forward transform
-(the column tree is needed by all coupling blocks) and its share of the
-backward/nearfield work.  Row accumulation order does not depend on the rank
-count, so 1- and N-GPU results are bitwise identical.
+to equal chunks) over NCCL; every rank then runs its own task list of the
+fused matvec kernel and writes its own rows of y.  No value is reduced across
+ranks.  Within a rank the bitwise-symmetric single-layer nearfield is
+streamed once per block pair whose two row leaves it owns (the cross-rank
+blocks one-sided), so per-rank nearfield bytes are ~1/N of the single-GPU
+symmetric stream.  Row results agree with the single-GPU operator to
+rounding (the per-row association of the nearfield partials differs); with
+the symmetric pairing switched off (H2B_NEAR_SYM=0) sharded and single-GPU
+one-sided plans are bitwise identical.
+
+CG on row-sharded vectors: solver.cg(..., allreduce=allreduce_sum(dist)).
 """
 
 import numpy as np
@@ -27,7 +41,6 @@ def leaf_costs(rt, near_C, far_K, ranks):
     cost = size * near_C + size * ranks + ranks * far_K
     leaves = rt.leaf_uids()
     order = leaves[np.argsort(rt.start[leaves], kind="stable")]
-    # charge each internal node's coupling to the leaf at its start
     first_leaf = {}
     for u in order:
         first_leaf[int(rt.start[u])] = int(u)
@@ -38,9 +51,9 @@ def leaf_costs(rt, near_C, far_K, ranks):
 
 
 def partition_rows(rt, near_C, far_K, ranks, world):
-    """Contiguous permuted row ranges [(lo, hi)] per rank, balanced by cost
-    (rt: row ClusterTree; near_C / far_K: per-node nearfield / coupling
-    matrix widths; ranks: per-node row-basis ranks)."""
+    """Contiguous permuted row ranges [(lo, hi)] per rank, cut at leaf
+    boundaries and balanced by cost (rt: row ClusterTree; near_C / far_K:
+    per-node nearfield / coupling matrix widths; ranks: per-node row ranks)."""
     order, cost = leaf_costs(rt, near_C, far_K, ranks)
     cum = np.cumsum(cost)
     total = cum[-1]
@@ -60,6 +73,20 @@ def partition_rows(rt, near_C, far_K, ranks, world):
     return ranges
 
 
+def block_tree_partition(bt, row_basis, col_basis, world):
+    """partition_rows from the block tree and the bases (before assembly)."""
+    from .containers import FarLayout, near_layout
+
+    rr = np.array([row_basis.rank[u] for u in range(bt.row_tree.n_nodes)], dtype=np.int64)
+    cr = np.array([col_basis.rank[u] for u in range(bt.col_tree.n_nodes)], dtype=np.int64)
+    return partition_rows(bt.row_tree, near_layout(bt).C, FarLayout(bt, rr, cr).K, rr, world)
+
+
+def operator_partition(H, world):
+    ranks = np.array([H.row_basis.rank[u] for u in range(H.row_tree.n_nodes)], dtype=np.int64)
+    return partition_rows(H.row_tree, H.near_layout.C, H.far_layout.K, ranks, world)
+
+
 def owned_nodes(tree, lo, hi):
     """Row clusters whose range intersects [lo, hi), parents first (by depth)."""
     hit = np.flatnonzero((tree.start < hi) & (tree.end > lo))
@@ -76,9 +103,84 @@ def gather_layout(ranges, n):
     return chunk, pad_index
 
 
-def operator_partition(H, world):
-    ranks = np.array([H.row_basis.rank[u] for u in range(H.row_tree.n_nodes)], dtype=np.int64)
-    return partition_rows(H.row_tree, H.near_layout.C, H.far_layout.K, ranks, world)
+class BlockTreeView:
+    """The block tree restricted to one rank's rows: the near blocks of its row
+    leaves and the far blocks of the row clusters intersecting its range, in
+    the full lists' order (near_index / far_index: positions in the full
+    lists).  Same trees as the full block tree; usable wherever a BlockTree is
+    (layouts, assembly, matvec plans)."""
+
+    def __init__(self, bt, lo, hi):
+        rt = bt.row_tree
+        self.full = bt
+        self.row_tree, self.col_tree, self.eta = bt.row_tree, bt.col_tree, bt.eta
+        self.lo, self.hi = lo, hi
+        nu, fu = bt.near_uids, bt.far_uids
+        leaf_in = (rt.start >= lo) & (rt.end <= hi)
+        touches = (rt.start < hi) & (rt.end > lo)
+        self.near_index = np.flatnonzero(leaf_in[nu[:, 0]]) if len(nu) else np.zeros(0, dtype=np.int64)
+        self.far_index = np.flatnonzero(touches[fu[:, 0]]) if len(fu) else np.zeros(0, dtype=np.int64)
+        self.near_uids = nu[self.near_index]
+        self.far_uids = fu[self.far_index]
+        self._far = self._near = None
+        self._near_layout = None
+
+    @property
+    def far(self):
+        if self._far is None:
+            full = self.full.far
+            self._far = [full[i] for i in self.far_index]
+        return self._far
+
+    @property
+    def near(self):
+        if self._near is None:
+            full = self.full.near
+            self._near = [full[i] for i in self.near_index]
+        return self._near
+
+
+class RowShard:
+    """One rank's share of a row-sharded H^2 operator: partition, view of the
+    block tree, sharded assembly and the rank's matvec plan."""
+
+    def __init__(self, bt, row_basis, col_basis, rank, world, ranges=None):
+        if bt.row_tree.n_dofs != bt.col_tree.n_dofs:
+            raise ValueError("row sharding with the x all-gather needs a square operator")
+        self.bt, self.rb, self.cb = bt, row_basis, col_basis
+        self.rank, self.world = rank, world
+        self.ranges = ranges if ranges is not None else block_tree_partition(bt, row_basis, col_basis, world)
+        self.lo, self.hi = self.ranges[rank]
+        self.view = BlockTreeView(bt, self.lo, self.hi)
+        rt = bt.row_tree
+        self.owned = owned_nodes(rt, self.lo, self.hi)
+        self.own_panels = np.zeros(rt.n_dofs, dtype=bool)
+        self.own_panels[rt.perm[self.lo : self.hi]] = True
+        self.chunk, self.pad_index = gather_layout(self.ranges, rt.n_dofs)
+        self.S = self.D = None
+
+    def assemble(self, ctx, kind, q, q_singular=None):
+        """Integrate this rank's couplings and nearfield (device)."""
+        from .containers import assemble_couplings, assemble_nearfield_sharded
+
+        self.S = assemble_couplings(ctx, kind, self.view, self.rb, self.cb, q)
+        self.D = assemble_nearfield_sharded(ctx, kind, self.view, q, q_singular, self.own_panels)
+        return self.S, self.D
+
+    def near_entries(self):
+        from .containers import near_layout
+
+        return near_layout(self.view).entries
+
+    def plan(self):
+        from .containers import FarLayout, MatvecPlan, near_layout
+
+        rt = self.bt.row_tree
+        rr = np.array([self.rb.rank[u] for u in range(rt.n_nodes)], dtype=np.int64)
+        cr = np.array([self.cb.rank[u] for u in range(self.bt.col_tree.n_nodes)], dtype=np.int64)
+        row_local = np.arange(rt.n_dofs, dtype=np.int64) - self.lo  # only owned rows are written
+        return MatvecPlan(self.view, self.rb, self.cb, self.S, self.D, FarLayout(self.view, rr, cr),
+                          near_layout(self.view), owned=self.owned, col_perm=self.pad_index, row_perm=row_local)
 
 
 class LocalMatvec:
@@ -93,37 +195,54 @@ class LocalMatvec:
         return y
 
 
-
 class ShardedMatvec:
-    """Row-sharded matvec: apply(x, y) takes the full natural-order x on every
-    rank (the bench's input) or, via apply_local, this rank's permuted slice."""
+    """Row-sharded matvec of one rank.  apply_local(x_loc, y_loc) takes this
+    rank's permuted slice of x and returns its permuted rows of y (the CG
+    path); apply(x, y) takes a full natural-order x and scatters the rank's
+    rows into y (bench / tests).  `dist` provides all_gather_into_tensor.
 
-    def __init__(self, H, rank, world, dist):
+    Built either from a RowShard (sharded assembly: the rank holds only its
+    share of the operator) or, for tests, from a full single-GPU H2Matrix."""
+
+    def __init__(self, src, rank, world, dist):
         import torch
 
-        from .containers import MatvecPlan
+        if isinstance(src, RowShard):
+            shard = src
+            if shard.S is None:
+                raise ValueError("RowShard.assemble() first")
+        else:
+            H = src
+            shard = RowShard(H.block_tree, H.row_basis, H.col_basis, rank, world,
+                             ranges=operator_partition(H, world))
+            shard.view = H.block_tree  # full operator arrays: every block present
+            shard.S, shard.D = H.S_dev, H.D_dev
+        self.shard, self.rank, self.world, self.dist = shard, rank, world, dist
+        self.lo, self.hi, self.chunk = shard.lo, shard.hi, shard.chunk
+        if shard.view is shard.bt:
+            from .containers import MatvecPlan
 
-        if H.shape[0] != H.shape[1]:
-            raise ValueError("row sharding with the x all-gather needs a square operator")
-        self.H, self.rank, self.world, self.dist = H, rank, world, dist
-        rt = H.row_tree
-        self.ranges = operator_partition(H, world)
-        lo, hi = self.ranges[rank]
-        self.lo, self.hi = lo, hi
-        # padded gather layout: permuted position p of rank r -> r*chunk + (p - lo_r)
-        self.chunk, pad_index = gather_layout(self.ranges, rt.n_dofs)
-        row_local = np.arange(rt.n_dofs, dtype=np.int64) - lo  # only owned rows are written
-        owned = owned_nodes(rt, lo, hi)
-        self.plan = MatvecPlan(H.block_tree, H.row_basis, H.col_basis, H.S_dev, H.D_dev, H.far_layout,
-                               H.near_layout, owned=owned, col_perm=pad_index, row_perm=row_local)
+            rt = shard.bt.row_tree
+            H = src
+            self.plan = MatvecPlan(H.block_tree, H.row_basis, H.col_basis, H.S_dev, H.D_dev, H.far_layout,
+                                   H.near_layout, owned=shard.owned, col_perm=shard.pad_index,
+                                   row_perm=np.arange(rt.n_dofs, dtype=np.int64) - shard.lo)
+        else:
+            self.plan = shard.plan()
+        rt = shard.bt.row_tree
         self.xbuf = torch.zeros(world * self.chunk, dtype=torch.float64, device="cuda")
         self.xloc = torch.zeros(self.chunk, dtype=torch.float64, device="cuda")
-        self.yloc = torch.zeros(max(hi - lo, 1), dtype=torch.float64, device="cuda")
-        self.perm_dev = torch.from_numpy(rt.perm[lo:hi].copy()).cuda()
+        self.yloc = torch.zeros(max(self.hi - self.lo, 1), dtype=torch.float64, device="cuda")
+        self.perm_dev = torch.from_numpy(rt.perm[self.lo : self.hi].copy()).cuda()
 
-    def apply_local(self, x_local_perm, y_local_perm):
-        """x_local_perm: this rank's permuted slice of x (hi-lo); returns its rows of y."""
+    def info(self):
+        return self.plan.info()
+
+    def apply_local(self, x_local_perm, y_local_perm=None):
+        """x_local_perm: this rank's permuted slice of x (hi - lo); returns its rows of y."""
         n = self.hi - self.lo
+        if y_local_perm is None:
+            y_local_perm = self.yloc[:n].clone()
         self.xloc[:n].copy_(x_local_perm)
         self.dist.all_gather_into_tensor(self.xbuf, self.xloc)
         _lib.check(_lib.lib().h2b_matvec(self.plan.handle, self.xbuf.data_ptr(), y_local_perm.data_ptr(),
@@ -131,7 +250,7 @@ class ShardedMatvec:
         return y_local_perm
 
     def apply(self, x, y):
-        """Bench entry: full natural-order x -> this rank's rows written into y[perm]."""
+        """Full natural-order x -> this rank's rows written into y[perm]."""
         n = self.hi - self.lo
         self.xloc[:n].copy_(x[self.perm_dev])
         self.dist.all_gather_into_tensor(self.xbuf, self.xloc)
@@ -139,3 +258,20 @@ class ShardedMatvec:
                                          _lib.stream_ptr()))
         y[self.perm_dev] = self.yloc[:n]
         return y
+
+    def diagonal_local(self):
+        """This rank's rows of the operator diagonal (permuted order)."""
+        import torch
+
+        d = torch.zeros(max(self.hi - self.lo, 1), dtype=torch.float64, device="cuda")
+        _lib.check(_lib.lib().h2b_diagonal(self.plan.handle, d.data_ptr(), _lib.stream_ptr()))
+        return d[: self.hi - self.lo]
+
+
+def allreduce_sum(dist, group=None):
+    """In-place sum of a small device tensor over the ranks (CG scalars)."""
+
+    def f(t):
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+
+    return f

@@ -118,6 +118,35 @@ class TouchTable:
             self.c.h_half_off = _lib.ptr(self.half_off)
         return self.half_list
 
+    def subset(self, own_panels, half):
+        """A descriptor whose pair lists keep only the pairs touching an owned
+        panel (half: the unordered list, either panel owned; else the ordered
+        list, row panel owned), case segments preserved.  Cached per mask."""
+        t = D.torch()
+        key = (bytes(np.packbits(np.asarray(own_panels, dtype=bool))), half)
+        if getattr(self, "_subset", None) is not None and self._subset[0] == key:
+            return self._subset[1]
+        own = t.from_numpy(np.ascontiguousarray(own_panels, dtype=bool)).cuda()
+        F = self.dmesh.mesh.n_triangles
+        rows = t.repeat_interleave(t.arange(F, device="cuda", dtype=t.int32), t.diff(self.row_ptr))
+        lst, off = (self.half_list, self.half_off) if half else (self.case_list, self.case_off)
+        parts, new_off = [], [0]
+        for k in range(3):
+            seg = lst[int(off[k]) : int(off[k + 1])].long()
+            m = own[rows[seg].long()]
+            if half:
+                m = m | own[self.col[seg].long()]
+            parts.append(seg[m].to(t.int32))
+            new_off.append(new_off[-1] + int(parts[-1].numel()))
+        sub = t.cat(parts) if new_off[-1] else t.zeros(1, dtype=t.int32, device="cuda")
+        sub_off = np.array(new_off, dtype=np.int64)
+        c = _lib.Touch(self.c.n_panels, self.c.n_pairs, self.c.d_row_ptr, self.c.d_col, self.c.d_info,
+                       sub.data_ptr() if not half else self.c.d_case_list,
+                       _lib.ptr(sub_off) if not half else self.c.h_case_off,
+                       sub.data_ptr() if half else None, _lib.ptr(sub_off) if half else None)
+        self._subset = (key, c, sub, sub_off)
+        return c
+
     def keys(self):
         """Sorted int64 keys pa * F + pb (reference SingularTable.keys)."""
         F = self.dmesh.mesh.n_triangles
@@ -160,12 +189,19 @@ class SingularTable:
         if compute:
             self.compute()
 
-    def compute(self):
-        """(Re)evaluate every touching pair on the device (stream-ordered).
-        Single layer: one evaluation per unordered pair (symmetric table)."""
+    def compute(self, own_panels=None):
+        """(Re)evaluate the touching pairs on the device (stream-ordered).
+        Single layer: one evaluation per unordered pair (symmetric table).
+        own_panels (bool per panel, row sharding): only the pairs this rank's
+        blocks look up -- single layer: every unordered pair with an owned
+        panel (both ordered entries are written); double layer: the ordered
+        pairs whose row panel is owned.  Other entries are left untouched."""
         if self.kind == SLP:
             self.touch.ensure_half()
-        _lib.check(_lib.lib().h2b_singular(ctypes.byref(self.dmesh.c), ctypes.byref(self.touch.c),
+        c = self.touch.c
+        if own_panels is not None:
+            c = self.touch.subset(own_panels, half=self.kind == SLP)
+        _lib.check(_lib.lib().h2b_singular(ctypes.byref(self.dmesh.c), ctypes.byref(c),
                                            kind_code(self.kind), self.rules, self.values_dev.data_ptr(),
                                            D.stream()))
 
@@ -220,8 +256,23 @@ def tile_jobs(jobs):
                 if diag and i > j:
                     continue
                 m = mo + j * mld + i if mo >= 0 else -1
-                out.append((r0 + i, min(TILE, nr - i), c0 + j, min(TILE, nc - j), o + i * ld + j, ld, m, mld))
+                oo = o + i * ld + j if o >= 0 else -1
+                out.append((r0 + i, min(TILE, nr - i), c0 + j, min(TILE, nc - j), oo, ld, m, mld))
     return np.array(out, dtype=np.int64).reshape(-1, 8)
+
+
+def block_partners(uids):
+    """For every block (t, s) of a block list (n, 2), the index of block (s, t)
+    in the same list, or -1; a diagonal block is its own partner."""
+    uids = np.asarray(uids, dtype=np.int64).reshape(-1, 2)
+    n = len(uids)
+    if n == 0:
+        return np.zeros(0, dtype=np.int64)
+    key = uids[:, 0] * (uids.max() + 1) + uids[:, 1]
+    tkey = uids[:, 1] * (uids.max() + 1) + uids[:, 0]
+    order = np.argsort(key, kind="stable")
+    pos = np.minimum(np.searchsorted(key[order], tkey), n - 1)
+    return np.where(key[order][pos] == tkey, order[pos], -1)
 
 
 def mirror_jobs(jobs, uids):
@@ -231,23 +282,40 @@ def mirror_jobs(jobs, uids):
     upper triangle.  jobs: (n, 6) in the order of uids (n, 2)."""
     jobs = np.asarray(jobs, dtype=np.int64).reshape(-1, 6)
     uids = np.asarray(uids, dtype=np.int64).reshape(-1, 2)
-    n = len(jobs)
     out = _as_job8(jobs).copy()
-    if n == 0:
+    if len(jobs) == 0:
         return out
-    key = uids[:, 0] * (uids.max() + 1) + uids[:, 1]
-    tkey = uids[:, 1] * (uids.max() + 1) + uids[:, 0]
-    order = np.argsort(key, kind="stable")
-    pos = np.searchsorted(key[order], tkey)
-    pos = np.minimum(pos, n - 1)
-    has = key[order][pos] == tkey
-    partner = np.where(has, order[pos], -1)
-    t, s = uids[:, 0], uids[:, 1]
-    keep = (partner < 0) | (t <= s)
+    partner = block_partners(uids)
+    keep = (partner < 0) | (uids[:, 0] <= uids[:, 1])
     m = keep & (partner >= 0)
     out[m, 6] = jobs[partner[m], 4]
     out[m, 7] = jobs[partner[m], 5]
     return out[keep]
+
+
+def mirror_jobs_owned(jobs, uids, dst_off, dst_ld):
+    """The jobs of mirror_jobs restricted to the blocks one rank stores (row
+    sharding).  jobs (n, 6) / uids (n, 2): the FULL block list (integration
+    geometry of every block); dst_off / dst_ld (n,): where this rank stores
+    block i, or -1.  Every kept job integrates its block pair in the same
+    orientation as the single-GPU job list, so the stored values are the same
+    bits; a job whose direct block belongs to another rank becomes
+    mirror-only (out_off = -1)."""
+    jobs = np.asarray(jobs, dtype=np.int64).reshape(-1, 6)
+    uids = np.asarray(uids, dtype=np.int64).reshape(-1, 2)
+    if len(jobs) == 0:
+        return np.zeros((0, 8), dtype=np.int64)
+    partner = block_partners(uids)
+    keep = (partner < 0) | (uids[:, 0] <= uids[:, 1])
+    out = _as_job8(jobs).copy()
+    out[:, 4] = dst_off
+    out[:, 5] = dst_ld
+    m = keep & (partner >= 0)
+    pm = partner[m]
+    out[m, 6] = dst_off[pm]
+    out[m, 7] = dst_ld[pm]
+    out = out[keep]
+    return out[(out[:, 4] >= 0) | (out[:, 6] >= 0)]
 
 
 class SlpJobs:

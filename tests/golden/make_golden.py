@@ -22,6 +22,8 @@ What is pinned (all produced by the reference's own public functions):
   near_cfg0.npz    sampled split-order nearfield blocks (kernels.py:365-468)
   h2_cfg0.npz      full GCA basis + sampled couplings + matvec x/y of config 0
   h2_cfg1.npz      pivots/ranks digests + matvec x/y of config 1
+  h2_cfg3p.npz     config-3 parameters (m=5, eta=1.5, leaf 64, q 3/4) at sphere
+                   level 6: pivots/ranks + matvec / rmatvec x/y + samples
   h2_dlp4.npz      level-4 double-layer H^2 (P0 x P1) matvec x/y + basis
   sample_l8.npz    config-2 size (sphere level 8): a seeded sample of single- and
                    double-layer near blocks with the split orders (regular 3,
@@ -326,6 +328,34 @@ def gen_h2_cfg1():
     np.savez_compressed(os.path.join(HERE, "h2_cfg1.npz"), **out)
 
 
+def gen_h2_cfg3p():
+    """BASELINE.json config-3 parameters (GCA m=5, eta=1.5, leaf 64, orders
+    3/4, single layer) at a reference-tractable size: sphere level 6."""
+    mesh, ctx, bt, rb, cb = build_world(6, 64, 1.5, 5, 1e-4, kernels.SLP)
+    log("cfg3p basis")
+    H = split_h2(ctx, kernels.SLP, bt, rb, cb, 3, 4)
+    log("cfg3p h2 assembled")
+    rng = np.random.default_rng(3)
+    xs = [rng.standard_normal(H.shape[1]) for _ in range(2)]
+    out = {"x0": xs[0], "y0": H.matvec(xs[0]), "x1": xs[1], "y1": H.matvec(xs[1])}
+    out["yt0"] = H.rmatvec(xs[0])
+    ba = basis_arrays("", rb, bt.row_tree)
+    out["ranks"] = ba["ranks"]
+    out["pivots"] = ba["pivots"]
+    out["V_sum"] = np.array([ba["V"].sum(), np.abs(ba["V"]).sum()])
+    out["E_sum"] = np.array([ba["E"].sum(), np.abs(ba["E"]).sum()])
+    rep = H.storage_report()
+    out["storage"] = np.array([rep["basis"], rep["coupling"], rep["lowrank"], rep["nearfield"]], dtype=np.int64)
+    out["diag"] = H.diagonal()
+    rng = np.random.default_rng(11)
+    nsel = np.sort(rng.choice(len(H.near), 16, replace=False))
+    fsel = np.sort(rng.choice(len(H.far), 32, replace=False))
+    out["near_sel"], out["far_sel"] = nsel, fsel
+    out["near_vals"] = np.concatenate([H.near[i][1].ravel() for i in nsel])
+    out["far_vals"] = np.concatenate([H.far[i][1].ravel() for i in fsel])
+    np.savez_compressed(os.path.join(HERE, "h2_cfg3p.npz"), **out)
+
+
 def gen_h2_dlp4():
     mesh, ctx, bt, rb, cb = build_world(4, 32, 2.0, 3, 1e-4, kernels.DLP)
     log("dlp4 bases")
@@ -471,6 +501,7 @@ def main():
         ("h2_cfg0", gen_h2_cfg0),
         ("h2_dlp4", gen_h2_dlp4),
         ("h2_cfg1", gen_h2_cfg1),
+        ("h2_cfg3p", gen_h2_cfg3p),
         ("cube", gen_cube),
         ("sample_l8", gen_sample_l8),
     ]

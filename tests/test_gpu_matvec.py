@@ -145,8 +145,10 @@ class _FakeGather:
 
 def test_row_sharded_plans_reproduce_single_gpu_bitwise(cfg0):
     """Rank r's plan (owned clusters only, padded all-gather layout, local
-    row indices) evaluated for r = 0..W-1 on one GPU: the assembled rows equal
-    the single-GPU matvec bit for bit."""
+    row indices) evaluated for r = 0..W-1 on one GPU.  Streaming every block
+    one-sided (H2B_NEAR_SYM=0) the assembled rows equal the single-GPU
+    one-sided matvec bit for bit; with the default in-rank symmetric pairing
+    they agree to rounding."""
     import torch
 
     from paper_2001_05523_b200 import distributed as DD
@@ -156,8 +158,6 @@ def test_row_sharded_plans_reproduce_single_gpu_bitwise(cfg0):
     g, m, t0, bt, b, H = cfg0
     n = H.shape[0]
     x = torch.from_numpy(np.random.default_rng(5).uniform(-1, 1, n)).cuda()
-    # the single-GPU plan streams the symmetric nearfield once per block pair
-    # (other rounding); sharded plans stream every block, as this plan does
     os.environ["H2B_NEAR_SYM"] = "0"
     try:
         one_sided = MatvecPlan(bt, b, b, H.S_dev, H.D_dev, H.far_layout, H.near_layout)
@@ -166,18 +166,28 @@ def test_row_sharded_plans_reproduce_single_gpu_bitwise(cfg0):
     assert not one_sided.info()["near_symmetric"] and H.plan().info()["near_symmetric"]
     y_ref = one_sided.apply(x)
     assert rel(y_ref.cpu().numpy(), H.matvec(x).cpu().numpy()) < 1e-14
-    for world in (2, 3):
-        ranges = DD.operator_partition(H, world)
-        chunk, pad = DD.gather_layout(ranges, n)
-        xp = x[torch.from_numpy(t0.perm).cuda()]
-        full = torch.zeros(world * chunk, dtype=torch.float64, device="cuda")
-        full[torch.from_numpy(pad).cuda()] = xp
-        y = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
-        for r in range(world):
-            op = DD.ShardedMatvec(H, r, world, _FakeGather(full))
-            op.apply(x, y)
-        assert not torch.isnan(y).any()
-        assert torch.equal(y, y_ref), world
+    for sym in (False, True):
+        for world in (2, 3):
+            ranges = DD.operator_partition(H, world)
+            chunk, pad = DD.gather_layout(ranges, n)
+            xp = x[torch.from_numpy(t0.perm).cuda()]
+            full = torch.zeros(world * chunk, dtype=torch.float64, device="cuda")
+            full[torch.from_numpy(pad).cuda()] = xp
+            y = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
+            for r in range(world):
+                if not sym:
+                    os.environ["H2B_NEAR_SYM"] = "0"
+                try:
+                    op = DD.ShardedMatvec(H, r, world, _FakeGather(full))
+                finally:
+                    os.environ.pop("H2B_NEAR_SYM", None)
+                assert op.info()["near_symmetric"] == sym
+                op.apply(x, y)
+            assert not torch.isnan(y).any()
+            if sym:
+                assert rel(y.cpu().numpy(), y_ref.cpu().numpy()) < 1e-14, world
+            else:
+                assert torch.equal(y, y_ref), world
 
 
 def test_host_vectors_pinned_pageable_device_agree(cfg0):

@@ -1,0 +1,244 @@
+"""Row-sharded operator on one GPU: every rank's assembly,
+plan and CG share computed rank by rank in one process (the all-gather of x
+replaced by the full padded vector), checked against the single-GPU operator.
+
+* sharded assembly: each rank stores only its blocks, and every stored entry
+  is the same bits as the single-GPU assembly (couplings + nearfield,
+  reference work split of containers.py:79-98 and gca.py:194-205);
+* sharded plans: the gathered rows agree with the single-GPU matvec (in-rank
+  symmetric nearfield: to rounding; DLP one-sided: bit for bit), and each
+  rank streams ~1/N of the nearfield bytes;
+* distributed CG: two processes on this GPU (gloo for the host-side
+  collectives; the kernels of the two ranks never wait on each other) take the
+  single-GPU iteration count and solution."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from .helpers import rel, sphere, trees
+
+pytestmark = pytest.mark.gpu
+
+
+class _FakeGather:
+    def __init__(self, full):
+        self.full = full
+
+    def all_gather_into_tensor(self, buf, loc):
+        buf.copy_(self.full)
+
+
+def _world(level, leaf, m=3, eta=2.0, kind="slp", threads=8):
+    from paper_2001_05523_b200 import clustering as C
+    from paper_2001_05523_b200 import gca
+    from paper_2001_05523_b200.containers import AssemblyContext
+
+    mesh = sphere(level)
+    t0, t1 = trees(mesh, leaf)
+    ctx = AssemblyContext(mesh)
+    rb = gca.build_basis(ctx, t0, gca.P0_SLP, m, 1e-4, threads=threads)
+    if kind == "slp":
+        bt, cb = C.BlockTree(t0, t0, eta), rb
+    else:
+        bt, cb = C.BlockTree(t0, t1, eta), gca.build_basis(ctx, t1, gca.P1_DLP, m, 1e-4, threads=threads)
+    H = gca.assemble_h2(ctx, kind, bt, rb, cb, 3, q_singular=4)
+    return ctx, bt, rb, cb, H
+
+
+@pytest.fixture(scope="module")
+def slp5():
+    return _world(5, 32)
+
+
+def _flat_index(off, rows, cols, ld):
+    parts = [o + np.arange(r)[:, None] * l + np.arange(c)[None, :] for o, r, c, l in zip(off, rows, cols, ld)]
+    return np.concatenate([p.ravel() for p in parts]) if parts else np.zeros(0, dtype=np.int64)
+
+
+def _same_blocks(dev_a, lay_a, idx_a, dev_b, lay_b, idx_b):
+    import torch
+
+    ia = _flat_index(lay_a.blk_off[idx_a], lay_a.blk_rows[idx_a], lay_a.blk_cols[idx_a], lay_a.blk_ld[idx_a])
+    ib = _flat_index(lay_b.blk_off[idx_b], lay_b.blk_rows[idx_b], lay_b.blk_cols[idx_b], lay_b.blk_ld[idx_b])
+    return torch.equal(dev_a[torch.from_numpy(ia).cuda()], dev_b[torch.from_numpy(ib).cuda()])
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_sharded_assembly_same_bits(slp5, world):
+    from paper_2001_05523_b200 import distributed as DD
+    from paper_2001_05523_b200.containers import FarLayout, near_layout
+
+    ctx, bt, rb, cb, H = slp5
+    ranks = np.array([rb.rank[u] for u in range(bt.row_tree.n_nodes)], dtype=np.int64)
+    stored_near = np.zeros(len(bt.near_uids), dtype=int)
+    stored = 0
+    for r in range(world):
+        sh = DD.RowShard(bt, rb, cb, r, world)
+        S, D = sh.assemble(ctx, "slp", 3, 4)
+        nl, fl = near_layout(sh.view), FarLayout(sh.view, ranks, ranks)
+        k = np.arange(len(sh.view.near_uids))
+        assert _same_blocks(D, nl, k, H.D_dev, H.near_layout, sh.view.near_index)
+        k = np.arange(len(sh.view.far_uids))
+        assert _same_blocks(S, fl, k, H.S_dev, H.far_layout, sh.view.far_index)
+        stored_near[sh.view.near_index] += 1
+        stored += D.numel()
+    assert (stored_near == 1).all()  # every near block on exactly one rank
+    if world > 1:
+        assert stored < 1.05 * H.D_dev.numel()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_plans_match_single_gpu(slp5, world):
+    import torch
+
+    from paper_2001_05523_b200 import distributed as DD
+
+    ctx, bt, rb, cb, H = slp5
+    n = H.shape[0]
+    one = H.plan().info()
+    assert one["near_symmetric"]
+    x = torch.from_numpy(np.random.default_rng(world).standard_normal(n)).cuda()
+    y_ref = H.matvec(x)
+    d_ref = torch.from_numpy(H.diagonal()).cuda()
+    y = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
+    near_bytes = []
+    for r in range(world):
+        sh = DD.RowShard(bt, rb, cb, r, world)
+        sh.assemble(ctx, "slp", 3, 4)
+        xp = x[torch.from_numpy(bt.row_tree.perm).cuda()]
+        full = torch.zeros(world * sh.chunk, dtype=torch.float64, device="cuda")
+        full[torch.from_numpy(sh.pad_index).cuda()] = xp
+        op = DD.ShardedMatvec(sh, r, world, _FakeGather(full))
+        info = op.info()
+        assert info["near_symmetric"]
+        near_bytes.append(info["near_bytes"])
+        op.apply(x, y)
+        yl = op.apply_local(xp[sh.lo : sh.hi])
+        assert torch.equal(yl, y[op.perm_dev])
+        assert torch.equal(op.diagonal_local(), d_ref[op.perm_dev])
+    assert not torch.isnan(y).any()
+    assert rel(y.cpu().numpy(), y_ref.cpu().numpy()) < 1e-14
+    # every rank streams about 1/world of the single-GPU symmetric nearfield
+    assert max(near_bytes) < 1.6 * one["near_bytes"] / world
+    assert sum(near_bytes) < 1.35 * one["near_bytes"]
+
+
+def test_sharded_dlp_bitwise():
+    """Double layer (P0 rows x P1 columns, one-sided on one GPU and sharded):
+    sharded assembly + plans reproduce the single-GPU matvec bit for bit."""
+    import torch
+
+    from paper_2001_05523_b200 import distributed as DD
+
+    ctx, bt, rb, cb, H = _world(4, 32, kind="dlp")
+    n_r, n_c = H.shape
+    x = torch.from_numpy(np.random.default_rng(2).uniform(-1, 1, n_c)).cuda()
+    y_ref = H.matvec(x)
+    world = 2
+    # DLP is not square: the column vector is gathered in full
+    from paper_2001_05523_b200.containers import FarLayout, MatvecPlan, near_layout
+
+    rr = np.array([rb.rank[u] for u in range(bt.row_tree.n_nodes)], dtype=np.int64)
+    cr = np.array([cb.rank[u] for u in range(bt.col_tree.n_nodes)], dtype=np.int64)
+    ranges = DD.partition_rows(bt.row_tree, near_layout(bt).C, FarLayout(bt, rr, cr).K, rr, world)
+    y = torch.full((n_r,), float("nan"), dtype=torch.float64, device="cuda")
+    for r, (lo, hi) in enumerate(ranges):
+        view = DD.BlockTreeView(bt, lo, hi)
+        own = np.zeros(n_r, dtype=bool)
+        own[bt.row_tree.perm[lo:hi]] = True
+        from paper_2001_05523_b200.containers import assemble_couplings, assemble_nearfield_sharded
+
+        S = assemble_couplings(ctx, "dlp", view, rb, cb, 3)
+        Dn = assemble_nearfield_sharded(ctx, "dlp", view, 3, 4, own)
+        plan = MatvecPlan(view, rb, cb, S, Dn, FarLayout(view, rr, cr), near_layout(view),
+                          owned=DD.owned_nodes(bt.row_tree, lo, hi),
+                          row_perm=np.arange(n_r, dtype=np.int64) - lo)
+        yl = torch.empty(hi - lo, dtype=torch.float64, device="cuda")
+        from paper_2001_05523_b200 import _lib
+
+        _lib.check(_lib.lib().h2b_matvec(plan.handle, x.data_ptr(), yl.data_ptr(), _lib.stream_ptr()))
+        y[torch.from_numpy(bt.row_tree.perm[lo:hi]).cuda()] = yl
+    assert torch.equal(y, y_ref)
+
+
+# ---- distributed CG: two processes on this GPU ---------------------------------
+
+class _Staged:
+    """torch.distributed through host copies (gloo has no CUDA all-gather)."""
+
+    def __init__(self, dist):
+        self.dist = dist
+        self.ReduceOp = dist.ReduceOp
+
+    def all_gather_into_tensor(self, buf, loc):
+        b = buf.cpu()
+        self.dist.all_gather_into_tensor(b, loc.cpu())
+        buf.copy_(b)
+
+    def all_reduce(self, t, op=None, group=None):
+        c = t.cpu()
+        self.dist.all_reduce(c, op=op or self.dist.ReduceOp.SUM)
+        t.copy_(c)
+
+
+def _cg_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2001_05523_b200 import distributed as DD
+        from paper_2001_05523_b200 import solver, spaces
+
+        ctx, bt, rb, cb, H = _world(5, 32, threads=2)
+        sd = _Staged(dist)
+        sh = DD.RowShard(bt, rb, cb, rank, world)
+        sh.assemble(ctx, "slp", 3, 4)
+        op = DD.ShardedMatvec(sh, rank, world, sd)
+        b = spaces.load_vector(spaces.DofSpace(spaces.P0, ctx.mesh), lambda X, t: X[..., 0] ** 2 - X[..., 1] ** 2)
+        perm = bt.row_tree.perm
+        b_loc = torch.from_numpy(b[perm[sh.lo : sh.hi]].copy()).cuda()
+        res = solver.cg(op.apply_local, b_loc, 1e-8, 500, precond_diag=op.diagonal_local(),
+                        allreduce=DD.allreduce_sum(sd))
+        x_loc = res.x.cpu().numpy()
+        parts = [None] * world
+        dist.all_gather_object(parts, (sh.lo, sh.hi, x_loc))
+        if rank == 0:
+            x = np.zeros(len(perm))
+            for lo, hi, xl in parts:
+                x[perm[lo:hi]] = xl
+            one = solver.cg(H.plan().apply_device, torch.from_numpy(b).cuda(), 1e-8, 500,
+                            precond_diag=H.diagonal())
+            xo = one.x.cpu().numpy()
+            out.put((res.iterations, one.iterations, res.converged,
+                     float(np.linalg.norm(x - xo) / np.linalg.norm(xo))))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distributed_cg_two_ranks():
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_cg_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    it_sh, it_one, conv, dx = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert conv
+    assert abs(it_sh - it_one) <= 1, (it_sh, it_one)
+    assert dx < 1e-7
