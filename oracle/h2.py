@@ -4,6 +4,7 @@ Reference: /root/reference/pkg/src/h2bem/containers.py
   ClusterBasis.forward   :201-212  leaves V^T x, parents sum_ch E_ch^T xhat_ch
   ClusterBasis.backward  :214-228  top-down yhat_ch += E_ch yhat_t, leaves y += V yhat
   H2Matrix.matvec        :254-270  permute, forward, couplings, backward, nearfield, un-permute
+  H2Matrix.rmatvec       :272-288  the same with the roles of the trees/bases swapped, S^T, D^T
   H2Matrix.diagonal      :290-301
 """
 
@@ -65,6 +66,24 @@ def matvec(row_tree, col_tree, rV, rE, rrank, cV, cE, crank, far, S, near, Dn, x
         yp[row_tree.start[t] : row_tree.end[t]] += Db @ xp[col_tree.start[s] : col_tree.end[s]]
     y = np.empty_like(yp)
     y[row_tree.perm] = yp
+    return y
+
+
+def rmatvec(row_tree, col_tree, rV, rE, rrank, cV, cE, crank, far, S, near, Dn, x):
+    """y = A^T x (containers.py:272-288): forward over the ROW basis, S_b^T
+    into the column clusters, backward over the COLUMN basis, D_b^T."""
+    xp = np.asarray(x, dtype=float)[row_tree.perm]
+    yp = np.zeros(len(col_tree.perm))
+    xhat = forward(row_tree, rV, rE, rrank, xp)
+    yhat = {}
+    for (t, s), Sb in zip(far, S):
+        c = Sb.T @ xhat[int(t)]
+        yhat[int(s)] = yhat[int(s)] + c if int(s) in yhat else c
+    backward(col_tree, cV, cE, yhat, yp)
+    for (t, s), Db in zip(near, Dn):
+        yp[col_tree.start[s] : col_tree.end[s]] += Db.T @ xp[row_tree.start[t] : row_tree.end[t]]
+    y = np.empty_like(yp)
+    y[col_tree.perm] = yp
     return y
 
 
