@@ -556,6 +556,42 @@ __device__ __forceinline__ void load_rec(const Shared& s, const int64_t* src, in
     __syncthreads();
 }
 
+// The forward products of a warp (lane c owns coefficient c, ranks <= 32), in
+// ONE summation order whichever task path runs them (a task takes the
+// one-warp path only when its whole climb fits; the value of a coefficient must
+// not depend on that, so row sharding -- which shortens climbs -- keeps the
+// single-GPU bits).  Leaf: x_hat[c] = sum_r V[r, c] x[r] (even / odd rows in
+// two chains); climb: x_hat_p[c] = E_c0^T x_hat_c0 + E_c1^T x_hat_c1 (two
+// chains each).
+__device__ __forceinline__ double leaf_coef(const double* V, int size, int k, const double* xv, int lane) {
+    double a0 = 0.0, a1 = 0.0;
+    int r = 0;
+    for (; r + 1 < size; r += 2) {
+        a0 = fma(V[(int64_t)r * k + lane], xv[r], a0);
+        a1 = fma(V[(int64_t)(r + 1) * k + lane], xv[r + 1], a1);
+    }
+    if (r < size) a0 = fma(V[(int64_t)r * k + lane], xv[r], a0);
+    return a0 + a1;
+}
+
+__device__ __forceinline__ double climb_coef(const double* E0, const double* E1, int k0, int k1, int kp,
+                                             const double* v, int lane) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int r = 0;
+    for (; r + 1 < k0; r += 2) {
+        a0 = fma(E0[r * kp + lane], v[r], a0);
+        a1 = fma(E0[(r + 1) * kp + lane], v[r + 1], a1);
+    }
+    if (r < k0) a0 = fma(E0[r * kp + lane], v[r], a0);
+    r = 0;
+    for (; r + 1 < k1; r += 2) {
+        a2 = fma(E1[r * kp + lane], v[k0 + r], a2);
+        a3 = fma(E1[(r + 1) * kp + lane], v[k0 + r + 1], a3);
+    }
+    if (r < k1) a2 = fma(E1[r * kp + lane], v[k0 + r], a2);
+    return (a0 + a1) + (a2 + a3);
+}
+
 // Forward task on one warp (chain latency: no block barriers).  Lane c owns
 // output coefficient c (ranks <= 32), the leaf has <= 64 rows; operands in
 // shared memory, the climb's transfer matrices copied by the warp (cp.async)
@@ -587,14 +623,7 @@ __device__ void forward_warp(const double* __restrict__ c_V, const double* __res
     mbar_wait(s.bar, s.parity);
     double own = 0.0;
     if (lane < k) {
-        double a0 = 0.0, a1 = 0.0;
-        int r = 0;
-        for (; r + 1 < size; r += 2) {
-            a0 = fma(V[(int64_t)r * k + lane], s.va[r], a0);
-            a1 = fma(V[(int64_t)(r + 1) * k + lane], s.va[r + 1], a1);
-        }
-        if (r < size) a0 = fma(V[(int64_t)r * k + lane], s.va[r], a0);
-        own = a0 + a1;
+        own = leaf_coef(V, size, k, s.va, lane);
         ll_store(xhat + 2 * (xhat_off + lane), own, epoch);
     }
     mark(s.mark, 0);
@@ -621,21 +650,7 @@ __device__ void forward_warp(const double* __restrict__ c_V, const double* __res
         if (j < 2) mark(s.mark, 1 + 2 * j);
         own = 0.0;
         if (lane < kp) {
-            const double* e1 = buf + p0;
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-            int r = 0;
-            for (; r + 1 < k0; r += 2) {
-                a0 = fma(buf[r * kp + lane], s.va[r], a0);
-                a1 = fma(buf[(r + 1) * kp + lane], s.va[r + 1], a1);
-            }
-            if (r < k0) a0 = fma(buf[r * kp + lane], s.va[r], a0);
-            r = 0;
-            for (; r + 1 < k1; r += 2) {
-                a2 = fma(e1[r * kp + lane], s.va[k0 + r], a2);
-                a3 = fma(e1[(r + 1) * kp + lane], s.va[k0 + r + 1], a3);
-            }
-            if (r < k1) a2 = fma(e1[r * kp + lane], s.va[k0 + r], a2);
-            own = (a0 + a1) + (a2 + a3);
+            own = climb_coef(buf, buf + p0, k0, k1, kp, s.va, lane);
             ll_store(xhat + 2 * (lv[5] + lane), own, epoch);
         }
         if (j < 2) mark(s.mark, 2 + 2 * j);
@@ -683,7 +698,11 @@ __device__ void task_forward(const double* __restrict__ c_V, const double* __res
             kk = kp;
         }
     }
-    small_cols_dot(V, size, k, s.va, s.vb, s.red);  // own coefficients stay in s.vb
+    if (k <= 32) {  // the one-warp order (see leaf_coef)
+        if (threadIdx.x < k) s.vb[threadIdx.x] = leaf_coef(V, size, k, s.va, threadIdx.x);
+    } else {
+        small_cols_dot(V, size, k, s.va, s.vb, s.red);  // own coefficients stay in s.vb
+    }
     __syncthreads();
     mark(s.mark, 0);
     {
@@ -711,7 +730,10 @@ __device__ void task_forward(const double* __restrict__ c_V, const double* __res
         cp_async_wait_all();
         __syncthreads();
         if (j < 2) mark(s.mark, 1 + 2 * j);
-        if (in_smem) {
+        if (in_smem && kp <= 32) {  // the one-warp order (see climb_coef)
+            if (threadIdx.x < kp) s.vb[threadIdx.x] = climb_coef(buf, buf + n0, k0, k1, kp, s.va, threadIdx.x);
+            __syncthreads();
+        } else if (in_smem) {
             small_cols_dot(buf, k0 + k1, kp, s.va, s.vb, s.red);
             __syncthreads();
         } else {

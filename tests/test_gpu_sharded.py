@@ -153,6 +153,9 @@ def test_sharded_dlp_bitwise():
 
         S = assemble_couplings(ctx, "dlp", view, rb, cb, 3)
         Dn = assemble_nearfield_sharded(ctx, "dlp", view, 3, 4, own)
+        nl, fl = near_layout(view), FarLayout(view, rr, cr)
+        assert _same_blocks(Dn, nl, np.arange(len(view.near_uids)), H.D_dev, H.near_layout, view.near_index)
+        assert _same_blocks(S, fl, np.arange(len(view.far_uids)), H.S_dev, H.far_layout, view.far_index)
         plan = MatvecPlan(view, rb, cb, S, Dn, FarLayout(view, rr, cr), near_layout(view),
                           owned=DD.owned_nodes(bt.row_tree, lo, hi),
                           row_perm=np.arange(n_r, dtype=np.int64) - lo)
