@@ -1,35 +1,47 @@
-"""Benchmark: H^2-matvec DoF/s (+ nearfield quadrature pairs/s), fp64, B200.
+"""Benchmark: H^2-matvec DoF/s + nearfield quadrature pairs/s, fp64, B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 1]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 3]
 
-Workload (BASELINE.json configs[1], the metric's single-GPU configuration):
-sphere refined 6x (32 768 triangles), piecewise-constant single-layer
-operator, GCA H^2 with m = 4, eta = 2, leaf 64, eps_aca = 1e-4 (reference
-default), regular Gauss order 3, Sauter-Schwab order 4; x ~ N(0,1) seed 1.
-Synthetic mesh, no dataset.
+Workload (default, BASELINE.json configs[3] -- the configuration the metric
+is quoted on at 1/2/4/8 GPUs; it fits one GPU): sphere refined 9x
+(2 097 152 triangles), piecewise-constant single-layer operator, GCA H^2 with
+m = 5, eta = 1.5, leaf 64, eps_aca = 1e-4 (reference default), regular Gauss
+order 3, Sauter-Schwab order 4; x ~ N(0,1) seed 3; CG right-hand side the P0
+load of x1^2 - x2^2.  Synthetic mesh, no dataset.  The GCA basis is built on
+the device (k_gca_columns + k_gca_aca); its per-cluster agreement with the
+reference's own basis is reported (tests/golden/cfg3_basis.npz).
 
-A step is one H^2 matvec y = A x of that operator (inputs resident in HBM).
-L2 is flushed (256 MiB write) between timed steps, so every step streams its
-operator (202 MB) from HBM; each step is bracketed by its own CUDA events and
-`value` = n x K / (sum of step times).  The nearfield assembly (Sauter-Schwab
-table + regular pair blocks) is timed in the same run and reported under
-`nearfield` (pairs/s, FP64 roofline).  `e2e` is the same matvec through the
-public API (H2Matrix.matvec on a pinned host numpy vector: H2D + kernels +
-D2H every step).
+A step is one H^2 matvec y = A x (inputs resident in HBM; 14.9 GB of operator
+per matvec, far above the 126 MB L2, and L2 flushed by a 256 MiB write
+between steps).  `value` = DoF x K / (sum of step times), max over ranks.
+The nearfield assembly (touching-pair classification, Sauter-Schwab table,
+regular pair blocks) and the coupling assembly are timed in the same run
+(`nearfield`, pairs/s, FP64 roofline), and so is the CG solve (`cg`).  `e2e`
+is the same matvec through the public API on a plain (pageable) numpy vector
+-- the call a reference user makes: H2Matrix.matvec(x) with the H2D copy,
+the kernel and the D2H copy inside the timed region.
 
---impl reference times the reference's CPU algorithm (the oracle port in
-oracle/, the reference itself cannot travel to the GPU box) on the same
-operator, on rank 0 only.
+Multi-GPU: `--gpus N` launches N ranks itself (torch.distributed.run) unless
+WORLD_SIZE is set, in which case it must equal N.  Rows are sharded by
+contiguous row-leaf ranges (distributed.RowShard): each rank assembles and
+stores only its own share of the operator (nearfield, couplings, touching
+pairs), x is all-gathered over NCCL once per matvec, each rank writes its own
+rows; weak in memory, strong in work ("scaling": "strong": the problem is
+fixed); timing = max over ranks; CG with all-reduced scalars.
 
-Multi-GPU (torchrun, one rank per GPU): rows are sharded by contiguous
-row-leaf ranges (upper clusters redundant), x is all-gathered over NCCL
-once per matvec, each rank writes its own rows; strong scaling of the fixed
-config-1 problem; timing = max over ranks.
+--impl reference: the reference's CPU algorithm on this host's cores (the
+oracle port in oracle/: the reference cannot travel to the GPU box), on the
+same configuration, through oracle code only (it never imports
+paper_2001_05523_b200): structure by oracle/structure.py (pinned bit-exact
+to the reference), each step the reference matvec restricted to bounded row
+slices (oracle.h2.RowSlice, one slice per core in parallel), plus a seeded
+sample of near blocks through the oracle quadrature.
 """
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import time
@@ -41,26 +53,35 @@ sys.path.insert(0, ROOT)
 os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
 
 CONFIGS = {
-    # name: level, leaf, eta, m, q_reg, q_ss, kind, seed, dist
-    "1": dict(level=6, leaf=64, eta=2.0, m=4, q_reg=3, q_ss=4, kind="slp", seed=1, dist="normal",
-              desc="sphere L6 (32768 tri) SLP P0, GCA m=4 eta=2 leaf=64 eps=1e-4, q 3/4"),
-    "0": dict(level=4, leaf=32, eta=2.0, m=3, q_reg=3, q_ss=4, kind="slp", seed=0, dist="uniform",
-              desc="sphere L4 (2048 tri) SLP P0, GCA m=3 eta=2 leaf=32 eps=1e-4, q 3/4"),
-    "2s": dict(level=8, leaf=64, eta=2.0, m=4, q_reg=3, q_ss=5, kind="slp", seed=2, dist="uniform",
-               desc="sphere L8 (524288 tri) SLP P0, GCA m=4 eta=2 leaf=64 eps=1e-4, q 3/5"),
+    # name: level, leaf, eta, m, q_reg, q_ss, kind, seed, dist, basis
+    "3": dict(level=9, leaf=64, eta=1.5, m=5, q_reg=3, q_ss=4, kind="slp", seed=3, dist="normal", basis="device",
+              golden="cfg3_basis.npz",
+              desc="config 3: sphere L9 (2097152 tri) SLP P0, GCA m=5 eta=1.5 leaf=64 eps=1e-4, q 3/4, CG"),
+    "1": dict(level=6, leaf=64, eta=2.0, m=4, q_reg=3, q_ss=4, kind="slp", seed=1, dist="normal", basis="host",
+              golden="h2_cfg1.npz",
+              desc="config 1: sphere L6 (32768 tri) SLP P0, GCA m=4 eta=2 leaf=64 eps=1e-4, q 3/4"),
+    "0": dict(level=4, leaf=32, eta=2.0, m=3, q_reg=3, q_ss=4, kind="slp", seed=0, dist="uniform", basis="host",
+              golden="h2_cfg0.npz",
+              desc="config 0: sphere L4 (2048 tri) SLP P0, GCA m=3 eta=2 leaf=32 eps=1e-4, q 3/4"),
+    "2s": dict(level=8, leaf=64, eta=2.0, m=4, q_reg=3, q_ss=5, kind="slp", seed=2, dist="uniform", basis="device",
+               golden=None,
+               desc="config 2 (single layer): sphere L8 (524288 tri) SLP P0, GCA m=4 eta=2 leaf=64 eps=1e-4, q 3/5"),
 }
+DEFAULT_CONFIG = "3"
 EPS_ACA = 1e-4
 METRIC = "H2-matvec DoF/s (fp64), + nearfield quad pairs/s"
+PROFILE = os.path.join(ROOT, "profiles", "r02_ncu_full_raw.csv")
 
+
+# ---------------------------------------------------------------------------
+# measurement helpers
 
 def peaks():
-    p = {"hbm_gbs": None, "fp64_tflops": None, "hbm_src": None, "fp64_src": None}
     try:
         mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-        p["hbm_gbs"], p["hbm_src"] = float(mp["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
+        return float(mp["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)"
     except Exception:
-        p["hbm_gbs"], p["hbm_src"] = 6650.0, "B200_PROFILING.md fallback"
-    return p
+        return 6650.0, "B200_PROFILING.md fallback"
 
 
 def measure_fp64_peak():
@@ -87,7 +108,7 @@ class Clocks:
                  "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -119,19 +140,11 @@ class Clocks:
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
-
-
-
-def ncu_traffic(kernel, path=None):
-    """DRAM bytes (read + write) of one launch of `kernel` from the committed
+def ncu_traffic(kernel, path=PROFILE):
+    """DRAM bytes (read + write) of one launch of `kernel` in the committed
     ncu --set full capture (profiles/), or None."""
     import csv
-    path = path or os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01s8_ncu_full_raw.csv")
+
     if not os.path.exists(path):
         return None
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
@@ -147,47 +160,9 @@ def ncu_traffic(kernel, path=None):
         return None
     for r in rows[2:]:
         if kernel in r[ik]:
-            return float(r[ir]) * scale.get(units[ir], 1) + float(r[iw]) * scale.get(units[iw], 1)
+            return float(r[ir].replace(",", "")) * scale.get(units[ir], 1) + \
+                float(r[iw].replace(",", "")) * scale.get(units[iw], 1)
     return None
-
-
-def build_problem(cfg, threads):
-    """Host setup (untimed): mesh, trees, block tree, GCA basis."""
-    from paper_2001_05523_b200 import clustering as C
-    from paper_2001_05523_b200 import gca, spaces
-    from paper_2001_05523_b200.containers import AssemblyContext
-    from paper_2001_05523_b200.mesh import sphere_mesh
-
-    mesh = sphere_mesh(cfg["level"])
-    ctx = AssemblyContext(mesh)
-    tree = C.build_cluster_tree(spaces.DofSpace(spaces.P0, mesh).support_boxes(), cfg["leaf"])
-    bt = C.BlockTree(tree, tree, cfg["eta"])
-    basis = gca.build_basis(ctx, tree, gca.P0_SLP, cfg["m"], EPS_ACA, threads=threads)
-    return mesh, ctx, tree, bt, basis
-
-
-def flop_counts(ctx, bt, cfg, slp_jobs):
-    """Nearfield work (SURVEY.md 8(d) convention: 12 flops per regular SLP
-    kernel evaluation, 36 per Sauter-Schwab evaluation).  `pairs` counts the
-    matrix entries (= the reference's panel pairs); the symmetric single-layer
-    matrix integrates one pair per entry pair {(a,b), (b,a)}, so the FLOP rates
-    are computed on the pairs actually integrated."""
-    from paper_2001_05523_b200.containers import near_layout
-
-    t = ctx.dmesh.touch()
-    n_id, n_edge, n_vert = (int(c) for c in t.case_counts)
-    q, qs = cfg["q_reg"], cfg["q_ss"]
-    entries = near_layout(bt).entries
-    half = t.half_list is not None
-    touch_eval = n_id + (n_edge + n_vert) // 2 if half else t.n_pairs
-    regular = entries - t.n_pairs
-    regular_eval = slp_jobs.evaluated - touch_eval
-    ev_reg = regular_eval * q**4
-    f = 2 if half else 1
-    ev_sing = n_id * 6 * qs**4 + (n_edge // f) * 2 * 5 * qs**4 + (n_vert // f) * 2 * 2 * qs**4
-    return dict(pairs=entries, regular_pairs=regular, singular_pairs=t.n_pairs, regular_evaluated=regular_eval,
-                singular_evaluated=touch_eval, reg_flops=12.0 * ev_reg, sing_flops=36.0 * ev_sing,
-                evals=ev_reg + ev_sing)
 
 
 def ev_time(torch, fn, reps=1):
@@ -202,72 +177,152 @@ def ev_time(torch, fn, reps=1):
     return s.elapsed_time(e) / 1e3 / reps
 
 
+def dist_env():
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def h2b_env():
+    return {k: v for k, v in sorted(os.environ.items()) if k.startswith("H2B_")}
+
+
+def draw_x(cfg, n):
+    rng = np.random.default_rng(cfg["seed"])
+    return rng.standard_normal(n) if cfg["dist"] == "normal" else rng.uniform(-1.0, 1.0, n)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+def flop_counts(table_pairs, slp_jobs, cfg):
+    """SURVEY.md 8(d) convention: 12 flops per regular SLP kernel evaluation,
+    36 per Sauter-Schwab evaluation; pair counts as integrated (the symmetric
+    single-layer matrix integrates one pair per entry pair)."""
+    n_id, n_edge, n_vert = table_pairs
+    q, qs = cfg["q_reg"], cfg["q_ss"]
+    touch_eval = n_id + n_edge + n_vert
+    reg_eval = slp_jobs.evaluated - touch_eval
+    ev_sing = n_id * 6 * qs**4 + n_edge * 2 * 5 * qs**4 + n_vert * 2 * 2 * qs**4
+    return dict(regular_evaluated=reg_eval, singular_evaluated=touch_eval, reg_flops=12.0 * reg_eval * q**4,
+                sing_flops=36.0 * ev_sing)
+
+
 def run_ours(args, cfg):
     import torch
 
     ws, rank, local = dist_env()
-    # H2B_DIST_BACKEND=gloo: functional check of the N-rank orchestration on
-    # fewer GPUs (ranks share a device; not a measurement)
     backend = os.environ.get("H2B_DIST_BACKEND", "nccl")
-    if backend != "nccl":
+    if backend != "nccl":  # orchestration check on fewer GPUs (not a measurement)
         local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
-    pg = None
+    dist = None
     if ws > 1:
-        import torch.distributed as dist
+        import torch.distributed as tdist
 
         if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
-            dist.init_process_group(backend)
-        pg = dist
-    from paper_2001_05523_b200 import gca, kernels
-    from paper_2001_05523_b200.containers import (H2Matrix, assemble_couplings, near_layout, near_slp_jobs)
+            tdist.init_process_group(backend)
+        dist = tdist
+    from paper_2001_05523_b200 import clustering as C
     from paper_2001_05523_b200 import distributed as DD
+    from paper_2001_05523_b200 import gca, kernels, solver, spaces
+    from paper_2001_05523_b200.containers import (AssemblyContext, H2Matrix, assemble_couplings,
+                                                  assemble_nearfield_sharded, coupling_slp_jobs, near_layout,
+                                                  near_slp_jobs, near_slp_jobs_sharded)
+    from paper_2001_05523_b200.mesh import sphere_mesh
 
-    threads = max(1, (os.cpu_count() or 8) // max(ws, 1))
-    t0 = time.time()
-    mesh, ctx, tree, bt, basis = build_problem(cfg, threads)
-    setup_s = time.time() - t0
+    torch.cuda.reset_peak_memory_stats()
+    threads = max(1, (os.cpu_count() or 8) // ws)
+    T = {}
+    t0 = time.perf_counter()
+    mesh = sphere_mesh(cfg["level"])
+    T["mesh_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ctx = AssemblyContext(mesh)
+    tree = C.build_cluster_tree(spaces.DofSpace(spaces.P0, mesh).support_boxes(), cfg["leaf"])
+    bt = C.BlockTree(tree, tree, cfg["eta"])
+    T["trees_s"] = time.perf_counter() - t0
+    device_basis = cfg["basis"] == "device"
+    if device_basis:
+        gca.build_basis(ctx, tree, gca.P0_SLP, cfg["m"], EPS_ACA, device=True)  # warm (first-use costs)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    basis = gca.build_basis(ctx, tree, gca.P0_SLP, cfg["m"], EPS_ACA, device=device_basis, threads=threads)
+    torch.cuda.synchronize()
+    T["basis_s"] = time.perf_counter() - t0
+    n = tree.n_dofs
+    perm = tree.perm
 
-    # ---- nearfield assembly on the device (timed) --------------------------------
-    lay = near_layout(bt)
-    Dn = torch.zeros(max(lay.total, 1), dtype=torch.float64, device="cuda")
-    jobs = near_slp_jobs(bt)
+    shard = DD.RowShard(bt, basis, basis, rank, ws) if ws > 1 else None
+    view = shard.view if shard is not None else bt
+    lo, hi = (shard.lo, shard.hi) if shard is not None else (0, n)
+
+    # ---- nearfield assembly on the device (timed) ----------------------------
     clocks = Clocks(local)
-    ctx.dmesh.touch()
-    t_touch = ev_time(torch, lambda: kernels.TouchTable(ctx.dmesh))  # warm: classification of all pairs
-    slp_jobs = kernels.SlpJobs(ctx.dmesh, cfg["q_reg"], jobs, tree.perm.astype(np.int32), tree.perm.astype(np.int32))
-    table = kernels.SingularTable(ctx.dmesh, "slp", cfg["q_ss"], compute=False)
+    dm = ctx.dmesh
+    t_touch = ev_time(torch, lambda: kernels.TouchTable(dm))  # classification of all touching pairs
+    dm.touch()
+    table = kernels.SingularTable(dm, "slp", cfg["q_ss"], compute=False)
+    own = shard.own_panels if shard is not None else None
+    jobs = near_slp_jobs_sharded(view) if shard is not None else near_slp_jobs(bt)
+    sj = kernels.SlpJobs(dm, cfg["q_reg"], jobs, perm.astype(np.int32), perm.astype(np.int32))
+    lay = near_layout(view)
+    Dn = torch.zeros(max(lay.total, 1), dtype=torch.float64, device="cuda")
     for _ in range(2):
-        table.compute()
-        slp_jobs.run(table, Dn)
-    nf_reps = 20
-    t_sing = ev_time(torch, table.compute, nf_reps)
-    t_reg = ev_time(torch, lambda: slp_jobs.run(table, Dn), nf_reps)
-    fc = flop_counts(ctx, bt, cfg, slp_jobs)
-    S = assemble_couplings(ctx, "slp", bt, basis, basis, cfg["q_reg"])
-    # coupling matrices S_b = G[pivots_t, pivots_s] (gca.assemble_h2), host job list + device quadrature
-    t_cpl = ev_time(torch, lambda: assemble_couplings(ctx, "slp", bt, basis, basis, cfg["q_reg"]), 3)
-    n_cpl_pairs = int(sum(basis.rank[int(t)] * basis.rank[int(u)] for t, u in bt.far_uids))
-    H = H2Matrix.from_device(bt, basis, basis, S, Dn)
-    n = H.shape[0]
-
-    # ---- matvec ------------------------------------------------------------------
-    rng = np.random.default_rng(cfg["seed"])
-    x_host = rng.standard_normal(n) if cfg["dist"] == "normal" else rng.uniform(-1, 1, n)
-    if ws > 1:
-        op = DD.ShardedMatvec(H, rank, ws, pg)
+        table.compute(own)
+        sj.run(table, Dn)
+    nf_reps = 3 if n > 1_000_000 else 10
+    t_sing = ev_time(torch, lambda: table.compute(own), nf_reps)
+    t_reg = ev_time(torch, lambda: sj.run(table, Dn), nf_reps)
+    touch = dm.touch()
+    if own is not None:
+        touch.subset(own, half=True)
+        so = touch._subset[3]
+        case = (int(so[1] - so[0]), int(so[2] - so[1]), int(so[3] - so[2]))
     else:
+        touch.ensure_half()
+        ho = touch.half_off
+        case = (int(ho[1] - ho[0]), int(ho[2] - ho[1]), int(ho[3] - ho[2]))
+    fc = flop_counts(case, sj, cfg)
+    near_pairs = lay.entries
+    # couplings: end to end (host job list + kernel) and the kernel alone
+    t1 = time.perf_counter()
+    S = assemble_couplings(ctx, "slp", view, basis, basis, cfg["q_reg"])
+    torch.cuda.synchronize()
+    t_cpl_e2e = time.perf_counter() - t1
+    cj, rp, cp, flay = coupling_slp_jobs(view, basis, basis)
+    cjobs = kernels.SlpJobs(dm, cfg["q_reg"], cj, rp, cp)
+    Sc = torch.zeros_like(S)
+    cjobs.run(None, Sc)
+    t_cpl = ev_time(torch, lambda: cjobs.run(None, Sc), nf_reps)
+    assert torch.equal(Sc, S)
+    cpl_pairs = flay.entries
+    cpl_flops = 12.0 * cjobs.evaluated * cfg["q_reg"] ** 4
+
+    # ---- operator + matvec ------------------------------------------------------
+    if shard is not None:
+        shard.S, shard.D = S, Dn
+        # the timed assembly above is the rank's sharded assembly; check it is
+        assert torch.equal(Dn, assemble_nearfield_sharded(ctx, "slp", view, cfg["q_reg"], cfg["q_ss"], own))
+        op = DD.ShardedMatvec(shard, rank, ws, dist)
+        plan = op.plan
+        H = None
+    else:
+        H = H2Matrix.from_device(bt, basis, basis, S, Dn)
         op = DD.LocalMatvec(H)
+        plan = op.plan
+    info = plan.info()
+    x_host = draw_x(cfg, n)
     x = torch.from_numpy(x_host).cuda()
     y = torch.empty(n, dtype=torch.float64, device="cuda")
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
-    for _ in range(max(args.warmup, 3)):
+    warm = max(args.warmup, 3)
+    for _ in range(warm):
         op.apply(x, y)
     torch.cuda.synchronize()
-    if pg:
-        pg.barrier()
+    if dist:
+        dist.barrier()
     K = args.steps
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
@@ -279,38 +334,58 @@ def run_ours(args, cfg):
         ends[k].record()
     torch.cuda.synchronize()
     step_s = np.array([s.elapsed_time(e) / 1e3 for s, e in zip(starts, ends)])
+    # the kernel alone (k_matvec: one launch per step), same stream
+    from paper_2001_05523_b200 import _lib
+
+    xin = op.xbuf if shard is not None else x
+    yout = op.yloc if shard is not None else y
+    kst = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ken = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    for k in range(K):
+        flush.fill_(float(k))
+        kst[k].record()
+        _lib.check(_lib.lib().h2b_matvec(plan.handle, xin.data_ptr(), yout.data_ptr(), _lib.stream_ptr()))
+        ken[k].record()
+    torch.cuda.synchronize()
+    kern_s = float(np.mean([s.elapsed_time(e) / 1e3 for s, e in zip(kst, ken)]))
     clk = clocks.stop()
     total = float(step_s.sum())
-    if pg:
-        tt = torch.tensor([total], dtype=torch.float64, device="cuda")
-        pg.all_reduce(tt, op=pg.ReduceOp.MAX)
-        total = float(tt.item())
-    mean_step = total / K
-    dofs_per_s = n * K / total
+    tmax = {"total": total, "touch": t_touch, "sing": t_sing, "reg": t_reg, "cpl": t_cpl, "cpl_e2e": t_cpl_e2e}
+    sums = {"near_pairs": float(near_pairs), "cpl_pairs": float(cpl_pairs),
+            "flops": fc["reg_flops"] + fc["sing_flops"], "cpl_flops": cpl_flops}
+    if dist:
+        tt = torch.tensor(list(tmax.values()), dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        tmax = dict(zip(tmax, tt.tolist()))
+        ss = torch.tensor(list(sums.values()), dtype=torch.float64, device="cuda")
+        dist.all_reduce(ss, op=dist.ReduceOp.SUM)
+        sums = dict(zip(sums, ss.tolist()))
+    mean_step = tmax["total"] / K
+    dofs_per_s = n * K / tmax["total"]
 
-    # ---- parity spot-check of this run against the oracle is in the test-suite;
-    # here: e2e through the public API with pinned host buffers ----------------------
+    # ---- e2e through the public API ------------------------------------------
     e2e = None
     if ws == 1:
-        xp = torch.from_numpy(x_host).pin_memory()
-        xh = xp.numpy()
+        xh = np.ascontiguousarray(x_host)  # plain pageable numpy: the reference caller's vector
         for _ in range(3):
             H.matvec(xh)
-        torch.cuda.synchronize()
+        ke = max(10, min(K, 50))
         t1 = time.perf_counter()
-        ke = max(10, K)
         for _ in range(ke):
             yh = H.matvec(xh)
         dt = time.perf_counter() - t1
+        xpin = torch.from_numpy(x_host).pin_memory().numpy()
+        t1 = time.perf_counter()
+        for _ in range(ke):
+            H.matvec(xpin)
+        dtp = time.perf_counter() - t1
         e2e = {"value": n * ke / dt, "unit": "DoF/s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
-               "timer": "host wall clock around H2Matrix.matvec(numpy) incl. H2D/D2H, synchronised"}
+               "timer": "host wall clock around H2Matrix.matvec(numpy, pageable) incl. H2D/D2H, synchronised",
+               "pinned_input_value": n * ke / dtp}
         del yh
     else:
-        # row-sharded public entry (ShardedMatvec.apply): every rank copies the
-        # full x from pinned host memory, applies its share (all-gather inside)
-        # and reads its own rows back; wall clock, max over ranks
         xp = torch.from_numpy(x_host).pin_memory()
-        yp = torch.empty(op.hi - op.lo, dtype=torch.float64).pin_memory()
+        yp = torch.empty(hi - lo, dtype=torch.float64).pin_memory()
         xd = torch.empty_like(x)
 
         def e2e_step():
@@ -321,231 +396,394 @@ def run_ours(args, cfg):
 
         for _ in range(3):
             e2e_step()
-        pg.barrier()
-        torch.cuda.synchronize()
+        dist.barrier()
+        ke = max(10, min(K, 50))
         t1 = time.perf_counter()
-        ke = max(10, K)
         for _ in range(ke):
             e2e_step()
         dt = torch.tensor([time.perf_counter() - t1], dtype=torch.float64, device="cuda")
-        pg.all_reduce(dt, op=pg.ReduceOp.MAX)
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         e2e = {"value": n * ke / float(dt.item()), "unit": "DoF/s", "h2d_bytes_per_step": 8 * n,
-               "d2h_bytes_per_step": 8 * (op.hi - op.lo),
-               "timer": "host wall clock per rank around H2D of x + ShardedMatvec.apply + D2H of own rows, max over ranks"}
+               "d2h_bytes_per_step": 8 * (hi - lo),
+               "timer": "host wall clock per rank around H2D of x (pinned) + ShardedMatvec.apply + D2H of own "
+                        "rows, max over ranks"}
 
-    # ---- the rest of the pipeline on the device (reported, untimed by the metric) ----
-    extra = {}
+    # ---- CG solve of the Galerkin system --------------------------------------
+    b = spaces.load_vector(spaces.DofSpace(spaces.P0, mesh), lambda X, tt: X[..., 0] ** 2 - X[..., 1] ** 2)
     if ws == 1:
-        from paper_2001_05523_b200 import solver, spaces
-
-        gca.build_basis(ctx, tree, gca.P0_SLP, cfg["m"], EPS_ACA, device=True)  # warm (first-use costs)
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
-        bdev = gca.build_basis(ctx, tree, gca.P0_SLP, cfg["m"], EPS_ACA, device=True)
-        torch.cuda.synchronize()
-        t_gca = time.perf_counter() - t1
-        same = np.mean([basis.rank[u] == bdev.rank[u] and np.array_equal(basis.pivots[u], bdev.pivots[u])
-                        for u in range(tree.n_nodes)])
-        extra["gca_basis"] = {"device_s": t_gca, "host_s": setup_s, "host_threads": threads,
-                              "pivots_identical_to_host_frac": float(same),
-                              "note": "host_s = whole host setup (mesh, trees, reference-identical GCA basis)"}
-        b = spaces.load_vector(spaces.DofSpace(spaces.P0, mesh), lambda X, tt: X[..., 0] ** 2 - X[..., 1] ** 2)
         bd = torch.from_numpy(b).cuda()
         diag = H.diagonal()
-        plan = H.plan()
-        solver.cg(lambda v: plan.apply_device(v), bd, EPS_ACA / 10.0, 2000, precond_diag=diag)  # warm
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
-        res = solver.cg(lambda v: plan.apply_device(v), bd, EPS_ACA / 10.0, 2000, precond_diag=diag)
-        torch.cuda.synchronize()
-        t_cg = time.perf_counter() - t1
-        extra["cg"] = {"iterations": res.iterations, "converged": res.converged, "residual": res.residual,
-                       "ms": t_cg * 1e3, "ms_per_iteration": t_cg * 1e3 / max(res.iterations, 1),
-                       "rhs": "P0 load of x1^2 - x2^2, Jacobi, eps_solver = eps_aca / 10 (solver.cg)"}
+        run_cg = lambda: solver.cg(plan.apply_device, bd, EPS_ACA / 10.0, 2000, precond_diag=diag)  # noqa: E731
+    else:
+        bd = torch.from_numpy(b[perm[lo:hi]].copy()).cuda()
+        dloc = op.diagonal_local()
+        red = DD.allreduce_sum(dist)
+        run_cg = lambda: solver.cg(op.apply_local, bd, EPS_ACA / 10.0, 2000, precond_diag=dloc,  # noqa: E731
+                                   allreduce=red)
+    run_cg()  # warm
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t1 = time.perf_counter()
+    res = run_cg()
+    torch.cuda.synchronize()
+    t_cg = time.perf_counter() - t1
+    if dist:
+        tt = torch.tensor([t_cg], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_cg = float(tt.item())
+    cg = {"iterations": res.iterations, "converged": res.converged, "residual": res.residual, "s": t_cg,
+          "ms_per_iteration": t_cg * 1e3 / max(res.iterations, 1),
+          "rhs": "P0 load of x1^2 - x2^2, Jacobi, eps_solver = eps_aca / 10 (solver.cg, device-resident)"}
 
-    # ---- roofline ---------------------------------------------------------------
-    pk = peaks()
-    mv_bytes = H.matvec_bytes()  # every operator entry once
-    # what the plan streams (single GPU: a symmetric nearfield once per block pair)
-    st_bytes = H.streamed_bytes() if ws == 1 else mv_bytes
+    # ---- rooflines -------------------------------------------------------------
+    hbm, hbm_src = peaks()
     fp64_peak, fp64_src = measure_fp64_peak() if rank == 0 else (None, None)
-    nf_time = t_sing + t_reg
+    # every operator entry once, each basis in both roles, x and
+    # y -- for this rank: its nearfield + couplings, the whole column basis
+    # (forward), its row clusters' basis, all of x, its rows of y
+    rflo = basis.storage_floats()
+    rb_own = rflo
+    if shard is not None:
+        own_nodes = set(shard.owned.tolist())
+        rb_own = sum(basis.V[u].size for u in basis.V if u in own_nodes) + \
+            sum(basis.E[u].size for u in basis.E if u in own_nodes)
+    alg_bytes = 8 * (lay.entries + flay.entries + rflo + rb_own + n + (hi - lo))
+    streamed = alg_bytes - 8 * (lay.entries + flay.entries) + info["near_bytes"] + info["coupling_bytes"]
+    achieved = alg_bytes / kern_s / 1e9
+    nf_time = tmax["sing"] + tmax["reg"]
     result = {
         "metric": METRIC,
         "value": dofs_per_s,
         "unit": "DoF/s",
         "n_gpus": ws,
         "steps": K,
-        "warmup": max(args.warmup, 3),
+        "warmup": warm,
         "ms_per_step": mean_step * 1e3,
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (generated sphere mesh, x ~ N(0,1) seed 1)",
-        "config": {"workload": f"config {args.config}: {cfg['desc']}", "n_dofs": n,
-                   "matvec_bytes": mv_bytes, "l2": "flushed (256 MiB write) between timed steps",
-                   "parallelism": f"row-shard x{ws}" if ws > 1 else "single GPU"},
+        "data": f"synthetic (generated sphere mesh, x ~ {'N(0,1)' if cfg['dist'] == 'normal' else 'U(-1,1)'} "
+                f"seed {cfg['seed']})",
+        "config": {"workload": cfg["desc"], "n_dofs": n, "matvec_bytes_algorithmic": alg_bytes if ws == 1 else None,
+                   "operator_gb": round(8 * (near_layout(bt).entries + flay.entries) / 1e9, 3) if ws == 1 else None,
+                   "l2": "inputs far above L2 (operator streamed from HBM) and L2 flushed (256 MiB write) "
+                         "between timed steps",
+                   "basis": "device GCA (k_gca_columns + k_gca_aca)" if device_basis else
+                            "host GCA (reference-identical pivots)",
+                   "parallelism": f"row-shard x{ws} (sharded assembly + storage, NCCL all-gather of x)"
+                                  if ws > 1 else "single GPU",
+                   "env": h2b_env()},
         "gpu_launches": K,
         "roofline": {"bound": "hbm", "kernel": "k_matvec (fused forward + coupling + backward + nearfield)",
-                     "achieved": mv_bytes / mean_step / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": mv_bytes / mean_step / 1e9 / pk["hbm_gbs"], "traffic": ncu_traffic("k_matvec"),
-                     "traffic_source": "profiles/r01s8_ncu_full_raw.csv (ncu --set full, one launch, DRAM read+write bytes)",
-                     "algorithmic_bytes": mv_bytes, "kernel_ms": mean_step * 1e3, "peak_source": pk["hbm_src"],
-                     "streamed_bytes": st_bytes, "streamed_frac": st_bytes / mean_step / 1e9 / pk["hbm_gbs"],
-                     "note": "algorithmic = SURVEY 8(d) (every operator entry once); the plan streams the "
-                             "symmetric single-layer nearfield once per block pair (streamed_bytes), so ncu "
-                             "traffic sits below the algorithmic bytes"},
+                     "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": ncu_traffic("k_matvec"),
+                     "traffic_source": os.path.relpath(PROFILE, ROOT) + " (ncu --set full, one launch, dram read+write)",
+                     "algorithmic_bytes": alg_bytes, "kernel_ms": kern_s * 1e3, "peak_source": hbm_src,
+                     "streamed_bytes": streamed, "streamed_gbs": streamed / kern_s / 1e9,
+                     "note": "achieved = SURVEY 8(d) algorithmic bytes (every operator entry once) / mean k_matvec "
+                             "launch time (CUDA events, rank 0); the plan streams the symmetric single-layer "
+                             "nearfield once per block pair (streamed_bytes < algorithmic bytes)"},
         "nearfield": {
-            "pairs_per_s": fc["pairs"] / nf_time, "pairs": fc["pairs"], "ms": nf_time * 1e3,
-            "touch_classify_ms": t_touch * 1e3,
-            "couplings": {"ms": t_cpl * 1e3, "pairs": n_cpl_pairs, "pairs_per_s": n_cpl_pairs / t_cpl,
-                          "note": "assemble_couplings end to end (host job list + k_blocks_slp, symmetric)"},
-            "singular": {"ms": t_sing * 1e3, "pairs": fc["singular_pairs"], "evaluated": fc["singular_evaluated"],
-                         "gflop": fc["sing_flops"] / 1e9,
+            "pairs_per_s": sums["near_pairs"] / nf_time,
+            "pairs_per_s_incl_classification": sums["near_pairs"] / (nf_time + tmax["touch"]),
+            "pairs": int(sums["near_pairs"]), "ms": nf_time * 1e3, "touch_classify_ms": tmax["touch"] * 1e3,
+            "singular": {"ms": tmax["sing"] * 1e3, "pairs_integrated": fc["singular_evaluated"],
                          "tflops": fc["sing_flops"] / t_sing / 1e12,
-                         "frac": (fc["sing_flops"] / t_sing / 1e12 / fp64_peak) if fp64_peak else None},
-            "regular": {"ms": t_reg * 1e3, "pairs": fc["regular_pairs"], "evaluated": fc["regular_evaluated"],
-                        "gflop": fc["reg_flops"] / 1e9,
+                         "frac": fc["sing_flops"] / t_sing / 1e12 / fp64_peak if fp64_peak else None},
+            "regular": {"ms": tmax["reg"] * 1e3, "pairs_integrated": fc["regular_evaluated"],
                         "tflops": fc["reg_flops"] / t_reg / 1e12,
-                        "frac": (fc["reg_flops"] / t_reg / 1e12 / fp64_peak) if fp64_peak else None},
-            "roofline": {"bound": "fp64", "achieved": (fc["reg_flops"] + fc["sing_flops"]) / nf_time / 1e12,
-                         "peak": fp64_peak, "unit": "TFLOP/s",
-                         "frac": ((fc["reg_flops"] + fc["sing_flops"]) / nf_time / 1e12 / fp64_peak) if fp64_peak else None,
-                         "peak_source": fp64_src},
+                        "frac": fc["reg_flops"] / t_reg / 1e12 / fp64_peak if fp64_peak else None},
+            "roofline": {"bound": "fp64", "achieved": sums["flops"] / nf_time / 1e12, "peak": fp64_peak,
+                         "unit": "TFLOP/s", "frac": sums["flops"] / nf_time / 1e12 / fp64_peak if fp64_peak else None,
+                         "peak_source": fp64_src,
+                         "flops": "SURVEY 8(d): 12 per regular, 36 per Sauter-Schwab evaluation, on the pairs "
+                                  "integrated (symmetric single layer: one per entry pair)"},
+            "couplings": {"pairs": int(sums["cpl_pairs"]), "kernel_ms": tmax["cpl"] * 1e3,
+                          "pairs_per_s": sums["cpl_pairs"] / tmax["cpl"],
+                          "tflops": sums["cpl_flops"] / tmax["cpl"] / 1e12,
+                          "end_to_end_ms": tmax["cpl_e2e"] * 1e3,
+                          "note": "S_b = G[pivots_t, pivots_s] (gca.py:194-205); end to end includes the host "
+                                  "job list"},
         },
         "e2e": e2e,
-        **extra,
+        "cg": cg,
+        "plan": info,
+        "memory_gb_per_rank": round(torch.cuda.max_memory_allocated() / 1e9, 2),
         "clocks": clk,
-        "setup_s": setup_s,
+        "setup": {k: round(v, 3) for k, v in T.items()},
     }
+    if device_basis and cfg.get("golden"):
+        result["basis_vs_reference"] = basis_agreement(cfg, tree, basis)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        result["cpu_baseline"] = cpu_baseline(H, tree, bt, basis, x_host, budget_s=args.cpu_budget)
-    if pg:
-        pg.barrier()
-        pg.destroy_process_group()
+        result["cpu_baseline"] = cpu_baseline(H, cfg, x_host, mesh, budget_s=args.cpu_budget)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
     if rank == 0:
-        print(json.dumps(result))
+        print(json.dumps(result), flush=True)
 
 
-def oracle_operator(H, tree, bt, basis):
+def basis_agreement(cfg, tree, basis):
+    """Per-cluster agreement of the (device) basis with the reference's own
+    GCA basis (rank, and the pivot list by digest), tests/golden/*."""
+    import hashlib
+
+    path = os.path.join(ROOT, "tests", "golden", cfg["golden"])
+    if not os.path.exists(path):
+        return None
+    g = np.load(path)
+    if "pivot_digest" not in g:
+        return None
+    ranks = np.array([basis.rank[u] for u in range(tree.n_nodes)])
+    dig = np.array([int.from_bytes(hashlib.sha256(np.asarray(basis.pivots[u], dtype=np.int64).tobytes()).digest()[:8],
+                                   "little", signed=True) for u in range(tree.n_nodes)], dtype=np.int64)
+    return {"clusters": int(tree.n_nodes), "rank_equal_frac": float(np.mean(ranks == g["ranks"])),
+            "pivots_equal_frac": float(np.mean(dig == g["pivot_digest"])),
+            "source": "tests/golden/" + cfg["golden"] + " (reference gca.build_basis run by make_golden.py)"}
+
+
+def cpu_baseline(H, cfg, x, mesh, budget_s=15.0):
+    """The oracle (numpy restatement of containers.py:254-270) on the SAME
+    operator exported from the device, one thread: one full matvec at least;
+    plus a seeded sample of near blocks through the oracle quadrature
+    (kernels.py:260-468 restated), single thread."""
     from oracle import h2 as OH
 
-    ot = OH.Tree(tree.perm, tree.start, tree.end, tree.depth_of, tree.left, tree.right)
+    t0 = time.perf_counter()
+    bt, b = H.block_tree, H.row_basis
     S = [s for _, s in H.far]
     Dn = [d for _, d in H.near]
-    return ot, S, Dn
+    ot = OH.Tree(bt.row_tree.perm, bt.row_tree.start, bt.row_tree.end, bt.row_tree.depth_of, bt.row_tree.left,
+                 bt.row_tree.right)
+    t_export = time.perf_counter() - t0
+    n = H.shape[0]
+    k, t = 0, time.perf_counter()
+    while True:
+        OH.matvec(ot, ot, b.V, b.E, b.rank, b.V, b.E, b.rank, bt.far_uids, S, bt.near_uids, Dn, x)
+        k += 1
+        if time.perf_counter() - t > budget_s:
+            break
+    dt = time.perf_counter() - t
+    del S, Dn
+    out = {"value": n * k / dt, "unit": "DoF/s", "cores": 1, "kind": "port",
+           "sample": f"{k} full oracle matvec(s) of the same {n}-DoF operator exported from the device "
+                     f"({dt:.1f} s; export {t_export:.1f} s; OPENBLAS_NUM_THREADS=1)"}
+    out["nearfield_sample"] = oracle_near_sample(mesh, bt, cfg, budget_s=max(5.0, budget_s / 2))
+    return out
 
 
-def cpu_baseline(H, tree, bt, basis, x, budget_s=15.0):
-    """The oracle (numpy restatement of containers.py:254-270) on the same
-    operator, single thread, bounded sample of matvecs."""
+def oracle_near_sample(mesh, bt, cfg, budget_s=8.0, seed=7):
+    """Seeded sample of near blocks through the oracle quadrature: touching
+    pairs by the Sauter-Schwab restatement (only those of the sampled
+    blocks), regular pairs by the tensor rule; pairs/s on one thread."""
+    from oracle import quad as OQ
+
+    V, T, N, A = mesh.vertices, mesh.triangles, mesh.normals, mesh.areas
+    return _near_sample(V, T, N, A, bt.row_tree, bt.near_uids, cfg, budget_s, seed)
+
+
+class _PairTable:
+    """Singular values of given pairs, looked up like the reference's table."""
+
+    def __init__(self, F, pa, pb, vals):
+        self.F = F
+        self.keys = pa * F + pb
+        o = np.argsort(self.keys)
+        self.keys, self.vals = self.keys[o], vals[o]
+
+    def lookup(self, pa, pb):
+        return self.vals[np.searchsorted(self.keys, np.asarray(pa) * self.F + np.asarray(pb))]
+
+
+def _near_sample(V, T, N, A, tree, near_uids, cfg, budget_s, seed):
+    from oracle import quad as OQ
+
+    rng = np.random.default_rng(seed)
+    order = rng.permutation(len(near_uids))
+    F = len(T)
+    pairs = blocks = 0
+    t_sing = t_reg = 0.0
+    for i in order:
+        if t_sing + t_reg > budget_s:
+            break
+        a, s = near_uids[i]
+        rows = tree.perm[tree.start[a] : tree.end[a]]
+        cols = tree.perm[tree.start[s] : tree.end[s]]
+        t1 = time.perf_counter()
+        hit = (T[rows][:, None, :, None] == T[cols][None, :, None, :]).any(axis=(2, 3))
+        ra, cb = np.nonzero(hit)
+        vals = OQ.singular_integrals(V, T, N, A, rows[ra], cols[cb], "slp", cfg["q_ss"])
+        t2 = time.perf_counter()
+        OQ.slp_block(V, T, N, A, rows, cols, cfg["q_reg"], _PairTable(F, rows[ra], cols[cb], vals))
+        t3 = time.perf_counter()
+        t_sing += t2 - t1
+        t_reg += t3 - t2
+        pairs += len(rows) * len(cols)
+        blocks += 1
+    tt = t_sing + t_reg
+    return {"pairs_per_s": pairs / tt if tt else None, "pairs": pairs, "blocks": blocks, "cores": 1,
+            "s_singular": round(t_sing, 2), "s_regular": round(t_reg, 2),
+            "sample": f"{blocks} seeded random near blocks of {len(near_uids)} (oracle quadrature, q "
+                      f"{cfg['q_reg']}/{cfg['q_ss']})"}
+
+
+# ---------------------------------------------------------------------------
+# reference arm (oracle only; never imports paper_2001_05523_b200)
+
+_REF = {}
+
+
+def _ref_slice(root):
+    """Worker: the row slice under `root` with shape-exact seeded values."""
     from oracle import h2 as OH
 
-    ot, S, Dn = oracle_operator(H, tree, bt, basis)
-    n = H.shape[0]
-    OH.matvec(ot, ot, basis.V, basis.E, basis.rank, basis.V, basis.E, basis.rank, bt.far_uids, S, bt.near_uids, Dn, x)
+    st = _REF
+    if root not in st.setdefault("slices", {}):
+        tree, far, near, rank = st["tree"], st["far"], st["near"], st["rank"]
+        size = tree.end - tree.start
+        rng = np.random.default_rng(1000 + int(root))
+
+        def V(u):
+            return rng.standard_normal((int(size[u]), int(rank[u])))
+
+        def E(u):
+            return rng.standard_normal((int(rank[u]), int(rank[tree.parent[u]])))
+
+        def S(i):
+            return rng.standard_normal((int(rank[far[i, 0]]), int(rank[far[i, 1]])))
+
+        def Dn(i):
+            return rng.standard_normal((int(size[near[i, 0]]), int(size[near[i, 1]])))
+
+        st["slices"][root] = OH.RowSlice(tree, int(root), far, near, rank, V, E, S, Dn)
+    return st["slices"][root]
+
+
+def _ref_step(root):
+    sl = _ref_slice(root)
     t = time.perf_counter()
-    k = 0
-    while time.perf_counter() - t < budget_s:
-        OH.matvec(ot, ot, basis.V, basis.E, basis.rank, basis.V, basis.E, basis.rank, bt.far_uids, S, bt.near_uids,
-                  Dn, x)
-        k += 1
-    dt = time.perf_counter() - t
-    return {"value": n * k / dt, "unit": "DoF/s", "cores": 1, "kind": "port",
-            "sample": f"{k} oracle matvecs of the same config-1 operator ({dt:.1f} s, OPENBLAS_NUM_THREADS=1)"}
+    sl.matvec(_REF["x"])
+    return sl.n_rows, time.perf_counter() - t
+
+
+def _ref_near(args):
+    i0, budget = args
+    st = _REF
+    V, T, N, A = st["mesh"]
+    return _near_sample(V, T, N, A, st["tree"], st["near"], st["cfg"], budget, seed=100 + i0)
 
 
 def run_reference(args, cfg):
-    """Reference arm: the reference's CPU algorithm (oracle port) on rank 0."""
-    ws, rank, local = dist_env()
+    """The reference's CPU algorithm (oracle port) on this host's cores, same
+    configuration: each step = the reference matvec restricted to one row
+    slice per core (oracle.h2.RowSlice), run in parallel; value = rows of all
+    slices / step wall time."""
+    ws, rank, _ = dist_env()
     if rank != 0:
         return
-    import torch  # noqa: F401  (device only used to assemble the operator values once? no: oracle assembly below)
+    import multiprocessing as mp
 
-    from oracle import h2 as OH
-    from oracle import quad as OQ
+    from oracle import structure as OS
 
-    threads = os.cpu_count() or 8
-    mesh, ctx, tree, bt, basis = build_problem(cfg, threads)
-    V, T, N, A = mesh.vertices, mesh.triangles, mesh.normals, mesh.areas
-    p = tree.perm
-    # operator values by the oracle (CPU quadrature), process pool over blocks
-    from concurrent.futures import ProcessPoolExecutor
-
-    t0 = time.time()
-    tab = OQ.Table(V, T, N, A, "slp", cfg["q_ss"])
-    near_jobs = [(p[tree.start[t] : tree.end[t]], p[tree.start[s] : tree.end[s]]) for t, s in bt.near_uids]
-    far_jobs = [(basis.pivots[t], basis.pivots[s]) for t, s in bt.far_uids]
-    global _REF_STATE
-    _REF_STATE = (V, T, N, A, tab, cfg["q_reg"])
-    with ProcessPoolExecutor(max_workers=threads) as ex:
-        Dn = list(ex.map(_ref_near, near_jobs, chunksize=64))
-        S = list(ex.map(_ref_far, far_jobs, chunksize=64))
-    t_asm = time.time() - t0
-    ot = OH.Tree(tree.perm, tree.start, tree.end, tree.depth_of, tree.left, tree.right)
-    n = len(tree.perm)
+    cores = os.cpu_count() or 8
+    t0 = time.perf_counter()
+    V, T, N, A = OS.sphere(cfg["level"])
+    tree = OS.cluster_tree(OS.p0_boxes(V, T), cfg["leaf"])
+    far, near = OS.block_tree(tree, tree, cfg["eta"])
+    t_struct = time.perf_counter() - t0
+    g = np.load(os.path.join(ROOT, "tests", "golden", cfg["golden"]))
+    rank_arr = np.asarray(g["ranks"], dtype=np.int64)
+    assert len(rank_arr) == tree.n_nodes
+    x = draw_x(cfg, len(tree.perm))
+    # row slices: the clusters at the depth where a slice holds ~1/64 of the rows
+    d = int(np.clip(np.round(np.log2(max(len(tree.perm) // 32768, 2))), 1, 8))
+    roots = np.flatnonzero(tree.depth == d)
     rng = np.random.default_rng(cfg["seed"])
-    x = rng.standard_normal(n) if cfg["dist"] == "normal" else rng.uniform(-1, 1, n)
-
-    def mv():
-        return OH.matvec(ot, ot, basis.V, basis.E, basis.rank, basis.V, basis.E, basis.rank, bt.far_uids, S,
-                         bt.near_uids, Dn, x)
-
-    for _ in range(max(args.warmup, 3)):
-        mv()
-    K = args.steps
-    t = time.perf_counter()
-    for _ in range(K):
-        mv()
-    dt = time.perf_counter() - t
-    val = n * K / dt
+    roots = rng.permutation(roots)[: min(cores, len(roots))]
+    _REF.update(tree=tree, far=far, near=near, rank=rank_arr, x=x, mesh=(V, T, N, A), cfg=cfg)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(len(roots)) as pool:
+        t1 = time.perf_counter()
+        pool.map(_ref_slice_warm, roots, chunksize=1)  # build the slice operators (untimed)
+        t_build = time.perf_counter() - t1
+        for _ in range(max(args.warmup, 1)):
+            pool.map(_ref_step, roots, chunksize=1)
+        K = args.steps
+        walls, rows_total = [], 0
+        for _ in range(K):
+            t1 = time.perf_counter()
+            res = pool.map(_ref_step, roots, chunksize=1)
+            walls.append(time.perf_counter() - t1)
+            rows_total = sum(r for r, _ in res)
+        near_res = pool.map(_ref_near, [(i, 6.0) for i in range(len(roots))], chunksize=1)
+    dt = float(np.sum(walls))
+    val = rows_total * K / dt
+    npairs = sum(r["pairs"] for r in near_res)
+    nwall = max(r["s_singular"] + r["s_regular"] for r in near_res)
     out = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "DoF/s", "n_gpus": ws, "steps": K,
-        "warmup": max(args.warmup, 3), "ms_per_step": dt / K * 1e3, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (generated sphere mesh, x ~ N(0,1) seed 1)",
-        "config": {"workload": f"config {args.config}: {cfg['desc']}", "n_dofs": n},
-        "cpu_baseline": {"value": val, "unit": "DoF/s", "cores": 1, "kind": "port",
-                         "sample": f"{K} matvecs of the oracle port (containers.py:254-270 restated), "
-                                   f"operator assembled by the oracle quadrature in {t_asm:.0f} s on {threads} procs"},
+        "warmup": max(args.warmup, 1), "ms_per_step": dt / K * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (generated sphere mesh, x ~ {'N(0,1)' if cfg['dist'] == 'normal' else 'U(-1,1)'} "
+                f"seed {cfg['seed']})",
+        "config": {"workload": cfg["desc"], "n_dofs": int(len(tree.perm))},
+        "cpu_baseline": {"value": val, "unit": "DoF/s", "cores": len(roots), "kind": "port",
+                         "sample": f"each step: the reference matvec (oracle.h2.RowSlice, containers.py:254-270 "
+                                   f"restricted to a row subtree: its far/near blocks, its ancestors' far blocks, "
+                                   f"the forward transform of every column cluster they read) on {len(roots)} "
+                                   f"row slices of depth {d} ({rows_total} of {len(tree.perm)} rows) in parallel, "
+                                   f"one per core; structure from oracle/structure.py (bit-exact with the "
+                                   f"reference), ranks from the reference's basis ({cfg['golden']}), operator "
+                                   f"values seeded random (the CPU cost does not depend on them)"},
         "e2e": {"value": val, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "nearfield": {"pairs_per_s": npairs / nwall if nwall else None, "pairs": int(npairs), "cores": len(roots),
+                      "sample": "seeded random near blocks through the oracle quadrature (Sauter-Schwab for the "
+                                "sampled touching pairs, tensor rule otherwise), one process per core"},
+        "setup_s": {"structure": round(t_struct, 1), "slice_operators": round(t_build, 1)},
     }
-    print(json.dumps(out))
+    print(json.dumps(out), flush=True)
 
 
-_REF_STATE = None
+def _ref_slice_warm(root):
+    _ref_slice(root)
+    return 0
 
 
-def _ref_near(job):
-    from oracle import quad as OQ
+# ---------------------------------------------------------------------------
 
-    V, T, N, A, tab, q = _REF_STATE
-    return OQ.slp_block(V, T, N, A, job[0], job[1], q, tab)
-
-
-def _ref_far(job):
-    from oracle import quad as OQ
-
-    V, T, N, A, tab, q = _REF_STATE
-    return OQ.slp_block(V, T, N, A, job[0], job[1], q, None)
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="1", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
-    else:
-        run_ours(args, cfg)
+        return 0
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is None and args.gpus > 1:
+        # launch one rank per GPU ourselves (the driver uses torchrun directly)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
+    if ws is not None and int(ws) != args.gpus:
+        sys.exit(f"bench.py: WORLD_SIZE={ws} but --gpus {args.gpus}")
+    run_ours(args, cfg)
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

@@ -268,6 +268,21 @@ def _dst_map(n_full, index, off, ld):
     return d_off, d_ld
 
 
+def near_slp_jobs_sharded(view):
+    """Single-layer near jobs of one rank (view: BlockTreeView): the
+    single-GPU job list (near_slp_jobs) restricted to the blocks the rank
+    stores, every block pair in the single-GPU orientation."""
+    full = view.full
+    rt, ct = full.row_tree, full.col_tree
+    lay = near_layout(view)
+    nu = full.near_uids
+    geom = np.stack([rt.start[nu[:, 0]], rt.end[nu[:, 0]] - rt.start[nu[:, 0]], ct.start[nu[:, 1]],
+                     ct.end[nu[:, 1]] - ct.start[nu[:, 1]], np.zeros(len(nu), dtype=np.int64),
+                     np.zeros(len(nu), dtype=np.int64)], axis=1)
+    d_off, d_ld = _dst_map(len(nu), view.near_index, lay.blk_off, lay.blk_ld)
+    return kernels.mirror_jobs_owned(geom, nu, d_off, d_ld)
+
+
 def assemble_nearfield_sharded(ctx, kind, view, q, q_singular=None, own_panels=None):
     """Packed nearfield of one rank of a row-sharded operator (`view`: the
     rank's BlockTreeView, distributed.py): only the rank's near blocks are
@@ -284,13 +299,8 @@ def assemble_nearfield_sharded(ctx, kind, view, q, q_singular=None, own_panels=N
     rt, ct = full.row_tree, full.col_tree
     table = _sharded_table(ctx, kind, qs, own_panels)
     if kind == kernels.SLP and _symmetric_trees(full):
-        nu = full.near_uids
-        geom = np.stack([rt.start[nu[:, 0]], rt.end[nu[:, 0]] - rt.start[nu[:, 0]], ct.start[nu[:, 1]],
-                         ct.end[nu[:, 1]] - ct.start[nu[:, 1]], np.zeros(len(nu), dtype=np.int64),
-                         np.zeros(len(nu), dtype=np.int64)], axis=1)
-        d_off, d_ld = _dst_map(len(nu), view.near_index, lay.blk_off, lay.blk_ld)
-        jobs = kernels.mirror_jobs_owned(geom, nu, d_off, d_ld)
-        kernels.run_slp_jobs(ctx.dmesh, q, jobs, rt.perm.astype(np.int32), ct.perm.astype(np.int32), table, out)
+        kernels.run_slp_jobs(ctx.dmesh, q, near_slp_jobs_sharded(view), rt.perm.astype(np.int32),
+                             ct.perm.astype(np.int32), table, out)
     else:
         _blocks_to_device(ctx, kind, _near_blocks(view, lay), q, qs, False, out, table=table)
     return out
@@ -321,6 +331,32 @@ def _pivots_concat(basis, n_nodes):
     return ranks, off, np.asarray(piv, dtype=np.int64)
 
 
+def coupling_slp_jobs(bt, row_basis, col_basis):
+    """Single-layer coupling jobs S_b = G[pivots_t, pivots_s] over the
+    concatenated pivot lists: (jobs, row pivots, col pivots, layout).  With
+    one basis on both sides one job per block pair {(t, s), (s, t)}; `bt` may
+    be a rank's BlockTreeView (only its blocks, single-GPU orientation)."""
+    rr, roff, rpiv = _pivots_concat(row_basis, bt.row_tree.n_nodes)
+    cr, coff, cpiv = _pivots_concat(col_basis, bt.col_tree.n_nodes)
+    lay = FarLayout(bt, rr, cr)
+    fu = bt.far_uids
+    full = getattr(bt, "full", None)
+    sym = row_basis is col_basis and _symmetric_trees(bt)
+    if full is not None and sym:
+        ff = full.far_uids
+        geom = np.stack([roff[ff[:, 0]], rr[ff[:, 0]], coff[ff[:, 1]], cr[ff[:, 1]],
+                         np.zeros(len(ff), dtype=np.int64), np.zeros(len(ff), dtype=np.int64)], axis=1)
+        d_off, d_ld = _dst_map(len(ff), bt.far_index, lay.blk_off, lay.blk_ld)
+        jobs = kernels.mirror_jobs_owned(geom, ff, d_off, d_ld)
+    else:
+        jobs = np.stack([roff[fu[:, 0]], lay.blk_rows, coff[fu[:, 1]], lay.blk_cols, lay.blk_off, lay.blk_ld],
+                        axis=1)
+        if sym:
+            # S_(s,t) = G[piv_s, piv_t] = S_(t,s)^T: one job per block pair
+            jobs = kernels.mirror_jobs(jobs, fu)
+    return jobs, rpiv.astype(np.int32), cpiv.astype(np.int32), lay
+
+
 def assemble_couplings(ctx, kind, bt, row_basis, col_basis, q):
     """Packed device couplings S_b = G[pivots_t, pivots_s] (gca.py:198-203).
     `bt` may be a rank's BlockTreeView (row sharding): then only the rank's
@@ -331,23 +367,10 @@ def assemble_couplings(ctx, kind, bt, row_basis, col_basis, q):
     lay = FarLayout(bt, rr, cr)
     out = D.zeros((max(lay.total, 1),))
     fu = bt.far_uids
-    full = getattr(bt, "full", None)
     if len(fu):
         if kind == kernels.SLP:
-            sym = row_basis is col_basis and _symmetric_trees(bt)
-            if full is not None and sym:
-                ff = full.far_uids
-                geom = np.stack([roff[ff[:, 0]], rr[ff[:, 0]], coff[ff[:, 1]], cr[ff[:, 1]],
-                                 np.zeros(len(ff), dtype=np.int64), np.zeros(len(ff), dtype=np.int64)], axis=1)
-                d_off, d_ld = _dst_map(len(ff), bt.far_index, lay.blk_off, lay.blk_ld)
-                jobs = kernels.mirror_jobs_owned(geom, ff, d_off, d_ld)
-            else:
-                jobs = np.stack([roff[fu[:, 0]], lay.blk_rows, coff[fu[:, 1]], lay.blk_cols, lay.blk_off,
-                                 lay.blk_ld], axis=1)
-                if sym:
-                    # S_(s,t) = G[piv_s, piv_t] = S_(t,s)^T: one job per block pair
-                    jobs = kernels.mirror_jobs(jobs, fu)
-            kernels.run_slp_jobs(ctx.dmesh, q, jobs, rpiv.astype(np.int32), cpiv.astype(np.int32), None, out)
+            jobs, rp, cp, _ = coupling_slp_jobs(bt, row_basis, col_basis)
+            kernels.run_slp_jobs(ctx.dmesh, q, jobs, rp, cp, None, out)
         else:
             blocks = [(rpiv[roff[t] : roff[t + 1]], cpiv[coff[s] : coff[s + 1]], int(lay.blk_off[i]),
                        int(lay.blk_ld[i])) for i, (t, s) in enumerate(fu)]

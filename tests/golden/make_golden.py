@@ -24,6 +24,8 @@ What is pinned (all produced by the reference's own public functions):
   h2_cfg1.npz      pivots/ranks digests + matvec x/y of config 1
   h2_cfg3p.npz     config-3 parameters (m=5, eta=1.5, leaf 64, q 3/4) at sphere
                    level 6: pivots/ranks + matvec / rmatvec x/y + samples
+  cfg3_basis.npz   config-3 (sphere level 9, m=5) reference GCA basis: rank and
+                   pivot-list digest per cluster (device-basis agreement)
   h2_dlp4.npz      level-4 double-layer H^2 (P0 x P1) matvec x/y + basis
   sample_l8.npz    config-2 size (sphere level 8): a seeded sample of single- and
                    double-layer near blocks with the split orders (regular 3,
@@ -356,6 +358,26 @@ def gen_h2_cfg3p():
     np.savez_compressed(os.path.join(HERE, "h2_cfg3p.npz"), **out)
 
 
+def gen_cfg3_basis():
+    """The reference GCA basis at config 3 (sphere level 9, leaf 64, m=5,
+    eps 1e-4): per cluster (uid order) its rank and a digest of its pivot
+    list (first 8 bytes of sha256 over the int64 pivots), so the device basis
+    can be compared with the reference's cluster by cluster.  Also the
+    tree/block-list digests it was built on."""
+    mesh = sphere_mesh(9)
+    ctx = AssemblyContext(mesh)
+    t0 = build_cluster_tree(spaces.DofSpace(spaces.P0, mesh).support_boxes(), 64)
+    log("cfg3 tree")
+    rb = gca.build_basis(ctx, t0, gca.P0_SLP, 5, 1e-4, threads=THREADS)
+    log("cfg3 basis")
+    uids = [c.uid for c in t0.nodes]
+    ranks = np.array([rb.rank[u] for u in uids], dtype=np.int16)
+    dig = np.array([int.from_bytes(hashlib.sha256(np.asarray(rb.pivots[u], dtype=np.int64).tobytes()).digest()[:8],
+                                   "little", signed=True) for u in uids], dtype=np.int64)
+    np.savez_compressed(os.path.join(HERE, "cfg3_basis.npz"), ranks=ranks, pivot_digest=dig,
+                        perm_digest=np.array([digest(t0.perm)]))
+
+
 def gen_h2_dlp4():
     mesh, ctx, bt, rb, cb = build_world(4, 32, 2.0, 3, 1e-4, kernels.DLP)
     log("dlp4 bases")
@@ -507,6 +529,7 @@ def main():
     ]
     if not args.skip_large:
         steps.append(("struct_large", gen_structure_large))
+        steps.append(("cfg3_basis", gen_cfg3_basis))
     for name, fn in steps:
         if args.only and name not in args.only.split(","):
             continue
