@@ -20,7 +20,8 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     from paper_2001_05523_b200.containers import AssemblyContext, near_layout, near_slp_jobs
     from paper_2001_05523_b200.mesh import sphere_mesh
 
-    m = sphere_mesh(6)
+    level = int(os.environ.get("NF_LEVEL", "6"))
+    m = sphere_mesh(level)
     ctx = AssemblyContext(m)
     tree = C.build_cluster_tree(spaces.DofSpace(spaces.P0, m).support_boxes(), 64)
     bt = C.BlockTree(tree, tree, 2.0)
@@ -32,7 +33,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
         sj.run(tab, Dn)
     t = bench.ev_time(torch, lambda: sj.run(tab, Dn), 20)
     h = Dn.cpu().numpy()
-    ref_path = "/tmp/nf_ref.npy"
+    ref_path = f"/tmp/nf_ref_{level}.npy"
     if not os.path.exists(ref_path):
         np.save(ref_path, h)
     ref = np.load(ref_path)
@@ -40,7 +41,10 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     t_ev = ctx.dmesh.touch()
     n_touch_eval = int(t_ev.case_counts[0] + (t_ev.case_counts[1] + t_ev.case_counts[2]) // 2)
     fl = (sj.evaluated - n_touch_eval) * 81 * 12
-    res = {"slp_ms": t * 1e3, "slp_tflops": fl / t / 1e12, "err_vs_first": err}
+    res = {"level": level, "slp_ms": t * 1e3, "slp_tflops": fl / t / 1e12, "err_vs_first": err}
+    if os.environ.get("NF_DLP", "1") == "0":
+        print(json.dumps(res))
+        sys.exit(0)
     # double layer (P0 rows x P1 columns): the regular pair-block kernel with the vertex scatter
     import ctypes
 
