@@ -207,6 +207,23 @@ def flop_counts(table_pairs, slp_jobs, cfg):
                 sing_flops=36.0 * ev_sing)
 
 
+def build_problem(cfg, threads):
+    """Mesh, assembly context, cluster tree, block tree and GCA basis of a
+    configuration (tools/ profiling drivers; run_ours times the same steps)."""
+    from paper_2001_05523_b200 import clustering as C
+    from paper_2001_05523_b200 import gca, spaces
+    from paper_2001_05523_b200.containers import AssemblyContext
+    from paper_2001_05523_b200.mesh import sphere_mesh
+
+    mesh = sphere_mesh(cfg["level"])
+    ctx = AssemblyContext(mesh)
+    tree = C.build_cluster_tree(spaces.DofSpace(spaces.P0, mesh).support_boxes(), cfg["leaf"])
+    bt = C.BlockTree(tree, tree, cfg["eta"])
+    basis = gca.build_basis(ctx, tree, gca.P0_SLP, cfg["m"], EPS_ACA, device=cfg["basis"] == "device",
+                            threads=threads)
+    return mesh, ctx, tree, bt, basis
+
+
 def run_ours(args, cfg):
     import torch
 

@@ -212,6 +212,19 @@ def _symmetric_trees(bt):
                         and np.array_equal(rt.end, ct.end))
 
 
+def _partners(bt, which):
+    """kernels.block_partners of the block tree's far or near list, cached."""
+    attr = "_h2b_partners_" + which
+    hit = getattr(bt, attr, None)
+    if hit is None:
+        hit = kernels.block_partners(bt.far_uids if which == "far" else bt.near_uids)
+        try:
+            setattr(bt, attr, hit)
+        except AttributeError:
+            pass
+    return hit
+
+
 def near_slp_jobs(bt):
     """Pair-block jobs of the single-layer nearfield.  With one tree on both
     sides the matrix is symmetric (G(a,b) = G(b,a) for P0 x P0, and the
@@ -223,7 +236,7 @@ def near_slp_jobs(bt):
     nu = bt.near_uids
     jobs = np.stack([rt.start[nu[:, 0]], lay.blk_rows, ct.start[nu[:, 1]], lay.blk_cols, lay.blk_off, lay.blk_ld],
                     axis=1)
-    return kernels.mirror_jobs(jobs, nu) if _symmetric_trees(bt) else jobs
+    return kernels.mirror_jobs(jobs, nu, _partners(bt, "near")) if _symmetric_trees(bt) else jobs
 
 
 def assemble_nearfield_device(ctx, kind, bt, q, q_singular=None, cache=None):
@@ -280,7 +293,7 @@ def near_slp_jobs_sharded(view):
                      ct.end[nu[:, 1]] - ct.start[nu[:, 1]], np.zeros(len(nu), dtype=np.int64),
                      np.zeros(len(nu), dtype=np.int64)], axis=1)
     d_off, d_ld = _dst_map(len(nu), view.near_index, lay.blk_off, lay.blk_ld)
-    return kernels.mirror_jobs_owned(geom, nu, d_off, d_ld)
+    return kernels.mirror_jobs_owned(geom, nu, d_off, d_ld, _partners(full, "near"))
 
 
 def assemble_nearfield_sharded(ctx, kind, view, q, q_singular=None, own_panels=None):
@@ -323,12 +336,48 @@ def _view(flat, off, nr, nc, ld):
     return np.lib.stride_tricks.as_strided(flat[off:], shape=(nr, nc), strides=(8 * ld, 8)).copy()
 
 
+def _basis_ranks(basis, n_nodes):
+    """Per-node ranks as an array (cached on the basis with its pivot lists)."""
+    return _pivots_concat(basis, n_nodes)[0]
+
+
 def _pivots_concat(basis, n_nodes):
+    """(ranks, offsets, concatenated pivots) of a basis in uid order, cached on
+    the basis object (keyed by the node count and the identity of its dicts)."""
+    key = (n_nodes, id(basis.rank), id(basis.pivots), len(basis.rank))
+    hit = getattr(basis, "_h2b_concat", None)
+    if hit is not None and hit[0] == key:
+        return hit[1]
     ranks = np.array([basis.rank[u] for u in range(n_nodes)], dtype=np.int64)
     off = np.zeros(n_nodes + 1, dtype=np.int64)
     np.cumsum(ranks, out=off[1:])
     piv = np.concatenate([np.asarray(basis.pivots[u], dtype=np.int64) for u in range(n_nodes)]) if n_nodes else []
-    return ranks, off, np.asarray(piv, dtype=np.int64)
+    res = (ranks, off, np.asarray(piv, dtype=np.int64))
+    try:
+        basis._h2b_concat = (key, res)
+    except AttributeError:
+        pass
+    return res
+
+
+def far_layout(bt, row_basis, col_basis):
+    """FarLayout of a block tree (or view) for two bases, cached on the block
+    tree per (row basis, column basis) pair."""
+    rr = _basis_ranks(row_basis, bt.row_tree.n_nodes)
+    cr = _basis_ranks(col_basis, bt.col_tree.n_nodes)
+    cache = getattr(bt, "_h2b_far_layouts", None)
+    if cache is None:
+        cache = []
+        try:
+            bt._h2b_far_layouts = cache
+        except AttributeError:
+            return FarLayout(bt, rr, cr)
+    for r0, c0, lay in cache:
+        if r0 is rr and c0 is cr:
+            return lay
+    lay = FarLayout(bt, rr, cr)
+    cache.append((rr, cr, lay))
+    return lay
 
 
 def coupling_slp_jobs(bt, row_basis, col_basis):
@@ -338,7 +387,7 @@ def coupling_slp_jobs(bt, row_basis, col_basis):
     be a rank's BlockTreeView (only its blocks, single-GPU orientation)."""
     rr, roff, rpiv = _pivots_concat(row_basis, bt.row_tree.n_nodes)
     cr, coff, cpiv = _pivots_concat(col_basis, bt.col_tree.n_nodes)
-    lay = FarLayout(bt, rr, cr)
+    lay = far_layout(bt, row_basis, col_basis)
     fu = bt.far_uids
     full = getattr(bt, "full", None)
     sym = row_basis is col_basis and _symmetric_trees(bt)
@@ -347,13 +396,13 @@ def coupling_slp_jobs(bt, row_basis, col_basis):
         geom = np.stack([roff[ff[:, 0]], rr[ff[:, 0]], coff[ff[:, 1]], cr[ff[:, 1]],
                          np.zeros(len(ff), dtype=np.int64), np.zeros(len(ff), dtype=np.int64)], axis=1)
         d_off, d_ld = _dst_map(len(ff), bt.far_index, lay.blk_off, lay.blk_ld)
-        jobs = kernels.mirror_jobs_owned(geom, ff, d_off, d_ld)
+        jobs = kernels.mirror_jobs_owned(geom, ff, d_off, d_ld, _partners(full, "far"))
     else:
         jobs = np.stack([roff[fu[:, 0]], lay.blk_rows, coff[fu[:, 1]], lay.blk_cols, lay.blk_off, lay.blk_ld],
                         axis=1)
         if sym:
             # S_(s,t) = G[piv_s, piv_t] = S_(t,s)^T: one job per block pair
-            jobs = kernels.mirror_jobs(jobs, fu)
+            jobs = kernels.mirror_jobs(jobs, fu, _partners(bt, "far"))
     return jobs, rpiv.astype(np.int32), cpiv.astype(np.int32), lay
 
 
@@ -364,7 +413,7 @@ def assemble_couplings(ctx, kind, bt, row_basis, col_basis, q):
     single-GPU orientation (same bits)."""
     rr, roff, rpiv = _pivots_concat(row_basis, bt.row_tree.n_nodes)
     cr, coff, cpiv = _pivots_concat(col_basis, bt.col_tree.n_nodes)
-    lay = FarLayout(bt, rr, cr)
+    lay = far_layout(bt, row_basis, col_basis)
     out = D.zeros((max(lay.total, 1),))
     fu = bt.far_uids
     if len(fu):
@@ -575,9 +624,7 @@ class H2Matrix:
     @classmethod
     def from_device(cls, block_tree, row_basis, col_basis, S, Dn):
         self = cls.__new__(cls)
-        rr = np.array([row_basis.rank[u] for u in range(block_tree.row_tree.n_nodes)], dtype=np.int64)
-        cr = np.array([col_basis.rank[u] for u in range(block_tree.col_tree.n_nodes)], dtype=np.int64)
-        self._init(block_tree, row_basis, col_basis, S, Dn, FarLayout(block_tree, rr, cr))
+        self._init(block_tree, row_basis, col_basis, S, Dn, far_layout(block_tree, row_basis, col_basis))
         return self
 
     def _init(self, bt, rb, cb, S, Dn, far_layout):

@@ -16,6 +16,7 @@
 // reference's _dist2, kernels.py:75-85, without its cancellation because both
 // point sets are shifted to a block-local origin first).
 
+#include <climits>
 #include <cstdlib>
 
 #include <cub/device/device_scan.cuh>
@@ -34,8 +35,8 @@ constexpr int kSlpUnroll = H2B_SLP_UNROLL_OUTER;
 namespace h2b {
 namespace {
 
-constexpr int kMaxCand = 128;   // touching candidates per panel (3 x vertex valence)
 constexpr int kTile = 64;       // max rows / columns of one pair-block job
+constexpr int kSlpLd = kTile + 1;  // padded point stride of the SLP stage (staging stores ~2-way, not 9-way, bank conflicts)
 constexpr int kDlpMaxPanels = 128;  // max column panels of one DLP job
 constexpr int kDlpRowChunk = 8;
 
@@ -70,34 +71,39 @@ __global__ void k_panel_points(const double* __restrict__ V, const int32_t* __re
 
 // ----------------------------------------------------------------------------
 // touching pairs
-__device__ int gather_touching(const int32_t* __restrict__ T, const int64_t* __restrict__ vt_ptr,
-                               const int32_t* __restrict__ vt_idx, int64_t a, int* cand, int* flags) {
-    int n = 0;
+// The touching panels of panel a (sharing >= 1 vertex, a itself included),
+// ascending and unique: a three-way merge of its vertices' incident-triangle
+// lists (each ascending, Mesh.vertex_triangle_csr), streamed to f(b, i) with
+// no per-thread candidate array.
+template <class Fn>
+__device__ __forceinline__ int for_each_touching(const int32_t* __restrict__ T, const int64_t* __restrict__ vt_ptr,
+                                                 const int32_t* __restrict__ vt_idx, int64_t a, Fn&& f) {
+    int64_t p[3], e[3];
+    int h[3];
+#pragma unroll
     for (int k = 0; k < 3; ++k) {
         const int v = T[3 * a + k];
-        for (int64_t p = vt_ptr[v]; p < vt_ptr[v + 1]; ++p) {
-            if (n < kMaxCand) cand[n] = vt_idx[p];
+        p[k] = vt_ptr[v];
+        e[k] = vt_ptr[v + 1];
+        h[k] = p[k] < e[k] ? vt_idx[p[k]] : INT_MAX;
+    }
+    int n = 0, last = -1;
+    while (true) {
+        const int m = min(h[0], min(h[1], h[2]));
+        if (m == INT_MAX) break;
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            if (h[k] == m) {
+                ++p[k];
+                h[k] = p[k] < e[k] ? vt_idx[p[k]] : INT_MAX;
+            }
+        if (m != last) {
+            f(m, n);
             ++n;
+            last = m;
         }
     }
-    if (n > kMaxCand) {
-        atomicOr(flags, kFlagCandidates);
-        n = kMaxCand;
-    }
-    // insertion sort + unique
-    for (int i = 1; i < n; ++i) {
-        const int v = cand[i];
-        int j = i - 1;
-        while (j >= 0 && cand[j] > v) {
-            cand[j + 1] = cand[j];
-            --j;
-        }
-        cand[j + 1] = v;
-    }
-    int m = 0;
-    for (int i = 0; i < n; ++i)
-        if (m == 0 || cand[m - 1] != cand[i]) cand[m++] = cand[i];
-    return m;
+    return n;
 }
 
 // quadrature.py:90-118: case = #shared vertices (3 when identical); shared
@@ -149,17 +155,13 @@ __global__ void k_touch_count(const int32_t* __restrict__ T, int64_t F,
     if (threadIdx.x < 4) sc[threadIdx.x] = 0;
     __syncthreads();
     if (a < F) {
-        int cand[kMaxCand];
-        const int m = gather_touching(T, vt_ptr, vt_idx, a, cand, flags);
-        counts[a] = m;
-        int ta[3] = {T[3 * a], T[3 * a + 1], T[3 * a + 2]};
+        const int ta[3] = {T[3 * a], T[3 * a + 1], T[3 * a + 2]};
         int c[4] = {0, 0, 0, 0};
-        for (int i = 0; i < m; ++i) {
-            const int b = cand[i];
-            int tb[3] = {T[3 * b], T[3 * b + 1], T[3 * b + 2]};
-            const int code = classify(ta, tb, b == a) & 3;
-            c[code]++;
-        }
+        const int m = for_each_touching(T, vt_ptr, vt_idx, a, [&](int b, int) {
+            const int tb[3] = {T[3 * b], T[3 * b + 1], T[3 * b + 2]};
+            c[classify(ta, tb, b == a) & 3]++;
+        });
+        counts[a] = m;
         for (int k = 1; k < 4; ++k)
             if (c[k]) atomicAdd(&sc[k], (unsigned long long)c[k]);
         if (c[0]) atomicOr(flags, kFlagCandidates);  // cannot happen on a valid mesh
@@ -171,34 +173,71 @@ __global__ void k_touch_count(const int32_t* __restrict__ T, int64_t F,
 __global__ void k_touch_fill(const int32_t* __restrict__ T, int64_t F,
                              const int64_t* __restrict__ vt_ptr, const int32_t* __restrict__ vt_idx,
                              const int64_t* __restrict__ row_ptr, int32_t* __restrict__ col,
-                             int32_t* __restrict__ info, int32_t* __restrict__ case_list,
-                             unsigned long long* __restrict__ case_cursor, int* flags) {
+                             int32_t* __restrict__ info, int32_t* __restrict__ seg_count, int* flags) {
     const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (a >= F) return;
-    int cand[kMaxCand];
-    const int m = gather_touching(T, vt_ptr, vt_idx, a, cand, flags);
-    int ta[3] = {T[3 * a], T[3 * a + 1], T[3 * a + 2]};
+    const int ta[3] = {T[3 * a], T[3 * a + 1], T[3 * a + 2]};
     const int64_t base = row_ptr[a];
-    for (int i = 0; i < m; ++i) {
-        const int b = cand[i];
-        int tb[3] = {T[3 * b], T[3 * b + 1], T[3 * b + 2]};
+    int c[3] = {0, 0, 0};
+    for_each_touching(T, vt_ptr, vt_idx, a, [&](int b, int i) {
+        const int tb[3] = {T[3 * b], T[3 * b + 1], T[3 * b + 2]};
         const int inf = classify(ta, tb, b == a);
         col[base + i] = b;
         info[base + i] = inf;
-        // case-grouped list: identical, edge, vertex segments (order within a
-        // segment is irrelevant: values are written per pair id)
         const int code = inf & 3;
+        c[code == H2B_IDENTICAL ? 0 : (code == H2B_EDGE ? 1 : 2)]++;
+    });
+    // per-panel case counts, segment-major: one scan over [3][F] gives every
+    // pair its slot in the case-grouped list (no contended atomics: a global
+    // cursor per case serialised ~27 M atomics at config 3)
+    seg_count[a] = c[0];
+    seg_count[F + a] = c[1];
+    seg_count[2 * F + a] = c[2];
+}
+
+// case-grouped pair list: segment k, rows ascending, columns ascending
+__global__ void k_touch_list(const int64_t* __restrict__ row_ptr, int64_t F, const int32_t* __restrict__ info,
+                             const int32_t* __restrict__ seg_pos, int32_t* __restrict__ case_list) {
+    const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= F) return;
+    int pos[3] = {seg_pos[a], seg_pos[F + a], seg_pos[2 * F + a]};
+    for (int64_t p = row_ptr[a]; p < row_ptr[a + 1]; ++p) {
+        const int code = info[p] & 3;
         const int seg = code == H2B_IDENTICAL ? 0 : (code == H2B_EDGE ? 1 : 2);
-        const unsigned long long slot = atomicAdd(&case_cursor[seg], 1ull);
-        case_list[slot] = (int32_t)(base + i);
+        case_list[pos[seg]++] = (int32_t)p;
     }
 }
 
-// unordered touching pairs (a < b) of the edge and vertex segments
-__global__ void k_touch_half(const int64_t* __restrict__ row_ptr, int64_t F, const int32_t* __restrict__ col,
-                             const int32_t* __restrict__ info, const int32_t* __restrict__ case_list,
-                             int64_t lo, int64_t hi, int32_t* __restrict__ half,
-                             unsigned long long* __restrict__ cursor);
+// unordered (a < b) edge / vertex pairs per row panel, segment-major [2][F]
+__global__ void k_half_count(const int64_t* __restrict__ row_ptr, int64_t F, const int32_t* __restrict__ col,
+                             const int32_t* __restrict__ info, int32_t* __restrict__ cnt) {
+    const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= F) return;
+    int ce = 0, cv = 0;
+    for (int64_t p = row_ptr[a]; p < row_ptr[a + 1]; ++p) {
+        if (col[p] <= a) continue;
+        const int code = info[p] & 3;
+        ce += code == H2B_EDGE;
+        cv += code == H2B_VERTEX;
+    }
+    cnt[a] = ce;
+    cnt[F + a] = cv;
+}
+
+__global__ void k_half_fill(const int64_t* __restrict__ row_ptr, int64_t F, const int32_t* __restrict__ col,
+                            const int32_t* __restrict__ info, const int32_t* __restrict__ pos_in,
+                            int64_t base, int32_t* __restrict__ half) {
+    const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= F) return;
+    int64_t pe = base + pos_in[a], pv = base + pos_in[F + a];
+    for (int64_t p = row_ptr[a]; p < row_ptr[a + 1]; ++p) {
+        if (col[p] <= a) continue;
+        const int code = info[p] & 3;
+        if (code == H2B_EDGE) half[pe++] = (int32_t)p;
+        else if (code == H2B_VERTEX) half[pv++] = (int32_t)p;
+    }
+}
+
 
 // case code + permutations of arbitrary pairs (kernels.pair_integrals),
 // counted per segment: 0 identical, 1 edge, 2 vertex, 3 disjoint
@@ -464,19 +503,6 @@ __global__ void __launch_bounds__(128) k_singular(const double* __restrict__ V, 
     }
 }
 
-__global__ void k_touch_half(const int64_t* __restrict__ row_ptr, int64_t F, const int32_t* __restrict__ col,
-                             const int32_t* __restrict__ info, const int32_t* __restrict__ case_list,
-                             int64_t lo, int64_t hi, int32_t* __restrict__ half,
-                             unsigned long long* __restrict__ cursor) {
-    const int64_t e = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= hi) return;
-    const int32_t pid = case_list[e];
-    const int64_t a = find_row(row_ptr, F, pid);
-    if (a >= col[pid]) return;
-    const int seg = (info[pid] & 3) == H2B_EDGE ? 0 : 1;
-    half[atomicAdd(&cursor[seg], 1ull)] = pid;
-}
-
 // ----------------------------------------------------------------------------
 // regular SLP pair blocks
 __device__ __forceinline__ bool shares_vertex(const int* ra, const int* cb) {
@@ -499,7 +525,7 @@ __device__ __forceinline__ int64_t touch_find(const int64_t* __restrict__ row_pt
 // 1/(4 pi r) = t (3 - p t^2) / (8 sqrt(2) pi)
 constexpr double kSlpFold = 1.0 / (8.0 * 1.4142135623730950488016887 * kPi);
 
-template <int Q, int JC, int MINB, int R>
+template <int Q, int JC, int MINB, int R, int UJ, int S>
 __global__ void __launch_bounds__(H2B_SLP_THREADS, MINB) k_blocks_slp(const double* __restrict__ P, int64_t F,
                                                    const int32_t* __restrict__ T,
                                                    const int64_t* __restrict__ jobs,
@@ -510,9 +536,9 @@ __global__ void __launch_bounds__(H2B_SLP_THREADS, MINB) k_blocks_slp(const doub
                                                    const double* __restrict__ t_val,
                                                    double* __restrict__ out, int* __restrict__ flags) {
     extern __shared__ double smem[];
-    double* rx = smem;                 // [5][Q][kTile]: x', y', z', -|x'|^2/2, W
-    double* cx = smem + 5 * Q * kTile; // [5][Q][kTile]: y', ..., W / (8 sqrt2 pi)
-    int* rv = reinterpret_cast<int*>(cx + 5 * Q * kTile);  // [kTile][3]
+    double* rx = smem;                 // [5][Q][kSlpLd]: x', y', z', -|x'|^2/2, W
+    double* cx = smem + 5 * Q * kSlpLd; // [5][Q][kSlpLd]: y', ..., W / (8 sqrt2 pi)
+    int* rv = reinterpret_cast<int*>(cx + 5 * Q * kSlpLd);  // [kTile][3]
     int* cv = rv + 3 * kTile;
     int* rp = cv + 3 * kTile;
     int* cp = rp + kTile;
@@ -537,12 +563,12 @@ __global__ void __launch_bounds__(H2B_SLP_THREADS, MINB) k_blocks_slp(const doub
         const int pnl = row_idx[row_off + r];
         const int64_t g = (int64_t)pnl * Q + i;
         const double x = P[g] - ox, y = P[FQ + g] - oy, z = P[2 * FQ + g] - oz;
-        const int s = i * kTile + r;
+        const int s = i * kSlpLd + r;
         rx[s] = -x;  // negated: r^2/2 = |x'|^2/2 + |y'|^2/2 + (-x').y'
-        rx[Q * kTile + s] = -y;
-        rx[2 * Q * kTile + s] = -z;
-        rx[3 * Q * kTile + s] = 0.5 * fma(z, z, fma(y, y, x * x));
-        rx[4 * Q * kTile + s] = P[3 * FQ + g];
+        rx[Q * kSlpLd + s] = -y;
+        rx[2 * Q * kSlpLd + s] = -z;
+        rx[3 * Q * kSlpLd + s] = 0.5 * fma(z, z, fma(y, y, x * x));
+        rx[4 * Q * kSlpLd + s] = P[3 * FQ + g];
         if (i == 0) {
             rp[r] = pnl;
             rv[3 * r] = T[3 * pnl];
@@ -555,12 +581,16 @@ __global__ void __launch_bounds__(H2B_SLP_THREADS, MINB) k_blocks_slp(const doub
         const int pnl = col_idx[col_off + c];
         const int64_t g = (int64_t)pnl * Q + j;
         const double x = P[g] - ox, y = P[FQ + g] - oy, z = P[2 * FQ + g] - oz;
-        const int s = j * kTile + c;
-        cx[s] = x;
-        cx[Q * kTile + s] = y;
-        cx[2 * Q * kTile + s] = z;
-        cx[3 * Q * kTile + s] = 0.5 * fma(z, z, fma(y, y, x * x));
-        cx[4 * Q * kTile + s] = P[3 * FQ + g] * kSlpFold;
+        const int s = j * kSlpLd + c;
+        // column point scaled by cw = 1 / w^2 (w = W kSlpFold > 0): the seed of
+        // rsqrt(cw p) is already w t, so the weight costs no product per pair
+        const double w = P[3 * FQ + g] * kSlpFold;
+        const double cw = 1.0 / (w * w);
+        cx[s] = cw * x;
+        cx[Q * kSlpLd + s] = cw * y;
+        cx[2 * Q * kSlpLd + s] = cw * z;
+        cx[3 * Q * kSlpLd + s] = cw * (0.5 * fma(z, z, fma(y, y, x * x)));
+        cx[4 * Q * kSlpLd + s] = cw;
         if (j == 0) {
             cp[c] = pnl;
             cv[3 * c] = T[3 * pnl];
@@ -572,11 +602,92 @@ __global__ void __launch_bounds__(H2B_SLP_THREADS, MINB) k_blocks_slp(const doub
 
     int lflags = 0;
     const int np = tri ? nc * (nc + 1) / 2 : nr * nc;
+    if constexpr (S > 1) {
+        // S lanes per panel pair, each holding Q/S column points in registers
+        // for the whole pair (fewer live registers -> more point pairs in
+        // flight); partial sums combined by shuffles in lane order
+        static_assert(Q % S == 0 && S <= 32, "split must divide the rule");
+        constexpr int PW = 32 / S, JS = Q / S;
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        const int slot = lane / S, sub = lane - slot * S;
+        for (int pb = wid * PW; pb < np; pb += nw * PW) {
+            const int p = pb + slot;
+            const bool act = slot < PW && p < np;
+            int a = 0, b = 0;
+            if (act) {
+                if (tri) {
+                    b = (int)((sqrtf(8.0f * (float)p + 1.0f) - 1.0f) * 0.5f);
+                    if ((b + 1) * (b + 2) / 2 <= p) ++b;
+                    if (b * (b + 1) / 2 > p) --b;
+                    a = p - b * (b + 1) / 2;
+                } else {
+                    a = p / nc;
+                    b = p - a * nc;
+                }
+            }
+            const bool touch = act && shares_vertex(rv + 3 * a, cv + 3 * b);
+            double part = 0.0;
+            if (act && !touch) {
+                double y0[JS], y1[JS], y2[JS], yh[JS], yw[JS];
+#pragma unroll
+                for (int k = 0; k < JS; ++k) {
+                    const int sj = (sub * JS + k) * kSlpLd + b;
+                    y0[k] = cx[sj];
+                    y1[k] = cx[Q * kSlpLd + sj];
+                    y2[k] = cx[2 * Q * kSlpLd + sj];
+                    yh[k] = cx[3 * Q * kSlpLd + sj];
+                    yw[k] = cx[4 * Q * kSlpLd + sj];
+                }
+#pragma unroll UJ
+                for (int i = 0; i < Q; ++i) {
+                    const int si = i * kSlpLd + a;
+                    const double x0 = rx[si], x1 = rx[Q * kSlpLd + si], x2 = rx[2 * Q * kSlpLd + si];
+                    const double xh = rx[3 * Q * kSlpLd + si], xw = rx[4 * Q * kSlpLd + si];
+                    double acc = 0.0;
+#pragma unroll
+                    for (int k = 0; k < JS; ++k) {
+                        const double pa = fma(x0, y0[k], fma(x1, y1[k], fma(x2, y2[k], fma(xh, yw[k], yh[k]))));
+                        const double ta = rsqrt_seed(pa);
+                        acc = fma(ta, fma(-pa, ta * ta, 3.0), acc);
+                    }
+                    part = fma(xw, acc, part);
+                }
+            }
+            double tot = part;
+#pragma unroll
+            for (int o = 1; o < S; ++o) {
+                const double v = __shfl_down_sync(0xffffffffu, part, o);
+                if (sub == 0) tot += v;
+            }
+            if (!act || sub != 0) continue;
+            double val = tot;
+            if (touch) {
+                if (t_row_ptr == nullptr) {
+                    lflags |= kFlagTouching;
+                    val = 0.0;
+                } else {
+                    const int64_t k = touch_find(t_row_ptr, t_col, rp[a], cp[b]);
+                    if (k < 0) {
+                        lflags |= kFlagMissing;
+                        val = 0.0;
+                    } else {
+                        val = t_val[k];
+                    }
+                }
+            }
+            if (!isfinite(val)) lflags |= kFlagNonFinite;
+            if (out_off >= 0) out[out_off + (int64_t)a * ld + b] = val;
+            if (m_off >= 0 && !(tri && a == b)) out[m_off + (int64_t)b * m_ld + a] = val;
+        }
+        if (lflags) atomicOr(flags, lflags);
+        return;
+    }
     for (int p = threadIdx.x; p < np; p += blockDim.x) {
         int a, b;
         if (tri) {
             // p = b (b + 1) / 2 + a, 0 <= a <= b
-            b = (int)((sqrt(8.0 * p + 1.0) - 1.0) * 0.5);
+            // single-precision root (p < 2080: exact after the corrections)
+            b = (int)((sqrtf(8.0f * (float)p + 1.0f) - 1.0f) * 0.5f);
             if ((b + 1) * (b + 2) / 2 <= p) ++b;
             if (b * (b + 1) / 2 > p) --b;
             a = p - b * (b + 1) / 2;
@@ -600,18 +711,18 @@ __global__ void __launch_bounds__(H2B_SLP_THREADS, MINB) k_blocks_slp(const doub
             }
         } else {
             double tot = 0.0;
-#pragma unroll kSlpUnroll
+#pragma unroll UJ
             for (int j0 = 0; j0 < Q; j0 += JC) {
                 double y0[JC], y1[JC], y2[JC], yh[JC], yw[JC];
 #pragma unroll
                 for (int j = 0; j < JC; ++j) {
                     if (j0 + j < Q) {
-                        const int s = (j0 + j) * kTile + b;
+                        const int s = (j0 + j) * kSlpLd + b;
                         y0[j] = cx[s];
-                        y1[j] = cx[Q * kTile + s];
-                        y2[j] = cx[2 * Q * kTile + s];
-                        yh[j] = cx[3 * Q * kTile + s];
-                        yw[j] = cx[4 * Q * kTile + s];
+                        y1[j] = cx[Q * kSlpLd + s];
+                        y2[j] = cx[2 * Q * kSlpLd + s];
+                        yh[j] = cx[3 * Q * kSlpLd + s];
+                        yw[j] = cx[4 * Q * kSlpLd + s];
                     }
                 }
                 // R row points per step: R independent accumulation chains
@@ -620,9 +731,9 @@ __global__ void __launch_bounds__(H2B_SLP_THREADS, MINB) k_blocks_slp(const doub
                     double xa[R][5], acc[R];
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
-                        const int si = (i0 + r < Q ? i0 + r : Q - 1) * kTile + a;
+                        const int si = (i0 + r < Q ? i0 + r : Q - 1) * kSlpLd + a;
 #pragma unroll
-                        for (int f = 0; f < 5; ++f) xa[r][f] = rx[f * Q * kTile + si];
+                        for (int f = 0; f < 5; ++f) xa[r][f] = rx[f * Q * kSlpLd + si];
                         acc[r] = 0.0;
                     }
 #pragma unroll
@@ -631,12 +742,13 @@ __global__ void __launch_bounds__(H2B_SLP_THREADS, MINB) k_blocks_slp(const doub
 #pragma unroll
                             for (int r = 0; r < R; ++r) {
                                 if (i0 + r < Q) {
-                                    // p = |x'|^2/2 + |y'|^2/2 - x'.y' = r^2/2, t ~ rsqrt(p);
-                                    // one Newton step folded: 1/r ~ t (3 - p t^2) / (2 sqrt 2)
+                                    // p = c (|x'|^2/2 + |y'|^2/2 - x'.y') = c r^2/2 (4 FMA),
+                                    // t ~ rsqrt(p) = w sqrt(2) / r; one Newton step folded:
+                                    // w / r ~ t (3 - p t^2) / (2 sqrt 2)  (7 FP64 ops per point pair)
                                     const double pa = fma(xa[r][0], y0[j], fma(xa[r][1], y1[j],
-                                                                             fma(xa[r][2], y2[j], xa[r][3] + yh[j])));
+                                                      fma(xa[r][2], y2[j], fma(xa[r][3], yw[j], yh[j]))));
                                     const double ta = rsqrt_seed(pa);
-                                    acc[r] = fma(yw[j] * ta, fma(-pa, ta * ta, 3.0), acc[r]);
+                                    acc[r] = fma(ta, fma(-pa, ta * ta, 3.0), acc[r]);
                                 }
                             }
                         }
@@ -873,12 +985,18 @@ int alloc_flags(int** d, cudaStream_t st) {
 #ifndef H2B_SLP9_R
 #define H2B_SLP9_R 2
 #endif
+#ifndef H2B_SLP9_UJ
+#define H2B_SLP9_UJ 16  // unroll of the column-chunk loop (16: fully)
+#endif
+#ifndef H2B_SLP9_S
+#define H2B_SLP9_S 1    // lanes per panel pair (1: one thread per pair)
+#endif
 
-template <int Q, int JC, int MINB = 2, int R = 2>
+template <int Q, int JC, int MINB = 2, int R = 2, int UJ = 16, int S = 1>
 int launch_slp(const h2b_mesh* m, const double* P, const h2b_jobs* jobs, const h2b_touch* t,
                const double* tv, double* out, int* flags, cudaStream_t st) {
-    const size_t sm = (size_t)10 * Q * kTile * sizeof(double) + (size_t)8 * kTile * sizeof(int);
-    auto kern = k_blocks_slp<Q, JC, MINB, R>;
+    const size_t sm = (size_t)10 * Q * kSlpLd * sizeof(double) + (size_t)8 * kTile * sizeof(int);
+    auto kern = k_blocks_slp<Q, JC, MINB, R, UJ, S>;
     H2B_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     const int64_t nj = jobs->n_jobs;
     for (int64_t j0 = 0; j0 < nj; j0 += 2147483647LL) {
@@ -966,24 +1084,41 @@ extern "C" int h2b_touch_count(const h2b_mesh* m, int64_t* d_row_ptr, int64_t* h
     return ok();
 }
 
+// exclusive scan of n int32 counts into d_pos (n + 1 entries, int32)
+static int scan_counts(const int32_t* d_cnt, int32_t* d_pos, int64_t n, cudaStream_t st) {
+    size_t tmp_bytes = 0;
+    H2B_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_cnt, d_pos, n + 1, st));
+    void* tmp;
+    H2B_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, st));
+    H2B_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, d_cnt, d_pos, n + 1, st));
+    H2B_CUDA_TRY(cudaFreeAsync(tmp, st));
+    return 0;
+}
+
 extern "C" int h2b_touch_fill(const h2b_mesh* m, const int64_t* d_row_ptr, const int64_t* h_case_count,
                               int32_t* d_col, int32_t* d_info, int32_t* d_case_list, void* stream) {
     if (!m || !d_row_ptr || !h_case_count || !d_col || !d_info || !d_case_list)
         return fail(H2B_ERR_INVALID, "h2b_touch_fill: bad argument");
     cudaStream_t st = as_stream(stream);
     const int64_t F = m->n_triangles;
+    if (h_case_count[3] >= (int64_t)INT32_MAX) return fail(H2B_ERR_INVALID, "h2b_touch_fill: > 2^31 touching pairs");
     int* flags;
     if (int rc = alloc_flags(&flags, st)) return rc;
-    unsigned long long hcur[3] = {0ull, (unsigned long long)h_case_count[0],
-                                  (unsigned long long)(h_case_count[0] + h_case_count[1])};
-    unsigned long long* cur;
-    H2B_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&cur), sizeof(hcur), st));
-    H2B_CUDA_TRY(cudaMemcpyAsync(cur, hcur, sizeof(hcur), cudaMemcpyHostToDevice, st));
-    if (F > 0)
-        k_touch_fill<<<(unsigned)((F + 127) / 128), 128, 0, st>>>(m->d_triangles, F, m->d_vt_ptr, m->d_vt_idx,
-                                                                 d_row_ptr, d_col, d_info, d_case_list, cur, flags);
-    H2B_CUDA_TRY(cudaGetLastError());
-    H2B_CUDA_TRY(cudaFreeAsync(cur, st));
+    if (F > 0) {
+        int32_t *cnt, *pos;
+        H2B_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&cnt), (3 * F + 1) * sizeof(int32_t), st));
+        H2B_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&pos), (3 * F + 1) * sizeof(int32_t), st));
+        H2B_CUDA_TRY(cudaMemsetAsync(cnt + 3 * F, 0, sizeof(int32_t), st));
+        const unsigned g = (unsigned)((F + 127) / 128);
+        k_touch_fill<<<g, 128, 0, st>>>(m->d_triangles, F, m->d_vt_ptr, m->d_vt_idx, d_row_ptr, d_col, d_info, cnt,
+                                         flags);
+        H2B_CUDA_TRY(cudaGetLastError());
+        if (int rc = scan_counts(cnt, pos, 3 * F, st)) return rc;
+        k_touch_list<<<g, 128, 0, st>>>(d_row_ptr, F, d_info, pos, d_case_list);
+        H2B_CUDA_TRY(cudaGetLastError());
+        H2B_CUDA_TRY(cudaFreeAsync(pos, st));
+        H2B_CUDA_TRY(cudaFreeAsync(cnt, st));
+    }
     return check_flags(flags, st);
 }
 
@@ -991,26 +1126,35 @@ extern "C" int h2b_touch_half(const h2b_touch* t, int32_t* d_half_list, int64_t*
     if (!t || !d_half_list || !h_half_off || !t->h_case_off) return fail(H2B_ERR_INVALID, "h2b_touch_half: bad argument");
     cudaStream_t st = as_stream(stream);
     const int64_t* co = t->h_case_off;
+    const int64_t F = t->n_panels;
     const int64_t n_id = co[1] - co[0], n_edge = co[2] - co[1], n_vert = co[3] - co[2];
     if ((n_edge & 1) || (n_vert & 1)) return fail(H2B_ERR_INVALID, "h2b_touch_half: touching relation not symmetric");
     const int64_t off[4] = {0, n_id, n_id + n_edge / 2, n_id + n_edge / 2 + n_vert / 2};
     if (n_id > 0)
         H2B_CUDA_TRY(cudaMemcpyAsync(d_half_list, t->d_case_list + co[0], n_id * sizeof(int32_t),
                                      cudaMemcpyDeviceToDevice, st));
-    unsigned long long hcur[2] = {(unsigned long long)off[1], (unsigned long long)off[2]}, hend[2];
-    unsigned long long* cur;
-    H2B_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&cur), sizeof(hcur), st));
-    H2B_CUDA_TRY(cudaMemcpyAsync(cur, hcur, sizeof(hcur), cudaMemcpyHostToDevice, st));
-    const int64_t n = co[3] - co[1];
-    if (n > 0)
-        k_touch_half<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(t->d_row_ptr, t->n_panels, t->d_col, t->d_info,
-                                                                 t->d_case_list, co[1], co[3], d_half_list, cur);
-    H2B_CUDA_TRY(cudaGetLastError());
-    H2B_CUDA_TRY(cudaMemcpyAsync(hend, cur, sizeof(hend), cudaMemcpyDeviceToHost, st));
-    H2B_CUDA_TRY(cudaFreeAsync(cur, st));
-    H2B_CUDA_TRY(cudaStreamSynchronize(st));
-    if ((int64_t)hend[0] != off[2] || (int64_t)hend[1] != off[3])
-        return fail(H2B_ERR_INVALID, "h2b_touch_half: touching relation not symmetric");
+    if (F > 0 && n_edge + n_vert > 0) {
+        // per row panel: its (a < b) edge and vertex pairs, segment-major;
+        // one scan places them (rows ascending, columns ascending)
+        int32_t *cnt, *pos;
+        H2B_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&cnt), (2 * F + 1) * sizeof(int32_t), st));
+        H2B_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&pos), (2 * F + 1) * sizeof(int32_t), st));
+        H2B_CUDA_TRY(cudaMemsetAsync(cnt + 2 * F, 0, sizeof(int32_t), st));
+        const unsigned g = (unsigned)((F + 127) / 128);
+        k_half_count<<<g, 128, 0, st>>>(t->d_row_ptr, F, t->d_col, t->d_info, cnt);
+        H2B_CUDA_TRY(cudaGetLastError());
+        if (int rc = scan_counts(cnt, pos, 2 * F, st)) return rc;
+        int32_t hpos[2];  // start of the vertex part, total
+        H2B_CUDA_TRY(cudaMemcpyAsync(hpos, pos + F, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        H2B_CUDA_TRY(cudaMemcpyAsync(hpos + 1, pos + 2 * F, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        k_half_fill<<<g, 128, 0, st>>>(t->d_row_ptr, F, t->d_col, t->d_info, pos, off[1], d_half_list);
+        H2B_CUDA_TRY(cudaGetLastError());
+        H2B_CUDA_TRY(cudaFreeAsync(pos, st));
+        H2B_CUDA_TRY(cudaFreeAsync(cnt, st));
+        H2B_CUDA_TRY(cudaStreamSynchronize(st));
+        if ((int64_t)hpos[0] != n_edge / 2 || (int64_t)hpos[1] != n_edge / 2 + n_vert / 2)
+            return fail(H2B_ERR_INVALID, "h2b_touch_half: touching relation not symmetric");
+    }
     for (int i = 0; i < 4; ++i) h_half_off[i] = off[i];
     return ok();
 }
@@ -1077,7 +1221,7 @@ extern "C" int h2b_pair_blocks_slp(const h2b_mesh* m, const double* d_panel_poin
     switch (Q) {
         case 1: rc = launch_slp<1, 1>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
         case 4: rc = launch_slp<4, 4>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
-        case 9: rc = launch_slp<9, H2B_SLP9_JC, H2B_SLP9_MINB, H2B_SLP9_R>(m, d_panel_points, jobs, t, d_touch_values, d_out,
+        case 9: rc = launch_slp<9, H2B_SLP9_JC, H2B_SLP9_MINB, H2B_SLP9_R, H2B_SLP9_UJ, H2B_SLP9_S>(m, d_panel_points, jobs, t, d_touch_values, d_out,
                                                                         flags, st);
             break;
         case 16: rc = launch_slp<16, 8>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;

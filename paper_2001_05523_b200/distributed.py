@@ -75,11 +75,10 @@ def partition_rows(rt, near_C, far_K, ranks, world):
 
 def block_tree_partition(bt, row_basis, col_basis, world):
     """partition_rows from the block tree and the bases (before assembly)."""
-    from .containers import FarLayout, near_layout
+    from .containers import _basis_ranks, far_layout, near_layout
 
-    rr = np.array([row_basis.rank[u] for u in range(bt.row_tree.n_nodes)], dtype=np.int64)
-    cr = np.array([col_basis.rank[u] for u in range(bt.col_tree.n_nodes)], dtype=np.int64)
-    return partition_rows(bt.row_tree, near_layout(bt).C, FarLayout(bt, rr, cr).K, rr, world)
+    rr = _basis_ranks(row_basis, bt.row_tree.n_nodes)
+    return partition_rows(bt.row_tree, near_layout(bt).C, far_layout(bt, row_basis, col_basis).K, rr, world)
 
 
 def operator_partition(H, world):
@@ -173,13 +172,11 @@ class RowShard:
         return near_layout(self.view).entries
 
     def plan(self):
-        from .containers import FarLayout, MatvecPlan, near_layout
+        from .containers import MatvecPlan, far_layout, near_layout
 
         rt = self.bt.row_tree
-        rr = np.array([self.rb.rank[u] for u in range(rt.n_nodes)], dtype=np.int64)
-        cr = np.array([self.cb.rank[u] for u in range(self.bt.col_tree.n_nodes)], dtype=np.int64)
         row_local = np.arange(rt.n_dofs, dtype=np.int64) - self.lo  # only owned rows are written
-        return MatvecPlan(self.view, self.rb, self.cb, self.S, self.D, FarLayout(self.view, rr, cr),
+        return MatvecPlan(self.view, self.rb, self.cb, self.S, self.D, far_layout(self.view, self.rb, self.cb),
                           near_layout(self.view), owned=self.owned, col_perm=self.pad_index, row_perm=row_local)
 
 

@@ -275,17 +275,18 @@ def block_partners(uids):
     return np.where(key[order][pos] == tkey, order[pos], -1)
 
 
-def mirror_jobs(jobs, uids):
+def mirror_jobs(jobs, uids, partner=None):
     """Symmetric single-layer blocks (same tree and basis on both sides, so
     block (s, t) = block (t, s)^T): keep one job per block pair {(t, s), (s, t)}
     with the other written as its mirror; a diagonal block (t, t) keeps its
     upper triangle.  jobs: (n, 6) in the order of uids (n, 2)."""
     jobs = np.asarray(jobs, dtype=np.int64).reshape(-1, 6)
     uids = np.asarray(uids, dtype=np.int64).reshape(-1, 2)
-    out = _as_job8(jobs).copy()
+    out = _as_job8(jobs)
     if len(jobs) == 0:
         return out
-    partner = block_partners(uids)
+    if partner is None:
+        partner = block_partners(uids)
     keep = (partner < 0) | (uids[:, 0] <= uids[:, 1])
     m = keep & (partner >= 0)
     out[m, 6] = jobs[partner[m], 4]
@@ -293,7 +294,7 @@ def mirror_jobs(jobs, uids):
     return out[keep]
 
 
-def mirror_jobs_owned(jobs, uids, dst_off, dst_ld):
+def mirror_jobs_owned(jobs, uids, dst_off, dst_ld, partner=None):
     """The jobs of mirror_jobs restricted to the blocks one rank stores (row
     sharding).  jobs (n, 6) / uids (n, 2): the FULL block list (integration
     geometry of every block); dst_off / dst_ld (n,): where this rank stores
@@ -305,9 +306,10 @@ def mirror_jobs_owned(jobs, uids, dst_off, dst_ld):
     uids = np.asarray(uids, dtype=np.int64).reshape(-1, 2)
     if len(jobs) == 0:
         return np.zeros((0, 8), dtype=np.int64)
-    partner = block_partners(uids)
+    if partner is None:
+        partner = block_partners(uids)
     keep = (partner < 0) | (uids[:, 0] <= uids[:, 1])
-    out = _as_job8(jobs).copy()
+    out = _as_job8(jobs)
     out[:, 4] = dst_off
     out[:, 5] = dst_ld
     m = keep & (partner >= 0)

@@ -1,9 +1,8 @@
-# scratch GPU script (session r02b): touch table rewrite + SLP variants
+# scratch GPU script (session r02e)
 set -x
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -x -k "touch or singular or quadrature or sharded or nearfield" > gpurun_out/r02b_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r02b_pytest.log
-./tools/_bin/mufu_probe > gpurun_out/r02b_mufu.txt 2>&1
-NF_LEVEL=8 NF_DLP=0 timeout 900 python tools/nf_variants.py old base r3 j3r3 t256j3r3 r1 > gpurun_out/r02b_nfv.txt 2>&1
-timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/r02b_bench.json 2> gpurun_out/r02b_bench.err; echo "bench rc=$?" >> gpurun_out/r02b_bench.err
-timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/r02b_ref.json 2> gpurun_out/r02b_ref.err; echo "ref rc=$?" >> gpurun_out/r02b_ref.err
-tail -3 gpurun_out/r02b_pytest.log; cat gpurun_out/r02b_mufu.txt gpurun_out/r02b_nfv.txt; tail -3 gpurun_out/r02b_bench.err; tail -3 gpurun_out/r02b_ref.err
+NF_LEVEL=8 NF_DLP=0 timeout 900 python tools/nf_variants.py prev r3b s3u3 s3u9 s3u1 s3u3t256 s3u1t256 s9u9 s9u9t256 > gpurun_out/r02e_nfv.txt 2>&1
+timeout 600 python tools/mv_run.py --config 3 --matvecs 2 > gpurun_out/r02e_mvrun_plain.log 2>&1; echo "mvrun rc=$?" >> gpurun_out/r02e_mvrun_plain.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_matvec" -c 1 -o gpurun_out/r02e_mv3 python tools/mv_run.py --config 3 --matvecs 2 > gpurun_out/r02e_ncu_mv3.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --csv --log-file gpurun_out/r02e_launches.csv python bench.py --steps 5 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+cat gpurun_out/r02e_nfv.txt; tail -2 gpurun_out/r02e_mvrun_plain.log; tail -3 gpurun_out/r02e_ncu_mv3.log; wc -l gpurun_out/r02e_launches.csv
