@@ -284,6 +284,28 @@ int h2b_basis_forward(const h2b_basis* b, const double* d_xp, double* d_xhat, vo
  * place; d_yp is accumulated into. */
 int h2b_basis_backward(const h2b_basis* b, double* d_yhat, double* d_yp, void* stream);
 
+/* Hypersingular P1 x P1 blocks (kernels.hyp_block, kernels.py:471-511) from
+ * single-layer panel-pair values d_vals (h2b_pair_blocks_slp over each
+ * block's incident row x column panels, row-major n_pb wide at v_off):
+ * out[out_off + i ld + j] = sum over incident panels a of row vertex i and b
+ * of column vertex j of <curl_a(i), curl_b(j)> V_ab, in the reference's
+ * np.add.at order.  d_desc: int64 x 8 per block (nr, nc, v_off, n_pb, r_inc,
+ * c_inc, out_off, ld); incidences of row vertex i of a block:
+ * [d_r_ptr[r_inc + i], d_r_ptr[r_inc + i + 1]) into d_r_pos (panel position in
+ * the block's row panel list) and d_r_cl (3 * panel + local vertex: row of the
+ * (3F x 3) curl table d_curls); the same for columns.  Raises
+ * H2B_ERR_NONFINITE on a non-finite entry.  Synchronises. */
+int h2b_hyp_scatter(int64_t n_blocks, const int64_t* d_desc, const int32_t* d_r_ptr, const int32_t* d_r_pos,
+                    const int32_t* d_r_cl, const int32_t* d_c_ptr, const int32_t* d_c_pos, const int32_t* d_c_cl,
+                    const double* d_curls, const double* d_vals, double* d_out, void* stream);
+
+/* Block transpose between two packed layouts (H2Matrix.rmatvec,
+ * containers.py:272-288, runs the matvec on the transposed operator): for each
+ * of n_blocks descriptors (src_off, src_ld, rows, cols, dst_off, dst_ld),
+ * int64 x 6 on the device, dst[dst_off + j dst_ld + i] = src[src_off + i src_ld + j].
+ * Entries of dst outside the blocks are left untouched. */
+int h2b_transpose_blocks(int64_t n_blocks, const int64_t* d_desc, const double* d_src, double* d_dst, void* stream);
+
 /* ====================== CG vector kernels (device) ========================= */
 
 /* Fused passes of the Jacobi-preconditioned CG iteration (solver.cg,
@@ -392,10 +414,12 @@ int h2b_matvec_host(h2b_plan* plan, const double* h_x, double* h_y, void* stream
  * with the environment variable H2B_TRACE=1 (3 words per CTA ticket: start
  * ns, end ns, SM id; then 5 words of ticket-range boundaries). */
 int h2b_plan_trace(h2b_plan* plan, unsigned long long* h_out, int64_t cap);
-/* Plan facts (7 words): symmetric nearfield in use (0/1; single-GPU plans whose
+/* Plan facts (9 words): symmetric nearfield in use (0/1; single-GPU plans whose
  * nearfield is symmetric bit for bit stream each block pair once), nearfield
  * bytes per matvec, nearfield tasks, coupling tasks, partial-vector bytes,
- * symmetric couplings in use (0/1; same rule for S), coupling bytes per matvec. */
+ * symmetric couplings in use (always 0), coupling bytes per matvec, TMA stage
+ * bytes per CTA (chosen at plan creation from the CTA's other shared memory;
+ * environment H2B_STAGE_KB overrides), dynamic shared memory per CTA. */
 int h2b_plan_info(h2b_plan* plan, int64_t* h_out);
 /* Multi-right-hand-side product Y = A X for 1 <= nrhs <= 16 device vectors
  * (X: n_cols x nrhs, Y: n_rows x nrhs, row-major, natural dof order) over the

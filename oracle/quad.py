@@ -8,6 +8,8 @@ Reference: /root/reference/pkg/src/h2bem/
   kernels.touching_pairs          kernels.py:333-343
   kernels.panel_pair_matrix       kernels.py:365-434
   kernels.slp_block / dlp_block   kernels.py:437-468
+  kernels.triangle_curls          kernels.py:229-239
+  kernels.hyp_block               kernels.py:471-511
 
 Distances are direct differences (not the reference's Gram identity); the two
 agree to ~1e-12 relative, far inside the 1e-10 bar.
@@ -182,4 +184,45 @@ def dlp_block(V, T, N, A, vt_ptr, vt_idx, rows, cols, q, table=None):
     for l in range(3):
         keep = np.flatnonzero(cj[:, l] >= 0)
         np.add.at(block.T, cj[keep, l], vals[:, keep, l].T)
+    return block
+
+
+def triangle_curls(V, T, A):
+    """Surface curl of each P1 hat per panel, (F, 3, 3) -- kernels.py:229-239:
+    curls[f, l] = (V_{l+1} - V_{l+2}) / (2 area_f)."""
+    c = V[T]
+    out = np.empty_like(c)
+    for l in range(3):
+        out[:, l, :] = c[:, (l + 1) % 3, :] - c[:, (l + 2) % 3, :]
+    return out / (2.0 * A)[:, None, None]
+
+
+def hyp_block(V, T, N, A, vt_ptr, vt_idx, rows, cols, q, table=None, curls=None):
+    """Hypersingular P1 x P1 block through the surface-curl representation --
+    kernels.py:471-511: w_ij = sum over incident panel pairs (a, b) of
+    <curl_a(i), curl_b(j)> times the single-layer panel-pair integral."""
+    rows = np.asarray(rows, dtype=np.int64)
+    cols = np.asarray(cols, dtype=np.int64)
+    if curls is None:
+        curls = triangle_curls(V, T, A)
+    pa = np.unique(np.concatenate([vt_idx[vt_ptr[v] : vt_ptr[v + 1]] for v in rows]))
+    pb = np.unique(np.concatenate([vt_idx[vt_ptr[v] : vt_ptr[v + 1]] for v in cols]))
+    vals = pair_matrix(V, T, N, A, pa, pb, "slp", q, table)
+    rpos = -np.ones(len(V), dtype=np.int64)
+    rpos[rows] = np.arange(len(rows))
+    cpos = -np.ones(len(V), dtype=np.int64)
+    cpos[cols] = np.arange(len(cols))
+    ri, cj = rpos[T[pa]], cpos[T[pb]]
+    ca, cb = curls[pa], curls[pb]
+    block = np.zeros((len(rows), len(cols)))
+    for la in range(3):
+        ka = ri[:, la] >= 0
+        if not ka.any():
+            continue
+        for lb in range(3):
+            kb = cj[:, lb] >= 0
+            if not kb.any():
+                continue
+            dots = ca[ka, la, :] @ cb[kb, lb, :].T
+            np.add.at(block, (ri[ka, la][:, None], cj[kb, lb][None, :]), vals[np.ix_(ka, kb)] * dots)
     return block

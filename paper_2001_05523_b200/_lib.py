@@ -108,7 +108,7 @@ EXPORTS = (
     "h2b_diagonal", "h2b_plan_trace", "h2b_plan_info", "h2b_dlp_jobs_build", "h2b_dlp_jobs_sizes", "h2b_dlp_jobs_copy",
     "h2b_dlp_jobs_free", "h2b_gca_columns", "h2b_gca_aca", "h2b_cg_workspace_size", "h2b_cg_dot", "h2b_cg_step",
     "h2b_cg_direction", "h2b_matmat_create", "h2b_matmat_destroy", "h2b_matmat", "h2b_pair_integrals",
-    "h2b_basis_forward", "h2b_basis_backward",
+    "h2b_basis_forward", "h2b_basis_backward", "h2b_transpose_blocks", "h2b_hyp_scatter",
 )
 
 _lib = None
@@ -166,6 +166,8 @@ def lib():
                                          ctypes.POINTER(Rule), vp, vp]
         L.h2b_basis_forward.argtypes = [ctypes.POINTER(Basis), vp, vp, vp]
         L.h2b_basis_backward.argtypes = [ctypes.POINTER(Basis), vp, vp, vp]
+        L.h2b_transpose_blocks.argtypes = [ctypes.c_int64, vp, vp, vp, vp]
+        L.h2b_hyp_scatter.argtypes = [ctypes.c_int64] + [vp] * 11
         L.h2b_gca_aca.argtypes = [ctypes.POINTER(GcaBatch), ctypes.c_double, vp, vp, vp, vp, ctypes.c_int32, vp, vp]
         _lib = L
     return _lib

@@ -673,6 +673,13 @@ class H2Matrix:
         return self.plan().apply(x)
 
     def rmatvec(self, x):
+        """x^T A (containers.py:272-288).  A single-layer operator assembled
+        with one basis on both sides is symmetric entry by entry (mirrored
+        couplings and nearfield), so its transpose is the operator itself and
+        the matvec plan is reused; otherwise the couplings and nearfield are
+        transposed on the device (h2b_transpose_blocks) into a plan for A^T."""
+        if getattr(self, "symmetric", False):
+            return self.matvec(x)
         if self._tplan is None:
             self._tplan = _transposed_plan(self)
         return self._tplan.apply(x)
@@ -899,11 +906,11 @@ class MatvecPlan:
         """Plan facts (h2b_plan_info): whether the nearfield is streamed once
         per block pair (single-GPU plans of a bitwise symmetric nearfield), the
         nearfield bytes one matvec streams, task counts."""
-        out = (ctypes.c_int64 * 7)()
+        out = (ctypes.c_int64 * 9)()
         _lib.check(_lib.lib().h2b_plan_info(self.handle, out))
         return {"near_symmetric": bool(out[0]), "near_bytes": int(out[1]), "near_tasks": int(out[2]),
                 "coupling_tasks": int(out[3]), "partial_bytes": int(out[4]), "coupling_symmetric": bool(out[5]),
-                "coupling_bytes": int(out[6])}
+                "coupling_bytes": int(out[6]), "stage_bytes": int(out[7]), "smem_per_cta": int(out[8])}
 
 
 class MatmatPlan:
@@ -978,20 +985,16 @@ def _transposed_plan(H):
 
 
 def _transpose_packed(src, la, lb, total):
-    """Gather map: entry (i, j) of block b in layout `la` -> (j, i) in `lb`."""
-    t = D.torch()
-    idx = np.zeros(total, dtype=np.int64)
-    mask = np.zeros(total, dtype=bool)
-    for b in range(len(la.blk_off)):
-        nr, nc = int(la.blk_rows[b]), int(la.blk_cols[b])
-        if nr == 0 or nc == 0:
-            continue
-        i = np.arange(nr)[:, None]
-        j = np.arange(nc)[None, :]
-        s = la.blk_off[b] + i * la.blk_ld[b] + j
-        d = lb.blk_off[b] + j * lb.blk_ld[b] + i
-        idx[d.ravel()] = s.ravel()
-        mask[d.ravel()] = True
-    out = src[D.dev(idx)]
-    out[D.dev(~mask)] = 0.0
-    return out.contiguous()
+    """Repack on the device (h2b_transpose_blocks): entry (i, j) of block b in
+    layout `la` -> (j, i) of block b in layout `lb`; padding stays zero."""
+    out = D.zeros((total,))
+    n = len(la.blk_off)
+    if n:
+        desc = np.stack([la.blk_off, la.blk_ld, la.blk_rows, la.blk_cols, lb.blk_off, lb.blk_ld],
+                        axis=1).astype(np.int64)
+        keep = (desc[:, 2] > 0) & (desc[:, 3] > 0)
+        desc = np.ascontiguousarray(desc[keep])
+        dd = D.dev(desc, np.int64)
+        _lib.check(_lib.lib().h2b_transpose_blocks(len(desc), dd.data_ptr(), src.data_ptr(), out.data_ptr(),
+                                                   D.stream()))
+    return out

@@ -11,6 +11,7 @@
 //             leaf  yp[start_t + i] += sum_c V_t[i, c] y_hat_t[c]
 // Every output is written by one lane in a fixed order (deterministic).
 
+#include <algorithm>
 #include <vector>
 
 #include "device_common.cuh"
@@ -92,10 +93,46 @@ int check_basis(const h2b_basis* b) {
     return ok();
 }
 
+// one CTA per block: dst[dst_off + j * dst_ld + i] = src[src_off + i * src_ld + j]
+// through a 32 x 33 shared tile (coalesced on both sides)
+__global__ void k_transpose_blocks(const int64_t* __restrict__ desc, const double* __restrict__ src,
+                                   double* __restrict__ dst) {
+    __shared__ double tile[32][33];
+    const int64_t* d = desc + 6 * (int64_t)blockIdx.x;
+    const int64_t s_off = d[0], s_ld = d[1], rows = d[2], cols = d[3], d_off = d[4], d_ld = d[5];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+    for (int64_t i0 = 0; i0 < rows; i0 += 32)
+        for (int64_t j0 = 0; j0 < cols; j0 += 32) {
+            for (int r = ty; r < 32; r += 8) {
+                const int64_t i = i0 + r, j = j0 + tx;
+                if (i < rows && j < cols) tile[r][tx] = src[s_off + i * s_ld + j];
+            }
+            __syncthreads();
+            for (int r = ty; r < 32; r += 8) {
+                const int64_t j = j0 + r, i = i0 + tx;
+                if (i < rows && j < cols) dst[d_off + j * d_ld + i] = tile[tx][r];
+            }
+            __syncthreads();
+        }
+}
+
 }  // namespace
 }  // namespace h2b
 
 using namespace h2b;
+
+extern "C" int h2b_transpose_blocks(int64_t n_blocks, const int64_t* d_desc, const double* d_src, double* d_dst,
+                                    void* stream) {
+    if (n_blocks < 0 || (n_blocks > 0 && (!d_desc || !d_src || !d_dst)))
+        return fail(H2B_ERR_INVALID, "h2b_transpose_blocks: bad argument");
+    cudaStream_t st = as_stream(stream);
+    for (int64_t b0 = 0; b0 < n_blocks; b0 += 2147483647LL) {
+        const unsigned g = (unsigned)std::min<int64_t>(n_blocks - b0, 2147483647LL);
+        k_transpose_blocks<<<g, 256, 0, st>>>(d_desc + 6 * b0, d_src, d_dst);
+    }
+    H2B_CUDA_TRY(cudaGetLastError());
+    return ok();
+}
 
 extern "C" int h2b_basis_forward(const h2b_basis* b, const double* d_xp, double* d_xhat, void* stream) {
     if (int rc = check_basis(b)) return rc;

@@ -64,10 +64,9 @@ constexpr int kThreads = H2B_THREADS;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxVec = 512;        // max rank / leaf size of the vectors kept in smem
 constexpr int kMaxDepth = 32;
-#ifndef H2B_STAGE_KB
-#define H2B_STAGE_KB 24
-#endif
-constexpr int kStageBytes = H2B_STAGE_KB * 1024;  // TMA staging buffer per CTA (one band)
+// TMA staging buffer per CTA (one band): chosen per plan at creation
+// (plan_stage_bytes) from the shared memory the rest of the CTA needs
+constexpr int kStageMin = 16 * 1024, kStageMax = 40 * 1024;
 
 // record layouts (int64 words)
 constexpr int kBandWords = 24;  // src_off, cols, rows, gidx_off, out_off, is_last, has_cpl, kind, then the
@@ -101,6 +100,7 @@ struct h2b_plan {
     int n_near, n_cpl;
     int max_cols, vec_len;
     int smem;
+    int stage_bytes;     // TMA staging buffer per CTA (plan_stage_bytes)
     int64_t e_bytes_r;
     double* dx;
     double* dy;
@@ -261,6 +261,9 @@ __device__ __forceinline__ void mark(unsigned long long* m, int i) {
 #define H2B_ROWBLOCK 4
 #endif
 constexpr int kRowBlock = H2B_ROWBLOCK;  // rows per warp in rows_dot's many-rows mode
+// widest right-hand side gathered at once (multiple of 128: see task_band);
+// wider band rows are processed in chunks of it
+constexpr int kChunkCols = 768;
 
 __host__ __device__ constexpr int log2c(int n) { return n <= 1 ? 0 : 1 + log2c(n / 2); }
 
@@ -499,7 +502,8 @@ __device__ __forceinline__ void gather_ll(double* rhs, const uint64_t* ll, const
 struct Shared {
     unsigned long long* mark;  // trace slots of this CTA (5 phase marks) or null
     uint64_t* bar;             // mbarrier of the staging buffer
-    char* stage;               // kStageBytes, 128-byte aligned
+    char* stage;               // stage_bytes, 128-byte aligned
+    int stage_bytes;           // the plan's staging buffer size
     double* rhs;               // max_cols
     double* va;                // 2 vec_len ([x_hat_c0; x_hat_c1] in the climb)
     double* vb;                // vec_len (vec_len = max rank / leaf size)
@@ -524,7 +528,7 @@ __device__ __forceinline__ double load_x(const Shared& s, const double* __restri
 // Thread 0 starts staging `bytes` (TMA bulk copy when it fits and is 16-byte
 // aligned; otherwise a plain arrive).  Returns where to read the data from.
 __device__ __forceinline__ const double* stage_issue(const Shared& s, const double* src, int64_t bytes) {
-    const bool fits = bytes > 0 && bytes <= kStageBytes && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+    const bool fits = bytes > 0 && bytes <= s.stage_bytes && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
                       (bytes & 15) == 0;
     if (threadIdx.x == 0) {
         if (fits) {
@@ -537,8 +541,8 @@ __device__ __forceinline__ const double* stage_issue(const Shared& s, const doub
     return fits ? reinterpret_cast<const double*>(s.stage) : src;
 }
 
-__device__ __forceinline__ bool band_staged(int64_t bytes, const double* src) {
-    return bytes > 0 && bytes <= kStageBytes && (reinterpret_cast<uintptr_t>(src) & 15) == 0 && (bytes & 15) == 0;
+__device__ __forceinline__ bool band_staged(const Shared& s, int64_t bytes, const double* src) {
+    return bytes > 0 && bytes <= s.stage_bytes && (reinterpret_cast<uintptr_t>(src) & 15) == 0 && (bytes & 15) == 0;
 }
 
 __device__ void prefetch_slice(const double* base, int64_t bytes, int part, int parts) {
@@ -715,7 +719,7 @@ __device__ void task_forward(const double* __restrict__ c_V, const double* __res
         const int64_t* lv = s.rec + kFwdHead + kFwdLevel * j;
         const int k0 = (int)lv[0], kp = (int)lv[1];
         const int n0 = k0 * kp, n1 = k1 * kp;
-        const bool in_smem = (n0 + n1) * 8 <= kStageBytes;
+        const bool in_smem = (n0 + n1) * 8 <= s.stage_bytes;
         __syncthreads();  // previous users of buf / va are done
         if (in_smem) {
             const double* E0 = c_E + lv[2];
@@ -900,7 +904,7 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
         }
         return;
     }
-    const bool e_smem = par_off >= 0 && k * kp <= kStageBytes / 8;
+    const bool e_smem = par_off >= 0 && k * kp <= s.stage_bytes / 8;
     // transfer / leaf basis matrices are staged TRANSPOSED, so that the
     // thread-per-row products below read consecutive words (no bank conflicts)
     if (e_smem)
@@ -938,7 +942,7 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
     }
     const int size = (int)d[8];
     const int nv = size * k;
-    const bool v_smem = nv <= kStageBytes / 8;
+    const bool v_smem = nv <= s.stage_bytes / 8;
     const double* Vg = r_V + v_off;
     if (v_smem) {
         for (int i = threadIdx.x; i < nv; i += kThreads) {
@@ -967,10 +971,59 @@ __device__ void task_band(const h2b_layout& L, const double* __restrict__ x, con
                           const Shared& s) {
     const int64_t src_off = s.rec[0], gi_off = s.rec[3], out_off = s.rec[4];
     const int cols = (int)s.rec[1], rows = (int)s.rec[2];
-    if (rows > 0) {
+    if (rows > 0 && cols > kChunkCols) {
+        // wide row (a cluster with many couplings): the right-hand side is
+        // gathered kChunkCols columns at a time so shared memory stays small;
+        // rows <= kWarps (the host cuts such bands so), one row per warp, and
+        // every lane walks its columns in the order rows_dot uses, carrying
+        // its four chains across chunks (chunks are multiples of 128
+        // columns): the same bits as the unchunked product
         const double* base = kCoupling ? L.S : L.D;
         const int64_t bytes = (int64_t)rows * cols * 8;
-        const double* M = s.issued ? (band_staged(bytes, base + src_off) ? reinterpret_cast<const double*>(s.stage)
+        const double* M = s.issued ? (band_staged(s, bytes, base + src_off) ? reinterpret_cast<const double*>(s.stage)
+                                                                         : base + src_off)
+                                   : stage_issue(s, base + src_off, bytes);
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        const double* row = M + (int64_t)min(warp, rows - 1) * cols;
+        const int32_t* gidx = (kCoupling ? L.s_gidx : L.d_gidx) + gi_off;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int c = lane;
+        for (int c0 = 0; c0 < cols; c0 += kChunkCols) {
+            const int cn = min(kChunkCols, cols - c0);
+            if (c0 > 0) __syncthreads();  // the previous chunk is consumed
+            if (kCoupling)
+                gather_ll(s.rhs, xhat, gidx + c0, cn, epoch);
+            else if (s.xll)
+                gather_ll(s.rhs, s.xll, gidx + c0, cn, epoch);
+            else
+                gather(s.rhs, x, gidx + c0, cn);
+            if (c0 == 0) mbar_wait(s.bar, s.parity);
+            __syncthreads();
+            const double* v = s.rhs - c0;
+            if (warp < rows) {
+                for (; c + 96 < cols && c < c0 + cn; c += 128) {
+                    a0 = fma(row[c], v[c], a0);
+                    a1 = fma(row[c + 32], v[c + 32], a1);
+                    a2 = fma(row[c + 64], v[c + 64], a2);
+                    a3 = fma(row[c + 96], v[c + 96], a3);
+                }
+                if (c0 + cn == cols)
+                    for (; c < cols; c += 32) a0 = fma(row[c], v[c], a0);
+            }
+        }
+        if (warp < rows) {
+            double sum = (a0 + a1) + (a2 + a3);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            if (lane == 0) s.va[warp] = sum;
+        }
+        __syncthreads();
+        uint64_t* dst = out + 2 * out_off;
+        for (int i = threadIdx.x; i < rows; i += blockDim.x) ll_store(dst + 2 * i, s.va[i], epoch);
+    } else if (rows > 0) {
+        const double* base = kCoupling ? L.S : L.D;
+        const int64_t bytes = (int64_t)rows * cols * 8;
+        const double* M = s.issued ? (band_staged(s, bytes, base + src_off) ? reinterpret_cast<const double*>(s.stage)
                                                                          : base + src_off)
                                    : stage_issue(s, base + src_off, bytes);
         mark(s.mark, 0);
@@ -1112,7 +1165,7 @@ __device__ void task_panel(const double* __restrict__ base, const int32_t* __res
     const int64_t tr_off = s.rec[8], rg_off = s.rec[10];
     const int skip = (int)s.rec[9];
     const int64_t bytes = ((int64_t)rows * cols * 8 + 15) & ~int64_t(15);  // panels are padded to 16 bytes
-    const double* M = s.issued ? (band_staged(bytes, base + src_off) ? reinterpret_cast<const double*>(s.stage)
+    const double* M = s.issued ? (band_staged(s, bytes, base + src_off) ? reinterpret_cast<const double*>(s.stage)
                                                                      : base + src_off)
                                : stage_issue(s, base + src_off, bytes);
     mark(s.mark, 0);
@@ -1135,7 +1188,7 @@ struct KArgs {
     const int64_t* fwd_off;
     int64_t band_base, band_bytes, dgidx_bytes;
     int n_near, n_cpl, n_near_a, n_inner_bands;
-    int max_cols, vec_len;
+    int max_cols, vec_len, stage_bytes;
     int64_t e_bytes_r;
     uint64_t *xhat, *ycpl, *yfin, *ynear;
     unsigned long long* ctrl;
@@ -1275,7 +1328,8 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
     Shared s;
     s.bar = reinterpret_cast<uint64_t*>(smraw);
     s.stage = smraw + 128;
-    s.rhs = reinterpret_cast<double*>(smraw + 128 + kStageBytes);
+    s.stage_bytes = a.stage_bytes;
+    s.rhs = reinterpret_cast<double*>(smraw + 128 + a.stage_bytes);
     s.va = s.rhs + a.max_cols;
     s.vb = s.va + 2 * a.vec_len;
     s.red = s.vb + a.vec_len;
@@ -1391,7 +1445,37 @@ struct SymNear {
     int64_t dsym_len = 0, ppart_len = 0, near_bytes = 0;
 };
 
-int build_sym_near(const h2b_layout& L, const std::vector<int32_t>& rstart, const std::vector<int32_t>& rsize,
+// Staging buffer of a plan: the TMA stage plus the rest of the CTA's shared
+// memory (other_smem: the gathered right-hand side and vectors) decide how
+// many CTAs an SM holds (at most H2B_MINB by registers).  Measured (sphere
+// L6 / L8 / L9-m5, 16-40 KB): 24 KB at 6 CTAs/SM is best where it fits
+// (L6 56 us vs 62 us at 28 KB; L8 765 vs 838 us); where the wide coupling rows
+// of config 3 leave room for only 5 CTAs at 24 KB, 20 KB at 6 CTAs wins
+// (3.63 vs 3.81 ms).  So: the largest stage <= 24 KB that keeps H2B_MINB CTAs
+// per SM, else the one with the most bytes in flight per SM.  H2B_STAGE_KB
+// overrides (tuning experiments).
+int plan_stage_bytes(int other_smem) {
+    if (const char* e = getenv("H2B_STAGE_KB")) {
+        const int kb = atoi(e);
+        if (kb * 1024 >= kStageMin && kb * 1024 <= kStageMax) return kb * 1024;
+    }
+    constexpr int kSmPerSM = 233472, kPerCtaFixed = 1024 + 1792;  // driver reserve + static shared memory
+    auto ctas = [&](int st) { return std::min(H2B_MINB, kSmPerSM / (st + other_smem + kPerCtaFixed)); };
+    for (int st = 24 * 1024; st >= kStageMin; st -= 4096)
+        if (ctas(st) >= H2B_MINB) return st;
+    int best = kStageMin;
+    int64_t best_score = -1;
+    for (int st = kStageMin; st <= kStageMax; st += 4096) {
+        const int64_t score = (int64_t)ctas(st) * st;
+        if (ctas(st) >= 1 && score >= best_score) {
+            best_score = score;
+            best = st;
+        }
+    }
+    return best;
+}
+
+int build_sym_near(int stage_bytes, const h2b_layout& L, const std::vector<int32_t>& rstart, const std::vector<int32_t>& rsize,
                    const std::vector<int32_t>& cstart, const std::vector<int32_t>& csize,
                    const std::vector<int64_t>& rvoff, const std::vector<int32_t>& dcols,
                    const std::vector<int64_t>& doff, const std::vector<int64_t>& dgoff, SymNear& S) {
@@ -1491,7 +1575,7 @@ int build_sym_near(const h2b_layout& L, const std::vector<int32_t>& rstart, cons
             tcol[t].push_back(W);
             W += rsize[b.first];
         }
-        int wmax = std::min(64, std::max(2, (int)(kStageBytes / 8 / std::max(rows, 1))));
+        int wmax = std::min(64, std::max(2, (int)(stage_bytes / 8 / std::max(rows, 1))));
         if ((rows & 1) && (wmax & 1)) --wmax;
         const int64_t gbase = g;
         for (const auto& b : up[t])
@@ -1610,20 +1694,29 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
     const int vec_len = (std::max(maxk, maxleaf) + 1) & ~1;
     // symmetric nearfield: each leaf's partials are summed in the leaf's final
     // task (separate sum tasks in the nearfield stream measured slower)
-    SymNear sym;
-    if (sym_flags & kSymNear)
-        if (int rc = build_sym_near(L, rstart, rsize, cstart, csize, rvoff, dcols, doff, dgoff, sym)) return rc;
     // gathered right-hand side per task: a panel (<= 64 columns) where the
     // symmetric layouts are used, else the widest row of D / S
-    maxcols = std::max(2, maxk);
-    for (int i = 0; i < L.r_nodes; ++i) {
-        maxcols = std::max(maxcols, sym.on ? std::min<int>(dcols[i], 64) : dcols[i]);
-        maxcols = std::max(maxcols, scols[i]);
-    }
-    maxcols = (maxcols + 1) & ~1;
-    const int smem =
-        128 + kStageBytes +
-        (int)sizeof(double) * (maxcols + 3 * vec_len + (sym.on ? 2 * vec_len + kWarps * 64 : kWarps * 32));
+    auto cols_needed = [&](bool sym_on) {
+        int mc = std::max(2, maxk);
+        for (int i = 0; i < L.r_nodes; ++i) {
+            mc = std::max(mc, sym_on ? std::min<int>(dcols[i], 64) : dcols[i]);
+            mc = std::max(mc, scols[i]);
+        }
+        return std::min((mc + 1) & ~1, std::max(kChunkCols, (maxk + 1) & ~1));
+    };
+    auto other_smem = [&](bool sym_on) {
+        return 128 + (int)sizeof(double) * (cols_needed(sym_on) + 3 * vec_len +
+                                             (sym_on ? 2 * vec_len + kWarps * 64 : kWarps * 32));
+    };
+    // symmetric nearfield: each leaf's partials are summed in the leaf's final
+    // task (separate sum tasks in the nearfield stream measured slower)
+    const bool want_sym = (sym_flags & kSymNear) != 0;
+    const int stage = plan_stage_bytes(other_smem(want_sym));
+    SymNear sym;
+    if (want_sym)
+        if (int rc = build_sym_near(stage, L, rstart, rsize, cstart, csize, rvoff, dcols, doff, dgoff, sym)) return rc;
+    maxcols = cols_needed(sym.on);
+    const int smem = stage + other_smem(sym.on);
     if (smem > 227 * 1024) return fail(H2B_ERR_INVALID, "h2b_plan_create: gathered right-hand side exceeds shared memory");
 
     std::vector<int64_t> rec, fwd_off(L.c_leaves);
@@ -1661,7 +1754,7 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
         rec.insert(rec.end(), {cstart[leaf], csize[leaf], crank[leaf], cvoff[leaf], cxoff[leaf], 0, 0});
         const size_t hdr = rec.size() - kFwdHead;
         bool warp_ok = crank[leaf] <= 32 && csize[leaf] <= 64 &&
-                       (int64_t)csize[leaf] * crank[leaf] * 8 <= kStageBytes;
+                       (int64_t)csize[leaf] * crank[leaf] * 8 <= stage;
         int node = leaf, n = 0;
         while (true) {
             const int p = cparent[node];
@@ -1671,7 +1764,7 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
             rec.insert(rec.end(), {crank[c0], crank[p], ceoff[c0], ceoff[node], cxoff[c0], cxoff[p]});
             warp_ok = warp_ok && crank[c0] <= 32 && crank[p] <= 32 &&
                       8 * ((((int64_t)crank[c0] * crank[p] + 1) & ~int64_t(1)) +
-                           (((int64_t)crank[node] * crank[p] + 1) & ~int64_t(1))) <= kStageBytes;
+                           (((int64_t)crank[node] * crank[p] + 1) & ~int64_t(1))) <= stage;
             node = p;
             ++n;
         }
@@ -1685,7 +1778,8 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
     const int64_t band_base = (int64_t)rec.size();
     auto bands_to = [&](std::vector<int64_t>& out, int cols, int rows, int64_t src, int64_t gi, int64_t outo,
                         int kind) {
-        const int per = std::max(1, (int)(kStageBytes / (8 * std::max(cols, 1))));
+        int per = std::max(1, (int)(stage / (8 * std::max(cols, 1))));
+        if (cols > kChunkCols) per = std::min(per, kWarps);  // chunked rows: one row per warp
         int n = 0;
         for (int r0 = 0; r0 < rows; r0 += per, ++n) {
             const int nr = std::min(per, rows - r0);
@@ -1721,7 +1815,7 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
             const int kk = rrank[u], kq = par >= 0 ? rrank[par] : 0;
             const bool lf = rvoff[u] >= 0;
             dw[18] = (kk <= 32 && kq <= 32 && (!lf || rsize[u] <= 64) &&
-                      8 * ((((int64_t)kk * kq + 1) & ~int64_t(1)) + (lf ? (int64_t)rsize[u] * kk : 0)) <= kStageBytes)
+                      8 * ((((int64_t)kk * kq + 1) & ~int64_t(1)) + (lf ? (int64_t)rsize[u] * kk : 0)) <= stage)
                          ? 1 : 0;  // one-warp downward step
         }
         std::vector<int64_t> tmp;
@@ -1808,6 +1902,7 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
     p->max_cols = maxcols;
     p->vec_len = vec_len;
     p->smem = smem;
+    p->stage_bytes = stage;
     p->e_bytes_r = e_bytes_r;
     H2B_CUDA_TRY(cudaGetDevice(&p->device));
     H2B_CUDA_TRY(cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming));
@@ -1977,6 +2072,7 @@ int launch_matvec(h2b_plan* p, const double* d_x, const double* xh, double* y, c
     a.n_cpl = p->n_cpl;
     a.max_cols = p->max_cols;
     a.vec_len = p->vec_len;
+    a.stage_bytes = p->stage_bytes;
     a.e_bytes_r = p->e_bytes_r;
     a.xhat = p->xhat;
     a.ycpl = p->ycpl;
@@ -2065,7 +2161,8 @@ extern "C" int h2b_plan_trace(h2b_plan* p, unsigned long long* h_out, int64_t ca
 // Plan facts: [0] symmetric nearfield in use (0/1), [1] nearfield bytes one
 // matvec streams, [2] nearfield tasks, [3] coupling tasks, [4] bytes of the
 // symmetric partial vectors (LL form), [5] symmetric couplings in use (0/1),
-// [6] coupling bytes one matvec streams.
+// [6] coupling bytes one matvec streams, [7] TMA stage bytes per CTA,
+// [8] dynamic shared memory per CTA.
 extern "C" int h2b_plan_info(h2b_plan* p, int64_t* h_out) {
     if (!p || !h_out) return fail(H2B_ERR_INVALID, "h2b_plan_info: null pointer");
     h_out[0] = p->dsym != nullptr;
@@ -2075,6 +2172,8 @@ extern "C" int h2b_plan_info(h2b_plan* p, int64_t* h_out) {
     h_out[4] = p->ppart_len * 16;
     h_out[5] = 0;  // (symmetric coupling panels: measured slower, removed)
     h_out[6] = p->cpl_bytes;
+    h_out[7] = p->stage_bytes;
+    h_out[8] = p->smem;
     return ok();
 }
 

@@ -525,7 +525,7 @@ __device__ __forceinline__ int64_t touch_find(const int64_t* __restrict__ row_pt
 // 1/(4 pi r) = t (3 - p t^2) / (8 sqrt(2) pi)
 constexpr double kSlpFold = 1.0 / (8.0 * 1.4142135623730950488016887 * kPi);
 
-template <int Q, int JC, int MINB, int R, int UJ, int S>
+template <int Q, int JC, int MINB, int R, int UJ>
 __global__ void __launch_bounds__(H2B_SLP_THREADS, MINB) k_blocks_slp(const double* __restrict__ P, int64_t F,
                                                    const int32_t* __restrict__ T,
                                                    const int64_t* __restrict__ jobs,
@@ -602,86 +602,6 @@ __global__ void __launch_bounds__(H2B_SLP_THREADS, MINB) k_blocks_slp(const doub
 
     int lflags = 0;
     const int np = tri ? nc * (nc + 1) / 2 : nr * nc;
-    if constexpr (S > 1) {
-        // S lanes per panel pair, each holding Q/S column points in registers
-        // for the whole pair (fewer live registers -> more point pairs in
-        // flight); partial sums combined by shuffles in lane order
-        static_assert(Q % S == 0 && S <= 32, "split must divide the rule");
-        constexpr int PW = 32 / S, JS = Q / S;
-        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-        const int slot = lane / S, sub = lane - slot * S;
-        for (int pb = wid * PW; pb < np; pb += nw * PW) {
-            const int p = pb + slot;
-            const bool act = slot < PW && p < np;
-            int a = 0, b = 0;
-            if (act) {
-                if (tri) {
-                    b = (int)((sqrtf(8.0f * (float)p + 1.0f) - 1.0f) * 0.5f);
-                    if ((b + 1) * (b + 2) / 2 <= p) ++b;
-                    if (b * (b + 1) / 2 > p) --b;
-                    a = p - b * (b + 1) / 2;
-                } else {
-                    a = p / nc;
-                    b = p - a * nc;
-                }
-            }
-            const bool touch = act && shares_vertex(rv + 3 * a, cv + 3 * b);
-            double part = 0.0;
-            if (act && !touch) {
-                double y0[JS], y1[JS], y2[JS], yh[JS], yw[JS];
-#pragma unroll
-                for (int k = 0; k < JS; ++k) {
-                    const int sj = (sub * JS + k) * kSlpLd + b;
-                    y0[k] = cx[sj];
-                    y1[k] = cx[Q * kSlpLd + sj];
-                    y2[k] = cx[2 * Q * kSlpLd + sj];
-                    yh[k] = cx[3 * Q * kSlpLd + sj];
-                    yw[k] = cx[4 * Q * kSlpLd + sj];
-                }
-#pragma unroll UJ
-                for (int i = 0; i < Q; ++i) {
-                    const int si = i * kSlpLd + a;
-                    const double x0 = rx[si], x1 = rx[Q * kSlpLd + si], x2 = rx[2 * Q * kSlpLd + si];
-                    const double xh = rx[3 * Q * kSlpLd + si], xw = rx[4 * Q * kSlpLd + si];
-                    double acc = 0.0;
-#pragma unroll
-                    for (int k = 0; k < JS; ++k) {
-                        const double pa = fma(x0, y0[k], fma(x1, y1[k], fma(x2, y2[k], fma(xh, yw[k], yh[k]))));
-                        const double ta = rsqrt_seed(pa);
-                        acc = fma(ta, fma(-pa, ta * ta, 3.0), acc);
-                    }
-                    part = fma(xw, acc, part);
-                }
-            }
-            double tot = part;
-#pragma unroll
-            for (int o = 1; o < S; ++o) {
-                const double v = __shfl_down_sync(0xffffffffu, part, o);
-                if (sub == 0) tot += v;
-            }
-            if (!act || sub != 0) continue;
-            double val = tot;
-            if (touch) {
-                if (t_row_ptr == nullptr) {
-                    lflags |= kFlagTouching;
-                    val = 0.0;
-                } else {
-                    const int64_t k = touch_find(t_row_ptr, t_col, rp[a], cp[b]);
-                    if (k < 0) {
-                        lflags |= kFlagMissing;
-                        val = 0.0;
-                    } else {
-                        val = t_val[k];
-                    }
-                }
-            }
-            if (!isfinite(val)) lflags |= kFlagNonFinite;
-            if (out_off >= 0) out[out_off + (int64_t)a * ld + b] = val;
-            if (m_off >= 0 && !(tri && a == b)) out[m_off + (int64_t)b * m_ld + a] = val;
-        }
-        if (lflags) atomicOr(flags, lflags);
-        return;
-    }
     for (int p = threadIdx.x; p < np; p += blockDim.x) {
         int a, b;
         if (tri) {
@@ -957,6 +877,50 @@ __global__ void __launch_bounds__(256, MINB) k_blocks_dlp(const double* __restri
     if (lflags) atomicOr(flags, lflags);
 }
 
+
+// ----------------------------------------------------------------------------
+// hypersingular P1 x P1 blocks through the surface-curl representation
+// (kernels.py:471-511): w_ij = sum over the incident panels a of i and b of j
+// of <curl_a(i), curl_b(j)> V_ab, V_ab the single-layer panel-pair integrals
+// (k_blocks_slp into a scratch buffer first).  One CTA per block, one thread
+// per entry; contributions added in the reference's np.add.at order (local
+// vertex of i, local vertex of j, then row panel, then column panel).
+// desc per block (int64 x 8): nr, nc, v_off, n_pb, r_inc, c_inc, out_off, ld.
+// Incidence entries: pos (panel position in the block's row / column panel
+// list) and cl = 3 * panel + local vertex (row of the (3F, 3) curl table).
+__global__ void k_hyp_scatter(const int64_t* __restrict__ desc, const int32_t* __restrict__ r_ptr,
+                              const int32_t* __restrict__ r_pos, const int32_t* __restrict__ r_cl,
+                              const int32_t* __restrict__ c_ptr, const int32_t* __restrict__ c_pos,
+                              const int32_t* __restrict__ c_cl, const double* __restrict__ curls,
+                              const double* __restrict__ vals, double* __restrict__ out, int* __restrict__ flags) {
+    const int64_t* d = desc + 8 * (int64_t)blockIdx.x;
+    const int nr = (int)d[0], nc = (int)d[1];
+    const int64_t v_off = d[2], npb = d[3], ri = d[4], ci = d[5], o_off = d[6], ld = d[7];
+    int lflags = 0;
+    for (int e = threadIdx.x; e < nr * nc; e += blockDim.x) {
+        const int i = e / nc, j = e - i * nc;
+        const int ra = r_ptr[ri + i], re = r_ptr[ri + i + 1], ca = c_ptr[ci + j], ce = c_ptr[ci + j + 1];
+        double sum = 0.0;
+        for (int la = 0; la < 3; ++la)
+            for (int lb = 0; lb < 3; ++lb)
+                for (int p = ra; p < re; ++p) {
+                    const int cla = r_cl[p];
+                    if (cla % 3 != la) continue;
+                    const double x0 = curls[3 * cla], x1 = curls[3 * cla + 1], x2 = curls[3 * cla + 2];
+                    const double* vrow = vals + v_off + (int64_t)r_pos[p] * npb;
+                    for (int q = ca; q < ce; ++q) {
+                        const int clb = c_cl[q];
+                        if (clb % 3 != lb) continue;
+                        const double dot = fma(x2, curls[3 * clb + 2], fma(x1, curls[3 * clb + 1], x0 * curls[3 * clb]));
+                        sum += vrow[c_pos[q]] * dot;
+                    }
+                }
+        if (!isfinite(sum)) lflags |= kFlagNonFinite;
+        out[o_off + (int64_t)i * ld + j] = sum;
+    }
+    if (lflags) atomicOr(flags, lflags);
+}
+
 int check_flags(int* d_flags, cudaStream_t st) {
     int h = 0;
     H2B_CUDA_TRY(cudaMemcpyAsync(&h, d_flags, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -983,20 +947,17 @@ int alloc_flags(int** d, cudaStream_t st) {
 #define H2B_SLP9_MINB 4
 #endif
 #ifndef H2B_SLP9_R
-#define H2B_SLP9_R 2
+#define H2B_SLP9_R 3  // row points per step (sphere L8: 3 rows 5.85 ms, 2 rows 6.09 ms, 1 row 5.96 ms)
 #endif
 #ifndef H2B_SLP9_UJ
 #define H2B_SLP9_UJ 16  // unroll of the column-chunk loop (16: fully)
 #endif
-#ifndef H2B_SLP9_S
-#define H2B_SLP9_S 1    // lanes per panel pair (1: one thread per pair)
-#endif
 
-template <int Q, int JC, int MINB = 2, int R = 2, int UJ = 16, int S = 1>
+template <int Q, int JC, int MINB = 2, int R = 2, int UJ = 16>
 int launch_slp(const h2b_mesh* m, const double* P, const h2b_jobs* jobs, const h2b_touch* t,
                const double* tv, double* out, int* flags, cudaStream_t st) {
     const size_t sm = (size_t)10 * Q * kSlpLd * sizeof(double) + (size_t)8 * kTile * sizeof(int);
-    auto kern = k_blocks_slp<Q, JC, MINB, R, UJ, S>;
+    auto kern = k_blocks_slp<Q, JC, MINB, R, UJ>;
     H2B_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     const int64_t nj = jobs->n_jobs;
     for (int64_t j0 = 0; j0 < nj; j0 += 2147483647LL) {
@@ -1221,7 +1182,7 @@ extern "C" int h2b_pair_blocks_slp(const h2b_mesh* m, const double* d_panel_poin
     switch (Q) {
         case 1: rc = launch_slp<1, 1>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
         case 4: rc = launch_slp<4, 4>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
-        case 9: rc = launch_slp<9, H2B_SLP9_JC, H2B_SLP9_MINB, H2B_SLP9_R, H2B_SLP9_UJ, H2B_SLP9_S>(m, d_panel_points, jobs, t, d_touch_values, d_out,
+        case 9: rc = launch_slp<9, H2B_SLP9_JC, H2B_SLP9_MINB, H2B_SLP9_R, H2B_SLP9_UJ>(m, d_panel_points, jobs, t, d_touch_values, d_out,
                                                                         flags, st);
             break;
         case 16: rc = launch_slp<16, 8>(m, d_panel_points, jobs, t, d_touch_values, d_out, flags, st); break;
@@ -1325,4 +1286,24 @@ extern "C" int h2b_pair_integrals(const h2b_mesh* m, int64_t n, const int32_t* d
     H2B_CUDA_TRY(cudaFreeAsync(list, st));
     H2B_CUDA_TRY(cudaFreeAsync(cnt, st));
     return ok();
+}
+
+extern "C" int h2b_hyp_scatter(int64_t n_blocks, const int64_t* d_desc, const int32_t* d_r_ptr,
+                               const int32_t* d_r_pos, const int32_t* d_r_cl, const int32_t* d_c_ptr,
+                               const int32_t* d_c_pos, const int32_t* d_c_cl, const double* d_curls,
+                               const double* d_vals, double* d_out, void* stream) {
+    if (n_blocks < 0 || (n_blocks > 0 && (!d_desc || !d_r_ptr || !d_r_pos || !d_r_cl || !d_c_ptr || !d_c_pos ||
+                                          !d_c_cl || !d_curls || !d_vals || !d_out)))
+        return fail(H2B_ERR_INVALID, "h2b_hyp_scatter: bad argument");
+    if (n_blocks == 0) return ok();
+    cudaStream_t st = as_stream(stream);
+    int* flags;
+    if (int rc = alloc_flags(&flags, st)) return rc;
+    for (int64_t b0 = 0; b0 < n_blocks; b0 += 2147483647LL) {
+        const unsigned g = (unsigned)std::min<int64_t>(n_blocks - b0, 2147483647LL);
+        k_hyp_scatter<<<g, 256, 0, st>>>(d_desc + 8 * b0, d_r_ptr, d_r_pos, d_r_cl, d_c_ptr, d_c_pos, d_c_cl,
+                                          d_curls, d_vals, d_out, flags);
+    }
+    H2B_CUDA_TRY(cudaGetLastError());
+    return check_flags(flags, st);
 }

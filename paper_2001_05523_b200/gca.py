@@ -438,9 +438,13 @@ def assemble_h2(ctx, kind, block_tree, row_basis, col_basis, q_near, nearfield_c
     """H^2 operator with S_b = G[pivots_t, pivots_s] (regular quadrature at
     q_near, touching pairs rejected) and the dense nearfield (regular order
     q_near, Sauter-Schwab order q_singular, default q_near), all on the GPU."""
-    from .containers import H2Matrix, assemble_couplings, assemble_nearfield_device
+    from .containers import H2Matrix, _symmetric_trees, assemble_couplings, assemble_nearfield_device
 
     qs = q_near if q_singular is None else q_singular
     S = assemble_couplings(ctx, kind, block_tree, row_basis, col_basis, q_near)
     D = assemble_nearfield_device(ctx, kind, block_tree, q_near, qs, cache=nearfield_cache)
-    return H2Matrix.from_device(block_tree, row_basis, col_basis, S, D)
+    H = H2Matrix.from_device(block_tree, row_basis, col_basis, S, D)
+    # single layer, one basis, one tree: couplings and nearfield are assembled
+    # as mirrors of each other, so A = A^T entry by entry
+    H.symmetric = kind == kernels.SLP and row_basis is col_basis and _symmetric_trees(block_tree)
+    return H

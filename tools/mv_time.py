@@ -50,5 +50,5 @@ t = float(np.mean(ts)) * 1e-3
 b = H.matvec_bytes()
 sb = H.streamed_bytes()
 print(f"matvec {t*1e6:.1f} us (mean of fastest {len(ts)}), {b/t/1e9:.0f} GB/s algorithmic = "
-      f"{b/t/1e9/bench.peaks()['hbm_gbs']*100:.1f} % of HBM; streamed {sb/1e6:.1f} MB = {sb/t/1e9:.0f} GB/s")
+      f"{b/t/1e9/bench.peaks()[0]*100:.1f} % of HBM; streamed {sb/1e6:.1f} MB = {sb/t/1e9:.0f} GB/s")
 print("plan", plan.info())
