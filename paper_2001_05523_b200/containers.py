@@ -47,6 +47,13 @@ class AssemblyContext:
     def vertex_tris(self):
         return self.mesh.vertex_triangles()
 
+    @property
+    def curls(self):
+        """Per-panel surface curls of the P1 hats (kernels.triangle_curls)."""
+        if getattr(self, "_curls", None) is None:
+            self._curls = kernels.triangle_curls(self.mesh)
+        return self._curls
+
     def host_panel_quad(self, q):
         """Host panel points (GCA Green columns); reference: panel_quad(q)."""
         if q not in self._host_pq:
@@ -87,13 +94,15 @@ def _blocks_to_device(ctx, kind, blocks, q, q_singular, require_disjoint, out, t
                              ci.astype(np.int32), table, out)
     elif kind == kernels.DLP:
         kernels.run_dlp_jobs(ctx.dmesh, q, kernels.build_dlp_jobs(ctx.mesh, blocks), table, out)
+    elif kind == kernels.HYP:
+        kernels.run_hyp_blocks(ctx.dmesh, q, blocks, table, out)
     else:
         raise ValueError(f"unknown operator kind {kind!r}")
 
 
 def dense_block(ctx, kind, row_dofs, col_dofs, q, require_disjoint=False, q_singular=None):
     """Dense Galerkin block over original dof lists (containers.py:48-66)."""
-    if kind not in (kernels.SLP, kernels.DLP):
+    if kind not in (kernels.SLP, kernels.DLP, kernels.HYP):
         raise ValueError(f"unknown operator kind {kind!r}")
     rows = np.asarray(row_dofs, dtype=np.int64)
     cols = np.asarray(col_dofs, dtype=np.int64)
@@ -106,7 +115,7 @@ def dense_block(ctx, kind, row_dofs, col_dofs, q, require_disjoint=False, q_sing
 
 def assemble_dense(ctx, kind, q, cap=ORACLE_CAP, q_singular=None):
     mesh = ctx.mesh
-    nr = mesh.n_triangles
+    nr = mesh.n_vertices if kind == kernels.HYP else mesh.n_triangles
     nc = mesh.n_triangles if kind == kernels.SLP else mesh.n_vertices
     if max(nr, nc) > cap:
         raise ValueError(f"dense oracle dimension {max(nr, nc)} exceeds cap {cap}")

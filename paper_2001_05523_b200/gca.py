@@ -174,6 +174,27 @@ def p1_potentials(ctx, verts, Z, kind, q, z_normals=None, pq=None):
     return out
 
 
+def curl_potentials(ctx, verts, Z, kind, q, z_normals=None, pq=None):
+    """Surface-curl-weighted hat potentials, one component per direction:
+    out[r, n, d] = int (curl phi_{verts[r]})_d kernel(., Z[n]) (kernels.py:
+    172-196): P0 panel potentials scattered with the per-panel curls."""
+    mesh = ctx.mesh
+    verts = np.asarray(verts, dtype=np.int64)
+    Z = np.atleast_2d(Z)
+    curls = ctx.curls
+    panels = _incident_panels(ctx, verts)
+    vals = panel_potentials(mesh, panels, Z, kind, q, z_normals=z_normals, pq=pq)
+    pos = -np.ones(mesh.n_vertices, dtype=np.int64)
+    pos[verts] = np.arange(len(verts))
+    out = np.zeros((len(verts), len(Z), 3))
+    ri = pos[mesh.triangles[panels]]
+    for l in range(3):
+        keep = np.flatnonzero(ri[:, l] >= 0)
+        if len(keep):
+            np.add.at(out, ri[keep, l], vals[keep, :, None] * curls[panels[keep], l, None, :])
+    return out
+
+
 def green_columns(ctx, flavor, dofs, gq, q_single):
     """L whose rows span the cluster's farfield interaction space: sqrt(w)-scaled
     potentials against the Green kernels, [value | normal derivative] (2k cols)."""
@@ -186,6 +207,12 @@ def green_columns(ctx, flavor, dofs, gq, q_single):
     elif flavor == P1_DLP:
         a = p1_potentials(ctx, dofs, gq.points, kernels.K_DN_X, q_single, pq=pq)
         c = p1_potentials(ctx, dofs, gq.points, kernels.K_DN_X_DN_Z, q_single, z_normals=gq.normals, pq=pq)
+    elif flavor == P1_CURL:
+        # 6k columns: the three curl components of the value and of the
+        # normal-derivative potentials
+        a = curl_potentials(ctx, dofs, gq.points, kernels.K_VALUE, q_single, pq=pq)
+        c = curl_potentials(ctx, dofs, gq.points, kernels.K_DN_Z, q_single, z_normals=gq.normals, pq=pq)
+        return np.hstack([a[:, :, d] * sw for d in range(3)] + [c[:, :, d] * sw for d in range(3)])
     else:
         raise ValueError(f"unknown basis flavor {flavor!r}")
     return np.hstack([a * sw, c * sw])

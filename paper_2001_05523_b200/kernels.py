@@ -78,6 +78,12 @@ class DeviceMesh:
             self._touch = TouchTable(self)
         return self._touch
 
+    def curls(self):
+        """(3F, 3) device copy of triangle_curls (hypersingular blocks)."""
+        if "curls" not in self._pp:
+            self._pp["curls"] = D.dev(np.ascontiguousarray(triangle_curls(self.mesh).reshape(-1, 3)))
+        return self._pp["curls"]
+
 
 class TouchTable:
     """All ordered touching panel pairs (sharing >= 1 vertex, incl. identical),
@@ -637,4 +643,108 @@ def dlp_block(mesh, rows, cols, q, vertex_tris=None, require_disjoint=False, pq=
     table = None if require_disjoint else _table_for(dm, DLP, q, singular)
     out = D.zeros((len(rows) * len(cols),))
     run_dlp_jobs(dm, q, build_dlp_jobs(dm.mesh, [(rows, cols, 0, len(cols))]), table, out)
+    return D.host(out).reshape(len(rows), len(cols))
+
+
+# ---------------------------------------------------------------------------
+# hypersingular operator (surface-curl representation, kernels.py:229-239,
+# 471-511): single-layer panel-pair values of each block's incident panels
+# (k_blocks_slp) contracted with the P1 hat curls (k_hyp_scatter)
+
+def triangle_curls(mesh):
+    """Surface curl n x grad of each P1 hat, constant per panel (kernels.py:
+    229-239): (F, 3, 3), curls[f, l] = (V_{l+1} - V_{l+2}) / (2 area_f)."""
+    c = mesh.vertices[mesh.triangles]
+    out = np.empty_like(c)
+    for l in range(3):
+        out[:, l, :] = c[:, (l + 1) % 3, :] - c[:, (l + 2) % 3, :]
+    return out / (2.0 * mesh.areas)[:, None, None]
+
+
+def _vertex_incidence(mesh, verts, panels):
+    """Per vertex (in order) its incident panels, ascending: counts, position
+    in `panels` (sorted) and 3 * panel + local vertex index."""
+    vptr, vidx = mesh.vertex_triangle_csr()
+    verts = np.asarray(verts, dtype=np.int64)
+    counts = vptr[verts + 1] - vptr[verts]
+    starts = np.repeat(vptr[verts], counts)
+    flat = vidx[starts + (np.arange(int(counts.sum())) - np.repeat(np.cumsum(counts) - counts, counts))]
+    owner = np.repeat(verts, counts)
+    local = np.argmax(mesh.triangles[flat] == owner[:, None], axis=1)
+    return counts, np.searchsorted(panels, flat), 3 * flat + local
+
+
+def hyp_jobs(mesh, blocks):
+    """Host job description of hypersingular blocks (row vertices, column
+    vertices, out_off, ld): the single-layer pair jobs over each block's
+    incident panels and the incidence lists of k_hyp_scatter."""
+    vptr, vidx = mesh.vertex_triangle_csr()
+
+    def incident(v):
+        v = np.asarray(v, dtype=np.int64)
+        if len(v) == 0:
+            return np.zeros(0, dtype=np.int64)
+        return np.unique(np.concatenate([vidx[vptr[a] : vptr[a + 1]] for a in v]))
+
+    jobs, desc, pa_l, pb_l = [], [], [], []
+    rp, rpos, rcl, cp, cpos, ccl = [], [], [], [], [], []
+    v_off = pa_off = pb_off = rbase = cbase = rinc = cinc = 0
+    for rows, cols, off, ld in blocks:
+        pa, pb = incident(rows), incident(cols)
+        rc, rps, rcls = _vertex_incidence(mesh, rows, pa)
+        cc, cps, ccls = _vertex_incidence(mesh, cols, pb)
+        jobs.append((pa_off, len(pa), pb_off, len(pb), v_off, len(pb)))
+        desc.append((len(rows), len(cols), v_off, len(pb), rbase, cbase, off, ld))
+        rp.append(rinc + np.concatenate([[0], np.cumsum(rc)]))
+        cp.append(cinc + np.concatenate([[0], np.cumsum(cc)]))
+        rpos.append(rps)
+        rcl.append(rcls)
+        cpos.append(cps)
+        ccl.append(ccls)
+        pa_l.append(pa)
+        pb_l.append(pb)
+        rinc += int(rc.sum())
+        cinc += int(cc.sum())
+        rbase += len(rows) + 1
+        cbase += len(cols) + 1
+        v_off += len(pa) * len(pb)
+        pa_off += len(pa)
+        pb_off += len(pb)
+    cat = lambda a, dt: np.concatenate(a).astype(dt) if a and sum(len(x) for x in a) else np.zeros(1, dtype=dt)
+    return dict(jobs=np.array(jobs, dtype=np.int64).reshape(-1, 6), desc=np.array(desc, dtype=np.int64).reshape(-1, 8),
+                pa=cat(pa_l, np.int32), pb=cat(pb_l, np.int32), v_total=v_off,
+                r_ptr=cat(rp, np.int32), r_pos=cat(rpos, np.int32), r_cl=cat(rcl, np.int32),
+                c_ptr=cat(cp, np.int32), c_pos=cat(cpos, np.int32), c_cl=cat(ccl, np.int32))
+
+
+def run_hyp_blocks(dmesh, q, blocks, table, out):
+    """Hypersingular blocks into `out` (device float64); table None: touching
+    pairs rejected (ValueError), else taken from the single-layer table."""
+    blocks = list(blocks)
+    if not blocks:
+        return
+    J = hyp_jobs(dmesh.mesh, blocks)
+    vals = D.zeros((max(J["v_total"], 1),))
+    run_slp_jobs(dmesh, q, J["jobs"], J["pa"], J["pb"], table, vals)
+    t = {k: D.dev(J[k], np.int32) for k in ("r_ptr", "r_pos", "r_cl", "c_ptr", "c_pos", "c_cl")}
+    desc = D.dev(J["desc"], np.int64)
+    _lib.check(_lib.lib().h2b_hyp_scatter(len(J["desc"]), desc.data_ptr(), t["r_ptr"].data_ptr(),
+                                          t["r_pos"].data_ptr(), t["r_cl"].data_ptr(), t["c_ptr"].data_ptr(),
+                                          t["c_pos"].data_ptr(), t["c_cl"].data_ptr(), dmesh.curls().data_ptr(),
+                                          vals.data_ptr(), out.data_ptr(), D.stream()))
+
+
+def hyp_block(mesh, rows, cols, q, vertex_tris=None, curls=None, require_disjoint=False, pq=None, singular=None):
+    """Dense hypersingular block, P1 rows x P1 columns (vertex ids), through
+    the surface-curl representation (kernels.py:471-511); ValueError on a
+    touching pair when require_disjoint.  `vertex_tris` / `curls` / `pq` are
+    accepted for signature compatibility (the device mesh holds its own)."""
+    dm = device_mesh(mesh)
+    rows = np.asarray(rows, dtype=np.int64)
+    cols = np.asarray(cols, dtype=np.int64)
+    if len(rows) == 0 or len(cols) == 0:
+        return np.zeros((len(rows), len(cols)))
+    table = None if require_disjoint else _table_for(dm, SLP, q, singular)
+    out = D.zeros((len(rows) * len(cols),))
+    run_hyp_blocks(dm, q, [(rows, cols, 0, len(cols))], table, out)
     return D.host(out).reshape(len(rows), len(cols))

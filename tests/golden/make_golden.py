@@ -126,6 +126,9 @@ def split_nearfield(ctx, kind, bt, q_reg, q_ss):
         rows, cols = rt.dofs(b.row), ct.dofs(b.col)
         if kind == kernels.SLP:
             return kernels.slp_block(ctx.mesh, rows, cols, q_reg, pq=pq, singular=table)
+        if kind == kernels.HYP:
+            return kernels.hyp_block(ctx.mesh, rows, cols, q_reg, ctx.vertex_tris, ctx.curls, pq=pq,
+                                     singular=table)
         return kernels.dlp_block(ctx.mesh, rows, cols, q_reg, ctx.vertex_tris, pq=pq, singular=table)
 
     return pmap(build, bt.near, THREADS)
@@ -275,6 +278,11 @@ def build_world(level, leaf, eta, m, eps, kind):
         bt = BlockTree(t0, t0, eta)
         rb = gca.build_basis(ctx, t0, gca.P0_SLP, m, eps, threads=THREADS)
         cb = rb
+    elif kind == kernels.HYP:
+        t1 = build_cluster_tree(spaces.DofSpace(spaces.P1, mesh).support_boxes(), leaf)
+        bt = BlockTree(t1, t1, eta)
+        rb = gca.build_basis(ctx, t1, gca.P1_CURL, m, eps, threads=THREADS)
+        cb = rb
     else:
         t1 = build_cluster_tree(spaces.DofSpace(spaces.P1, mesh).support_boxes(), leaf)
         bt = BlockTree(t0, t1, eta)
@@ -395,6 +403,30 @@ def gen_h2_dlp4():
     out["far_vals"] = np.concatenate([H.far[i][1].ravel() for i in fsel])
     out["near_sum"] = np.array([float(sum(d.sum() for _, d in H.near))])
     np.savez_compressed(os.path.join(HERE, "h2_dlp4.npz"), **out)
+
+
+def gen_h2_hyp4():
+    """Hypersingular H^2 operator (P1 x P1, curl representation) at sphere
+    level 4, leaf 32, eta 2, m 3, q 3 / 4: bases, samples, one matvec."""
+    mesh, ctx, bt, rb, cb = build_world(4, 32, 2.0, 3, 1e-4, kernels.HYP)
+    log("hyp4 basis")
+    H = split_h2(ctx, kernels.HYP, bt, rb, cb, 3, 4)
+    log("hyp4 h2 assembled")
+    x = np.random.default_rng(11).uniform(-1.0, 1.0, H.shape[1])
+    out = {"x": x, "y": H.matvec(x), "yt": H.rmatvec(x)}
+    out.update(basis_arrays("", rb, bt.row_tree))
+    rng = np.random.default_rng(12)
+    nsel = np.sort(rng.choice(len(H.near), 24, replace=False))
+    fsel = np.sort(rng.choice(len(H.far), 32, replace=False))
+    out["near_sel"], out["far_sel"] = nsel, fsel
+    out["near_vals"] = np.concatenate([H.near[i][1].ravel() for i in nsel])
+    out["far_vals"] = np.concatenate([H.far[i][1].ravel() for i in fsel])
+    out["near_sum"] = np.array([float(sum(d.sum() for _, d in H.near))])
+    # one dense hypersingular block through the kernel-level entry point
+    rows, cols = np.array([0, 3, 17, 100, 511]), np.array([0, 1, 2, 40, 300, 1025])
+    out["hb_rows"], out["hb_cols"] = rows, cols
+    out["hb_q3"] = kernels.hyp_block(mesh, rows, cols, 3, singular=ctx.singular_table(kernels.HYP, 3))
+    np.savez_compressed(os.path.join(HERE, "h2_hyp4.npz"), **out)
 
 
 class _OnDemandTable:
@@ -522,6 +554,7 @@ def main():
         ("pairs", gen_pairs),
         ("h2_cfg0", gen_h2_cfg0),
         ("h2_dlp4", gen_h2_dlp4),
+        ("h2_hyp4", gen_h2_hyp4),
         ("h2_cfg1", gen_h2_cfg1),
         ("h2_cfg3p", gen_h2_cfg3p),
         ("cube", gen_cube),
