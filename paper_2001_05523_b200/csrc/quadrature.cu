@@ -28,6 +28,13 @@
 #define H2B_SLP_UNROLL_OUTER 16
 #endif
 constexpr int kSlpUnroll = H2B_SLP_UNROLL_OUTER;
+#ifndef H2B_DLP_XN_REG
+#define H2B_DLP_XN_REG 0  // x'.n of the row points in registers per pair (needs the row loop unrolled)
+#endif
+#ifndef H2B_DLP_UI
+#define H2B_DLP_UI 3      // unroll of the row-point loop (sphere L8 DLP regular: 52.4 ms at 3, 55.2 ms at 1)
+#endif
+constexpr int kDlpUnroll = H2B_DLP_UI;
 #ifndef H2B_SLP_THREADS
 #define H2B_SLP_THREADS 128  // threads per pair-block CTA (128 x 4 CTAs/SM measured 2 % faster than 256 x 2)
 #endif
@@ -717,8 +724,8 @@ __global__ void __launch_bounds__(256, MINB) k_blocks_dlp(const double* __restri
                                                    double* __restrict__ out, int* __restrict__ flags) {
     extern __shared__ double smem[];
     constexpr int RT = kTile, PT = kDlpMaxPanels;
-    double* rx = smem;                  // [5][Q][RT]
-    double* px = rx + 5 * Q * RT;       // [6][Q][PT]: y', -|y'|^2/2, W, (y'.n) W
+    double* rx = smem;                  // [6][Q][RT]: ci x', ci (-|x'|^2/2), ci, 1/ci
+    double* px = rx + 6 * Q * RT;       // [6][Q][PT]: y', -|y'|^2/2, W, (y'.n) W
     double* pn = px + 6 * Q * PT;       // [3][PT]
     double* scr = pn + 3 * PT;          // [kDlpRowChunk][PT][3]
     int* rv = reinterpret_cast<int*>(scr + kDlpRowChunk * PT * 3);
@@ -745,11 +752,15 @@ __global__ void __launch_bounds__(256, MINB) k_blocks_dlp(const double* __restri
         const int64_t g = (int64_t)pnl * Q + i;
         const double x = P[g] - ox, y = P[FQ + g] - oy, z = P[2 * FQ + g] - oz;
         const int s = i * RT + r;
-        rx[s] = x;
-        rx[Q * RT + s] = y;
-        rx[2 * Q * RT + s] = z;
-        rx[3 * Q * RT + s] = -0.5 * fma(z, z, fma(y, y, x * x));
-        rx[4 * Q * RT + s] = P[3 * FQ + g];
+        // row point scaled by ci = w^(-2/3): rsqrt(-ci g)^3 = w t^3, so the
+        // row weight rides in the seed (no product per point pair)
+        const double ci = 1.0 / cbrt(P[3 * FQ + g] * P[3 * FQ + g]);
+        rx[s] = ci * x;
+        rx[Q * RT + s] = ci * y;
+        rx[2 * Q * RT + s] = ci * z;
+        rx[3 * Q * RT + s] = ci * (-0.5 * fma(z, z, fma(y, y, x * x)));
+        rx[4 * Q * RT + s] = ci;
+        rx[5 * Q * RT + s] = 1.0 / ci;
         if (i == 0) {
             rp[r] = pnl;
             rv[3 * r] = T[3 * pnl];
@@ -807,12 +818,22 @@ __global__ void __launch_bounds__(256, MINB) k_blocks_dlp(const double* __restri
                 }
             } else {
                 const double n0 = pn[b], n1 = pn[PT + b], n2 = pn[2 * PT + b];
+#if H2B_DLP_XN_REG
+                // x'.n per row point (unscaled), once per pair
+                double xn[Q];
+#pragma unroll
+                for (int i = 0; i < Q; ++i) {
+                    const int s = i * RT + a;
+                    xn[i] = rx[5 * Q * RT + s] * fma(rx[2 * Q * RT + s], n2, fma(rx[Q * RT + s], n1, rx[s] * n0));
+                }
+#endif
                 double t0 = 0.0, t1 = 0.0, t2 = 0.0;
 #pragma unroll 1
                 for (int j0 = 0; j0 < Q; j0 += JC) {
-                    double y0[JC], y1[JC], y2[JC], yh[JC], yw[JC], yn[JC];
+                    double y0[JC], y1[JC], y2[JC], yh[JC], yw[JC], yn[JC], K[JC];
 #pragma unroll
                     for (int j = 0; j < JC; ++j) {
+                        K[j] = 0.0;
                         if (j0 + j < Q) {
                             const int s = (j0 + j) * PT + b;
                             y0[j] = px[s];
@@ -823,30 +844,36 @@ __global__ void __launch_bounds__(256, MINB) k_blocks_dlp(const double* __restri
                             yn[j] = px[5 * Q * PT + s];
                         }
                     }
-#pragma unroll(JC < Q ? 1 : Q)
+                    // K_j = sum_i w_i k_ij: g' = ci g (4 FMA), u = rsqrt(-g')^3 = w_i t^3,
+                    // 1/r^3 Newton factor (5/3 + g t^2), (x' - y').n w_j (10 FP64 ops)
+#pragma unroll kDlpUnroll
                     for (int i = 0; i < Q; ++i) {
                         const int s = i * RT + a;
                         const double x0 = rx[s], x1 = rx[Q * RT + s], x2 = rx[2 * Q * RT + s];
-                        const double xh = rx[3 * Q * RT + s], xw = rx[4 * Q * RT + s];
-                        const double xn = fma(x2, n2, fma(x1, n1, x0 * n0));
-                        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+                        const double xh = rx[3 * Q * RT + s], ci = rx[4 * Q * RT + s];
+#if H2B_DLP_XN_REG
+                        const double xni = xn[i];
+#else
+                        const double xni = rx[5 * Q * RT + s] * fma(x2, n2, fma(x1, n1, x0 * n0));
+#endif
 #pragma unroll
                         for (int j = 0; j < JC; ++j) {
                             if (j0 + j < Q) {
-                                const double g = fma(x0, y0[j], fma(x1, y1[j], fma(x2, y2[j], xh + yh[j])));
+                                const double g = fma(x0, y0[j], fma(x1, y1[j], fma(x2, y2[j], fma(ci, yh[j], xh))));
                                 const double t = rsqrt_seed(-g);
                                 const double s2 = t * t;
                                 const double c3 = fma(g, s2, 5.0 / 3.0);
-                                // (x' - y').n w = x'.n w - (y'.n) w
-                                const double k = (fma(xn, yw[j], -yn[j]) * c3) * (s2 * t);
-                                a0 = fma(k, c_lam[3 * (j0 + j)], a0);
-                                a1 = fma(k, c_lam[3 * (j0 + j) + 1], a1);
-                                a2 = fma(k, c_lam[3 * (j0 + j) + 2], a2);
+                                K[j] = fma(fma(xni, yw[j], -yn[j]) * c3, s2 * t, K[j]);
                             }
                         }
-                        t0 = fma(xw, a0, t0);
-                        t1 = fma(xw, a1, t1);
-                        t2 = fma(xw, a2, t2);
+                    }
+#pragma unroll
+                    for (int j = 0; j < JC; ++j) {
+                        if (j0 + j < Q) {
+                            t0 = fma(K[j], c_lam[3 * (j0 + j)], t0);
+                            t1 = fma(K[j], c_lam[3 * (j0 + j) + 1], t1);
+                            t2 = fma(K[j], c_lam[3 * (j0 + j) + 2], t2);
+                        }
                     }
                 }
                 v0 = t0;
@@ -980,7 +1007,7 @@ int launch_slp(const h2b_mesh* m, const double* P, const h2b_jobs* jobs, const h
 template <int Q, int JC = Q, int MINB = 1>
 int launch_dlp(const h2b_mesh* m, const double* P, const h2b_dlp_jobs* jobs, const h2b_touch* t,
                const double* tv, double* out, int* flags, cudaStream_t st) {
-    const size_t sm = (size_t)(5 * Q * kTile + 6 * Q * kDlpMaxPanels + 3 * kDlpMaxPanels +
+    const size_t sm = (size_t)(6 * Q * kTile + 6 * Q * kDlpMaxPanels + 3 * kDlpMaxPanels +
                                kDlpRowChunk * kDlpMaxPanels * 3) * sizeof(double) +
                       (size_t)(4 * kTile + 4 * kDlpMaxPanels) * sizeof(int);
     auto kern = k_blocks_dlp<Q, JC, MINB>;
