@@ -322,7 +322,11 @@ def run_ours(args, cfg):
         shard.S, shard.D = S, Dn
         # the timed assembly above is the rank's sharded assembly; check it is
         assert torch.equal(Dn, assemble_nearfield_sharded(ctx, "slp", view, cfg["q_reg"], cfg["q_ss"], own))
-        op = DD.ShardedMatvec(shard, rank, ws, dist)
+        # H2B_COMM=native: the x all-gather runs inside the C-ABI call
+        # (h2b_plan_set_comm + h2b_matvec_sharded, libh2b's own NCCL
+        # communicator); default: torch.distributed's all_gather_into_tensor
+        comm = DD.NativeComm(rank, ws, local, dist) if os.environ.get("H2B_COMM") == "native" else None
+        op = DD.ShardedMatvec(shard, rank, ws, dist, comm=comm)
         plan = op.plan
         H = None
     else:

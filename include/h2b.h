@@ -421,6 +421,28 @@ int h2b_plan_trace(h2b_plan* plan, unsigned long long* h_out, int64_t cap);
  * bytes per CTA (chosen at plan creation from the CTA's other shared memory;
  * environment H2B_STAGE_KB overrides), dynamic shared memory per CTA. */
 int h2b_plan_info(h2b_plan* plan, int64_t* h_out);
+/* ====================== multi-GPU (row-sharded plans) ==================== */
+
+/* A plan created for one rank of a row sharding (h2b_layout.owned / row_perm,
+ * col_perm = position of every permuted column dof in the gathered x of
+ * nranks equal chunks) plus an NCCL communicator: h2b_matvec_sharded takes
+ * the rank's chunk of x (permuted order), all-gathers it over NCCL on the
+ * call's stream and writes the rank's rows of y.  NCCL is
+ * opened at first use (libnccl.so.2); comm is an ncclComm_t. */
+#define H2B_COMM_ID_BYTES 128
+/* ncclGetUniqueId into h_id (H2B_COMM_ID_BYTES); rank 0 shares it. */
+int h2b_comm_unique_id(void* h_id);
+/* ncclCommInitRank on `device` (collective over the nranks callers). */
+int h2b_comm_init(void** comm, int nranks, const void* h_id, int rank, int device);
+int h2b_comm_destroy(void* comm);
+/* Attach the communicator: this plan is rank `rank` of `nranks`, each rank's
+ * x chunk is `chunk` doubles (gathered buffer nranks x chunk). */
+int h2b_plan_set_comm(h2b_plan* plan, void* comm, int rank, int nranks, int64_t chunk);
+/* y_local = this rank's rows of A x from x_local = this rank's x chunk (both
+ * permuted order, device memory): ncclAllGather + the fused matvec, stream
+ * ordered. */
+int h2b_matvec_sharded(h2b_plan* plan, const double* d_x_local, double* d_y_local, void* stream);
+
 /* Multi-right-hand-side product Y = A X for 1 <= nrhs <= 16 device vectors
  * (X: n_cols x nrhs, Y: n_rows x nrhs, row-major, natural dof order) over the
  * same packed operator as a matvec plan (single-GPU layouts).  The reference

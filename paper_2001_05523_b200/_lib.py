@@ -109,6 +109,7 @@ EXPORTS = (
     "h2b_dlp_jobs_free", "h2b_gca_columns", "h2b_gca_aca", "h2b_cg_workspace_size", "h2b_cg_dot", "h2b_cg_step",
     "h2b_cg_direction", "h2b_matmat_create", "h2b_matmat_destroy", "h2b_matmat", "h2b_pair_integrals",
     "h2b_basis_forward", "h2b_basis_backward", "h2b_transpose_blocks", "h2b_hyp_scatter",
+    "h2b_comm_unique_id", "h2b_comm_init", "h2b_comm_destroy", "h2b_plan_set_comm", "h2b_matvec_sharded",
 )
 
 _lib = None
@@ -168,6 +169,11 @@ def lib():
         L.h2b_basis_backward.argtypes = [ctypes.POINTER(Basis), vp, vp, vp]
         L.h2b_transpose_blocks.argtypes = [ctypes.c_int64, vp, vp, vp, vp]
         L.h2b_hyp_scatter.argtypes = [ctypes.c_int64] + [vp] * 11
+        L.h2b_comm_unique_id.argtypes = [vp]
+        L.h2b_comm_init.argtypes = [ctypes.POINTER(vp), ctypes.c_int, vp, ctypes.c_int, ctypes.c_int]
+        L.h2b_comm_destroy.argtypes = [vp]
+        L.h2b_plan_set_comm.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int64]
+        L.h2b_matvec_sharded.argtypes = [vp, vp, vp, vp]
         L.h2b_gca_aca.argtypes = [ctypes.POINTER(GcaBatch), ctypes.c_double, vp, vp, vp, vp, ctypes.c_int32, vp, vp]
         _lib = L
     return _lib

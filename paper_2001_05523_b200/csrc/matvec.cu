@@ -53,6 +53,7 @@
 #include <vector>
 
 #include "device_common.cuh"
+#include "nccl_api.h"
 
 namespace h2b {
 namespace {
@@ -125,6 +126,11 @@ struct h2b_plan {
     cudaEvent_t done = nullptr;
     cudaStream_t last = nullptr;
     bool launched = false;
+    // row sharding over NCCL (h2b_plan_set_comm)
+    void* comm = nullptr;
+    int comm_rank = 0, comm_size = 1;
+    int64_t comm_chunk = 0;
+    double* xgath = nullptr;  // comm_size x comm_chunk gathered x
 };
 
 namespace h2b {
@@ -2045,7 +2051,7 @@ extern "C" int h2b_debug_stuck(h2b_plan* p, unsigned long long* out) {
 extern "C" int h2b_plan_destroy(h2b_plan* p) {
     if (!p) return ok();
     void* bufs[] = {p->xhat, p->ycpl, p->yfin, p->ynear, p->ctrl, p->rec,  p->fwd_off, p->dx,
-                    p->dy,   p->trace, p->xll, p->dsym,  p->gsym, p->ppart, p->nsum};
+                    p->dy,   p->trace, p->xll, p->dsym,  p->gsym, p->ppart, p->nsum, p->xgath};
     for (void* q : bufs)
         if (q) cudaFree(q);
     if (p->hy) cudaFreeHost(p->hy);
@@ -2138,6 +2144,39 @@ extern "C" int h2b_matvec_host(h2b_plan* p, const double* h_x, double* h_y, void
     H2B_CUDA_TRY(cudaStreamSynchronize(st));
     if (staged_y) std::memcpy(h_y, p->hy, sizeof(double) * p->L.n_rows);
     return ok();
+}
+
+extern "C" int h2b_plan_set_comm(h2b_plan* p, void* comm, int rank, int nranks, int64_t chunk) {
+    if (!p || !comm || nranks < 1 || rank < 0 || rank >= nranks || chunk < 1)
+        return fail(H2B_ERR_INVALID, "h2b_plan_set_comm: bad argument");
+    if ((int64_t)nranks * chunk < p->L.n_cols)
+        return fail(H2B_ERR_INVALID, "h2b_plan_set_comm: gathered x shorter than the plan's columns");
+    if (!nccl_api()) return fail(H2B_ERR_INVALID, "h2b_plan_set_comm: libnccl.so.2 not found");
+    std::lock_guard<std::mutex> g(p->mu);
+    if (p->xgath) {
+        cudaFree(p->xgath);
+        p->xgath = nullptr;
+    }
+    H2B_CUDA_TRY(cudaSetDevice(p->device));
+    H2B_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&p->xgath), sizeof(double) * nranks * chunk));
+    p->comm = comm;
+    p->comm_rank = rank;
+    p->comm_size = nranks;
+    p->comm_chunk = chunk;
+    return ok();
+}
+
+extern "C" int h2b_matvec_sharded(h2b_plan* p, const double* d_x_local, double* d_y_local, void* stream) {
+    if (!p || !d_x_local || !d_y_local) return fail(H2B_ERR_INVALID, "h2b_matvec_sharded: null pointer");
+    if (!p->comm) return fail(H2B_ERR_INVALID, "h2b_matvec_sharded: no communicator (h2b_plan_set_comm)");
+    std::lock_guard<std::mutex> g(p->mu);
+    cudaStream_t st = as_stream(stream);
+    const NcclApi* api = nccl_api();
+    if (p->launched && p->last != st) H2B_CUDA_TRY(cudaStreamWaitEvent(st, p->done, 0));
+    const ncclResult_t r = api->all_gather(d_x_local, p->xgath, (size_t)p->comm_chunk, ncclFloat64,
+                                           static_cast<ncclComm_t>(p->comm), st);
+    if (r != ncclSuccess) return nccl_fail(api, r, "ncclAllGather");
+    return launch_matvec(p, p->xgath, nullptr, d_y_local, st);
 }
 
 // Diagnostics: the per-CTA timeline of the last matvec when the plan was

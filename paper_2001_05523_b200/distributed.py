@@ -29,6 +29,8 @@ one-sided plans are bitwise identical.
 CG on row-sharded vectors: solver.cg(..., allreduce=allreduce_sum(dist)).
 """
 
+import ctypes
+
 import numpy as np
 
 from . import _lib
@@ -192,6 +194,31 @@ class LocalMatvec:
         return y
 
 
+class NativeComm:
+    """An NCCL communicator owned by libh2b (h2b_comm_init): a sharded plan
+    with it attached runs its x all-gather inside h2b_matvec_sharded, so the
+    whole sharded matvec is one C-ABI call.  Rank 0 draws the unique id;
+    `dist` (torch.distributed, any backend) broadcasts it when world > 1."""
+
+    def __init__(self, rank, world, device=0, dist=None):
+        L = _lib.lib()
+        uid = (ctypes.c_char * 128)()
+        if rank == 0:
+            _lib.check(L.h2b_comm_unique_id(uid))
+        if world > 1:
+            box = [bytes(uid)]
+            dist.broadcast_object_list(box, src=0)
+            ctypes.memmove(uid, box[0], 128)
+        self.handle = ctypes.c_void_p()
+        _lib.check(L.h2b_comm_init(ctypes.byref(self.handle), world, uid, rank, device))
+        self.rank, self.world = rank, world
+
+    def close(self):
+        if self.handle:
+            _lib.check(_lib.lib().h2b_comm_destroy(self.handle))
+            self.handle = ctypes.c_void_p()
+
+
 class ShardedMatvec:
     """Row-sharded matvec of one rank.  apply_local(x_loc, y_loc) takes this
     rank's permuted slice of x and returns its permuted rows of y (the CG
@@ -201,7 +228,7 @@ class ShardedMatvec:
     Built either from a RowShard (sharded assembly: the rank holds only its
     share of the operator) or, for tests, from a full single-GPU H2Matrix."""
 
-    def __init__(self, src, rank, world, dist):
+    def __init__(self, src, rank, world, dist, comm=None):
         import torch
 
         if isinstance(src, RowShard):
@@ -231,6 +258,9 @@ class ShardedMatvec:
         self.xloc = torch.zeros(self.chunk, dtype=torch.float64, device="cuda")
         self.yloc = torch.zeros(max(self.hi - self.lo, 1), dtype=torch.float64, device="cuda")
         self.perm_dev = torch.from_numpy(rt.perm[self.lo : self.hi].copy()).cuda()
+        self.comm = comm
+        if comm is not None:
+            _lib.check(_lib.lib().h2b_plan_set_comm(self.plan.handle, comm.handle, rank, world, self.chunk))
 
     def info(self):
         return self.plan.info()
@@ -241,18 +271,24 @@ class ShardedMatvec:
         if y_local_perm is None:
             y_local_perm = self.yloc[:n].clone()
         self.xloc[:n].copy_(x_local_perm)
-        self.dist.all_gather_into_tensor(self.xbuf, self.xloc)
-        _lib.check(_lib.lib().h2b_matvec(self.plan.handle, self.xbuf.data_ptr(), y_local_perm.data_ptr(),
-                                         _lib.stream_ptr()))
+        self._gather_apply(y_local_perm)
         return y_local_perm
+
+    def _gather_apply(self, y):
+        if self.comm is not None:
+            # all-gather (NCCL) + fused matvec in one C-ABI call
+            _lib.check(_lib.lib().h2b_matvec_sharded(self.plan.handle, self.xloc.data_ptr(), y.data_ptr(),
+                                                     _lib.stream_ptr()))
+        else:
+            self.dist.all_gather_into_tensor(self.xbuf, self.xloc)
+            _lib.check(_lib.lib().h2b_matvec(self.plan.handle, self.xbuf.data_ptr(), y.data_ptr(),
+                                             _lib.stream_ptr()))
 
     def apply(self, x, y):
         """Full natural-order x -> this rank's rows written into y[perm]."""
         n = self.hi - self.lo
         self.xloc[:n].copy_(x[self.perm_dev])
-        self.dist.all_gather_into_tensor(self.xbuf, self.xloc)
-        _lib.check(_lib.lib().h2b_matvec(self.plan.handle, self.xbuf.data_ptr(), self.yloc.data_ptr(),
-                                         _lib.stream_ptr()))
+        self._gather_apply(self.yloc)
         y[self.perm_dev] = self.yloc[:n]
         return y
 

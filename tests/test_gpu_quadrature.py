@@ -93,7 +93,9 @@ def test_require_disjoint_raises(ctx4):
     with pytest.raises(ValueError, match="touching"):
         dense_block(ctx4, "slp", [0, 1], [0, 5], 3, require_disjoint=True)
     with pytest.raises(ValueError):
-        dense_block(ctx4, "hyp", [0], [1], 3)
+        dense_block(ctx4, "xyz", [0], [1], 3)  # unknown kind (hyp is supported: tests/test_hyp.py)
+    with pytest.raises(ValueError, match="touching"):
+        dense_block(ctx4, "hyp", [0], [258], 3, require_disjoint=True)  # two vertices of panel 0
 
 
 @pytest.fixture(scope="module")

@@ -245,3 +245,27 @@ def test_distributed_cg_two_ranks():
     assert conv
     assert abs(it_sh - it_one) <= 1, (it_sh, it_one)
     assert dx < 1e-7
+
+
+def test_native_comm_single_rank(slp5):
+    """h2b_plan_set_comm + h2b_matvec_sharded (the NCCL all-gather inside the
+    C-ABI call) with one rank: the rank's rows equal the
+    single-GPU matvec.  (Two NCCL ranks cannot share one GPU; the multi-rank
+    host logic is covered by the gloo tests.)"""
+    import torch
+
+    from paper_2001_05523_b200 import distributed as DD
+
+    ctx, bt, rb, cb, H = slp5
+    comm = DD.NativeComm(0, 1, torch.cuda.current_device())
+    try:
+        op = DD.ShardedMatvec(H, 0, 1, None, comm=comm)
+        x = torch.randn(H.shape[1], dtype=torch.float64, device="cuda")
+        y = torch.zeros_like(x)
+        op.apply(x, y)
+        ref = H.matvec(x)
+        assert rel(y.cpu().numpy(), ref.cpu().numpy()) < 1e-13
+        yl = op.apply_local(x[op.perm_dev])
+        assert torch.equal(yl, y[op.perm_dev])
+    finally:
+        comm.close()

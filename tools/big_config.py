@@ -49,7 +49,7 @@ pk = bench.peaks()
 print(json.dumps({
     "config": cfg["desc"], "n": n, "setup_s": round(t_setup, 1),
     "matvec_ms": t * 1e3, "dofs_per_s": n / t, "matvec_bytes": mv_bytes, "achieved_gbs": mv_bytes / t / 1e9,
-    "hbm_frac": mv_bytes / t / 1e9 / pk["hbm_gbs"],
+    "hbm_frac": mv_bytes / t / 1e9 / pk[0],
     "nearfield_ms": (t_sing + t_reg) * 1e3, "pairs_per_s": fc["pairs"] / (t_sing + t_reg),
     "singular_ms": t_sing * 1e3, "regular_ms": t_reg * 1e3, "evaluated_regular": fc["regular_evaluated"],
     "nearfield_tflops": (fc["reg_flops"] + fc["sing_flops"]) / (t_sing + t_reg) / 1e12,

@@ -49,6 +49,6 @@ print(json.dumps({
     "operator": f"DLP sphere L{level}: {nr} P0 rows x {nc} P1 columns, m=4 eta=2 leaf=64, q 3/5",
     "setup_s": round(t_setup, 1), "assembly_s": round(t_asm, 3),
     "matvec_ms": t * 1e3, "row_dofs_per_s": nr / t, "matvec_bytes": mv_bytes,
-    "achieved_gbs": mv_bytes / t / 1e9, "hbm_frac": mv_bytes / t / 1e9 / pk["hbm_gbs"],
+    "achieved_gbs": mv_bytes / t / 1e9, "hbm_frac": mv_bytes / t / 1e9 / pk[0],
     "bitwise_repeat": bool(torch.equal(y1, y2)), "linearity_rel": float(lin.norm() / y1.norm()),
 }))

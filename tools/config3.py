@@ -98,7 +98,7 @@ y2 = plan.apply_device(x).clone()
 lin = plan.apply_device(0.7 * x - 1.3 * z) - (0.7 * plan.apply_device(x) - 1.3 * plan.apply_device(z))
 sym = float(torch.dot(z, plan.apply_device(x)) - torch.dot(x, plan.apply_device(z)))
 out["matvec"] = {"ms": t * 1e3, "dofs_per_s": n / t, "bytes": mv_bytes, "achieved_gbs": mv_bytes / t / 1e9,
-                 "hbm_frac": mv_bytes / t / 1e9 / pk["hbm_gbs"], "bitwise_repeat": bool(torch.equal(y1, y2)),
+                 "hbm_frac": mv_bytes / t / 1e9 / pk[0], "bitwise_repeat": bool(torch.equal(y1, y2)),
                  "linearity_rel": float(lin.norm() / y1.norm()),
                  "symmetry_rel": abs(sym) / float(torch.dot(z, y1).abs())}
 

@@ -1,6 +1,4 @@
-# scratch GPU script (session r02j): DLP kernel variants at sphere L8
+# scratch GPU script (session r02l): one test
 set -x
-mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -x -k "dlp or DLP" > gpurun_out/r02j_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r02j_pytest.log
-NF_LEVEL=8 timeout 1500 python tools/nf_variants.py dold dnew dui3 dj9 > gpurun_out/r02j_nfv.txt 2>&1
-tail -3 gpurun_out/r02j_pytest.log; cat gpurun_out/r02j_nfv.txt
+timeout 600 python -m pytest tests/test_gpu_quadrature.py -m gpu -q -k require_disjoint > gpurun_out/r02l2_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r02l2_pytest.log
+tail -3 gpurun_out/r02l2_pytest.log
