@@ -87,6 +87,17 @@ typedef struct {
 int h2b_block_tree(const h2b_tree* row, const h2b_tree* col, double eta, int64_t* h_far,
                    int64_t far_cap, int64_t* h_near, int64_t near_cap, int64_t* h_n_far,
                    int64_t* h_n_near);
+/* The same two builders on the device, same arguments and
+ * outputs (host arrays), bit-exact with the host builders: the cluster tree
+ * level by level (block reductions for boxes and midpoints, one scan for the
+ * stable split), the block tree one recursion level at a time with the
+ * depth-first order restored from subtree counts. */
+int h2b_cluster_tree_device(const double* h_boxes, int64_t n, int64_t r_leaf, int64_t* h_perm,
+                            int64_t* h_n_nodes, int64_t* h_start, int64_t* h_end, int64_t* h_depth,
+                            int64_t* h_left, int64_t* h_right, double* h_node_boxes);
+int h2b_block_tree_device(const h2b_tree* row, const h2b_tree* col, double eta, int64_t* h_far,
+                          int64_t far_cap, int64_t* h_near, int64_t near_cap, int64_t* h_n_far,
+                          int64_t* h_n_near);
 
 /* ======================= Galerkin quadrature (device) ====================== */
 

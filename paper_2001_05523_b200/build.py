@@ -22,7 +22,7 @@ LIB = os.path.join(OUT_DIR, "libh2b.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = ["errors.cpp", "structure.cpp", "dlp_jobs.cpp", "comm.cpp", "quadrature.cu", "matvec.cu", "gca.cu", "solver.cu",
-           "matmat.cu", "basis.cu"]
+           "matmat.cu", "basis.cu", "tree_dev.cu"]
 HEADERS = ["h2b_internal.h", "device_common.cuh", "nccl_api.h"]
 
 

@@ -113,8 +113,10 @@ class ClusterTree:
                          _lib.ptr(self._ct_keep[2]))
 
 
-def build_cluster_tree(boxes, r_leaf):
-    """Geometric bisection of support boxes (clustering.py:78-121)."""
+def build_cluster_tree(boxes, r_leaf, device=False):
+    """Geometric bisection of support boxes (clustering.py:78-121).
+    device=True builds it on the GPU (h2b_cluster_tree_device, bit-exact with
+    the host builder)."""
     boxes = np.ascontiguousarray(boxes, dtype=np.float64)
     n = len(boxes)
     if n == 0:
@@ -126,9 +128,10 @@ def build_cluster_tree(boxes, r_leaf):
     nn = np.zeros(1, dtype=np.int64)
     start, end, depth, left, right = (np.empty(cap, dtype=np.int64) for _ in range(5))
     nb = np.empty((cap, 2, 3))
-    rc = _lib.lib().h2b_cluster_tree(_lib.ptr(boxes), n, int(r_leaf), _lib.ptr(perm), _lib.ptr(nn),
-                                    _lib.ptr(start), _lib.ptr(end), _lib.ptr(depth), _lib.ptr(left),
-                                    _lib.ptr(right), _lib.ptr(nb))
+    L = _lib.lib()
+    fn = L.h2b_cluster_tree_device if device else L.h2b_cluster_tree
+    rc = fn(_lib.ptr(boxes), n, int(r_leaf), _lib.ptr(perm), _lib.ptr(nn), _lib.ptr(start), _lib.ptr(end),
+            _lib.ptr(depth), _lib.ptr(left), _lib.ptr(right), _lib.ptr(nb))
     _lib.check(rc)
     m = int(nn[0])
     return ClusterTree(perm, start[:m].copy(), end[:m].copy(), depth[:m].copy(), left[:m].copy(),
@@ -153,7 +156,9 @@ class BlockTree:
     `near_uids` are the (n, 2) [row uid, col uid] arrays; `.far` / `.near` the
     reference's Block lists (built lazily)."""
 
-    def __init__(self, row_tree, col_tree, eta):
+    def __init__(self, row_tree, col_tree, eta, device=False):
+        """device=True runs the recursion on the GPU (h2b_block_tree_device,
+        same lists in the same order)."""
         if eta <= 0.0:
             raise ValueError("eta must be positive")
         self.row_tree = row_tree
@@ -167,8 +172,9 @@ class BlockTree:
         while True:
             far = np.empty((cap, 2), dtype=np.int64)
             near = np.empty((cap, 2), dtype=np.int64)
-            rc = L.h2b_block_tree(ctypes.byref(rt), ctypes.byref(ct), float(eta), _lib.ptr(far), cap,
-                                  _lib.ptr(near), cap, _lib.ptr(nf), _lib.ptr(nn))
+            fn = L.h2b_block_tree_device if device else L.h2b_block_tree
+            rc = fn(ctypes.byref(rt), ctypes.byref(ct), float(eta), _lib.ptr(far), cap, _lib.ptr(near), cap,
+                    _lib.ptr(nf), _lib.ptr(nn))
             if rc == _lib.H2B_ERR_CAPACITY:
                 cap = int(max(nf[0], nn[0])) + 1
                 continue
