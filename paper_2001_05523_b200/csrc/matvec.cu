@@ -269,7 +269,10 @@ __device__ __forceinline__ void mark(unsigned long long* m, int i) {
 constexpr int kRowBlock = H2B_ROWBLOCK;  // rows per warp in rows_dot's many-rows mode
 // widest right-hand side gathered at once (multiple of 128: see task_band);
 // wider band rows are processed in chunks of it
-constexpr int kChunkCols = 768;
+#ifndef H2B_CHUNK_COLS
+#define H2B_CHUNK_COLS 768
+#endif
+constexpr int kChunkCols = H2B_CHUNK_COLS;
 
 __host__ __device__ constexpr int log2c(int n) { return n <= 1 ? 0 : 1 + log2c(n / 2); }
 

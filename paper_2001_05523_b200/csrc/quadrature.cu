@@ -359,11 +359,15 @@ __global__ void __launch_bounds__(128) k_singular(const double* __restrict__ V, 
             double* d = srule + e * kRuleStride;
             if (KIND == H2B_SLP && kase != H2B_DISJOINT) {
                 // sums and differences of the two charts' coordinates: both
-                // orientations of a symmetrised pair share the sum terms
-                d[0] = p[0] + p[2];
-                d[1] = p[1] + p[3];
-                d[2] = p[0] - p[2];
-                d[3] = p[1] - p[3];
+                // orientations of a symmetrised pair share the sum terms.
+                // Scaled by 1/w: the distance vectors come out divided by the
+                // weight, so the rsqrt seed of r^2/w^2 is already w t (the
+                // weight costs no product per evaluation; w > 0)
+                const double iw = 1.0 / w;
+                d[0] = (p[0] + p[2]) * iw;
+                d[1] = (p[1] + p[3]) * iw;
+                d[2] = (p[0] - p[2]) * iw;
+                d[3] = (p[1] - p[3]) * iw;
                 d[4] = w;
             } else {
                 d[0] = p[0];
@@ -414,11 +418,11 @@ __global__ void __launch_bounds__(128) k_singular(const double* __restrict__ V, 
                 for (int e = 0; e < cn; ++e) {
                     const double* d = srule + e * kRuleStride;
                     const double du = d[2], dv = d[3];  // u1 - u2, v1 - v2
-                    const double r2 = fma(du, fma(du, g11, dv * g12), (dv * dv) * g22);
+                    const double r2 = fma(du, fma(du, g11, dv * g12), (dv * dv) * g22);  // r^2 / w^2
                     const double t = rsqrt_seed(r2);
                     const double s = t * t;
                     const double c = fma(-r2, s, 3.0);
-                    acc0 = fma(d[4] * t, c, acc0);
+                    acc0 = fma(t, c, acc0);
                 }
             } else {
                 // shared vertex first in both charts, so base = 0 and
@@ -437,7 +441,7 @@ __global__ void __launch_bounds__(128) k_singular(const double* __restrict__ V, 
 #pragma unroll 2
                 for (int e = 0; e < cn; ++e) {
                     const double* d = srule + e * kRuleStride;
-                    const double su = d[0], sv = d[1], mu = d[2], mv = d[3], w = d[4];
+                    const double su = d[0], sv = d[1], mu = d[2], mv = d[3];  // scaled by 1/w
                     double dp[3], dm[3];
 #pragma unroll
                     for (int k = 0; k < 3; ++k) {
@@ -450,13 +454,13 @@ __global__ void __launch_bounds__(128) k_singular(const double* __restrict__ V, 
                     double t = rsqrt_seed(r2);
                     double sq = t * t;
                     double cc = fma(-r2, sq, 3.0);
-                    acc0 = fma(w * t, cc, acc0);
+                    acc0 = fma(t, cc, acc0);
                     // orientation-swapped rule (kernels.py:303-309)
                     r2 = fma(dm[2], dm[2], fma(dm[1], dm[1], dm[0] * dm[0]));
                     t = rsqrt_seed(r2);
                     sq = t * t;
                     cc = fma(-r2, sq, 3.0);
-                    acc1 = fma(w * t, cc, acc1);
+                    acc1 = fma(t, cc, acc1);
                 }
             }
         } else {

@@ -13,7 +13,7 @@ while [ $# -ge 2 ]; do
   name=$1; flags=$2; shift 2
   $NVCC -c ${SRC:-paper_2001_05523_b200/csrc/matvec.cu} -o $OUT/$name.o -O3 -std=c++17 -Xcompiler -fPIC -I include \
     $ARCH -lineinfo --expt-relaxed-constexpr $flags
-  $NVCC -shared -o $OUT/$name.so $OBJ/errors.cpp.o $OBJ/structure.cpp.o $OBJ/dlp_jobs.cpp.o $OBJ/quadrature.cu.o $OBJ/gca.cu.o $OBJ/solver.cu.o $OBJ/matmat.cu.o $OBJ/basis.cu.o $OBJ/comm.cpp.o $OUT/$name.o $ARCH \
+  $NVCC -shared -o $OUT/$name.so $(ls $OBJ/*.o | grep -v matvec.cu.o) $OUT/$name.o $ARCH \
     -lcudart_static -lrt -ldl -lpthread
   echo "built $OUT/$name.so ($flags)"
 done

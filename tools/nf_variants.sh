@@ -12,7 +12,7 @@ while [ $# -ge 2 ]; do
   name=$1; flags=$2; shift 2
   $NVCC -c ${QSRC:-paper_2001_05523_b200/csrc/quadrature.cu} -o $OUT/$name.q.o -O3 -std=c++17 -Xcompiler -fPIC -I include \
     $ARCH -lineinfo --expt-relaxed-constexpr -Xptxas -v $flags 2>&1 | grep -A2 "k_blocks_slpILi9" | grep -E "spill|Used" | tr '\n' ' '; echo
-  $NVCC -shared -o $OUT/$name.so $OBJ/errors.cpp.o $OBJ/structure.cpp.o $OBJ/dlp_jobs.cpp.o $OUT/$name.q.o $OBJ/matvec.cu.o $OBJ/gca.cu.o $OBJ/solver.cu.o $OBJ/matmat.cu.o $OBJ/basis.cu.o $OBJ/comm.cpp.o $ARCH \
+  $NVCC -shared -o $OUT/$name.so $(ls $OBJ/*.o | grep -v quadrature.cu.o) $OUT/$name.q.o $ARCH \
     -lcudart_static -lrt -ldl -lpthread
   echo "built $OUT/$name.so ($flags)"
 done
