@@ -290,8 +290,11 @@ def run_ours(args, cfg):
         table.compute(own)
         sj.run(table, Dn)
     nf_reps = 3 if n > 1_000_000 else 10
+    nf_clocks = Clocks(local)  # clocks during the FP64-bound quadrature alone
     t_sing = ev_time(torch, lambda: table.compute(own), nf_reps)
     t_reg = ev_time(torch, lambda: sj.run(table, Dn), nf_reps)
+    t_reg_each = [ev_time(torch, lambda: sj.run(table, Dn), 1) for _ in range(nf_reps)]
+    nf_clk = nf_clocks.stop()
     touch = dm.touch()
     if own is not None:
         touch.subset(own, half=True)
@@ -515,7 +518,9 @@ def run_ours(args, cfg):
                          "frac": fc["sing_flops"] / t_sing / 1e12 / fp64_peak if fp64_peak else None},
             "regular": {"ms": tmax["reg"] * 1e3, "pairs_integrated": fc["regular_evaluated"],
                         "tflops": fc["reg_flops"] / t_reg / 1e12,
-                        "frac": fc["reg_flops"] / t_reg / 1e12 / fp64_peak if fp64_peak else None},
+                        "frac": fc["reg_flops"] / t_reg / 1e12 / fp64_peak if fp64_peak else None,
+                        "ms_each_launch": [round(t * 1e3, 3) for t in t_reg_each]},
+            "clocks": nf_clk,
             "roofline": {"bound": "fp64", "achieved": sums["flops"] / nf_time / 1e12, "peak": fp64_peak,
                          "unit": "TFLOP/s", "frac": sums["flops"] / nf_time / 1e12 / fp64_peak if fp64_peak else None,
                          "peak_source": fp64_src,

@@ -1,5 +1,5 @@
 set -x
-timeout 900 python -m pytest tests -m gpu -q -x -k "singular or quadrature or nearfield or cfg or hyp or touch" > gpurun_out/r02u_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r02u_pytest.log
-timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/r02u_bench.json 2> gpurun_out/r02u_bench.err
-tail -n 3 gpurun_out/r02u_pytest.log
-python -c "import json;d=json.load(open('gpurun_out/r02u_bench.json'));nf=d['nearfield'];print(d['ms_per_step'], nf['singular'], nf['regular']['ms'], nf['roofline']['frac'])"
+timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/r02w_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r02w_pytest.log
+tail -n 3 gpurun_out/r02w_pytest.log
+for c in 1 2s 3; do for m in 0 0.2 0.4; do echo "== $c mix $m"; H2B_FWD_MIX=$m timeout 400 python tools/mv_time.py $c 2>&1 | grep -E "^matvec"; done; done > gpurun_out/r02w_mv.txt 2>&1
+grep -E "^== |^matvec" gpurun_out/r02w_mv.txt

@@ -29,7 +29,8 @@ for k in range(5):
     flush.fill_(float(k))
     y = plan.apply_device(x)
 torch.cuda.synchronize()
-n = 8 * 200000
+info = plan.info()
+n = 8 * (info['near_tasks'] + info['coupling_tasks'] + len(tree.leaf_uids()) + 64)
 buf = np.zeros(n, dtype=np.uint64)
 _lib.check(_lib.lib().h2b_plan_trace(plan.handle, buf.ctypes.data, n))
 total = None
