@@ -597,7 +597,34 @@ def cpu_baseline(H, cfg, x, mesh, budget_s=15.0):
            "sample": f"{k} full oracle matvec(s) of the same {n}-DoF operator exported from the device "
                      f"({dt:.1f} s; export {t_export:.1f} s; OPENBLAS_NUM_THREADS=1)"}
     out["nearfield_sample"] = oracle_near_sample(mesh, bt, cfg, budget_s=max(5.0, budget_s / 2))
+    out["coupling_sample"] = oracle_coupling_sample(mesh, bt, b, cfg, budget_s=max(3.0, budget_s / 4))
     return out
+
+
+def oracle_coupling_sample(mesh, bt, basis, cfg, budget_s=4.0, seed=11):
+    """Seeded sample of coupling blocks S_b = G[pivots_t, pivots_s]
+    (gca.py:194-205) through the oracle's regular tensor rule (require_disjoint:
+    no singular table); pairs/s on one thread."""
+    from oracle import quad as OQ
+
+    V, T, N, A = mesh.vertices, mesh.triangles, mesh.normals, mesh.areas
+    rng = np.random.default_rng(seed)
+    order = rng.permutation(len(bt.far_uids))
+    pairs = blocks = 0
+    t0 = time.perf_counter()
+    for i in order:
+        if time.perf_counter() - t0 > budget_s:
+            break
+        t, s_ = bt.far_uids[i]
+        rows = np.asarray(basis.pivots[int(t)], dtype=np.int64)
+        cols = np.asarray(basis.pivots[int(s_)], dtype=np.int64)
+        OQ.slp_block(V, T, N, A, rows, cols, cfg["q_reg"], None)
+        pairs += len(rows) * len(cols)
+        blocks += 1
+    dt = time.perf_counter() - t0
+    return {"pairs_per_s": pairs / dt if dt else None, "pairs": pairs, "blocks": blocks, "cores": 1,
+            "sample": f"{blocks} seeded random far blocks of {len(bt.far_uids)} (oracle tensor rule, q "
+                      f"{cfg['q_reg']}, pivots of the bench's basis)"}
 
 
 def oracle_near_sample(mesh, bt, cfg, budget_s=8.0, seed=7):
@@ -701,6 +728,31 @@ def _ref_near(args):
     return _near_sample(V, T, N, A, st["tree"], st["near"], st["cfg"], budget, seed=100 + i0)
 
 
+def _ref_cpl(args):
+    """Worker: seeded far blocks through the oracle tensor rule, pivot sets
+    drawn from each cluster's dofs with the reference basis's ranks."""
+    from oracle import quad as OQ
+
+    i0, budget = args
+    st = _REF
+    V, T, N, A = st["mesh"]
+    tree, far, rank = st["tree"], st["far"], st["rank"]
+    rng = np.random.default_rng(200 + i0)
+    pairs = blocks = 0
+    t0 = time.perf_counter()
+    for i in rng.permutation(len(far)):
+        if time.perf_counter() - t0 > budget:
+            break
+        piv = []
+        for u in far[i]:
+            dofs = tree.perm[tree.start[u] : tree.end[u]]
+            piv.append(rng.choice(dofs, size=min(int(rank[u]), len(dofs)), replace=False))
+        OQ.slp_block(V, T, N, A, piv[0], piv[1], st["cfg"]["q_reg"], None)
+        pairs += len(piv[0]) * len(piv[1])
+        blocks += 1
+    return {"pairs": pairs, "blocks": blocks, "s": time.perf_counter() - t0}
+
+
 def run_reference(args, cfg):
     """The reference's CPU algorithm (oracle port) on this host's cores, same
     configuration: each step = the reference matvec restricted to one row
@@ -744,6 +796,7 @@ def run_reference(args, cfg):
             walls.append(time.perf_counter() - t1)
             rows_total = sum(r for r, _ in res)
         near_res = pool.map(_ref_near, [(i, 6.0) for i in range(len(roots))], chunksize=1)
+        cpl_res = pool.map(_ref_cpl, [(i, 3.0) for i in range(len(roots))], chunksize=1)
     dt = float(np.sum(walls))
     val = rows_total * K / dt
     npairs = sum(r["pairs"] for r in near_res)
@@ -764,6 +817,10 @@ def run_reference(args, cfg):
                                    f"reference), ranks from the reference's basis ({cfg['golden']}), operator "
                                    f"values seeded random (the CPU cost does not depend on them)"},
         "e2e": {"value": val, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "couplings": {"pairs_per_s": sum(r["pairs"] for r in cpl_res) / max(r["s"] for r in cpl_res),
+                      "pairs": int(sum(r["pairs"] for r in cpl_res)), "cores": len(roots),
+                      "sample": "seeded random far blocks through the oracle tensor rule (pivot sets of the "
+                                "reference basis's ranks), one process per core"},
         "nearfield": {"pairs_per_s": npairs / nwall if nwall else None, "pairs": int(npairs), "cores": len(roots),
                       "sample": "seeded random near blocks through the oracle quadrature (Sauter-Schwab for the "
                                 "sampled touching pairs, tensor rule otherwise), one process per core"},
