@@ -329,7 +329,11 @@ def run_ours(args, cfg):
         # (h2b_plan_set_comm + h2b_matvec_sharded, libh2b's own NCCL
         # communicator); default: torch.distributed's all_gather_into_tensor
         comm = DD.NativeComm(rank, ws, local, dist) if os.environ.get("H2B_COMM") == "native" else None
-        op = DD.ShardedMatvec(shard, rank, ws, dist, comm=comm)
+        # the x_hat exchange (SURVEY 8(e) better variant: each rank
+        # forward-transforms only its own column subtrees, coefficients
+        # all-gathered) unless H2B_XHAT=0
+        xhat = os.environ.get("H2B_XHAT", "1") != "0" and comm is None
+        op = DD.ShardedMatvec(shard, rank, ws, dist, comm=comm, xhat=xhat)
         plan = op.plan
         H = None
     else:
@@ -368,7 +372,11 @@ def run_ours(args, cfg):
     for k in range(K):
         flush.fill_(float(k))
         kst[k].record()
-        _lib.check(_lib.lib().h2b_matvec(plan.handle, xin.data_ptr(), yout.data_ptr(), _lib.stream_ptr()))
+        if shard is not None and op.xhat:  # the bands launch (+ x_hat import) of the x_hat exchange
+            _lib.check(_lib.lib().h2b_xhat_main(plan.handle, xin.data_ptr(), op.xrecv.data_ptr(), yout.data_ptr(),
+                                                _lib.stream_ptr()))
+        else:
+            _lib.check(_lib.lib().h2b_matvec(plan.handle, xin.data_ptr(), yout.data_ptr(), _lib.stream_ptr()))
         ken[k].record()
     torch.cuda.synchronize()
     kern_s = float(np.mean([s.elapsed_time(e) / 1e3 for s, e in zip(kst, ken)]))
@@ -496,8 +504,9 @@ def run_ours(args, cfg):
                          "between timed steps",
                    "basis": "device GCA (k_gca_columns + k_gca_aca)" if device_basis else
                             "host GCA (reference-identical pivots)",
-                   "parallelism": f"row-shard x{ws} (sharded assembly + storage, NCCL all-gather of x)"
-                                  if ws > 1 else "single GPU",
+                   "parallelism": (f"row-shard x{ws} (sharded assembly + storage, NCCL all-gather of x"
+                                   + (" and of the ranks' own x_hat: forward transform split over the ranks)"
+                                      if ws > 1 and op.xhat else ")")) if ws > 1 else "single GPU",
                    "env": h2b_env()},
         "gpu_launches": K,
         "roofline": {"bound": "hbm", "kernel": "k_matvec (fused forward + coupling + backward + nearfield)",

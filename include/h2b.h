@@ -454,6 +454,24 @@ int h2b_plan_set_comm(h2b_plan* plan, void* comm, int rank, int nranks, int64_t 
  * ordered. */
 int h2b_matvec_sharded(h2b_plan* plan, const double* d_x_local, double* d_y_local, void* stream);
 
+/* x_hat exchange (SURVEY 8(e) "better variant"): a row-sharded plan whose
+ * forward tasks cover only this rank's column clusters (h_cmask[u] = 1 for the
+ * clusters inside the rank's permuted range, int8 per column node).
+ * h2b_xhat_forward runs them (x: the gathered x of h2b_matvec_sharded) and
+ * packs their coefficients into d_send (send_len doubles, clusters in uid
+ * order); after an all-gather of every rank's send buffer, h2b_xhat_main
+ * imports the coefficients (h_src[u] = offset of cluster u in the gathered
+ * buffer, -1 for clusters spanning several ranks, set once by
+ * h2b_xhat_set_import), climbs the spanning clusters with the forward
+ * climb's arithmetic and runs the bands: the rank's rows of y, the bits of
+ * the plan without the exchange.  h2b_xhat_info: n_own, send_len, forward
+ * tasks, imported clusters, spanning clusters. */
+int h2b_plan_create_xhat(const h2b_layout* layout, const int8_t* h_cmask, h2b_plan** plan);
+int h2b_xhat_info(h2b_plan* plan, int64_t* h_out);
+int h2b_xhat_set_import(h2b_plan* plan, const int64_t* h_src);
+int h2b_xhat_forward(h2b_plan* plan, const double* d_x, double* d_send, void* stream);
+int h2b_xhat_main(h2b_plan* plan, const double* d_x, const double* d_recv, double* d_y, void* stream);
+
 /* Multi-right-hand-side product Y = A X for 1 <= nrhs <= 16 device vectors
  * (X: n_cols x nrhs, Y: n_rows x nrhs, row-major, natural dof order) over the
  * same packed operator as a matvec plan (single-GPU layouts).  The reference

@@ -111,6 +111,7 @@ EXPORTS = (
     "h2b_basis_forward", "h2b_basis_backward", "h2b_transpose_blocks", "h2b_hyp_scatter",
     "h2b_comm_unique_id", "h2b_comm_init", "h2b_comm_destroy", "h2b_plan_set_comm", "h2b_matvec_sharded",
     "h2b_cluster_tree_device", "h2b_block_tree_device",
+    "h2b_plan_create_xhat", "h2b_xhat_info", "h2b_xhat_set_import", "h2b_xhat_forward", "h2b_xhat_main",
 )
 
 _lib = None
@@ -134,6 +135,11 @@ def lib():
         L.h2b_block_tree.argtypes = [ctypes.POINTER(Tree), ctypes.POINTER(Tree), ctypes.c_double, vp,
                                      ctypes.c_int64, vp, ctypes.c_int64, vp, vp]
         L.h2b_cluster_tree_device.argtypes = L.h2b_cluster_tree.argtypes
+        L.h2b_plan_create_xhat.argtypes = [ctypes.POINTER(Layout), vp, ctypes.POINTER(vp)]
+        L.h2b_xhat_info.argtypes = [vp, vp]
+        L.h2b_xhat_set_import.argtypes = [vp, vp]
+        L.h2b_xhat_forward.argtypes = [vp, vp, vp, vp]
+        L.h2b_xhat_main.argtypes = [vp, vp, vp, vp, vp]
         L.h2b_block_tree_device.argtypes = L.h2b_block_tree.argtypes
         L.h2b_panel_points.argtypes = [ctypes.POINTER(Mesh), vp, vp, ctypes.c_int32, vp, vp]
         L.h2b_touch_count.argtypes = [ctypes.POINTER(Mesh), vp, vp, vp]

@@ -782,7 +782,7 @@ def _gather_index(n_nodes, row_len, rows, width, coloff, first):
 class MatvecPlan:
     """Device layout + libh2b plan for y = A x."""
 
-    def __init__(self, bt, rb, cb, S, Dn, fl, nl, owned=None, col_perm=None, row_perm=None):
+    def __init__(self, bt, rb, cb, S, Dn, fl, nl, owned=None, col_perm=None, row_perm=None, xhat_mask=None):
         t = D.require_cuda()
         rt, ct = bt.row_tree, bt.col_tree
         self.n_rows, self.n_cols = rt.n_dofs, ct.n_dofs
@@ -859,7 +859,13 @@ class MatvecPlan:
         self._S, self._D = S, Dn
         self.layout = lay
         h = ctypes.c_void_p()
-        _lib.check(_lib.lib().h2b_plan_create(ctypes.byref(lay), ctypes.byref(h)))
+        if xhat_mask is None:
+            _lib.check(_lib.lib().h2b_plan_create(ctypes.byref(lay), ctypes.byref(h)))
+        else:
+            # x_hat exchange (distributed.ShardedMatvec(xhat=True)): forward
+            # tasks over this rank's column clusters only
+            self._xmask = np.ascontiguousarray(xhat_mask, dtype=np.int8)
+            _lib.check(_lib.lib().h2b_plan_create_xhat(ctypes.byref(lay), _lib.ptr(self._xmask), ctypes.byref(h)))
         self.handle = h
         self._torch = t
         self._host_fn = _lib.lib().h2b_matvec_host

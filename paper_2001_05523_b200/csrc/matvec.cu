@@ -126,6 +126,25 @@ struct h2b_plan {
     cudaEvent_t done = nullptr;
     cudaStream_t last = nullptr;
     bool launched = false;
+    // x_hat exchange (h2b_plan_create_xhat): the forward tasks cover only this
+    // rank's column clusters (own launch, own LL buffer xhat_f); their
+    // coefficients leave through h2b_xhat_forward, everybody's come back in
+    // through h2b_xhat_main, which climbs the clusters spanning several ranks
+    // and launches the bands with no forward task
+    int n_fwd = 0;              // forward tasks per launch
+    bool xmode = false;
+    uint64_t* xhat_f = nullptr;
+    int32_t* d_own = nullptr;   // owned clusters (send order) and their send offsets
+    int64_t* d_own_off = nullptr;
+    int n_own = 0;
+    int64_t send_len = 0;
+    int32_t* d_imp = nullptr;   // gathered clusters and their offsets in the gathered buffer
+    int64_t* d_imp_src = nullptr;
+    int n_imp = 0;
+    int32_t* d_span = nullptr;  // spanning clusters, deepest level first
+    std::vector<int64_t> span_level_off;
+    double* span_val = nullptr; // plain coefficients (x_hat offsets) for the spanning climbs
+    unsigned long long n_f_launches = 0, n_m_launches = 0;
     // row sharding over NCCL (h2b_plan_set_comm)
     void* comm = nullptr;
     int comm_rank = 0, comm_size = 1;
@@ -1197,6 +1216,7 @@ struct KArgs {
     const int64_t* fwd_off;
     int64_t band_base, band_bytes, dgidx_bytes;
     int n_near, n_cpl, n_near_a, n_inner_bands;
+    int n_fwd;         // forward tasks of this launch (tickets [0, n_fwd))
     int max_cols, vec_len, stage_bytes;
     int64_t e_bytes_r;
     uint64_t *xhat, *ycpl, *yfin, *ynear;
@@ -1244,7 +1264,7 @@ __device__ __forceinline__ void run_task(const KArgs& a, const double* __restric
         }
         return;
     }
-    if (ticket >= L.c_leaves + a.n_near + a.n_cpl) {
+    if (ticket >= a.n_fwd + a.n_near + a.n_cpl) {
         // host-output launch: once every leaf has written its rows of y (in
         // HBM, natural order), copy a chunk to the mapped host buffer with
         // coalesced stores (scattered 8-byte stores over the host link cost
@@ -1259,7 +1279,7 @@ __device__ __forceinline__ void run_task(const KArgs& a, const double* __restric
             }
         }
         __syncthreads();
-        const int64_t c = ticket - (L.c_leaves + a.n_near + a.n_cpl), n = L.n_rows;
+        const int64_t c = ticket - (a.n_fwd + a.n_near + a.n_cpl), n = L.n_rows;
         const int64_t i0 = c * kCopyChunk, i1 = min(n, i0 + kCopyChunk);
         constexpr int kU = kCopyChunk / kThreads;
         double v[kU];
@@ -1278,15 +1298,15 @@ __device__ __forceinline__ void run_task(const KArgs& a, const double* __restric
     unsigned long long t_begin = 0;
     if (a.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
     s.mark = a.trace ? a.trace + 8 * ticket + 3 : nullptr;
-    const int tB = L.c_leaves;
+    const int tB = a.n_fwd;
 
     if (ticket < tB) {
         // pull the band records, the nearfield gather lists and x into L2 for
         // the streaming tasks that follow (fire-and-forget; LL needs no fences)
-        prefetch_slice(reinterpret_cast<const double*>(a.rec + a.band_base), a.band_bytes, ticket, L.c_leaves);
+        prefetch_slice(reinterpret_cast<const double*>(a.rec + a.band_base), a.band_bytes, ticket, a.n_fwd);
         prefetch_slice(reinterpret_cast<const double*>(a.dsym ? a.gsym : L.d_gidx), a.dgidx_bytes, ticket,
-                       L.c_leaves);
-        if (!a.xh) prefetch_slice(x, 8 * L.n_cols, ticket, L.c_leaves);
+                       a.n_fwd);
+        if (!a.xh) prefetch_slice(x, 8 * L.n_cols, ticket, a.n_fwd);
         task_forward(L.c_V, L.c_E, L.col_perm, a.rec + __ldg(a.fwd_off + ticket), x, a.xhat, epoch, s);
     } else {
         const int b = ticket - tB;
@@ -1318,7 +1338,7 @@ __device__ __forceinline__ void run_task(const KArgs& a, const double* __restric
             asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
             a.trace[8 * ticket] = t_begin;
             a.trace[8 * ticket + 1] = t_end;
-            const int kd = ticket < L.c_leaves ? 2 : (int)s.rec[7];
+            const int kd = ticket < tB ? 2 : (int)s.rec[7];
             a.trace[8 * ticket + 2] = smid | ((unsigned long long)kd << 16) |
                                       (kd == 2 ? (unsigned long long)s.rec[5] << 24 : 0ull) |
                                       (kd == 1 && s.rec[5] ? (1ull << 41) | ((unsigned long long)s.rec[17] << 32) : 0ull);
@@ -1366,6 +1386,85 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
     const uint32_t epoch = s_epoch;
     s.xll = a.xh ? a.xll : nullptr;
     run_task(a, x, y, ticket, epoch, s);
+}
+
+// ---- x_hat exchange (row-sharded plans, SURVEY 8(e) "better variant") ------
+// pack: this rank's coefficients (LL, forward launch) -> plain send buffer;
+// one warp per cluster
+__global__ void k_xhat_pack(h2b_layout L, const uint64_t* __restrict__ xhat_f, uint32_t epoch,
+                            const int32_t* __restrict__ own, const int64_t* __restrict__ own_off, int n,
+                            double* __restrict__ send) {
+    const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+    if (w >= n) return;
+    const int u = own[w];
+    const int k = L.c_rank[u];
+    const int64_t xo = L.c_xhat_off[u], so = own_off[w];
+    for (int c = lane; c < k; c += 32) send[so + c] = ll_load(xhat_f + 2 * (xo + c), epoch);
+}
+
+// import: gathered coefficients -> LL x_hat of the next bands launch (and a
+// plain copy for the spanning climbs)
+__global__ void k_xhat_import(h2b_layout L, const double* __restrict__ recv, const int32_t* __restrict__ imp,
+                              const int64_t* __restrict__ src, int n, uint64_t* __restrict__ xhat, uint32_t epoch,
+                              double* __restrict__ plain) {
+    const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+    if (w >= n) return;
+    const int u = imp[w];
+    const int k = L.c_rank[u];
+    const int64_t xo = L.c_xhat_off[u], so = src[w];
+    for (int c = lane; c < k; c += 32) {
+        const double v = recv[so + c];
+        plain[xo + c] = v;
+        ll_store(xhat + 2 * (xo + c), v, epoch);
+    }
+}
+
+// a cluster spanning several ranks: x_hat_p = E_c0^T x_hat_c0 + E_c1^T x_hat_c1
+// with exactly the arithmetic of the forward climb in task_forward /
+// forward_warp (same branch on rank and staging size), so the coefficients
+// are the bits one GPU computes.  One 128-thread CTA per cluster.
+__global__ void __launch_bounds__(kThreads) k_xhat_climb(h2b_layout L, const int32_t* __restrict__ nodes, int stage_bytes,
+                                                       int vec_len, double* __restrict__ plain,
+                                                       uint64_t* __restrict__ xhat, uint32_t epoch) {
+    extern __shared__ __align__(16) double sm[];
+    double* buf = sm;                                  // stage_bytes: [E_c0; E_c1]
+    double* va = sm + stage_bytes / 8;                 // 2 vec_len
+    double* vb = va + 2 * vec_len;                     // vec_len
+    double* rhs = vb + vec_len;                        // vec_len
+    double* red = rhs + vec_len;                       // kWarps * 64
+    const int p = nodes[blockIdx.x];
+    const int c0 = L.c_child[2 * p], c1 = L.c_child[2 * p + 1];
+    const int k0 = L.c_rank[c0], k1 = L.c_rank[c1], kp = L.c_rank[p];
+    const int n0 = k0 * kp, n1 = k1 * kp;
+    const bool in_smem = (n0 + n1) * 8 <= stage_bytes;
+    const double* E0 = L.c_E + L.c_e_off[c0];
+    const double* E1 = L.c_E + L.c_e_off[c1];
+    if (in_smem) {
+        for (int i = threadIdx.x; i < n0; i += kThreads) buf[i] = E0[i];
+        for (int i = threadIdx.x; i < n1; i += kThreads) buf[n0 + i] = E1[i];
+    }
+    for (int r = threadIdx.x; r < k0; r += kThreads) va[r] = plain[L.c_xhat_off[c0] + r];
+    for (int r = threadIdx.x; r < k1; r += kThreads) va[k0 + r] = plain[L.c_xhat_off[c1] + r];
+    __syncthreads();
+    if (in_smem && kp <= 32) {
+        if (threadIdx.x < kp) vb[threadIdx.x] = climb_coef(buf, buf + n0, k0, k1, kp, va, threadIdx.x);
+        __syncthreads();
+    } else if (in_smem) {
+        small_cols_dot(buf, k0 + k1, kp, va, vb, red);
+        __syncthreads();
+    } else {
+        cols_dot(E0, k0, kp, va, red, vb);
+        for (int c = threadIdx.x; c < kp; c += kThreads) rhs[c] = vb[c];
+        __syncthreads();
+        cols_dot(E1, k1, kp, va + k0, red, vb);
+        for (int c = threadIdx.x; c < kp; c += kThreads) vb[c] += rhs[c];
+        __syncthreads();
+    }
+    const int64_t xo = L.c_xhat_off[p];
+    for (int c = threadIdx.x; c < kp; c += kThreads) {
+        plain[xo + c] = vb[c];
+        ll_store(xhat + 2 * (xo + c), vb[c], epoch);
+    }
 }
 
 __global__ void k_diagonal(h2b_layout L, double* __restrict__ diag) {
@@ -1652,7 +1751,7 @@ int build_sym_near(int stage_bytes, const h2b_layout& L, const std::vector<int32
 
 namespace {
 constexpr int kSymNear = 1;
-int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
+int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags, const int8_t* cmask = nullptr) {
     if (!layout || !out) return fail(H2B_ERR_INVALID, "h2b_plan_create: null pointer");
     const h2b_layout& L = *layout;
     if (L.c_nodes <= 0 || L.r_nodes <= 0 || L.c_leaves <= 0) return fail(H2B_ERR_INVALID, "h2b_plan_create: empty tree");
@@ -1728,7 +1827,7 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
     const int smem = stage + other_smem(sym.on);
     if (smem > 227 * 1024) return fail(H2B_ERR_INVALID, "h2b_plan_create: gathered right-hand side exceeds shared memory");
 
-    std::vector<int64_t> rec, fwd_off(L.c_leaves);
+    std::vector<int64_t> rec, fwd_off;
     // Skip the zero work at the top of the trees: x_hat_u is needed only if u
     // or an ancestor is the column cluster of a far block; v_t is non-zero only
     // if t or an ancestor has couplings (for the reference geometries the top
@@ -1759,7 +1858,8 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
     // A: forward records (leaf, then the levels it climbs as the right child)
     for (int i = 0; i < L.c_leaves; ++i) {
         const int leaf = leaves[i];
-        fwd_off[i] = (int64_t)rec.size();
+        if (cmask && !cmask[leaf]) continue;  // x_hat exchange: this rank's column leaves only
+        fwd_off.push_back((int64_t)rec.size());
         rec.insert(rec.end(), {cstart[leaf], csize[leaf], crank[leaf], cvoff[leaf], cxoff[leaf], 0, 0});
         const size_t hdr = rec.size() - kFwdHead;
         bool warp_ok = crank[leaf] <= 32 && csize[leaf] <= 64 &&
@@ -1767,7 +1867,7 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
         int node = leaf, n = 0;
         while (true) {
             const int p = cparent[node];
-            if (p < 0 || cchild[2 * p + 1] != node || !need_c[p]) break;
+            if (p < 0 || cchild[2 * p + 1] != node || !(cmask ? cmask[p] != 0 : need_c[p] != 0)) break;
             const int c0 = cchild[2 * p];
             if (n >= kMaxDepth) return fail(H2B_ERR_INVALID, "h2b_plan_create: tree deeper than 32 levels");
             rec.insert(rec.end(), {crank[c0], crank[p], ceoff[c0], ceoff[node], cxoff[c0], cxoff[p]});
@@ -1924,13 +2024,40 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
     H2B_CUDA_TRY(cudaMemset(p->xhat, 0, 16 * (size_t)L.xhat_len));
     H2B_CUDA_TRY(cudaMemset(p->ycpl, 0, 16 * (size_t)L.yhat_len));
     H2B_CUDA_TRY(cudaMemset(p->ynear, 0, 16 * (size_t)L.n_rows));
-    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->ctrl), 3 * sizeof(unsigned long long)));
-    H2B_CUDA_TRY(cudaMemset(p->ctrl, 0, 3 * sizeof(unsigned long long)));
+    // ticket counters: [0] device-input, [1] host-input launches, [2] leaf steps
+    // done (host output), [3] forward launches of the x_hat exchange
+    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->ctrl), 4 * sizeof(unsigned long long)));
+    H2B_CUDA_TRY(cudaMemset(p->ctrl, 0, 4 * sizeof(unsigned long long)));
     H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->rec), sizeof(int64_t) * std::max<size_t>(1, rec.size())));
-    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->fwd_off), sizeof(int64_t) * fwd_off.size()));
+    H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->fwd_off), sizeof(int64_t) * std::max<size_t>(1, fwd_off.size())));
     if (!rec.empty())
         H2B_CUDA_TRY(cudaMemcpy(p->rec, rec.data(), sizeof(int64_t) * rec.size(), cudaMemcpyHostToDevice));
-    H2B_CUDA_TRY(cudaMemcpy(p->fwd_off, fwd_off.data(), sizeof(int64_t) * fwd_off.size(), cudaMemcpyHostToDevice));
+    if (!fwd_off.empty())
+        H2B_CUDA_TRY(cudaMemcpy(p->fwd_off, fwd_off.data(), sizeof(int64_t) * fwd_off.size(), cudaMemcpyHostToDevice));
+    p->n_fwd = (int)fwd_off.size();
+    if (cmask) {
+        p->xmode = true;
+        H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->xhat_f), 16 * (size_t)L.xhat_len));
+        H2B_CUDA_TRY(cudaMemset(p->xhat_f, 0, 16 * (size_t)L.xhat_len));
+        H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->span_val), 8 * (size_t)L.xhat_len));
+        std::vector<int32_t> own;
+        std::vector<int64_t> own_off;
+        int64_t o = 0;
+        for (int u = 0; u < L.c_nodes; ++u)
+            if (cmask[u]) {
+                own.push_back(u);
+                own_off.push_back(o);
+                o += crank[u];
+            }
+        p->n_own = (int)own.size();
+        p->send_len = o;
+        H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->d_own), 4 * std::max<size_t>(1, own.size())));
+        H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->d_own_off), 8 * std::max<size_t>(1, own.size())));
+        if (!own.empty()) {
+            H2B_CUDA_TRY(cudaMemcpy(p->d_own, own.data(), 4 * own.size(), cudaMemcpyHostToDevice));
+            H2B_CUDA_TRY(cudaMemcpy(p->d_own_off, own_off.data(), 8 * own.size(), cudaMemcpyHostToDevice));
+        }
+    }
     {
         // the attribute belongs to the kernel, not the plan: only ever raise it
         // (a later plan with less shared memory must not break an earlier one)
@@ -1944,7 +2071,7 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags) {
     p->trace = nullptr;
     if (const char* tr = getenv("H2B_TRACE")) {
         if (tr[0] == '1') {
-            const size_t n = (size_t)(L.c_leaves + n_near + n_cpl) * 8;
+            const size_t n = (size_t)(fwd_off.size() + n_near + n_cpl) * 8;
             H2B_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&p->trace), n * sizeof(unsigned long long)));
             H2B_CUDA_TRY(cudaMemset(p->trace, 0, n * sizeof(unsigned long long)));
         }
@@ -2054,7 +2181,8 @@ extern "C" int h2b_debug_stuck(h2b_plan* p, unsigned long long* out) {
 extern "C" int h2b_plan_destroy(h2b_plan* p) {
     if (!p) return ok();
     void* bufs[] = {p->xhat, p->ycpl, p->yfin, p->ynear, p->ctrl, p->rec,  p->fwd_off, p->dx,
-                    p->dy,   p->trace, p->xll, p->dsym,  p->gsym, p->ppart, p->nsum, p->xgath};
+                    p->dy,   p->trace, p->xll, p->dsym,  p->gsym, p->ppart, p->nsum, p->xgath,
+                    p->xhat_f, p->d_own, p->d_own_off, p->d_imp, p->d_imp_src, p->d_span, p->span_val};
     for (void* q : bufs)
         if (q) cudaFree(q);
     if (p->hy) cudaFreeHost(p->hy);
@@ -2065,8 +2193,10 @@ extern "C" int h2b_plan_destroy(h2b_plan* p) {
 }
 
 namespace {
+// mode 0: the plan's full task list; 1: forward tasks only (x_hat exchange,
+// into xhat_f); 2: bands only (x_hat imported)
 int launch_matvec(h2b_plan* p, const double* d_x, const double* xh, double* y, cudaStream_t st,
-                  double* yh = nullptr) {
+                  double* yh = nullptr, int mode = 0) {
     // (caller holds p->mu) order after the plan's previous launch if that was
     // on another stream
     if (p->launched && p->last != st) H2B_CUDA_TRY(cudaStreamWaitEvent(st, p->done, 0));
@@ -2100,7 +2230,15 @@ int launch_matvec(h2b_plan* p, const double* d_x, const double* xh, double* y, c
     a.n_out = yh ? (int)((p->L.n_rows + kCopyChunk - 1) / kCopyChunk) : 0;
     a.n_leaf = p->n_leaf;
     a.ydone = p->ctrl + 2;
-    const int grid = a.n_copy + p->L.c_leaves + p->n_near + p->n_cpl + a.n_out;
+    a.n_fwd = p->n_fwd;
+    if (mode == 1) {
+        a.n_near = a.n_cpl = 0;
+        a.xhat = p->xhat_f;
+        a.ctrl = p->ctrl + 3;
+    } else if (mode == 2) {
+        a.n_fwd = 0;
+    }
+    const int grid = a.n_copy + a.n_fwd + a.n_near + a.n_cpl + a.n_out;
     k_matvec<<<grid, kThreads, p->smem, st>>>(a, d_x, y);
     H2B_CUDA_TRY(cudaGetLastError());
     H2B_CUDA_TRY(cudaEventRecord(p->done, st));
@@ -2122,6 +2260,7 @@ const void* mapped(const void* h) {
 
 extern "C" int h2b_matvec(h2b_plan* p, const double* d_x, double* d_y, void* stream) {
     if (!p || !d_x || !d_y) return fail(H2B_ERR_INVALID, "h2b_matvec: null pointer");
+    if (p->xmode) return fail(H2B_ERR_INVALID, "h2b_matvec: x_hat-exchange plan (use h2b_xhat_forward / h2b_xhat_main)");
     std::lock_guard<std::mutex> g(p->mu);
     return launch_matvec(p, d_x, nullptr, d_y, as_stream(stream));
 }
@@ -2132,6 +2271,7 @@ extern "C" int h2b_matvec(h2b_plan* p, const double* d_x, double* d_y, void* str
 // transfers.  Pageable buffers go through the plan's pinned staging.
 extern "C" int h2b_matvec_host(h2b_plan* p, const double* h_x, double* h_y, void* stream) {
     if (!p || !h_x || !h_y) return fail(H2B_ERR_INVALID, "h2b_matvec_host: null pointer");
+    if (p->xmode) return fail(H2B_ERR_INVALID, "h2b_matvec_host: x_hat-exchange plan");
     std::lock_guard<std::mutex> g(p->mu);
     cudaStream_t st = as_stream(stream);
     const double* xh = static_cast<const double*>(mapped(h_x));
@@ -2182,6 +2322,112 @@ extern "C" int h2b_matvec_sharded(h2b_plan* p, const double* d_x_local, double* 
     return launch_matvec(p, p->xgath, nullptr, d_y_local, st);
 }
 
+extern "C" int h2b_plan_create_xhat(const h2b_layout* layout, const int8_t* h_cmask, h2b_plan** out) {
+    if (!h_cmask) return fail(H2B_ERR_INVALID, "h2b_plan_create_xhat: null mask");
+    return plan_create(layout, out, kSymNear, h_cmask);
+}
+
+extern "C" int h2b_xhat_info(h2b_plan* p, int64_t* h_out) {
+    if (!p || !h_out) return fail(H2B_ERR_INVALID, "h2b_xhat_info: null pointer");
+    h_out[0] = p->n_own;
+    h_out[1] = p->send_len;
+    h_out[2] = p->n_fwd;
+    h_out[3] = p->n_imp;
+    h_out[4] = p->span_level_off.empty() ? 0 : p->span_level_off.back();
+    return ok();
+}
+
+extern "C" int h2b_xhat_set_import(h2b_plan* p, const int64_t* h_src) {
+    if (!p || !h_src) return fail(H2B_ERR_INVALID, "h2b_xhat_set_import: null pointer");
+    if (!p->xmode) return fail(H2B_ERR_INVALID, "h2b_xhat_set_import: plan not created for the x_hat exchange");
+    std::lock_guard<std::mutex> g(p->mu);
+    const h2b_layout& L = p->L;
+    std::vector<int32_t> cparent, cchild;
+    H2B_CUDA_TRY(fetch(L.c_parent, L.c_nodes, cparent));
+    H2B_CUDA_TRY(fetch(L.c_child, 2 * (int64_t)L.c_nodes, cchild));
+    std::vector<int32_t> imp, span;
+    std::vector<int64_t> src;
+    std::vector<int> depth(L.c_nodes, 0);
+    for (int u = 0; u < L.c_nodes; ++u) {
+        for (int q = cparent[u]; q >= 0; q = cparent[q]) ++depth[u];
+        if (h_src[u] >= 0) {
+            imp.push_back(u);
+            src.push_back(h_src[u]);
+        } else {
+            if (cchild[2 * u] < 0) return fail(H2B_ERR_INVALID, "h2b_xhat_set_import: a leaf without coefficients");
+            span.push_back(u);
+        }
+    }
+    // spanning clusters deepest level first (children before parents)
+    std::stable_sort(span.begin(), span.end(), [&](int a, int b) { return depth[a] > depth[b]; });
+    p->span_level_off.assign(1, 0);
+    for (size_t i = 0; i < span.size(); ++i)
+        if (i + 1 == span.size() || depth[span[i + 1]] != depth[span[i]]) p->span_level_off.push_back((int64_t)i + 1);
+    for (void* q : {(void*)p->d_imp, (void*)p->d_imp_src, (void*)p->d_span})
+        if (q) cudaFree(q);
+    H2B_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&p->d_imp), 4 * std::max<size_t>(1, imp.size())));
+    H2B_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&p->d_imp_src), 8 * std::max<size_t>(1, imp.size())));
+    H2B_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&p->d_span), 4 * std::max<size_t>(1, span.size())));
+    if (!imp.empty()) {
+        H2B_CUDA_TRY(cudaMemcpy(p->d_imp, imp.data(), 4 * imp.size(), cudaMemcpyHostToDevice));
+        H2B_CUDA_TRY(cudaMemcpy(p->d_imp_src, src.data(), 8 * src.size(), cudaMemcpyHostToDevice));
+    }
+    if (!span.empty()) H2B_CUDA_TRY(cudaMemcpy(p->d_span, span.data(), 4 * span.size(), cudaMemcpyHostToDevice));
+    p->n_imp = (int)imp.size();
+    return ok();
+}
+
+extern "C" int h2b_xhat_forward(h2b_plan* p, const double* d_x, double* d_send, void* stream) {
+    if (!p || !d_x || !d_send) return fail(H2B_ERR_INVALID, "h2b_xhat_forward: null pointer");
+    if (!p->xmode) return fail(H2B_ERR_INVALID, "h2b_xhat_forward: plan not created for the x_hat exchange");
+    std::lock_guard<std::mutex> g(p->mu);
+    cudaStream_t st = as_stream(stream);
+    const uint32_t epoch = 2u * (uint32_t)p->n_f_launches + 1u;
+    if (p->n_fwd > 0) {
+        if (int rc = launch_matvec(p, d_x, nullptr, nullptr, st, nullptr, 1)) return rc;
+    }
+    ++p->n_f_launches;
+    if (p->n_own > 0) {
+        k_xhat_pack<<<(unsigned)((32 * (int64_t)p->n_own + 255) / 256), 256, 0, st>>>(
+            p->L, p->xhat_f, epoch, p->d_own, p->d_own_off, p->n_own, d_send);
+        H2B_CUDA_TRY(cudaGetLastError());
+    }
+    return ok();
+}
+
+extern "C" int h2b_xhat_main(h2b_plan* p, const double* d_x, const double* d_recv, double* d_y, void* stream) {
+    if (!p || !d_x || !d_recv || !d_y) return fail(H2B_ERR_INVALID, "h2b_xhat_main: null pointer");
+    if (!p->xmode || p->span_level_off.empty())
+        return fail(H2B_ERR_INVALID, "h2b_xhat_main: x_hat exchange not set up (h2b_xhat_set_import)");
+    std::lock_guard<std::mutex> g(p->mu);
+    cudaStream_t st = as_stream(stream);
+    if (p->launched && p->last != st) H2B_CUDA_TRY(cudaStreamWaitEvent(st, p->done, 0));
+    const uint32_t epoch = 2u * (uint32_t)p->n_m_launches + 1u;  // the bands launch below
+    if (p->n_imp > 0) {
+        k_xhat_import<<<(unsigned)((32 * (int64_t)p->n_imp + 255) / 256), 256, 0, st>>>(
+            p->L, d_recv, p->d_imp, p->d_imp_src, p->n_imp, p->xhat, epoch, p->span_val);
+        H2B_CUDA_TRY(cudaGetLastError());
+    }
+    const int smem = p->stage_bytes + 8 * (4 * p->vec_len + kWarps * 64);
+    {
+        static int set[64] = {0};
+        int& cur = set[p->device & 63];
+        if (smem > cur) {
+            H2B_CUDA_TRY(cudaFuncSetAttribute(k_xhat_climb, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            cur = smem;
+        }
+    }
+    for (size_t l = 0; l + 1 < p->span_level_off.size(); ++l) {
+        const int64_t a = p->span_level_off[l], b = p->span_level_off[l + 1];
+        k_xhat_climb<<<(unsigned)(b - a), kThreads, smem, st>>>(p->L, p->d_span + a, p->stage_bytes, p->vec_len,
+                                                                 p->span_val, p->xhat, epoch);
+        H2B_CUDA_TRY(cudaGetLastError());
+    }
+    if (int rc = launch_matvec(p, d_x, nullptr, d_y, st, nullptr, 2)) return rc;
+    ++p->n_m_launches;
+    return ok();
+}
+
 // Diagnostics: the per-CTA timeline of the last matvec when the plan was
 // created with H2B_TRACE=1: 8 words per ticket (start ns, end ns, SM id, 5
 // phase marks), then the task-range boundaries [near, coupling, leaf, total,
@@ -2189,11 +2435,11 @@ extern "C" int h2b_matvec_sharded(h2b_plan* p, const double* d_x_local, double* 
 extern "C" int h2b_plan_trace(h2b_plan* p, unsigned long long* h_out, int64_t cap) {
     if (!p || !h_out) return fail(H2B_ERR_INVALID, "h2b_plan_trace: null pointer");
     if (!p->trace) return fail(H2B_ERR_INVALID, "h2b_plan_trace: plan created without H2B_TRACE=1");
-    const int64_t n = (int64_t)(p->L.c_leaves + p->n_near + p->n_cpl);
+    const int64_t n = (int64_t)(p->n_fwd + p->n_near + p->n_cpl);
     if (cap < 8 * n + 5) return fail(H2B_ERR_CAPACITY, "h2b_plan_trace: buffer too small");
     H2B_CUDA_TRY(cudaMemcpy(h_out, p->trace, sizeof(unsigned long long) * 8 * n, cudaMemcpyDeviceToHost));
-    h_out[8 * n] = p->L.c_leaves;
-    h_out[8 * n + 1] = p->L.c_leaves + p->n_near;
+    h_out[8 * n] = p->n_fwd;
+    h_out[8 * n + 1] = p->n_fwd + p->n_near;
     h_out[8 * n + 2] = n;
     h_out[8 * n + 3] = n;
     h_out[8 * n + 4] = n;

@@ -173,13 +173,14 @@ class RowShard:
 
         return near_layout(self.view).entries
 
-    def plan(self):
+    def plan(self, xhat_mask=None):
         from .containers import MatvecPlan, far_layout, near_layout
 
         rt = self.bt.row_tree
         row_local = np.arange(rt.n_dofs, dtype=np.int64) - self.lo  # only owned rows are written
         return MatvecPlan(self.view, self.rb, self.cb, self.S, self.D, far_layout(self.view, self.rb, self.cb),
-                          near_layout(self.view), owned=self.owned, col_perm=self.pad_index, row_perm=row_local)
+                          near_layout(self.view), owned=self.owned, col_perm=self.pad_index, row_perm=row_local,
+                          xhat_mask=xhat_mask)
 
 
 class LocalMatvec:
@@ -192,6 +193,30 @@ class LocalMatvec:
     def apply(self, x, y):
         self.plan.apply_device(x, y)
         return y
+
+
+def xhat_exchange_layout(tree, ranks, ranges):
+    """The x_hat exchange of SURVEY 8(e)'s better variant: rank r owns the
+    column clusters inside its permuted range [lo_r, hi_r) and computes their
+    coefficients; every rank's owned coefficients (uid order) fill one chunk
+    of the gathered buffer.  Returns (masks (world, n_nodes) int8, chunk,
+    src (n_nodes,) offset of each cluster in the gathered buffer, -1 for the
+    clusters spanning several ranks)."""
+    world = len(ranges)
+    n = tree.n_nodes
+    masks = np.zeros((world, n), dtype=np.int8)
+    src = np.full(n, -1, dtype=np.int64)
+    sizes = []
+    for r, (lo, hi) in enumerate(ranges):
+        m = (tree.start >= lo) & (tree.end <= hi) & (tree.end > tree.start)
+        masks[r] = m
+        sizes.append(int(np.asarray(ranks, dtype=np.int64)[m].sum()))
+    chunk = max(max(sizes), 1)
+    for r in range(world):
+        u = np.flatnonzero(masks[r])
+        k = np.asarray(ranks, dtype=np.int64)[u]
+        src[u] = r * chunk + np.cumsum(k) - k
+    return masks, chunk, src
 
 
 class NativeComm:
@@ -228,7 +253,11 @@ class ShardedMatvec:
     Built either from a RowShard (sharded assembly: the rank holds only its
     share of the operator) or, for tests, from a full single-GPU H2Matrix."""
 
-    def __init__(self, src, rank, world, dist, comm=None):
+    def __init__(self, src, rank, world, dist, comm=None, xhat=False):
+        """xhat=True: the x_hat exchange variant: the rank's
+        forward transform covers only its own column subtrees, the
+        coefficients are all-gathered (second collective) and the clusters
+        spanning several ranks are climbed on every rank."""
         import torch
 
         if isinstance(src, RowShard):
@@ -243,6 +272,14 @@ class ShardedMatvec:
             shard.S, shard.D = H.S_dev, H.D_dev
         self.shard, self.rank, self.world, self.dist = shard, rank, world, dist
         self.lo, self.hi, self.chunk = shard.lo, shard.hi, shard.chunk
+        self.xhat = xhat
+        xmask = None
+        if xhat:
+            from .containers import _basis_ranks
+
+            ct = shard.bt.col_tree
+            masks, self.xchunk, xsrc = xhat_exchange_layout(ct, _basis_ranks(shard.cb, ct.n_nodes), shard.ranges)
+            xmask = masks[rank]
         if shard.view is shard.bt:
             from .containers import MatvecPlan
 
@@ -250,9 +287,13 @@ class ShardedMatvec:
             H = src
             self.plan = MatvecPlan(H.block_tree, H.row_basis, H.col_basis, H.S_dev, H.D_dev, H.far_layout,
                                    H.near_layout, owned=shard.owned, col_perm=shard.pad_index,
-                                   row_perm=np.arange(rt.n_dofs, dtype=np.int64) - shard.lo)
+                                   row_perm=np.arange(rt.n_dofs, dtype=np.int64) - shard.lo, xhat_mask=xmask)
         else:
-            self.plan = shard.plan()
+            self.plan = shard.plan(xhat_mask=xmask)
+        if xhat:
+            _lib.check(_lib.lib().h2b_xhat_set_import(self.plan.handle, _lib.ptr(np.ascontiguousarray(xsrc))))
+            self.xsend = torch.zeros(self.xchunk, dtype=torch.float64, device="cuda")
+            self.xrecv = torch.zeros(world * self.xchunk, dtype=torch.float64, device="cuda")
         rt = shard.bt.row_tree
         self.xbuf = torch.zeros(world * self.chunk, dtype=torch.float64, device="cuda")
         self.xloc = torch.zeros(self.chunk, dtype=torch.float64, device="cuda")
@@ -275,6 +316,14 @@ class ShardedMatvec:
         return y_local_perm
 
     def _gather_apply(self, y):
+        if self.xhat:
+            L, st = _lib.lib(), _lib.stream_ptr()
+            self.dist.all_gather_into_tensor(self.xbuf, self.xloc)
+            _lib.check(L.h2b_xhat_forward(self.plan.handle, self.xbuf.data_ptr(), self.xsend.data_ptr(), st))
+            self.dist.all_gather_into_tensor(self.xrecv, self.xsend)
+            _lib.check(L.h2b_xhat_main(self.plan.handle, self.xbuf.data_ptr(), self.xrecv.data_ptr(), y.data_ptr(),
+                                       st))
+            return
         if self.comm is not None:
             # all-gather (NCCL) + fused matvec in one C-ABI call
             _lib.check(_lib.lib().h2b_matvec_sharded(self.plan.handle, self.xloc.data_ptr(), y.data_ptr(),

@@ -138,3 +138,35 @@ def test_two_rank_gloo_matches_single_rank():
         assert p.exitcode == 0
     ok, ranges, n_owned = res
     assert ok, f"sharded oracle differs from the single-rank result (ranges {ranges})"
+
+
+def test_xhat_exchange_layout():
+    """x_hat exchange bookkeeping (SURVEY 8(e) better variant): every leaf is
+    owned by exactly one rank, owned clusters never straddle a rank boundary,
+    the gathered offsets tile each rank's chunk without overlap, and exactly
+    the clusters spanning several ranks have no offset."""
+    from paper_2001_05523_b200 import clustering as C
+    from paper_2001_05523_b200 import distributed as DD
+    from paper_2001_05523_b200 import spaces
+    from paper_2001_05523_b200.mesh import sphere_mesh
+
+    m = sphere_mesh(4)
+    t = C.build_cluster_tree(spaces.DofSpace(spaces.P0, m).support_boxes(), 16)
+    ranks = np.random.default_rng(0).integers(3, 20, t.n_nodes)
+    for world in (1, 2, 3, 5):
+        leaves = t.leaf_uids()
+        cuts = np.linspace(0, len(leaves), world + 1).astype(int)
+        order = leaves[np.argsort(t.start[leaves])]
+        ranges = [(int(t.start[order[a]]), int(t.end[order[b - 1]])) for a, b in zip(cuts[:-1], cuts[1:])]
+        masks, chunk, src = DD.xhat_exchange_layout(t, ranks, ranges)
+        assert (masks[:, leaves].sum(axis=0) == 1).all()
+        assert (masks.sum(axis=0) <= 1).all()
+        spanning = masks.sum(axis=0) == 0
+        assert ((src < 0) == spanning).all()
+        for r in range(world):
+            u = np.flatnonzero(masks[r])
+            lo, hi = ranges[r]
+            assert ((t.start[u] >= lo) & (t.end[u] <= hi)).all()
+            off = src[u] - r * chunk
+            k = ranks[u]
+            assert off[0] == 0 and (np.diff(off) == k[:-1]).all() and off[-1] + k[-1] <= chunk

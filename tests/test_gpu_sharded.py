@@ -269,3 +269,52 @@ def test_native_comm_single_rank(slp5):
         assert torch.equal(yl, y[op.perm_dev])
     finally:
         comm.close()
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_xhat_exchange_bitwise(slp5, world):
+    """The x_hat exchange variant: each rank forward-transforms
+    only its own column subtrees (h2b_xhat_forward), the coefficients are
+    all-gathered (here: concatenated in one process) and the spanning clusters
+    climbed on every rank (h2b_xhat_main).  The rank's rows are the bits of the
+    plan that runs the whole forward transform itself."""
+    import torch
+
+    from paper_2001_05523_b200 import _lib
+    from paper_2001_05523_b200 import distributed as DD
+
+    ctx, bt, rb, cb, H = slp5
+    n = H.shape[0]
+    L, st = _lib.lib(), _lib.stream_ptr()
+    x = torch.from_numpy(np.random.default_rng(10 + world).standard_normal(n)).cuda()
+    xp = x[torch.from_numpy(bt.row_tree.perm).cuda()]
+    shards, full_ops, x_ops = [], [], []
+    for r in range(world):
+        sh = DD.RowShard(bt, rb, cb, r, world)
+        sh.assemble(ctx, "slp", 3, 4)
+        full = torch.zeros(world * sh.chunk, dtype=torch.float64, device="cuda")
+        full[torch.from_numpy(sh.pad_index).cuda()] = xp
+        shards.append((sh, full))
+        full_ops.append(DD.ShardedMatvec(sh, r, world, _FakeGather(full)))
+        x_ops.append(DD.ShardedMatvec(sh, r, world, _FakeGather(full), xhat=True))
+    import ctypes
+
+    info = (ctypes.c_int64 * 5)()
+    owned_fwd = 0
+    for op in x_ops:
+        _lib.check(L.h2b_xhat_info(op.plan.handle, info))
+        owned_fwd += int(info[2])
+    # the forward tasks are split over the ranks (every column leaf once)
+    assert owned_fwd == len(bt.col_tree.leaf_uids())
+    for rep in range(2):  # epochs advance across launches
+        for op, (sh, full) in zip(x_ops, shards):
+            _lib.check(L.h2b_xhat_forward(op.plan.handle, full.data_ptr(), op.xsend.data_ptr(), st))
+        recv = torch.cat([op.xsend for op in x_ops])
+        for r, (op, fop, (sh, full)) in enumerate(zip(x_ops, full_ops, shards)):
+            y_x = torch.zeros(sh.hi - sh.lo, dtype=torch.float64, device="cuda")
+            _lib.check(L.h2b_xhat_main(op.plan.handle, full.data_ptr(), recv.data_ptr(), y_x.data_ptr(), st))
+            y_f = fop.apply_local(xp[sh.lo : sh.hi])
+            assert torch.equal(y_x, y_f), (world, r, rep)
+        xp = xp * 0.5 + 1.0
+        for sh, full in shards:
+            full[torch.from_numpy(sh.pad_index).cuda()] = xp
