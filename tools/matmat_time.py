@@ -57,7 +57,7 @@ def timed(fn, reps=30):
 
 
 mv_bytes = H.matvec_bytes()
-hbm = bench.peaks()["hbm_gbs"]
+hbm = bench.peaks()[0]
 x = torch.randn(n, dtype=torch.float64, device="cuda")
 t_mv = timed(lambda: plan.apply_device(x))
 res = {"workload": name, "n": n, "matvec_ms": t_mv * 1e3, "matvec_dofs_per_s": n / t_mv, "runs": []}
