@@ -229,6 +229,7 @@ int h2b_dlp_jobs_free(h2b_dlp_build* b);
  * K_VALUE | K_DN_Z), P1 rows are vertices (hat functions, K_DN_X | K_DN_X_DN_Z). */
 #define H2B_GCA_P0_SLP 0
 #define H2B_GCA_P1_DLP 1
+#define H2B_GCA_P1_CURL 2  /* hypersingular: curl-weighted P0 potentials, 6 n_green columns */
 
 /* One tree level of clusters (independent).  Cluster c has rows
  * d_rows[d_row_ptr[c] : d_row_ptr[c+1]] (leaf: its dofs; inner: its children's
@@ -243,6 +244,7 @@ typedef struct {
     int32_t max_rows;
     const double* d_green;
     const int64_t* d_l_off;
+    int32_t n_cols;  /* columns of L (0: 2 n_green; 6 n_green for H2B_GCA_P1_CURL) */
 } h2b_gca_batch;
 
 /* Green-quadrature columns L (rows x 2k, row-major) of every cluster
@@ -252,6 +254,13 @@ typedef struct {
  * entries -> H2B_ERR_INVALID.  Synchronises. */
 int h2b_gca_columns(const h2b_mesh* m, const double* d_panel_points, int32_t Q, const double* d_lam, int flavor,
                     const h2b_gca_batch* b, double* d_L, void* stream);
+/* The P1_CURL flavor (gca.green_columns for HYP, src/gca.py:106-117 with
+ * kernels.curl_potentials src/kernels.py:172-196): rows are vertices, L is
+ * rows x 6 n_green = [a_x | a_y | a_z | c_x | c_y | c_z], a / c the K_VALUE /
+ * K_DN_Z panel potentials of the incident panels weighted by the hat's
+ * constant surface curl on each panel (d_curls: 3F x 3, kernels.triangle_curls). */
+int h2b_gca_columns_curl(const h2b_mesh* m, const double* d_panel_points, int32_t Q, const double* d_curls,
+                         const h2b_gca_batch* b, double* d_L, void* stream);
 /* Fully pivoted ACA with inverse core on every L (lowrank.aca_inverse_core,
  * src/lowrank.py:154-184) and the interpolation matrix V = L[:, sigma]
  * inv(L[tau, sigma]) (gca.cross_interpolate).  Outputs: d_rank[c], local pivot

@@ -70,6 +70,7 @@ class GcaBatch(ctypes.Structure):
     _fields_ = [
         ("n_clusters", ctypes.c_int64), ("d_row_ptr", vp), ("d_rows", vp), ("n_green", ctypes.c_int32),
         ("max_rows", ctypes.c_int32), ("d_green", vp), ("d_l_off", vp),
+        ("n_cols", ctypes.c_int32),
     ]
 
 
@@ -111,7 +112,7 @@ EXPORTS = (
     "h2b_basis_forward", "h2b_basis_backward", "h2b_transpose_blocks", "h2b_hyp_scatter",
     "h2b_comm_unique_id", "h2b_comm_init", "h2b_comm_destroy", "h2b_plan_set_comm", "h2b_matvec_sharded",
     "h2b_cluster_tree_device", "h2b_block_tree_device",
-    "h2b_plan_create_xhat", "h2b_xhat_info", "h2b_xhat_set_import", "h2b_xhat_forward", "h2b_xhat_main",
+    "h2b_gca_columns_curl", "h2b_plan_create_xhat", "h2b_xhat_info", "h2b_xhat_set_import", "h2b_xhat_forward", "h2b_xhat_main",
 )
 
 _lib = None
@@ -183,6 +184,8 @@ def lib():
         L.h2b_comm_destroy.argtypes = [vp]
         L.h2b_plan_set_comm.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int64]
         L.h2b_matvec_sharded.argtypes = [vp, vp, vp, vp]
+        L.h2b_gca_columns_curl.argtypes = [ctypes.POINTER(Mesh), vp, ctypes.c_int32, vp, ctypes.POINTER(GcaBatch), vp,
+                                           vp]
         L.h2b_gca_aca.argtypes = [ctypes.POINTER(GcaBatch), ctypes.c_double, vp, vp, vp, vp, ctypes.c_int32, vp, vp]
         _lib = L
     return _lib

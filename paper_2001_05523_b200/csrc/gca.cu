@@ -73,6 +73,41 @@ __global__ void __launch_bounds__(kColThreads) k_gca_columns(const double* __res
                 // (x - z).n_z / r^3
                 vc = fma(wt * (t * t), fma(dz, nzz, fma(dy, nzy, dx * nzx)), vc);
             }
+        } else if (FLAVOR == H2B_GCA_P1_CURL) {
+            // hat of vertex rows[r]: P0 potentials of its incident panels, each
+            // weighted by the hat's (constant) surface curl on that panel
+            const int v = b.d_rows[r0 + r];
+            double a3[3] = {0.0, 0.0, 0.0}, c3[3] = {0.0, 0.0, 0.0};
+            for (int64_t ip = vt_ptr[v]; ip < vt_ptr[v + 1]; ++ip) {
+                const int p = vt_idx[ip];
+                const int l = T[3 * p] == v ? 0 : (T[3 * p + 1] == v ? 1 : 2);
+                double pa = 0.0, pc = 0.0;
+                for (int q = 0; q < Q; ++q) {
+                    const int64_t gq = (int64_t)p * Q + q;
+                    const double dx = __ldg(P + gq) - zx, dy = __ldg(P + FQ + gq) - zy,
+                                 dz = __ldg(P + 2 * FQ + gq) - zz;
+                    const double w = __ldg(P + 3 * FQ + gq);
+                    const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+                    const double t = inv_sqrt(r2);
+                    const double wt = w * t;
+                    pa = fma(wt, 1.0, pa);
+                    pc = fma(wt * (t * t), fma(dz, nzz, fma(dy, nzy, dx * nzx)), pc);
+                }
+                const double* cu = lam + 3 * (3 * (int64_t)p + l);  // curls[p, l, :]
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    a3[d] = fma(cu[d], pa, a3[d]);
+                    c3[d] = fma(cu[d], pc, c3[d]);
+                }
+            }
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                const double a = a3[d] * inv4pi * sw, cc = c3[d] * inv4pi * sw;
+                if (!isfinite(a) || !isfinite(cc)) bad = 1;
+                Lc[(int64_t)r * 6 * k + d * k + j] = a;
+                Lc[(int64_t)r * 6 * k + (3 + d) * k + j] = cc;
+            }
+            continue;
         } else {
             // hat function of vertex rows[r]: incident panels, barycentric weight of its corner
             const int v = b.d_rows[r0 + r];
@@ -163,7 +198,7 @@ __global__ void __launch_bounds__(kAcaThreads) k_gca_aca(h2b_gca_batch b, double
     const int c = blockIdx.x;
     const int64_t r0 = b.d_row_ptr[c];
     const int rows = (int)(b.d_row_ptr[c + 1] - r0);
-    const int ncol = 2 * b.n_green;
+    const int ncol = b.n_cols > 0 ? b.n_cols : 2 * b.n_green;
     const int64_t n = (int64_t)rows * ncol;
     const double* Lc = L + b.d_l_off[c];
     // shared layout: col[max_rows] | rowp[ncol] | red (3 x (warps+1)) | tau, sigma | R (if it fits)
@@ -328,16 +363,38 @@ extern "C" int h2b_gca_columns(const h2b_mesh* m, const double* d_panel_points, 
     return ok();
 }
 
+extern "C" int h2b_gca_columns_curl(const h2b_mesh* m, const double* d_panel_points, int32_t Q, const double* d_curls,
+                                    const h2b_gca_batch* b, double* d_L, void* stream) {
+    if (!m || !d_panel_points || !d_curls || !b || !d_L || Q < 1)
+        return fail(H2B_ERR_INVALID, "h2b_gca_columns_curl: bad argument");
+    if (b->n_clusters == 0) return ok();
+    cudaStream_t st = as_stream(stream);
+    int* flags;
+    H2B_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&flags), sizeof(int), st));
+    H2B_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(int), st));
+    const size_t sm = (size_t)b->n_green * kGreenStride * sizeof(double);
+    k_gca_columns<H2B_GCA_P1_CURL><<<(unsigned)b->n_clusters, kColThreads, sm, st>>>(
+        d_panel_points, m->n_triangles, Q, m->d_triangles, m->d_normals, m->d_vt_ptr, m->d_vt_idx, d_curls, *b, d_L,
+        flags);
+    H2B_CUDA_TRY(cudaGetLastError());
+    int h = 0;
+    H2B_CUDA_TRY(cudaMemcpyAsync(&h, flags, sizeof(int), cudaMemcpyDeviceToHost, st));
+    H2B_CUDA_TRY(cudaStreamSynchronize(st));
+    H2B_CUDA_TRY(cudaFreeAsync(flags, st));
+    if (h) return fail(H2B_ERR_INVALID, "matrix contains non-finite entries");
+    return ok();
+}
+
 extern "C" int h2b_gca_aca(const h2b_gca_batch* b, double eps, const double* d_L, double* d_scratch, int32_t* d_rank,
                            int32_t* d_tau, int32_t tau_cap, double* d_V, void* stream) {
-    if (!b || !d_L || !d_scratch || !d_rank || !d_tau || !d_V || tau_cap < 2 * b->n_green)
+    const int64_t ncol = b ? (b->n_cols > 0 ? b->n_cols : 2 * (int64_t)b->n_green) : 0;
+    if (!b || !d_L || !d_scratch || !d_rank || !d_tau || !d_V || tau_cap < ncol)
         return fail(H2B_ERR_INVALID, "h2b_gca_aca: bad argument");
     if (b->n_clusters == 0) return ok();
     cudaStream_t st = as_stream(stream);
     int dev, max_optin;
     H2B_CUDA_TRY(cudaGetDevice(&dev));
     H2B_CUDA_TRY(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    const int64_t ncol = 2 * (int64_t)b->n_green;
     const int64_t head = b->max_rows + ncol + 3 * (kAcaWarps + 1) + tau_cap;
     // shared memory: the header plus the largest residual of the batch, capped
     int64_t want = head + (int64_t)b->max_rows * ncol;

@@ -317,7 +317,7 @@ def green_points_batch_device(boxes, m):
     return out
 
 
-_GCA_FLAVOR_CODE = {P0_SLP: 0, P1_DLP: 1}
+_GCA_FLAVOR_CODE = {P0_SLP: 0, P1_DLP: 1, P1_CURL: 2}
 
 
 def build_basis_device(ctx, tree, flavor, m, eps_aca, q_single=None):
@@ -341,7 +341,7 @@ def build_basis_device(ctx, tree, flavor, m, eps_aca, q_single=None):
     basis = ClusterBasis(tree)
     depth = tree.depth_of
     k = 6 * m * m
-    ncol = 2 * k
+    ncol = 6 * k if flavor == P1_CURL else 2 * k  # curl: three components of both potentials
     for d in range(int(depth.max()), -1, -1):
         level = np.flatnonzero(depth == d)
         rows, boxes = [], []
@@ -358,12 +358,16 @@ def build_basis_device(ctx, tree, flavor, m, eps_aca, q_single=None):
         d_ptr, d_rows = D.dev(ptr), D.dev(np.concatenate(rows), np.int32)
         d_green, d_loff = green_points_batch_device(np.stack(boxes), m), D.dev(l_off)
         b = _lib.GcaBatch(len(level), d_ptr.data_ptr(), d_rows.data_ptr(), k, int(nr.max()), d_green.data_ptr(),
-                          d_loff.data_ptr())
+                          d_loff.data_ptr(), ncol)
         Lm, scratch, Vm = D.empty((total,)), D.empty((total,)), D.empty((total,))
         rank = D.empty((len(level),), "int32")
         tau = D.empty((len(level) * ncol,), "int32")
-        _lib.check(L_.h2b_gca_columns(ctypes.byref(ctx.dmesh.c), pp.data_ptr(), Q, lam.data_ptr(),
-                                      _GCA_FLAVOR_CODE[flavor], ctypes.byref(b), Lm.data_ptr(), D.stream()))
+        if flavor == P1_CURL:
+            _lib.check(L_.h2b_gca_columns_curl(ctypes.byref(ctx.dmesh.c), pp.data_ptr(), Q, ctx.dmesh.curls().data_ptr(),
+                                               ctypes.byref(b), Lm.data_ptr(), D.stream()))
+        else:
+            _lib.check(L_.h2b_gca_columns(ctypes.byref(ctx.dmesh.c), pp.data_ptr(), Q, lam.data_ptr(),
+                                          _GCA_FLAVOR_CODE[flavor], ctypes.byref(b), Lm.data_ptr(), D.stream()))
         _lib.check(L_.h2b_gca_aca(ctypes.byref(b), float(eps_aca), Lm.data_ptr(), scratch.data_ptr(),
                                   rank.data_ptr(), tau.data_ptr(), ncol, Vm.data_ptr(), D.stream()))
         # download only the used part of every V slot (rows x rank of rows x 2k):

@@ -28,7 +28,7 @@ def _compare(bh, bd, tree):
     return frac, worst
 
 
-@pytest.mark.parametrize("flavor", ["p0_slp", "p1_dlp"])
+@pytest.mark.parametrize("flavor", ["p0_slp", "p1_dlp", "p1_curl"])
 def test_device_basis_matches_host_cfg0(flavor):
     from paper_2001_05523_b200 import gca
     from paper_2001_05523_b200.containers import AssemblyContext
@@ -65,6 +65,29 @@ def test_device_basis_operator_accuracy_cfg0():
     eh = np.linalg.norm(Hh.matvec(x) - ref) / np.linalg.norm(ref)
     ed = np.linalg.norm(Hd.matvec(x) - ref) / np.linalg.norm(ref)
     assert ed < 1e-3 and ed <= 2.0 * eh + 1e-12, (ed, eh)
+
+
+def test_device_curl_basis_hyp_operator():
+    """P1_CURL basis on the GPU (h2b_gca_columns_curl + h2b_gca_aca with 6k
+    columns) -> hypersingular H^2 operator: agrees with the reference's matvec
+    on tests/golden/h2_hyp4.npz to the GCA tolerance, like the host basis."""
+    from paper_2001_05523_b200 import clustering as C
+    from paper_2001_05523_b200 import gca
+    from paper_2001_05523_b200.containers import AssemblyContext
+
+    from .conftest import golden
+
+    g = golden("h2_hyp4.npz")
+    m = sphere(4)
+    _, t1 = trees(m, 32)
+    ctx = AssemblyContext(m)
+    bt = C.BlockTree(t1, t1, 2.0)
+    bd = gca.build_basis(ctx, t1, gca.P1_CURL, 3, 1e-4, device=True)
+    ranks = np.array([bd.rank[u] for u in range(t1.n_nodes)])
+    assert np.abs(ranks - g["ranks"]).max() <= 2
+    Hd = gca.assemble_h2(ctx, "hyp", bt, bd, bd, 3, q_singular=4)
+    y = Hd.matvec(g["x"])
+    assert np.linalg.norm(y - g["y"]) / np.linalg.norm(g["y"]) < 1e-3
 
 
 def test_problem_setup_with_device_basis():
