@@ -74,7 +74,9 @@ constexpr int kBandWords = 24;  // src_off, cols, rows, gidx_off, out_off, is_la
                                 // downward-step record of the band's cluster (coupling bands):
                                 // k, parent y_hat offset (-1 root), k_parent, e_off, y_hat offset,
                                 // is_leaf, v_off, start (size = rows of a leaf)
-constexpr int kFwdHead = 7;     // start, size, k, v_off, xhat_off, n_climb, warp_ok
+constexpr int kFwdHead = 8;     // start, size, k, v_off, xhat_off, n_climb, warp_ok, offset of the climb levels
+constexpr int kFwdStride = 40;  // forward records are fixed-stride (record = ticket * stride: no index round
+                                // trip): the header, then the leaf's first 64 x indices (col_perm, int32)
 constexpr int kFwdLevel = 6;    // k0, kp, e_off_c0, e_off_own, xhat_off_c0, xhat_off_parent
 constexpr int kCopyChunk = 1024;  // x values per copy task (host-input launches)
 constexpr int kKindNear = 0, kKindCpl = 1;  // band record kinds (word 7)
@@ -103,6 +105,7 @@ struct h2b_plan {
     int smem;
     int stage_bytes;     // TMA staging buffer per CTA (plan_stage_bytes)
     int64_t e_bytes_r;
+    double* dpack = nullptr;  // downward-step operands [E_t^T | V_t^T] per cluster (k_pack_descent)
     double* dx;
     double* dy;
     double* hy;         // pinned host staging of the result (h2b_matvec_host)
@@ -223,6 +226,11 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 }
 
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// 1-D bulk prefetch into L2 (16-byte aligned, size % 16 == 0)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
     asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
@@ -545,6 +553,7 @@ struct Shared {
     bool near_sym;             // nearfield as symmetric column panels
     uint32_t parity;           // mbarrier phase of the staging slot in use
     bool issued;               // band bulk copy already issued by the caller
+    const double* dpack;       // downward-step operands [E_t^T | V_t^T] per cluster (plan-owned copy)
 };
 
 // x[i]: from the LL copy made by this launch's copy tasks (host input) or
@@ -629,15 +638,18 @@ __device__ __forceinline__ double climb_coef(const double* E0, const double* E1,
 // shared memory, the climb's transfer matrices copied by the warp (cp.async)
 // while the sibling's coefficients are awaited.
 __device__ void forward_warp(const double* __restrict__ c_V, const double* __restrict__ c_E,
-                             const int64_t* __restrict__ col_perm, const double* __restrict__ x, uint64_t* xhat,
-                             uint32_t epoch, const Shared& s) {
+                             const double* __restrict__ x, uint64_t* xhat, uint32_t epoch, const Shared& s,
+                             int ix0, int ix1) {
     const int lane = threadIdx.x;
-    const int start = (int)s.rec[0], size = (int)s.rec[1], k = (int)s.rec[2];
+    const int size = (int)s.rec[1], k = (int)s.rec[2];
     const int64_t v_off = s.rec[3], xhat_off = s.rec[4];
     const int n_climb = (int)s.rec[5];
     const double* V = stage_issue(s, c_V + v_off, ((int64_t)size * k * 8 + 15) & ~int64_t(15));
-    for (int i = kFwdHead + lane; i < kFwdHead + kFwdLevel * n_climb; i += 32) s.rec[i] = __ldg(s.rec_src + i);
-    for (int r = lane; r < size; r += 32) s.va[r] = load_x(s, x, __ldg(col_perm + start + r), epoch);
+    // x through the permutation: the indices came with the record (ix0, ix1:
+    // rows lane and lane + 32), so the values are one round trip away
+    if (lane < size) s.va[lane] = load_x(s, x, ix0, epoch);
+    if (lane + 32 < size) s.va[lane + 32] = load_x(s, x, ix1, epoch);
+    for (int i = lane; i < kFwdLevel * n_climb; i += 32) s.rec[kFwdHead + i] = __ldg(s.rec_src + i);
     __syncwarp();
     {
         int kk = k;  // pull the climb's transfer matrices into L2
@@ -695,20 +707,27 @@ __device__ void forward_warp(const double* __restrict__ c_V, const double* __res
 
 __device__ void task_forward(const double* __restrict__ c_V, const double* __restrict__ c_E,
                                        const int64_t* __restrict__ col_perm, const int64_t* rec, const double* __restrict__ x,
-                             uint64_t* xhat, uint32_t epoch, const Shared& s) {
-    // header, then (block path) the climb levels
+                             uint64_t* xhat, uint32_t epoch, const Shared& s, const int64_t* rec_base) {
+    // header and the leaf's x indices in one round trip, then (block path) the
+    // climb levels
+    int ix0 = 0, ix1 = 0;
+    if (threadIdx.x < 32) {
+        const int32_t* ip = reinterpret_cast<const int32_t*>(rec + kFwdHead);
+        ix0 = __ldg(ip + threadIdx.x);
+        ix1 = __ldg(ip + 32 + threadIdx.x);
+    }
     for (int i = threadIdx.x; i < kFwdHead; i += kThreads) s.rec[i] = __ldg(rec + i);
     __syncthreads();
-    const_cast<Shared&>(s).rec_src = rec;
+    const_cast<Shared&>(s).rec_src = rec_base + s.rec[7];  // the climb levels
     if (!s.rec[6]) {
         const int nc = (int)s.rec[5];
-        for (int i = kFwdHead + threadIdx.x; i < kFwdHead + kFwdLevel * nc; i += kThreads) s.rec[i] = __ldg(rec + i);
+        for (int i = threadIdx.x; i < kFwdLevel * nc; i += kThreads) s.rec[kFwdHead + i] = __ldg(s.rec_src + i);
     }
     const int start = (int)s.rec[0], size = (int)s.rec[1], k = (int)s.rec[2];
     const int64_t v_off = s.rec[3], xhat_off = s.rec[4];
     const int n_climb = (int)s.rec[5];
     if (s.rec[6]) {  // every rank <= 32 and the leaf <= 64 rows: one warp, no block barriers
-        if (threadIdx.x < 32) forward_warp(c_V, c_E, col_perm, x, xhat, epoch, s);
+        if (threadIdx.x < 32) forward_warp(c_V, c_E, x, xhat, epoch, s, ix0, ix1);
         return;
     }
     const double* V = stage_issue(s, c_V + v_off, ((int64_t)size * k * 8 + 15) & ~int64_t(15));
@@ -857,9 +876,14 @@ __device__ void near_sum(const Shared& s, const int64_t* list, int n, int size, 
     }
 }
 
+// `par`: the staging barrier's next phase.  The operands come from the plan's
+// packed copy s.dpack: per cluster E_t^T (k_parent x k, padded to an even
+// length) followed by V_t^T (k x |t|, leaves), so ONE bulk copy stages what
+// the thread-per-row products read (the one-warp step used to transpose both
+// with 8-byte cp.async copies: ~5 us of a 10 us leaf task at config 3).
 __device__ void descent(const double* __restrict__ r_E, const double* __restrict__ r_V,
                                   const int64_t* __restrict__ row_perm, const int64_t* d, const uint64_t* ycpl, uint64_t* yfin,
-                        const uint64_t* ynear, double* y, uint32_t epoch, bool has_cpl, const Shared& s) {
+                        const uint64_t* ynear, double* y, uint32_t epoch, bool has_cpl, const Shared& s, uint32_t par) {
     const int k = (int)d[0], kp = (int)d[2];
     const int64_t par_off = d[1], e_off = d[3], yoff = d[4];
     const bool leaf = d[5] != 0;
@@ -883,20 +907,15 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
         const int lane = threadIdx.x;
         const int size = leaf ? (int)d[8] : 0;
         double* Vt = Es + ((k * kp + 1) & ~1);
-        // E_t^T and V_t^T staged by the warp while the inputs are awaited
-        if (par_off >= 0)
-            for (int i = lane; i < k * kp; i += 32) {
-                const int r = i / kp, c = i - r * kp;
-                cp_async8(Es + c * k + r, r_E + e_off + i);
-            }
-        if (leaf)
-            for (int i = lane; i < size * k; i += 32) {
-                const int r = i / k, c = i - r * k;
-                cp_async8(Vt + c * size + r, r_V + v_off + i);
-            }
+        // [E_t^T | V_t^T] by one bulk copy while the inputs are awaited
+        const uint32_t pbytes = 8u * (uint32_t)(((k * kp + 1) & ~1) + ((size * k + 1) & ~1));
+        if (pbytes && lane == 0) {
+            mbar_expect_tx(s.bar, pbytes);
+            bulk_g2s(Es, s.dpack + d[13], pbytes, s.bar);
+        }
         double v = (has_cpl && lane < k) ? ll_load(ycpl + 2 * (yoff + lane), epoch) : 0.0;
         if (par_off >= 0 && lane < kp) s.rhs[lane] = ll_load(yfin + 2 * (par_off + lane), epoch);
-        cp_async_wait_all();
+        if (pbytes) mbar_wait(s.bar, par);
         __syncwarp();
         mark(s.mark, 4);
         if (par_off >= 0 && lane < k) {
@@ -932,14 +951,15 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
         }
         return;
     }
-    const bool e_smem = par_off >= 0 && k * kp <= s.stage_bytes / 8;
-    // transfer / leaf basis matrices are staged TRANSPOSED, so that the
-    // thread-per-row products below read consecutive words (no bank conflicts)
-    if (e_smem)
-        for (int i = threadIdx.x; i < k * kp; i += kThreads) {
-            const int r = i / kp, c = i - r * kp;
-            cp_async8(Es + c * k + r, r_E + e_off + i);
-        }
+    const int ne = (k * kp + 1) & ~1;  // E_t^T in the packed copy (padded to an even length)
+    const bool e_smem = par_off >= 0 && k > 0 && ne <= s.stage_bytes / 8;
+    // transfer / leaf basis matrices are staged TRANSPOSED (the packed copy
+    // holds them so), so that the thread-per-row products below read
+    // consecutive words (no bank conflicts)
+    if (e_smem && threadIdx.x == 0) {
+        mbar_expect_tx(s.bar, 8u * (uint32_t)ne);
+        bulk_g2s(Es, s.dpack + d[13], 8u * (uint32_t)ne, s.bar);
+    }
     const uint64_t* yc = ycpl + 2 * yoff;
     for (int i = threadIdx.x; i < k; i += kThreads)
         s.va[i] = has_cpl ? ll_load(yc + 2 * i, epoch) : 0.0;
@@ -949,7 +969,10 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
         const uint64_t* yp = yfin + 2 * par_off;
         for (int i = threadIdx.x; i < kp; i += kThreads) s.rhs[i] = ll_load(yp + 2 * i, epoch);
     }
-    cp_async_wait_all();
+    if (e_smem) {
+        mbar_wait(s.bar, par);
+        par ^= 1u;
+    }
     __syncthreads();
     mark(s.mark, 4);
     if (par_off >= 0 && k > 0) {
@@ -969,15 +992,15 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
         return;
     }
     const int size = (int)d[8];
-    const int nv = size * k;
-    const bool v_smem = nv <= s.stage_bytes / 8;
+    const int nv = (size * k + 1) & ~1;
+    const bool v_smem = k > 0 && nv <= s.stage_bytes / 8;
     const double* Vg = r_V + v_off;
-    if (v_smem) {
-        for (int i = threadIdx.x; i < nv; i += kThreads) {
-            const int r = i / k, c = i - r * k;
-            cp_async8(Es + c * size + r, Vg + i);
+    if (v_smem) {  // (the E_t^T product above ended with a block barrier: Es is free)
+        if (threadIdx.x == 0) {
+            mbar_expect_tx(s.bar, 8u * (uint32_t)nv);
+            bulk_g2s(Es, s.dpack + d[13] + ne, 8u * (uint32_t)nv, s.bar);
         }
-        cp_async_wait_all();
+        mbar_wait(s.bar, par);
     }
     __syncthreads();
     if (k > 0) {
@@ -1076,7 +1099,8 @@ __device__ void task_band(const h2b_layout& L, const double* __restrict__ x, con
     }
     if (kCoupling && s.rec[5]) {
         __syncthreads();
-        descent(L.r_E, L.r_V, L.row_perm, s.rec + 8, ycpl, yfin, ynear, y, epoch, s.rec[6] != 0, s);
+        descent(L.r_E, L.r_V, L.row_perm, s.rec + 8, ycpl, yfin, ynear, y, epoch, s.rec[6] != 0, s,
+                s.parity ^ ((rows > 0 || s.issued) ? 1u : 0u));
     }
 }
 
@@ -1233,6 +1257,7 @@ struct KArgs {
     const int32_t* gsym;
     uint64_t* ppart;
     const int64_t* nsum;
+    const double* dpack;     // downward-step operands (transposed row basis)
 };
 
 #ifndef H2B_MINB
@@ -1307,14 +1332,15 @@ __device__ __forceinline__ void run_task(const KArgs& a, const double* __restric
         prefetch_slice(reinterpret_cast<const double*>(a.dsym ? a.gsym : L.d_gidx), a.dgidx_bytes, ticket,
                        a.n_fwd);
         if (!a.xh) prefetch_slice(x, 8 * L.n_cols, ticket, a.n_fwd);
-        task_forward(L.c_V, L.c_E, L.col_perm, a.rec + __ldg(a.fwd_off + ticket), x, a.xhat, epoch, s);
+        task_forward(L.c_V, L.c_E, L.col_perm, a.rec + (int64_t)kFwdStride * ticket, x, a.xhat, epoch, s, a.rec);
     } else {
         const int b = ticket - tB;
-        // the first bands pull the row-basis transfer matrices into L2
-        const int np = min(a.n_near + a.n_cpl, 512);
-        if (b < np) prefetch_slice(L.r_E, a.e_bytes_r, b, np);
         load_rec(s, a.rec + a.band_base + (int64_t)kBandWords * b, kBandWords);
         const int kind = (int)s.rec[7];
+        // a cluster's last band: pull its downward-step operands into L2 now
+        // (the bulk copy after the band's product then hits L2)
+        if (kind == kKindCpl && s.rec[5] && s.rec[22] > 0 && threadIdx.x == 32)
+            bulk_prefetch_l2(a.dpack + s.rec[21], (uint32_t)s.rec[22]);
         if (kind == kKindNearSym)
             task_panel(a.dsym, a.gsym, x, a.ppart, epoch, s);
         else if (kind == kKindNear)
@@ -1366,6 +1392,7 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
     s.near_sym = a.dsym != nullptr;
     s.ppart = a.ppart;
     s.nsum = a.nsum;
+    s.dpack = a.dpack;
     s.rec = s_rec;
     s.parity = 0;
     s.issued = false;
@@ -1465,6 +1492,28 @@ __global__ void __launch_bounds__(kThreads) k_xhat_climb(h2b_layout L, const int
         plain[xo + c] = vb[c];
         ll_store(xhat + 2 * (xo + c), vb[c], epoch);
     }
+}
+
+// Plan creation: the operands of every downward step, transposed into the
+// layout the step's products read (one CTA per step): E_t^T (k_parent x k),
+// then V_t^T (k x |t|) for leaves; see descent().
+__global__ void k_pack_descent(const double* __restrict__ r_E, const double* __restrict__ r_V,
+                               const int64_t* __restrict__ desc, double* __restrict__ pack) {
+    const int64_t* d = desc + 6 * (int64_t)blockIdx.x;
+    const int64_t e_off = d[0], v_off = d[3];
+    const int k = (int)d[1], kp = (int)d[2], size = (int)d[4];
+    double* out = pack + d[5];
+    if (e_off >= 0)
+        for (int i = threadIdx.x; i < k * kp; i += blockDim.x) {
+            const int r = i / kp, c = i - r * kp;
+            out[(int64_t)c * k + r] = r_E[e_off + i];
+        }
+    out += (((int64_t)k * kp + 1) & ~int64_t(1));
+    if (v_off >= 0)
+        for (int i = threadIdx.x; i < size * k; i += blockDim.x) {
+            const int r = i / k, c = i - r * k;
+            out[(int64_t)c * size + r] = r_V[v_off + i];
+        }
 }
 
 __global__ void k_diagonal(h2b_layout L, double* __restrict__ diag) {
@@ -1855,13 +1904,30 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags, const i
         for (int u = 0; u < L.r_nodes; ++u) hasv[u] = (scols[u] > 0 && rrank[u] > 0) ? 1 : 0;
         top_down(L.r_nodes, rparent, hasv);
     }
-    // A: forward records (leaf, then the levels it climbs as the right child)
-    for (int i = 0; i < L.c_leaves; ++i) {
-        const int leaf = leaves[i];
-        if (cmask && !cmask[leaf]) continue;  // x_hat exchange: this rank's column leaves only
-        fwd_off.push_back((int64_t)rec.size());
-        rec.insert(rec.end(), {cstart[leaf], csize[leaf], crank[leaf], cvoff[leaf], cxoff[leaf], 0, 0});
-        const size_t hdr = rec.size() - kFwdHead;
+    // A: forward records: fixed-stride headers (with the leaf's first 64 x
+    // indices), then per task the levels it climbs as the right child
+    std::vector<int> fleaves;
+    for (int i = 0; i < L.c_leaves; ++i)
+        if (!cmask || cmask[leaves[i]]) fleaves.push_back(leaves[i]);  // x_hat exchange: this rank's column leaves only
+    std::vector<int64_t> cperm;
+    H2B_CUDA_TRY(fetch(L.col_perm, L.n_cols, cperm));
+    rec.assign((size_t)kFwdStride * fleaves.size(), 0);
+    for (size_t fi = 0; fi < fleaves.size(); ++fi) {
+        const int leaf = fleaves[fi];
+        fwd_off.push_back((int64_t)(kFwdStride * fi));
+        const size_t hdr = (size_t)kFwdStride * fi;
+        {
+            const int64_t h[kFwdHead] = {cstart[leaf], csize[leaf], crank[leaf], cvoff[leaf], cxoff[leaf], 0, 0,
+                                         (int64_t)rec.size()};
+            std::copy(h, h + kFwdHead, rec.begin() + hdr);
+            int32_t ix[2 * (kFwdStride - kFwdHead)] = {0};
+            for (int r = 0; r < std::min<int>(csize[leaf], 2 * (kFwdStride - kFwdHead)); ++r) {
+                const int64_t q = cperm[(size_t)cstart[leaf] + r];
+                if (q < 0 || q > INT32_MAX) return fail(H2B_ERR_INVALID, "h2b_plan_create: column index out of range");
+                ix[r] = (int32_t)q;
+            }
+            std::memcpy(rec.data() + hdr + kFwdHead, ix, sizeof(ix));
+        }
         bool warp_ok = crank[leaf] <= 32 && csize[leaf] <= 64 &&
                        (int64_t)csize[leaf] * crank[leaf] * 8 <= stage;
         int node = leaf, n = 0;
@@ -1898,6 +1964,8 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags, const i
         return n;
     };
     int n_cpl = 0;
+    int64_t pack_len = 0;             // doubles in the packed downward-step operands
+    std::vector<int64_t> pack_desc;   // per step: e_off (-1), k, k_parent, v_off (-1), size, pack offset
     // Coupling bands of cluster u: all but the last to `early`; the last one
     // (an empty band when u has no couplings) runs u's downward step and goes
     // to `late`.
@@ -1923,8 +1991,14 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags, const i
             dw[23] = u;  // (plan building only)
             const int kk = rrank[u], kq = par >= 0 ? rrank[par] : 0;
             const bool lf = rvoff[u] >= 0;
-            dw[18] = (kk <= 32 && kq <= 32 && (!lf || rsize[u] <= 64) &&
-                      8 * ((((int64_t)kk * kq + 1) & ~int64_t(1)) + (lf ? (int64_t)rsize[u] * kk : 0)) <= stage)
+            // packed operands of the step: E_u^T (kq x kk), then V_u^T (kk x |u|)
+            const int64_t ne = ((int64_t)kk * kq + 1) & ~int64_t(1);
+            const int64_t nv = lf ? (((int64_t)rsize[u] * kk + 1) & ~int64_t(1)) : 0;
+            dw[21] = pack_len;
+            dw[22] = 8 * (ne + nv);
+            pack_desc.insert(pack_desc.end(), {par >= 0 ? reoff[u] : -1, kk, kq, lf ? rvoff[u] : -1, rsize[u], pack_len});
+            pack_len += ne + nv;
+            dw[18] = (kk <= 32 && kq <= 32 && (!lf || rsize[u] <= 64) && 8 * (ne + nv) <= stage)
                          ? 1 : 0;  // one-warp downward step
         }
         std::vector<int64_t> tmp;
@@ -2035,6 +2109,22 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags, const i
     if (!fwd_off.empty())
         H2B_CUDA_TRY(cudaMemcpy(p->fwd_off, fwd_off.data(), sizeof(int64_t) * fwd_off.size(), cudaMemcpyHostToDevice));
     p->n_fwd = (int)fwd_off.size();
+    {
+        // the downward steps' operands, transposed once (plan-owned copy)
+        H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->dpack), 8 * (size_t)pack_len));
+        H2B_CUDA_TRY(cudaMemset(p->dpack, 0, 8 * (size_t)std::max<int64_t>(pack_len, 2)));
+        const int64_t nd = (int64_t)pack_desc.size() / 6;
+        if (nd > 0) {
+            int64_t* d_desc = nullptr;
+            H2B_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&d_desc), 8 * pack_desc.size()));
+            H2B_CUDA_TRY(cudaMemcpy(d_desc, pack_desc.data(), 8 * pack_desc.size(), cudaMemcpyHostToDevice));
+            k_pack_descent<<<(unsigned)nd, 128>>>(L.r_E, L.r_V, d_desc, p->dpack);
+            cudaError_t e = cudaGetLastError();
+            if (e == cudaSuccess) e = cudaDeviceSynchronize();
+            cudaFree(d_desc);
+            H2B_CUDA_TRY(e);
+        }
+    }
     if (cmask) {
         p->xmode = true;
         H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->xhat_f), 16 * (size_t)L.xhat_len));
@@ -2181,7 +2271,7 @@ extern "C" int h2b_debug_stuck(h2b_plan* p, unsigned long long* out) {
 extern "C" int h2b_plan_destroy(h2b_plan* p) {
     if (!p) return ok();
     void* bufs[] = {p->xhat, p->ycpl, p->yfin, p->ynear, p->ctrl, p->rec,  p->fwd_off, p->dx,
-                    p->dy,   p->trace, p->xll, p->dsym,  p->gsym, p->ppart, p->nsum, p->xgath,
+                    p->dy,   p->trace, p->xll, p->dsym, p->dpack,  p->gsym, p->ppart, p->nsum, p->xgath,
                     p->xhat_f, p->d_own, p->d_own_off, p->d_imp, p->d_imp_src, p->d_span, p->span_val};
     for (void* q : bufs)
         if (q) cudaFree(q);
@@ -2226,6 +2316,7 @@ int launch_matvec(h2b_plan* p, const double* d_x, const double* xh, double* y, c
     a.gsym = p->gsym;
     a.ppart = p->ppart;
     a.nsum = p->nsum;
+    a.dpack = p->dpack;
     a.yh = yh;
     a.n_out = yh ? (int)((p->L.n_rows + kCopyChunk - 1) / kCopyChunk) : 0;
     a.n_leaf = p->n_leaf;
