@@ -50,6 +50,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "device_common.cuh"
@@ -179,12 +180,17 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 
 #ifdef H2B_LL_TIMEOUT
-__device__ unsigned long long g_mbar_stuck[2];
+__device__ unsigned long long g_mbar_stuck[4];  // block + 1, parity, abandoned waits, longest wait (ns)
 #endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #ifdef H2B_LL_TIMEOUT
-    // debug builds: an abandoned wait is recorded instead of hanging the GPU
-    for (long long it = 0;; ++it) {
+    // debug builds: a wait abandoned after 2 s is recorded instead of hanging
+    // the GPU, and the longest wait is kept.  (The bound is on time: a bare
+    // test_wait loop bounded by an iteration count reported waits that the
+    // polling itself had slowed down.)
+    unsigned long long t0, t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (true) {
         uint32_t ok;
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
@@ -193,10 +199,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             : "=r"(ok)
             : "r"(smem_u32(bar)), "r"(parity)
             : "memory");
-        if (ok) return;
-        if (it > (1ll << 20)) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (ok) {
+            atomicMax(&g_mbar_stuck[3], t1 - t0);
+            return;
+        }
+        if (t1 - t0 > 2000000000ull) {
             g_mbar_stuck[0] = blockIdx.x + 1;
             g_mbar_stuck[1] = parity;
+            atomicAdd(&g_mbar_stuck[2], 1ull);
             return;
         }
     }
@@ -554,6 +565,7 @@ struct Shared {
     uint32_t parity;           // mbarrier phase of the staging slot in use
     bool issued;               // band bulk copy already issued by the caller
     const double* dpack;       // downward-step operands [E_t^T | V_t^T] per cluster (plan-owned copy)
+    int64_t pf;                // this thread's partial vector to pull into L2 (leaf final tasks), or -1
 };
 
 // x[i]: from the LL copy made by this launch's copy tasks (host input) or
@@ -913,6 +925,10 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
             mbar_expect_tx(s.bar, pbytes);
             bulk_g2s(Es, s.dpack + d[13], pbytes, s.bar);
         }
+        // (the rows' output indices now: their latency would sit at the very end of the task)
+        int64_t rp0 = 0, rp1 = 0;
+        if (leaf && lane < size) rp0 = __ldg(row_perm + start + lane);
+        if (leaf && lane + 32 < size) rp1 = __ldg(row_perm + start + lane + 32);
         double v = (has_cpl && lane < k) ? ll_load(ycpl + 2 * (yoff + lane), epoch) : 0.0;
         if (par_off >= 0 && lane < kp) s.rhs[lane] = ll_load(yfin + 2 * (par_off + lane), epoch);
         if (pbytes) mbar_wait(s.bar, par);
@@ -946,7 +962,7 @@ __device__ void descent(const double* __restrict__ r_E, const double* __restrict
                 a1 = fma(Vt[(r + 1) * size + i], s.vb[r + 1], a1);
             }
             if (r < k) a0 = fma(Vt[r * size + i], s.vb[r], a0);
-            y[__ldg(row_perm + start + i)] =
+            y[i < 32 ? rp0 : rp1] =
                 (sym ? s.yn[i] : ll_load(ynear + 2 * ((int64_t)start + i), epoch)) + (a0 + a1);
         }
         return;
@@ -1086,6 +1102,12 @@ __device__ void task_band(const h2b_layout& L, const double* __restrict__ x, con
             else
                 gather(s.rhs, x, L.d_gidx + gi_off, cols);
         mark(s.mark, 1);
+        if (kCoupling && s.pf >= 0) {
+            // leaf final: its nearfield partial vectors (|t| LL words each) into L2 for near_sum
+            const char* q = reinterpret_cast<const char*>(s.ppart + 2 * s.pf);
+            const int lines = ((int)s.rec[16] * 16 + 127) / 128 + 1;
+            for (int l = 0; l < lines; ++l) asm volatile("prefetch.global.L2 [%0];" ::"l"(q + 128 * l));
+        }
         mbar_wait(s.bar, s.parity);
         __syncthreads();
         mark(s.mark, 2);
@@ -1341,6 +1363,13 @@ __device__ __forceinline__ void run_task(const KArgs& a, const double* __restric
         // (the bulk copy after the band's product then hits L2)
         if (kind == kKindCpl && s.rec[5] && s.rec[22] > 0 && threadIdx.x == 32)
             bulk_prefetch_l2(a.dpack + s.rec[21], (uint32_t)s.rec[22]);
+        // ... and a leaf's nearfield partial vectors (symmetric nearfield; summed by
+        // near_sum after the band's product): list entry m -> the |t| LL words at
+        // ppart + 2 list[m], one 128-byte line per 8 rows
+        // (the list entry is loaded here and used after the band's gather is under way, task_band)
+        s.pf = -1;
+        if (kind == kKindCpl && s.rec[5] && a.ppart && s.rec[13] && (int)threadIdx.x < (int)s.rec[20])
+            s.pf = __ldg(a.nsum + s.rec[19] + threadIdx.x);
         if (kind == kKindNearSym)
             task_panel(a.dsym, a.gsym, x, a.ppart, epoch, s);
         else if (kind == kKindNear)
@@ -2260,10 +2289,12 @@ extern "C" int h2b_debug_stuck(h2b_plan* p, unsigned long long* out) {
     out[5] = reinterpret_cast<unsigned long long>(p->yfin);
     out[6] = reinterpret_cast<unsigned long long>(p->ynear);
     out[7] = h[3];  // the word found at the abandoned address
-    unsigned long long mb[2];
+    unsigned long long mb[4];
     H2B_CUDA_TRY(cudaMemcpyFromSymbol(mb, g_mbar_stuck, sizeof(mb)));
     out[8] = mb[0];
     out[9] = mb[1];
+    out[10] = mb[2];  // abandoned mbarrier waits
+    out[11] = mb[3];  // longest mbarrier wait (ns)
     return 0;
 }
 #endif
@@ -2338,6 +2369,28 @@ int launch_matvec(h2b_plan* p, const double* d_x, const double* xh, double* y, c
     return ok();
 }
 
+// memcpy over several host threads (a pageable x of config 3 is 16.8 MB: ~1 ms
+// on one core, which was a fifth of the end-to-end matvec)
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+    const unsigned hw = std::thread::hardware_concurrency();
+    const int nt = bytes < (size_t(2) << 20) ? 1 : (int)std::min<unsigned>(8, std::max(1u, hw));
+    if (nt <= 1) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    const size_t per = ((bytes + nt - 1) / nt + 4095) & ~size_t(4095);
+    std::vector<std::thread> th;
+    for (int i = 1; i < nt; ++i) {
+        const size_t o = per * i;
+        if (o >= bytes) break;
+        th.emplace_back([=] {
+            std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, std::min(per, bytes - o));
+        });
+    }
+    std::memcpy(dst, src, std::min(per, bytes));
+    for (auto& t : th) t.join();
+}
+
 // device-accessible pointer of pinned (page-locked, mapped) host memory, or null
 const void* mapped(const void* h) {
     cudaPointerAttributes at;
@@ -2367,7 +2420,7 @@ extern "C" int h2b_matvec_host(h2b_plan* p, const double* h_x, double* h_y, void
     cudaStream_t st = as_stream(stream);
     const double* xh = static_cast<const double*>(mapped(h_x));
     if (!xh) {
-        std::memcpy(p->hx, h_x, sizeof(double) * p->L.n_cols);
+        par_memcpy(p->hx, h_x, sizeof(double) * p->L.n_cols);
         xh = static_cast<const double*>(mapped(p->hx));
     }
     double* yh = static_cast<double*>(const_cast<void*>(mapped(h_y)));
@@ -2376,7 +2429,7 @@ extern "C" int h2b_matvec_host(h2b_plan* p, const double* h_x, double* h_y, void
     if (!xh || !yh) return fail(H2B_ERR_CUDA, "h2b_matvec_host: pinned staging is not device-mapped");
     if (int rc = launch_matvec(p, nullptr, xh, p->dy, st, yh)) return rc;
     H2B_CUDA_TRY(cudaStreamSynchronize(st));
-    if (staged_y) std::memcpy(h_y, p->hy, sizeof(double) * p->L.n_rows);
+    if (staged_y) par_memcpy(h_y, p->hy, sizeof(double) * p->L.n_rows);
     return ok();
 }
 

@@ -1,4 +1,4 @@
-"""Where the end-to-end (numpy in / numpy out) matvec time goes at config 1."""
+"""Where the end-to-end (numpy in / numpy out) matvec time goes (config from argv, default 1)."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
@@ -8,7 +8,7 @@ import bench
 from paper_2001_05523_b200 import _lib
 from paper_2001_05523_b200.containers import H2Matrix, assemble_couplings, near_layout
 
-cfg = bench.CONFIGS["1"]
+cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "1"]
 mesh, ctx, tree, bt, basis = bench.build_problem(cfg, os.cpu_count() or 8)
 lay = near_layout(bt)
 Dn = torch.zeros(max(lay.total, 1), dtype=torch.float64, device="cuda")
@@ -22,7 +22,11 @@ xd = torch.from_numpy(xh).cuda()
 L = _lib.lib()
 
 
-def wall(fn, reps=300):
+REPS = 300 if cfg["level"] <= 6 else 40
+
+
+def wall(fn, reps=None):
+    reps = reps or REPS
     for _ in range(10):
         fn()
     torch.cuda.synchronize()
@@ -55,3 +59,22 @@ def copies():
 
 
 print("H2D + device + D2H (torch)  ", wall(copies))
+
+
+xpage = np.array(xh)
+
+
+def copies_pageable():
+    xd.copy_(torch.from_numpy(xpage))
+    y = plan.apply_device(xd)
+    out = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    out.copy_(y, non_blocking=True)
+    torch.cuda.synchronize()
+    return out.numpy()
+
+
+print("pageable H2D (torch) + device + D2H pinned ", wall(copies_pageable))
+t0 = time.perf_counter()
+for _ in range(20):
+    z = np.array(xh)
+print("numpy copy of x (one core)  ", f"{(time.perf_counter() - t0) / 20 * 1e6:.1f} us")

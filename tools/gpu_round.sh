@@ -1,9 +1,13 @@
-# Session check on one B200 (run under gpurun): matvec tests, task trace, timings.
-R=${1:-r02af}
+R=${1:-r02ap}
 OUT=gpurun_out
 mkdir -p $OUT
 set -x
-timeout 1500 python -m pytest tests/test_gpu_matvec.py tests/test_gpu_sharded.py tests/test_gpu_parity_large.py tests/test_gpu_symmetric.py tests/test_gpu_dropin.py -m gpu -q -x > $OUT/${R}_pytest.log 2>&1; echo "pytest rc=$?" >> $OUT/${R}_pytest.log
-timeout 900 python tools/mv_trace.py 3 > $OUT/${R}_trace.txt 2>&1
-for c in 1 2 3; do timeout 900 python tools/mv_time.py $c 2>&1 | grep -v "^plan" >> $OUT/${R}_mvtime.txt; done
-tail -n 3 $OUT/${R}_pytest.log; head -8 $OUT/${R}_trace.txt; tail -5 $OUT/${R}_mvtime.txt
+V=$PWD/paper_2001_05523_b200/_lib/variants
+H2B_LIB_PATH=$V/tail.so timeout 900 python -m pytest tests/test_gpu_matvec.py tests/test_gpu_symmetric.py -m gpu -q -x > $OUT/${R}_pytest_tail.log 2>&1; echo "pytest rc=$?" >> $OUT/${R}_pytest_tail.log
+for c in 1 2s 3; do
+  for v in main tail main tail; do
+    if [ $v = main ]; then L=$PWD/paper_2001_05523_b200/_lib/libh2b.so; else L=$V/$v.so; fi
+    echo "config $c $v: $(H2B_LIB_PATH=$L timeout 900 python tools/mv_time.py $c 2>&1 | grep '^matvec')" >> $OUT/${R}_mvtime.txt
+  done
+done
+tail -3 $OUT/${R}_pytest_tail.log; cat $OUT/${R}_mvtime.txt
