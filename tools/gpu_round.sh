@@ -1,13 +1,17 @@
-R=${1:-r02ap}
+R=${1:-r02ar}
 OUT=gpurun_out
 mkdir -p $OUT
 set -x
 V=$PWD/paper_2001_05523_b200/_lib/variants
-H2B_LIB_PATH=$V/tail.so timeout 900 python -m pytest tests/test_gpu_matvec.py tests/test_gpu_symmetric.py -m gpu -q -x > $OUT/${R}_pytest_tail.log 2>&1; echo "pytest rc=$?" >> $OUT/${R}_pytest_tail.log
+for c in 1 3; do H2B_LIB_PATH=$V/dbg_fs.so timeout 300 python tools/ll_debug.py $c 2>&1 | grep "stuck\|launch" > $OUT/${R}_lldebug_$c.txt; done
+cat $OUT/${R}_lldebug_*.txt
+if grep -q "stuck addr 0x0 .*abandoned 0" $OUT/${R}_lldebug_1.txt && grep -q "stuck addr 0x0 .*abandoned 0" $OUT/${R}_lldebug_3.txt; then
+H2B_LIB_PATH=$V/fs2k_i50.so timeout 900 python -m pytest tests/test_gpu_matvec.py tests/test_gpu_symmetric.py tests/test_gpu_sharded.py -m gpu -q -x > $OUT/${R}_pytest.log 2>&1; echo "pytest rc=$?" >> $OUT/${R}_pytest.log
 for c in 1 2s 3; do
-  for v in main tail main tail; do
+  for v in main fs2k fs2k_i50 fs4k_i30; do
     if [ $v = main ]; then L=$PWD/paper_2001_05523_b200/_lib/libh2b.so; else L=$V/$v.so; fi
     echo "config $c $v: $(H2B_LIB_PATH=$L timeout 900 python tools/mv_time.py $c 2>&1 | grep '^matvec')" >> $OUT/${R}_mvtime.txt
   done
 done
-tail -3 $OUT/${R}_pytest_tail.log; cat $OUT/${R}_mvtime.txt
+fi
+tail -3 $OUT/${R}_pytest.log; cat $OUT/${R}_mvtime.txt
