@@ -416,7 +416,11 @@ typedef struct h2b_plan h2b_plan;
  * NULL) whose row and column trees coincide and whose nearfield blocks satisfy
  * D_(t,s) == D_(s,t)^T bit for bit (checked on the device) packs a copy of the
  * upper blocks and streams each block pair once; later changes to D are not
- * seen by such a plan (create a new one).  Environment knobs read here (test
+ * seen by such a plan (create a new one).  Every plan also owns a transposed
+ * copy of the row basis it applies ([E_t^T | V_t^T] per row cluster,
+ * 8 (sum |V_t| + sum |E_t|) bytes: the operands of the downward steps in the
+ * layout their products read, staged by one bulk copy each); later changes
+ * to r_V / r_E are likewise not seen.  Environment knobs read here (test
  * and diagnostics only): H2B_NEAR_SYM=0 (stream every block, one-sided),
  * H2B_TRACE=1 (per-task timeline).
  * A plan owns one ticket counter and one set of inter-CTA scratch buffers, so

@@ -81,6 +81,8 @@ constexpr int kFwdStride = 40;  // forward records are fixed-stride (record = ti
 constexpr int kFwdLevel = 6;    // k0, kp, e_off_c0, e_off_own, xhat_off_c0, xhat_off_parent
 constexpr int kCopyChunk = 1024;  // x values per copy task (host-input launches)
 constexpr int kKindNear = 0, kKindCpl = 1;  // band record kinds (word 7)
+constexpr int kFwdAhead = 2048;              // forward tasks pull the record of the task this many tickets on into L2
+constexpr int64_t kUpfrontMax = 24 << 20;   // records + gather lists prefetched up front when at most this many bytes
 // symmetric nearfield band (see task_panel): words 8..10 = offset of the
 // transposed outputs (column c -> 8 + c), leading diagonal-block columns
 // without a transposed output, gather offset of the row leaf's own x
@@ -223,10 +225,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 
 // 1-D TMA bulk copy global -> shared (16-byte aligned, size % 16 == 0)
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    // operator bytes are read once per matvec: evict-first in L2, so the
+    // stream does not push out what is reused (x, x_hat, partials, records);
+    // config 1 51.6 -> 49.6 us, larger configurations neutral
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
             smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
 }
 
@@ -516,6 +523,8 @@ __device__ __forceinline__ void gather(double* rhs, const double* __restrict__ s
 // entries whose producer has not published yet)
 __device__ __forceinline__ void gather_ll(double* rhs, const uint64_t* ll, const int32_t* idx, int n,
                                           uint32_t epoch) {
+    uint64_t pol_el;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_el));
     constexpr int kU = 1024 / kThreads;
     for (int base = 0; base < n; base += kU * kThreads) {
         int ix[kU];
@@ -529,9 +538,9 @@ __device__ __forceinline__ void gather_ll(double* rhs, const uint64_t* ll, const
         for (int u = 0; u < kU; ++u) {
             w0[u] = w1[u] = 0;
             if (ix[u] >= 0)
-                asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];"
+                asm volatile("ld.relaxed.gpu.global.L2::cache_hint.v2.b64 {%0, %1}, [%2], %3;"
                              : "=l"(w0[u]), "=l"(w1[u])
-                             : "l"(ll + 2 * (int64_t)ix[u]));
+                             : "l"(ll + 2 * (int64_t)ix[u]), "l"(pol_el));
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
@@ -1350,10 +1359,15 @@ __device__ __forceinline__ void run_task(const KArgs& a, const double* __restric
     if (ticket < tB) {
         // pull the band records, the nearfield gather lists and x into L2 for
         // the streaming tasks that follow (fire-and-forget; LL needs no fences)
+        // (records and lists only when they fit L2 beside everything else:
+        // launch_matvec passes zero lengths otherwise)
         prefetch_slice(reinterpret_cast<const double*>(a.rec + a.band_base), a.band_bytes, ticket, a.n_fwd);
         prefetch_slice(reinterpret_cast<const double*>(a.dsym ? a.gsym : L.d_gidx), a.dgidx_bytes, ticket,
                        a.n_fwd);
         if (!a.xh) prefetch_slice(x, 8 * L.n_cols, ticket, a.n_fwd);
+        // the record of the forward task kFwdAhead tickets on (no dependent load)
+        if (threadIdx.x == 64 && ticket + kFwdAhead < a.n_fwd)
+            bulk_prefetch_l2(a.rec + (int64_t)kFwdStride * (ticket + kFwdAhead), 8 * kFwdStride);
         task_forward(L.c_V, L.c_E, L.col_perm, a.rec + (int64_t)kFwdStride * ticket, x, a.xhat, epoch, s, a.rec);
     } else {
         const int b = ticket - tB;
@@ -2328,6 +2342,11 @@ int launch_matvec(h2b_plan* p, const double* d_x, const double* xh, double* y, c
     a.band_base = p->band_base;
     a.band_bytes = 8 * (int64_t)kBandWords * (p->n_near + p->n_cpl);
     a.dgidx_bytes = p->dgidx_bytes;
+    // The forward tasks pull the band records and nearfield gather lists into
+    // L2 up front only when these are small: at config 1 (2 MB) that saves 4 %,
+    // at configs 2 and 3 (70 / 190 MB against a 126 MB L2 that also holds x,
+    // x_hat and the partial vectors) it costs 2 % (same-box A/B).
+    if (a.band_bytes + a.dgidx_bytes > kUpfrontMax) a.band_bytes = a.dgidx_bytes = 0;
     a.n_near = p->n_near;
     a.n_cpl = p->n_cpl;
     a.max_cols = p->max_cols;
