@@ -527,8 +527,17 @@ __device__ __forceinline__ bool shares_vertex(const int* ra, const int* cb) {
 
 __device__ __forceinline__ int64_t touch_find(const int64_t* __restrict__ row_ptr,
                                               const int32_t* __restrict__ col, int a, int b) {
-    for (int64_t p = row_ptr[a]; p < row_ptr[a + 1]; ++p)
-        if (col[p] == b) return p;
+    // (a row holds the ~12 panels touching panel a: eight independent loads
+    // per step instead of one dependent load per entry)
+    const int64_t p0 = row_ptr[a], p1 = row_ptr[a + 1];
+    for (int64_t p = p0; p < p1; p += 8) {
+        int c[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) c[u] = p + u < p1 ? __ldg(col + p + u) : -1;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (c[u] == b) return p + u;
+    }
     return -1;
 }
 
