@@ -1,7 +1,11 @@
-R=${1:-r02aw}
+R=${1:-r02az}
 OUT=gpurun_out
 mkdir -p $OUT
 set -x
-timeout 1500 python -m pytest tests/test_gpu_quadrature.py tests/test_gpu_scale.py tests/test_gpu_symmetric.py tests/test_hyp.py -m gpu -q -x > $OUT/${R}_pytest.log 2>&1; echo "pytest rc=$?" >> $OUT/${R}_pytest.log
-timeout 1200 python bench.py --no-cpu-baseline > $OUT/${R}_bench.json 2> $OUT/${R}_bench.log; echo "bench rc=$?" >> $OUT/${R}_bench.log
-tail -n 3 $OUT/${R}_pytest.log; tail -n 2 $OUT/${R}_bench.log
+V=$PWD/paper_2001_05523_b200/_lib/variants
+for c in 1 2s 3; do
+  for v in prev p0s32 p0s128 p0s512 p1s128 p1s512; do
+    echo "config $c $v: $(H2B_LIB_PATH=$V/$v.so timeout 900 python tools/mv_time.py $c 2>&1 | grep '^matvec')" >> $OUT/${R}_mvtime.txt
+  done
+done
+cat $OUT/${R}_mvtime.txt
