@@ -1,4 +1,4 @@
-R=${1:-r02ba}
+R=${1:-r02bb}
 OUT=gpurun_out
 mkdir -p $OUT
 set -x
