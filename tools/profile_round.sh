@@ -2,7 +2,7 @@
 # Round profiling on one B200 (run under gpurun).  Plain runs first (each must
 # exit 0), then the launch list and one full ncu capture per hot kernel.
 #   bash tools/profile_round.sh r02f
-R=${1:-r02aq}
+R=${1:-r02bd}
 OUT=gpurun_out
 mkdir -p $OUT
 set -x
