@@ -402,17 +402,24 @@ def run_ours(args, cfg):
         for _ in range(3):
             H.matvec(xh)
         ke = max(10, min(K, 50))
+        each = []
         t1 = time.perf_counter()
         for _ in range(ke):
+            t2 = time.perf_counter()
             yh = H.matvec(xh)
+            each.append(time.perf_counter() - t2)
         dt = time.perf_counter() - t1
         xpin = torch.from_numpy(x_host).pin_memory().numpy()
+        for _ in range(3):
+            H.matvec(xpin)
         t1 = time.perf_counter()
         for _ in range(ke):
             H.matvec(xpin)
         dtp = time.perf_counter() - t1
         e2e = {"value": n * ke / dt, "unit": "DoF/s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
                "timer": "host wall clock around H2Matrix.matvec(numpy, pageable) incl. H2D/D2H, synchronised",
+               "calls": ke, "ms_per_call": {"mean": dt / ke * 1e3, "median": float(np.median(each)) * 1e3,
+                                            "min": float(np.min(each)) * 1e3, "max": float(np.max(each)) * 1e3},
                "pinned_input_value": n * ke / dtp}
         del yh
     else:

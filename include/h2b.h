@@ -223,6 +223,22 @@ int h2b_dlp_jobs_copy(const h2b_dlp_build* b, int64_t* jobs, int32_t* row_idx, i
                       int32_t* inc, int64_t* inc_base);
 int h2b_dlp_jobs_free(h2b_dlp_build* b);
 
+/* Host-side job list of h2b_pair_blocks_slp for a list of n blocks
+ * (t, s) = h_uids[i] (n x 2): rows h_row_off[t] .. + h_row_cnt[t] of the row
+ * index list, columns h_col_off[s] .. + h_col_cnt[s] of the column index list,
+ * written at h_blk_off[i] with leading dimension h_blk_ld[i] (the packed
+ * layouts of containers.py:79-98 nearfield / gca.py:194-205 couplings).
+ * h2b_block_partners: for every block the index of block (s, t), or -1.
+ * h2b_block_jobs with mirrored != 0 (symmetric single layer, block (s, t) =
+ * block (t, s)^T) keeps one job per block pair, which also writes the
+ * transpose at the partner's place; h_jobs holds 8 n words, *h_n_jobs jobs
+ * are written. */
+int h2b_block_partners(int64_t n, const int64_t* h_uids, int64_t* h_partner);
+int h2b_block_jobs(int64_t n, const int64_t* h_uids, const int64_t* h_row_off, const int64_t* h_row_cnt,
+                   const int64_t* h_col_off, const int64_t* h_col_cnt, const int64_t* h_blk_off,
+                   const int64_t* h_blk_ld, int mirrored, const int64_t* h_partner, int64_t* h_jobs,
+                   int64_t* h_n_jobs);
+
 /* ================= GCA cluster-basis construction (device) ================= */
 
 /* Basis flavors (gca.P0_SLP / gca.P1_DLP): P0 rows are panels (potentials

@@ -113,6 +113,7 @@ EXPORTS = (
     "h2b_comm_unique_id", "h2b_comm_init", "h2b_comm_destroy", "h2b_plan_set_comm", "h2b_matvec_sharded",
     "h2b_cluster_tree_device", "h2b_block_tree_device",
     "h2b_gca_columns_curl", "h2b_plan_create_xhat", "h2b_xhat_info", "h2b_xhat_set_import", "h2b_xhat_forward", "h2b_xhat_main",
+    "h2b_block_partners", "h2b_block_jobs",
 )
 
 _lib = None
@@ -162,6 +163,8 @@ def lib():
         L.h2b_dlp_jobs_build.argtypes = [ctypes.c_int64, vp, vp, vp, ctypes.c_int64, vp, vp, vp, vp, vp, vp,
                                          ctypes.POINTER(vp)]
         L.h2b_dlp_jobs_sizes.argtypes = [vp, vp]
+        L.h2b_block_partners.argtypes = [ctypes.c_int64, vp, vp]
+        L.h2b_block_jobs.argtypes = [ctypes.c_int64, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int, vp, vp, vp]
         L.h2b_dlp_jobs_copy.argtypes = [vp, vp, vp, vp, vp, vp, vp]
         L.h2b_dlp_jobs_free.argtypes = [vp]
         L.h2b_gca_columns.argtypes = [ctypes.POINTER(Mesh), vp, ctypes.c_int32, vp, ctypes.c_int,

@@ -21,7 +21,7 @@ OBJ_DIR = os.path.join(OUT_DIR, "obj")
 LIB = os.path.join(OUT_DIR, "libh2b.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["errors.cpp", "structure.cpp", "dlp_jobs.cpp", "comm.cpp", "quadrature.cu", "matvec.cu", "gca.cu", "solver.cu",
+SOURCES = ["errors.cpp", "structure.cpp", "dlp_jobs.cpp", "block_jobs.cpp", "comm.cpp", "quadrature.cu", "matvec.cu", "gca.cu", "solver.cu",
            "matmat.cu", "basis.cu", "tree_dev.cu"]
 HEADERS = ["h2b_internal.h", "device_common.cuh", "nccl_api.h"]
 

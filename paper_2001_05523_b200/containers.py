@@ -243,9 +243,8 @@ def near_slp_jobs(bt):
     lay = near_layout(bt)
     rt, ct = bt.row_tree, bt.col_tree
     nu = bt.near_uids
-    jobs = np.stack([rt.start[nu[:, 0]], lay.blk_rows, ct.start[nu[:, 1]], lay.blk_cols, lay.blk_off, lay.blk_ld],
-                    axis=1)
-    return kernels.mirror_jobs(jobs, nu, _partners(bt, "near")) if _symmetric_trees(bt) else jobs
+    return kernels.block_jobs(nu, rt.start, rt.end - rt.start, ct.start, ct.end - ct.start, lay.blk_off, lay.blk_ld,
+                              _partners(bt, "near") if _symmetric_trees(bt) else None)
 
 
 def assemble_nearfield_device(ctx, kind, bt, q, q_singular=None, cache=None):
@@ -407,11 +406,9 @@ def coupling_slp_jobs(bt, row_basis, col_basis):
         d_off, d_ld = _dst_map(len(ff), bt.far_index, lay.blk_off, lay.blk_ld)
         jobs = kernels.mirror_jobs_owned(geom, ff, d_off, d_ld, _partners(full, "far"))
     else:
-        jobs = np.stack([roff[fu[:, 0]], lay.blk_rows, coff[fu[:, 1]], lay.blk_cols, lay.blk_off, lay.blk_ld],
-                        axis=1)
-        if sym:
-            # S_(s,t) = G[piv_s, piv_t] = S_(t,s)^T: one job per block pair
-            jobs = kernels.mirror_jobs(jobs, fu, _partners(bt, "far"))
+        # symmetric: S_(s,t) = G[piv_s, piv_t] = S_(t,s)^T, one job per block pair
+        jobs = kernels.block_jobs(fu, roff[:-1], rr, coff[:-1], cr, lay.blk_off, lay.blk_ld,
+                                  _partners(bt, "far") if sym else None)
     return jobs, rpiv.astype(np.int32), cpiv.astype(np.int32), lay
 
 

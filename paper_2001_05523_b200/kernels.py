@@ -269,7 +269,35 @@ def tile_jobs(jobs):
 
 def block_partners(uids):
     """For every block (t, s) of a block list (n, 2), the index of block (s, t)
-    in the same list, or -1; a diagonal block is its own partner."""
+    in the same list, or -1; a diagonal block is its own partner.  Native
+    (h2b_block_partners); same output as _block_partners_py."""
+    uids = np.ascontiguousarray(uids, dtype=np.int64).reshape(-1, 2)
+    out = np.empty(len(uids), dtype=np.int64)
+    _lib.check(_lib.lib().h2b_block_partners(len(uids), _lib.ptr(uids), _lib.ptr(out)))
+    return out
+
+
+def block_jobs(uids, row_off, row_cnt, col_off, col_cnt, blk_off, blk_ld, partner=None):
+    """(m, 8) pair-block jobs of the blocks (t, s) = uids[i]: rows
+    row_off[t] .. + row_cnt[t], columns col_off[s] .. + col_cnt[s], stored at
+    blk_off[i] / blk_ld[i].  With `partner` (block_partners of uids; symmetric
+    single layer) one job per block pair that also writes the mirror -- the
+    output of mirror_jobs on the stacked job columns, built in one native pass
+    (h2b_block_jobs)."""
+    c = lambda a: np.ascontiguousarray(a, dtype=np.int64)
+    uids = c(uids).reshape(-1, 2)
+    n = len(uids)
+    arrs = [c(a) for a in (row_off, row_cnt, col_off, col_cnt, blk_off, blk_ld)]
+    part = c(partner) if partner is not None else None
+    jobs = np.empty((n, 8), dtype=np.int64)
+    m = np.zeros(1, dtype=np.int64)
+    _lib.check(_lib.lib().h2b_block_jobs(n, _lib.ptr(uids), *(_lib.ptr(a) for a in arrs), int(part is not None),
+                                         _lib.ptr(part), _lib.ptr(jobs), _lib.ptr(m)))
+    return jobs[: int(m[0])]
+
+
+def _block_partners_py(uids):
+    """numpy restatement of block_partners (tests)."""
     uids = np.asarray(uids, dtype=np.int64).reshape(-1, 2)
     n = len(uids)
     if n == 0:

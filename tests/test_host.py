@@ -212,3 +212,44 @@ def test_gca_pivots_bit_exact_cube_shell():
     b = gca.build_basis(AssemblyContext(m), t0, gca.P0_SLP, 3, 1e-4, threads=4)
     assert np.array_equal(np.array([b.rank[u] for u in range(t0.n_nodes)]), g["slp_ranks"])
     assert np.array_equal(np.concatenate([b.pivots[u] for u in range(t0.n_nodes)]), g["slp_pivots"])
+
+
+def test_native_block_jobs_match_numpy_restatement():
+    """h2b_block_partners / h2b_block_jobs (one native pass) against the numpy
+    chain they replace (block partners by sort + search, stacked job columns,
+    mirror_jobs), on the sphere level-4 block tree with made-up ranks: far
+    blocks (coupling jobs) and near blocks, mirrored and one-sided."""
+    from paper_2001_05523_b200 import clustering, kernels, mesh, spaces
+
+    m = mesh.sphere_mesh(4)
+    tree = clustering.build_cluster_tree(spaces.DofSpace(spaces.P0, m).support_boxes(), 16)
+    bt = clustering.BlockTree(tree, tree, 1.2)
+    rng = np.random.default_rng(5)
+    rank = rng.integers(3, 20, tree.n_nodes).astype(np.int64)
+    off = np.zeros(tree.n_nodes + 1, dtype=np.int64)
+    np.cumsum(rank, out=off[1:])
+    for uids, r_off, r_cnt in ((bt.far_uids, off[:-1], rank), (bt.near_uids, tree.start, tree.end - tree.start)):
+        uids = np.asarray(uids, dtype=np.int64)
+        part = kernels.block_partners(uids)
+        assert np.array_equal(part, kernels._block_partners_py(uids))
+        assert (part >= 0).all()  # one tree on both sides: every block has its transpose
+        blk_ld = r_cnt[uids[:, 1]] + 3
+        blk_off = np.cumsum(r_cnt[uids[:, 0]] * blk_ld) - r_cnt[uids[:, 0]] * blk_ld
+        six = np.stack([r_off[uids[:, 0]], r_cnt[uids[:, 0]], r_off[uids[:, 1]], r_cnt[uids[:, 1]], blk_off, blk_ld],
+                       axis=1)
+        got = kernels.block_jobs(uids, r_off, r_cnt, r_off, r_cnt, blk_off, blk_ld, part)
+        assert np.array_equal(got, kernels.mirror_jobs(six, uids, part))
+        assert len(got) < len(uids)
+        one = kernels.block_jobs(uids, r_off, r_cnt, r_off, r_cnt, blk_off, blk_ld, None)
+        assert np.array_equal(one, kernels._as_job8(six))
+    # a list with unpaired blocks and a diagonal block
+    uids = np.array([(0, 1), (2, 2), (1, 0), (3, 1), (0, 3)], dtype=np.int64)
+    part = kernels.block_partners(uids)
+    assert part.tolist() == [2, 1, 0, -1, -1]
+    cnt = np.array([4, 5, 6, 7], dtype=np.int64)
+    o = np.array([0, 4, 9, 15], dtype=np.int64)
+    bo = np.arange(5, dtype=np.int64) * 100
+    bl = cnt[uids[:, 1]]
+    six = np.stack([o[uids[:, 0]], cnt[uids[:, 0]], o[uids[:, 1]], cnt[uids[:, 1]], bo, bl], axis=1)
+    assert np.array_equal(kernels.block_jobs(uids, o, cnt, o, cnt, bo, bl, part), kernels.mirror_jobs(six, uids, part))
+    assert len(kernels.block_jobs(uids[:0], o, cnt, o, cnt, bo[:0], bl[:0], part[:0])) == 0
