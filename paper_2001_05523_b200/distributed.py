@@ -362,6 +362,52 @@ class ShardedMatvec:
         return d[: self.hi - self.lo]
 
 
+class ShardedOperator:
+    """The reference's operator interface (matvec / diagonal on full
+    natural-order vectors, containers.py:254-301) over a row-sharded operator:
+    what ProblemSetup.operator returns when RunParams.devices > 1.  Every rank
+    passes the same x and receives the full y (its own rows computed here, the
+    others summed in by one all-reduce); solvers that keep their vectors
+    sharded use `.sharded` (ShardedMatvec.apply_local) directly."""
+
+    def __init__(self, sharded):
+        self.sharded = sharded
+        n = sharded.shard.bt.row_tree.n_dofs
+        self.shape = (n, n)
+
+    def _full(self, fill):
+        import torch
+
+        mv = self.sharded
+        y = torch.zeros(self.shape[0], dtype=torch.float64, device="cuda")
+        fill(y)
+        if mv.world > 1:
+            mv.dist.all_reduce(y, op=mv.dist.ReduceOp.SUM)
+        return y
+
+    def matvec(self, x):
+        import torch
+
+        from . import device as D
+
+        dev_in = isinstance(x, torch.Tensor)
+        xd = x if dev_in else D.dev(np.ascontiguousarray(x, dtype=np.float64))
+        if xd.dtype != torch.float64 or xd.ndim != 1 or xd.numel() != self.shape[1]:
+            raise ValueError(f"expected a float64 vector of length {self.shape[1]}")
+        y = self._full(lambda y: self.sharded.apply(xd, y))
+        return y if dev_in else D.host(y)
+
+    def diagonal(self):
+        from . import device as D
+
+        mv = self.sharded
+
+        def fill(y):
+            y[mv.perm_dev] = mv.diagonal_local()
+
+        return D.host(self._full(fill))
+
+
 def allreduce_sum(dist, group=None):
     """In-place sum of a small device tensor over the ranks (CG scalars)."""
 

@@ -21,6 +21,7 @@ class ProblemSetup:
     _operators: dict = field(default_factory=dict)
     _bases: dict = field(default_factory=dict)
     _nearfield: dict = field(default_factory=dict)
+    dist: object = None  # collective provider for params.devices > 1 (default: torch.distributed)
 
     def __post_init__(self):
         p = self.params
@@ -62,12 +63,35 @@ class ProblemSetup:
             col_tree = "p0" if kind == kernels.SLP else "p1"
             rb = self.basis(row_tree, rf)
             cb = rb if (rf == cf and row_tree == col_tree) else self.basis(col_tree, cf)
+            if getattr(p, "devices", 1) > 1:
+                op = self._sharded_operator(kind, rb, cb, qs)
+                self._operators[key] = op
+                return op
             op = gca.assemble_h2(self.ctx, kind, self.block_tree(kind), rb, cb, p.q_near,
                                  nearfield_cache=nf_cache, q_singular=qs)
         else:
             raise ValueError(f"unknown or unsupported method {method!r}")
         self._operators[key] = op
         return op
+
+
+    def _sharded_operator(self, kind, rb, cb, qs):
+        """params.devices > 1: this process is one rank of a row-sharded
+        operator (one process per GPU); it integrates, stores and applies only
+        its row clusters' blocks (distributed.RowShard / ShardedMatvec)."""
+        import torch.distributed as td
+
+        from .distributed import RowShard, ShardedMatvec, ShardedOperator
+
+        p = self.params
+        if not td.is_available() or not td.is_initialized():
+            raise ValueError("RunParams.devices > 1 needs an initialised torch.distributed process group")
+        world, rank = td.get_world_size(), td.get_rank()
+        if world != p.devices:
+            raise ValueError(f"RunParams.devices = {p.devices} but the process group has {world} ranks")
+        shard = RowShard(self.block_tree(kind), rb, cb, rank, world)
+        shard.assemble(self.ctx, kind, p.q_near, qs)
+        return ShardedOperator(ShardedMatvec(shard, rank, world, self.dist if self.dist is not None else td))
 
 
 def setup_sphere(level, params):

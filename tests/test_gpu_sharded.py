@@ -318,3 +318,65 @@ def test_xhat_exchange_bitwise(slp5, world):
         xp = xp * 0.5 + 1.0
         for sh, full in shards:
             full[torch.from_numpy(sh.pad_index).cuda()] = xp
+
+
+# ---- RunParams.devices: the driver's sharded operator ---------------------------
+
+def _driver_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2001_05523_b200 import driver, mesh
+        from paper_2001_05523_b200.params import RunParams
+
+        prm = dict(order=3, q_near=3, q_singular=4, r_leaf=16, eta=1.0, eps_aca=1e-4, threads=2)
+        m = mesh.sphere_mesh(4)
+        sh = driver.ProblemSetup(m, RunParams(devices=world, **prm).resolved(), dist=_Staged(dist))
+        op = sh.operator("slp")
+        x = np.random.default_rng(11).standard_normal(m.n_triangles)
+        y = op.matvec(x)
+        d = op.diagonal()
+        yt = op.matvec(torch.from_numpy(x).cuda())
+        assert isinstance(yt, torch.Tensor) and np.array_equal(yt.cpu().numpy(), y)
+        try:
+            driver.ProblemSetup(m, RunParams(devices=world + 1, **prm).resolved()).operator("slp")
+            bad = False
+        except ValueError:
+            bad = True
+        if rank == 0:
+            one = driver.ProblemSetup(m, RunParams(**prm).resolved()).operator("slp")
+            y1, d1 = one.matvec(x), one.diagonal()
+            out.put((float(np.linalg.norm(y - y1) / np.linalg.norm(y1)), float(np.abs(d - d1).max()), bad,
+                     op.sharded.info()["near_bytes"], one.plan().info()["near_bytes"]))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_driver_devices_two_ranks():
+    """RunParams.devices = 2: ProblemSetup.operator hands
+    each rank a row-sharded operator with the reference's matvec / diagonal
+    interface; full vectors in and out equal the single-GPU operator, a rank
+    count that differs from the process group raises."""
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_driver_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    dy, dd, bad, nb_sh, nb_one = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert dy < 1e-13 and dd == 0.0 and bad
+    assert nb_sh < nb_one  # the rank streams its share of the nearfield only
