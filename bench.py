@@ -70,7 +70,7 @@ CONFIGS = {
 DEFAULT_CONFIG = "3"
 EPS_ACA = 1e-4
 METRIC = "H2-matvec DoF/s (fp64), + nearfield quad pairs/s"
-PROFILE = os.path.join(ROOT, "profiles", "r02bd_ncu_full_raw.csv")
+PROFILE = os.path.join(ROOT, "profiles", "r02bp_ncu_full_raw.csv")
 
 
 # ---------------------------------------------------------------------------
@@ -97,7 +97,11 @@ def measure_fp64_peak():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks
+    line).  One sampler per run: sub-intervals are cut out of its record by
+    timestamp (mark / stop(t0, t1)) -- a second nvidia-smi would double the
+    perturbation, and its start-up (NVML init) stalls driver calls for tens of
+    milliseconds."""
 
     def __init__(self, gpu_index=0):
         self.proc = None
@@ -105,7 +109,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={gpu_index}",
-                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "--query-gpu=timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
                  "--format=csv,noheader,nounits", "-lms", "50"],
@@ -113,26 +117,42 @@ class Clocks:
         except Exception:
             self.proc = None
 
-    def stop(self):
+    @staticmethod
+    def mark():
+        return time.time()
+
+    def stop(self, t0=None, t1=None):
+        """Stop the sampler (first call) and summarise the samples, all of
+        them or those stamped within [t0, t1] (time.time() values)."""
+        import datetime
+
         if self.proc is None:
             return None
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
+        if self.proc.poll() is None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in open(self.path):
             f = [x.strip() for x in line.split(",")]
-            if len(f) < 8:
+            if len(f) < 9:
                 continue
+            if t0 is not None:
+                try:
+                    ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                except ValueError:
+                    continue
+                if ts < t0 - 0.05 or ts > t1 + 0.05:
+                    continue
             try:
-                sm.append(float(f[0]))
-                mx = max(mx, float(f[1]))
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
             except ValueError:
                 continue
-            for n, v in zip(names, f[4:8]):
+            for n, v in zip(names, f[5:9]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
         if not sm:
@@ -277,8 +297,10 @@ def run_ours(args, cfg):
 
     # ---- nearfield assembly on the device (timed) ----------------------------
     clocks = Clocks(local)
+    time.sleep(1.0)  # nvidia-smi's start-up (NVML init) stalls driver calls for tens of ms: keep it out of the timings
     dm = ctx.dmesh
-    t_touch = ev_time(torch, lambda: kernels.TouchTable(dm))  # classification of all touching pairs
+    kernels.TouchTable(dm)  # warm-up (allocator)
+    t_touch = ev_time(torch, lambda: kernels.TouchTable(dm), 3)  # classification of all touching pairs
     dm.touch()
     table = kernels.SingularTable(dm, "slp", cfg["q_ss"], compute=False)
     own = shard.own_panels if shard is not None else None
@@ -290,11 +312,11 @@ def run_ours(args, cfg):
         table.compute(own)
         sj.run(table, Dn)
     nf_reps = 3 if n > 1_000_000 else 10
-    nf_clocks = Clocks(local)  # clocks during the FP64-bound quadrature alone
+    nf_m0 = clocks.mark()  # clocks during the FP64-bound quadrature alone: a slice of the one sampler's record
     t_sing = ev_time(torch, lambda: table.compute(own), nf_reps)
     t_reg = ev_time(torch, lambda: sj.run(table, Dn), nf_reps)
     t_reg_each = [ev_time(torch, lambda: sj.run(table, Dn), 1) for _ in range(nf_reps)]
-    nf_clk = nf_clocks.stop()
+    nf_m1 = clocks.mark()
     touch = dm.touch()
     if own is not None:
         touch.subset(own, half=True)
@@ -381,6 +403,7 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     kern_s = float(np.mean([s.elapsed_time(e) / 1e3 for s, e in zip(kst, ken)]))
     clk = clocks.stop()
+    nf_clk = clocks.stop(nf_m0, nf_m1)
     total = float(step_s.sum())
     tmax = {"total": total, "touch": t_touch, "sing": t_sing, "reg": t_reg, "cpl": t_cpl, "cpl_e2e": t_cpl_e2e}
     sums = {"near_pairs": float(near_pairs), "cpl_pairs": float(cpl_pairs),
@@ -400,8 +423,11 @@ def run_ours(args, cfg):
     if ws == 1:
         xh = np.ascontiguousarray(x_host)  # plain pageable numpy: the reference caller's vector
         for _ in range(5):
-            H.matvec(xh)
+            yh = H.matvec(xh)  # keeps the previous result alive, as the timed loop does: both pinned blocks exist
         ke = max(10, min(K, 50))
+        import gc
+
+        gc.collect()  # a full collection over the setup's ~1e6 objects inside the loop costs 10+ ms
         each = []
         t1 = time.perf_counter()
         for _ in range(ke):
