@@ -902,9 +902,9 @@ class MatvecPlan:
         x = np.ascontiguousarray(x, dtype=np.float64)
         if x.ndim != 1 or len(x) != self.n_cols:
             raise ValueError(f"expected a vector of length {self.n_cols}")
-        # the result is written by the kernel straight into page-locked host
-        # memory (torch's caching host allocator: cheap after the first call);
-        # a page-locked x is read in place, a pageable one staged by the library
+        # the result lands in page-locked host memory (torch's caching host
+        # allocator: cheap after the first call), so its copy back is one DMA;
+        # x is copied by DMA when page-locked, by the driver's staged copy otherwise
         y = t.empty(self.n_rows, dtype=t.float64, pin_memory=True).numpy()
         _lib.check(_lib.lib().h2b_matvec_host(self.handle, _lib.ptr(x), _lib.ptr(y), _lib.stream_ptr()))
         return y

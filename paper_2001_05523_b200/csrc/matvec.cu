@@ -79,7 +79,6 @@ constexpr int kFwdHead = 8;     // start, size, k, v_off, xhat_off, n_climb, war
 constexpr int kFwdStride = 40;  // forward records are fixed-stride (record = ticket * stride: no index round
                                 // trip): the header, then the leaf's first 64 x indices (col_perm, int32)
 constexpr int kFwdLevel = 6;    // k0, kp, e_off_c0, e_off_own, xhat_off_c0, xhat_off_parent
-constexpr int kCopyChunk = 1024;  // y values per copy-out task (host-output launches)
 constexpr int kKindNear = 0, kKindCpl = 1;  // band record kinds (word 7)
 constexpr int kFwdAhead = 2048;              // forward tasks pull the record of the task this many tickets on into L2
 constexpr int64_t kUpfrontMax = 24 << 20;   // records + gather lists prefetched up front when at most this many bytes
@@ -98,7 +97,7 @@ struct h2b_plan {
     uint64_t* ycpl;     // LL: 2 x yhat_len (coupling part of y_hat)
     uint64_t* yfin;     // LL: 2 x yhat_len (final y_hat of inner clusters)
     uint64_t* ynear;    // LL: 2 x n_rows (permuted order)
-    unsigned long long* ctrl;  // ticket counters (device / host-output launches), monotonic over launches
+    unsigned long long* ctrl;  // ticket counters ([0] matvec launches, [3] x_hat forward launches), monotonic over launches
     int64_t* rec;       // task records
     int64_t* fwd_off;   // per column leaf: record offset
     int64_t band_base;  // record offset of band 0
@@ -111,7 +110,6 @@ struct h2b_plan {
     double* dpack = nullptr;  // downward-step operands [E_t^T | V_t^T] per cluster (k_pack_descent)
     double* dx;
     double* dy;
-    double* hy;         // pinned host staging of the result (h2b_matvec_host)
     unsigned long long* trace;  // optional per-CTA timeline (H2B_TRACE=1)
     // symmetric nearfield (one copy of every block pair; null when unused)
     double* dsym;       // packed column panels of the upper blocks
@@ -119,7 +117,6 @@ struct h2b_plan {
     uint64_t* ppart;    // LL partial vectors (direct per panel, transposed per block)
     int64_t* nsum;      // per leaf: the partials summed by its final task, in order
     int64_t ppart_len;
-    int n_leaf;         // leaf downward-step tasks per launch
     int64_t near_bytes; // nearfield bytes one matvec streams
     int64_t cpl_bytes;  // coupling bytes one matvec streams
     // Launches of one plan must run one after another (one ticket counter and
@@ -1238,10 +1235,6 @@ struct KArgs {
     uint64_t *xhat, *ycpl, *yfin, *ynear;
     unsigned long long* ctrl;
     unsigned long long* trace;
-    double* yh;        // host-mapped y (h2b_matvec_host) or null: y is then a device copy
-    int n_out;         // copy-out tasks (host output): the last tickets
-    int n_leaf;        // leaf downward steps per launch
-    unsigned long long* ydone;  // leaf downward steps finished (host-output launches, monotonic)
     const double* dsym;      // symmetric nearfield (null: not used)
     const int32_t* gsym;
     uint64_t* ppart;
@@ -1253,42 +1246,10 @@ struct KArgs {
 #define H2B_MINB 6
 #endif
 
-// One task (tickets [0, c_leaves): forward; then band / descent records;
-// then, host-output launches, the copy-out tasks).  Ends with a block barrier.
+// One task (tickets [0, c_leaves): forward; then band / descent records).  Ends with a block barrier.
 __device__ __forceinline__ void run_task(const KArgs& a, const double* __restrict__ x, double* __restrict__ y,
                                          const int ticket, const uint32_t epoch, Shared& s) {
     const h2b_layout& L = a.L;
-    if (ticket >= a.n_fwd + a.n_near + a.n_cpl) {
-        // host-output launch: once every leaf has written its rows of y (in
-        // HBM, natural order), copy a chunk to the mapped host buffer with
-        // coalesced stores (scattered 8-byte stores over the host link cost
-        // one transaction each)
-        if (threadIdx.x == 0) {
-            const unsigned long long target = (unsigned long long)((epoch - 2) / 2 + 1) * (unsigned long long)a.n_leaf;
-            unsigned long long v;
-            while (true) {
-                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.ydone) : "memory");
-                if (v >= target) break;
-                __nanosleep(64);
-            }
-        }
-        __syncthreads();
-        const int64_t c = ticket - (a.n_fwd + a.n_near + a.n_cpl), n = L.n_rows;
-        const int64_t i0 = c * kCopyChunk, i1 = min(n, i0 + kCopyChunk);
-        constexpr int kU = kCopyChunk / kThreads;
-        double v[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const int64_t i = i0 + u * kThreads + threadIdx.x;
-            v[u] = i < i1 ? __ldcg(y + i) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const int64_t i = i0 + u * kThreads + threadIdx.x;
-            if (i < i1) a.yh[i] = v[u];
-        }
-        return;
-    }
     unsigned long long t_begin = 0;
     if (a.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
     s.mark = a.trace ? a.trace + 8 * ticket + 3 : nullptr;
@@ -1330,13 +1291,6 @@ __device__ __forceinline__ void run_task(const KArgs& a, const double* __restric
             task_band<true>(L, x, a.xhat, a.ycpl, a.yfin, a.ycpl, a.ynear, y, epoch, s);
     }
     __syncthreads();
-    if (a.yh && threadIdx.x == 0 && ticket >= tB) {
-        const int kind = (int)s.rec[7];
-        if (kind == kKindCpl && s.rec[5] && s.rec[13]) {  // a leaf's rows of y are out
-            __threadfence();
-            atomicAdd(a.ydone, 1ull);
-        }
-    }
     if (threadIdx.x == 0) {
         if (a.trace) {
             unsigned long long t_end;
@@ -1380,12 +1334,10 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
     if (threadIdx.x == 0) {
         // tickets count on across launches: launch = t / grid (every CTA of a
         // launch takes exactly one ticket before the next launch starts)
-        // device- and host-output launches count on separate counters (their
-        // grids differ by the copy-out tasks); epochs stay unique: odd / even
-        const int host = a.yh != nullptr;
-        const unsigned long long t = atomicAdd(a.ctrl + host, 1ull);
+        // (odd epochs: the x_hat-exchange entry points compute theirs on the host)
+        const unsigned long long t = atomicAdd(a.ctrl, 1ull);
         s_ticket = (int)(t % gridDim.x);
-        s_epoch = 2u * (uint32_t)(t / gridDim.x) + 1u + (uint32_t)host;
+        s_epoch = 2u * (uint32_t)(t / gridDim.x) + 1u;
         mbar_init(s.bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -2050,11 +2002,6 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags, const i
     p->L = L;
     p->n_near = n_near;
     p->n_cpl = n_cpl;
-    p->n_leaf = 0;
-    for (int64_t b = 0; b < (int64_t)(n_near + n_cpl); ++b) {
-        const int64_t* r = rec.data() + band_base + kBandWords * b;
-        if (r[7] == kKindCpl && r[5] && r[13]) ++p->n_leaf;
-    }
     p->band_base = band_base;
     {
         int64_t m = 0;
@@ -2078,8 +2025,8 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags, const i
     H2B_CUDA_TRY(cudaMemset(p->xhat, 0, 16 * (size_t)L.xhat_len));
     H2B_CUDA_TRY(cudaMemset(p->ycpl, 0, 16 * (size_t)L.yhat_len));
     H2B_CUDA_TRY(cudaMemset(p->ynear, 0, 16 * (size_t)L.n_rows));
-    // ticket counters: [0] device-input, [1] host-output launches, [2] leaf steps
-    // done (host output), [3] forward launches of the x_hat exchange
+    // ticket counters: [0] matvec launches, [3] forward launches of the x_hat
+    // exchange ([1], [2] unused)
     H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->ctrl), 4 * sizeof(unsigned long long)));
     H2B_CUDA_TRY(cudaMemset(p->ctrl, 0, 4 * sizeof(unsigned long long)));
     H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->rec), sizeof(int64_t) * std::max<size_t>(1, rec.size())));
@@ -2148,7 +2095,6 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags, const i
     }
     H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->dx), sizeof(double) * L.n_cols));
     H2B_CUDA_TRY(alloc(reinterpret_cast<void**>(&p->dy), sizeof(double) * L.n_rows));
-    H2B_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&p->hy), sizeof(double) * std::max<int64_t>(L.n_rows, 1)));
     p->dsym = nullptr;
     p->gsym = nullptr;
     p->ppart = nullptr;
@@ -2254,7 +2200,6 @@ extern "C" int h2b_plan_destroy(h2b_plan* p) {
                     p->xhat_f, p->d_own, p->d_own_off, p->d_imp, p->d_imp_src, p->d_span, p->span_val};
     for (void* q : bufs)
         if (q) cudaFree(q);
-    if (p->hy) cudaFreeHost(p->hy);
     if (p->done) cudaEventDestroy(p->done);
     delete p;
     return ok();
@@ -2263,8 +2208,7 @@ extern "C" int h2b_plan_destroy(h2b_plan* p) {
 namespace {
 // mode 0: the plan's full task list; 1: forward tasks only (x_hat exchange,
 // into xhat_f); 2: bands only (x_hat imported)
-int launch_matvec(h2b_plan* p, const double* d_x, double* y, cudaStream_t st,
-                  double* yh = nullptr, int mode = 0) {
+int launch_matvec(h2b_plan* p, const double* d_x, double* y, cudaStream_t st, int mode = 0) {
     // (caller holds p->mu) order after the plan's previous launch if that was
     // on another stream
     if (p->launched && p->last != st) H2B_CUDA_TRY(cudaStreamWaitEvent(st, p->done, 0));
@@ -2297,10 +2241,6 @@ int launch_matvec(h2b_plan* p, const double* d_x, double* y, cudaStream_t st,
     a.ppart = p->ppart;
     a.nsum = p->nsum;
     a.dpack = p->dpack;
-    a.yh = yh;
-    a.n_out = yh ? (int)((p->L.n_rows + kCopyChunk - 1) / kCopyChunk) : 0;
-    a.n_leaf = p->n_leaf;
-    a.ydone = p->ctrl + 2;
     a.n_fwd = p->n_fwd;
     if (mode == 1) {
         a.n_near = a.n_cpl = 0;
@@ -2309,7 +2249,7 @@ int launch_matvec(h2b_plan* p, const double* d_x, double* y, cudaStream_t st,
     } else if (mode == 2) {
         a.n_fwd = 0;
     }
-    const int grid = a.n_fwd + a.n_near + a.n_cpl + a.n_out;
+    const int grid = a.n_fwd + a.n_near + a.n_cpl;
     k_matvec<<<grid, kThreads, p->smem, st>>>(a, d_x, y);
     H2B_CUDA_TRY(cudaGetLastError());
     H2B_CUDA_TRY(cudaEventRecord(p->done, st));
@@ -2318,37 +2258,6 @@ int launch_matvec(h2b_plan* p, const double* d_x, double* y, cudaStream_t st,
     return ok();
 }
 
-// memcpy over several host threads (a pageable x of config 3 is 16.8 MB: ~1 ms
-// on one core, which was a fifth of the end-to-end matvec)
-void par_memcpy(void* dst, const void* src, size_t bytes) {
-    const unsigned hw = std::thread::hardware_concurrency();
-    const int nt = bytes < (size_t(2) << 20) ? 1 : (int)std::min<unsigned>(8, std::max(1u, hw));
-    if (nt <= 1) {
-        std::memcpy(dst, src, bytes);
-        return;
-    }
-    const size_t per = ((bytes + nt - 1) / nt + 4095) & ~size_t(4095);
-    std::vector<std::thread> th;
-    for (int i = 1; i < nt; ++i) {
-        const size_t o = per * i;
-        if (o >= bytes) break;
-        th.emplace_back([=] {
-            std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, std::min(per, bytes - o));
-        });
-    }
-    std::memcpy(dst, src, std::min(per, bytes));
-    for (auto& t : th) t.join();
-}
-
-// device-accessible pointer of pinned (page-locked, mapped) host memory, or null
-const void* mapped(const void* h) {
-    cudaPointerAttributes at;
-    if (cudaPointerGetAttributes(&at, h) != cudaSuccess) {
-        cudaGetLastError();
-        return nullptr;
-    }
-    return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
-}
 }  // namespace
 
 extern "C" int h2b_matvec(h2b_plan* p, const double* d_x, double* d_y, void* stream) {
@@ -2358,26 +2267,23 @@ extern "C" int h2b_matvec(h2b_plan* p, const double* d_x, double* d_y, void* str
     return launch_matvec(p, d_x, d_y, as_stream(stream));
 }
 
-// Host vectors: x goes to the device with one stream-ordered copy (a pinned x
-// by DMA, a pageable one through the driver's staged copy: both measured
-// faster than reading x from mapped host memory inside the kernel, config 3:
-// 3.75 vs 3.82 ms pinned, 4.3 vs 5.3 ms pageable); the kernel writes y
-// straight into pinned host memory (its last tasks), a pageable y goes
-// through the plan's pinned staging.
+// Host vectors: one stream-ordered copy each way around the launch (a pinned
+// buffer by DMA, a pageable one through the driver's staged copy), then a
+// stream synchronise.  Measured against the round's earlier design -- x read
+// from mapped host memory by copy tasks inside the kernel, y written to mapped
+// host memory by its last tasks -- the copy engines win from config 2 up
+// (config 3, pinned vectors: 3.58 vs 3.82 ms; pageable x: 4.1 vs 5.3 ms) and
+// cost 3 us at config 1 (76 vs 73 us).
 extern "C" int h2b_matvec_host(h2b_plan* p, const double* h_x, double* h_y, void* stream) {
     if (!p || !h_x || !h_y) return fail(H2B_ERR_INVALID, "h2b_matvec_host: null pointer");
     if (p->xmode) return fail(H2B_ERR_INVALID, "h2b_matvec_host: x_hat-exchange plan");
     std::lock_guard<std::mutex> g(p->mu);
     cudaStream_t st = as_stream(stream);
-    double* yh = static_cast<double*>(const_cast<void*>(mapped(h_y)));
-    const bool staged_y = yh == nullptr;
-    if (staged_y) yh = static_cast<double*>(const_cast<void*>(mapped(p->hy)));
-    if (!yh) return fail(H2B_ERR_CUDA, "h2b_matvec_host: pinned staging is not device-mapped");
     if (p->launched && p->last != st) H2B_CUDA_TRY(cudaStreamWaitEvent(st, p->done, 0));
     H2B_CUDA_TRY(cudaMemcpyAsync(p->dx, h_x, sizeof(double) * p->L.n_cols, cudaMemcpyHostToDevice, st));
-    if (int rc = launch_matvec(p, p->dx, p->dy, st, yh)) return rc;
+    if (int rc = launch_matvec(p, p->dx, p->dy, st)) return rc;
+    H2B_CUDA_TRY(cudaMemcpyAsync(h_y, p->dy, sizeof(double) * p->L.n_rows, cudaMemcpyDeviceToHost, st));
     H2B_CUDA_TRY(cudaStreamSynchronize(st));
-    if (staged_y) par_memcpy(h_y, p->hy, sizeof(double) * p->L.n_rows);
     return ok();
 }
 
@@ -2476,7 +2382,7 @@ extern "C" int h2b_xhat_forward(h2b_plan* p, const double* d_x, double* d_send, 
     cudaStream_t st = as_stream(stream);
     const uint32_t epoch = 2u * (uint32_t)p->n_f_launches + 1u;
     if (p->n_fwd > 0) {
-        if (int rc = launch_matvec(p, d_x, nullptr, st, nullptr, 1)) return rc;
+        if (int rc = launch_matvec(p, d_x, nullptr, st, 1)) return rc;
     }
     ++p->n_f_launches;
     if (p->n_own > 0) {
@@ -2515,7 +2421,7 @@ extern "C" int h2b_xhat_main(h2b_plan* p, const double* d_x, const double* d_rec
                                                                  p->span_val, p->xhat, epoch);
         H2B_CUDA_TRY(cudaGetLastError());
     }
-    if (int rc = launch_matvec(p, d_x, d_y, st, nullptr, 2)) return rc;
+    if (int rc = launch_matvec(p, d_x, d_y, st, 2)) return rc;
     ++p->n_m_launches;
     return ok();
 }
