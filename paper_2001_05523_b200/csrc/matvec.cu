@@ -1246,13 +1246,14 @@ struct KArgs {
 #define H2B_MINB 6
 #endif
 
-// One task (tickets [0, c_leaves): forward; then band / descent records).  Ends with a block barrier.
+// One task (tickets [0, c_leaves): forward; then band / descent records).
+template <bool kTrace>
 __device__ __forceinline__ void run_task(const KArgs& a, const double* __restrict__ x, double* __restrict__ y,
                                          const int ticket, const uint32_t epoch, Shared& s) {
     const h2b_layout& L = a.L;
     unsigned long long t_begin = 0;
-    if (a.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
-    s.mark = a.trace ? a.trace + 8 * ticket + 3 : nullptr;
+    if (kTrace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
+    s.mark = kTrace ? a.trace + 8 * ticket + 3 : nullptr;
     const int tB = a.n_fwd;
 
     if (ticket < tB) {
@@ -1290,9 +1291,10 @@ __device__ __forceinline__ void run_task(const KArgs& a, const double* __restric
         else
             task_band<true>(L, x, a.xhat, a.ycpl, a.yfin, a.ycpl, a.ynear, y, epoch, s);
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (a.trace) {
+    if (kTrace) {
+        // (diagnostic instantiation only: the product kernel ends with its task)
+        __syncthreads();
+        if (threadIdx.x == 0) {
             unsigned long long t_end;
             unsigned smid;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
@@ -1309,6 +1311,7 @@ __device__ __forceinline__ void run_task(const KArgs& a, const double* __restric
 
 
 
+template <bool kTrace>
 __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, const double* __restrict__ x,
                                                        double* __restrict__ y) {
     extern __shared__ __align__(128) char smraw[];
@@ -1344,7 +1347,7 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
     __syncthreads();
     const int ticket = s_ticket;
     const uint32_t epoch = s_epoch;
-    run_task(a, x, y, ticket, epoch, s);
+    run_task<kTrace>(a, x, y, ticket, epoch, s);
 }
 
 // ---- x_hat exchange (row-sharded plans, SURVEY 8(e) "better variant") ------
@@ -2081,7 +2084,8 @@ int plan_create(const h2b_layout* layout, h2b_plan** out, int sym_flags, const i
         static int smem_set[64] = {0};
         int& cur = smem_set[p->device & 63];
         if (p->smem > cur) {
-            H2B_CUDA_TRY(cudaFuncSetAttribute(k_matvec, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem));
+            H2B_CUDA_TRY(cudaFuncSetAttribute(k_matvec<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem));
+            H2B_CUDA_TRY(cudaFuncSetAttribute(k_matvec<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem));
             cur = p->smem;
         }
     }
@@ -2250,7 +2254,10 @@ int launch_matvec(h2b_plan* p, const double* d_x, double* y, cudaStream_t st, in
         a.n_fwd = 0;
     }
     const int grid = a.n_fwd + a.n_near + a.n_cpl;
-    k_matvec<<<grid, kThreads, p->smem, st>>>(a, d_x, y);
+    if (p->trace)
+        k_matvec<true><<<grid, kThreads, p->smem, st>>>(a, d_x, y);  // diagnostic timeline (H2B_TRACE=1 at plan creation)
+    else
+        k_matvec<false><<<grid, kThreads, p->smem, st>>>(a, d_x, y);
     H2B_CUDA_TRY(cudaGetLastError());
     H2B_CUDA_TRY(cudaEventRecord(p->done, st));
     p->last = st;
