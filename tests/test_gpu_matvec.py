@@ -191,9 +191,11 @@ def test_row_sharded_plans_reproduce_single_gpu_bitwise(cfg0):
 
 
 def test_host_vectors_pinned_pageable_device_agree(cfg0):
-    """h2b_matvec_host reads x in place when it is page-locked (else through
-    the plan's staging) and writes y into page-locked memory: all paths give
-    the device result bit for bit, in any interleaving of launches."""
+    """h2b_matvec_host copies x to the device and y back with the copy engines
+    (page-locked buffers by DMA, pageable ones through the driver's staged
+    copies): every combination of page-locked / pageable x and y, on the
+    default stream or another one, gives the device result bit for bit, in any
+    interleaving of launches."""
     import torch
 
     g, m, t0, bt, b, H = cfg0
@@ -206,6 +208,24 @@ def test_host_vectors_pinned_pageable_device_agree(cfg0):
         assert isinstance(y_page, np.ndarray) and isinstance(y_pin, np.ndarray)
         assert np.array_equal(y_page, y_dev) and np.array_equal(y_pin, y_dev)
         assert np.array_equal(H.matvec(torch.from_numpy(x).cuda()).cpu().numpy(), y_dev)
+    # the C ABI itself: pageable and page-locked results, a side stream, then
+    # the default stream again (a launch on another stream waits for the last)
+    from paper_2001_05523_b200 import _lib
+
+    L, plan = _lib.lib(), H.plan()
+    side = torch.cuda.Stream()
+    yp = torch.empty(H.shape[0], dtype=torch.float64).pin_memory().numpy()
+    for xin in (x, xp):
+        for yout in (np.empty(H.shape[0]), yp):
+            for st in (None, side.cuda_stream, None):
+                yout[:] = np.nan
+                _lib.check(L.h2b_matvec_host(plan.handle, _lib.ptr(xin), _lib.ptr(yout), st))
+                assert np.array_equal(yout, y_dev)
+    with torch.cuda.stream(side):
+        y_side = H.matvec(torch.from_numpy(x).cuda())
+    assert np.array_equal(H.matvec(x), y_dev)
+    side.synchronize()
+    assert np.array_equal(y_side.cpu().numpy(), y_dev)
 
 
 def _h2_on(level, leaf, eta=2.0, m=3, kind="slp"):
