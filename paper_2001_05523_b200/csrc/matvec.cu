@@ -50,7 +50,6 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
-#include <thread>
 #include <vector>
 
 #include "device_common.cuh"
@@ -566,7 +565,6 @@ struct Shared {
     const int64_t* nsum;       // their per-leaf lists
     bool near_sym;             // nearfield as symmetric column panels
     uint32_t parity;           // mbarrier phase of the staging slot in use
-    bool issued;               // band bulk copy already issued by the caller
     const double* dpack;       // downward-step operands [E_t^T | V_t^T] per cluster (plan-owned copy)
     int64_t pf;                // this thread's partial vector to pull into L2 (leaf final tasks), or -1
 };
@@ -586,10 +584,6 @@ __device__ __forceinline__ const double* stage_issue(const Shared& s, const doub
         }
     }
     return fits ? reinterpret_cast<const double*>(s.stage) : src;
-}
-
-__device__ __forceinline__ bool band_staged(const Shared& s, int64_t bytes, const double* src) {
-    return bytes > 0 && bytes <= s.stage_bytes && (reinterpret_cast<uintptr_t>(src) & 15) == 0 && (bytes & 15) == 0;
 }
 
 __device__ void prefetch_slice(const double* base, int64_t bytes, int part, int parts) {
@@ -1045,9 +1039,7 @@ __device__ void task_band(const h2b_layout& L, const double* __restrict__ x, con
         // columns): the same bits as the unchunked product
         const double* base = kCoupling ? L.S : L.D;
         const int64_t bytes = (int64_t)rows * cols * 8;
-        const double* M = s.issued ? (band_staged(s, bytes, base + src_off) ? reinterpret_cast<const double*>(s.stage)
-                                                                         : base + src_off)
-                                   : stage_issue(s, base + src_off, bytes);
+        const double* M = stage_issue(s, base + src_off, bytes);
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
         const double* row = M + (int64_t)min(warp, rows - 1) * cols;
         const int32_t* gidx = (kCoupling ? L.s_gidx : L.d_gidx) + gi_off;
@@ -1086,9 +1078,7 @@ __device__ void task_band(const h2b_layout& L, const double* __restrict__ x, con
     } else if (rows > 0) {
         const double* base = kCoupling ? L.S : L.D;
         const int64_t bytes = (int64_t)rows * cols * 8;
-        const double* M = s.issued ? (band_staged(s, bytes, base + src_off) ? reinterpret_cast<const double*>(s.stage)
-                                                                         : base + src_off)
-                                   : stage_issue(s, base + src_off, bytes);
+        const double* M = stage_issue(s, base + src_off, bytes);
         mark(s.mark, 0);
         if (kCoupling)
             gather_ll(s.rhs, xhat, L.s_gidx + gi_off, cols, epoch);
@@ -1109,13 +1099,11 @@ __device__ void task_band(const h2b_layout& L, const double* __restrict__ x, con
         mark(s.mark, 3);
         uint64_t* dst = out + 2 * out_off;
         for (int i = threadIdx.x; i < rows; i += blockDim.x) ll_store(dst + 2 * i, s.va[i], epoch);
-    } else if (s.issued) {
-        mbar_wait(s.bar, s.parity);  // the plain arrive of an empty band
     }
     if (kCoupling && s.rec[5]) {
         __syncthreads();
         descent(L.r_E, L.r_V, L.row_perm, s.rec + 8, ycpl, yfin, ynear, y, epoch, s.rec[6] != 0, s,
-                s.parity ^ ((rows > 0 || s.issued) ? 1u : 0u));
+                s.parity ^ (rows > 0 ? 1u : 0u));
     }
 }
 
@@ -1209,9 +1197,7 @@ __device__ void task_panel(const double* __restrict__ base, const int32_t* __res
     const int64_t tr_off = s.rec[8], rg_off = s.rec[10];
     const int skip = (int)s.rec[9];
     const int64_t bytes = ((int64_t)rows * cols * 8 + 15) & ~int64_t(15);  // panels are padded to 16 bytes
-    const double* M = s.issued ? (band_staged(s, bytes, base + src_off) ? reinterpret_cast<const double*>(s.stage)
-                                                                     : base + src_off)
-                               : stage_issue(s, base + src_off, bytes);
+    const double* M = stage_issue(s, base + src_off, bytes);
     mark(s.mark, 0);
     const bool tr = skip < cols;
     gather2(s.rhs, gl + gi_off, cols, s.vb, gl + rg_off, tr ? rows : 0, x);
@@ -1333,7 +1319,6 @@ __global__ void __launch_bounds__(kThreads, H2B_MINB) k_matvec(const KArgs a, co
     s.dpack = a.dpack;
     s.rec = s_rec;
     s.parity = 0;
-    s.issued = false;
     if (threadIdx.x == 0) {
         // tickets count on across launches: launch = t / grid (every CTA of a
         // launch takes exactly one ticket before the next launch starts)
