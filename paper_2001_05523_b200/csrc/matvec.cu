@@ -49,7 +49,11 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
+#include <condition_variable>
 #include <mutex>
+#include <thread>
+#include <unistd.h>
 #include <vector>
 
 #include "device_common.cuh"
@@ -109,6 +113,7 @@ struct h2b_plan {
     double* dpack = nullptr;  // downward-step operands [E_t^T | V_t^T] per cluster (k_pack_descent)
     double* dx;
     double* dy;
+    double* hx = nullptr;  // page-locked staging of a pageable host x (h2b_matvec_host)
     unsigned long long* trace;  // optional per-CTA timeline (H2B_TRACE=1)
     // symmetric nearfield (one copy of every block pair; null when unused)
     double* dsym;       // packed column panels of the upper blocks
@@ -2184,6 +2189,7 @@ extern "C" int h2b_debug_stuck(h2b_plan* p, unsigned long long* out) {
 
 extern "C" int h2b_plan_destroy(h2b_plan* p) {
     if (!p) return ok();
+    if (p->hx) cudaFreeHost(p->hx);
     void* bufs[] = {p->xhat, p->ycpl, p->yfin, p->ynear, p->ctrl, p->rec,  p->fwd_off, p->dx,
                     p->dy,   p->trace, p->dsym, p->dpack,  p->gsym, p->ppart, p->nsum, p->xgath,
                     p->xhat_f, p->d_own, p->d_own_off, p->d_imp, p->d_imp_src, p->d_span, p->span_val};
@@ -2259,20 +2265,158 @@ extern "C" int h2b_matvec(h2b_plan* p, const double* d_x, double* d_y, void* str
     return launch_matvec(p, d_x, d_y, as_stream(stream));
 }
 
-// Host vectors: one stream-ordered copy each way around the launch (a pinned
-// buffer by DMA, a pageable one through the driver's staged copy), then a
-// stream synchronise.  Measured against the round's earlier design -- x read
-// from mapped host memory by copy tasks inside the kernel, y written to mapped
-// host memory by its last tasks -- the copy engines win from config 2 up
-// (config 3, pinned vectors: 3.58 vs 3.82 ms; pageable x: 4.1 vs 5.3 ms) and
-// cost 3 us at config 1 (76 vs 73 us).
+namespace {
+// A pageable x of config 3 is 16.8 MB: the driver's staged host-to-device copy
+// moves it at the speed of one core's memcpy (~1 ms), a third of the matvec.
+// StagePool copies it into the plan's page-locked staging buffer with a few
+// persistent host threads, piece by piece, while the calling thread hands every
+// finished piece to the copy engine (cudaMemcpyAsync): memcpy and DMA overlap
+// and the memcpy runs on several cores.  (Threads spawned per call cost more
+// than they saved; in-kernel polling of arrival flags was slower still.)
+class StagePool {
+public:
+    static constexpr size_t kPiece = size_t(1) << 20;
+    static StagePool& get() {
+        static StagePool pool;
+        return pool;
+    }
+    // false: not usable here (forked child, thread start failed): use the plain copy
+    bool usable() { return pid_ == getpid() && !th_.empty(); }
+    std::mutex use;  // one staged copy at a time
+
+    // dst (page-locked) <- src, then DMA to dev piece by piece on st
+    cudaError_t copy(double* dev, double* dst, const double* src, size_t bytes, cudaStream_t st) {
+        const size_t np = (bytes + kPiece - 1) / kPiece;
+        {
+            // workers become active under this lock only: with none active the
+            // job may change (a straggler of the last job finds no piece left)
+            std::unique_lock<std::mutex> g(m_);
+            while (active_.load(std::memory_order_acquire) != 0) {
+                g.unlock();
+                std::this_thread::yield();
+                g.lock();
+            }
+            if (done_.size() < np) done_ = std::vector<std::atomic<uint32_t>>(np);
+            dst_ = reinterpret_cast<char*>(dst);
+            src_ = reinterpret_cast<const char*>(src);
+            bytes_ = bytes;
+            np_ = np;
+            next_.store(0, std::memory_order_relaxed);
+            ++seq_;
+        }
+        cv_.notify_all();
+        const uint32_t seq = seq_;
+        for (size_t k = 0; k < np; ++k) {
+            while (done_[k].load(std::memory_order_acquire) != seq) {
+                if (!work_one(seq)) std::this_thread::yield();
+            }
+            const size_t o = k * kPiece, n = std::min(kPiece, bytes - o);
+            const cudaError_t e = cudaMemcpyAsync(reinterpret_cast<char*>(dev) + o, dst_ + o, n, cudaMemcpyHostToDevice, st);
+            if (e != cudaSuccess) {
+                // let the remaining pieces finish before the buffers go away
+                for (size_t j = k + 1; j < np; ++j)
+                    while (done_[j].load(std::memory_order_acquire) != seq)
+                        if (!work_one(seq)) std::this_thread::yield();
+                return e;
+            }
+        }
+        return cudaSuccess;
+    }
+
+private:
+    StagePool() : pid_(getpid()) {
+        const unsigned hw = std::thread::hardware_concurrency();
+        const int nt = (int)std::min(3u, hw > 1 ? hw - 1 : 0u);
+        try {
+            for (int i = 0; i < nt; ++i) th_.emplace_back([this] { run(); });
+        } catch (...) {
+        }
+    }
+    ~StagePool() {
+        if (pid_ != getpid()) {  // forked child: the threads are not ours
+            for (auto& t : th_) t.detach();
+            return;
+        }
+        {
+            std::lock_guard<std::mutex> g(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    bool work_one(uint32_t seq) {
+        const size_t k = next_.fetch_add(1, std::memory_order_relaxed);
+        if (k >= np_) return false;
+        const size_t o = k * kPiece;
+        std::memcpy(dst_ + o, src_ + o, std::min(kPiece, bytes_ - o));
+        done_[k].store(seq, std::memory_order_release);
+        return true;
+    }
+    void run() {
+        uint32_t seen = 0;
+        for (;;) {
+            uint32_t seq;
+            {
+                std::unique_lock<std::mutex> g(m_);
+                cv_.wait(g, [&] { return stop_ || seq_ != seen; });
+                if (stop_) return;
+                seen = seq = seq_;
+                active_.fetch_add(1, std::memory_order_acq_rel);
+            }
+            while (work_one(seq)) {
+            }
+            active_.fetch_sub(1, std::memory_order_acq_rel);
+        }
+    }
+    pid_t pid_;
+    std::vector<std::thread> th_;
+    std::mutex m_;
+    std::condition_variable cv_;
+    bool stop_ = false;
+    uint32_t seq_ = 0;
+    std::atomic<int> active_{0};
+    std::atomic<size_t> next_{0};
+    size_t np_ = 0, bytes_ = 0;
+    char* dst_ = nullptr;
+    const char* src_ = nullptr;
+    std::vector<std::atomic<uint32_t>> done_;
+};
+
+bool page_locked(const void* h) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, h) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+}  // namespace
+
+// Host vectors: one stream-ordered copy each way around the launch (a
+// page-locked buffer by DMA; a large pageable x through StagePool, a small one
+// or a pageable y through the driver's staged copy), then a stream
+// synchronise.  Measured against the round's earlier design -- x read from
+// mapped host memory by copy tasks inside the kernel, y written to mapped host
+// memory by its last tasks -- the copy engines win from config 2 up (config 3,
+// pinned vectors: 3.46 vs 3.82 ms) and cost 3 us at config 1 (76 vs 73 us).
 extern "C" int h2b_matvec_host(h2b_plan* p, const double* h_x, double* h_y, void* stream) {
     if (!p || !h_x || !h_y) return fail(H2B_ERR_INVALID, "h2b_matvec_host: null pointer");
     if (p->xmode) return fail(H2B_ERR_INVALID, "h2b_matvec_host: x_hat-exchange plan");
     std::lock_guard<std::mutex> g(p->mu);
     cudaStream_t st = as_stream(stream);
     if (p->launched && p->last != st) H2B_CUDA_TRY(cudaStreamWaitEvent(st, p->done, 0));
-    H2B_CUDA_TRY(cudaMemcpyAsync(p->dx, h_x, sizeof(double) * p->L.n_cols, cudaMemcpyHostToDevice, st));
+    const size_t xbytes = sizeof(double) * p->L.n_cols;
+    bool staged = false;
+    if (xbytes >= 4 * StagePool::kPiece && !page_locked(h_x)) {
+        StagePool& pool = StagePool::get();
+        if (pool.usable()) {
+            if (!p->hx) H2B_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&p->hx), xbytes));
+            std::lock_guard<std::mutex> u(pool.use);
+            H2B_CUDA_TRY(pool.copy(p->dx, p->hx, h_x, xbytes, st));
+            staged = true;
+        }
+    }
+    if (!staged) H2B_CUDA_TRY(cudaMemcpyAsync(p->dx, h_x, xbytes, cudaMemcpyHostToDevice, st));
     if (int rc = launch_matvec(p, p->dx, p->dy, st)) return rc;
     H2B_CUDA_TRY(cudaMemcpyAsync(h_y, p->dy, sizeof(double) * p->L.n_rows, cudaMemcpyDeviceToHost, st));
     H2B_CUDA_TRY(cudaStreamSynchronize(st));
