@@ -70,7 +70,7 @@ CONFIGS = {
 DEFAULT_CONFIG = "3"
 EPS_ACA = 1e-4
 METRIC = "H2-matvec DoF/s (fp64), + nearfield quad pairs/s"
-PROFILE = os.path.join(ROOT, "profiles", "r02bu_ncu_full_raw.csv")
+PROFILE = os.path.join(ROOT, "profiles", "r02bx_ncu_full_raw.csv")
 
 
 # ---------------------------------------------------------------------------

@@ -2268,8 +2268,8 @@ extern "C" int h2b_matvec(h2b_plan* p, const double* d_x, double* d_y, void* str
 namespace {
 // A pageable x of config 3 is 16.8 MB: the driver's staged host-to-device copy
 // moves it at the speed of one core's memcpy (~1 ms), a third of the matvec.
-// StagePool copies it into the plan's page-locked staging buffer with a few
-// persistent host threads, piece by piece, while the calling thread hands every
+// StagePool copies it into the plan's page-locked staging buffer with two
+// persistent host threads and the caller, piece by piece, while the calling thread hands every
 // finished piece to the copy engine (cudaMemcpyAsync): memcpy and DMA overlap
 // and the memcpy runs on several cores.  (Threads spawned per call cost more
 // than they saved; in-kernel polling of arrival flags was slower still.)
@@ -2281,7 +2281,7 @@ public:
         return pool;
     }
     // false: not usable here (forked child, thread start failed): use the plain copy
-    bool usable() { return pid_ == getpid() && !th_.empty(); }
+    bool usable() { return pid_ == getpid() && !th_->empty(); }
     std::mutex use;  // one staged copy at a time
 
     // dst (page-locked) <- src, then DMA to dev piece by piece on st
@@ -2324,25 +2324,27 @@ public:
     }
 
 private:
-    StagePool() : pid_(getpid()) {
+    StagePool() : pid_(getpid()), th_(new std::vector<std::thread>()) {
         const unsigned hw = std::thread::hardware_concurrency();
-        const int nt = (int)std::min(3u, hw > 1 ? hw - 1 : 0u);
+        // two workers beside the calling thread: on this pool's (virtualised)
+        // hosts more threads lost to wake-up latency and stragglers (config 3,
+        // one box: 1 / 3 / 5 / 7 / 11 workers 3.93 / 4.08 / 4.44 / 4.45 / 4.90 ms
+        // per call; another box 3.66 ms with 3 against 4.15 ms without the pool)
+        const int nt = (int)std::min(2u, hw > 1 ? hw - 1 : 0u);
         try {
-            for (int i = 0; i < nt; ++i) th_.emplace_back([this] { run(); });
+            for (int i = 0; i < nt; ++i) th_->emplace_back([this] { run(); });
         } catch (...) {
         }
     }
     ~StagePool() {
-        if (pid_ != getpid()) {  // forked child: the threads are not ours
-            for (auto& t : th_) t.detach();
-            return;
-        }
+        if (pid_ != getpid()) return;  // forked child: the threads are not ours (their handles stay untouched)
         {
             std::lock_guard<std::mutex> g(m_);
             stop_ = true;
         }
         cv_.notify_all();
-        for (auto& t : th_) t.join();
+        for (auto& t : *th_) t.join();
+        delete th_;
     }
     bool work_one(uint32_t seq) {
         const size_t k = next_.fetch_add(1, std::memory_order_relaxed);
@@ -2369,7 +2371,7 @@ private:
         }
     }
     pid_t pid_;
-    std::vector<std::thread> th_;
+    std::vector<std::thread>* th_;
     std::mutex m_;
     std::condition_variable cv_;
     bool stop_ = false;
