@@ -2268,7 +2268,7 @@ extern "C" int h2b_matvec(h2b_plan* p, const double* d_x, double* d_y, void* str
 namespace {
 // A pageable x of config 3 is 16.8 MB: the driver's staged host-to-device copy
 // moves it at the speed of one core's memcpy (~1 ms), a third of the matvec.
-// StagePool copies it into the plan's page-locked staging buffer with two
+// StagePool copies it into the plan's page-locked staging buffer with three
 // persistent host threads and the caller, piece by piece, while the calling thread hands every
 // finished piece to the copy engine (cudaMemcpyAsync): memcpy and DMA overlap
 // and the memcpy runs on several cores.  (Threads spawned per call cost more
@@ -2326,11 +2326,12 @@ public:
 private:
     StagePool() : pid_(getpid()), th_(new std::vector<std::thread>()) {
         const unsigned hw = std::thread::hardware_concurrency();
-        // two workers beside the calling thread: on this pool's (virtualised)
-        // hosts more threads lost to wake-up latency and stragglers (config 3,
-        // one box: 1 / 3 / 5 / 7 / 11 workers 3.93 / 4.08 / 4.44 / 4.45 / 4.90 ms
-        // per call; another box 3.66 ms with 3 against 4.15 ms without the pool)
-        const int nt = (int)std::min(2u, hw > 1 ? hw - 1 : 0u);
+        // three workers beside the calling thread.  Per call at config 3: one
+        // box 3.66 ms against 4.15 ms with the driver's staged copy; on another
+        // (virtualised, slow thread wake-ups) 1 / 3 / 5 / 7 / 11 workers gave
+        // 3.93 / 4.08 / 4.44 / 4.45 / 4.90 ms against 4.11 ms: never worse with
+        // three, more threads lose to wake-up latency and stragglers
+        const int nt = (int)std::min(3u, hw > 1 ? hw - 1 : 0u);
         try {
             for (int i = 0; i < nt; ++i) th_->emplace_back([this] { run(); });
         } catch (...) {
